@@ -1,0 +1,163 @@
+/*
+ * mgcg.h -- C ABI of the B200-native (sm_100a, fp64) fine-grid solve path of
+ * Ferrari & Sigmund, "Towards solving large-scale topology optimization problems
+ * with buckling constraints at the cost of linear analyses" (arXiv 1909.13585).
+ *
+ * What the library computes (PAPER.md line numbers, section / equation):
+ *   - K(x) u = f for a batch of right-hand sides: the linear analysis (LA) of
+ *     Alg. 1 l.2, the adjoint systems K z_i = phi_i' (grad_u G) phi_i
+ *     of Eq. 5 (:133-136) and the fine-scale BVP K Phi = G Psi of Eq. 6 / Alg. 2
+ *     l.15 (:161-165, :732).  Solver: conjugate gradients preconditioned by a
+ *     geometric multigrid built on the nested discretisations {Omega_j}
+ *     (Appendix A; block/multi-RHS use :760-761).
+ *   - K_e = E_kappa(x_e) K_e0 and G_e = E_sigma(x_e) G_e0[u_e] (Eq. 2
+ *     :101-108); K_e0 is the standard bilinear Q4 (plane stress, thickness 1) /
+ *     trilinear H8 unit-element stiffness (SURVEY.md 8(c) reading r1, r2).
+ *   - Coarse operators by Galerkin projection K^l = I^1_l K I^l_1 (PAPER.md:155,
+ *     Alg. 2 l.5 :705) with bilinear/trilinear interpolation I^j_{j+1} (:146).
+ *   - y = G(u) phi, the stress-stiffness product used as RHS in Eq. 6 (:163) and
+ *     in the residual Eq. 7 (:181); stress at the element centroid (reading r15).
+ *
+ * Conventions (all entry points):
+ *   - Array arguments are device pointers unless stated otherwise; mgcg_solve and
+ *     stress_stiffness_apply also accept host pointers (detected with
+ *     cudaPointerGetAttributes) and then copy in/out on the handle's stream.
+ *   - Vectors are RHS-major, shape (nrhs, n), fp64; DOF index = d*node + comp;
+ *     nodes in C order over (N0+1, N1+1[, N2+1]), axis 0 slowest; comp c is the
+ *     displacement along axis c.  Element arrays (E_e, Es_e) in C order over
+ *     (N0, N1[, N2]).
+ *   - Dirichlet: `fixed[dof] != 0` marks a fixed DOF.  K's fixed rows/columns are
+ *     identity, G's are zero; solutions and G-products are 0 at fixed DOFs and
+ *     right-hand sides are masked there.
+ *   - Ownership: mg_setup copies E_e and fixed; all other arrays are borrowed for
+ *     the duration of the call.  The handle owns its device workspace.
+ *   - Errors: every call returns mg_status; argument errors have no side
+ *     effects; mg_last_error() gives a one-line description of the last failure
+ *     on the calling thread.
+ */
+#ifndef MGCG_H
+#define MGCG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MG_MAX_RHS 64
+#define MG_MAX_LEVELS 12
+
+typedef enum {
+    MG_OK = 0,
+    MG_ERR_ARG = 1,          /* NULL pointer, bad dim/levels/nrhs/tol            */
+    MG_ERR_NONDIVISIBLE = 2, /* N_i not divisible by 2^(levels-1)   */
+    MG_ERR_DIM = 3,          /* size mismatch / too large                         */
+    MG_ERR_MODULUS = 4,      /* E_e <= 0 or not finite                            */
+    MG_ERR_BREAKDOWN = 5,    /* p.Kp <= 0 in CG: operator not SPD                 */
+    MG_ERR_MAXITER = 6,      /* max_iter reached; x holds the last iterate        */
+    MG_ERR_OOM = 7,
+    MG_ERR_CUDA = 8,
+    MG_ERR_NCCL = 9,
+    MG_ERR_SINGULAR = 10     /* coarsest-level factorisation hit a non-positive pivot */
+} mg_status;
+
+/* Structured grid: dim = 2 (Q4) or 3 (H8); nel[k] element count along axis k
+ * (nel[2] ignored in 2D); nu = Poisson ratio (0.3). Unit elements. */
+typedef struct {
+    int dim;
+    int nel[3];
+    double nu;
+} mg_grid;
+
+/* Multigrid / CG options; pass NULL for defaults {0.6, 1, 1, 1000}.
+ * omega: damped-Jacobi factor; nu_pre / nu_post: sweeps per level (symmetric
+ * V-cycle requires nu_pre == nu_post >= 1); max_iter: CG iteration cap. */
+typedef struct {
+    double omega;
+    int nu_pre;
+    int nu_post;
+    int max_iter;
+} mg_opts;
+
+/* Per-solve report (host struct). iters[k]: CG iterations of RHS k; relres[k]:
+ * recursive ||r_k||/||b_k||; true_relres[k]: ||b_k - K x_k|| / ||b_k|| computed at
+ * exit; converged[k] = 1 if true_relres[k] <= tol. Times in milliseconds. */
+typedef struct {
+    int nrhs;
+    int iters[MG_MAX_RHS];
+    double relres[MG_MAX_RHS];
+    double true_relres[MG_MAX_RHS];
+    int converged[MG_MAX_RHS];
+    int max_iters;
+    int restarts;
+    int graph_launches;
+    long long kernel_launches;
+    double solve_ms;
+} mg_report;
+
+typedef struct mg_ctx* mg_handle;
+
+/* Build the hierarchy for one design (Alg. 2 l.1-2, l.5):
+ *   grid    element counts, nu.  Requires nel[k] % 2^(levels-1) == 0.
+ *   E_e     device, nelem fp64 moduli E_kappa(x_e) > 0 (Eq. 2), copied.
+ *   fixed   device, ndof uint8, nonzero = Dirichlet DOF, copied.
+ *   levels  1..MG_MAX_LEVELS, counting the finest level (reading r10).
+ *   opts    NULL or options.
+ *   stream  cudaStream_t (as void*) on which all work of this handle runs;
+ *           NULL = the legacy default stream.
+ *   out     receives the handle.
+ * Work: fine diagonal, Galerkin coarse operators on every level, coarsest
+ * dense SPD inverse; all on the device.  Synchronises the stream. */
+mg_status mg_setup(const mg_grid* grid, const double* E_e, const uint8_t* fixed,
+                   int levels, const mg_opts* opts, void* stream, mg_handle* out);
+
+/* Same grid and BCs, new design: recompute all level operators from E_e. */
+mg_status mg_update_modulus(mg_handle h, const double* E_e);
+
+/* Solve K x_k = rhs_k, k < nrhs, by multigrid-preconditioned CG
+ * from a zero initial guess, each RHS stopping when ||r_k|| <= tol ||b_k||
+ * (reading r12; confirmed by a true residual at exit).
+ *   rhs  (nrhs, ndof) fp64, device or host; masked to 0 at fixed DOFs.
+ *   x    (nrhs, ndof) fp64 output, device or host.
+ *   rep  NULL or a host report.
+ * Returns MG_ERR_MAXITER (x = last iterate) or MG_ERR_BREAKDOWN on failure.
+ * Synchronous with respect to the handle's stream. 1 <= nrhs <= MG_MAX_RHS. */
+mg_status mgcg_solve(mg_handle h, const double* rhs, int nrhs, double tol, double* x, mg_report* rep);
+
+/* y_k = G(u) phi_k for k < nphi (PAPER.md:99 G_e = E_sigma G_e0[u_e]; Eq. 6 :163):
+ *   Es_e  device, nelem fp64 stress moduli E_sigma(x_e) = x_e^p E_1 (Eq. 2 :106).
+ *   u     device, ndof fp64 displacement (taken as given, incl. fixed DOFs).
+ *   phi   (nphi, ndof) fp64; y (nphi, ndof) fp64 output; fixed rows/cols zero.
+ * Stress sigma_e = Es_e D0 B(centroid) u_e; G_e = (sum_ij sigma_ij H_ij) kron I_d.
+ * Device or host pointers. Asynchronous for device pointers. */
+mg_status stress_stiffness_apply(mg_handle h, const double* Es_e, const double* u,
+                                 const double* phi, int nphi, double* y);
+
+/* Diagnostics (used by the parity tests; all device pointers, asynchronous):
+ * y = A_level x for nrhs vectors (level 0 = fine matrix-free K; level >= 1 =
+ * Galerkin operator incl. identity rows at fixed DOFs). */
+mg_status mg_matvec(mg_handle h, int level, const double* x, int nrhs, double* y);
+/* z = B r : one symmetric V-cycle of the preconditioner on nrhs vectors. */
+mg_status mg_vcycle(mg_handle h, const double* r, int nrhs, double* z);
+/* coarse = P^T fine (restriction from `level` to level+1), masked (reading r11). */
+mg_status mg_restrict(mg_handle h, int level, const double* fine, int nrhs, double* coarse);
+/* fine = P coarse (prolongation from level+1 to `level`), masked. */
+mg_status mg_prolong(mg_handle h, int level, const double* coarse, int nrhs, double* fine);
+/* Element counts and DOF count of a level; nlevels if level < 0. */
+mg_status mg_level_info(mg_handle h, int level, int* nel3, long long* ndof, int* nlevels);
+/* diag(A_level) (ndof doubles, device). */
+mg_status mg_get_diagonal(mg_handle h, int level, double* d);
+/* Dense inverse of the coarsest operator (ndof_L x ndof_L, row-major, device). */
+mg_status mg_get_coarse_inverse(mg_handle h, double* Ainv);
+/* Number of CUDA kernels this handle has launched (graph nodes counted once per launch). */
+long long mg_kernel_launches(mg_handle h);
+
+mg_status mg_destroy(mg_handle h);
+const char* mg_strerror(mg_status s);
+const char* mg_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MGCG_H */

@@ -1,0 +1,152 @@
+"""B200-native (sm_100a, fp64) fine-grid solve path of Ferrari & Sigmund (arXiv 1909.13585).
+
+Thin Python binding over the C ABI in include/mgcg.h: the functions below have
+the C names and only marshal arguments (torch CUDA tensors or host numpy
+arrays -> raw pointers).  Every step of the path runs in the CUDA kernels of
+libmgcg.so; there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._lib import MgError, MgGrid, MgOpts, MgReport, check, lib
+
+__all__ = [
+    "Handle", "MgError", "mg_setup", "mg_update_modulus", "mgcg_solve", "stress_stiffness_apply",
+    "mg_matvec", "mg_vcycle", "mg_restrict", "mg_prolong", "mg_level_info", "mg_get_diagonal",
+    "mg_get_coarse_inverse", "mg_kernel_launches", "mg_destroy", "lib_path",
+]
+
+lib_path = _lib.LIB_PATH
+
+
+def _ptr(a, dtype):
+    """Raw pointer of a contiguous torch tensor (CUDA or CPU) or numpy array."""
+    if isinstance(a, np.ndarray):
+        if a.dtype != dtype or not a.flags.c_contiguous:
+            raise TypeError(f"expected C-contiguous numpy array of {dtype}, got {a.dtype}")
+        return ctypes.c_void_p(a.ctypes.data)
+    import torch
+    if not isinstance(a, torch.Tensor):
+        raise TypeError("expected a torch tensor or numpy array")
+    want = {np.float64: torch.float64, np.uint8: torch.uint8}[dtype]
+    if a.dtype != want or not a.is_contiguous():
+        raise TypeError(f"expected contiguous tensor of {want}, got {a.dtype}")
+    return ctypes.c_void_p(a.data_ptr())
+
+
+class Handle:
+    """Owns an mg_handle (one design on one grid)."""
+
+    def __init__(self, raw, dim, nel, levels, stream):
+        self.raw = raw
+        self.dim = dim
+        self.nel = tuple(nel)
+        self.levels = levels
+        self.stream = stream
+        self.ndof = dim * int(np.prod([n + 1 for n in nel]))
+        self.nelem = int(np.prod(nel))
+
+    def __del__(self):
+        try:
+            mg_destroy(self)
+        except Exception:
+            pass
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        except Exception:
+            pass
+        return ctypes.c_void_p(0)
+    return ctypes.c_void_p(getattr(stream, "cuda_stream", stream))
+
+
+def mg_setup(nel, E, fixed, levels, nu=0.3, omega=0.6, nu_pre=1, nu_post=1, max_iter=1000, stream=None):
+    dim = len(nel)
+    g = MgGrid(dim, (ctypes.c_int * 3)(*(list(nel) + [0] * (3 - dim))), nu)
+    o = MgOpts(omega, nu_pre, nu_post, max_iter)
+    raw = ctypes.c_void_p()
+    sp = _stream_ptr(stream)
+    check(lib.mg_setup(ctypes.byref(g), _ptr(E, np.float64), _ptr(fixed, np.uint8), levels, ctypes.byref(o), sp,
+                       ctypes.byref(raw)))
+    return Handle(raw, dim, nel, levels, sp)
+
+
+def mg_update_modulus(h, E):
+    check(lib.mg_update_modulus(h.raw, _ptr(E, np.float64)))
+
+
+def _report(rep, nrhs):
+    return dict(
+        iters=list(rep.iters[:nrhs]), relres=list(rep.relres[:nrhs]), true_relres=list(rep.true_relres[:nrhs]),
+        converged=list(rep.converged[:nrhs]), max_iters=rep.max_iters, restarts=rep.restarts,
+        graph_launches=rep.graph_launches, kernel_launches=rep.kernel_launches, solve_ms=rep.solve_ms,
+    )
+
+
+def mgcg_solve(h, rhs, tol, x, raise_on_error=True):
+    """Solve K x_k = rhs_k for all rows of rhs (nrhs, ndof); x is written in place."""
+    nrhs = rhs.shape[0]
+    rep = MgReport()
+    st = lib.mgcg_solve(h.raw, _ptr(rhs, np.float64), nrhs, tol, _ptr(x, np.float64), ctypes.byref(rep))
+    out = _report(rep, nrhs)
+    out["status"] = _lib.STATUS.get(st, st)
+    if raise_on_error:
+        check(st)
+    return out
+
+
+def stress_stiffness_apply(h, Es, u, phi, y):
+    check(lib.stress_stiffness_apply(h.raw, _ptr(Es, np.float64), _ptr(u, np.float64), _ptr(phi, np.float64),
+                                     phi.shape[0], _ptr(y, np.float64)))
+
+
+def mg_matvec(h, level, x, y):
+    check(lib.mg_matvec(h.raw, level, _ptr(x, np.float64), x.shape[0], _ptr(y, np.float64)))
+
+
+def mg_vcycle(h, r, z):
+    check(lib.mg_vcycle(h.raw, _ptr(r, np.float64), r.shape[0], _ptr(z, np.float64)))
+
+
+def mg_restrict(h, level, fine, coarse):
+    check(lib.mg_restrict(h.raw, level, _ptr(fine, np.float64), fine.shape[0], _ptr(coarse, np.float64)))
+
+
+def mg_prolong(h, level, coarse, fine):
+    check(lib.mg_prolong(h.raw, level, _ptr(coarse, np.float64), coarse.shape[0], _ptr(fine, np.float64)))
+
+
+def mg_level_info(h, level):
+    nel = (ctypes.c_int * 3)()
+    ndof = ctypes.c_longlong()
+    nl = ctypes.c_int()
+    check(lib.mg_level_info(h.raw, level, nel, ctypes.byref(ndof), ctypes.byref(nl)))
+    return dict(nel=tuple(nel[:h.dim]), ndof=ndof.value, nlevels=nl.value)
+
+
+def mg_get_diagonal(h, level, d):
+    check(lib.mg_get_diagonal(h.raw, level, _ptr(d, np.float64)))
+
+
+def mg_get_coarse_inverse(h, A):
+    check(lib.mg_get_coarse_inverse(h.raw, _ptr(A, np.float64)))
+
+
+def mg_kernel_launches(h):
+    return int(lib.mg_kernel_launches(h.raw))
+
+
+def mg_destroy(h):
+    if h is not None and getattr(h, "raw", None):
+        lib.mg_destroy(h.raw)
+        h.raw = None

@@ -1,0 +1,94 @@
+"""ctypes declarations of libmgcg.so (include/mgcg.h).  Marshalling only.
+
+The shared library is built in-tree by `__graft_entry__.build()` (or
+`make -C paper_1909_13585_b200/csrc`).  There is no fallback: if the library is
+missing this module raises at import time.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+MG_MAX_RHS = 64
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libmgcg.so")
+
+STATUS = {
+    0: "MG_OK", 1: "MG_ERR_ARG", 2: "MG_ERR_NONDIVISIBLE", 3: "MG_ERR_DIM", 4: "MG_ERR_MODULUS",
+    5: "MG_ERR_BREAKDOWN", 6: "MG_ERR_MAXITER", 7: "MG_ERR_OOM", 8: "MG_ERR_CUDA", 9: "MG_ERR_NCCL",
+    10: "MG_ERR_SINGULAR",
+}
+
+EXPORTED = [
+    "mg_setup", "mg_update_modulus", "mgcg_solve", "stress_stiffness_apply", "mg_matvec", "mg_vcycle",
+    "mg_restrict", "mg_prolong", "mg_level_info", "mg_get_diagonal", "mg_get_coarse_inverse",
+    "mg_kernel_launches", "mg_destroy", "mg_strerror", "mg_last_error",
+]
+
+
+class MgGrid(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int), ("nel", ctypes.c_int * 3), ("nu", ctypes.c_double)]
+
+
+class MgOpts(ctypes.Structure):
+    _fields_ = [("omega", ctypes.c_double), ("nu_pre", ctypes.c_int), ("nu_post", ctypes.c_int),
+                ("max_iter", ctypes.c_int)]
+
+
+class MgReport(ctypes.Structure):
+    _fields_ = [
+        ("nrhs", ctypes.c_int),
+        ("iters", ctypes.c_int * MG_MAX_RHS),
+        ("relres", ctypes.c_double * MG_MAX_RHS),
+        ("true_relres", ctypes.c_double * MG_MAX_RHS),
+        ("converged", ctypes.c_int * MG_MAX_RHS),
+        ("max_iters", ctypes.c_int),
+        ("restarts", ctypes.c_int),
+        ("graph_launches", ctypes.c_int),
+        ("kernel_launches", ctypes.c_longlong),
+        ("solve_ms", ctypes.c_double),
+    ]
+
+
+class MgError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+        super().__init__(f"{self.name}: {msg}")
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libmgcg.so not built ({LIB_PATH}); run __graft_entry__.build() -- no CPU fallback exists")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I, D, LL = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_longlong
+    sig = {
+        "mg_setup": ([ctypes.POINTER(MgGrid), P, P, I, ctypes.POINTER(MgOpts), P, ctypes.POINTER(P)], I),
+        "mg_update_modulus": ([P, P], I),
+        "mgcg_solve": ([P, P, I, D, P, ctypes.POINTER(MgReport)], I),
+        "stress_stiffness_apply": ([P, P, P, P, I, P], I),
+        "mg_matvec": ([P, I, P, I, P], I),
+        "mg_vcycle": ([P, P, I, P], I),
+        "mg_restrict": ([P, I, P, I, P], I),
+        "mg_prolong": ([P, I, P, I, P], I),
+        "mg_level_info": ([P, I, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(LL), ctypes.POINTER(ctypes.c_int)], I),
+        "mg_get_diagonal": ([P, I, P], I),
+        "mg_get_coarse_inverse": ([P, P], I),
+        "mg_kernel_launches": ([P], LL),
+        "mg_destroy": ([P], I),
+        "mg_strerror": ([I], ctypes.c_char_p),
+        "mg_last_error": ([], ctypes.c_char_p),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    return lib
+
+
+lib = _load()
+
+
+def check(status: int):
+    if status != 0:
+        raise MgError(status, lib.mg_last_error().decode())

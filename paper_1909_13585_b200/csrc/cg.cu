@@ -1,0 +1,225 @@
+// Batched preconditioned CG vector kernels (mgPCG PAPER.md:758,
+// multi-RHS :760-761).  Per RHS k:
+//   alpha_k = (r.z)_k / (p.q)_k ; x += alpha p ; r -= alpha q ; stop when
+//   ||r_k|| <= tol ||b_k|| ; beta_k = (r.z)_new / (r.z)_old ; p = z + beta p.
+// Dot products: per-warp shuffle reductions written to a partial array, then
+// summed in a fixed order by `cg_scalars` (deterministic, no atomics).
+#include "kernels.h"
+
+#define MG_MAX_RHS_DEV 64
+
+static constexpr int VEC_THREADS = 256;
+
+int vec_blocks(long long n) {
+    long long b = (n + VEC_THREADS * 4 - 1) / (VEC_THREADS * 4);
+    if (b > 1184) b = 1184;   // 8 x 148 SMs
+    if (b < 1) b = 1;
+    return (int)b;
+}
+
+__device__ __forceinline__ void block_partial(double v, double* partial, long long slot) {
+    __shared__ double red[VEC_THREADS / 32];
+    v = warp_sum(v);
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        double s = lane < (VEC_THREADS / 32) ? red[lane] : 0.0;
+        s = warp_sum(s);
+        if (lane == 0) partial[slot] = s;
+    }
+}
+
+// z = omega Dinv r
+__global__ void jacobi0_kernel(long long n, const double* __restrict__ r, const double* __restrict__ Dinv,
+                               double omega, double* __restrict__ z, const int* active, const int* done) {
+    const int rr = blockIdx.y;
+    if (done && *done) return;
+    if (active && !active[rr]) return;
+    const long long o = (long long)rr * n;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        z[o + i] = omega * Dinv[i] * r[o + i];
+}
+
+void cg_pointwise_jacobi(long long n, int R, const double* r, const double* Dinv, double omega, double* z,
+                         const int* active, const int* done, cudaStream_t s) {
+    dim3 g(vec_blocks(n), R);
+    jacobi0_kernel<<<g, VEC_THREADS, 0, s>>>(n, r, Dinv, omega, z, active, done);
+}
+
+// x += alpha p; r -= alpha q; partial r.r; z = omega Dinv r
+__global__ void __launch_bounds__(VEC_THREADS) cg_update_kernel(long long n, const double* __restrict__ alpha,
+                                                                const double* __restrict__ p,
+                                                                const double* __restrict__ q, double* __restrict__ x,
+                                                                double* __restrict__ r, const double* __restrict__ Dinv,
+                                                                double omega, double* __restrict__ z, double* partial,
+                                                                const int* active, const int* done) {
+    const int rr = blockIdx.y;
+    if (done && *done) return;
+    if (active && !active[rr]) return;
+    const double al = alpha[rr];
+    const long long o = (long long)rr * n;
+    double acc = 0.0;
+    const long long n2 = n >> 1;   // n is even (d*nodes with d in {2,3} -> handle odd tail)
+    const double2* p2 = reinterpret_cast<const double2*>(p + o);
+    const double2* q2 = reinterpret_cast<const double2*>(q + o);
+    double2* x2 = reinterpret_cast<double2*>(x + o);
+    double2* r2 = reinterpret_cast<double2*>(r + o);
+    double2* z2 = reinterpret_cast<double2*>(z + o);
+    const double2* d2 = reinterpret_cast<const double2*>(Dinv);
+    const bool aligned = ((o & 1) == 0);
+    if (aligned) {
+        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += (long long)gridDim.x * blockDim.x) {
+            double2 pv = p2[i], qv = q2[i], xv = x2[i], rv = r2[i], dv = d2[i];
+            xv.x = fma(al, pv.x, xv.x); xv.y = fma(al, pv.y, xv.y);
+            rv.x = fma(-al, qv.x, rv.x); rv.y = fma(-al, qv.y, rv.y);
+            x2[i] = xv; r2[i] = rv;
+            acc = fma(rv.x, rv.x, acc); acc = fma(rv.y, rv.y, acc);
+            z2[i] = make_double2(omega * dv.x * rv.x, omega * dv.y * rv.y);
+        }
+        if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+            long long i = n - 1;
+            x[o + i] = fma(al, p[o + i], x[o + i]);
+            double rv = fma(-al, q[o + i], r[o + i]);
+            r[o + i] = rv; acc = fma(rv, rv, acc);
+            z[o + i] = omega * Dinv[i] * rv;
+        }
+    } else {
+        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+            x[o + i] = fma(al, p[o + i], x[o + i]);
+            double rv = fma(-al, q[o + i], r[o + i]);
+            r[o + i] = rv; acc = fma(rv, rv, acc);
+            z[o + i] = omega * Dinv[i] * rv;
+        }
+    }
+    block_partial(acc, partial, (long long)rr * gridDim.x + blockIdx.x);
+}
+
+void cg_update(long long n, int R, const double* alpha, const double* p, const double* q, double* x, double* r,
+               const double* Dinv, double omega, double* z, double* partial, const int* active, const int* done,
+               cudaStream_t s) {
+    dim3 g(vec_blocks(n), R);
+    cg_update_kernel<<<g, VEC_THREADS, 0, s>>>(n, alpha, p, q, x, r, Dinv, omega, z, partial, active, done);
+}
+
+__global__ void __launch_bounds__(VEC_THREADS) dot_kernel(long long n, const double* __restrict__ a,
+                                                          const double* __restrict__ b, double* partial,
+                                                          const int* active, const int* done) {
+    const int rr = blockIdx.y;
+    if (done && *done) return;
+    if (active && !active[rr]) return;
+    const long long o = (long long)rr * n;
+    double acc = 0.0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        acc = fma(a[o + i], b[o + i], acc);
+    block_partial(acc, partial, (long long)rr * gridDim.x + blockIdx.x);
+}
+
+void vec_dot(long long n, int R, const double* a, const double* b, double* partial, const int* active,
+             const int* done, cudaStream_t s) {
+    dim3 g(vec_blocks(n), R);
+    dot_kernel<<<g, VEC_THREADS, 0, s>>>(n, a, b, partial, active, done);
+}
+
+// dst = src masked to zero at fixed DOFs
+__global__ void mask_copy_kernel(long long nnodes, int dim, const uint8_t* __restrict__ mask,
+                                 const double* __restrict__ src, double* __restrict__ dst) {
+    const int rr = blockIdx.y;
+    const long long n = nnodes * dim, o = (long long)rr * n;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long node = i / dim;
+        const int k = (int)(i - node * dim);
+        dst[o + i] = ((mask[node] >> k) & 1) ? 0.0 : src[o + i];
+    }
+}
+
+void vec_mask_copy(long long nnodes, int dim, int R, const uint8_t* mask, const double* src, double* dst,
+                   cudaStream_t s) {
+    dim3 g(vec_blocks(nnodes * dim), R);
+    mask_copy_kernel<<<g, VEC_THREADS, 0, s>>>(nnodes, dim, mask, src, dst);
+}
+
+// r = t for RHS flagged in `restart` (true-residual restart)
+__global__ void restart_copy_kernel(long long n, const double* __restrict__ t, double* __restrict__ r,
+                                    const int* restart) {
+    const int rr = blockIdx.y;
+    if (!restart[rr]) return;
+    const long long o = (long long)rr * n;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        r[o + i] = t[o + i];
+}
+
+void vec_axpy_masked_restart(long long n, int R, const double* t, double* r, const int* restart, cudaStream_t s) {
+    dim3 g(vec_blocks(n), R);
+    restart_copy_kernel<<<g, VEC_THREADS, 0, s>>>(n, t, r, restart);
+}
+
+// One CTA: warp w sums the partials of RHS w, w+16, ... in a fixed order, then
+// the scalar CG logic runs per RHS.
+__global__ void __launch_bounds__(512) scalars_kernel(int mode, int R, const double* __restrict__ partial, int items,
+                                                      CgCtl c, double tol) {
+    __shared__ int any_active;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x == 0) any_active = 0;
+    if (mode != SM_INIT && mode != SM_BB && mode != SM_TRUE && *c.done) return;
+    __syncthreads();
+    for (int r = wid; r < R; r += blockDim.x >> 5) {
+        const bool act = c.active[r] != 0;
+        double v = 0.0;
+        if (mode == SM_BB || mode == SM_TRUE || act) {
+            for (int i = lane; i < items; i += 32) v += partial[(long long)r * items + i];
+            v = warp_sum(v);
+        }
+        if (lane == 0) {
+            switch (mode) {
+                case SM_BB:   // v = b.b ; (re)activate RHS with nonzero b
+                    c.bb[r] = v;
+                    c.active[r] = v > 0.0 ? 1 : 0;
+                    c.iters[r] = 0;
+                    c.beta[r] = 0.0;
+                    c.rr[r] = v;
+                    break;
+                case SM_RZ0:  // initial r.z
+                    if (act) { c.rz[r] = v; c.beta[r] = 0.0; }
+                    break;
+                case SM_ALPHA:
+                    if (act) {
+                        c.pq[r] = v;
+                        if (!(v > 0.0)) {   // breakdown: operator or preconditioner not SPD
+                            c.alpha[r] = 0.0;
+                            c.active[r] = 0;
+                            atomicOr(c.status, 1);
+                        } else {
+                            c.alpha[r] = c.rz[r] / v;
+                        }
+                    }
+                    break;
+                case SM_CONV:
+                    if (act) {
+                        c.rr[r] = v;
+                        c.iters[r] += 1;
+                        if (v <= tol * tol * c.bb[r]) c.active[r] = 0;
+                    }
+                    break;
+                case SM_BETA:
+                    if (act) {
+                        c.beta[r] = v / c.rz[r];
+                        c.rz[r] = v;
+                    }
+                    break;
+                case SM_TRUE:
+                    c.tt[r] = v;
+                    break;
+                default:
+                    break;
+            }
+            if (c.active[r]) atomicOr(&any_active, 1);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *c.done = any_active ? 0 : 1;
+}
+
+void cg_scalars(int mode, int R, const double* partial, int items, CgCtl c, double tol, cudaStream_t s) {
+    scalars_kernel<<<1, 512, 0, s>>>(mode, R, partial, items, c, tol);
+}

@@ -1,0 +1,336 @@
+// Coarse levels: Galerkin operators K^{l+1} = P^T K^l P (Alg. 2 l.5
+// :705), stored as assembled 3^d-point block stencils, and the
+// stencil-based smoothing / residual kernels of the V-cycle.
+//
+// Galerkin is computed exactly by coarse-element agglomeration:
+//   K_E = M_E ( sum_{children c of E} Q_c^T (M_c K_c M_c) Q_c ) M_E
+// where Q_c interpolates the coarse element's nodal DOFs to child c's nodal DOFs
+// (tensor product of the 1-D weights {1, 1/2, 0}) and M are the 0/1 free-DOF masks
+// (reading r11: P is masked on both sides).  The level's operator is then
+//   A = sum_E A_E^T K_E A_E + (I - M)
+// assembled into a per-node stencil of 3^d blocks (d x d); a coarse DOF whose
+// Galerkin diagonal is exactly 0 (P column zero on the free fine DOFs) is marked
+// fixed, which leaves the preconditioner unchanged.
+#include "kernels.h"
+
+__constant__ double c_K0g[576];
+__constant__ double c_Q[8 * 8 * 8];   // [child][fine local node a][coarse local node b]
+
+void galerkin_set_constants(int dim, const double* K0, cudaStream_t s) {
+    int nl = dim * (1 << dim);
+    cudaMemcpyToSymbolAsync(c_K0g, K0, sizeof(double) * nl * nl, 0, cudaMemcpyHostToDevice, s);
+    // Q[c][a][b] = prod_k w(c_k + a_k, b_k), w(pos, b) = 1 if pos == 2b, 1/2 if pos == 1, else 0
+    static double Q[512];
+    int na = 1 << dim;
+    for (int c = 0; c < na; ++c)
+        for (int a = 0; a < na; ++a)
+            for (int b = 0; b < na; ++b) {
+                double v = 1.0;
+                for (int k = 0; k < dim; ++k) {
+                    int sh = dim - 1 - k;
+                    int pos = ((c >> sh) & 1) + ((a >> sh) & 1);
+                    int bb = (b >> sh) & 1;
+                    double w = (pos == 1) ? 0.5 : (pos == 2 * bb ? 1.0 : 0.0);
+                    v *= w;
+                }
+                Q[(c * na + a) * na + b] = v;
+            }
+    cudaMemcpyToSymbolAsync(c_Q, Q, sizeof(double) * na * na * na, 0, cudaMemcpyHostToDevice, s);
+}
+
+__device__ __forceinline__ void node_coords(const LevelGeom& g, long long node, int* idx) {
+    long long t = node;
+    for (int k = g.dim - 1; k >= 0; --k) { idx[k] = (int)(t % g.nn[k]); t /= g.nn[k]; }
+}
+
+// ---------------------------------------------------------------- element matrices
+// Level-0 element matrices E_e M K0 M (only needed when levels == 1).
+template <int DIM>
+__global__ void elements_from_E_kernel(LevelGeom g, const double* __restrict__ E, const uint8_t* __restrict__ mask,
+                                       double* elm) {
+    constexpr int NA = 1 << DIM, NL = DIM * NA;
+    long long e = blockIdx.x;
+    int t = threadIdx.x;  // NL*NL threads
+    int row = t / NL, col = t % NL;
+    int ei[3] = {0, 0, 0};
+    long long tt = e;
+    for (int k = DIM - 1; k >= 0; --k) { ei[k] = (int)(tt % g.N[k]); tt /= g.N[k]; }
+    auto local_free = [&](int ld) {
+        int a = ld / DIM, comp = ld % DIM;
+        long long node = 0;
+        for (int k = 0; k < DIM; ++k) node = node * g.nn[k] + ei[k] + ((a >> (DIM - 1 - k)) & 1);
+        return ((mask[node] >> comp) & 1) ? 0.0 : 1.0;
+    };
+    elm[e * NL * NL + t] = E[e] * c_K0g[row * NL + col] * local_free(row) * local_free(col);
+}
+
+void elements_from_E(const LevelGeom& g, const double* E, const uint8_t* mask, double* elm, cudaStream_t s) {
+    if (g.dim == 2)
+        elements_from_E_kernel<2><<<(unsigned)g.nelem, 64, 0, s>>>(g, E, mask, elm);
+    else
+        elements_from_E_kernel<3><<<(unsigned)g.nelem, 576, 0, s>>>(g, E, mask, elm);
+}
+
+// One CTA per coarse element; thread (row, col) owns one entry of K_E.
+template <int DIM, bool FROM_E>
+__global__ void galerkin_kernel(LevelGeom gc, LevelGeom gf, const double* __restrict__ E,
+                                const double* __restrict__ elm_f, const uint8_t* __restrict__ mask_f,
+                                const uint8_t* __restrict__ mask_c, double* __restrict__ elm_c) {
+    constexpr int NA = 1 << DIM, NL = DIM * NA;
+    __shared__ double Kc[NL * NL];
+    __shared__ double T[NL * NL];
+    __shared__ double fr[NL];
+    const long long Ec = blockIdx.x;
+    const int t = threadIdx.x;
+    const int row = t / NL, col = t % NL;
+    int ci[3] = {0, 0, 0};
+    long long tt = Ec;
+    for (int k = DIM - 1; k >= 0; --k) { ci[k] = (int)(tt % gc.N[k]); tt /= gc.N[k]; }
+    double acc = 0.0;
+    for (int ch = 0; ch < NA; ++ch) {
+        int fi[3];
+        for (int k = 0; k < DIM; ++k) fi[k] = 2 * ci[k] + ((ch >> (DIM - 1 - k)) & 1);
+        long long fe = fi[0];
+        for (int k = 1; k < DIM; ++k) fe = fe * gf.N[k] + fi[k];
+        if (FROM_E) {
+            if (t < NL) {
+                int a = t / DIM, comp = t % DIM;
+                long long node = 0;
+                for (int k = 0; k < DIM; ++k) node = node * gf.nn[k] + fi[k] + ((a >> (DIM - 1 - k)) & 1);
+                fr[t] = ((mask_f[node] >> comp) & 1) ? 0.0 : 1.0;
+            }
+            __syncthreads();
+            Kc[t] = E[fe] * c_K0g[t] * fr[row] * fr[col];
+        } else {
+            Kc[t] = elm_f[fe * NL * NL + t];   // already masked at level l-1
+        }
+        __syncthreads();
+        // T[(a,k),(b2,k2)] = sum_a2 Kc[(a,k),(a2,k2)] Q[a2][b2]
+        {
+            const int b2 = col / DIM, k2 = col % DIM;
+            double s = 0.0;
+#pragma unroll
+            for (int a2 = 0; a2 < NA; ++a2) s = fma(Kc[row * NL + a2 * DIM + k2], c_Q[(ch * NA + a2) * NA + b2], s);
+            T[t] = s;
+        }
+        __syncthreads();
+        {
+            const int b = row / DIM, k = row % DIM;
+#pragma unroll
+            for (int a = 0; a < NA; ++a) acc = fma(c_Q[(ch * NA + a) * NA + b], T[(a * DIM + k) * NL + col], acc);
+        }
+        __syncthreads();
+    }
+    // coarse masks
+    auto cfree = [&](int ld) {
+        int a = ld / DIM, comp = ld % DIM;
+        long long node = 0;
+        for (int k = 0; k < DIM; ++k) node = node * gc.nn[k] + ci[k] + ((a >> (DIM - 1 - k)) & 1);
+        return ((mask_c[node] >> comp) & 1) ? 0.0 : 1.0;
+    };
+    elm_c[Ec * NL * NL + t] = acc * cfree(row) * cfree(col);
+}
+
+void galerkin_elements(const LevelGeom& gc, const LevelGeom& gf, const double* E, const double* elm_f,
+                       const uint8_t* mask_f, const uint8_t* mask_c, double* elm_c, cudaStream_t s) {
+    unsigned bl = (unsigned)gc.nelem;
+    if (gc.dim == 2) {
+        if (E) galerkin_kernel<2, true><<<bl, 64, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c);
+        else galerkin_kernel<2, false><<<bl, 64, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c);
+    } else {
+        if (E) galerkin_kernel<3, true><<<bl, 576, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c);
+        else galerkin_kernel<3, false><<<bl, 576, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c);
+    }
+}
+
+// ---------------------------------------------------------------- stencil assembly
+// st[(s*DIM + k)*DIM + k2][node] = sum over elements containing node (local a) and
+// node+delta_s (local b = a + delta_s) of elm[E][(a,k),(b,k2)]; identity at fixed DOFs.
+template <int DIM>
+__global__ void stencil_kernel(LevelGeom g, const double* __restrict__ elm, const uint8_t* __restrict__ mask,
+                               double* __restrict__ st) {
+    constexpr int NA = 1 << DIM, NL = DIM * NA;
+    constexpr int NS = DIM == 2 ? 9 : 27;
+    long long node = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int s = blockIdx.y;
+    if (node >= g.nnodes) return;
+    int idx[3] = {0, 0, 0};
+    node_coords(g, node, idx);
+    int dlt[3];
+    {
+        int ss = s;
+        for (int k = DIM - 1; k >= 0; --k) { dlt[k] = ss % 3 - 1; ss /= 3; }
+    }
+    double acc[DIM * DIM];
+#pragma unroll
+    for (int q = 0; q < DIM * DIM; ++q) acc[q] = 0.0;
+    for (int a = 0; a < NA; ++a) {
+        int b = 0;
+        bool ok = true;
+        long long el = 0;
+        for (int k = 0; k < DIM; ++k) {
+            int ab = (a >> (DIM - 1 - k)) & 1;
+            int bb = ab + dlt[k];
+            if (bb < 0 || bb > 1) ok = false;
+            b = b * 2 + (bb & 1);
+            int ek = idx[k] - ab;
+            if (ek < 0 || ek >= g.N[k]) ok = false;
+            el = el * g.N[k] + ek;
+        }
+        if (!ok) continue;
+        const double* m = elm + el * NL * NL;
+#pragma unroll
+        for (int k = 0; k < DIM; ++k)
+#pragma unroll
+            for (int k2 = 0; k2 < DIM; ++k2) acc[k * DIM + k2] += m[(a * DIM + k) * NL + b * DIM + k2];
+    }
+    const int mb = mask[node];
+    const bool center = (s == NS / 2);
+#pragma unroll
+    for (int k = 0; k < DIM; ++k)
+#pragma unroll
+        for (int k2 = 0; k2 < DIM; ++k2) {
+            double v = acc[k * DIM + k2];
+            if (center && k == k2 && ((mb >> k) & 1)) v = 1.0;
+            st[((long long)(s * DIM + k) * DIM + k2) * g.nnodes + node] = v;
+        }
+}
+
+void stencil_from_elements(const LevelGeom& g, const double* elm, uint8_t* mask, double* st, cudaStream_t s) {
+    int th = 128;
+    dim3 grid((unsigned)((g.nnodes + th - 1) / th), g.dim == 2 ? 9 : 27);
+    if (g.dim == 2)
+        stencil_kernel<2><<<grid, th, 0, s>>>(g, elm, mask, st);
+    else
+        stencil_kernel<3><<<grid, th, 0, s>>>(g, elm, mask, st);
+}
+
+// Diagonal from the stencil centre; free DOFs with zero Galerkin diagonal become fixed.
+template <int DIM>
+__global__ void stencil_diag_kernel(LevelGeom g, uint8_t* mask, double* st, double* Dinv, double* D) {
+    constexpr int NS = DIM == 2 ? 9 : 27;
+    long long node = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (node >= g.nnodes) return;
+    int mb = mask[node];
+    for (int k = 0; k < DIM; ++k) {
+        double* dp = st + ((long long)((NS / 2) * DIM + k) * DIM + k) * g.nnodes + node;
+        double dv = *dp;
+        if (!((mb >> k) & 1) && !(dv > 0.0)) {
+            mb |= 1 << k;
+            *dp = 1.0;
+            dv = 1.0;
+        }
+        if (D) D[DIM * node + k] = dv;
+        Dinv[DIM * node + k] = 1.0 / dv;
+    }
+    mask[node] = (uint8_t)mb;
+}
+
+void stencil_diag(const LevelGeom& g, const double* /*st*/, uint8_t* mask, double* st_rw, double* Dinv, double* D,
+                  cudaStream_t s) {
+    int th = 256;
+    unsigned bl = (unsigned)((g.nnodes + th - 1) / th);
+    if (g.dim == 2)
+        stencil_diag_kernel<2><<<bl, th, 0, s>>>(g, mask, st_rw, Dinv, D);
+    else
+        stencil_diag_kernel<3><<<bl, th, 0, s>>>(g, mask, st_rw, Dinv, D);
+}
+
+// ---------------------------------------------------------------- stencil operator kernels
+// Thread per node; all R vectors (chunks of RB) accumulated in registers so the
+// stencil (3^d d^2 doubles per node) is read once per chunk.
+template <int DIM, int OP, int RB>
+__global__ void __launch_bounds__(128) coarse_kernel(CoarseArgs a, int r0) {
+    constexpr int NS = DIM == 2 ? 9 : 27;
+    long long node = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (node >= a.g.nnodes) return;
+    if (a.done && *a.done) return;
+    int idx[3] = {0, 0, 0};
+    node_coords(a.g, node, idx);
+    const int nr = min(RB, a.R - r0);
+    bool act[RB];
+#pragma unroll
+    for (int q = 0; q < RB; ++q) act[q] = (q < nr) && (!a.active || a.active[r0 + q]);
+    double acc[RB][DIM];
+#pragma unroll
+    for (int q = 0; q < RB; ++q)
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) acc[q][k] = 0.0;
+    const long long nn = a.g.nnodes;
+#pragma unroll 1
+    for (int s = 0; s < NS; ++s) {
+        int dl[3] = {0, 0, 0};
+        int ss = s;
+        for (int k = DIM - 1; k >= 0; --k) { dl[k] = ss % 3 - 1; ss /= 3; }
+        bool ok = true;
+        long long q = 0;
+        for (int k = 0; k < DIM; ++k) {
+            int c = idx[k] + dl[k];
+            if (c < 0 || c >= a.g.nn[k]) ok = false;
+            q = q * a.g.nn[k] + c;
+        }
+        if (!ok) continue;
+        double blk[DIM * DIM];
+#pragma unroll
+        for (int e = 0; e < DIM * DIM; ++e) blk[e] = a.st[(long long)(s * DIM * DIM + e) * nn + node];
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr) {
+            if (!act[rr]) continue;
+            const double* xv = a.x + (long long)(r0 + rr) * a.g.ndof + (long long)DIM * q;
+            double xq[DIM];
+#pragma unroll
+            for (int k2 = 0; k2 < DIM; ++k2) xq[k2] = xv[k2];
+#pragma unroll
+            for (int k = 0; k < DIM; ++k)
+#pragma unroll
+                for (int k2 = 0; k2 < DIM; ++k2) acc[rr][k] = fma(blk[k * DIM + k2], xq[k2], acc[rr][k]);
+        }
+    }
+#pragma unroll
+    for (int rr = 0; rr < RB; ++rr) {
+        if (!act[rr]) continue;
+        const long long o = (long long)(r0 + rr) * a.g.ndof + (long long)DIM * node;
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) {
+            double v;
+            if (OP == COP_MATVEC) v = acc[rr][k];
+            else if (OP == COP_RESID) v = a.b[o + k] - acc[rr][k];
+            else v = a.x[o + k] + a.omega * a.Dinv[(long long)DIM * node + k] * (a.b[o + k] - acc[rr][k]);
+            a.y[o + k] = v;
+        }
+    }
+}
+
+template <int DIM, int OP>
+static void launch_coarse_dim(const CoarseArgs& a, cudaStream_t s) {
+    int th = 128;
+    unsigned bl = (unsigned)((a.g.nnodes + th - 1) / th);
+    for (int r0 = 0; r0 < a.R;) {
+        int rem = a.R - r0;
+        if (rem > 8) {
+            coarse_kernel<DIM, OP, 16><<<bl, th, 0, s>>>(a, r0);
+            r0 += 16;
+        } else if (rem > 4) {
+            coarse_kernel<DIM, OP, 8><<<bl, th, 0, s>>>(a, r0);
+            r0 += 8;
+        } else if (rem > 1) {
+            coarse_kernel<DIM, OP, 4><<<bl, th, 0, s>>>(a, r0);
+            r0 += 4;
+        } else {
+            coarse_kernel<DIM, OP, 1><<<bl, th, 0, s>>>(a, r0);
+            r0 += 1;
+        }
+    }
+}
+
+void coarse_apply(int op, const CoarseArgs& a, cudaStream_t s) {
+    if (a.g.dim == 2) {
+        if (op == COP_MATVEC) launch_coarse_dim<2, COP_MATVEC>(a, s);
+        else if (op == COP_RESID) launch_coarse_dim<2, COP_RESID>(a, s);
+        else launch_coarse_dim<2, COP_JACOBI>(a, s);
+    } else {
+        if (op == COP_MATVEC) launch_coarse_dim<3, COP_MATVEC>(a, s);
+        else if (op == COP_RESID) launch_coarse_dim<3, COP_RESID>(a, s);
+        else launch_coarse_dim<3, COP_JACOBI>(a, s);
+    }
+}

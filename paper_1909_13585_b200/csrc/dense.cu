@@ -1,0 +1,231 @@
+// Coarsest-level direct solve on the device ("dense
+// factorization"; the paper's coarsest solve is unstated).
+// Setup: the coarsest Galerkin operator (n_L <= a few thousand DOFs) is assembled
+// dense and inverted in place by blocked Gauss-Jordan (SPD => no pivoting needed,
+// block 32).  Per V-cycle: z = A^-1 r for all R vectors, one warp per row, so the
+// solve is a bandwidth-bound dense product instead of a latency-bound triangular
+// sweep.
+#include "kernels.h"
+
+static constexpr int GJ_NB = 32;
+
+template <int DIM>
+__global__ void dense_from_stencil_kernel(LevelGeom g, const double* __restrict__ st, double* A, long long ld) {
+    constexpr int NS = DIM == 2 ? 9 : 27;
+    long long node = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    int s = blockIdx.y;
+    if (node >= g.nnodes) return;
+    int idx[3] = {0, 0, 0};
+    long long t = node;
+    for (int k = DIM - 1; k >= 0; --k) { idx[k] = (int)(t % g.nn[k]); t /= g.nn[k]; }
+    int ss = s;
+    int dl[3];
+    for (int k = DIM - 1; k >= 0; --k) { dl[k] = ss % 3 - 1; ss /= 3; }
+    long long q = 0;
+    for (int k = 0; k < DIM; ++k) {
+        int c = idx[k] + dl[k];
+        if (c < 0 || c >= g.nn[k]) return;
+        q = q * g.nn[k] + c;
+    }
+    for (int k = 0; k < DIM; ++k)
+        for (int k2 = 0; k2 < DIM; ++k2)
+            A[(DIM * node + k) * ld + DIM * q + k2] = st[((long long)(s * DIM + k) * DIM + k2) * g.nnodes + node];
+    (void)NS;
+}
+
+void dense_from_stencil(const LevelGeom& g, const double* st, double* A, long long ld, cudaStream_t s) {
+    int th = 128;
+    dim3 grid((unsigned)((g.nnodes + th - 1) / th), g.dim == 2 ? 9 : 27);
+    if (g.dim == 2)
+        dense_from_stencil_kernel<2><<<grid, th, 0, s>>>(g, st, A, ld);
+    else
+        dense_from_stencil_kernel<3><<<grid, th, 0, s>>>(g, st, A, ld);
+}
+
+__global__ void pad_identity_kernel(double* A, long long n, long long npad) {
+    long long i = n + blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < npad) A[i * npad + i] = 1.0;
+}
+
+void dense_pad_identity(double* A, long long n, long long npad, cudaStream_t s) {
+    if (npad > n) pad_identity_kernel<<<1, GJ_NB, 0, s>>>(A, n, npad);
+}
+
+// In-place Gauss-Jordan inverse of the NB x NB diagonal block k (one CTA, NB*NB threads).
+__global__ void gj_diag_kernel(double* A, long long ld, int k0, double* P, int* status) {
+    __shared__ double S[GJ_NB][GJ_NB + 1];
+    const int i = threadIdx.y, j = threadIdx.x;
+    S[i][j] = A[(k0 + i) * ld + k0 + j];
+    __syncthreads();
+    for (int p = 0; p < GJ_NB; ++p) {
+        const double piv = S[p][p];
+        const double sip = S[i][p], spj = S[p][j], sij = S[i][j];
+        __syncthreads();
+        if (!(piv > 0.0)) {
+            if (i == 0 && j == 0) atomicOr(status, 2);
+        }
+        const double ip = 1.0 / piv;
+        double v;
+        if (i == p && j == p) v = ip;
+        else if (i == p) v = spj * ip;
+        else if (j == p) v = -sip * ip;
+        else v = sij - sip * spj * ip;
+        S[i][j] = v;
+        __syncthreads();
+    }
+    P[i * GJ_NB + j] = S[i][j];
+}
+
+// Rrow[t][j] = sum_s P[t][s] A[k0+s][j]   (new row panel), Ccol[i][t] = A[i][k0+t] (old column panel)
+__global__ void gj_panels_kernel(const double* A, long long ld, long long n, int k0, const double* P, double* Rrow,
+                                 double* Ccol) {
+    __shared__ double Ps[GJ_NB][GJ_NB];
+    const int tid = threadIdx.x;
+    for (int e = tid; e < GJ_NB * GJ_NB; e += blockDim.x) Ps[e / GJ_NB][e % GJ_NB] = P[e];
+    __syncthreads();
+    long long j = (long long)blockIdx.x * blockDim.x + tid;
+    if (j >= n) return;
+    double col[GJ_NB];
+#pragma unroll
+    for (int s = 0; s < GJ_NB; ++s) col[s] = A[(k0 + s) * ld + j];
+#pragma unroll 4
+    for (int t = 0; t < GJ_NB; ++t) {
+        double acc = 0.0;
+#pragma unroll
+        for (int s = 0; s < GJ_NB; ++s) acc = fma(Ps[t][s], col[s], acc);
+        Rrow[t * n + j] = acc;
+    }
+    // column panel: row j of A's column block (A symmetric in exact arithmetic, but
+    // read the column explicitly to stay exact for the unsymmetric rounding)
+#pragma unroll
+    for (int t = 0; t < GJ_NB; ++t) Ccol[j * GJ_NB + t] = A[j * ld + k0 + t];
+}
+
+// A[i][j] -= sum_t Ccol[i][t] Rrow[t][j] for all i, j (64x64 tile per CTA, 4x4 per thread).
+__global__ void __launch_bounds__(256) gj_update_kernel(double* A, long long ld, long long n, const double* Ccol,
+                                                        const double* Rrow) {
+    __shared__ double Cs[64][GJ_NB + 1];
+    __shared__ double Rs[GJ_NB][64 + 1];
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    const long long i0 = (long long)blockIdx.y * 64, j0 = (long long)blockIdx.x * 64;
+    for (int e = threadIdx.x; e < 64 * GJ_NB; e += 256) {
+        int r = e / GJ_NB, t = e % GJ_NB;
+        long long i = i0 + r;
+        Cs[r][t] = i < n ? Ccol[i * GJ_NB + t] : 0.0;
+        int t2 = e / 64, c = e % 64;
+        long long j = j0 + c;
+        Rs[t2][c] = j < n ? Rrow[t2 * n + j] : 0.0;
+    }
+    __syncthreads();
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+#pragma unroll 8
+    for (int t = 0; t < GJ_NB; ++t) {
+        double cv[4], rv[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) cv[a] = Cs[ty + 16 * a][t];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) rv[b] = Rs[t][tx + 16 * b];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = fma(cv[a], rv[b], acc[a][b]);
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        long long i = i0 + ty + 16 * a;
+        if (i >= n) continue;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            long long j = j0 + tx + 16 * b;
+            if (j < n) A[i * ld + j] -= acc[a][b];
+        }
+    }
+}
+
+// Overwrite the pivot row/column panels: A[k][j] = Rrow, A[i][k] = -Ccol[i] P, A[k][k] = P.
+__global__ void gj_fix_kernel(double* A, long long ld, long long n, int k0, const double* P, const double* Rrow,
+                              const double* Ccol) {
+    __shared__ double Ps[GJ_NB][GJ_NB];
+    for (int e = threadIdx.x; e < GJ_NB * GJ_NB; e += blockDim.x) Ps[e / GJ_NB][e % GJ_NB] = P[e];
+    __syncthreads();
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const bool inblk = (i >= k0 && i < k0 + GJ_NB);
+    if (inblk) {
+        int t = (int)(i - k0);
+        for (long long j = 0; j < n; ++j) {
+            if (j >= k0 && j < k0 + GJ_NB) A[i * ld + j] = Ps[t][j - k0];
+            else A[i * ld + j] = Rrow[t * n + j];
+        }
+    } else {
+        double c[GJ_NB];
+#pragma unroll
+        for (int s = 0; s < GJ_NB; ++s) c[s] = Ccol[i * GJ_NB + s];
+#pragma unroll 4
+        for (int t = 0; t < GJ_NB; ++t) {
+            double acc = 0.0;
+#pragma unroll
+            for (int s = 0; s < GJ_NB; ++s) acc = fma(c[s], Ps[s][t], acc);
+            A[i * ld + k0 + t] = -acc;
+        }
+    }
+}
+
+void dense_spd_inverse(double* A, long long npad, double* work, int* d_status, cudaStream_t s) {
+    double* P = work;
+    double* Rrow = work + GJ_NB * GJ_NB;
+    double* Ccol = Rrow + npad * GJ_NB;
+    const long long n = npad;
+    for (long long k0 = 0; k0 < n; k0 += GJ_NB) {
+        gj_diag_kernel<<<1, dim3(GJ_NB, GJ_NB), 0, s>>>(A, n, (int)k0, P, d_status);
+        gj_panels_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(A, n, n, (int)k0, P, Rrow, Ccol);
+        dim3 g((unsigned)((n + 63) / 64), (unsigned)((n + 63) / 64));
+        gj_update_kernel<<<g, 256, 0, s>>>(A, n, n, Ccol, Rrow);
+        gj_fix_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(A, n, n, (int)k0, P, Rrow, Ccol);
+    }
+}
+
+// z[r][i] = sum_j Ainv[i][j] rvec[r][j]; one warp per row, RB vectors per pass.
+template <int RB>
+__global__ void __launch_bounds__(256) dense_apply_kernel(const double* __restrict__ Ainv, long long ld, long long n,
+                                                          const double* __restrict__ rv, double* __restrict__ z, int R,
+                                                          int r0, const int* active, const int* done) {
+    const int lane = threadIdx.x & 31;
+    long long i = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= n) return;
+    if (done && *done) return;
+    const int nr = min(RB, R - r0);
+    bool act[RB];
+#pragma unroll
+    for (int q = 0; q < RB; ++q) act[q] = q < nr && (!active || active[r0 + q]);
+    double acc[RB];
+#pragma unroll
+    for (int q = 0; q < RB; ++q) acc[q] = 0.0;
+    const double* row = Ainv + i * ld;
+    for (long long j = lane; j < n; j += 32) {
+        const double a = row[j];
+#pragma unroll
+        for (int q = 0; q < RB; ++q)
+            if (act[q]) acc[q] = fma(a, rv[(long long)(r0 + q) * n + j], acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < RB; ++q) {
+        double v = warp_sum(acc[q]);
+        if (lane == 0 && act[q]) z[(long long)(r0 + q) * n + i] = v;
+    }
+}
+
+void dense_apply(const double* Ainv, long long ld, long long n, const double* r, double* z, int R, const int* active,
+                 const int* done, cudaStream_t s) {
+    unsigned bl = (unsigned)((n + 7) / 8);
+    for (int r0 = 0; r0 < R;) {
+        int rem = R - r0;
+        if (rem > 4) { dense_apply_kernel<8><<<bl, 256, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); r0 += 8; }
+        else if (rem > 1) { dense_apply_kernel<4><<<bl, 256, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); r0 += 4; }
+        else { dense_apply_kernel<1><<<bl, 256, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); r0 += 1; }
+    }
+}

@@ -1,0 +1,100 @@
+// Host-side launcher declarations shared by the translation units of libmgcg.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "common.cuh"
+
+// ---------------------------------------------------------------- fine level (matrix-free)
+enum FineOp { FOP_MATVEC = 0, FOP_RESID = 1, FOP_JACOBI = 2, FOP_CGP = 3 };
+
+struct FineArgs {
+    LevelGeom g;
+    const double* E;        // nelem
+    const uint8_t* mask;    // nnodes, bit k = comp k fixed
+    const double* x;        // input vectors (R, ndof)      [MATVEC/RESID/JACOBI]
+    const double* z;        // CGP: p_new = z + beta p_in
+    const double* pin;
+    double* pout;
+    const double* b;        // RESID/JACOBI right-hand side
+    const double* Dinv;     // JACOBI: ndof
+    double* y;              // output vectors (R, ndof)
+    double omega;
+    const double* beta;     // CGP: per RHS
+    const int* active;      // per RHS or NULL
+    const int* done;        // or NULL
+    double* partial;        // dot partials [R][items] or NULL
+    int R;
+};
+
+void fine_set_constants(int dim, const double* K0, cudaStream_t s);
+// Launch one fine-level layer-march kernel; returns number of dot partial items per RHS.
+int fine_apply(int op, const FineArgs& a, cudaStream_t s);
+int fine_items(const LevelGeom& g);
+void fine_diag(const LevelGeom& g, const double* E, const uint8_t* mask, double* Dinv, double* D, cudaStream_t s);
+
+// ---------------------------------------------------------------- coarse levels (assembled stencils)
+enum CoarseOp { COP_MATVEC = 0, COP_RESID = 1, COP_JACOBI = 2 };
+
+struct CoarseArgs {
+    LevelGeom g;
+    const double* st;       // stencil, SoA [3^d*d*d][nnodes]
+    const double* x;
+    const double* b;
+    const double* Dinv;
+    double* y;
+    double omega;
+    const int* active;
+    const int* done;
+    int R;
+};
+void coarse_apply(int op, const CoarseArgs& a, cudaStream_t s);
+
+// Galerkin: coarse element matrices from children (level l-1) element matrices, or
+// from E_e * K0 when from_E (level 0 children).
+void galerkin_set_constants(int dim, const double* K0, cudaStream_t s);
+void galerkin_elements(const LevelGeom& gc, const LevelGeom& gf, const double* E /*if from_E*/,
+                       const double* elm_f, const uint8_t* mask_f, const uint8_t* mask_c,
+                       double* elm_c, cudaStream_t s);
+void elements_from_E(const LevelGeom& g, const double* E, const uint8_t* mask, double* elm, cudaStream_t s);
+void stencil_from_elements(const LevelGeom& g, const double* elm, uint8_t* mask, double* st, cudaStream_t s);
+void stencil_diag(const LevelGeom& g, const double* st, uint8_t* mask, double* st_rw, double* Dinv, double* D,
+                  cudaStream_t s);
+
+// ---------------------------------------------------------------- transfers
+void restrict_apply(const LevelGeom& gf, const LevelGeom& gc, const uint8_t* mf, const uint8_t* mc,
+                    const double* fine, double* coarse, int R, const int* active, const int* done, cudaStream_t s);
+void prolong_add(const LevelGeom& gf, const LevelGeom& gc, const uint8_t* mf, const uint8_t* mc,
+                 const double* coarse, double* fine, int R, const int* active, const int* done, bool accumulate,
+                 cudaStream_t s);
+
+// ---------------------------------------------------------------- dense coarsest
+void dense_from_stencil(const LevelGeom& g, const double* st, double* A, long long ld, cudaStream_t s);
+void dense_pad_identity(double* A, long long n, long long npad, cudaStream_t s);
+// In-place SPD inverse by blocked Gauss-Jordan (block 32). Work buffers sized npad*32*2 + 32*32.
+// Returns via *d_status (device int) nonzero if a non-positive pivot is met.
+void dense_spd_inverse(double* A, long long npad, double* work, int* d_status, cudaStream_t s);
+void dense_apply(const double* Ainv, long long ld, long long n, const double* r, double* z, int R,
+                 const int* active, const int* done, cudaStream_t s);
+
+// ---------------------------------------------------------------- CG vector ops and reductions
+int vec_blocks(long long n);
+void cg_pointwise_jacobi(long long n, int R, const double* r, const double* Dinv, double omega, double* z,
+                         const int* active, const int* done, cudaStream_t s);
+// x += alpha p; r -= alpha q; z = omega Dinv r; partial r.r
+void cg_update(long long n, int R, const double* alpha, const double* p, const double* q, double* x, double* r,
+               const double* Dinv, double omega, double* z, double* partial, const int* active, const int* done,
+               cudaStream_t s);
+void vec_dot(long long n, int R, const double* a, const double* b, double* partial, const int* active,
+             const int* done, cudaStream_t s);
+void vec_mask_copy(long long nnodes, int dim, int R, const uint8_t* mask, const double* src, double* dst,
+                   cudaStream_t s);
+void vec_axpy_masked_restart(long long n, int R, const double* t, double* r, const int* restart, cudaStream_t s);
+
+enum ScalarMode { SM_INIT = 0, SM_ALPHA = 1, SM_CONV = 2, SM_BETA = 3, SM_RZ0 = 4, SM_TRUE = 5, SM_BB = 6 };
+void cg_scalars(int mode, int R, const double* partial, int items, CgCtl c, double tol, cudaStream_t s);
+
+// ---------------------------------------------------------------- stress stiffness G(u) phi
+void stress_set_constants(int dim, double nu, cudaStream_t s);
+void stress_sigma(const LevelGeom& g, const double* Es, const double* u, double* sig, cudaStream_t s);
+void stress_apply(const LevelGeom& g, const double* sig, const uint8_t* mask, const double* phi, double* y,
+                  int nphi, cudaStream_t s);

@@ -1,0 +1,131 @@
+// Grid transfers between consecutive levels (PAPER.md:146 I^j_{j+1}, I^{j+1}_j;
+// Alg. 2 l.9 :715).
+// P = bilinear / trilinear nodal interpolation (tensor product of the 1-D stencil
+// [1/2, 1, 1/2]), restriction R = P^T, both masked by the free-DOF masks of the
+// two levels (reading r11: P_m = M_f P M_c).
+#include "kernels.h"
+
+// coarse(I,k) = free_c(I,k) * sum_{delta in {-1,0,1}^d} w(delta) free_f(2I+delta,k) fine(2I+delta,k)
+template <int DIM>
+__global__ void restrict_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* __restrict__ mf,
+                                const uint8_t* __restrict__ mc, const double* __restrict__ fine,
+                                double* __restrict__ coarse, int R, const int* active, const int* done) {
+    long long I = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (I >= gc.nnodes) return;
+    if (done && *done) return;
+    int ci[3] = {0, 0, 0};
+    long long t = I;
+    for (int k = DIM - 1; k >= 0; --k) { ci[k] = (int)(t % gc.nn[k]); t /= gc.nn[k]; }
+    const int mcb = mc[I];
+    constexpr int NS = DIM == 2 ? 9 : 27;
+    long long fnode[NS];
+    double wgt[NS];
+    int fm[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        int ss = s;
+        long long q = 0;
+        double w = 1.0;
+        bool ok = true;
+        int dl[3];
+        for (int k = DIM - 1; k >= 0; --k) { dl[k] = ss % 3 - 1; ss /= 3; }
+        for (int k = 0; k < DIM; ++k) {
+            int f = 2 * ci[k] + dl[k];
+            if (f < 0 || f >= gf.nn[k]) ok = false;
+            q = q * gf.nn[k] + f;
+            if (dl[k] != 0) w *= 0.5;
+        }
+        fnode[s] = ok ? q : -1;
+        wgt[s] = w;
+        fm[s] = ok ? mf[q] : 0xff;
+    }
+    for (int r = 0; r < R; ++r) {
+        if (active && !active[r]) continue;
+        const double* fv = fine + (long long)r * gf.ndof;
+        double acc[DIM];
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) acc[k] = 0.0;
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            if (fnode[s] < 0) continue;
+#pragma unroll
+            for (int k = 0; k < DIM; ++k)
+                if (!((fm[s] >> k) & 1)) acc[k] = fma(wgt[s], fv[DIM * fnode[s] + k], acc[k]);
+        }
+        double* cv = coarse + (long long)r * gc.ndof + DIM * I;
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) cv[k] = ((mcb >> k) & 1) ? 0.0 : acc[k];
+    }
+}
+
+void restrict_apply(const LevelGeom& gf, const LevelGeom& gc, const uint8_t* mf, const uint8_t* mc,
+                    const double* fine, double* coarse, int R, const int* active, const int* done, cudaStream_t s) {
+    int th = 128;
+    unsigned bl = (unsigned)((gc.nnodes + th - 1) / th);
+    if (gf.dim == 2)
+        restrict_kernel<2><<<bl, th, 0, s>>>(gf, gc, mf, mc, fine, coarse, R, active, done);
+    else
+        restrict_kernel<3><<<bl, th, 0, s>>>(gf, gc, mf, mc, fine, coarse, R, active, done);
+}
+
+// fine(i,k) (+)= free_f(i,k) * sum_I w free_c(I,k) coarse(I,k): along each axis an even
+// fine index takes the coincident coarse node (w = 1), an odd one the two neighbours (1/2 each).
+template <int DIM>
+__global__ void prolong_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* __restrict__ mf,
+                               const uint8_t* __restrict__ mc, const double* __restrict__ coarse,
+                               double* __restrict__ fine, int R, const int* active, const int* done, bool accumulate) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= gf.nnodes) return;
+    if (done && *done) return;
+    int fi[3] = {0, 0, 0};
+    long long t = i;
+    for (int k = DIM - 1; k >= 0; --k) { fi[k] = (int)(t % gf.nn[k]); t /= gf.nn[k]; }
+    const int mfb = mf[i];
+    constexpr int NC = 1 << DIM;
+    long long cn[NC];
+    double wgt[NC];
+    int cm[NC];
+#pragma unroll
+    for (int s = 0; s < NC; ++s) {
+        long long q = 0;
+        double w = 1.0;
+        bool ok = true;
+        for (int k = 0; k < DIM; ++k) {
+            int bit = (s >> (DIM - 1 - k)) & 1;
+            int c;
+            if (fi[k] & 1) { c = (fi[k] >> 1) + bit; w *= 0.5; }
+            else { if (bit) { ok = false; } c = fi[k] >> 1; }
+            q = q * gc.nn[k] + c;
+        }
+        cn[s] = ok ? q : 0; wgt[s] = ok ? w : 0.0; cm[s] = ok ? mc[q] : 0xff;
+    }
+    for (int r = 0; r < R; ++r) {
+        if (active && !active[r]) continue;
+        const double* cv = coarse + (long long)r * gc.ndof;
+        double acc[DIM];
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) acc[k] = 0.0;
+#pragma unroll
+        for (int s = 0; s < NC; ++s)
+#pragma unroll
+            for (int k = 0; k < DIM; ++k)
+                if (!((cm[s] >> k) & 1)) acc[k] = fma(wgt[s], cv[DIM * cn[s] + k], acc[k]);
+        double* fv = fine + (long long)r * gf.ndof + DIM * i;
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) {
+            double v = ((mfb >> k) & 1) ? 0.0 : acc[k];
+            fv[k] = accumulate ? fv[k] + v : v;
+        }
+    }
+}
+
+void prolong_add(const LevelGeom& gf, const LevelGeom& gc, const uint8_t* mf, const uint8_t* mc,
+                 const double* coarse, double* fine, int R, const int* active, const int* done, bool accumulate,
+                 cudaStream_t s) {
+    int th = 128;
+    unsigned bl = (unsigned)((gf.nnodes + th - 1) / th);
+    if (gf.dim == 2)
+        prolong_kernel<2><<<bl, th, 0, s>>>(gf, gc, mf, mc, coarse, fine, R, active, done, accumulate);
+    else
+        prolong_kernel<3><<<bl, th, 0, s>>>(gf, gc, mf, mc, coarse, fine, R, active, done, accumulate);
+}

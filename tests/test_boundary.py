@@ -1,0 +1,66 @@
+"""The C-ABI library builds for sm_100a, loads without a GPU, and exports every
+symbol include/mgcg.h declares (CPU; no compute calls)."""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LIB = os.path.join(ROOT, "paper_1909_13585_b200", "_lib", "libmgcg.so")
+HDR = os.path.join(ROOT, "include", "mgcg.h")
+
+
+@pytest.fixture(scope="module")
+def libpath():
+    if not os.path.exists(LIB):
+        subprocess.run(["make", "-C", os.path.join(ROOT, "paper_1909_13585_b200", "csrc"), "-j8"], check=True)
+    return LIB
+
+
+def header_functions():
+    txt = open(HDR).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:mg_status|const char\*|long long)\s+(\w+)\s*\(", txt, flags=re.M)))
+
+
+def test_header_declares_the_north_star_calls():
+    fns = header_functions()
+    for name in ("mg_setup", "mgcg_solve", "stress_stiffness_apply"):
+        assert name in fns
+
+
+def test_library_exports_all_header_symbols(libpath):
+    lib = ctypes.CDLL(libpath)
+    for name in header_functions():
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", libpath], capture_output=True, text=True).stdout
+    for name in header_functions():
+        assert re.search(rf"\bT {name}$", out, flags=re.M), name
+
+
+def test_binding_names_match_header(libpath):
+    import paper_1909_13585_b200 as mg
+    from paper_1909_13585_b200 import _lib
+    assert sorted(_lib.EXPORTED) == header_functions()
+    for name in header_functions():
+        if name not in ("mg_strerror", "mg_last_error"):
+            assert hasattr(mg, name), name
+    assert _lib.lib.mg_strerror(2).decode().startswith("element counts")
+
+
+def test_sass_is_sm100a(libpath):
+    out = subprocess.run(["cuobjdump", "-lelf", libpath], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_product_path_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_1909_13585_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(from|import)\s+oracle\b", src, flags=re.M), f
+                assert "oracle/" not in src.replace("oracle/`", ""), f
