@@ -1,0 +1,346 @@
+"""Benchmark of the fine-grid solve path (BASELINE.json metric) on B200.
+
+One step = one pass of the whole hot path for one design:
+  mg_update_modulus (a1: fine diagonal, Galerkin coarse operators, coarsest inverse)
+  + mgcg_solve of all R right-hand sides to rel. residual tol (a2-a7)
+  + stress_stiffness_apply G(u) phi for the config's phi vectors (a8; u = state solution).
+metric: fine-grid DOF*RHS*iter/s = n * sum_k iters_k / t_step  (plus MGCG solves/s).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl reference]
+
+N > 1 is launched by torchrun (one process per GPU); round 1 runs independent
+replicas per rank (weak scaling, no data-path collective), see DESIGN.md.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads import generate, get_config, n_dofs  # noqa: E402
+
+METRIC = "fine-grid DOF*RHS*iter/s (MGCG, fp64, rel. residual 1e-10)"
+UNIT = "DOF*RHS*iter/s"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                smax = float(p[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def traffic_from_profiles(cfg_name):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get(cfg_name)
+    return None
+
+
+# --------------------------------------------------------------------------- our arm
+def run_ours(args, cfg):
+    import torch
+    import paper_1909_13585_b200 as mg
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    # replicas: each rank its own seeded design of the same config (weak scaling)
+    inp = generate(cfg if rank == 0 else get_config(cfg.name, seed=cfg.seed + 100 * rank))
+    n = n_dofs(cfg.nel)
+    R = cfg.nrhs
+    nphi = max(cfg.nphi, 0)
+    E = torch.from_numpy(inp["E"]).to(dev)
+    Es = torch.from_numpy(inp["Es"]).to(dev)
+    fixed = torch.from_numpy(inp["fixed"]).to(dev)
+    rhs = torch.from_numpy(inp["rhs"]).to(dev)
+    phi = torch.from_numpy(inp["phi"]).to(dev) if nphi else None
+    x = torch.empty_like(rhs)
+    y = torch.empty((nphi, n), dtype=torch.float64, device=dev) if nphi else None
+    stream = torch.cuda.current_stream()
+    t0 = time.time()
+    h = mg.mg_setup(cfg.nel, E, fixed, cfg.levels)
+    torch.cuda.synchronize()
+    setup_first_s = time.time() - t0
+
+    def step():
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record(stream)
+        mg.mg_update_modulus(h, E)
+        ev[1].record(stream)
+        rep = mg.mgcg_solve(h, rhs, cfg.tol, x)
+        ev[2].record(stream)
+        if nphi:
+            mg.stress_stiffness_apply(h, Es, x[0], phi, y)
+        ev[3].record(stream)
+        return rep, ev
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    l0 = mg.mg_kernel_launches(h)
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    reps, evs = [], []
+    for _ in range(args.steps):
+        rep, ev = step()
+        reps.append(rep)
+        evs.append(ev)
+    end.record(stream)
+    torch.cuda.synchronize()
+    launches = mg.mg_kernel_launches(h) - l0
+    ms_total = start.elapsed_time(end)
+    phases = np.array([[e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3])] for e in evs])
+    dofiters = [n * sum(r["iters"]) for r in reps]
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+        d = torch.tensor([float(sum(dofiters))], dtype=torch.float64, device=dev)
+        dist.all_reduce(d, op=dist.ReduceOp.SUM)
+        total_dofiters = float(d.item())
+    else:
+        total_dofiters = float(sum(dofiters))
+    clocks = clk.stop()
+    ms_step = ms_total / args.steps
+    value = total_dofiters / (ms_total / 1e3)
+
+    # ---- dominant kernel (fine EbE operator) timed alone with CUDA events on the launch stream
+    hbm, peak_kind = peaks()
+    xr = torch.randn((R, n), dtype=torch.float64, device=dev)
+    yr = torch.empty_like(xr)
+    for _ in range(3):
+        mg.mg_matvec(h, 0, xr, yr)
+    nrep = 20
+    flush = torch.empty(int(256e6) // 8, dtype=torch.float64, device=dev)
+    kt = []
+    for _ in range(nrep):
+        flush.fill_(1.0)   # evict L2 (inputs are larger than L2 anyway)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        mg.mg_matvec(h, 0, xr, yr)
+        b.record(stream)
+        b.synchronize()
+        kt.append(a.elapsed_time(b))
+    kms = float(np.median(kt))
+    m = int(np.prod(cfg.nel))
+    alg_bytes = 8.0 * (2.0 * n * R + m)
+    achieved = alg_bytes / (kms / 1e3) / 1e9
+    del flush
+
+    # ---- e2e: same step through the C ABI with pinned HOST buffers (H2D/D2H inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: torch.from_numpy(a).pin_memory().numpy()
+        hE, hEs, hrhs = pin(inp["E"]), pin(inp["Es"]), pin(inp["rhs"])
+        hphi = pin(inp["phi"]) if nphi else None
+        hx = torch.empty((R, n), dtype=torch.float64).pin_memory().numpy()
+        hy = torch.empty((max(nphi, 1), n), dtype=torch.float64).pin_memory().numpy()
+
+        def e2e_step():
+            mg.mg_update_modulus(h, hE)
+            rep = mg.mgcg_solve(h, hrhs, cfg.tol, hx)
+            if nphi:
+                mg.stress_stiffness_apply(h, hEs, np.ascontiguousarray(hx[0]), hphi, hy[:nphi])
+            return rep
+
+        e2e_step()
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        its = 0
+        for _ in range(max(1, min(args.steps, 3))):
+            rep = e2e_step()
+            its += n * sum(rep["iters"])
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t1
+        nst = max(1, min(args.steps, 3))
+        h2d = 8 * (inp["E"].size + R * n + (inp["Es"].size + n + nphi * n if nphi else 0))
+        d2h = 8 * (R * n + nphi * n)
+        e2e = {"value": its / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": 1e3 * dt / nst}
+
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE recipe)",
+        "config": {"workload": f"{cfg.name}: {'Q4' if cfg.dim == 2 else 'H8'} {'x'.join(map(str, cfg.nel))}, "
+                               f"{R} RHS, {cfg.levels} levels, G(u)phi x{nphi}",
+                   "ndof": n, "nrhs": R, "levels": cfg.levels, "tol": cfg.tol,
+                   "parallelism": "replicas" if ws > 1 else "single",
+                   "l2": "inputs larger than L2 (fine R-vector %.0f MB)" % (8 * n * R / 1e6)},
+        "solves_per_s": 1e3 / ms_step,
+        "phase_ms": {"setup": float(phases[:, 0].mean()), "solve": float(phases[:, 1].mean()),
+                     "stress_apply": float(phases[:, 2].mean())},
+        "iters": reps[-1]["iters"], "true_relres_max": max(reps[-1]["true_relres"]),
+        "first_setup_s": setup_first_s,
+        "gpu_launches": int(launches),
+        "roofline": {"kernel": "fine_ebe_matvec (fine2d/3d_kernel)", "bound": "hbm", "achieved": achieved,
+                     "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": traffic_from_profiles(cfg.name), "alg_bytes_per_launch": alg_bytes,
+                     "kernel_ms": kms},
+        "clocks": clocks,
+        "e2e": e2e,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        result["cpu_baseline"] = cpu_baseline(cfg, inp)
+    if ws > 1:
+        torch.distributed.barrier()
+    mg.mg_destroy(h)
+    return result if rank == 0 else None
+
+
+# --------------------------------------------------------------------------- oracle (CPU) arm
+def oracle_sample(cfg, inp):
+    """Bounded sample of the same workload with the CPU oracle as it stands:
+    assemble K, build the scipy MG hierarchy, PCG-solve the state RHS (1 of R) to tol."""
+    from oracle import assemble, mg as omg, solve
+    t = time.perf_counter()
+    K = assemble.assemble_K(cfg.nel, inp["E"], inp["fixed"])
+    H = omg.Hierarchy(cfg.nel, K, inp["fixed"], cfg.levels)
+    V = solve._VCycle(H, 0.6, 1)
+    _, it = solve.pcg(K, inp["rhs"][0], V.apply, cfg.tol)
+    dt = time.perf_counter() - t
+    return n_dofs(cfg.nel) * it / dt, dt, it
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def cpu_baseline(cfg, inp):
+    v, dt, it = oracle_sample(cfg, inp)
+    return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{cfg.name}: scipy assembly + Galerkin MG hierarchy + PCG of the state RHS (1 of {cfg.nrhs}) "
+                      f"to {cfg.tol:g}, {it} iterations, {dt:.1f} s (SpMV/SuperLU single-threaded; "
+                      f"{cpu_cores()} cores visible)"}
+
+
+def run_reference(args, cfg):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return None
+    inp = generate(cfg)
+    for _ in range(args.warmup if args.warmup <= 1 else 1):
+        pass   # the oracle has no warm-up state; one sample per step
+    vals, dts = [], []
+    steps = max(1, min(args.steps, 3))
+    for _ in range(steps):
+        v, dt, it = oracle_sample(cfg, inp)
+        vals.append(v)
+        dts.append(dt)
+    value = float(np.median(vals))
+    return {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * float(np.median(dts)), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE recipe)",
+        "config": {"workload": f"{cfg.name} (oracle sample: state RHS only)", "ndof": n_dofs(cfg.nel)},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"{cfg.name}: assembly + MG hierarchy + PCG of the state RHS to {cfg.tol:g}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    cfg = get_config(args.config)
+    res = run_reference(args, cfg) if args.impl == "reference" else run_ours(args, cfg)
+    if res is not None:
+        print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()

@@ -157,7 +157,7 @@ void vec_axpy_masked_restart(long long n, int R, const double* t, double* r, con
 // One CTA: warp w sums the partials of RHS w, w+16, ... in a fixed order, then
 // the scalar CG logic runs per RHS.
 __global__ void __launch_bounds__(512) scalars_kernel(int mode, int R, const double* __restrict__ partial, int items,
-                                                      CgCtl c, double tol) {
+                                                      CgCtl c, double tol, int aux) {
     __shared__ int any_active;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if (threadIdx.x == 0) any_active = 0;
@@ -177,6 +177,8 @@ __global__ void __launch_bounds__(512) scalars_kernel(int mode, int R, const dou
                     c.active[r] = v > 0.0 ? 1 : 0;
                     c.iters[r] = 0;
                     c.beta[r] = 0.0;
+                    c.alpha[r] = 0.0;
+                    c.xalpha[r] = 0.0;
                     c.rr[r] = v;
                     break;
                 case SM_RZ0:  // initial r.z
@@ -192,6 +194,8 @@ __global__ void __launch_bounds__(512) scalars_kernel(int mode, int R, const dou
                         } else {
                             c.alpha[r] = c.rz[r] / v;
                         }
+                        c.xalpha[r] = c.alpha[r];   // x += alpha p applied later (deferred)
+                        c.xbuf[r] = aux;
                     }
                     break;
                 case SM_CONV:
@@ -209,6 +213,7 @@ __global__ void __launch_bounds__(512) scalars_kernel(int mode, int R, const dou
                     break;
                 case SM_TRUE:
                     c.tt[r] = v;
+                    c.xalpha[r] = 0.0;
                     break;
                 default:
                     break;
@@ -220,6 +225,51 @@ __global__ void __launch_bounds__(512) scalars_kernel(int mode, int R, const dou
     if (threadIdx.x == 0) *c.done = any_active ? 0 : 1;
 }
 
-void cg_scalars(int mode, int R, const double* partial, int items, CgCtl c, double tol, cudaStream_t s) {
-    scalars_kernel<<<1, 512, 0, s>>>(mode, R, partial, items, c, tol);
+void cg_scalars(int mode, int R, const double* partial, int items, CgCtl c, double tol, cudaStream_t s, int aux) {
+    scalars_kernel<<<1, 512, 0, s>>>(mode, R, partial, items, c, tol, aux);
+}
+
+// r_out = r_in - alpha q ; partial r.r ; z1 = omega Dinv r_out
+__global__ void __launch_bounds__(VEC_THREADS) rupdate_kernel(long long n, const double* __restrict__ alpha,
+                                                              const double* __restrict__ rin,
+                                                              const double* __restrict__ q, double* __restrict__ rout,
+                                                              const double* __restrict__ Dinv, double omega,
+                                                              double* __restrict__ z1, double* partial,
+                                                              const int* active, const int* done) {
+    const int rr = blockIdx.y;
+    if (done && *done) return;
+    if (active && !active[rr]) return;
+    const double al = alpha[rr];
+    const long long o = (long long)rr * n;
+    double acc = 0.0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double v = fma(-al, q[o + i], rin[o + i]);
+        rout[o + i] = v;
+        acc = fma(v, v, acc);
+        if (z1) z1[o + i] = omega * Dinv[i] * v;
+    }
+    block_partial(acc, partial, (long long)rr * gridDim.x + blockIdx.x);
+}
+
+void cg_rupdate(long long n, int R, const double* alpha, const double* rin, const double* q, double* rout,
+                const double* Dinv, double omega, double* z1, double* partial, const int* active, const int* done,
+                cudaStream_t s) {
+    dim3 g(vec_blocks(n), R);
+    rupdate_kernel<<<g, VEC_THREADS, 0, s>>>(n, alpha, rin, q, rout, Dinv, omega, z1, partial, active, done);
+}
+
+__global__ void flush_x_kernel(long long n, CgCtl c, const double* __restrict__ p0, const double* __restrict__ p1,
+                               double* __restrict__ x) {
+    const int rr = blockIdx.y;
+    const double al = c.xalpha[rr];
+    if (al == 0.0) return;
+    const double* p = c.xbuf[rr] ? p1 : p0;
+    const long long o = (long long)rr * n;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        x[o + i] = fma(al, p[o + i], x[o + i]);
+}
+
+void cg_flush_x(long long n, int R, CgCtl c, const double* p0, const double* p1, double* x, cudaStream_t s) {
+    dim3 g(vec_blocks(n), R);
+    flush_x_kernel<<<g, VEC_THREADS, 0, s>>>(n, c, p0, p1, x);
 }

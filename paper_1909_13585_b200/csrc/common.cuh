@@ -24,6 +24,8 @@ struct CgCtl {
     double* bb;       // b.b
     double* pq;       // p.q
     double* tt;       // true residual t.t
+    double* xalpha;   // deferred x update alpha (applied by the next CGP kernel or the flush)
+    int* xbuf;        // which p buffer holds the p of xalpha (0/1)
     int* active;      // 1 = still iterating
     int* iters;
     int* done;        // 1 = no active RHS

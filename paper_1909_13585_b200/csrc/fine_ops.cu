@@ -30,6 +30,7 @@ static constexpr int CHUNK2 = 32;
 static constexpr int CHUNK3 = 16;
 
 int fine_items(const LevelGeom& g) {
+    if (g.dim == 2) return march2_items(M2_MATVEC, g, nullptr);
     int ncols = g.nn[g.dim - 1];
     int nct = (ncols + COLS_PER_WARP - 1) / COLS_PER_WARP;
     int chunk = g.dim == 2 ? CHUNK2 : CHUNK3;
@@ -68,7 +69,7 @@ __device__ __forceinline__ void load_node(const FineArgs& a, long long vbase, lo
 // Epilogue at an owned output node.  acc = (K M x) row values, raw = unmasked x.
 template <int DIM, int OP>
 __device__ __forceinline__ void finish_node(const FineArgs& a, long long vbase, long long node, int mbits,
-                                            const double* acc, const double* raw, double& dot) {
+                                            const double* acc, const double* raw, double& dot, double xal) {
     const long long o = vbase + (long long)DIM * node;
     double out[DIM];
 #pragma unroll
@@ -83,98 +84,16 @@ __device__ __forceinline__ void finish_node(const FineArgs& a, long long vbase, 
             out[k] = raw[k] + a.omega * a.Dinv[(long long)DIM * node + k] * (bk - ax);
             dot += bk * out[k];
         }
-        if (OP == FOP_CGP) dot += raw[k] * ax;
+        if (OP == FOP_CGP) {
+            dot += raw[k] * ax;
+            if (a.xv) a.xv[o + k] = fma(xal, a.pin[o + k], a.xv[o + k]);   // deferred x += alpha p
+        }
     }
     if (DIM == 2) {
         *reinterpret_cast<double2*>(a.y + o) = make_double2(out[0], out[1]);
     } else {
 #pragma unroll
         for (int k = 0; k < DIM; ++k) a.y[o + k] = out[k];
-    }
-}
-
-// ------------------------------------------------------------------ 2D (Q4)
-template <int OP>
-__global__ void __launch_bounds__(128) fine2d_kernel(FineArgs a, int nct, int nch) {
-    const int lane = threadIdx.x & 31;
-    const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int items = nct * nch;
-    if (w >= (long long)a.R * items) return;
-    if (a.done && *a.done) return;
-    const int r = (int)(w % a.R);
-    const int item = (int)(w / a.R);
-    if (a.active && !a.active[r]) return;
-    const int ct = item % nct, ch = item / nct;
-    const int n0 = a.g.nn[0], n1 = a.g.nn[1], N0 = a.g.N[0], N1 = a.g.N[1];
-    const int c = ct * COLS_PER_WARP + lane - 1;
-    const bool cin = (c >= 0) && (c < n1);
-    const bool own = cin && lane >= 1 && lane <= COLS_PER_WARP;
-    const int i0 = ch * CHUNK2, i1 = min(i0 + CHUNK2, n0);
-    const long long vbase = (long long)r * a.g.ndof;
-    const double beta = (OP == FOP_CGP) ? a.beta[r] : 0.0;
-
-    double A[3][2], B[3][2];     // masked windows of planes L and L+1 (cols c-1, c, c+1)
-    double rawA[2], rawB[2];     // unmasked own values
-    int mA, mB;
-    double carry[2] = {0.0, 0.0};
-    double dot = 0.0;
-
-    {   // plane i0 - 1
-        const int P = i0 - 1;
-        const bool v = cin && P >= 0;
-        double m[2];
-        load_node<2, OP>(a, vbase, (long long)P * n1 + c, v, rawA, m, beta, mA);
-#pragma unroll
-        for (int k = 0; k < 2; ++k) { A[1][k] = m[k]; A[0][k] = shfl_up1(m[k]); A[2][k] = shfl_dn1(m[k]); }
-    }
-    for (int L = i0 - 1; L < i1; ++L) {
-        const int P = L + 1;
-        const bool v = cin && P < n0;
-        double m[2];
-        load_node<2, OP>(a, vbase, (long long)P * n1 + c, v, rawB, m, beta, mB);
-        if (OP == FOP_CGP && own && P >= i0 && P < i1) {
-            *reinterpret_cast<double2*>(a.pout + vbase + 2LL * ((long long)P * n1 + c)) = make_double2(rawB[0], rawB[1]);
-        }
-#pragma unroll
-        for (int k = 0; k < 2; ++k) { B[1][k] = m[k]; B[0][k] = shfl_up1(m[k]); B[2][k] = shfl_dn1(m[k]); }
-        // element moduli of layer L: e=0 -> element column c-1, e=1 -> column c
-        double Ec = 0.0;
-        if (L >= 0 && L < N0 && c >= 0 && c < N1) Ec = a.E[(long long)L * N1 + c];
-        double Ee[2];
-        Ee[1] = Ec;
-        Ee[0] = shfl_up1(Ec);
-        if (c - 1 < 0) Ee[0] = 0.0;
-        double lo[2] = {carry[0], carry[1]}, hi[2] = {0.0, 0.0};
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            const int a1 = 1 - e;            // own node's local bit along axis 1
-            double tl[2] = {0.0, 0.0}, th[2] = {0.0, 0.0};
-#pragma unroll
-            for (int b0 = 0; b0 < 2; ++b0)
-#pragma unroll
-                for (int b1 = 0; b1 < 2; ++b1)
-#pragma unroll
-                    for (int k2 = 0; k2 < 2; ++k2) {
-                        const double xv = b0 ? B[e + b1][k2] : A[e + b1][k2];
-                        const int col = (b0 * 2 + b1) * 2 + k2;
-#pragma unroll
-                        for (int k = 0; k < 2; ++k) {
-                            tl[k] = fma(c_K0[((0 * 2 + a1) * 2 + k) * 8 + col], xv, tl[k]);
-                            th[k] = fma(c_K0[((1 * 2 + a1) * 2 + k) * 8 + col], xv, th[k]);
-                        }
-                    }
-#pragma unroll
-            for (int k = 0; k < 2; ++k) { lo[k] = fma(Ee[e], tl[k], lo[k]); hi[k] = fma(Ee[e], th[k], hi[k]); }
-        }
-        if (own && L >= i0) finish_node<2, OP>(a, vbase, (long long)L * n1 + c, mA, lo, rawA, dot);
-        carry[0] = hi[0]; carry[1] = hi[1];
-#pragma unroll
-        for (int q = 0; q < 3; ++q) { A[q][0] = B[q][0]; A[q][1] = B[q][1]; }
-        rawA[0] = rawB[0]; rawA[1] = rawB[1]; mA = mB;
-    }
-    if (a.partial) {
-        dot = warp_sum(dot);
-        if (lane == 0) a.partial[(long long)r * items + item] = dot;
     }
 }
 
@@ -200,6 +119,7 @@ __global__ void __launch_bounds__(128) fine3d_kernel(FineArgs a, int nct, int nc
     const int i0 = ch * CHUNK3, i1 = min(i0 + CHUNK3, n0);
     const long long vbase = (long long)r * a.g.ndof;
     const double beta = (OP == FOP_CGP) ? a.beta[r] : 0.0;
+    const double xal = (OP == FOP_CGP && a.xv) ? a.xalpha[r] : 0.0;
 
     double A[3][3][3], B[3][3][3];   // [row j-1..j+1][col c-1..c+1][comp]
     double rawA[3], rawB[3];
@@ -270,7 +190,7 @@ __global__ void __launch_bounds__(128) fine3d_kernel(FineArgs a, int nct, int nc
                     hi[k] = fma(Ee[ej][ec], th[k], hi[k]);
                 }
             }
-        if (own && L >= i0) finish_node<3, OP>(a, vbase, ((long long)L * n1 + j) * n2 + c, mA, lo, rawA, dot);
+        if (own && L >= i0) finish_node<3, OP>(a, vbase, ((long long)L * n1 + j) * n2 + c, mA, lo, rawA, dot, xal);
         carry[0] = hi[0]; carry[1] = hi[1]; carry[2] = hi[2];
 #pragma unroll
         for (int q = 0; q < 3; ++q)
@@ -296,13 +216,26 @@ static void launch_fine(const FineArgs& a, cudaStream_t s) {
     long long warps = (long long)a.R * fine_items(g);
     int wpb = 4;
     long long blocks = (warps + wpb - 1) / wpb;
-    if (g.dim == 2)
-        fine2d_kernel<OP><<<(unsigned)blocks, 32 * wpb, 0, s>>>(a, nct, nch);
-    else
-        fine3d_kernel<OP><<<(unsigned)blocks, 32 * wpb, 0, s>>>(a, nct, nch);
+    fine3d_kernel<OP><<<(unsigned)blocks, 32 * wpb, 0, s>>>(a, nct, nch);
 }
 
 int fine_apply(int op, const FineArgs& a, cudaStream_t s) {
+    if (a.g.dim == 2) {   // 2D: prefetching march kernels of fine2d.cu
+        March2Args m{};
+        m.g = a.g; m.E = a.E; m.mask = a.mask; m.omega = a.omega; m.active = a.active; m.done = a.done;
+        m.partial = a.partial; m.R = a.R;
+        int mop;
+        switch (op) {
+            case FOP_MATVEC: mop = M2_MATVEC; m.x = a.x; m.y = a.y; break;
+            case FOP_RESID: mop = M2_RESID; m.x = a.x; m.x2 = a.b; m.y = a.y; break;
+            case FOP_JACOBI: mop = M2_JACOBI; m.x = a.x; m.x2 = a.b; m.y = a.y; break;
+            default:
+                mop = M2_CGP; m.x = a.z; m.x2 = a.pin; m.y2 = a.pout; m.y = a.y; m.beta = a.beta;
+                m.xv = a.xv; m.xalpha = a.xalpha;
+                break;
+        }
+        return march2_apply(mop, m, a.nu_paper != 0, s);
+    }
     switch (op) {
         case FOP_MATVEC: launch_fine<FOP_MATVEC>(a, s); break;
         case FOP_RESID: launch_fine<FOP_RESID>(a, s); break;

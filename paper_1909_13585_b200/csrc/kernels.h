@@ -20,10 +20,13 @@ struct FineArgs {
     double* y;              // output vectors (R, ndof)
     double omega;
     const double* beta;     // CGP: per RHS
+    double* xv;             // CGP: x += xalpha * p_in at owned nodes (deferred CG update) or NULL
+    const double* xalpha;
     const int* active;      // per RHS or NULL
     const int* done;        // or NULL
     double* partial;        // dot partials [R][items] or NULL
     int R;
+    int nu_paper;           // 1: nu == 0.3 -> compile-time K0
 };
 
 void fine_set_constants(int dim, const double* K0, cudaStream_t s);
@@ -31,6 +34,34 @@ void fine_set_constants(int dim, const double* K0, cudaStream_t s);
 int fine_apply(int op, const FineArgs& a, cudaStream_t s);
 int fine_items(const LevelGeom& g);
 void fine_diag(const LevelGeom& g, const double* E, const uint8_t* mask, double* Dinv, double* D, cudaStream_t s);
+
+// ---------------------------------------------------------------- 2D fused march kernels (fine2d.cu)
+enum March2Op { M2_MATVEC = 0, M2_RESID = 1, M2_JACOBI = 2, M2_CGP = 3, M2_RESTRICT = 4, M2_POST = 5 };
+
+struct March2Args {
+    LevelGeom g, gc;              // fine level and next-coarser level (RESTRICT / POST)
+    const double* E;
+    const uint8_t* mask;
+    const uint8_t* maskc;
+    const double* x;              // MATVEC/RESID/JACOBI: x ; CGP: z ; RESTRICT: r_in ; POST: r
+    const double* x2;             // RESID/JACOBI: b ; CGP: p_in ; RESTRICT: q
+    double* xv;                   // CGP: x (deferred update x += xalpha p_in)
+    double* y;                    // MATVEC/RESID/JACOBI: y ; CGP: q ; POST: z
+    double* y2;                   // CGP: p_out ; RESTRICT: r_out
+    double* coarse;               // RESTRICT: r_c = P^T t
+    const double* ec;             // POST: coarse correction e_c
+    double omega;
+    const double* alpha;
+    const double* beta;
+    const double* xalpha;
+    const int* active;
+    const int* done;
+    double* partial;
+    int R;
+};
+void fine2d_set_constants(const double* K0, cudaStream_t s);
+int march2_apply(int op, const March2Args& a, bool nu_paper, cudaStream_t s);
+int march2_items(int op, const LevelGeom& g, const LevelGeom* gc);
 
 // ---------------------------------------------------------------- coarse levels (assembled stencils)
 enum CoarseOp { COP_MATVEC = 0, COP_RESID = 1, COP_JACOBI = 2 };
@@ -89,9 +120,16 @@ void vec_dot(long long n, int R, const double* a, const double* b, double* parti
 void vec_mask_copy(long long nnodes, int dim, int R, const uint8_t* mask, const double* src, double* dst,
                    cudaStream_t s);
 void vec_axpy_masked_restart(long long n, int R, const double* t, double* r, const int* restart, cudaStream_t s);
+// r_out = r_in - alpha q ; partial r_out.r_out ; z1 = omega Dinv r_out (z1 may be NULL)
+void cg_rupdate(long long n, int R, const double* alpha, const double* rin, const double* q, double* rout,
+                const double* Dinv, double omega, double* z1, double* partial, const int* active, const int* done,
+                cudaStream_t s);
+// x += xalpha * p_{xbuf} for every RHS with a pending deferred update
+void cg_flush_x(long long n, int R, CgCtl c, const double* p0, const double* p1, double* x, cudaStream_t s);
 
 enum ScalarMode { SM_INIT = 0, SM_ALPHA = 1, SM_CONV = 2, SM_BETA = 3, SM_RZ0 = 4, SM_TRUE = 5, SM_BB = 6 };
-void cg_scalars(int mode, int R, const double* partial, int items, CgCtl c, double tol, cudaStream_t s);
+void cg_scalars(int mode, int R, const double* partial, int items, CgCtl c, double tol, cudaStream_t s,
+                int aux = 0);
 
 // ---------------------------------------------------------------- stress stiffness G(u) phi
 void stress_set_constants(int dim, double nu, cudaStream_t s);

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "../../include/mgcg.h"
+#include "element.cuh"
 #include "kernels.h"
 
 // ---------------------------------------------------------------- error plumbing
@@ -47,35 +48,10 @@ static mg_status fail(mg_status s, const std::string& msg) {
 // B^T D0 B (standard Q4/H8, PAPER.md:111 reading r1).  Local DOF = d*a + comp,
 // local node a in C order (axis 0 most significant).
 static void element_stiffness(int dim, double nu, std::vector<double>& K) {
-    const double M[2][2] = {{1.0 / 3, 1.0 / 6}, {1.0 / 6, 1.0 / 3}};
-    const double D[2][2] = {{1.0, -1.0}, {-1.0, 1.0}};
-    const double C[2][2] = {{-0.5, -0.5}, {0.5, 0.5}};
-    const int na = 1 << dim, nl = dim * na;
-    const double mu = 1.0 / (2 * (1 + nu));
-    const double lam = dim == 2 ? nu / (1 - nu * nu) : nu / ((1 + nu) * (1 - 2 * nu));
-    auto S = [&](int i, int j, int a, int b) {
-        double v = 1.0;
-        for (int k = 0; k < dim; ++k) {
-            int ak = (a >> (dim - 1 - k)) & 1, bk = (b >> (dim - 1 - k)) & 1;
-            double f;
-            if (k == i && k == j) f = D[ak][bk];
-            else if (k == i) f = C[ak][bk];
-            else if (k == j) f = C[bk][ak];
-            else f = M[ak][bk];
-            v *= f;
-        }
-        return v;
-    };
+    const int nl = dim * (1 << dim);
     K.assign(nl * nl, 0.0);
-    for (int a = 0; a < na; ++a)
-        for (int b = 0; b < na; ++b)
-            for (int i = 0; i < dim; ++i)
-                for (int j = 0; j < dim; ++j) {
-                    double v = lam * S(i, j, a, b) + mu * S(j, i, a, b);
-                    if (i == j)
-                        for (int k = 0; k < dim; ++k) v += mu * S(k, k, a, b);
-                    K[(a * dim + i) * nl + b * dim + j] = v;
-                }
+    for (int r = 0; r < nl; ++r)
+        for (int c = 0; c < nl; ++c) K[r * nl + c] = dim == 2 ? k0_entry<2>(nu, r, c) : k0_entry<3>(nu, r, c);
 }
 
 // ---------------------------------------------------------------- small kernels
@@ -119,6 +95,8 @@ struct Level {
 struct mg_ctx {
     int dim = 0, L = 0;
     double nu = 0.3;
+    bool nu_paper = true;     // nu == 0.3: compile-time K0 in the fine kernels
+    bool fused2d = false;     // 2D, L >= 2, V(1,1): fused RESTRICT / POST fine kernels
     mg_opts opts{0.6, 1, 1, 1000};
     cudaStream_t user = nullptr, stream = nullptr;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
@@ -128,10 +106,11 @@ struct mg_ctx {
     // coarsest dense inverse
     double* Ainv = nullptr;
     long long nL = 0, npad = 0;
-    // fine vectors
+    // fine vectors (R x ndof each)
     int Ralloc = 0;
-    double *b = nullptr, *x = nullptr, *r = nullptr, *z = nullptr, *t = nullptr, *q = nullptr, *p0 = nullptr,
-           *p1 = nullptr;
+    double *b = nullptr, *x = nullptr, *r0 = nullptr, *r1 = nullptr, *p0 = nullptr, *p1 = nullptr, *q = nullptr,
+           *zf = nullptr, *z = nullptr, *t = nullptr;
+    double* zpre = nullptr;   // generic path: buffer holding the pre-smoothed z after blk_restrict
     double* partial = nullptr;
     long long partial_cap = 0;
     // CG control block
@@ -145,8 +124,6 @@ struct mg_ctx {
     long long n_init = 0, n_restart = 0, n_iter = 0, n_true = 0;
     int graph_R = -1;
     double graph_tol = -1.0;
-    double* zfinal = nullptr;   // level-0 buffer holding z after a V-cycle
-    int rz_items = 0;
     // stress
     double* sig = nullptr;
     // stats
@@ -249,7 +226,7 @@ static mg_status compute_operators(mg_ctx* c) {
 }
 
 static void free_vectors(mg_ctx* c) {
-    double** fv[] = {&c->b, &c->x, &c->r, &c->z, &c->t, &c->q, &c->p0, &c->p1, &c->partial};
+    double** fv[] = {&c->b, &c->x, &c->r0, &c->r1, &c->p0, &c->p1, &c->q, &c->zf, &c->z, &c->t, &c->partial};
     for (auto p : fv)
         if (*p) { cudaFree(*p); *p = nullptr; }
     for (int l = 1; l < c->L; ++l) {
@@ -269,7 +246,7 @@ static mg_status ensure_vectors(mg_ctx* c, int R) {
     CU(cudaStreamSynchronize(c->stream));
     free_vectors(c);
     const long long n = G0(c).ndof;
-    double** fv[] = {&c->b, &c->x, &c->r, &c->z, &c->t, &c->q, &c->p0, &c->p1};
+    double** fv[] = {&c->b, &c->x, &c->r0, &c->r1, &c->p0, &c->p1, &c->q, &c->zf, &c->z, &c->t};
     for (auto p : fv) CU(cudaMalloc(p, sizeof(double) * n * R));
     for (int l = 1; l < c->L; ++l) {
         long long nl = c->lv[l].g.ndof;
@@ -278,6 +255,12 @@ static mg_status ensure_vectors(mg_ctx* c, int R) {
         CU(cudaMalloc(&c->lv[l].w, sizeof(double) * nl * R));
     }
     long long items = fine_items(G0(c));
+    if (c->dim == 2) {
+        for (int op : {M2_CGP, M2_RESTRICT, M2_POST, M2_RESID}) {
+            long long it = march2_items(op, G0(c), c->L > 1 ? &c->lv[1].g : &c->lv[0].g);
+            items = it > items ? it : items;
+        }
+    }
     long long vb = vec_blocks(n);
     c->partial_cap = (items > vb ? items : vb) * (long long)R;
     CU(cudaMalloc(&c->partial, sizeof(double) * c->partial_cap));
@@ -285,7 +268,7 @@ static mg_status ensure_vectors(mg_ctx* c, int R) {
     return MG_OK;
 }
 
-// ---------------------------------------------------------------- V-cycle recording
+// ---------------------------------------------------------------- recording helpers
 struct Rec {
     mg_ctx* c;
     int R;
@@ -294,12 +277,18 @@ struct Rec {
     long long launches = 0;
 };
 
+static FineArgs fine_args(mg_ctx* c, const Rec& rc) {
+    FineArgs a{};
+    a.g = G0(c); a.E = c->E; a.mask = c->lv[0].mask; a.omega = c->opts.omega;
+    a.active = rc.active; a.done = rc.done; a.R = rc.R; a.nu_paper = c->nu_paper ? 1 : 0;
+    return a;
+}
+
 static void level_smooth(Rec& rc, int l, const double* r, const double* z, double* w, double* partial) {
     mg_ctx* c = rc.c;
     if (l == 0 && c->L > 1) {
-        FineArgs a{};
-        a.g = G0(c); a.E = c->E; a.mask = c->lv[0].mask; a.x = z; a.b = r; a.Dinv = c->lv[0].Dinv; a.y = w;
-        a.omega = c->opts.omega; a.active = rc.active; a.done = rc.done; a.partial = partial; a.R = rc.R;
+        FineArgs a = fine_args(c, rc);
+        a.x = z; a.b = r; a.Dinv = c->lv[0].Dinv; a.y = w; a.partial = partial;
         fine_apply(FOP_JACOBI, a, c->stream);
     } else {
         CoarseArgs a{};
@@ -313,9 +302,8 @@ static void level_smooth(Rec& rc, int l, const double* r, const double* z, doubl
 static void level_resid(Rec& rc, int l, const double* r, const double* z, double* w) {
     mg_ctx* c = rc.c;
     if (l == 0) {
-        FineArgs a{};
-        a.g = G0(c); a.E = c->E; a.mask = c->lv[0].mask; a.x = z; a.b = r; a.y = w;
-        a.active = rc.active; a.done = rc.done; a.R = rc.R;
+        FineArgs a = fine_args(c, rc);
+        a.x = z; a.b = r; a.y = w;
         fine_apply(FOP_RESID, a, c->stream);
     } else {
         CoarseArgs a{};
@@ -326,11 +314,9 @@ static void level_resid(Rec& rc, int l, const double* r, const double* z, double
     rc.launches++;
 }
 
-// Symmetric V(nu_pre, nu_post)-cycle on level l: z ~ A_l^-1 r.  Returns the buffer
-// holding z (z or w).  presmoothed: z already holds omega D^-1 r (fused in cg_update).
-// dot_partial (level 0): the last post-smoothing sweep also accumulates r.z.
-static double* vcycle(Rec& rc, int l, const double* r, double* z, double* w, bool presmoothed,
-                      double* dot_partial, bool* dot_done) {
+// Symmetric V(nu_pre, nu_post)-cycle on level l (generic kernels): z ~ A_l^-1 r.  Returns
+// the buffer holding z (z or w).  Used for levels >= 1 in the solve and for mg_vcycle.
+static double* vcycle(Rec& rc, int l, const double* r, double* z, double* w) {
     mg_ctx* c = rc.c;
     const Level& lv = c->lv[l];
     const int R = rc.R;
@@ -339,10 +325,8 @@ static double* vcycle(Rec& rc, int l, const double* r, double* z, double* w, boo
         rc.launches++;
         return z;
     }
-    if (!presmoothed) {
-        cg_pointwise_jacobi(lv.g.ndof, R, r, lv.Dinv, c->opts.omega, z, rc.active, rc.done, c->stream);
-        rc.launches++;
-    }
+    cg_pointwise_jacobi(lv.g.ndof, R, r, lv.Dinv, c->opts.omega, z, rc.active, rc.done, c->stream);
+    rc.launches++;
     for (int s = 1; s < c->opts.nu_pre; ++s) {
         level_smooth(rc, l, r, z, w, nullptr);
         std::swap(z, w);
@@ -351,31 +335,109 @@ static double* vcycle(Rec& rc, int l, const double* r, double* z, double* w, boo
     const Level& nx = c->lv[l + 1];
     restrict_apply(lv.g, nx.g, lv.mask, nx.mask, w, nx.r, R, rc.active, rc.done, c->stream);
     rc.launches++;
-    double* zc = vcycle(rc, l + 1, nx.r, nx.z, nx.w, false, nullptr, nullptr);
+    double* zc = vcycle(rc, l + 1, nx.r, nx.z, nx.w);
     prolong_add(lv.g, nx.g, lv.mask, nx.mask, zc, z, R, rc.active, rc.done, true, c->stream);
     rc.launches++;
     for (int s = 0; s < c->opts.nu_post; ++s) {
-        const bool last = (s == c->opts.nu_post - 1);
-        level_smooth(rc, l, r, z, w, (last && dot_partial) ? dot_partial : nullptr);
-        if (last && dot_partial && dot_done) *dot_done = (l == 0 && c->L > 1);
+        level_smooth(rc, l, r, z, w, nullptr);
         std::swap(z, w);
     }
     return z;
 }
 
-// Level-0 V-cycle with the r.z reduction; returns z buffer and the partial item count.
-static double* vcycle0_with_dot(Rec& rc, bool presmoothed, int* items) {
+// ---- fine-level blocks of one CG iteration (fused kernels in 2D, composed kernels otherwise)
+static March2Args march_args(mg_ctx* c, const Rec& rc) {
+    March2Args a{};
+    a.g = G0(c);
+    if (c->L > 1) { a.gc = c->lv[1].g; a.maskc = c->lv[1].mask; }
+    a.E = c->E; a.mask = c->lv[0].mask; a.omega = c->opts.omega;
+    a.alpha = c->ctl.alpha; a.beta = c->ctl.beta; a.xalpha = c->ctl.xalpha;
+    a.active = rc.active; a.done = rc.done; a.R = rc.R;
+    return a;
+}
+
+// p_out = zf + beta p_in ; q = K p_out ; partial p.q ; x += xalpha p_in.  Returns partial items.
+static int blk_cgp(Rec& rc, const double* pin, double* pout) {
     mg_ctx* c = rc.c;
-    bool dot_done = false;
-    double* zf = vcycle(rc, 0, c->r, c->z, c->t, presmoothed, c->partial, &dot_done);
-    if (dot_done) {
-        *items = fine_items(G0(c));
-    } else {
-        vec_dot(G0(c).ndof, rc.R, c->r, zf, c->partial, rc.active, rc.done, c->stream);
+    rc.launches++;
+    FineArgs a = fine_args(c, rc);
+    a.z = c->zf; a.pin = pin; a.pout = pout; a.y = c->q; a.beta = c->ctl.beta;
+    a.xv = c->x; a.xalpha = c->ctl.xalpha; a.partial = c->partial;
+    return fine_apply(FOP_CGP, a, c->stream);
+}
+
+// r_out = r_in - alpha q ; partial r.r ; pre-smooth z1 = omega D^-1 r_out ; r_1 = P^T (r_out - K z1)
+static int blk_restrict(Rec& rc, const double* rin, double* rout) {
+    mg_ctx* c = rc.c;
+    const long long n = G0(c).ndof;
+    if (c->fused2d) {
+        March2Args a = march_args(c, rc);
+        a.x = rin; a.x2 = c->q; a.y2 = rout; a.coarse = c->lv[1].r; a.partial = c->partial;
         rc.launches++;
-        *items = vec_blocks(G0(c).ndof);
+        return march2_apply(M2_RESTRICT, a, c->nu_paper, c->stream);
     }
-    return zf;
+    cg_rupdate(n, rc.R, c->ctl.alpha, rin, c->q, rout, c->lv[0].Dinv, c->opts.omega, c->L > 1 ? c->z : nullptr,
+               c->partial, rc.active, rc.done, c->stream);
+    rc.launches++;
+    const int items = vec_blocks(n);
+    if (c->L == 1) return items;
+    double *z = c->z, *w = c->t;
+    for (int s = 1; s < c->opts.nu_pre; ++s) {
+        level_smooth(rc, 0, rout, z, w, nullptr);
+        std::swap(z, w);
+    }
+    level_resid(rc, 0, rout, z, w);
+    restrict_apply(G0(c), c->lv[1].g, c->lv[0].mask, c->lv[1].mask, w, c->lv[1].r, rc.R, rc.active, rc.done,
+                   c->stream);
+    rc.launches++;
+    c->zpre = z;
+    return items;
+}
+
+// levels 1..L-1 of the V-cycle on lv[1].r; returns the level-1 correction buffer
+static double* coarse_cycle(Rec& rc) {
+    mg_ctx* c = rc.c;
+    if (c->L == 1) return nullptr;
+    return vcycle(rc, 1, c->lv[1].r, c->lv[1].z, c->lv[1].w);
+}
+
+// zf = post-smoothed (z1 + P ec) ; partial r.zf.  Returns partial items.
+static int blk_post(Rec& rc, const double* r, const double* ec) {
+    mg_ctx* c = rc.c;
+    const long long n = G0(c).ndof;
+    if (c->L == 1) {
+        dense_apply(c->Ainv, c->npad, c->nL, r, c->zf, rc.R, rc.active, rc.done, c->stream);
+        vec_dot(n, rc.R, r, c->zf, c->partial, rc.active, rc.done, c->stream);
+        rc.launches += 2;
+        return vec_blocks(n);
+    }
+    if (c->fused2d) {
+        March2Args a = march_args(c, rc);
+        a.x = r; a.ec = ec; a.y = c->zf; a.partial = c->partial;
+        rc.launches++;
+        return march2_apply(M2_POST, a, c->nu_paper, c->stream);
+    }
+    prolong_add(G0(c), c->lv[1].g, c->lv[0].mask, c->lv[1].mask, ec, c->zpre, rc.R, rc.active, rc.done, true,
+                c->stream);
+    rc.launches++;
+    double* src = c->zpre;
+    int items = vec_blocks(n);
+    if (c->opts.nu_post == 0) {
+        cudaMemcpyAsync(c->zf, src, sizeof(double) * n * rc.R, cudaMemcpyDeviceToDevice, c->stream);
+        vec_dot(n, rc.R, r, c->zf, c->partial, rc.active, rc.done, c->stream);
+        rc.launches++;
+        return items;
+    }
+    for (int s = 0; s < c->opts.nu_post; ++s) {
+        const bool last = s == c->opts.nu_post - 1;
+        double* dst = last ? c->zf : (src == c->z ? c->t : c->z);
+        FineArgs a = fine_args(c, rc);
+        a.x = src; a.b = r; a.Dinv = c->lv[0].Dinv; a.y = dst; a.partial = last ? c->partial : nullptr;
+        items = fine_apply(FOP_JACOBI, a, c->stream);
+        rc.launches++;
+        src = dst;
+    }
+    return items;
 }
 
 static mg_status capture_begin(mg_ctx* c) {
@@ -394,54 +456,59 @@ static mg_status capture_end(mg_ctx* c, cudaGraphExec_t* exec, long long* nodes)
     return MG_OK;
 }
 
+// Graphs (captured once per (R, tol)):
+//   init    : b.b, x = 0, p0 = 0, q = 0, r1 = b
+//   restart : z = B r (r1 -> r0, alpha = 0), r.z            (start and true-residual restarts)
+//   iter    : two CG iterations (p and r ping-pong buffers)
+//   true    : flush deferred x update, t = b - K x, t.t
 static mg_status build_graphs(mg_ctx* c, int R, double tol) {
-    (void)tol;
     for (cudaGraphExec_t* g : {&c->g_init, &c->g_restart, &c->g_iter, &c->g_true})
         if (*g) { cudaGraphExecDestroy(*g); *g = nullptr; }
     const LevelGeom& g0 = G0(c);
     const long long n = g0.ndof;
     const int vb = vec_blocks(n);
-    // Note: tol is read from the graph's kernel parameters, so graphs are rebuilt per tol.
     Rec rc{c, R, c->ctl.active, c->ctl.done};
-    // ---- restart: z = B r, rz  (used at start and after a true-residual restart)
+    // ---- restart / initial preconditioning
     TRY(capture_begin(c));
-    int items = 0;
-    c->zfinal = vcycle0_with_dot(rc, false, &items);
-    cg_scalars(SM_RZ0, R, c->partial, items, c->ctl, 0.0, c->stream);
+    {
+        blk_restrict(rc, c->r1, c->r0);
+        double* ec = coarse_cycle(rc);
+        const int k = blk_post(rc, c->r0, ec);
+        cg_scalars(SM_RZ0, R, c->partial, k, c->ctl, 0.0, c->stream);
+    }
     TRY(capture_end(c, &c->g_restart, &c->n_restart));
-    c->rz_items = items;
-    // ---- init: bb, x = 0, r = b, p0 = 0
+    // ---- init
     TRY(capture_begin(c));
     vec_dot(n, R, c->b, c->b, c->partial, nullptr, nullptr, c->stream);
     cg_scalars(SM_BB, R, c->partial, vb, c->ctl, 0.0, c->stream);
     CU(cudaMemsetAsync(c->x, 0, sizeof(double) * n * R, c->stream));
     CU(cudaMemsetAsync(c->p0, 0, sizeof(double) * n * R, c->stream));
-    CU(cudaMemcpyAsync(c->r, c->b, sizeof(double) * n * R, cudaMemcpyDeviceToDevice, c->stream));
+    CU(cudaMemsetAsync(c->q, 0, sizeof(double) * n * R, c->stream));
+    CU(cudaMemcpyAsync(c->r1, c->b, sizeof(double) * n * R, cudaMemcpyDeviceToDevice, c->stream));
     TRY(capture_end(c, &c->g_init, &c->n_init));
-    // ---- two CG iterations (p ping-pong)
+    // ---- two CG iterations
     TRY(capture_begin(c));
     for (int it = 0; it < 2; ++it) {
         double* pin = it == 0 ? c->p0 : c->p1;
         double* pout = it == 0 ? c->p1 : c->p0;
-        FineArgs a{};
-        a.g = g0; a.E = c->E; a.mask = c->lv[0].mask; a.z = c->zfinal; a.pin = pin; a.pout = pout; a.y = c->q;
-        a.beta = c->ctl.beta; a.active = c->ctl.active; a.done = c->ctl.done; a.partial = c->partial; a.R = R;
-        int fitems = fine_apply(FOP_CGP, a, c->stream);
-        cg_scalars(SM_ALPHA, R, c->partial, fitems, c->ctl, 0.0, c->stream);
-        cg_update(n, R, c->ctl.alpha, pout, c->q, c->x, c->r, c->lv[0].Dinv, c->opts.omega, c->z, c->partial,
-                  c->ctl.active, c->ctl.done, c->stream);
-        cg_scalars(SM_CONV, R, c->partial, vb, c->ctl, tol, c->stream);
-        int it_items = 0;
-        double* zf = vcycle0_with_dot(rc, c->L > 1, &it_items);
-        if (zf != c->zfinal) return fail(MG_ERR_CUDA, "internal: V-cycle output buffer mismatch");
-        cg_scalars(SM_BETA, R, c->partial, it_items, c->ctl, 0.0, c->stream);
+        double* rin = it == 0 ? c->r0 : c->r1;
+        double* rout = it == 0 ? c->r1 : c->r0;
+        int k = blk_cgp(rc, pin, pout);
+        cg_scalars(SM_ALPHA, R, c->partial, k, c->ctl, 0.0, c->stream, pout == c->p1 ? 1 : 0);
+        k = blk_restrict(rc, rin, rout);
+        cg_scalars(SM_CONV, R, c->partial, k, c->ctl, tol, c->stream);
+        double* ec = coarse_cycle(rc);
+        k = blk_post(rc, rout, ec);
+        cg_scalars(SM_BETA, R, c->partial, k, c->ctl, 0.0, c->stream);
     }
     TRY(capture_end(c, &c->g_iter, &c->n_iter));
-    // ---- true residual t = b - K x, t.t
+    // ---- true residual
     TRY(capture_begin(c));
     {
-        FineArgs a{};
-        a.g = g0; a.E = c->E; a.mask = c->lv[0].mask; a.x = c->x; a.b = c->b; a.y = c->t; a.R = R;
+        cg_flush_x(n, R, c->ctl, c->p0, c->p1, c->x, c->stream);
+        Rec all{c, R, nullptr, nullptr};
+        FineArgs a = fine_args(c, all);
+        a.x = c->x; a.b = c->b; a.y = c->t;
         fine_apply(FOP_RESID, a, c->stream);
         vec_dot(n, R, c->t, c->t, c->partial, nullptr, nullptr, c->stream);
         cg_scalars(SM_TRUE, R, c->partial, vb, c->ctl, 0.0, c->stream);
@@ -495,7 +562,10 @@ static mg_status setup_impl(mg_ctx* c, const mg_grid* grid, const double* E_e, c
         c->lv[l].g = make_geom(c->dim, Nl);
     }
     element_stiffness(c->dim, c->nu, c->K0);
+    c->nu_paper = (c->nu == MG_NU_PAPER);
+    c->fused2d = (c->dim == 2 && levels >= 2 && c->opts.nu_pre == 1 && c->opts.nu_post == 1);
     fine_set_constants(c->dim, c->K0.data(), s);
+    if (c->dim == 2) fine2d_set_constants(c->K0.data(), s);
     galerkin_set_constants(c->dim, c->K0.data(), s);
     stress_set_constants(c->dim, c->nu, s);
     const LevelGeom& g0 = G0(c);
@@ -536,15 +606,16 @@ static mg_status setup_impl(mg_ctx* c, const mg_grid* grid, const double* E_e, c
     CU(cudaMalloc(&c->Ainv, sizeof(double) * c->npad * c->npad));
     // control block
     const int MR = MG_MAX_RHS;
-    size_t bytes = sizeof(double) * 7 * MR + sizeof(int) * (4 * MR + 2);
+    size_t bytes = sizeof(double) * 8 * MR + sizeof(int) * (4 * MR + 4);
     CU(cudaMalloc(&c->ctl_mem, bytes));
     CU(cudaMemsetAsync(c->ctl_mem, 0, bytes, s));
     double* dp = (double*)c->ctl_mem;
     c->ctl.alpha = dp; c->ctl.beta = dp + MR; c->ctl.rz = dp + 2 * MR; c->ctl.rr = dp + 3 * MR;
-    c->ctl.bb = dp + 4 * MR; c->ctl.pq = dp + 5 * MR; c->ctl.tt = dp + 6 * MR;
-    int* ip = (int*)(dp + 7 * MR);
-    c->ctl.active = ip; c->ctl.iters = ip + MR; c->ctl.done = ip + 2 * MR; c->ctl.status = ip + 2 * MR + 1;
-    c->d_status = ip + 2 * MR + 2;
+    c->ctl.bb = dp + 4 * MR; c->ctl.pq = dp + 5 * MR; c->ctl.tt = dp + 6 * MR; c->ctl.xalpha = dp + 7 * MR;
+    int* ip = (int*)(dp + 8 * MR);
+    c->ctl.active = ip; c->ctl.iters = ip + MR; c->ctl.xbuf = ip + 2 * MR;
+    c->ctl.done = ip + 3 * MR; c->ctl.status = ip + 3 * MR + 1;
+    c->d_status = ip + 3 * MR + 2;
     CU(cudaMallocHost(&c->h_pinned, sizeof(int) * (2 * MR + 4)));
     CU(cudaMallocHost(&c->h_dbl, sizeof(double) * 4 * MR));
     TRY(compute_operators(c));
@@ -662,9 +733,10 @@ mg_status mgcg_solve(mg_handle c, const double* rhs, int nrhs, double tol, doubl
         }
         if (!nre || restarts >= 3) break;
         ++restarts;
-        int* d_restart = c->ctl.active;   // active := restart flags, then r = t for them
+        int* d_restart = c->ctl.active;   // active := restart flags, then r1 = t for them
         CU(cudaMemcpyAsync(d_restart, restart.data(), sizeof(int) * MG_MAX_RHS, cudaMemcpyHostToDevice, s));
-        vec_axpy_masked_restart(n, nrhs, c->t, c->r, d_restart, s);
+        vec_axpy_masked_restart(n, nrhs, c->t, c->r1, d_restart, s);
+        CU(cudaMemsetAsync(c->ctl.alpha, 0, sizeof(double) * MG_MAX_RHS, s));
         int zero = 0;
         CU(cudaMemcpyAsync(c->ctl.done, &zero, sizeof(int), cudaMemcpyHostToDevice, s));
         CU(cudaGraphLaunch(c->g_restart, s));
@@ -758,6 +830,7 @@ mg_status mg_matvec(mg_handle c, int level, const double* x, int nrhs, double* y
     if (level == 0) {
         FineArgs a{};
         a.g = G0(c); a.E = c->E; a.mask = c->lv[0].mask; a.x = x; a.y = y; a.R = nrhs;
+        a.nu_paper = c->nu_paper ? 1 : 0;
         fine_apply(FOP_MATVEC, a, c->stream);
     } else {
         CoarseArgs a{};
@@ -776,11 +849,15 @@ mg_status mg_vcycle(mg_handle c, const double* r, int nrhs, double* z) {
     TRY(ensure_vectors(c, nrhs));
     stream_enter(c);
     const long long n = G0(c).ndof;
-    CU(cudaMemcpyAsync(c->r, r, sizeof(double) * n * nrhs, cudaMemcpyDeviceToDevice, c->stream));
+    // the preconditioner exactly as the solve applies it (same fine blocks, alpha = 0)
+    CU(cudaMemcpyAsync(c->r1, r, sizeof(double) * n * nrhs, cudaMemcpyDeviceToDevice, c->stream));
+    CU(cudaMemsetAsync(c->ctl.alpha, 0, sizeof(double) * MG_MAX_RHS, c->stream));
+    CU(cudaMemsetAsync(c->q, 0, sizeof(double) * n * nrhs, c->stream));
     Rec rc{c, nrhs, nullptr, nullptr};
-    bool dd = false;
-    double* zf = vcycle(rc, 0, c->r, c->z, c->t, false, nullptr, &dd);
-    CU(cudaMemcpyAsync(z, zf, sizeof(double) * n * nrhs, cudaMemcpyDeviceToDevice, c->stream));
+    blk_restrict(rc, c->r1, c->r0);
+    double* ec = coarse_cycle(rc);
+    blk_post(rc, c->r0, ec);
+    CU(cudaMemcpyAsync(z, c->zf, sizeof(double) * n * nrhs, cudaMemcpyDeviceToDevice, c->stream));
     c->launches += rc.launches;
     CHECK_LAUNCH();
     stream_leave(c);
