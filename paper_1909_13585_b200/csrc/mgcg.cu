@@ -569,12 +569,12 @@ static mg_status setup_impl(mg_ctx* c, const mg_grid* grid, const double* E_e, c
     galerkin_set_constants(c->dim, c->K0.data(), s);
     stress_set_constants(c->dim, c->nu, s);
     const LevelGeom& g0 = G0(c);
-    CU(cudaMalloc(&c->E, sizeof(double) * g0.nelem));
+    CU(cudaMalloc(&c->E, sizeof(double) * g0.nelem + 64));   // +64: aligned bulk-copy tails
     CU(cudaMemcpyAsync(c->E, E_e, sizeof(double) * g0.nelem,
                        is_device_ptr(E_e) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
     for (int l = 0; l < levels; ++l) {
         Level& v = c->lv[l];
-        CU(cudaMalloc(&v.mask, v.g.nnodes));
+        CU(cudaMalloc(&v.mask, v.g.nnodes + 64));
         CU(cudaMalloc(&v.Dinv, sizeof(double) * v.g.ndof));
         CU(cudaMalloc(&v.D, sizeof(double) * v.g.ndof));
         if (l >= 1 || levels == 1) {
