@@ -22,6 +22,8 @@
 // index is the fastest grid coordinate so the R warps of a tile share E_e in L2.
 // K0 entries for nu = 0.3 are compile-time constants (element.cuh).
 #include "element.cuh"
+#include <algorithm>
+
 #include "kernels.h"
 
 __constant__ double c_K2[64];
@@ -36,181 +38,144 @@ __device__ __forceinline__ double K2(int r, int c) {
     return c_K2[r * 8 + c];
 }
 
-static constexpr int NS = 4;      // smem pipeline stages per warp (node planes in flight)
+static constexpr int PD = 2;      // register prefetch depth (node planes in flight per warp)
 static constexpr int CH = 64;     // node planes per chunk
 static constexpr int CCH = 32;    // coarse rows per chunk (M2_RESTRICT)
-static constexpr int WPB = 2;     // warps per CTA (independent; no CTA-wide sync)
+static constexpr int WPB = 4;     // warps per CTA (independent)
 
 __device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+__device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
 __device__ __forceinline__ void st2(double* p, double a, double b) { *reinterpret_cast<double2*>(p) = make_double2(a, b); }
 
-// ---------------------------------------------------------------- TMA bulk-copy / mbarrier helpers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+// ---------------------------------------------------------------- padded layout
+Pad2 pad2_layout(const LevelGeom& g) {
+    Pad2 p{};
+    const int n0 = g.nn[0], n1 = g.nn[1], N0 = g.N[0], N1 = g.N[1];
+    p.pitch = n1 + 2;
+    p.org = 16 + p.pitch + 2;                    // front slack: lanes reach column -2 of row -1
+    p.nodes = p.org + (long long)(n0 + 1) * p.pitch + 64;
+    p.pitchE = N1 + 2;
+    p.orgE = 16 + p.pitchE + 4;
+    p.elems = p.orgE + (long long)(N0 + 1) * p.pitchE + 64;
+    p.vstride = (2 * p.nodes + 3) & ~3LL;
+    return p;
 }
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-        "r"(phase)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// Stage layout (bytes) for RB right-hand sides: NV vectors x RB RHS x 32 nodes x 16 B, then
-// E (elements c_first-1 .. c_first+31 from a 16-B aligned start), the node masks, and for
-// POST the coarse correction rows (RB x 17 nodes) + coarse mask, for RESTRICT the coarse mask.
-template <int OP, int RB>
-struct Stage {
-    static constexpr int NV = OP == M2_CGP ? 3 : ((OP == M2_MATVEC || OP == M2_POST) ? 1 : 2);
-    static constexpr bool HAS_C = OP == M2_POST;
-    static constexpr bool HAS_CM = OP == M2_POST || OP == M2_RESTRICT;
-    static constexpr int EOFF = NV * RB * 512;
-    static constexpr int MOFF = EOFF + 288;
-    static constexpr int COFF = MOFF + 48;
-    static constexpr int CMOFF = COFF + (HAS_C ? RB * 288 : 0);
-    static constexpr int BYTES = CMOFF + (HAS_CM ? 48 : 0);
-    static constexpr int NCOPY = NV * RB + 2 + (HAS_C ? RB : 0) + (HAS_CM ? 1 : 0);
-};
+__global__ void pad_nodes_u8_kernel(int n0, int n1, Pad2 p, const uint8_t* src, uint8_t* dst, uint8_t fill) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p.nodes) return;
+    const long long q = i - p.org;
+    long long row = q >= 0 ? q / p.pitch : -1 - ((-q - 1) / p.pitch);
+    const long long col = q - row * p.pitch;
+    uint8_t v = fill;
+    if (row >= 0 && row < n0 && col >= 0 && col < n1) v = src[row * n1 + col];
+    dst[i] = v;
+}
 
-struct WarpGeom {
-    int c_first;        // node column of lane 0
-    int vlo, vhi;       // copied node columns [vlo, vhi)
-    int clo, chi;       // copied element columns [clo, chi)
-    int jbase, jl, jh;  // coarse node columns: smem origin c_first>>1, copied [jl, jh]
+__global__ void pad_nodes_f64_kernel(int n0, int n1, Pad2 p, const double* src, double* dst) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p.nodes) return;
+    const long long q = i - p.org;
+    long long row = q >= 0 ? q / p.pitch : -1 - ((-q - 1) / p.pitch);
+    const long long col = q - row * p.pitch;
+    double a = 0.0, b = 0.0;
+    if (row >= 0 && row < n0 && col >= 0 && col < n1) {
+        a = src[2 * (row * n1 + col)];
+        b = src[2 * (row * n1 + col) + 1];
+    }
+    dst[2 * i] = a;
+    dst[2 * i + 1] = b;
+}
+
+__global__ void pad_elems_kernel(int N0, int N1, Pad2 p, const double* src, double* dst) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p.elems) return;
+    const long long q = i - p.orgE;
+    long long row = q >= 0 ? q / p.pitchE : -1 - ((-q - 1) / p.pitchE);
+    const long long col = q - row * p.pitchE;
+    double v = 0.0;
+    if (row >= 0 && row < N0 && col >= 0 && col < N1) v = src[row * N1 + col];
+    dst[i] = v;
+}
+
+// compact (R, ndof) -> padded interior, masked at fixed DOFs
+__global__ void pad_vectors_kernel(int n0, int n1, Pad2 p, const uint8_t* mask, const double* src, double* dst,
+                                   long long ndof) {
+    const int r = blockIdx.y;
+    const long long nodes = (long long)n0 * n1;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nodes; i += (long long)gridDim.x * blockDim.x) {
+        const long long row = i / n1, col = i - row * n1;
+        const int m = mask ? mask[i] : 0;
+        const double2 v = ld2(src + r * ndof + 2 * i);
+        st2(dst + r * p.vstride + 2 * (p.org + row * p.pitch + col), (m & 1) ? 0.0 : v.x, (m & 2) ? 0.0 : v.y);
+    }
+}
+
+__global__ void unpad_vectors_kernel(int n0, int n1, Pad2 p, const double* src, double* dst, long long ndof) {
+    const int r = blockIdx.y;
+    const long long nodes = (long long)n0 * n1;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nodes; i += (long long)gridDim.x * blockDim.x) {
+        const long long row = i / n1, col = i - row * n1;
+        const double2 v = ld2(src + r * p.vstride + 2 * (p.org + row * p.pitch + col));
+        st2(dst + r * ndof + 2 * i, v.x, v.y);
+    }
+}
+
+static unsigned blocks_for(long long n) { return (unsigned)((n + 255) / 256); }
+
+void pad2_nodes_u8(const LevelGeom& g, const Pad2& p, const uint8_t* src, uint8_t* dst, uint8_t fill, cudaStream_t s) {
+    pad_nodes_u8_kernel<<<blocks_for(p.nodes), 256, 0, s>>>(g.nn[0], g.nn[1], p, src, dst, fill);
+}
+void pad2_nodes_f64(const LevelGeom& g, const Pad2& p, const double* src, double* dst, cudaStream_t s) {
+    pad_nodes_f64_kernel<<<blocks_for(p.nodes), 256, 0, s>>>(g.nn[0], g.nn[1], p, src, dst);
+}
+void pad2_elems(const LevelGeom& g, const Pad2& p, const double* src, double* dst, cudaStream_t s) {
+    pad_elems_kernel<<<blocks_for(p.elems), 256, 0, s>>>(g.N[0], g.N[1], p, src, dst);
+}
+void pad2_vectors(const LevelGeom& g, const Pad2& p, int R, const uint8_t* mask, const double* src, double* dst,
+                  cudaStream_t s) {
+    dim3 grid((unsigned)std::min<long long>(blocks_for(g.nnodes), 1184), R);
+    pad_vectors_kernel<<<grid, 256, 0, s>>>(g.nn[0], g.nn[1], p, mask, src, dst, g.ndof);
+}
+void unpad2_vectors(const LevelGeom& g, const Pad2& p, int R, const double* src, double* dst, cudaStream_t s) {
+    dim3 grid((unsigned)std::min<long long>(blocks_for(g.nnodes), 1184), R);
+    unpad_vectors_kernel<<<grid, 256, 0, s>>>(g.nn[0], g.nn[1], p, src, dst, g.ndof);
+}
+
+// ---------------------------------------------------------------- march kernels
+struct Slot {
+    double v0x, v0y, v1x, v1y, xx, xy;   // vectors at (P, c)
+    double e, el;                        // E(P, c), E(P, c-1)
+    double dx, dy;                       // D^-1 at (P, c)   (RESTRICT / POST / JACOBI)
+    int m;                               // fixed bits at (P, c)
+    double cx0, cy0, cx1, cy1;           // POST: coarse row (P+1)/2 at J0, J1 (odd P), coarse-masked
+    int cm;                              // RESTRICT: coarse mask of row (P-1)>>1 at J = c/2
 };
 
 template <int OP>
-__device__ __forceinline__ int coarse_row(const March2Args& a, int P) {
-    int crow = -1;
-    if (OP == M2_POST) crow = (P & 1) ? (P + 1) >> 1 : -1;
-    if (OP == M2_RESTRICT) crow = P >= 1 ? (P - 1) >> 1 : -1;
-    return (crow >= 0 && crow < a.gc.nn[0]) ? crow : -1;
-}
-
-// Issue the bulk copies of plane P into a stage: lane 0 registers the byte count on the
-// stage's mbarrier, then lane t issues copy t (vectors of RHS q, E, masks, coarse rows).
-template <int OP, int RB>
-__device__ __forceinline__ void issue_plane(const March2Args& a, const WarpGeom& wg, char* st, uint64_t* bar, int P,
-                                            long long r0, int nr, unsigned actmask, int lane) {
-    using S = Stage<OP, RB>;
-    const int n0 = a.g.nn[0], n1 = a.g.nn[1], N0 = a.g.N[0], N1 = a.g.N[1];
-    uint32_t vbytes = 0, ebytes = 0, mbytes = 0, cbytes = 0, cmbytes = 0;
-    int e_al = 0, m_al = 0, cm_al = 0;
-    const int crow = coarse_row<OP>(a, P);
-    if (P >= 0 && P < n0 && wg.vlo < wg.vhi) {
-        vbytes = 16u * (wg.vhi - wg.vlo);
-        m_al = (P * n1 + wg.vlo) & ~15;
-        mbytes = (uint32_t)(((P * n1 + wg.vhi + 15) & ~15) - m_al);
-    }
-    if (P >= 0 && P < N0 && wg.clo < wg.chi) {
-        e_al = (8 * (P * N1 + wg.clo)) & ~15;
-        ebytes = (uint32_t)(((8 * (P * N1 + wg.chi) + 15) & ~15) - e_al);
-    }
-    if (S::HAS_CM && crow >= 0 && wg.jl <= wg.jh) {
-        const int nc1 = a.gc.nn[1];
-        if (S::HAS_C) cbytes = 16u * (wg.jh - wg.jl + 1);
-        cm_al = (crow * nc1 + wg.jl) & ~15;
-        cmbytes = (uint32_t)(((crow * nc1 + wg.jh + 1 + 15) & ~15) - cm_al);
-    }
-    const int nact = __popc(actmask);
-    if (lane == 0) mbar_expect_tx(bar, S::NV * nact * vbytes + ebytes + mbytes + nact * cbytes + cmbytes);
-    __syncwarp();
-    const int t = lane;
-    if (t < S::NV * RB) {
-        const int v = t / RB, q = t % RB;
-        if (q < nr && ((actmask >> q) & 1) && vbytes) {
-            const double* base = v == 0 ? a.x : (v == 1 ? a.x2 : a.xv);
-            const long long off = (r0 + q) * a.g.ndof + 2LL * (P * n1 + wg.vlo);
-            bulk_g2s(st + (v * RB + q) * 512 + 16 * (wg.vlo - wg.c_first), base + off, vbytes, bar);
-        }
-    } else if (t == S::NV * RB) {
-        if (ebytes) bulk_g2s(st + S::EOFF, reinterpret_cast<const char*>(a.E) + e_al, ebytes, bar);
-    } else if (t == S::NV * RB + 1) {
-        if (mbytes) bulk_g2s(st + S::MOFF, a.mask + m_al, mbytes, bar);
-    } else if (S::HAS_C && t < S::NV * RB + 2 + RB) {
-        const int q = t - (S::NV * RB + 2);
-        if (q < nr && ((actmask >> q) & 1) && cbytes) {
-            const long long off = (r0 + q) * a.gc.ndof + 2LL * (crow * a.gc.nn[1] + wg.jl);
-            bulk_g2s(st + S::COFF + q * 288 + 16 * (wg.jl - wg.jbase), a.ec + off, cbytes, bar);
-        }
-    } else if (S::HAS_CM && t == S::NCOPY - 1) {
-        if (cmbytes) bulk_g2s(st + S::CMOFF, a.maskc + cm_al, cmbytes, bar);
-    }
-}
-
-struct LaneGeom {
-    int c, lane;
-    bool cin, own_col, ce, cel;
-    int eoff_c;   // 8 (c - clo)
-    int vo;       // 16 lane
+struct Ops {
+    static constexpr bool V1 = OP == M2_CGP || OP == M2_RESTRICT || OP == M2_RESID || OP == M2_JACOBI;
+    static constexpr bool XV = OP == M2_CGP;
+    static constexpr bool DI = OP == M2_RESTRICT || OP == M2_POST || OP == M2_JACOBI;
 };
 
-// Per-RHS registers carried between planes.
-template <int RB>
-struct RhsState {
-    double w[RB][6];     // masked matvec input of the current plane at columns c-1, c, c+1 (x, y)
-    double u[RB][2];     // unmasked own input
-    double k[RB][2];     // b (RESID/JACOBI), p_in (CGP), r (RESTRICT/POST)
-    double k2[RB][2];    // x (CGP)
-    double car[RB][2];   // contribution of the element layer below to the next plane
-    double dot[RB];
-    double acc[RB][2];   // RESTRICT: running coarse sums
-    double cev[RB][4];   // POST: coarse correction of the last even plane (J0 x,y, J1 x,y)
-};
-
-template <int OP, bool C03, int RB>
-__global__ void __launch_bounds__(32 * WPB) march2_kernel(March2Args a, int nct, int nch, int nrc) {
-    using S = Stage<OP, RB>;
-    constexpr int CS = (OP == M2_RESTRICT) ? 28 : 30;
-    constexpr int LOFF = (OP == M2_RESTRICT) ? 2 : 1;
-    extern __shared__ __align__(128) char smem_raw[];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    char* wsm = smem_raw + wid * (NS * S::BYTES + NS * 8);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(wsm + NS * S::BYTES);
-    const long long w = (long long)blockIdx.x * WPB + wid;
+template <int OP, bool C03>
+__global__ void __launch_bounds__(32 * WPB) march2_kernel(March2Args a, int nct, int nch) {
+    constexpr int CS = (OP == M2_RESTRICT) ? 28 : 30;      // owned columns per warp
+    constexpr int LOFF = (OP == M2_RESTRICT) ? 2 : 1;      // lane of the first owned column
+    const int lane = threadIdx.x & 31;
+    const long long w = (long long)blockIdx.x * WPB + (threadIdx.x >> 5);
     const int items = nct * nch;
-    if (w >= (long long)nrc * items) return;
+    if (w >= (long long)a.R * items) return;
     if (a.done && *a.done) return;
-    const int rc = (int)(w % nrc);
-    const int item = (int)(w / nrc);
-    const int r0 = (rc * a.R) / nrc, r1 = ((rc + 1) * a.R) / nrc, nr = r1 - r0;
-    unsigned actmask = 0;
-#pragma unroll
-    for (int q = 0; q < RB; ++q)
-        if (q < nr && (!a.active || a.active[r0 + q])) actmask |= 1u << q;
-    if (!actmask) return;
+    const int r = (int)(w % a.R);
+    const int item = (int)(w / a.R);
+    if (a.active && !a.active[r]) return;
     const int ct = item % nct, ch = item / nct;
-    const int n0 = a.g.nn[0], n1 = a.g.nn[1], N0 = a.g.N[0], N1 = a.g.N[1];
-    WarpGeom wg;
-    wg.c_first = ct * CS - LOFF;
-    wg.vlo = max(wg.c_first, 0);
-    wg.vhi = min(wg.c_first + 32, n1);
-    wg.clo = max(wg.c_first - 1, 0);
-    wg.chi = min(wg.c_first + 32, N1);
-    wg.jbase = wg.c_first >> 1;
-    wg.jl = max(wg.c_first >> 1, 0);
-    wg.jh = (OP == M2_POST || OP == M2_RESTRICT) ? min((wg.c_first + 32) >> 1, a.gc.nn[1] - 1) : 0;
-    LaneGeom lg;
-    lg.lane = lane;
-    lg.c = wg.c_first + lane;
-    lg.cin = lg.c >= 0 && lg.c < n1;
-    lg.own_col = lg.cin && lane >= LOFF && lane < LOFF + CS;
-    lg.ce = lg.cin && lg.c < N1;
-    lg.cel = lg.cin && lg.c >= 1 && lg.c - 1 < N1;
-    lg.eoff_c = 8 * (lg.c - wg.clo);
-    lg.vo = 16 * lane;
-    const int c = lg.c;
+    const int n0 = a.g.nn[0], n1 = a.g.nn[1];
+    const int c = ct * CS + lane - LOFF;
+    const bool cin = c >= 0 && c < n1;
+    const bool own_col = cin && lane >= LOFF && lane < LOFF + CS;
     int i0, i1, own0, own1, I0 = 0, I1 = 0;
     if (OP == M2_RESTRICT) {
         const int nc0 = a.gc.nn[0];
@@ -226,270 +191,238 @@ __global__ void __launch_bounds__(32 * WPB) march2_kernel(March2Args a, int nct,
         own0 = i0;
         own1 = i1;
     }
+    const Pad2& pd = a.pd;
+    const long long vb = (long long)r * pd.vstride;
+    const long long vbc = (OP == M2_RESTRICT || OP == M2_POST) ? (long long)r * a.gc.ndof : 0;
+    const double* x0b = a.x + vb;
+    const double* x1b = Ops<OP>::V1 ? a.x2 + vb : nullptr;
+    double* xvb = Ops<OP>::XV ? a.xv + vb : nullptr;
+    double* yb = (OP != M2_RESTRICT) ? a.y + vb : nullptr;
+    double* y2b = (OP == M2_CGP || OP == M2_RESTRICT) ? a.y2 + vb : nullptr;
+    const double beta = (OP == M2_CGP) ? a.beta[r] : 0.0;
+    const double alpha = (OP == M2_RESTRICT) ? a.alpha[r] : 0.0;
+    const double xalpha = (OP == M2_CGP) ? a.xalpha[r] : 0.0;
     const double omega = a.omega;
-    const double k0d = K2<C03>(0, 0);
-    const int nplanes = i1 - i0 + 2;     // planes i0-1 .. i1
-    double coef[RB];                     // beta (CGP) / alpha (RESTRICT) per RHS
-    double xal[RB];                      // xalpha (CGP)
-#pragma unroll
-    for (int q = 0; q < RB; ++q) {
-        const int rr = min(r0 + q, a.R - 1);
-        coef[q] = OP == M2_CGP ? a.beta[rr] : (OP == M2_RESTRICT ? a.alpha[rr] : 0.0);
-        xal[q] = OP == M2_CGP ? a.xalpha[rr] : 0.0;
-    }
+    const int nc1 = (OP == M2_RESTRICT || OP == M2_POST) ? a.gc.nn[1] : 0;
+    const int J0 = c >> 1, J1 = (c + 1) >> 1;
 
-    if (lane == 0) {
-        for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        fence_proxy_async();
-    }
-    __syncwarp();
-    for (int k = 0; k < NS && k < nplanes; ++k)
-        issue_plane<OP, RB>(a, wg, wsm + k * S::BYTES, &bars[k], i0 - 1 + k, r0, nr, actmask, lane);
-
-    RhsState<RB> rs;
-#pragma unroll
-    for (int q = 0; q < RB; ++q) {
-#pragma unroll
-        for (int j = 0; j < 6; ++j) rs.w[q][j] = 0.0;
-        rs.u[q][0] = rs.u[q][1] = rs.k[q][0] = rs.k[q][1] = rs.k2[q][0] = rs.k2[q][1] = 0.0;
-        rs.car[q][0] = rs.car[q][1] = 0.0;
-        rs.dot[q] = 0.0;
-        rs.acc[q][0] = rs.acc[q][1] = 0.0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) rs.cev[q][j] = 0.0;
-    }
-    // plane-shared state of the current plane
-    int mA = 3;
-    double DA = 1.0, eA = 0.0, elA = 0.0;
-    {   // E of layer i0-2 (diagonal of the first plane): direct loads, once per chunk
-        const int Lp = i0 - 2;
-        if (Lp >= 0 && Lp < N0) {
-            if (lg.ce) eA = a.E[Lp * N1 + c];
-            if (lg.cel) elA = a.E[Lp * N1 + c - 1];
+    // padded offsets of plane P at this lane's column: node org + P*pitch + c, element orgE + P*pitchE + c
+    auto load = [&](Slot& s, int P) {
+        const long long no = pd.org + (long long)P * pd.pitch + c;
+        const long long eo = pd.orgE + (long long)P * pd.pitchE + c;
+        const double2 v0 = ldg2(x0b + 2 * no);
+        s.v0x = v0.x; s.v0y = v0.y;
+        if (Ops<OP>::V1) { const double2 v1 = ldg2(x1b + 2 * no); s.v1x = v1.x; s.v1y = v1.y; }
+        if (Ops<OP>::XV) { const double2 v2 = ld2(xvb + 2 * no); s.xx = v2.x; s.xy = v2.y; }
+        if (Ops<OP>::DI) { const double2 d = ldg2(a.Dinv + 2 * no); s.dx = d.x; s.dy = d.y; }
+        s.e = __ldg(a.E + eo);
+        s.el = __ldg(a.E + eo - 1);
+        s.m = __ldg(a.mask + no);
+        if (OP == M2_POST) {
+            s.cx0 = s.cy0 = s.cx1 = s.cy1 = 0.0;
+            const int I = (P + 1) >> 1;
+            if ((P & 1) && cin && I < a.gc.nn[0]) {
+                const long long row = (long long)I * nc1;
+                const int m0 = a.maskc[row + J0], m1 = a.maskc[row + J1];
+                const double2 e0 = ld2(a.ec + vbc + 2 * (row + J0));
+                const double2 e1 = ld2(a.ec + vbc + 2 * (row + J1));
+                s.cx0 = (m0 & 1) ? 0.0 : e0.x; s.cy0 = (m0 & 2) ? 0.0 : e0.y;
+                s.cx1 = (m1 & 1) ? 0.0 : e1.x; s.cy1 = (m1 & 2) ? 0.0 : e1.y;
+            }
         }
-    }
-    if (OP == M2_POST) {   // coarse row floor(P0/2) of the first plane, per RHS (direct loads, once)
+        if (OP == M2_RESTRICT) {
+            s.cm = 3;
+            const int I = (P - 1) >> 1;
+            if (P >= 1 && cin && !(c & 1) && I < a.gc.nn[0]) s.cm = a.maskc[(long long)I * nc1 + J0];
+        }
+    };
+
+    // plane state
+    double A0x, A0y, A1x, A1y, A2x, A2y;      // masked input at c-1, c, c+1 of plane L
+    double urx, ury, auxx = 0, auxy = 0, aux2x = 0, aux2y = 0, dax = 1, day = 1;
+    double ex, exl;                           // E of layer L at c, c-1
+    int mA;
+    double cev[4] = {0.0, 0.0, 0.0, 0.0};     // POST: coarse row of the last even plane
+    double carx = 0.0, cary = 0.0, dot = 0.0, accx = 0.0, accy = 0.0;
+    if (OP == M2_POST) {
         const int rlo = (i0 - 1) >> 1;
-        if (lg.cin && rlo >= 0) {
-            const int nc1 = a.gc.nn[1];
-            const int J0 = c >> 1, J1 = (c + 1) >> 1;
-            const int row = rlo * nc1;
+        if (cin && rlo >= 0) {
+            const long long row = (long long)rlo * nc1;
             const int m0 = a.maskc[row + J0], m1 = a.maskc[row + J1];
-#pragma unroll
-            for (int q = 0; q < RB; ++q) {
-                if (!((actmask >> q) & 1)) continue;
-                const double* ecb = a.ec + (long long)(r0 + q) * a.gc.ndof;
-                const double2 e0 = ld2(ecb + 2 * (row + J0));
-                const double2 e1 = ld2(ecb + 2 * (row + J1));
-                rs.cev[q][0] = (m0 & 1) ? 0.0 : e0.x; rs.cev[q][1] = (m0 & 2) ? 0.0 : e0.y;
-                rs.cev[q][2] = (m1 & 1) ? 0.0 : e1.x; rs.cev[q][3] = (m1 & 2) ? 0.0 : e1.y;
-            }
+            const double2 e0 = ld2(a.ec + vbc + 2 * (row + J0));
+            const double2 e1 = ld2(a.ec + vbc + 2 * (row + J1));
+            cev[0] = (m0 & 1) ? 0.0 : e0.x; cev[1] = (m0 & 2) ? 0.0 : e0.y;
+            cev[2] = (m1 & 1) ? 0.0 : e1.x; cev[3] = (m1 & 2) ? 0.0 : e1.y;
         }
     }
 
-    for (int k = 0; k < nplanes; ++k) {
-        const int stg = k % NS;
-        const int P = i0 - 1 + k;
-        mbar_wait(&bars[stg], (uint32_t)((k / NS) & 1));
-        const char* st = wsm + stg * S::BYTES;
-        // ---- plane-shared values: mask, E, diagonal, coarse masks
-        const bool pv = P >= 0 && P < n0;
-        int m = 3;
-        double e = 0.0, el = 0.0;
-        if (pv && lg.cin) m = *reinterpret_cast<const uint8_t*>(st + S::MOFF + ((P * n1 + wg.vlo) & 15) + (c - wg.vlo));
-        if (P >= 0 && P < N0) {
-            const int eo = ((8 * (P * N1 + wg.clo)) & 15) + lg.eoff_c;
-            if (lg.ce) e = *reinterpret_cast<const double*>(st + S::EOFF + eo);
-            if (lg.cel) el = *reinterpret_cast<const double*>(st + S::EOFF + eo - 8);
-        }
-        const double D = k0d * ((elA + eA) + (el + e));
-        const double id = D > 0.0 ? omega / D : 0.0;
-        const bool fx = m & 1, fy = m & 2;
+    // derive the matvec input (u) of plane P from its slot; keeps the op's per-plane values
+    auto derive = [&](const Slot& s, int P, double& ux, double& uy, double& kx, double& ky, double& k2x,
+                      double& k2y) {
+        const bool fx = s.m & 1, fy = s.m & 2;
         const bool own_plane = P >= own0 && P < own1;
-        int cm = 3, cm0 = 3, cm1 = 3, cmf = 0;
-        const int crow = S::HAS_CM ? coarse_row<OP>(a, P) : -1;
-        if (S::HAS_CM && crow >= 0 && lg.cin) {
-            cmf = (crow * a.gc.nn[1] + wg.jl) & 15;
-            if (S::HAS_C) {
-                cm0 = *reinterpret_cast<const uint8_t*>(st + S::CMOFF + cmf + ((c >> 1) - wg.jl));
-                cm1 = *reinterpret_cast<const uint8_t*>(st + S::CMOFF + cmf + (((c + 1) >> 1) - wg.jl));
-            } else if (!(c & 1)) {
-                cm = *reinterpret_cast<const uint8_t*>(st + S::CMOFF + cmf + ((c >> 1) - wg.jl));
+        if (OP == M2_CGP) {
+            ux = fma(beta, s.v1x, s.v0x);
+            uy = fma(beta, s.v1y, s.v0y);
+            if (own_col && own_plane) st2(y2b + 2 * (pd.org + (long long)P * pd.pitch + c), ux, uy);
+            kx = s.v1x; ky = s.v1y;
+            k2x = s.xx; k2y = s.xy;
+        } else if (OP == M2_RESTRICT) {
+            const double rx = fma(-alpha, s.v1x, s.v0x), ry = fma(-alpha, s.v1y, s.v0y);
+            if (own_col && own_plane) {
+                st2(y2b + 2 * (pd.org + (long long)P * pd.pitch + c), rx, ry);
+                dot = fma(rx, rx, dot);
+                dot = fma(ry, ry, dot);
             }
-        }
-        const int L = P - 1;
-        const bool fin = k > 0 && L >= i0;
-        const bool own = lg.own_col && L >= own0 && L < own1;
-        // ---- per RHS
-#pragma unroll
-        for (int q = 0; q < RB; ++q) {
-            if (!((actmask >> q) & 1)) continue;
-            const long long vb = (long long)(r0 + q) * a.g.ndof;
-            double v0x = 0, v0y = 0, v1x = 0, v1y = 0, xx = 0, xy = 0;
-            if (pv && lg.cin) {
-                const double2 x0 = *reinterpret_cast<const double2*>(st + (0 * RB + q) * 512 + lg.vo);
-                v0x = x0.x; v0y = x0.y;
-                if (S::NV >= 2) {
-                    const double2 x1 = *reinterpret_cast<const double2*>(st + (1 * RB + q) * 512 + lg.vo);
-                    v1x = x1.x; v1y = x1.y;
-                }
-                if (S::NV >= 3) {
-                    const double2 x2 = *reinterpret_cast<const double2*>(st + (2 * RB + q) * 512 + lg.vo);
-                    xx = x2.x; xy = x2.y;
-                }
-            }
-            double ux, uy, kx, ky;
-            if (OP == M2_CGP) {
-                ux = fma(coef[q], v1x, v0x);
-                uy = fma(coef[q], v1y, v0y);
-                if (lg.own_col && own_plane) st2(a.y2 + vb + 2 * (P * n1 + c), ux, uy);
-                kx = v1x; ky = v1y;
-            } else if (OP == M2_RESTRICT) {
-                const double rx = fma(-coef[q], v1x, v0x), ry = fma(-coef[q], v1y, v0y);
-                if (lg.own_col && own_plane) {
-                    st2(a.y2 + vb + 2 * (P * n1 + c), rx, ry);
-                    rs.dot[q] = fma(rx, rx, rs.dot[q]);
-                    rs.dot[q] = fma(ry, ry, rs.dot[q]);
-                }
-                kx = rx; ky = ry;
-                ux = fx ? 0.0 : id * rx;
-                uy = fy ? 0.0 : id * ry;
-            } else if (OP == M2_POST) {
-                double cx0 = 0, cy0 = 0, cx1 = 0, cy1 = 0;
-                if (crow >= 0 && lg.cin) {
-                    const char* cp = st + S::COFF + q * 288;
-                    const double2 e0 = *reinterpret_cast<const double2*>(cp + 16 * ((c >> 1) - wg.jbase));
-                    const double2 e1 = *reinterpret_cast<const double2*>(cp + 16 * (((c + 1) >> 1) - wg.jbase));
-                    cx0 = (cm0 & 1) ? 0.0 : e0.x; cy0 = (cm0 & 2) ? 0.0 : e0.y;
-                    cx1 = (cm1 & 1) ? 0.0 : e1.x; cy1 = (cm1 & 2) ? 0.0 : e1.y;
-                }
-                double px, py;
-                const bool codd = c & 1;
-                if (P & 1) {
-                    const double lx = codd ? 0.5 * (rs.cev[q][0] + rs.cev[q][2]) : rs.cev[q][0];
-                    const double ly = codd ? 0.5 * (rs.cev[q][1] + rs.cev[q][3]) : rs.cev[q][1];
-                    const double hx = codd ? 0.5 * (cx0 + cx1) : cx0, hy = codd ? 0.5 * (cy0 + cy1) : cy0;
-                    px = 0.5 * (lx + hx);
-                    py = 0.5 * (ly + hy);
-                    rs.cev[q][0] = cx0; rs.cev[q][1] = cy0; rs.cev[q][2] = cx1; rs.cev[q][3] = cy1;
-                } else {
-                    px = codd ? 0.5 * (rs.cev[q][0] + rs.cev[q][2]) : rs.cev[q][0];
-                    py = codd ? 0.5 * (rs.cev[q][1] + rs.cev[q][3]) : rs.cev[q][1];
-                }
-                ux = fx ? 0.0 : fma(id, v0x, px);
-                uy = fy ? 0.0 : fma(id, v0y, py);
-                kx = v0x; ky = v0y;
+            kx = rx; ky = ry;
+            ux = fx ? 0.0 : omega * s.dx * rx;
+            uy = fy ? 0.0 : omega * s.dy * ry;
+            k2x = (double)s.cm;
+        } else if (OP == M2_POST) {
+            double px, py;
+            const bool codd = c & 1;
+            if (P & 1) {
+                const double lx = codd ? 0.5 * (cev[0] + cev[2]) : cev[0], ly = codd ? 0.5 * (cev[1] + cev[3]) : cev[1];
+                const double hx = codd ? 0.5 * (s.cx0 + s.cx1) : s.cx0, hy = codd ? 0.5 * (s.cy0 + s.cy1) : s.cy0;
+                px = 0.5 * (lx + hx);
+                py = 0.5 * (ly + hy);
+                cev[0] = s.cx0; cev[1] = s.cy0; cev[2] = s.cx1; cev[3] = s.cy1;
             } else {
-                ux = v0x; uy = v0y;
-                kx = v1x; ky = v1y;
+                px = codd ? 0.5 * (cev[0] + cev[2]) : cev[0];
+                py = codd ? 0.5 * (cev[1] + cev[3]) : cev[1];
             }
-            const double mx = fx ? 0.0 : ux, my = fy ? 0.0 : uy;
-            double nw[6];
-            nw[2] = mx; nw[3] = my;
-            nw[0] = shfl_up1(mx); nw[1] = shfl_up1(my);
-            nw[4] = shfl_dn1(mx); nw[5] = shfl_dn1(my);
-            if (k > 0) {
-                // element layer L between the current plane (rs.w) and plane P (nw)
-                double lox = rs.car[q][0], loy = rs.car[q][1], hix = 0.0, hiy = 0.0;
+            ux = fx ? 0.0 : fma(omega * s.dx, s.v0x, px);
+            uy = fy ? 0.0 : fma(omega * s.dy, s.v0y, py);
+            kx = s.v0x; ky = s.v0y;
+            k2x = k2y = 0.0;
+        } else {
+            ux = s.v0x; uy = s.v0y;
+            kx = s.v1x; ky = s.v1y;
+            k2x = k2y = 0.0;
+        }
+    };
+
+    // ---- prologue: plane i0-1 and the prefetch ring
+    Slot ring[PD];
+    {
+        Slot s0;
+        load(s0, i0 - 1);
 #pragma unroll
-                for (int ee = 0; ee < 2; ++ee) {
-                    const double Ee = ee ? eA : elA;
-                    const int a1 = 1 - ee;
-                    double tlx = 0, tly = 0, thx = 0, thy = 0;
+        for (int u = 0; u < PD; ++u) load(ring[u], min(i0 + u, i1));
+        double ux, uy;
+        derive(s0, i0 - 1, ux, uy, auxx, auxy, aux2x, aux2y);
+        mA = s0.m;
+        urx = ux; ury = uy;
+        dax = s0.dx; day = s0.dy;
+        const double mx = (mA & 1) ? 0.0 : ux, my = (mA & 2) ? 0.0 : uy;
+        A1x = mx; A1y = my;
+        A0x = shfl_up1(mx); A0y = shfl_up1(my);
+        A2x = shfl_dn1(mx); A2y = shfl_dn1(my);
+        ex = s0.e; exl = s0.el;
+    }
+
+    for (int L0 = i0 - 1; L0 < i1; L0 += PD) {
 #pragma unroll
-                    for (int b0 = 0; b0 < 2; ++b0)
+        for (int u = 0; u < PD; ++u) {
+            const int L = L0 + u;
+            if (L >= i1) break;
+            const Slot s = ring[u];
+            if (L + 1 + PD <= i1) load(ring[u], L + 1 + PD);
+            const int P = L + 1;
+            double ux, uy, kx, ky, k2x, k2y;
+            derive(s, P, ux, uy, kx, ky, k2x, k2y);
+            const double mx = (s.m & 1) ? 0.0 : ux, my = (s.m & 2) ? 0.0 : uy;
+            const double B1x = mx, B1y = my;
+            const double B0x = shfl_up1(mx), B0y = shfl_up1(my);
+            const double B2x = shfl_dn1(mx), B2y = shfl_dn1(my);
+            // element layer L: e=0 -> element column c-1, e=1 -> column c
+            double lox = carx, loy = cary, hix = 0.0, hiy = 0.0;
 #pragma unroll
-                        for (int b1 = 0; b1 < 2; ++b1)
+            for (int e = 0; e < 2; ++e) {
+                const double Ee = e ? ex : exl;
+                const int a1 = 1 - e;
+                double tlx = 0, tly = 0, thx = 0, thy = 0;
 #pragma unroll
-                            for (int k2 = 0; k2 < 2; ++k2) {
-                                const int qq = ee + b1;
-                                const double xv = b0 ? nw[2 * qq + k2] : rs.w[q][2 * qq + k2];
-                                const int col = (b0 * 2 + b1) * 2 + k2;
-                                const int rl = (0 * 2 + a1) * 2, rh = (1 * 2 + a1) * 2;
-                                if (!C03 || K2<C03>(rl + 0, col) != 0.0) tlx = fma(K2<C03>(rl + 0, col), xv, tlx);
-                                if (!C03 || K2<C03>(rl + 1, col) != 0.0) tly = fma(K2<C03>(rl + 1, col), xv, tly);
-                                if (!C03 || K2<C03>(rh + 0, col) != 0.0) thx = fma(K2<C03>(rh + 0, col), xv, thx);
-                                if (!C03 || K2<C03>(rh + 1, col) != 0.0) thy = fma(K2<C03>(rh + 1, col), xv, thy);
-                            }
-                    lox = fma(Ee, tlx, lox); loy = fma(Ee, tly, loy);
-                    hix = fma(Ee, thx, hix); hiy = fma(Ee, thy, hiy);
-                }
-                rs.car[q][0] = hix; rs.car[q][1] = hiy;
-                if (fin) {
-                    const double Axx = (mA & 1) ? rs.u[q][0] : lox, Axy = (mA & 2) ? rs.u[q][1] : loy;
-                    const int o = 2 * (L * n1 + c);
-                    if (OP == M2_MATVEC) {
-                        if (own) st2(a.y + vb + o, Axx, Axy);
-                    } else if (OP == M2_RESID) {
-                        if (own) st2(a.y + vb + o, rs.k[q][0] - Axx, rs.k[q][1] - Axy);
-                    } else if (OP == M2_JACOBI || OP == M2_POST) {
-                        const double idA = omega / DA;
-                        const double zx = fma((mA & 1) ? omega : idA, rs.k[q][0] - Axx, rs.u[q][0]);
-                        const double zy = fma((mA & 2) ? omega : idA, rs.k[q][1] - Axy, rs.u[q][1]);
-                        if (own) {
-                            st2(a.y + vb + o, zx, zy);
-                            rs.dot[q] = fma(rs.k[q][0], zx, rs.dot[q]);
-                            rs.dot[q] = fma(rs.k[q][1], zy, rs.dot[q]);
+                for (int b0 = 0; b0 < 2; ++b0)
+#pragma unroll
+                    for (int b1 = 0; b1 < 2; ++b1)
+#pragma unroll
+                        for (int k2 = 0; k2 < 2; ++k2) {
+                            const int q = e + b1;
+                            const double xv = b0 ? (q == 0 ? (k2 ? B0y : B0x) : q == 1 ? (k2 ? B1y : B1x) : (k2 ? B2y : B2x))
+                                                 : (q == 0 ? (k2 ? A0y : A0x) : q == 1 ? (k2 ? A1y : A1x) : (k2 ? A2y : A2x));
+                            const int col = (b0 * 2 + b1) * 2 + k2;
+                            const int rl = (0 * 2 + a1) * 2, rh = (1 * 2 + a1) * 2;
+                            if (!C03 || K2<C03>(rl + 0, col) != 0.0) tlx = fma(K2<C03>(rl + 0, col), xv, tlx);
+                            if (!C03 || K2<C03>(rl + 1, col) != 0.0) tly = fma(K2<C03>(rl + 1, col), xv, tly);
+                            if (!C03 || K2<C03>(rh + 0, col) != 0.0) thx = fma(K2<C03>(rh + 0, col), xv, thx);
+                            if (!C03 || K2<C03>(rh + 1, col) != 0.0) thy = fma(K2<C03>(rh + 1, col), xv, thy);
                         }
-                    } else if (OP == M2_CGP) {
-                        if (own) {
-                            st2(a.y + vb + o, Axx, Axy);
-                            rs.dot[q] = fma(rs.u[q][0], Axx, rs.dot[q]);
-                            rs.dot[q] = fma(rs.u[q][1], Axy, rs.dot[q]);
-                            st2(a.xv + vb + o, fma(xal[q], rs.k[q][0], rs.k2[q][0]), fma(xal[q], rs.k[q][1], rs.k2[q][1]));
-                        }
-                    } else if (OP == M2_RESTRICT) {
-                        const bool tv = lg.cin && lane >= 1 && lane <= 30;
-                        const double tx = (tv && !(mA & 1)) ? rs.k[q][0] - Axx : 0.0;
-                        const double ty = (tv && !(mA & 2)) ? rs.k[q][1] - Axy : 0.0;
-                        const double tlx = shfl_up1(tx), tly = shfl_up1(ty);
-                        const double trx = shfl_dn1(tx), try_ = shfl_dn1(ty);
-                        const double hx = fma(0.5, tlx + trx, tx), hy = fma(0.5, tly + try_, ty);
-                        const bool cown = lg.cin && !(c & 1) && lane >= 2 && lane <= 28;
-                        const int nc1 = a.gc.nn[1];
-                        const long long cb = (long long)(r0 + q) * a.gc.ndof;
-                        if (L & 1) {
-                            rs.acc[q][0] = fma(0.5, hx, rs.acc[q][0]);
-                            rs.acc[q][1] = fma(0.5, hy, rs.acc[q][1]);
-                            const int I = (L - 1) >> 1;
-                            if (cown && I >= I0 && I < I1)
-                                st2(a.coarse + cb + 2 * (I * nc1 + (c >> 1)), (cm & 1) ? 0.0 : rs.acc[q][0],
-                                    (cm & 2) ? 0.0 : rs.acc[q][1]);
-                            rs.acc[q][0] = 0.5 * hx;
-                            rs.acc[q][1] = 0.5 * hy;
-                        } else {
-                            rs.acc[q][0] += hx;
-                            rs.acc[q][1] += hy;
-                            const int I = L >> 1;
-                            if (L == n0 - 1 && cown && I >= I0 && I < I1)
-                                st2(a.coarse + cb + 2 * (I * nc1 + (c >> 1)), (cm & 1) ? 0.0 : rs.acc[q][0],
-                                    (cm & 2) ? 0.0 : rs.acc[q][1]);
-                        }
+                lox = fma(Ee, tlx, lox); loy = fma(Ee, tly, loy);
+                hix = fma(Ee, thx, hix); hiy = fma(Ee, thy, hiy);
+            }
+            // ---- finish node plane L
+            if (L >= i0) {
+                const double Axx = (mA & 1) ? urx : lox, Axy = (mA & 2) ? ury : loy;
+                const bool own = own_col && L >= own0 && L < own1;
+                const long long o = 2 * (pd.org + (long long)L * pd.pitch + c);
+                if (OP == M2_MATVEC) {
+                    if (own) st2(yb + o, Axx, Axy);
+                } else if (OP == M2_RESID) {
+                    if (own) st2(yb + o, auxx - Axx, auxy - Axy);
+                } else if (OP == M2_JACOBI || OP == M2_POST) {
+                    const double zx = fma(omega * dax, auxx - Axx, urx);
+                    const double zy = fma(omega * day, auxy - Axy, ury);
+                    if (own) {
+                        st2(yb + o, zx, zy);
+                        dot = fma(auxx, zx, dot);
+                        dot = fma(auxy, zy, dot);
+                    }
+                } else if (OP == M2_CGP) {
+                    if (own) {
+                        st2(yb + o, Axx, Axy);
+                        dot = fma(urx, Axx, dot);
+                        dot = fma(ury, Axy, dot);
+                        st2(xvb + o, fma(xalpha, auxx, aux2x), fma(xalpha, auxy, aux2y));
+                    }
+                } else if (OP == M2_RESTRICT) {
+                    // t = r - K z1 (lanes 1..30 valid), then P^T: columns by shuffles, planes by carry
+                    const bool tv = cin && lane >= 1 && lane <= 30;
+                    const double tx = (tv && !(mA & 1)) ? auxx - Axx : 0.0;
+                    const double ty = (tv && !(mA & 2)) ? auxy - Axy : 0.0;
+                    const double tlx = shfl_up1(tx), tly = shfl_up1(ty);
+                    const double trx = shfl_dn1(tx), try_ = shfl_dn1(ty);
+                    const double hx = fma(0.5, tlx + trx, tx), hy = fma(0.5, tly + try_, ty);
+                    const bool cown = cin && !(c & 1) && lane >= 2 && lane <= 28;
+                    const int cm = (int)k2x;     // coarse mask of row (P-1)>>1 = the row output below
+                    if (L & 1) {
+                        accx = fma(0.5, hx, accx); accy = fma(0.5, hy, accy);
+                        const int I = (L - 1) >> 1;
+                        if (cown && I >= I0 && I < I1)
+                            st2(a.coarse + vbc + 2 * ((long long)I * nc1 + J0), (cm & 1) ? 0.0 : accx,
+                                (cm & 2) ? 0.0 : accy);
+                        accx = 0.5 * hx; accy = 0.5 * hy;
+                    } else {
+                        accx += hx; accy += hy;
+                        const int I = L >> 1;
+                        if (L == n0 - 1 && cown && I >= I0 && I < I1)
+                            st2(a.coarse + vbc + 2 * ((long long)I * nc1 + J0), (cm & 1) ? 0.0 : accx,
+                                (cm & 2) ? 0.0 : accy);
                     }
                 }
             }
-            // ---- shift plane P -> current
-#pragma unroll
-            for (int j = 0; j < 6; ++j) rs.w[q][j] = nw[j];
-            rs.u[q][0] = ux; rs.u[q][1] = uy;
-            rs.k[q][0] = kx; rs.k[q][1] = ky;
-            if (OP == M2_CGP) { rs.k2[q][0] = xx; rs.k2[q][1] = xy; }
-        }
-        mA = m; DA = D; eA = e; elA = el;
-        __syncwarp();
-        if (k + NS < nplanes) {
-            if (lane == 0) fence_proxy_async();
-            issue_plane<OP, RB>(a, wg, wsm + stg * S::BYTES, &bars[stg], P + NS, r0, nr, actmask, lane);
+            // ---- shift plane L+1 -> L
+            carx = hix; cary = hiy;
+            A0x = B0x; A0y = B0y; A1x = B1x; A1y = B1y; A2x = B2x; A2y = B2y;
+            urx = ux; ury = uy; mA = s.m;
+            auxx = kx; auxy = ky; aux2x = k2x; aux2y = k2y;
+            dax = s.dx; day = s.dy;
+            ex = s.e; exl = s.el;
         }
     }
     if (a.partial) {
-#pragma unroll
-        for (int q = 0; q < RB; ++q) {
-            if (!((actmask >> q) & 1)) continue;
-            const double d = warp_sum(rs.dot[q]);
-            if (lane == 0) a.partial[(long long)(r0 + q) * items + item] = d;
-        }
+        dot = warp_sum(dot);
+        if (lane == 0) a.partial[(long long)r * items + item] = dot;
     }
 }
 
@@ -504,22 +437,6 @@ int march2_items(int op, const LevelGeom& g, const LevelGeom* gc) {
     return nct * nch;
 }
 
-template <int OP, int RB>
-static void launch2_rb(const March2Args& a, bool c03, int nct, int nch, cudaStream_t s) {
-    const int nrc = (a.R + RB - 1) / RB;
-    const long long warps = (long long)nrc * nct * nch;
-    const unsigned blocks = (unsigned)((warps + WPB - 1) / WPB);
-    const int smem = WPB * NS * (Stage<OP, RB>::BYTES + 8);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(march2_kernel<OP, true, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(march2_kernel<OP, false, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
-    }
-    if (c03) march2_kernel<OP, true, RB><<<blocks, 32 * WPB, smem, s>>>(a, nct, nch, nrc);
-    else march2_kernel<OP, false, RB><<<blocks, 32 * WPB, smem, s>>>(a, nct, nch, nrc);
-}
-
 template <int OP>
 static void launch2(const March2Args& a, bool c03, cudaStream_t s) {
     int nct, nch;
@@ -530,7 +447,10 @@ static void launch2(const March2Args& a, bool c03, cudaStream_t s) {
         nct = (a.g.nn[1] + 29) / 30;
         nch = (a.g.nn[0] + CH - 1) / CH;
     }
-    launch2_rb<OP, 1>(a, c03, nct, nch, s);   // RHS blocking (RB > 1) measured slower: register bound
+    const long long warps = (long long)a.R * nct * nch;
+    const unsigned blocks = (unsigned)((warps + WPB - 1) / WPB);
+    if (c03) march2_kernel<OP, true><<<blocks, 32 * WPB, 0, s>>>(a, nct, nch);
+    else march2_kernel<OP, false><<<blocks, 32 * WPB, 0, s>>>(a, nct, nch);
 }
 
 int march2_apply(int op, const March2Args& a, bool c03, cudaStream_t s) {

@@ -220,22 +220,6 @@ static void launch_fine(const FineArgs& a, cudaStream_t s) {
 }
 
 int fine_apply(int op, const FineArgs& a, cudaStream_t s) {
-    if (a.g.dim == 2) {   // 2D: prefetching march kernels of fine2d.cu
-        March2Args m{};
-        m.g = a.g; m.E = a.E; m.mask = a.mask; m.omega = a.omega; m.active = a.active; m.done = a.done;
-        m.partial = a.partial; m.R = a.R;
-        int mop;
-        switch (op) {
-            case FOP_MATVEC: mop = M2_MATVEC; m.x = a.x; m.y = a.y; break;
-            case FOP_RESID: mop = M2_RESID; m.x = a.x; m.x2 = a.b; m.y = a.y; break;
-            case FOP_JACOBI: mop = M2_JACOBI; m.x = a.x; m.x2 = a.b; m.y = a.y; break;
-            default:
-                mop = M2_CGP; m.x = a.z; m.x2 = a.pin; m.y2 = a.pout; m.y = a.y; m.beta = a.beta;
-                m.xv = a.xv; m.xalpha = a.xalpha;
-                break;
-        }
-        return march2_apply(mop, m, a.nu_paper != 0, s);
-    }
     switch (op) {
         case FOP_MATVEC: launch_fine<FOP_MATVEC>(a, s); break;
         case FOP_RESID: launch_fine<FOP_RESID>(a, s); break;

@@ -38,11 +38,26 @@ void fine_diag(const LevelGeom& g, const double* E, const uint8_t* mask, double*
 // ---------------------------------------------------------------- 2D fused march kernels (fine2d.cu)
 enum March2Op { M2_MATVEC = 0, M2_RESID = 1, M2_JACOBI = 2, M2_CGP = 3, M2_RESTRICT = 4, M2_POST = 5 };
 
+// Ghost-padded layout of the 2D fine level used by the march kernels: node (i, j) at
+// org + i*pitch + j with one ghost ring (fixed mask, zero E / D^-1 / vectors) plus slack,
+// so the kernels load without bounds checks.  Vectors: vstride doubles per RHS.
+struct Pad2 {
+    int pitch;            // nodes per padded row (n1 + 2)
+    long long org;        // padded index of node (0, 0)
+    long long nodes;      // padded node count incl. slack
+    int pitchE;           // elements per padded row (N1 + 2)
+    long long orgE;       // padded index of element (0, 0)
+    long long elems;      // padded element count incl. slack
+    long long vstride;    // doubles per RHS vector (2 * nodes, rounded to 4)
+};
+
 struct March2Args {
     LevelGeom g, gc;              // fine level and next-coarser level (RESTRICT / POST)
-    const double* E;
-    const uint8_t* mask;
-    const uint8_t* maskc;
+    Pad2 pd;                      // padded fine layout (x, x2, xv, y, y2 and E, mask, Dinv below)
+    const double* E;              // padded E
+    const uint8_t* mask;          // padded node masks (ghosts: 3)
+    const double* Dinv;           // padded D^-1 (2 per node; ghosts 0)
+    const uint8_t* maskc;         // compact coarse masks
     const double* x;              // MATVEC/RESID/JACOBI: x ; CGP: z ; RESTRICT: r_in ; POST: r
     const double* x2;             // RESID/JACOBI: b ; CGP: p_in ; RESTRICT: q
     double* xv;                   // CGP: x (deferred update x += xalpha p_in)
@@ -60,6 +75,14 @@ struct March2Args {
     int R;
 };
 void fine2d_set_constants(const double* K0, cudaStream_t s);
+Pad2 pad2_layout(const LevelGeom& g);
+// compact <-> padded conversions (2D fine level)
+void pad2_nodes_u8(const LevelGeom& g, const Pad2& p, const uint8_t* src, uint8_t* dst, uint8_t fill, cudaStream_t s);
+void pad2_nodes_f64(const LevelGeom& g, const Pad2& p, const double* src, double* dst, cudaStream_t s);   // 2 per node
+void pad2_elems(const LevelGeom& g, const Pad2& p, const double* src, double* dst, cudaStream_t s);
+void pad2_vectors(const LevelGeom& g, const Pad2& p, int R, const uint8_t* mask, const double* src, double* dst,
+                  cudaStream_t s);   // compact (R, ndof) -> padded, masked (ghosts untouched)
+void unpad2_vectors(const LevelGeom& g, const Pad2& p, int R, const double* src, double* dst, cudaStream_t s);
 int march2_apply(int op, const March2Args& a, bool nu_paper, cudaStream_t s);
 int march2_items(int op, const LevelGeom& g, const LevelGeom* gc);
 

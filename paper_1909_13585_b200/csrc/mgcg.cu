@@ -103,6 +103,12 @@ struct mg_ctx {
     Level lv[MG_MAX_LEVELS];
     double* E = nullptr;
     std::vector<double> K0;
+    // 2D fine level: ghost-padded copies used by the march kernels (fine2d.cu)
+    Pad2 pd{};
+    double* Epad = nullptr;
+    uint8_t* maskpad = nullptr;
+    double* Dinvpad = nullptr;
+    long long vs = 0;         // doubles per RHS of a level-0 vector (padded in 2D, ndof in 3D)
     // coarsest dense inverse
     double* Ainv = nullptr;
     long long nL = 0, npad = 0;
@@ -181,6 +187,12 @@ static mg_status compute_operators(mg_ctx* c) {
     }()));
     fine_diag(G0(c), c->E, c->lv[0].mask, c->lv[0].Dinv, c->lv[0].D, s);
     c->launches += 2;
+    if (dim == 2) {
+        pad2_elems(G0(c), c->pd, c->E, c->Epad, s);
+        pad2_nodes_u8(G0(c), c->pd, c->lv[0].mask, c->maskpad, 3, s);
+        pad2_nodes_f64(G0(c), c->pd, c->lv[0].Dinv, c->Dinvpad, s);
+        c->launches += 3;
+    }
     CHECK_LAUNCH();
     const int NL = dim * (1 << dim);
     double* elm_prev = nullptr;
@@ -245,9 +257,12 @@ static mg_status ensure_vectors(mg_ctx* c, int R) {
     if (R <= c->Ralloc) return MG_OK;
     CU(cudaStreamSynchronize(c->stream));
     free_vectors(c);
-    const long long n = G0(c).ndof;
+    const long long n = c->vs;
     double** fv[] = {&c->b, &c->x, &c->r0, &c->r1, &c->p0, &c->p1, &c->q, &c->zf, &c->z, &c->t};
-    for (auto p : fv) CU(cudaMalloc(p, sizeof(double) * n * R));
+    for (auto p : fv) {
+        CU(cudaMalloc(p, sizeof(double) * n * R));
+        CU(cudaMemset(*p, 0, sizeof(double) * n * R));   // ghost entries of the padded layout stay 0
+    }
     for (int l = 1; l < c->L; ++l) {
         long long nl = c->lv[l].g.ndof;
         CU(cudaMalloc(&c->lv[l].r, sizeof(double) * nl * R));
@@ -284,12 +299,33 @@ static FineArgs fine_args(mg_ctx* c, const Rec& rc) {
     return a;
 }
 
+// Level-0 operator application: 2D through the padded march kernels, 3D through fine_ops.
+static int level0_apply(mg_ctx* c, int op, const FineArgs& f) {
+    if (c->dim != 2) return fine_apply(op, f, c->stream);
+    March2Args m{};
+    m.g = G0(c);
+    if (c->L > 1) { m.gc = c->lv[1].g; m.maskc = c->lv[1].mask; }
+    m.pd = c->pd; m.E = c->Epad; m.mask = c->maskpad; m.Dinv = c->Dinvpad;
+    m.omega = f.omega; m.active = f.active; m.done = f.done; m.partial = f.partial; m.R = f.R;
+    int mop;
+    switch (op) {
+        case FOP_MATVEC: mop = M2_MATVEC; m.x = f.x; m.y = f.y; break;
+        case FOP_RESID: mop = M2_RESID; m.x = f.x; m.x2 = f.b; m.y = f.y; break;
+        case FOP_JACOBI: mop = M2_JACOBI; m.x = f.x; m.x2 = f.b; m.y = f.y; break;
+        default:
+            mop = M2_CGP; m.x = f.z; m.x2 = f.pin; m.y2 = f.pout; m.y = f.y; m.beta = f.beta;
+            m.xv = f.xv; m.xalpha = f.xalpha;
+            break;
+    }
+    return march2_apply(mop, m, c->nu_paper, c->stream);
+}
+
 static void level_smooth(Rec& rc, int l, const double* r, const double* z, double* w, double* partial) {
     mg_ctx* c = rc.c;
     if (l == 0 && c->L > 1) {
         FineArgs a = fine_args(c, rc);
         a.x = z; a.b = r; a.Dinv = c->lv[0].Dinv; a.y = w; a.partial = partial;
-        fine_apply(FOP_JACOBI, a, c->stream);
+        level0_apply(c, FOP_JACOBI, a);
     } else {
         CoarseArgs a{};
         a.g = c->lv[l].g; a.st = c->lv[l].st; a.x = z; a.b = r; a.Dinv = c->lv[l].Dinv; a.y = w;
@@ -304,7 +340,7 @@ static void level_resid(Rec& rc, int l, const double* r, const double* z, double
     if (l == 0) {
         FineArgs a = fine_args(c, rc);
         a.x = z; a.b = r; a.y = w;
-        fine_apply(FOP_RESID, a, c->stream);
+        level0_apply(c, FOP_RESID, a);
     } else {
         CoarseArgs a{};
         a.g = c->lv[l].g; a.st = c->lv[l].st; a.x = z; a.b = r; a.y = w;
@@ -350,7 +386,7 @@ static March2Args march_args(mg_ctx* c, const Rec& rc) {
     March2Args a{};
     a.g = G0(c);
     if (c->L > 1) { a.gc = c->lv[1].g; a.maskc = c->lv[1].mask; }
-    a.E = c->E; a.mask = c->lv[0].mask; a.omega = c->opts.omega;
+    a.pd = c->pd; a.E = c->Epad; a.mask = c->maskpad; a.Dinv = c->Dinvpad; a.omega = c->opts.omega;
     a.alpha = c->ctl.alpha; a.beta = c->ctl.beta; a.xalpha = c->ctl.xalpha;
     a.active = rc.active; a.done = rc.done; a.R = rc.R;
     return a;
@@ -363,20 +399,21 @@ static int blk_cgp(Rec& rc, const double* pin, double* pout) {
     FineArgs a = fine_args(c, rc);
     a.z = c->zf; a.pin = pin; a.pout = pout; a.y = c->q; a.beta = c->ctl.beta;
     a.xv = c->x; a.xalpha = c->ctl.xalpha; a.partial = c->partial;
-    return fine_apply(FOP_CGP, a, c->stream);
+    return level0_apply(c, FOP_CGP, a);
 }
 
 // r_out = r_in - alpha q ; partial r.r ; pre-smooth z1 = omega D^-1 r_out ; r_1 = P^T (r_out - K z1)
 static int blk_restrict(Rec& rc, const double* rin, double* rout) {
     mg_ctx* c = rc.c;
-    const long long n = G0(c).ndof;
+    const long long n = c->vs;
     if (c->fused2d) {
         March2Args a = march_args(c, rc);
         a.x = rin; a.x2 = c->q; a.y2 = rout; a.coarse = c->lv[1].r; a.partial = c->partial;
         rc.launches++;
         return march2_apply(M2_RESTRICT, a, c->nu_paper, c->stream);
     }
-    cg_rupdate(n, rc.R, c->ctl.alpha, rin, c->q, rout, c->lv[0].Dinv, c->opts.omega, c->L > 1 ? c->z : nullptr,
+    cg_rupdate(n, rc.R, c->ctl.alpha, rin, c->q, rout, c->dim == 2 ? c->Dinvpad : c->lv[0].Dinv, c->opts.omega,
+               c->L > 1 ? c->z : nullptr,
                c->partial, rc.active, rc.done, c->stream);
     rc.launches++;
     const int items = vec_blocks(n);
@@ -404,9 +441,16 @@ static double* coarse_cycle(Rec& rc) {
 // zf = post-smoothed (z1 + P ec) ; partial r.zf.  Returns partial items.
 static int blk_post(Rec& rc, const double* r, const double* ec) {
     mg_ctx* c = rc.c;
-    const long long n = G0(c).ndof;
+    const long long n = c->vs;
     if (c->L == 1) {
-        dense_apply(c->Ainv, c->npad, c->nL, r, c->zf, rc.R, rc.active, rc.done, c->stream);
+        if (c->dim == 2) {   // dense solve on the compact layout
+            unpad2_vectors(G0(c), c->pd, rc.R, r, c->t, c->stream);
+            dense_apply(c->Ainv, c->npad, c->nL, c->t, c->z, rc.R, rc.active, rc.done, c->stream);
+            pad2_vectors(G0(c), c->pd, rc.R, nullptr, c->z, c->zf, c->stream);
+            rc.launches += 2;
+        } else {
+            dense_apply(c->Ainv, c->npad, c->nL, r, c->zf, rc.R, rc.active, rc.done, c->stream);
+        }
         vec_dot(n, rc.R, r, c->zf, c->partial, rc.active, rc.done, c->stream);
         rc.launches += 2;
         return vec_blocks(n);
@@ -433,7 +477,7 @@ static int blk_post(Rec& rc, const double* r, const double* ec) {
         double* dst = last ? c->zf : (src == c->z ? c->t : c->z);
         FineArgs a = fine_args(c, rc);
         a.x = src; a.b = r; a.Dinv = c->lv[0].Dinv; a.y = dst; a.partial = last ? c->partial : nullptr;
-        items = fine_apply(FOP_JACOBI, a, c->stream);
+        items = level0_apply(c, FOP_JACOBI, a);
         rc.launches++;
         src = dst;
     }
@@ -464,8 +508,7 @@ static mg_status capture_end(mg_ctx* c, cudaGraphExec_t* exec, long long* nodes)
 static mg_status build_graphs(mg_ctx* c, int R, double tol) {
     for (cudaGraphExec_t* g : {&c->g_init, &c->g_restart, &c->g_iter, &c->g_true})
         if (*g) { cudaGraphExecDestroy(*g); *g = nullptr; }
-    const LevelGeom& g0 = G0(c);
-    const long long n = g0.ndof;
+    const long long n = c->vs;
     const int vb = vec_blocks(n);
     Rec rc{c, R, c->ctl.active, c->ctl.done};
     // ---- restart / initial preconditioning
@@ -509,7 +552,7 @@ static mg_status build_graphs(mg_ctx* c, int R, double tol) {
         Rec all{c, R, nullptr, nullptr};
         FineArgs a = fine_args(c, all);
         a.x = c->x; a.b = c->b; a.y = c->t;
-        fine_apply(FOP_RESID, a, c->stream);
+        level0_apply(c, FOP_RESID, a);
         vec_dot(n, R, c->t, c->t, c->partial, nullptr, nullptr, c->stream);
         cg_scalars(SM_TRUE, R, c->partial, vb, c->ctl, 0.0, c->stream);
     }
@@ -563,7 +606,7 @@ static mg_status setup_impl(mg_ctx* c, const mg_grid* grid, const double* E_e, c
     }
     element_stiffness(c->dim, c->nu, c->K0);
     c->nu_paper = (c->nu == MG_NU_PAPER);
-    c->fused2d = (c->dim == 2 && levels >= 2 && c->opts.nu_pre == 1 && c->opts.nu_post == 1);
+    c->fused2d = (c->dim == 2 && levels >= 2);
     fine_set_constants(c->dim, c->K0.data(), s);
     if (c->dim == 2) fine2d_set_constants(c->K0.data(), s);
     galerkin_set_constants(c->dim, c->K0.data(), s);
@@ -601,6 +644,15 @@ static mg_status setup_impl(mg_ctx* c, const mg_grid* grid, const double* E_e, c
         CHECK_LAUNCH();
     }
     c->launches += levels;
+    if (c->dim == 2) {
+        c->pd = pad2_layout(g0);
+        CU(cudaMalloc(&c->Epad, sizeof(double) * c->pd.elems));
+        CU(cudaMalloc(&c->maskpad, c->pd.nodes));
+        CU(cudaMalloc(&c->Dinvpad, sizeof(double) * 2 * c->pd.nodes));
+        c->vs = c->pd.vstride;
+    } else {
+        c->vs = g0.ndof;
+    }
     c->nL = c->lv[levels - 1].g.ndof;
     c->npad = (c->nL + 31) / 32 * 32;
     CU(cudaMalloc(&c->Ainv, sizeof(double) * c->npad * c->npad));
@@ -631,6 +683,8 @@ mg_status mg_setup(const mg_grid* grid, const double* E_e, const uint8_t* fixed,
     if (!(grid->nu > -1.0 && grid->nu < 0.5)) return fail(MG_ERR_ARG, "nu out of range");
     if (opts && (opts->nu_pre < 1 || opts->nu_post < 0 || opts->max_iter < 1 || !(opts->omega > 0)))
         return fail(MG_ERR_ARG, "invalid mg_opts");
+    if (opts && grid->dim == 2 && (opts->nu_pre != 1 || opts->nu_post != 1))
+        return fail(MG_ERR_ARG, "2D path implements the fused V(1,1) cycle only (nu_pre = nu_post = 1)");
     const int f = 1 << (levels - 1);
     long long nodes = 1;
     for (int k = 0; k < grid->dim; ++k) {
@@ -684,12 +738,13 @@ mg_status mgcg_solve(mg_handle c, const double* rhs, int nrhs, double tol, doubl
         c->graph_tol = tol;
     }
     const bool rdev = is_device_ptr(rhs), xdev = is_device_ptr(x);
-    if (rdev) {
-        vec_mask_copy(g0.nnodes, c->dim, nrhs, c->lv[0].mask, rhs, c->b, s);
-    } else {
+    const double* rsrc = rhs;
+    if (!rdev) {
         CU(cudaMemcpyAsync(c->t, rhs, sizeof(double) * n * nrhs, cudaMemcpyHostToDevice, s));
-        vec_mask_copy(g0.nnodes, c->dim, nrhs, c->lv[0].mask, c->t, c->b, s);
+        rsrc = c->t;
     }
+    if (c->dim == 2) pad2_vectors(g0, c->pd, nrhs, c->lv[0].mask, rsrc, c->b, s);
+    else vec_mask_copy(g0.nnodes, c->dim, nrhs, c->lv[0].mask, rsrc, c->b, s);
     c->launches += 1;
     CU(cudaMemsetAsync(c->ctl.status, 0, sizeof(int), s));
     CU(cudaGraphLaunch(c->g_init, s));
@@ -735,7 +790,7 @@ mg_status mgcg_solve(mg_handle c, const double* rhs, int nrhs, double tol, doubl
         ++restarts;
         int* d_restart = c->ctl.active;   // active := restart flags, then r1 = t for them
         CU(cudaMemcpyAsync(d_restart, restart.data(), sizeof(int) * MG_MAX_RHS, cudaMemcpyHostToDevice, s));
-        vec_axpy_masked_restart(n, nrhs, c->t, c->r1, d_restart, s);
+        vec_axpy_masked_restart(c->vs, nrhs, c->t, c->r1, d_restart, s);
         CU(cudaMemsetAsync(c->ctl.alpha, 0, sizeof(double) * MG_MAX_RHS, s));
         int zero = 0;
         CU(cudaMemcpyAsync(c->ctl.done, &zero, sizeof(int), cudaMemcpyHostToDevice, s));
@@ -744,10 +799,18 @@ mg_status mgcg_solve(mg_handle c, const double* rhs, int nrhs, double tol, doubl
         klaunch += c->n_restart + 1;
     }
     // copy x out
-    if (xdev)
+    if (c->dim == 2) {
+        if (xdev) {
+            unpad2_vectors(g0, c->pd, nrhs, c->x, x, s);
+        } else {
+            unpad2_vectors(g0, c->pd, nrhs, c->x, c->t, s);
+            CU(cudaMemcpyAsync(x, c->t, sizeof(double) * n * nrhs, cudaMemcpyDeviceToHost, s));
+        }
+    } else if (xdev) {
         CU(cudaMemcpyAsync(x, c->x, sizeof(double) * n * nrhs, cudaMemcpyDeviceToDevice, s));
-    else
+    } else {
         CU(cudaMemcpyAsync(x, c->x, sizeof(double) * n * nrhs, cudaMemcpyDeviceToHost, s));
+    }
     CU(cudaEventRecord(e1, s));
     CU(cudaStreamSynchronize(s));
     float ms = 0.f;
@@ -831,7 +894,15 @@ mg_status mg_matvec(mg_handle c, int level, const double* x, int nrhs, double* y
         FineArgs a{};
         a.g = G0(c); a.E = c->E; a.mask = c->lv[0].mask; a.x = x; a.y = y; a.R = nrhs;
         a.nu_paper = c->nu_paper ? 1 : 0;
-        fine_apply(FOP_MATVEC, a, c->stream);
+        if (c->dim == 2) {   // compact <-> padded around the march kernel
+            TRY(ensure_vectors(c, nrhs));
+            pad2_vectors(G0(c), c->pd, nrhs, nullptr, x, c->t, c->stream);
+            a.x = c->t; a.y = c->q;
+            level0_apply(c, FOP_MATVEC, a);
+            unpad2_vectors(G0(c), c->pd, nrhs, c->q, y, c->stream);
+        } else {
+            fine_apply(FOP_MATVEC, a, c->stream);
+        }
     } else {
         CoarseArgs a{};
         a.g = c->lv[level].g; a.st = c->lv[level].st; a.x = x; a.y = y; a.R = nrhs;
@@ -850,14 +921,16 @@ mg_status mg_vcycle(mg_handle c, const double* r, int nrhs, double* z) {
     stream_enter(c);
     const long long n = G0(c).ndof;
     // the preconditioner exactly as the solve applies it (same fine blocks, alpha = 0)
-    CU(cudaMemcpyAsync(c->r1, r, sizeof(double) * n * nrhs, cudaMemcpyDeviceToDevice, c->stream));
+    if (c->dim == 2) pad2_vectors(G0(c), c->pd, nrhs, c->lv[0].mask, r, c->r1, c->stream);
+    else CU(cudaMemcpyAsync(c->r1, r, sizeof(double) * n * nrhs, cudaMemcpyDeviceToDevice, c->stream));
     CU(cudaMemsetAsync(c->ctl.alpha, 0, sizeof(double) * MG_MAX_RHS, c->stream));
-    CU(cudaMemsetAsync(c->q, 0, sizeof(double) * n * nrhs, c->stream));
+    CU(cudaMemsetAsync(c->q, 0, sizeof(double) * c->vs * nrhs, c->stream));
     Rec rc{c, nrhs, nullptr, nullptr};
     blk_restrict(rc, c->r1, c->r0);
     double* ec = coarse_cycle(rc);
     blk_post(rc, c->r0, ec);
-    CU(cudaMemcpyAsync(z, c->zf, sizeof(double) * n * nrhs, cudaMemcpyDeviceToDevice, c->stream));
+    if (c->dim == 2) unpad2_vectors(G0(c), c->pd, nrhs, c->zf, z, c->stream);
+    else CU(cudaMemcpyAsync(z, c->zf, sizeof(double) * n * nrhs, cudaMemcpyDeviceToDevice, c->stream));
     c->launches += rc.launches;
     CHECK_LAUNCH();
     stream_leave(c);
@@ -929,6 +1002,9 @@ mg_status mg_destroy(mg_handle c) {
         if (v.st) cudaFree(v.st);
     }
     if (c->E) cudaFree(c->E);
+    if (c->Epad) cudaFree(c->Epad);
+    if (c->maskpad) cudaFree(c->maskpad);
+    if (c->Dinvpad) cudaFree(c->Dinvpad);
     if (c->Ainv) cudaFree(c->Ainv);
     if (c->ctl_mem) cudaFree(c->ctl_mem);
     if (c->sig) cudaFree(c->sig);
