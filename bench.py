@@ -187,29 +187,24 @@ def run_ours(args, cfg):
     ms_step = ms_total / args.steps
     value = total_dofiters / (ms_total / 1e3)
 
-    # ---- dominant kernel (fine EbE operator) timed alone with CUDA events on the launch stream
+    # ---- fine-level kernels of one CG iteration, timed standalone (same kernels and launch
+    # configuration as in the solve graph) with CUDA events on the handle's stream.
     hbm, peak_kind = peaks()
-    xr = torch.randn((R, n), dtype=torch.float64, device=dev)
-    yr = torch.empty_like(xr)
-    for _ in range(3):
-        mg.mg_matvec(h, 0, xr, yr)
-    nrep = 20
-    flush = torch.empty(int(256e6) // 8, dtype=torch.float64, device=dev)
-    kt = []
-    for _ in range(nrep):
-        flush.fill_(1.0)   # evict L2 (inputs are larger than L2 anyway)
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        mg.mg_matvec(h, 0, xr, yr)
-        b.record(stream)
-        b.synchronize()
-        kt.append(a.elapsed_time(b))
-    kms = float(np.median(kt))
+    kms = mg.mg_profile_kernels(h, R, reps=10)
     m = int(np.prod(cfg.nel))
-    alg_bytes = 8.0 * (2.0 * n * R + m)
-    achieved = alg_bytes / (kms / 1e3) / 1e9
-    del flush
+    nR = float(n) * R
+    coarse = 1.0 / (2 ** cfg.dim)
+    # algorithmic bytes per launch (what each kernel must move)
+    alg = {
+        "cgp": 8.0 * (6 * nR + m),                                   # z, p_in, x in; p_out, q, x out; E
+        "restrict": 8.0 * ((3 + coarse) * nR + m + n),               # r_in, q in; r_out, r_c out; E, D^-1
+        "post": 8.0 * ((2 + coarse) * nR + m + n),                   # r, e_c in; z out; E, D^-1
+        "matvec": 8.0 * (2 * nR + m),                                # x in, y out, E
+    }
+    kernels = {k: {"ms": kms[k], "alg_bytes": alg[k], "gbs": alg[k] / (kms[k] / 1e3) / 1e9,
+                   "frac": alg[k] / (kms[k] / 1e3) / 1e9 / hbm} for k in alg}
+    dom = "cgp"
+    achieved = kernels[dom]["gbs"]
 
     # ---- e2e: same step through the C ABI with pinned HOST buffers (H2D/D2H inside the timed region)
     e2e = None
@@ -257,10 +252,11 @@ def run_ours(args, cfg):
         "iters": reps[-1]["iters"], "true_relres_max": max(reps[-1]["true_relres"]),
         "first_setup_s": setup_first_s,
         "gpu_launches": int(launches),
-        "roofline": {"kernel": "fine_ebe_matvec (fine2d/3d_kernel)", "bound": "hbm", "achieved": achieved,
-                     "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": traffic_from_profiles(cfg.name), "alg_bytes_per_launch": alg_bytes,
-                     "kernel_ms": kms},
+        "roofline": {"kernel": "CG direction + fine EbE matvec (march2_kernel<M2_CGP> 2D / fine3d_kernel<FOP_CGP> 3D)",
+                     "bound": "hbm", "achieved": achieved, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": traffic_from_profiles(cfg.name),
+                     "alg_bytes_per_launch": alg[dom], "kernel_ms": kms[dom]},
+        "kernels": kernels,
         "clocks": clocks,
         "e2e": e2e,
     }

@@ -149,6 +149,12 @@ mg_status mg_level_info(mg_handle h, int level, int* nel3, long long* ndof, int*
 mg_status mg_get_diagonal(mg_handle h, int level, double* d);
 /* Dense inverse of the coarsest operator (ndof_L x ndof_L, row-major, device). */
 mg_status mg_get_coarse_inverse(mg_handle h, double* Ainv);
+/* Time the fine-level kernels of one CG iteration standalone (same kernels and launch
+ * configuration as inside the solve graph) on nrhs internal vectors, reps launches each,
+ * with CUDA events on the handle's stream.  ms[0..3] = average ms per launch of:
+ * CG direction + matvec (a2/a7), residual + restriction block (a3/a4), prolongation +
+ * post-smoothing block (a3/a4), plain matvec K x (a2).  Synchronous. */
+mg_status mg_profile_kernels(mg_handle h, int nrhs, int reps, double* ms);
 /* Number of CUDA kernels this handle has launched (graph nodes counted once per launch). */
 long long mg_kernel_launches(mg_handle h);
 

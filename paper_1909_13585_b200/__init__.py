@@ -18,7 +18,7 @@ from ._lib import MgError, MgGrid, MgOpts, MgReport, check, lib
 __all__ = [
     "Handle", "MgError", "mg_setup", "mg_update_modulus", "mgcg_solve", "stress_stiffness_apply",
     "mg_matvec", "mg_vcycle", "mg_restrict", "mg_prolong", "mg_level_info", "mg_get_diagonal",
-    "mg_get_coarse_inverse", "mg_kernel_launches", "mg_destroy", "lib_path",
+    "mg_get_coarse_inverse", "mg_kernel_launches", "mg_profile_kernels", "mg_destroy", "lib_path",
 ]
 
 lib_path = _lib.LIB_PATH
@@ -144,6 +144,13 @@ def mg_get_coarse_inverse(h, A):
 
 def mg_kernel_launches(h):
     return int(lib.mg_kernel_launches(h.raw))
+
+
+def mg_profile_kernels(h, nrhs, reps=10):
+    """Standalone timings (ms per launch) of the fine-level kernels of one CG iteration."""
+    ms = (ctypes.c_double * 4)()
+    check(lib.mg_profile_kernels(h.raw, nrhs, reps, ms))
+    return dict(cgp=ms[0], restrict=ms[1], post=ms[2], matvec=ms[3])
 
 
 def mg_destroy(h):

@@ -22,7 +22,7 @@ STATUS = {
 EXPORTED = [
     "mg_setup", "mg_update_modulus", "mgcg_solve", "stress_stiffness_apply", "mg_matvec", "mg_vcycle",
     "mg_restrict", "mg_prolong", "mg_level_info", "mg_get_diagonal", "mg_get_coarse_inverse",
-    "mg_kernel_launches", "mg_destroy", "mg_strerror", "mg_last_error",
+    "mg_kernel_launches", "mg_profile_kernels", "mg_destroy", "mg_strerror", "mg_last_error",
 ]
 
 
@@ -75,6 +75,7 @@ def _load():
         "mg_get_diagonal": ([P, I, P], I),
         "mg_get_coarse_inverse": ([P, P], I),
         "mg_kernel_launches": ([P], LL),
+        "mg_profile_kernels": ([P, I, I, ctypes.POINTER(ctypes.c_double)], I),
         "mg_destroy": ([P], I),
         "mg_strerror": ([I], ctypes.c_char_p),
         "mg_last_error": ([], ctypes.c_char_p),

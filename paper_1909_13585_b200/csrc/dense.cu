@@ -146,33 +146,31 @@ __global__ void __launch_bounds__(256) gj_update_kernel(double* A, long long ld,
     }
 }
 
-// Overwrite the pivot row/column panels: A[k][j] = Rrow, A[i][k] = -Ccol[i] P, A[k][k] = P.
-__global__ void gj_fix_kernel(double* A, long long ld, long long n, int k0, const double* P, const double* Rrow,
-                              const double* Ccol) {
+// Overwrite the pivot column panel: A[i][k] = -Ccol[i] P for rows i outside the pivot block.
+__global__ void gj_fix_cols_kernel(double* A, long long ld, long long n, int k0, const double* P, const double* Ccol) {
     __shared__ double Ps[GJ_NB][GJ_NB];
     for (int e = threadIdx.x; e < GJ_NB * GJ_NB; e += blockDim.x) Ps[e / GJ_NB][e % GJ_NB] = P[e];
     __syncthreads();
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const bool inblk = (i >= k0 && i < k0 + GJ_NB);
-    if (inblk) {
-        int t = (int)(i - k0);
-        for (long long j = 0; j < n; ++j) {
-            if (j >= k0 && j < k0 + GJ_NB) A[i * ld + j] = Ps[t][j - k0];
-            else A[i * ld + j] = Rrow[t * n + j];
-        }
-    } else {
-        double c[GJ_NB];
+    if (i >= n || (i >= k0 && i < k0 + GJ_NB)) return;
+    double c[GJ_NB];
 #pragma unroll
-        for (int s = 0; s < GJ_NB; ++s) c[s] = Ccol[i * GJ_NB + s];
+    for (int s = 0; s < GJ_NB; ++s) c[s] = Ccol[i * GJ_NB + s];
 #pragma unroll 4
-        for (int t = 0; t < GJ_NB; ++t) {
-            double acc = 0.0;
+    for (int t = 0; t < GJ_NB; ++t) {
+        double acc = 0.0;
 #pragma unroll
-            for (int s = 0; s < GJ_NB; ++s) acc = fma(c[s], Ps[s][t], acc);
-            A[i * ld + k0 + t] = -acc;
-        }
+        for (int s = 0; s < GJ_NB; ++s) acc = fma(c[s], Ps[s][t], acc);
+        A[i * ld + k0 + t] = -acc;
     }
+}
+
+// Overwrite the pivot row panel: A[k][j] = Rrow (j outside the block), A[k][k] = P.
+__global__ void gj_fix_rows_kernel(double* A, long long ld, long long n, int k0, const double* P, const double* Rrow) {
+    const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = blockIdx.y;
+    if (j >= n) return;
+    A[(k0 + t) * ld + j] = (j >= k0 && j < k0 + GJ_NB) ? P[t * GJ_NB + (j - k0)] : Rrow[t * n + j];
 }
 
 void dense_spd_inverse(double* A, long long npad, double* work, int* d_status, cudaStream_t s) {
@@ -185,7 +183,8 @@ void dense_spd_inverse(double* A, long long npad, double* work, int* d_status, c
         gj_panels_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(A, n, n, (int)k0, P, Rrow, Ccol);
         dim3 g((unsigned)((n + 63) / 64), (unsigned)((n + 63) / 64));
         gj_update_kernel<<<g, 256, 0, s>>>(A, n, n, Ccol, Rrow);
-        gj_fix_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(A, n, n, (int)k0, P, Rrow, Ccol);
+        gj_fix_cols_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(A, n, n, (int)k0, P, Ccol);
+        gj_fix_rows_kernel<<<dim3((unsigned)((n + 255) / 256), GJ_NB), 256, 0, s>>>(A, n, n, (int)k0, P, Rrow);
     }
 }
 

@@ -117,6 +117,7 @@ struct mg_ctx {
     double *b = nullptr, *x = nullptr, *r0 = nullptr, *r1 = nullptr, *p0 = nullptr, *p1 = nullptr, *q = nullptr,
            *zf = nullptr, *z = nullptr, *t = nullptr;
     double* zpre = nullptr;   // generic path: buffer holding the pre-smoothed z after blk_restrict
+    double *stage = nullptr, *stage2 = nullptr;   // compact (R x ndof) staging: host copies, 2D L == 1 solve
     double* partial = nullptr;
     long long partial_cap = 0;
     // CG control block
@@ -227,7 +228,7 @@ static mg_status compute_operators(mg_ctx* c) {
     CU(cudaMallocAsync(&work, sizeof(double) * (32 * 32 + 2 * c->npad * 32), s));
     CU(cudaMemsetAsync(c->d_status, 0, sizeof(int), s));
     dense_spd_inverse(c->Ainv, c->npad, work, c->d_status, s);
-    c->launches += 2 + 4 * (c->npad / 32);
+    c->launches += 2 + 5 * (c->npad / 32);
     CHECK_LAUNCH();
     CU(cudaFreeAsync(work, s));
     int st = 0;
@@ -238,7 +239,8 @@ static mg_status compute_operators(mg_ctx* c) {
 }
 
 static void free_vectors(mg_ctx* c) {
-    double** fv[] = {&c->b, &c->x, &c->r0, &c->r1, &c->p0, &c->p1, &c->q, &c->zf, &c->z, &c->t, &c->partial};
+    double** fv[] = {&c->b, &c->x, &c->r0, &c->r1, &c->p0, &c->p1, &c->q, &c->zf, &c->z, &c->t, &c->partial,
+                     &c->stage, &c->stage2};
     for (auto p : fv)
         if (*p) { cudaFree(*p); *p = nullptr; }
     for (int l = 1; l < c->L; ++l) {
@@ -263,6 +265,8 @@ static mg_status ensure_vectors(mg_ctx* c, int R) {
         CU(cudaMalloc(p, sizeof(double) * n * R));
         CU(cudaMemset(*p, 0, sizeof(double) * n * R));   // ghost entries of the padded layout stay 0
     }
+    CU(cudaMalloc(&c->stage, sizeof(double) * G0(c).ndof * R));
+    CU(cudaMalloc(&c->stage2, sizeof(double) * G0(c).ndof * R));
     for (int l = 1; l < c->L; ++l) {
         long long nl = c->lv[l].g.ndof;
         CU(cudaMalloc(&c->lv[l].r, sizeof(double) * nl * R));
@@ -444,9 +448,9 @@ static int blk_post(Rec& rc, const double* r, const double* ec) {
     const long long n = c->vs;
     if (c->L == 1) {
         if (c->dim == 2) {   // dense solve on the compact layout
-            unpad2_vectors(G0(c), c->pd, rc.R, r, c->t, c->stream);
-            dense_apply(c->Ainv, c->npad, c->nL, c->t, c->z, rc.R, rc.active, rc.done, c->stream);
-            pad2_vectors(G0(c), c->pd, rc.R, nullptr, c->z, c->zf, c->stream);
+            unpad2_vectors(G0(c), c->pd, rc.R, r, c->stage, c->stream);
+            dense_apply(c->Ainv, c->npad, c->nL, c->stage, c->stage2, rc.R, rc.active, rc.done, c->stream);
+            pad2_vectors(G0(c), c->pd, rc.R, nullptr, c->stage2, c->zf, c->stream);
             rc.launches += 2;
         } else {
             dense_apply(c->Ainv, c->npad, c->nL, r, c->zf, rc.R, rc.active, rc.done, c->stream);
@@ -740,8 +744,8 @@ mg_status mgcg_solve(mg_handle c, const double* rhs, int nrhs, double tol, doubl
     const bool rdev = is_device_ptr(rhs), xdev = is_device_ptr(x);
     const double* rsrc = rhs;
     if (!rdev) {
-        CU(cudaMemcpyAsync(c->t, rhs, sizeof(double) * n * nrhs, cudaMemcpyHostToDevice, s));
-        rsrc = c->t;
+        CU(cudaMemcpyAsync(c->stage, rhs, sizeof(double) * n * nrhs, cudaMemcpyHostToDevice, s));
+        rsrc = c->stage;
     }
     if (c->dim == 2) pad2_vectors(g0, c->pd, nrhs, c->lv[0].mask, rsrc, c->b, s);
     else vec_mask_copy(g0.nnodes, c->dim, nrhs, c->lv[0].mask, rsrc, c->b, s);
@@ -803,8 +807,8 @@ mg_status mgcg_solve(mg_handle c, const double* rhs, int nrhs, double tol, doubl
         if (xdev) {
             unpad2_vectors(g0, c->pd, nrhs, c->x, x, s);
         } else {
-            unpad2_vectors(g0, c->pd, nrhs, c->x, c->t, s);
-            CU(cudaMemcpyAsync(x, c->t, sizeof(double) * n * nrhs, cudaMemcpyDeviceToHost, s));
+            unpad2_vectors(g0, c->pd, nrhs, c->x, c->stage, s);
+            CU(cudaMemcpyAsync(x, c->stage, sizeof(double) * n * nrhs, cudaMemcpyDeviceToHost, s));
         }
     } else if (xdev) {
         CU(cudaMemcpyAsync(x, c->x, sizeof(double) * n * nrhs, cudaMemcpyDeviceToDevice, s));
@@ -986,6 +990,45 @@ mg_status mg_get_coarse_inverse(mg_handle c, double* Ainv) {
     stream_enter(c);
     CU(cudaMemcpy2DAsync(Ainv, sizeof(double) * c->nL, c->Ainv, sizeof(double) * c->npad, sizeof(double) * c->nL,
                          c->nL, cudaMemcpyDeviceToDevice, c->stream));
+    stream_leave(c);
+    return MG_OK;
+}
+
+mg_status mg_profile_kernels(mg_handle c, int nrhs, int reps, double* ms) {
+    if (!c || !ms) return fail(MG_ERR_ARG, "NULL argument");
+    if (nrhs < 1 || nrhs > MG_MAX_RHS || reps < 1) return fail(MG_ERR_ARG, "bad nrhs / reps");
+    TRY(ensure_vectors(c, nrhs));
+    stream_enter(c);
+    cudaStream_t s = c->stream;
+    Rec rc{c, nrhs, nullptr, nullptr};
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreate(&e0));
+    CU(cudaEventCreate(&e1));
+    for (int op = 0; op < 4; ++op) {
+        auto launch = [&]() {
+            switch (op) {
+                case 0: blk_cgp(rc, c->p0, c->p1); break;
+                case 1: blk_restrict(rc, c->r0, c->r1); break;
+                case 2: blk_post(rc, c->r1, c->L > 1 ? c->lv[1].z : nullptr); break;
+                default: {
+                    FineArgs a = fine_args(c, rc);
+                    a.x = c->p0; a.y = c->q;
+                    level0_apply(c, FOP_MATVEC, a);
+                }
+            }
+        };
+        launch();
+        CU(cudaEventRecord(e0, s));
+        for (int k = 0; k < reps; ++k) launch();
+        CU(cudaEventRecord(e1, s));
+        CU(cudaEventSynchronize(e1));
+        float t = 0.f;
+        cudaEventElapsedTime(&t, e0, e1);
+        ms[op] = t / reps;
+    }
+    CHECK_LAUNCH();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
     stream_leave(c);
     return MG_OK;
 }

@@ -201,10 +201,11 @@ def test_zero_and_duplicate_rhs():
     assert torch.equal(x[1], x[2])
 
 
-def test_host_buffers_match_device():
+@pytest.mark.parametrize("name", ["T3a", "T2b"])
+def test_host_buffers_match_device(name):
     import paper_1909_13585_b200 as mg
-    cfg, inp, K = case("T3a")
-    h = handle("T3a")
+    cfg, inp, K = case(name)
+    h = handle(name)
     xd = torch.empty((cfg.nrhs, K.shape[0]), dtype=torch.float64, device=DEV)
     mg.mgcg_solve(h, to_dev(inp["rhs"]), 1e-10, xd)
     xh = np.empty((cfg.nrhs, K.shape[0]))
@@ -242,4 +243,19 @@ def test_update_modulus_equals_fresh_setup():
     x2 = torch.empty_like(rhs)
     mg.mgcg_solve(h, rhs, 1e-10, x1)
     mg.mgcg_solve(h2, rhs, 1e-10, x2)
+    assert torch.equal(x1, x2)
+
+
+@pytest.mark.parametrize("name", ["T2c", "T3a"])
+def test_profile_kernels_leaves_solver_state_valid(name):
+    import paper_1909_13585_b200 as mg
+    cfg, inp, K = case(name)
+    h = handle(name)
+    rhs = to_dev(inp["rhs"])
+    x1 = torch.empty_like(rhs)
+    mg.mgcg_solve(h, rhs, 1e-10, x1)
+    ms = mg.mg_profile_kernels(h, cfg.nrhs, reps=2)
+    assert all(v > 0 for v in ms.values())
+    x2 = torch.empty_like(rhs)
+    mg.mgcg_solve(h, rhs, 1e-10, x2)
     assert torch.equal(x1, x2)
