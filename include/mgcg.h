@@ -111,6 +111,38 @@ typedef struct mg_ctx* mg_handle;
 mg_status mg_setup(const mg_grid* grid, const double* E_e, const uint8_t* fixed,
                    int levels, const mg_opts* opts, void* stream, mg_handle* out);
 
+/* Slab decomposition along axis 0 (BASELINE.json:5 "partitioned into slabs
+ * across 1/2/4/8 GPUs ... NCCL halo exchange ... allreduce for CG dot products").
+ * The global grid is cut at coarsest-level element boundaries into S = nranks * nslab slabs
+ * (mg_partition gives slab k's owned element layers [e_begin, e_end)); rank r (one process
+ * per GPU) holds slabs [r*nslab, (r+1)*nslab).  nslab > 1 keeps several slabs in one handle
+ * (exchanges by device copies; used to test the decomposition on one GPU).
+ *   rank, nranks  this process and the job size (nranks > 1 needs nccl_id)
+ *   nslab         slabs held by this rank (>= 1)
+ *   nccl_id       NCCL_UNIQUE_ID_BYTES (128) bytes from mg_nccl_unique_id on rank 0,
+ *                 broadcast by the caller; NULL when nranks == 1.
+ * With a dist, every array argument of every call covers THIS RANK's owned part only:
+ * element arrays its element layers [e_begin, e_end) (mg_local_info), vectors and `fixed`
+ * its node planes [e_begin, e_end) plus plane N0 on the last rank, same C order. */
+typedef struct {
+    int rank;
+    int nranks;
+    int nslab;
+    const void* nccl_id;
+} mg_dist;
+
+/* mg_setup with a decomposition (dist NULL = one slab = mg_setup).  Requires levels >= 2
+ * and S <= N0 / 2^(levels-1).  Collective over the nranks processes. */
+mg_status mg_setup_dist(const mg_grid* grid, const double* E_e, const uint8_t* fixed, int levels,
+                        const mg_opts* opts, const mg_dist* dist, void* stream, mg_handle* out);
+/* Host-only: owned element layers [e_begin, e_end) along axis 0 of slab `part` of `nparts`
+ * (coarsest-level layers split as evenly as possible). No device work. */
+mg_status mg_partition(const mg_grid* grid, int levels, int nparts, int part, int* e_begin, int* e_end);
+/* Host: 128-byte NCCL unique id for mg_dist.nccl_id (loads libnccl.so.2 with dlopen). */
+mg_status mg_nccl_unique_id(void* out128);
+/* This rank's owned DOF / element counts and its element-layer range. */
+mg_status mg_local_info(mg_handle h, long long* ndof_local, long long* nelem_local, int* e_begin, int* e_end);
+
 /* Same grid and BCs, new design: recompute all level operators from E_e. */
 mg_status mg_update_modulus(mg_handle h, const double* E_e);
 

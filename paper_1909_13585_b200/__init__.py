@@ -13,10 +13,11 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from ._lib import MgError, MgGrid, MgOpts, MgReport, check, lib
+from ._lib import MgDist, MgError, MgGrid, MgOpts, MgReport, check, lib
 
 __all__ = [
-    "Handle", "MgError", "mg_setup", "mg_update_modulus", "mgcg_solve", "stress_stiffness_apply",
+    "Handle", "MgError", "mg_setup", "mg_setup_dist", "mg_partition", "mg_nccl_unique_id", "mg_local_info",
+    "mg_update_modulus", "mgcg_solve", "stress_stiffness_apply",
     "mg_matvec", "mg_vcycle", "mg_restrict", "mg_prolong", "mg_level_info", "mg_get_diagonal",
     "mg_get_coarse_inverse", "mg_kernel_launches", "mg_profile_kernels", "mg_destroy", "lib_path",
 ]
@@ -79,6 +80,53 @@ def mg_setup(nel, E, fixed, levels, nu=0.3, omega=0.6, nu_pre=1, nu_post=1, max_
     check(lib.mg_setup(ctypes.byref(g), _ptr(E, np.float64), _ptr(fixed, np.uint8), levels, ctypes.byref(o), sp,
                        ctypes.byref(raw)))
     return Handle(raw, dim, nel, levels, sp)
+
+
+def _grid(nel, nu=0.3):
+    dim = len(nel)
+    return MgGrid(dim, (ctypes.c_int * 3)(*(list(nel) + [0] * (3 - dim))), nu)
+
+
+def mg_partition(nel, levels, nparts, part):
+    """Owned element layers [e_begin, e_end) along axis 0 of slab `part` (host only)."""
+    a, b = ctypes.c_int(), ctypes.c_int()
+    check(lib.mg_partition(ctypes.byref(_grid(nel)), levels, nparts, part, ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
+
+
+def mg_nccl_unique_id():
+    """128-byte NCCL unique id (bytes) for mg_setup_dist on nranks > 1."""
+    buf = ctypes.create_string_buffer(128)
+    check(lib.mg_nccl_unique_id(buf))
+    return buf.raw
+
+
+def mg_setup_dist(nel, E, fixed, levels, rank=0, nranks=1, nslab=1, nccl_id=None, nu=0.3, omega=0.6, nu_pre=1,
+                  nu_post=1, max_iter=1000, stream=None):
+    """Slab-decomposed setup: E / fixed (and all later vectors) cover this rank's owned part
+    (mg_local_info); nslab slabs are kept in this handle."""
+    dim = len(nel)
+    g = _grid(nel, nu)
+    o = MgOpts(omega, nu_pre, nu_post, max_iter)
+    idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+    d = MgDist(rank, nranks, nslab, ctypes.cast(idbuf, ctypes.c_void_p) if idbuf is not None else None)
+    raw = ctypes.c_void_p()
+    sp = _stream_ptr(stream)
+    check(lib.mg_setup_dist(ctypes.byref(g), _ptr(E, np.float64), _ptr(fixed, np.uint8), levels, ctypes.byref(o),
+                            ctypes.byref(d), sp, ctypes.byref(raw)))
+    h = Handle(raw, dim, nel, levels, sp)
+    info = mg_local_info(h)
+    h.ndof = info["ndof"]
+    h.nelem = info["nelem"]
+    h.e_range = (info["e_begin"], info["e_end"])
+    return h
+
+
+def mg_local_info(h):
+    nd, ne = ctypes.c_longlong(), ctypes.c_longlong()
+    a, b = ctypes.c_int(), ctypes.c_int()
+    check(lib.mg_local_info(h.raw, ctypes.byref(nd), ctypes.byref(ne), ctypes.byref(a), ctypes.byref(b)))
+    return dict(ndof=nd.value, nelem=ne.value, e_begin=a.value, e_end=b.value)
 
 
 def mg_update_modulus(h, E):

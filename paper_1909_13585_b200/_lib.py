@@ -20,7 +20,7 @@ STATUS = {
 }
 
 EXPORTED = [
-    "mg_setup", "mg_update_modulus", "mgcg_solve", "stress_stiffness_apply", "mg_matvec", "mg_vcycle",
+    "mg_setup", "mg_setup_dist", "mg_partition", "mg_nccl_unique_id", "mg_local_info", "mg_update_modulus", "mgcg_solve", "stress_stiffness_apply", "mg_matvec", "mg_vcycle",
     "mg_restrict", "mg_prolong", "mg_level_info", "mg_get_diagonal", "mg_get_coarse_inverse",
     "mg_kernel_launches", "mg_profile_kernels", "mg_destroy", "mg_strerror", "mg_last_error",
 ]
@@ -33,6 +33,11 @@ class MgGrid(ctypes.Structure):
 class MgOpts(ctypes.Structure):
     _fields_ = [("omega", ctypes.c_double), ("nu_pre", ctypes.c_int), ("nu_post", ctypes.c_int),
                 ("max_iter", ctypes.c_int)]
+
+
+class MgDist(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("nslab", ctypes.c_int),
+                ("nccl_id", ctypes.c_void_p)]
 
 
 class MgReport(ctypes.Structure):
@@ -57,13 +62,35 @@ class MgError(RuntimeError):
         super().__init__(f"{self.name}: {msg}")
 
 
+def _nccl_path():
+    """libnccl.so.2 shipped with torch (nvidia-nccl wheel); the library dlopens it for nranks > 1."""
+    try:
+        import nvidia.nccl
+        for d in nvidia.nccl.__path__:
+            p = os.path.join(d, "lib", "libnccl.so.2")
+            if os.path.exists(p):
+                return p
+    except Exception:
+        pass
+    return None
+
+
 def _load():
+    if "MG_NCCL_LIB" not in os.environ:
+        p = _nccl_path()
+        if p:
+            os.environ["MG_NCCL_LIB"] = p
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"libmgcg.so not built ({LIB_PATH}); run __graft_entry__.build() -- no CPU fallback exists")
     lib = ctypes.CDLL(LIB_PATH)
     P, I, D, LL = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_longlong
     sig = {
         "mg_setup": ([ctypes.POINTER(MgGrid), P, P, I, ctypes.POINTER(MgOpts), P, ctypes.POINTER(P)], I),
+        "mg_setup_dist": ([ctypes.POINTER(MgGrid), P, P, I, ctypes.POINTER(MgOpts), ctypes.POINTER(MgDist), P,
+                           ctypes.POINTER(P)], I),
+        "mg_partition": ([ctypes.POINTER(MgGrid), I, I, I, ctypes.POINTER(I), ctypes.POINTER(I)], I),
+        "mg_nccl_unique_id": ([P], I),
+        "mg_local_info": ([P, ctypes.POINTER(LL), ctypes.POINTER(LL), ctypes.POINTER(I), ctypes.POINTER(I)], I),
         "mg_update_modulus": ([P, P], I),
         "mgcg_solve": ([P, P, I, D, P, ctypes.POINTER(MgReport)], I),
         "stress_stiffness_apply": ([P, P, P, P, I, P], I),

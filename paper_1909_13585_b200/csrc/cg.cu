@@ -47,78 +47,33 @@ void cg_pointwise_jacobi(long long n, int R, const double* r, const double* Dinv
     jacobi0_kernel<<<g, VEC_THREADS, 0, s>>>(n, r, Dinv, omega, z, active, done);
 }
 
-// x += alpha p; r -= alpha q; partial r.r; z = omega Dinv r
-__global__ void __launch_bounds__(VEC_THREADS) cg_update_kernel(long long n, const double* __restrict__ alpha,
-                                                                const double* __restrict__ p,
-                                                                const double* __restrict__ q, double* __restrict__ x,
-                                                                double* __restrict__ r, const double* __restrict__ Dinv,
-                                                                double omega, double* __restrict__ z, double* partial,
-                                                                const int* active, const int* done) {
-    const int rr = blockIdx.y;
-    if (done && *done) return;
-    if (active && !active[rr]) return;
-    const double al = alpha[rr];
-    const long long o = (long long)rr * n;
-    double acc = 0.0;
-    const long long n2 = n >> 1;   // n is even (d*nodes with d in {2,3} -> handle odd tail)
-    const double2* p2 = reinterpret_cast<const double2*>(p + o);
-    const double2* q2 = reinterpret_cast<const double2*>(q + o);
-    double2* x2 = reinterpret_cast<double2*>(x + o);
-    double2* r2 = reinterpret_cast<double2*>(r + o);
-    double2* z2 = reinterpret_cast<double2*>(z + o);
-    const double2* d2 = reinterpret_cast<const double2*>(Dinv);
-    const bool aligned = ((o & 1) == 0);
-    if (aligned) {
-        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += (long long)gridDim.x * blockDim.x) {
-            double2 pv = p2[i], qv = q2[i], xv = x2[i], rv = r2[i], dv = d2[i];
-            xv.x = fma(al, pv.x, xv.x); xv.y = fma(al, pv.y, xv.y);
-            rv.x = fma(-al, qv.x, rv.x); rv.y = fma(-al, qv.y, rv.y);
-            x2[i] = xv; r2[i] = rv;
-            acc = fma(rv.x, rv.x, acc); acc = fma(rv.y, rv.y, acc);
-            z2[i] = make_double2(omega * dv.x * rv.x, omega * dv.y * rv.y);
-        }
-        if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
-            long long i = n - 1;
-            x[o + i] = fma(al, p[o + i], x[o + i]);
-            double rv = fma(-al, q[o + i], r[o + i]);
-            r[o + i] = rv; acc = fma(rv, rv, acc);
-            z[o + i] = omega * Dinv[i] * rv;
-        }
-    } else {
-        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-            x[o + i] = fma(al, p[o + i], x[o + i]);
-            double rv = fma(-al, q[o + i], r[o + i]);
-            r[o + i] = rv; acc = fma(rv, rv, acc);
-            z[o + i] = omega * Dinv[i] * rv;
-        }
-    }
-    block_partial(acc, partial, (long long)rr * gridDim.x + blockIdx.x);
-}
-
-void cg_update(long long n, int R, const double* alpha, const double* p, const double* q, double* x, double* r,
-               const double* Dinv, double omega, double* z, double* partial, const int* active, const int* done,
-               cudaStream_t s) {
-    dim3 g(vec_blocks(n), R);
-    cg_update_kernel<<<g, VEC_THREADS, 0, s>>>(n, alpha, p, q, x, r, Dinv, omega, z, partial, active, done);
-}
-
-__global__ void __launch_bounds__(VEC_THREADS) dot_kernel(long long n, const double* __restrict__ a,
+// partial[rr * pstride + block] = sum over i in [d0, d1) of a[rr][i] b[rr][i]  (vectors of stride n)
+__global__ void __launch_bounds__(VEC_THREADS) dot_kernel(long long n, long long d0, long long d1,
+                                                          const double* __restrict__ a,
                                                           const double* __restrict__ b, double* partial,
-                                                          const int* active, const int* done) {
+                                                          long long pstride, const int* active, const int* done) {
     const int rr = blockIdx.y;
     if (done && *done) return;
     if (active && !active[rr]) return;
     const long long o = (long long)rr * n;
     double acc = 0.0;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    for (long long i = d0 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < d1;
+         i += (long long)gridDim.x * blockDim.x)
         acc = fma(a[o + i], b[o + i], acc);
-    block_partial(acc, partial, (long long)rr * gridDim.x + blockIdx.x);
+    block_partial(acc, partial, (long long)rr * pstride + blockIdx.x);
 }
 
 void vec_dot(long long n, int R, const double* a, const double* b, double* partial, const int* active,
              const int* done, cudaStream_t s) {
-    dim3 g(vec_blocks(n), R);
-    dot_kernel<<<g, VEC_THREADS, 0, s>>>(n, a, b, partial, active, done);
+    vec_dot_range(n, 0, n, R, a, b, partial, vec_blocks(n), active, done, s);
+}
+
+int vec_dot_range(long long n, long long d0, long long d1, int R, const double* a, const double* b, double* partial,
+                  long long pstride, const int* active, const int* done, cudaStream_t s) {
+    const int nb = vec_blocks(d1 - d0);
+    dim3 g(nb, R);
+    dot_kernel<<<g, VEC_THREADS, 0, s>>>(n, d0, d1, a, b, partial, pstride, active, done);
+    return nb;
 }
 
 // dst = src masked to zero at fixed DOFs
@@ -157,7 +112,7 @@ void vec_axpy_masked_restart(long long n, int R, const double* t, double* r, con
 // One CTA: warp w sums the partials of RHS w, w+16, ... in a fixed order, then
 // the scalar CG logic runs per RHS.
 __global__ void __launch_bounds__(512) scalars_kernel(int mode, int R, const double* __restrict__ partial, int items,
-                                                      CgCtl c, double tol, int aux) {
+                                                      long long pstride, CgCtl c, double tol, int aux) {
     __shared__ int any_active;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if (threadIdx.x == 0) any_active = 0;
@@ -167,7 +122,7 @@ __global__ void __launch_bounds__(512) scalars_kernel(int mode, int R, const dou
         const bool act = c.active[r] != 0;
         double v = 0.0;
         if (mode == SM_BB || mode == SM_TRUE || act) {
-            for (int i = lane; i < items; i += 32) v += partial[(long long)r * items + i];
+            for (int i = lane; i < items; i += 32) v += partial[(long long)r * pstride + i];
             v = warp_sum(v);
         }
         if (lane == 0) {
@@ -225,8 +180,26 @@ __global__ void __launch_bounds__(512) scalars_kernel(int mode, int R, const dou
     if (threadIdx.x == 0) *c.done = any_active ? 0 : 1;
 }
 
-void cg_scalars(int mode, int R, const double* partial, int items, CgCtl c, double tol, cudaStream_t s, int aux) {
-    scalars_kernel<<<1, 512, 0, s>>>(mode, R, partial, items, c, tol, aux);
+void cg_scalars(int mode, int R, const double* partial, int items, CgCtl c, double tol, cudaStream_t s, int aux,
+                long long pstride) {
+    scalars_kernel<<<1, 512, 0, s>>>(mode, R, partial, items, pstride < 0 ? items : pstride, c, tol, aux);
+}
+
+// sums[r] = sum_i partial[r * pstride + i], i < items (fixed order; multi-rank dots are then
+// all-reduced and fed to cg_scalars with items = 1)
+__global__ void reduce_partials_kernel(int R, const double* __restrict__ partial, int items, long long pstride,
+                                       double* sums) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int r = wid; r < R; r += blockDim.x >> 5) {
+        double v = 0.0;
+        for (int i = lane; i < items; i += 32) v += partial[(long long)r * pstride + i];
+        v = warp_sum(v);
+        if (lane == 0) sums[r] = v;
+    }
+}
+
+void reduce_partials(int R, const double* partial, int items, long long pstride, double* sums, cudaStream_t s) {
+    reduce_partials_kernel<<<1, 512, 0, s>>>(R, partial, items, pstride, sums);
 }
 
 // r_out = r_in - alpha q ; partial r.r ; z1 = omega Dinv r_out
@@ -235,6 +208,7 @@ __global__ void __launch_bounds__(VEC_THREADS) rupdate_kernel(long long n, const
                                                               const double* __restrict__ q, double* __restrict__ rout,
                                                               const double* __restrict__ Dinv, double omega,
                                                               double* __restrict__ z1, double* partial,
+                                                              long long pstride, long long d0, long long d1,
                                                               const int* active, const int* done) {
     const int rr = blockIdx.y;
     if (done && *done) return;
@@ -245,17 +219,20 @@ __global__ void __launch_bounds__(VEC_THREADS) rupdate_kernel(long long n, const
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         const double v = fma(-al, q[o + i], rin[o + i]);
         rout[o + i] = v;
-        acc = fma(v, v, acc);
+        if (i >= d0 && i < d1) acc = fma(v, v, acc);
         if (z1) z1[o + i] = omega * Dinv[i] * v;
     }
-    block_partial(acc, partial, (long long)rr * gridDim.x + blockIdx.x);
+    block_partial(acc, partial, (long long)rr * pstride + blockIdx.x);
 }
 
-void cg_rupdate(long long n, int R, const double* alpha, const double* rin, const double* q, double* rout,
-                const double* Dinv, double omega, double* z1, double* partial, const int* active, const int* done,
-                cudaStream_t s) {
-    dim3 g(vec_blocks(n), R);
-    rupdate_kernel<<<g, VEC_THREADS, 0, s>>>(n, alpha, rin, q, rout, Dinv, omega, z1, partial, active, done);
+int cg_rupdate(long long n, int R, const double* alpha, const double* rin, const double* q, double* rout,
+               const double* Dinv, double omega, double* z1, double* partial, long long pstride, long long d0,
+               long long d1, const int* active, const int* done, cudaStream_t s) {
+    const int nb = vec_blocks(n);
+    dim3 g(nb, R);
+    rupdate_kernel<<<g, VEC_THREADS, 0, s>>>(n, alpha, rin, q, rout, Dinv, omega, z1, partial, pstride, d0, d1,
+                                              active, done);
+    return nb;
 }
 
 __global__ void flush_x_kernel(long long n, CgCtl c, const double* __restrict__ p0, const double* __restrict__ p1,

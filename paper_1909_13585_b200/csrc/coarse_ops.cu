@@ -75,7 +75,7 @@ void elements_from_E(const LevelGeom& g, const double* E, const uint8_t* mask, d
 template <int DIM, bool FROM_E>
 __global__ void galerkin_kernel(LevelGeom gc, LevelGeom gf, const double* __restrict__ E,
                                 const double* __restrict__ elm_f, const uint8_t* __restrict__ mask_f,
-                                const uint8_t* __restrict__ mask_c, double* __restrict__ elm_c) {
+                                const uint8_t* __restrict__ mask_c, double* __restrict__ elm_c, int off0) {
     constexpr int NA = 1 << DIM, NL = DIM * NA;
     __shared__ double Kc[NL * NL];
     __shared__ double T[NL * NL];
@@ -86,10 +86,12 @@ __global__ void galerkin_kernel(LevelGeom gc, LevelGeom gf, const double* __rest
     int ci[3] = {0, 0, 0};
     long long tt = Ec;
     for (int k = DIM - 1; k >= 0; --k) { ci[k] = (int)(tt % gc.N[k]); tt /= gc.N[k]; }
+    // slab ghost element layer (children not local): filled by the halo exchange instead
+    if (ci[0] < off0) return;
     double acc = 0.0;
     for (int ch = 0; ch < NA; ++ch) {
         int fi[3];
-        for (int k = 0; k < DIM; ++k) fi[k] = 2 * ci[k] + ((ch >> (DIM - 1 - k)) & 1);
+        for (int k = 0; k < DIM; ++k) fi[k] = 2 * ci[k] + ((ch >> (DIM - 1 - k)) & 1) - (k == 0 ? off0 : 0);
         long long fe = fi[0];
         for (int k = 1; k < DIM; ++k) fe = fe * gf.N[k] + fi[k];
         if (FROM_E) {
@@ -132,14 +134,14 @@ __global__ void galerkin_kernel(LevelGeom gc, LevelGeom gf, const double* __rest
 }
 
 void galerkin_elements(const LevelGeom& gc, const LevelGeom& gf, const double* E, const double* elm_f,
-                       const uint8_t* mask_f, const uint8_t* mask_c, double* elm_c, cudaStream_t s) {
+                       const uint8_t* mask_f, const uint8_t* mask_c, double* elm_c, cudaStream_t s, int off0) {
     unsigned bl = (unsigned)gc.nelem;
     if (gc.dim == 2) {
-        if (E) galerkin_kernel<2, true><<<bl, 64, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c);
-        else galerkin_kernel<2, false><<<bl, 64, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c);
+        if (E) galerkin_kernel<2, true><<<bl, 64, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0);
+        else galerkin_kernel<2, false><<<bl, 64, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0);
     } else {
-        if (E) galerkin_kernel<3, true><<<bl, 576, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c);
-        else galerkin_kernel<3, false><<<bl, 576, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c);
+        if (E) galerkin_kernel<3, true><<<bl, 576, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0);
+        else galerkin_kernel<3, false><<<bl, 576, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0);
     }
 }
 

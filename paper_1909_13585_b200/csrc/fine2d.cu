@@ -98,26 +98,28 @@ __global__ void pad_elems_kernel(int N0, int N1, Pad2 p, const double* src, doub
     dst[i] = v;
 }
 
-// compact (R, ndof) -> padded interior, masked at fixed DOFs
-__global__ void pad_vectors_kernel(int n0, int n1, Pad2 p, const uint8_t* mask, const double* src, double* dst,
-                                   long long ndof) {
+// compact (R, src_ndof) planes [0, nplanes) -> padded local planes [p0, p0 + nplanes), masked at
+// fixed DOFs (mask: compact local node masks or NULL)
+__global__ void pad_vectors_kernel(int nplanes, int p0, int n1, Pad2 p, const uint8_t* mask, const double* src,
+                                   double* dst, long long src_ndof) {
     const int r = blockIdx.y;
-    const long long nodes = (long long)n0 * n1;
+    const long long nodes = (long long)nplanes * n1;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nodes; i += (long long)gridDim.x * blockDim.x) {
-        const long long row = i / n1, col = i - row * n1;
-        const int m = mask ? mask[i] : 0;
-        const double2 v = ld2(src + r * ndof + 2 * i);
+        const long long row = i / n1 + p0, col = i - (i / n1) * n1;
+        const int m = mask ? mask[row * n1 + col] : 0;
+        const double2 v = ld2(src + r * src_ndof + 2 * i);
         st2(dst + r * p.vstride + 2 * (p.org + row * p.pitch + col), (m & 1) ? 0.0 : v.x, (m & 2) ? 0.0 : v.y);
     }
 }
 
-__global__ void unpad_vectors_kernel(int n0, int n1, Pad2 p, const double* src, double* dst, long long ndof) {
+__global__ void unpad_vectors_kernel(int nplanes, int p0, int n1, Pad2 p, const double* src, double* dst,
+                                     long long dst_ndof) {
     const int r = blockIdx.y;
-    const long long nodes = (long long)n0 * n1;
+    const long long nodes = (long long)nplanes * n1;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nodes; i += (long long)gridDim.x * blockDim.x) {
-        const long long row = i / n1, col = i - row * n1;
+        const long long row = i / n1 + p0, col = i - (i / n1) * n1;
         const double2 v = ld2(src + r * p.vstride + 2 * (p.org + row * p.pitch + col));
-        st2(dst + r * ndof + 2 * i, v.x, v.y);
+        st2(dst + r * dst_ndof + 2 * i, v.x, v.y);
     }
 }
 
@@ -134,12 +136,20 @@ void pad2_elems(const LevelGeom& g, const Pad2& p, const double* src, double* ds
 }
 void pad2_vectors(const LevelGeom& g, const Pad2& p, int R, const uint8_t* mask, const double* src, double* dst,
                   cudaStream_t s) {
-    dim3 grid((unsigned)std::min<long long>(blocks_for(g.nnodes), 1184), R);
-    pad_vectors_kernel<<<grid, 256, 0, s>>>(g.nn[0], g.nn[1], p, mask, src, dst, g.ndof);
+    pad2_vectors_planes(g, p, R, mask, 0, g.nn[0], src, g.ndof, dst, s);
 }
 void unpad2_vectors(const LevelGeom& g, const Pad2& p, int R, const double* src, double* dst, cudaStream_t s) {
-    dim3 grid((unsigned)std::min<long long>(blocks_for(g.nnodes), 1184), R);
-    unpad_vectors_kernel<<<grid, 256, 0, s>>>(g.nn[0], g.nn[1], p, src, dst, g.ndof);
+    unpad2_vectors_planes(g, p, R, 0, g.nn[0], src, dst, g.ndof, s);
+}
+void pad2_vectors_planes(const LevelGeom& g, const Pad2& p, int R, const uint8_t* mask, int p0, int nplanes,
+                         const double* src, long long src_ndof, double* dst, cudaStream_t s) {
+    dim3 grid((unsigned)std::min<long long>(blocks_for((long long)nplanes * g.nn[1]), 1184), R);
+    pad_vectors_kernel<<<grid, 256, 0, s>>>(nplanes, p0, g.nn[1], p, mask, src, dst, src_ndof);
+}
+void unpad2_vectors_planes(const LevelGeom& g, const Pad2& p, int R, int p0, int nplanes, const double* src,
+                           double* dst, long long dst_ndof, cudaStream_t s) {
+    dim3 grid((unsigned)std::min<long long>(blocks_for((long long)nplanes * g.nn[1]), 1184), R);
+    unpad_vectors_kernel<<<grid, 256, 0, s>>>(nplanes, p0, g.nn[1], p, src, dst, dst_ndof);
 }
 
 // ---------------------------------------------------------------- march kernels
@@ -176,14 +186,17 @@ __global__ void __launch_bounds__(32 * WPB) march2_kernel(March2Args a, int nct,
     const int c = ct * CS + lane - LOFF;
     const bool cin = c >= 0 && c < n1;
     const bool own_col = cin && lane >= LOFF && lane < LOFF + CS;
+    // off0 = 1 when the slab's local plane 0 is a ghost plane at an odd global index:
+    // coarse row I is coincident with local fine plane 2I - off0 (parities use P + off0).
+    const int off0 = a.off0;
     int i0, i1, own0, own1, I0 = 0, I1 = 0;
     if (OP == M2_RESTRICT) {
         const int nc0 = a.gc.nn[0];
         I0 = ch * CCH;
         I1 = min(I0 + CCH, nc0);
-        i0 = max(0, 2 * I0 - 1);
-        i1 = min(2 * I1, n0);
-        own0 = 2 * I0;
+        i0 = max(0, 2 * I0 - 1 - off0);
+        i1 = min(2 * I1 - off0, n0);
+        own0 = max(0, 2 * I0 - off0);
         own1 = i1;
     } else {
         i0 = ch * CH;
@@ -220,8 +233,9 @@ __global__ void __launch_bounds__(32 * WPB) march2_kernel(March2Args a, int nct,
         s.m = __ldg(a.mask + no);
         if (OP == M2_POST) {
             s.cx0 = s.cy0 = s.cx1 = s.cy1 = 0.0;
-            const int I = (P + 1) >> 1;
-            if ((P & 1) && cin && I < a.gc.nn[0]) {
+            const int Ps = P + off0;
+            const int I = (Ps + 1) >> 1;
+            if ((Ps & 1) && cin && I < a.gc.nn[0]) {
                 const long long row = (long long)I * nc1;
                 const int m0 = a.maskc[row + J0], m1 = a.maskc[row + J1];
                 const double2 e0 = ld2(a.ec + vbc + 2 * (row + J0));
@@ -232,8 +246,9 @@ __global__ void __launch_bounds__(32 * WPB) march2_kernel(March2Args a, int nct,
         }
         if (OP == M2_RESTRICT) {
             s.cm = 3;
-            const int I = (P - 1) >> 1;
-            if (P >= 1 && cin && !(c & 1) && I < a.gc.nn[0]) s.cm = a.maskc[(long long)I * nc1 + J0];
+            const int Ps = P + off0;
+            const int I = (Ps - 1) >> 1;
+            if (Ps >= 1 && cin && !(c & 1) && I < a.gc.nn[0]) s.cm = a.maskc[(long long)I * nc1 + J0];
         }
     };
 
@@ -245,7 +260,7 @@ __global__ void __launch_bounds__(32 * WPB) march2_kernel(March2Args a, int nct,
     double cev[4] = {0.0, 0.0, 0.0, 0.0};     // POST: coarse row of the last even plane
     double carx = 0.0, cary = 0.0, dot = 0.0, accx = 0.0, accy = 0.0;
     if (OP == M2_POST) {
-        const int rlo = (i0 - 1) >> 1;
+        const int rlo = (i0 - 1 + off0) >> 1;
         if (cin && rlo >= 0) {
             const long long row = (long long)rlo * nc1;
             const int m0 = a.maskc[row + J0], m1 = a.maskc[row + J1];
@@ -261,6 +276,7 @@ __global__ void __launch_bounds__(32 * WPB) march2_kernel(March2Args a, int nct,
                       double& k2y) {
         const bool fx = s.m & 1, fy = s.m & 2;
         const bool own_plane = P >= own0 && P < own1;
+        const bool slab_plane = P >= a.so0 && P < a.so1;   // dots: slab-owned planes only
         if (OP == M2_CGP) {
             ux = fma(beta, s.v1x, s.v0x);
             uy = fma(beta, s.v1y, s.v0y);
@@ -271,8 +287,10 @@ __global__ void __launch_bounds__(32 * WPB) march2_kernel(March2Args a, int nct,
             const double rx = fma(-alpha, s.v1x, s.v0x), ry = fma(-alpha, s.v1y, s.v0y);
             if (own_col && own_plane) {
                 st2(y2b + 2 * (pd.org + (long long)P * pd.pitch + c), rx, ry);
-                dot = fma(rx, rx, dot);
-                dot = fma(ry, ry, dot);
+                if (slab_plane) {
+                    dot = fma(rx, rx, dot);
+                    dot = fma(ry, ry, dot);
+                }
             }
             kx = rx; ky = ry;
             ux = fx ? 0.0 : omega * s.dx * rx;
@@ -281,7 +299,7 @@ __global__ void __launch_bounds__(32 * WPB) march2_kernel(March2Args a, int nct,
         } else if (OP == M2_POST) {
             double px, py;
             const bool codd = c & 1;
-            if (P & 1) {
+            if ((P + off0) & 1) {
                 const double lx = codd ? 0.5 * (cev[0] + cev[2]) : cev[0], ly = codd ? 0.5 * (cev[1] + cev[3]) : cev[1];
                 const double hx = codd ? 0.5 * (s.cx0 + s.cx1) : s.cx0, hy = codd ? 0.5 * (s.cy0 + s.cy1) : s.cy0;
                 px = 0.5 * (lx + hx);
@@ -365,6 +383,7 @@ __global__ void __launch_bounds__(32 * WPB) march2_kernel(March2Args a, int nct,
             if (L >= i0) {
                 const double Axx = (mA & 1) ? urx : lox, Axy = (mA & 2) ? ury : loy;
                 const bool own = own_col && L >= own0 && L < own1;
+                const bool sdot = own && L >= a.so0 && L < a.so1;   // slab-owned: counts in dots
                 const long long o = 2 * (pd.org + (long long)L * pd.pitch + c);
                 if (OP == M2_MATVEC) {
                     if (own) st2(yb + o, Axx, Axy);
@@ -375,19 +394,25 @@ __global__ void __launch_bounds__(32 * WPB) march2_kernel(March2Args a, int nct,
                     const double zy = fma(omega * day, auxy - Axy, ury);
                     if (own) {
                         st2(yb + o, zx, zy);
-                        dot = fma(auxx, zx, dot);
-                        dot = fma(auxy, zy, dot);
+                        if (sdot) {
+                            dot = fma(auxx, zx, dot);
+                            dot = fma(auxy, zy, dot);
+                        }
                     }
                 } else if (OP == M2_CGP) {
                     if (own) {
                         st2(yb + o, Axx, Axy);
-                        dot = fma(urx, Axx, dot);
-                        dot = fma(ury, Axy, dot);
+                        if (sdot) {
+                            dot = fma(urx, Axx, dot);
+                            dot = fma(ury, Axy, dot);
+                        }
                         st2(xvb + o, fma(xalpha, auxx, aux2x), fma(xalpha, auxy, aux2y));
                     }
                 } else if (OP == M2_RESTRICT) {
                     // t = r - K z1 (lanes 1..30 valid), then P^T: columns by shuffles, planes by carry
-                    const bool tv = cin && lane >= 1 && lane <= 30;
+                    // t counts only on slab-owned planes: the coarse ghost row above gets a
+                    // partial sum that the upper neighbour adds in (reverse halo exchange)
+                    const bool tv = cin && lane >= 1 && lane <= 30 && L >= a.so0 && L < a.so1;
                     const double tx = (tv && !(mA & 1)) ? auxx - Axx : 0.0;
                     const double ty = (tv && !(mA & 2)) ? auxy - Axy : 0.0;
                     const double tlx = shfl_up1(tx), tly = shfl_up1(ty);
@@ -395,16 +420,17 @@ __global__ void __launch_bounds__(32 * WPB) march2_kernel(March2Args a, int nct,
                     const double hx = fma(0.5, tlx + trx, tx), hy = fma(0.5, tly + try_, ty);
                     const bool cown = cin && !(c & 1) && lane >= 2 && lane <= 28;
                     const int cm = (int)k2x;     // coarse mask of row (P-1)>>1 = the row output below
-                    if (L & 1) {
+                    const int Ls = L + off0;
+                    if (Ls & 1) {
                         accx = fma(0.5, hx, accx); accy = fma(0.5, hy, accy);
-                        const int I = (L - 1) >> 1;
+                        const int I = (Ls - 1) >> 1;
                         if (cown && I >= I0 && I < I1)
                             st2(a.coarse + vbc + 2 * ((long long)I * nc1 + J0), (cm & 1) ? 0.0 : accx,
                                 (cm & 2) ? 0.0 : accy);
                         accx = 0.5 * hx; accy = 0.5 * hy;
                     } else {
                         accx += hx; accy += hy;
-                        const int I = L >> 1;
+                        const int I = Ls >> 1;
                         if (L == n0 - 1 && cown && I >= I0 && I < I1)
                             st2(a.coarse + vbc + 2 * ((long long)I * nc1 + J0), (cm & 1) ? 0.0 : accx,
                                 (cm & 2) ? 0.0 : accy);
@@ -422,7 +448,7 @@ __global__ void __launch_bounds__(32 * WPB) march2_kernel(March2Args a, int nct,
     }
     if (a.partial) {
         dot = warp_sum(dot);
-        if (lane == 0) a.partial[(long long)r * items + item] = dot;
+        if (lane == 0) a.partial[(long long)r * a.pstride + item] = dot;
     }
 }
 

@@ -69,7 +69,8 @@ __device__ __forceinline__ void load_node(const FineArgs& a, long long vbase, lo
 // Epilogue at an owned output node.  acc = (K M x) row values, raw = unmasked x.
 template <int DIM, int OP>
 __device__ __forceinline__ void finish_node(const FineArgs& a, long long vbase, long long node, int mbits,
-                                            const double* acc, const double* raw, double& dot, double xal) {
+                                            const double* acc, const double* raw, double& dot, double xal,
+                                            bool sdot) {
     const long long o = vbase + (long long)DIM * node;
     double out[DIM];
 #pragma unroll
@@ -82,10 +83,10 @@ __device__ __forceinline__ void finish_node(const FineArgs& a, long long vbase, 
         } else {  // JACOBI
             const double bk = a.b[o + k];
             out[k] = raw[k] + a.omega * a.Dinv[(long long)DIM * node + k] * (bk - ax);
-            dot += bk * out[k];
+            if (sdot) dot += bk * out[k];
         }
         if (OP == FOP_CGP) {
-            dot += raw[k] * ax;
+            if (sdot) dot += raw[k] * ax;
             if (a.xv) a.xv[o + k] = fma(xal, a.pin[o + k], a.xv[o + k]);   // deferred x += alpha p
         }
     }
@@ -190,7 +191,9 @@ __global__ void __launch_bounds__(128) fine3d_kernel(FineArgs a, int nct, int nc
                     hi[k] = fma(Ee[ej][ec], th[k], hi[k]);
                 }
             }
-        if (own && L >= i0) finish_node<3, OP>(a, vbase, ((long long)L * n1 + j) * n2 + c, mA, lo, rawA, dot, xal);
+        if (own && L >= i0)
+            finish_node<3, OP>(a, vbase, ((long long)L * n1 + j) * n2 + c, mA, lo, rawA, dot, xal,
+                               L >= a.so0 && L < a.so1);
         carry[0] = hi[0]; carry[1] = hi[1]; carry[2] = hi[2];
 #pragma unroll
         for (int q = 0; q < 3; ++q)
@@ -202,7 +205,7 @@ __global__ void __launch_bounds__(128) fine3d_kernel(FineArgs a, int nct, int nc
     }
     if (a.partial) {
         dot = warp_sum(dot);
-        if (lane == 0) a.partial[(long long)r * items + item] = dot;
+        if (lane == 0) a.partial[(long long)r * a.pstride + item] = dot;
     }
 }
 

@@ -24,9 +24,11 @@ struct FineArgs {
     const double* xalpha;
     const int* active;      // per RHS or NULL
     const int* done;        // or NULL
-    double* partial;        // dot partials [R][items] or NULL
+    double* partial;        // dot partials, RHS r item i at partial[r * pstride + i], or NULL
+    long long pstride;
     int R;
     int nu_paper;           // 1: nu == 0.3 -> compile-time K0
+    int so0, so1;           // slab-owned local node planes (dots)
 };
 
 void fine_set_constants(int dim, const double* K0, cudaStream_t s);
@@ -71,8 +73,11 @@ struct March2Args {
     const double* xalpha;
     const int* active;
     const int* done;
-    double* partial;
+    double* partial;              // dot partials, RHS r item i at partial[r * pstride + i]
+    long long pstride;
     int R;
+    int so0, so1;                 // slab-owned local node planes [so0, so1): dots and restriction sources
+    int off0;                     // 1 if local plane 0 is at an odd global plane (slab ghost), else 0
 };
 void fine2d_set_constants(const double* K0, cudaStream_t s);
 Pad2 pad2_layout(const LevelGeom& g);
@@ -83,6 +88,11 @@ void pad2_elems(const LevelGeom& g, const Pad2& p, const double* src, double* ds
 void pad2_vectors(const LevelGeom& g, const Pad2& p, int R, const uint8_t* mask, const double* src, double* dst,
                   cudaStream_t s);   // compact (R, ndof) -> padded, masked (ghosts untouched)
 void unpad2_vectors(const LevelGeom& g, const Pad2& p, int R, const double* src, double* dst, cudaStream_t s);
+// slab variants: local planes [p0, p0 + nplanes) <-> compact planes [0, nplanes) of (R, ndof_c) vectors
+void pad2_vectors_planes(const LevelGeom& g, const Pad2& p, int R, const uint8_t* mask, int p0, int nplanes,
+                         const double* src, long long src_ndof, double* dst, cudaStream_t s);
+void unpad2_vectors_planes(const LevelGeom& g, const Pad2& p, int R, int p0, int nplanes, const double* src,
+                           double* dst, long long dst_ndof, cudaStream_t s);
 int march2_apply(int op, const March2Args& a, bool nu_paper, cudaStream_t s);
 int march2_items(int op, const LevelGeom& g, const LevelGeom* gc);
 
@@ -108,18 +118,21 @@ void coarse_apply(int op, const CoarseArgs& a, cudaStream_t s);
 void galerkin_set_constants(int dim, const double* K0, cudaStream_t s);
 void galerkin_elements(const LevelGeom& gc, const LevelGeom& gf, const double* E /*if from_E*/,
                        const double* elm_f, const uint8_t* mask_f, const uint8_t* mask_c,
-                       double* elm_c, cudaStream_t s);
+                       double* elm_c, cudaStream_t s, int off0 = 0);
 void elements_from_E(const LevelGeom& g, const double* E, const uint8_t* mask, double* elm, cudaStream_t s);
 void stencil_from_elements(const LevelGeom& g, const double* elm, uint8_t* mask, double* st, cudaStream_t s);
 void stencil_diag(const LevelGeom& g, const double* st, uint8_t* mask, double* st_rw, double* Dinv, double* D,
                   cudaStream_t s);
 
 // ---------------------------------------------------------------- transfers
+// off0: 1 if the slab's local plane 0 is an (odd-global) ghost plane; [fo0, fo1): slab-owned fine
+// planes that contribute to the restriction (fo1 < 0: all).
 void restrict_apply(const LevelGeom& gf, const LevelGeom& gc, const uint8_t* mf, const uint8_t* mc,
-                    const double* fine, double* coarse, int R, const int* active, const int* done, cudaStream_t s);
+                    const double* fine, double* coarse, int R, const int* active, const int* done, cudaStream_t s,
+                    int off0 = 0, int fo0 = 0, int fo1 = -1);
 void prolong_add(const LevelGeom& gf, const LevelGeom& gc, const uint8_t* mf, const uint8_t* mc,
                  const double* coarse, double* fine, int R, const int* active, const int* done, bool accumulate,
-                 cudaStream_t s);
+                 cudaStream_t s, int off0 = 0);
 
 // ---------------------------------------------------------------- dense coarsest
 void dense_from_stencil(const LevelGeom& g, const double* st, double* A, long long ld, cudaStream_t s);
@@ -134,25 +147,26 @@ void dense_apply(const double* Ainv, long long ld, long long n, const double* r,
 int vec_blocks(long long n);
 void cg_pointwise_jacobi(long long n, int R, const double* r, const double* Dinv, double omega, double* z,
                          const int* active, const int* done, cudaStream_t s);
-// x += alpha p; r -= alpha q; z = omega Dinv r; partial r.r
-void cg_update(long long n, int R, const double* alpha, const double* p, const double* q, double* x, double* r,
-               const double* Dinv, double omega, double* z, double* partial, const int* active, const int* done,
-               cudaStream_t s);
 void vec_dot(long long n, int R, const double* a, const double* b, double* partial, const int* active,
              const int* done, cudaStream_t s);
+// dot over entries [d0, d1) of each RHS; partial[r * pstride + block]; returns the number of blocks
+int vec_dot_range(long long n, long long d0, long long d1, int R, const double* a, const double* b, double* partial,
+                  long long pstride, const int* active, const int* done, cudaStream_t s);
 void vec_mask_copy(long long nnodes, int dim, int R, const uint8_t* mask, const double* src, double* dst,
                    cudaStream_t s);
 void vec_axpy_masked_restart(long long n, int R, const double* t, double* r, const int* restart, cudaStream_t s);
-// r_out = r_in - alpha q ; partial r_out.r_out ; z1 = omega Dinv r_out (z1 may be NULL)
-void cg_rupdate(long long n, int R, const double* alpha, const double* rin, const double* q, double* rout,
-                const double* Dinv, double omega, double* z1, double* partial, const int* active, const int* done,
-                cudaStream_t s);
+// r_out = r_in - alpha q ; partial r_out.r_out over [d0, d1) ; z1 = omega Dinv r_out (z1 may be NULL).
+// Returns the number of partial items per RHS.
+int cg_rupdate(long long n, int R, const double* alpha, const double* rin, const double* q, double* rout,
+               const double* Dinv, double omega, double* z1, double* partial, long long pstride, long long d0,
+               long long d1, const int* active, const int* done, cudaStream_t s);
 // x += xalpha * p_{xbuf} for every RHS with a pending deferred update
 void cg_flush_x(long long n, int R, CgCtl c, const double* p0, const double* p1, double* x, cudaStream_t s);
 
 enum ScalarMode { SM_INIT = 0, SM_ALPHA = 1, SM_CONV = 2, SM_BETA = 3, SM_RZ0 = 4, SM_TRUE = 5, SM_BB = 6 };
 void cg_scalars(int mode, int R, const double* partial, int items, CgCtl c, double tol, cudaStream_t s,
-                int aux = 0);
+                int aux = 0, long long pstride = -1);
+void reduce_partials(int R, const double* partial, int items, long long pstride, double* sums, cudaStream_t s);
 
 // ---------------------------------------------------------------- stress stiffness G(u) phi
 void stress_set_constants(int dim, double nu, cudaStream_t s);

@@ -1,14 +1,27 @@
-// C-ABI host side of libmgcg: handle, hierarchy setup, CUDA-graph solve loop.
-// See include/mgcg.h for the contract and the paper passages each call follows.
+// C-ABI host side of libmgcg: handle, slab decomposition, hierarchy setup, CUDA-graph solve
+// loop.  See include/mgcg.h for the contract and the paper passages each call follows.
+//
+// Slabs: the global grid is cut along axis 0 into S = nranks x nslab slabs at
+// coarsest-level element boundaries.  Every slab holds its owned element layers plus the
+// ghost element layer below, and its owned node planes plus one ghost node plane on each
+// side with a neighbour, at every level.  All kernels run unchanged on the slab's local grid
+// (ghost rows of an operator output are wrong and never used); dots count owned planes
+// only; restriction sums from owned fine planes only, leaving a partial sum in the upper
+// coarse ghost plane that the owner adds in.  Validity of ghost planes is restored by the
+// exchanges in comm.cu at the points listed in DESIGN.md §7.  With S = 1 every exchange is
+// a no-op and the code path is the single-GPU one.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
 #include "../../include/mgcg.h"
+#include "comm.h"
 #include "element.cuh"
 #include "kernels.h"
 
@@ -40,6 +53,11 @@ static mg_status fail(mg_status s, const std::string& msg) {
         if (s_ != MG_OK) return s_;      \
     } while (0)
 
+#define COMM(expr)                                                                 \
+    do {                                                                           \
+        if (!(expr)) return fail(MG_ERR_NCCL, std::string("exchange: ") + comm_last_error()); \
+    } while (0)
+
 // ---------------------------------------------------------------- element stiffness (host)
 // K0[(a,i),(b,j)] = lam S_ij + mu S_ji + mu delta_ij sum_k S_kk with
 // S_ij[a,b] = int dN_a/dx_i dN_b/dx_j over the unit element, a product of 1-D
@@ -55,21 +73,27 @@ static void element_stiffness(int dim, double nu, std::vector<double>& K) {
 }
 
 // ---------------------------------------------------------------- small kernels
-__global__ void fixed_to_mask_kernel(long long nnodes, int dim, const uint8_t* fixed, uint8_t* mask) {
+// mask[dst0 + i] = fixed bits of node (src0 + i) of the user's fixed array, i < count
+__global__ void fixed_to_mask_kernel(long long count, int dim, const uint8_t* fixed, long long src0, uint8_t* mask,
+                                     long long dst0) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nnodes) return;
+    if (i >= count) return;
     int m = 0;
-    for (int k = 0; k < dim; ++k) m |= (fixed[dim * i + k] ? 1 : 0) << k;
-    mask[i] = (uint8_t)m;
+    for (int k = 0; k < dim; ++k) m |= (fixed[dim * (src0 + i) + k] ? 1 : 0) << k;
+    mask[dst0 + i] = (uint8_t)m;
 }
 
-__global__ void coarse_mask_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* mf, uint8_t* mc) {
+// a coarse DOF is fixed iff its coincident fine DOF is (reading r11); fine local plane of
+// coarse local plane I is 2I - off0 (slab ghost plane below has no local fine partner)
+__global__ void coarse_mask_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* mf, uint8_t* mc, int off0) {
     long long I = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (I >= gc.nnodes) return;
     long long t = I, q = 0;
     int ci[3] = {0, 0, 0};
     for (int k = gc.dim - 1; k >= 0; --k) { ci[k] = (int)(t % gc.nn[k]); t /= gc.nn[k]; }
-    for (int k = 0; k < gc.dim; ++k) q = q * gf.nn[k] + 2 * ci[k];
+    const int f0 = 2 * ci[0] - off0;
+    if (f0 < 0) return;
+    for (int k = 0; k < gc.dim; ++k) q = q * gf.nn[k] + (k == 0 ? f0 : 2 * ci[k]);
     mc[I] = mf[q];
 }
 
@@ -77,12 +101,12 @@ __global__ void check_modulus_kernel(long long n, const double* E, int* bad) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double v = E[i];
-    if (!(v > 0.0) || !isfinite(v)) atomicOr(bad, 1);
+    if (!(v > 0.0) || !isfinite(v)) atomicOr(bad, 4);
 }
 
 // ---------------------------------------------------------------- handle
 struct Level {
-    LevelGeom g;
+    LevelGeom g;              // local geometry of the slab at this level (incl. ghosts)
     uint8_t* mask = nullptr;
     double* Dinv = nullptr;
     double* D = nullptr;
@@ -90,6 +114,30 @@ struct Level {
     double* r = nullptr;      // vectors (levels >= 1), R x ndof
     double* z = nullptr;
     double* w = nullptr;
+    int o0 = 0, o1 = 0;       // owned local node planes [o0, o1)
+    int gp0 = 0;              // global node plane of local plane 0
+    long long pn = 0;         // nodes per plane
+};
+
+struct Slab {
+    int id = 0;               // global slab index
+    int e0 = 0, e1 = 0;       // owned global element layers at level 0
+    int gl = 0, gh = 0;       // ghost plane below / above
+    long long uoff = 0;       // node offset of the owned planes in the rank's user vectors
+    Level lv[MG_MAX_LEVELS];
+    double* E = nullptr;      // local elements (ghost layer first when gl)
+    double *elmA = nullptr, *elmB = nullptr;
+    // 2D fine level: ghost-padded copies used by the march kernels (fine2d.cu)
+    Pad2 pd{};
+    double* Epad = nullptr;
+    uint8_t* maskpad = nullptr;
+    double* Dinvpad = nullptr;
+    long long vs = 0;         // doubles per RHS of a level-0 vector (padded in 2D, ndof in 3D)
+    double *b = nullptr, *x = nullptr, *r0 = nullptr, *r1 = nullptr, *p0 = nullptr, *p1 = nullptr, *q = nullptr,
+           *zf = nullptr, *z = nullptr, *t = nullptr;
+    double* zpre = nullptr;
+    double *u = nullptr, *phi = nullptr, *gy = nullptr, *sig = nullptr, *Es = nullptr;   // G(u) phi (slab mode)
+    long long gphi_cap = 0;
 };
 
 struct mg_ctx {
@@ -100,44 +148,45 @@ struct mg_ctx {
     mg_opts opts{0.6, 1, 1, 1000};
     cudaStream_t user = nullptr, stream = nullptr;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
-    Level lv[MG_MAX_LEVELS];
-    double* E = nullptr;
+    LevelGeom G[MG_MAX_LEVELS];   // global geometry
+    std::vector<Slab> sl;         // this handle's slabs (axis-0 order)
+    int S = 1;                    // slabs in the job (nranks x nslab)
+    Comm comm;
+    std::vector<int> rank_p0, rank_p1;   // per rank: owned global fine node planes [p0, p1)
+    long long n_rank = 0, m_rank = 0;    // this rank's owned DOFs / elements
+    long long pn0 = 0;                   // fine nodes per plane
     std::vector<double> K0;
-    // 2D fine level: ghost-padded copies used by the march kernels (fine2d.cu)
-    Pad2 pd{};
-    double* Epad = nullptr;
-    uint8_t* maskpad = nullptr;
-    double* Dinvpad = nullptr;
-    long long vs = 0;         // doubles per RHS of a level-0 vector (padded in 2D, ndof in 3D)
-    // coarsest dense inverse
+    // coarsest level (global, replicated on every rank)
     double* Ainv = nullptr;
     long long nL = 0, npad = 0;
-    // fine vectors (R x ndof each)
+    double *cr = nullptr, *cz = nullptr;         // (R, nL) gathered coarsest vectors
+    double* stg = nullptr;                       // gathered coarsest stencil
+    double *cpack = nullptr, *cgath = nullptr;   // cross-rank gather staging
+    long long cpack_cap = 0;
+    double* gj_work = nullptr;
+    double* xtmp = nullptr;                      // NCCL reverse-add receive buffer
+    long long xtmp_cap = 0;
+    // shared solve state
     int Ralloc = 0;
-    double *b = nullptr, *x = nullptr, *r0 = nullptr, *r1 = nullptr, *p0 = nullptr, *p1 = nullptr, *q = nullptr,
-           *zf = nullptr, *z = nullptr, *t = nullptr;
-    double* zpre = nullptr;   // generic path: buffer holding the pre-smoothed z after blk_restrict
-    double *stage = nullptr, *stage2 = nullptr;   // compact (R x ndof) staging: host copies, 2D L == 1 solve
+    double *stage = nullptr, *stage2 = nullptr;  // (R, n_rank) staging: host copies, L == 1 dense solve
     double* partial = nullptr;
-    long long partial_cap = 0;
-    // CG control block
+    long long pst = 0;                           // partial stride per RHS
+    double* sums = nullptr;                      // multi-rank dot sums
     CgCtl ctl{};
     void* ctl_mem = nullptr;
     int* h_pinned = nullptr;     // done, status, iters[64]
     double* h_dbl = nullptr;     // bb, rr, tt [64] each
     int* d_status = nullptr;
-    // graphs
     cudaGraphExec_t g_init = nullptr, g_restart = nullptr, g_iter = nullptr, g_true = nullptr;
     long long n_init = 0, n_restart = 0, n_iter = 0, n_true = 0;
     int graph_R = -1;
     double graph_tol = -1.0;
-    // stress
-    double* sig = nullptr;
-    // stats
     long long launches = 0;
 };
 
-static const LevelGeom& G0(mg_ctx* c) { return c->lv[0].g; }
+static int nslab(const mg_ctx* c) { return (int)c->sl.size(); }
+static bool multi(const mg_ctx* c) { return c->S > 1; }
+static const LevelGeom& G0(mg_ctx* c) { return c->G[0]; }
 
 static LevelGeom make_geom(int dim, const int* N) {
     LevelGeom g{};
@@ -171,83 +220,242 @@ static void stream_leave(mg_ctx* c) {
     cudaStreamWaitEvent(c->user, c->ev_out, 0);
 }
 
+// ---------------------------------------------------------------- partition (host)
+// Slab k of S gets a contiguous run of coarsest-level element layers (sizes differ by at
+// most one), so every slab boundary is a node plane of every level.
+static bool partition(int N0, int levels, int S, int k, int* e0, int* e1) {
+    const int f = 1 << (levels - 1);
+    const int Nc = N0 / f;
+    if (S < 1 || k < 0 || k >= S || Nc < S) return false;
+    const int base = Nc / S, rem = Nc % S;
+    const int c0 = k * base + std::min(k, rem);
+    const int c1 = c0 + base + (k < rem ? 1 : 0);
+    *e0 = c0 * f;
+    *e1 = c1 * f;
+    return true;
+}
+
+// ---------------------------------------------------------------- plane fields
+static PlaneField node_field(const Slab& s, int l, void* base, int esize, long long per_node, long long vec_stride,
+                             int nvec) {
+    const Level& v = s.lv[l];
+    PlaneField f{};
+    f.base = base;
+    f.esize = esize;
+    f.plane_len = v.pn * per_node;
+    f.vec_stride = vec_stride;
+    f.nvec = nvec;
+    f.first_own = v.o0;
+    f.last_own = v.o1 - 1;
+    f.lo_ghost = s.gl ? 0 : -1;
+    f.hi_ghost = s.gh ? v.g.nn[0] - 1 : -1;
+    f.dirs = 3;
+    return f;
+}
+// level-l compact vectors (R, ndof_local)
+static PlaneField vec_field(mg_ctx* c, const Slab& s, int l, double* v, int R) {
+    return node_field(s, l, v, 8, c->dim, s.lv[l].g.ndof, R);
+}
+// level-0 vectors: padded in 2D, compact in 3D
+static PlaneField fine_field(mg_ctx* c, const Slab& s, double* v, int R) {
+    if (c->dim != 2) return vec_field(c, s, 0, v, R);
+    PlaneField f = node_field(s, 0, v + 2 * s.pd.org, 8, 2, s.pd.vstride, R);
+    f.plane_len = 2LL * s.pd.pitch;
+    return f;
+}
+// element arrays (per-element records of `per_elem` doubles): ghost layer below only
+static PlaneField elem_field(const Slab& s, int l, double* e, long long per_elem) {
+    const LevelGeom& g = s.lv[l].g;
+    PlaneField f{};
+    f.base = e;
+    f.esize = 8;
+    f.plane_len = g.nelem / g.N[0] * per_elem;
+    f.vec_stride = 0;
+    f.nvec = 1;
+    f.first_own = s.gl;
+    f.last_own = g.N[0] - 1;
+    f.lo_ghost = s.gl ? 0 : -1;
+    f.hi_ghost = -1;
+    f.dirs = 1;
+    return f;
+}
+
+static mg_status xchg(mg_ctx* c, const std::function<PlaneField(const Slab&)>& fn) {
+    if (!multi(c)) return MG_OK;
+    std::vector<PlaneField> f;
+    for (const Slab& s : c->sl) f.push_back(fn(s));
+    COMM(halo_forward(c->comm, f.data(), nslab(c), c->stream));
+    return MG_OK;
+}
+static mg_status xchg_add(mg_ctx* c, const std::function<PlaneField(const Slab&)>& fn) {
+    if (!multi(c)) return MG_OK;
+    std::vector<PlaneField> f;
+    for (const Slab& s : c->sl) f.push_back(fn(s));
+    COMM(halo_reverse_add(c->comm, f.data(), nslab(c), c->xtmp, c->stream));
+    return MG_OK;
+}
+
+// ---------------------------------------------------------------- coarsest level (global)
+// Gather the owned planes of a per-slab level-(L-1) field of nvec vectors into the global
+// array dst (nvec, nglob_per_vec) with planes of plen doubles.
+static mg_status gather_coarsest(mg_ctx* c, const std::function<double*(Slab&)>& src,
+                                 const std::function<long long(const Slab&)>& src_stride, long long plen, int nvec,
+                                 double* dst, long long dst_stride) {
+    cudaStream_t st = c->stream;
+    const int l = c->L - 1;
+    if (c->comm.nranks <= 1) {
+        for (Slab& s : c->sl) {
+            const Level& v = s.lv[l];
+            CU(cudaMemcpy2DAsync(dst + (long long)(v.gp0 + v.o0) * plen, dst_stride * 8, src(s) + v.o0 * plen,
+                                 src_stride(s) * 8, (v.o1 - v.o0) * plen * 8, nvec, cudaMemcpyDeviceToDevice, st));
+        }
+        return MG_OK;
+    }
+    // cross-rank: pack this rank's owned planes (padded to the largest rank), all-gather, unpack
+    const int f = 1 << l;
+    int maxp = 0;
+    for (int q = 0; q < c->comm.nranks; ++q) {
+        const int np = (c->rank_p1[q] - c->rank_p0[q]) / f + (q == c->comm.nranks - 1 ? 1 : 0);
+        maxp = std::max(maxp, np);
+    }
+    const long long chunk = (long long)maxp * plen;   // per vector
+    const long long need = chunk * nvec;
+    if (need > c->cpack_cap) return fail(MG_ERR_DIM, "coarsest gather buffer too small");
+    const int pr0 = c->rank_p0[c->comm.rank] / f;
+    for (Slab& s : c->sl) {
+        const Level& v = s.lv[l];
+        CU(cudaMemcpy2DAsync(c->cpack + (long long)(v.gp0 + v.o0 - pr0) * plen, chunk * 8, src(s) + v.o0 * plen,
+                             src_stride(s) * 8, (v.o1 - v.o0) * plen * 8, nvec, cudaMemcpyDeviceToDevice, st));
+    }
+    COMM(comm_allgather(c->comm, c->cpack, c->cgath, (size_t)need * 8, st));
+    for (int q = 0; q < c->comm.nranks; ++q) {
+        const int p0 = c->rank_p0[q] / f;
+        const int np = (c->rank_p1[q] - c->rank_p0[q]) / f + (q == c->comm.nranks - 1 ? 1 : 0);
+        CU(cudaMemcpy2DAsync(dst + (long long)p0 * plen, dst_stride * 8, c->cgath + q * need, chunk * 8, np * plen * 8,
+                             nvec, cudaMemcpyDeviceToDevice, st));
+    }
+    return MG_OK;
+}
+
+// z_{L-1} = A_{L-1}^{-1} r_{L-1}: gather the owned planes of every slab, one dense product
+// (replicated on every rank), scatter all local planes (owned and ghost) back.
+static mg_status coarsest_solve(mg_ctx* c, int R, const int* active, const int* done,
+                                const std::function<double*(Slab&)>& rsrc, const std::function<double*(Slab&)>& zdst) {
+    const int l = c->L - 1;
+    if (!multi(c)) {
+        Slab& s = c->sl[0];
+        dense_apply(c->Ainv, c->npad, c->nL, rsrc(s), zdst(s), R, active, done, c->stream);
+        c->launches++;
+        return MG_OK;
+    }
+    const long long plen = c->G[l].nnodes / c->G[l].nn[0] * c->dim;
+    TRY(gather_coarsest(c, rsrc, [&](const Slab& s) { return s.lv[l].g.ndof; }, plen, R, c->cr, c->nL));
+    dense_apply(c->Ainv, c->npad, c->nL, c->cr, c->cz, R, active, done, c->stream);
+    c->launches++;
+    for (Slab& s : c->sl) {
+        const Level& v = s.lv[l];
+        CU(cudaMemcpy2DAsync(zdst(s), v.g.ndof * 8, c->cz + (long long)v.gp0 * plen, c->nL * 8, v.g.nn[0] * plen * 8, R,
+                             cudaMemcpyDeviceToDevice, c->stream));
+    }
+    return MG_OK;
+}
+
 // ---------------------------------------------------------------- operators (per design)
 static mg_status compute_operators(mg_ctx* c) {
     cudaStream_t s = c->stream;
     const int L = c->L, dim = c->dim;
-    TRY(([&]() -> mg_status {
-        CU(cudaMemsetAsync(c->d_status, 0, sizeof(int), s));
-        long long m = G0(c).nelem;
-        check_modulus_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(m, c->E, c->d_status);
-        CHECK_LAUNCH();
-        int bad = 0;
-        CU(cudaMemcpyAsync(&bad, c->d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CU(cudaStreamSynchronize(s));
-        if (bad) return fail(MG_ERR_MODULUS, "E_e must be positive and finite");
-        return MG_OK;
-    }()));
-    fine_diag(G0(c), c->E, c->lv[0].mask, c->lv[0].Dinv, c->lv[0].D, s);
-    c->launches += 2;
-    if (dim == 2) {
-        pad2_elems(G0(c), c->pd, c->E, c->Epad, s);
-        pad2_nodes_u8(G0(c), c->pd, c->lv[0].mask, c->maskpad, 3, s);
-        pad2_nodes_f64(G0(c), c->pd, c->lv[0].Dinv, c->Dinvpad, s);
-        c->launches += 3;
+    const int NL = dim * (1 << dim);
+    // E ghost layers, modulus check
+    TRY(xchg(c, [&](const Slab& sl) { return elem_field(sl, 0, sl.E, 1); }));
+    CU(cudaMemsetAsync(c->d_status, 0, sizeof(int), s));
+    for (Slab& sl : c->sl) {
+        const long long m = sl.lv[0].g.nelem;
+        check_modulus_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(m, sl.E, c->d_status);
+        c->launches++;
     }
     CHECK_LAUNCH();
-    const int NL = dim * (1 << dim);
-    double* elm_prev = nullptr;
-    if (L == 1) {
-        CU(cudaMallocAsync(&elm_prev, sizeof(double) * G0(c).nelem * NL * NL, s));
-        elements_from_E(G0(c), c->E, c->lv[0].mask, elm_prev, s);
-        stencil_from_elements(G0(c), elm_prev, c->lv[0].mask, c->lv[0].st, s);
+    for (Slab& sl : c->sl) fine_diag(sl.lv[0].g, sl.E, sl.lv[0].mask, sl.lv[0].Dinv, sl.lv[0].D, s);
+    c->launches += nslab(c);
+    TRY(xchg(c, [&](const Slab& sl) { return node_field(sl, 0, sl.lv[0].Dinv, 8, dim, 0, 1); }));
+    TRY(xchg(c, [&](const Slab& sl) { return node_field(sl, 0, sl.lv[0].D, 8, dim, 0, 1); }));
+    if (dim == 2) {
+        for (Slab& sl : c->sl) {
+            pad2_elems(sl.lv[0].g, sl.pd, sl.E, sl.Epad, s);
+            pad2_nodes_u8(sl.lv[0].g, sl.pd, sl.lv[0].mask, sl.maskpad, 3, s);
+            pad2_nodes_f64(sl.lv[0].g, sl.pd, sl.lv[0].Dinv, sl.Dinvpad, s);
+            c->launches += 3;
+        }
+    }
+    CHECK_LAUNCH();
+    if (L == 1) {   // single level (one slab): the fine operator is the coarsest
+        Slab& sl = c->sl[0];
+        elements_from_E(sl.lv[0].g, sl.E, sl.lv[0].mask, sl.elmA, s);
+        stencil_from_elements(sl.lv[0].g, sl.elmA, sl.lv[0].mask, sl.lv[0].st, s);
         c->launches += 2;
         CHECK_LAUNCH();
     }
     for (int l = 1; l < L; ++l) {
-        Level& f = c->lv[l - 1];
-        Level& g = c->lv[l];
-        double* elm = nullptr;
-        CU(cudaMallocAsync(&elm, sizeof(double) * g.g.nelem * NL * NL, s));
-        galerkin_elements(g.g, f.g, l == 1 ? c->E : nullptr, elm_prev, f.mask, g.mask, elm, s);
+        for (Slab& sl : c->sl) {
+            Level& f = sl.lv[l - 1];
+            Level& g = sl.lv[l];
+            double* elm = (l & 1) ? sl.elmA : sl.elmB;
+            double* elm_prev = (l & 1) ? sl.elmB : sl.elmA;
+            galerkin_elements(g.g, f.g, l == 1 ? sl.E : nullptr, elm_prev, f.mask, g.mask, elm, s, sl.gl);
+            c->launches++;
+        }
         CHECK_LAUNCH();
-        if (elm_prev) CU(cudaFreeAsync(elm_prev, s));
-        elm_prev = elm;
-        stencil_from_elements(g.g, elm, g.mask, g.st, s);
-        stencil_diag(g.g, g.st, g.mask, g.st, g.Dinv, g.D, s);
-        c->launches += 3;
+        TRY(xchg(c, [&](const Slab& sl) { return elem_field(sl, l, (l & 1) ? sl.elmA : sl.elmB, NL * NL); }));
+        for (Slab& sl : c->sl) {
+            Level& g = sl.lv[l];
+            double* elm = (l & 1) ? sl.elmA : sl.elmB;
+            stencil_from_elements(g.g, elm, g.mask, g.st, s);
+            stencil_diag(g.g, g.st, g.mask, g.st, g.Dinv, g.D, s);
+            c->launches += 2;
+        }
         CHECK_LAUNCH();
+        TRY(xchg(c, [&](const Slab& sl) { return node_field(sl, l, sl.lv[l].mask, 1, 1, 0, 1); }));
+        TRY(xchg(c, [&](const Slab& sl) { return node_field(sl, l, sl.lv[l].Dinv, 8, dim, 0, 1); }));
+        TRY(xchg(c, [&](const Slab& sl) { return node_field(sl, l, sl.lv[l].D, 8, dim, 0, 1); }));
     }
-    if (elm_prev) CU(cudaFreeAsync(elm_prev, s));
-    // coarsest dense inverse
-    Level& cl = c->lv[L - 1];
+    // coarsest dense inverse (global coarsest operator on every rank)
+    const LevelGeom& gL = c->G[L - 1];
+    const int ns = dim == 2 ? 9 : 27;
+    const double* stc = c->sl[0].lv[L - 1].st;
+    if (multi(c)) {
+        TRY(gather_coarsest(c, [&](Slab& sl) { return sl.lv[L - 1].st; },
+                            [&](const Slab& sl) { return sl.lv[L - 1].g.nnodes; }, gL.nnodes / gL.nn[0],
+                            ns * dim * dim, c->stg, gL.nnodes));
+        stc = c->stg;
+    }
     CU(cudaMemsetAsync(c->Ainv, 0, sizeof(double) * c->npad * c->npad, s));
-    dense_from_stencil(cl.g, cl.st, c->Ainv, c->npad, s);
+    dense_from_stencil(gL, stc, c->Ainv, c->npad, s);
     dense_pad_identity(c->Ainv, c->nL, c->npad, s);
-    double* work = nullptr;
-    CU(cudaMallocAsync(&work, sizeof(double) * (32 * 32 + 2 * c->npad * 32), s));
-    CU(cudaMemsetAsync(c->d_status, 0, sizeof(int), s));
-    dense_spd_inverse(c->Ainv, c->npad, work, c->d_status, s);
+    CU(cudaMemsetAsync(c->gj_work, 0, sizeof(double) * (32 * 32 + 2 * c->npad * 32), s));
+    dense_spd_inverse(c->Ainv, c->npad, c->gj_work, c->d_status, s);
     c->launches += 2 + 5 * (c->npad / 32);
     CHECK_LAUNCH();
-    CU(cudaFreeAsync(work, s));
-    int st = 0;
-    CU(cudaMemcpyAsync(&st, c->d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
+    int st[1] = {0};
+    CU(cudaMemcpyAsync(st, c->d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
-    if (st) return fail(MG_ERR_SINGULAR, "coarsest operator: non-positive pivot in the SPD inverse");
+    if (st[0] & 4) return fail(MG_ERR_MODULUS, "E_e must be positive and finite");
+    if (st[0]) return fail(MG_ERR_SINGULAR, "coarsest operator: non-positive pivot in the SPD inverse");
     return MG_OK;
 }
 
 static void free_vectors(mg_ctx* c) {
-    double** fv[] = {&c->b, &c->x, &c->r0, &c->r1, &c->p0, &c->p1, &c->q, &c->zf, &c->z, &c->t, &c->partial,
-                     &c->stage, &c->stage2};
-    for (auto p : fv)
-        if (*p) { cudaFree(*p); *p = nullptr; }
-    for (int l = 1; l < c->L; ++l) {
-        double** lvv[] = {&c->lv[l].r, &c->lv[l].z, &c->lv[l].w};
-        for (auto p : lvv)
+    for (Slab& s : c->sl) {
+        double** fv[] = {&s.b, &s.x, &s.r0, &s.r1, &s.p0, &s.p1, &s.q, &s.zf, &s.z, &s.t};
+        for (auto p : fv)
             if (*p) { cudaFree(*p); *p = nullptr; }
+        for (int l = 1; l < c->L; ++l) {
+            double** lvv[] = {&s.lv[l].r, &s.lv[l].z, &s.lv[l].w};
+            for (auto p : lvv)
+                if (*p) { cudaFree(*p); *p = nullptr; }
+        }
     }
+    double** cv[] = {&c->partial, &c->stage, &c->stage2, &c->cr, &c->cz, &c->xtmp};
+    for (auto p : cv)
+        if (*p) { cudaFree(*p); *p = nullptr; }
     cudaGraphExec_t* gs[] = {&c->g_init, &c->g_restart, &c->g_iter, &c->g_true};
     for (auto g : gs)
         if (*g) { cudaGraphExecDestroy(*g); *g = nullptr; }
@@ -259,31 +467,80 @@ static mg_status ensure_vectors(mg_ctx* c, int R) {
     if (R <= c->Ralloc) return MG_OK;
     CU(cudaStreamSynchronize(c->stream));
     free_vectors(c);
-    const long long n = c->vs;
-    double** fv[] = {&c->b, &c->x, &c->r0, &c->r1, &c->p0, &c->p1, &c->q, &c->zf, &c->z, &c->t};
-    for (auto p : fv) {
-        CU(cudaMalloc(p, sizeof(double) * n * R));
-        CU(cudaMemset(*p, 0, sizeof(double) * n * R));   // ghost entries of the padded layout stay 0
+    long long pst = 0, xplane = 0;
+    for (Slab& s : c->sl) {
+        const long long n = s.vs;
+        double** fv[] = {&s.b, &s.x, &s.r0, &s.r1, &s.p0, &s.p1, &s.q, &s.zf, &s.z, &s.t};
+        for (auto p : fv) {
+            CU(cudaMalloc(p, sizeof(double) * n * R));
+            CU(cudaMemset(*p, 0, sizeof(double) * n * R));   // ghost entries of the padded layout stay 0
+        }
+        for (int l = 1; l < c->L; ++l) {
+            long long nl = s.lv[l].g.ndof;
+            CU(cudaMalloc(&s.lv[l].r, sizeof(double) * nl * R));
+            CU(cudaMalloc(&s.lv[l].z, sizeof(double) * nl * R));
+            CU(cudaMalloc(&s.lv[l].w, sizeof(double) * nl * R));
+            CU(cudaMemset(s.lv[l].r, 0, sizeof(double) * nl * R));
+            CU(cudaMemset(s.lv[l].z, 0, sizeof(double) * nl * R));
+            CU(cudaMemset(s.lv[l].w, 0, sizeof(double) * nl * R));
+            xplane = std::max(xplane, s.lv[l].pn * c->dim);
+        }
+        long long items = fine_items(s.lv[0].g);
+        if (c->dim == 2) {
+            for (int op : {M2_CGP, M2_RESTRICT, M2_POST, M2_RESID, M2_JACOBI}) {
+                long long it = march2_items(op, s.lv[0].g, c->L > 1 ? &s.lv[1].g : &s.lv[0].g);
+                items = std::max(items, it);
+            }
+        }
+        items = std::max<long long>(items, vec_blocks(n));
+        pst += items;
     }
-    CU(cudaMalloc(&c->stage, sizeof(double) * G0(c).ndof * R));
-    CU(cudaMalloc(&c->stage2, sizeof(double) * G0(c).ndof * R));
-    for (int l = 1; l < c->L; ++l) {
-        long long nl = c->lv[l].g.ndof;
-        CU(cudaMalloc(&c->lv[l].r, sizeof(double) * nl * R));
-        CU(cudaMalloc(&c->lv[l].z, sizeof(double) * nl * R));
-        CU(cudaMalloc(&c->lv[l].w, sizeof(double) * nl * R));
+    c->pst = pst;
+    CU(cudaMalloc(&c->partial, sizeof(double) * c->pst * R));
+    CU(cudaMalloc(&c->stage, sizeof(double) * c->n_rank * R));
+    CU(cudaMalloc(&c->stage2, sizeof(double) * c->n_rank * R));
+    if (multi(c)) {
+        CU(cudaMalloc(&c->cr, sizeof(double) * c->nL * R));
+        CU(cudaMalloc(&c->cz, sizeof(double) * c->nL * R));
+        c->xtmp_cap = xplane * R;
+        CU(cudaMalloc(&c->xtmp, sizeof(double) * std::max<long long>(c->xtmp_cap, 1)));
     }
-    long long items = fine_items(G0(c));
-    if (c->dim == 2) {
-        for (int op : {M2_CGP, M2_RESTRICT, M2_POST, M2_RESID}) {
-            long long it = march2_items(op, G0(c), c->L > 1 ? &c->lv[1].g : &c->lv[0].g);
-            items = it > items ? it : items;
+    c->Ralloc = R;
+    return MG_OK;
+}
+
+// ---------------------------------------------------------------- user vectors <-> slabs
+// user (R, n_rank) owned planes of this rank -> level-0 slab vectors (+ ghost exchange)
+static mg_status scatter_fine(mg_ctx* c, const double* src, int R, bool masked, double* Slab::*dst) {
+    for (Slab& s : c->sl) {
+        const Level& v = s.lv[0];
+        const int np = v.o1 - v.o0;
+        if (c->dim == 2) {
+            pad2_vectors_planes(v.g, s.pd, R, masked ? v.mask : nullptr, v.o0, np, src + 2 * s.uoff, c->n_rank,
+                                s.*dst, c->stream);
+        } else {
+            CU(cudaMemcpy2DAsync(s.*dst + v.o0 * v.pn * 3, v.g.ndof * 8, src + 3 * s.uoff, c->n_rank * 8,
+                                 np * v.pn * 3 * 8, R, cudaMemcpyDeviceToDevice, c->stream));
+            if (masked) vec_mask_copy(v.g.nnodes, 3, R, v.mask, s.*dst, s.*dst, c->stream);
+        }
+        c->launches++;
+    }
+    return xchg(c, [&](const Slab& s) { return fine_field(c, s, s.*dst, R); });
+}
+
+// level-0 slab vectors (owned planes) -> user (R, n_rank)
+static mg_status gather_fine(mg_ctx* c, double* Slab::*src, int R, double* dst) {
+    for (Slab& s : c->sl) {
+        const Level& v = s.lv[0];
+        const int np = v.o1 - v.o0;
+        if (c->dim == 2) {
+            unpad2_vectors_planes(v.g, s.pd, R, v.o0, np, s.*src, dst + 2 * s.uoff, c->n_rank, c->stream);
+            c->launches++;
+        } else {
+            CU(cudaMemcpy2DAsync(dst + 3 * s.uoff, c->n_rank * 8, s.*src + v.o0 * v.pn * 3, v.g.ndof * 8,
+                                 np * v.pn * 3 * 8, R, cudaMemcpyDeviceToDevice, c->stream));
         }
     }
-    long long vb = vec_blocks(n);
-    c->partial_cap = (items > vb ? items : vb) * (long long)R;
-    CU(cudaMalloc(&c->partial, sizeof(double) * c->partial_cap));
-    c->Ralloc = R;
     return MG_OK;
 }
 
@@ -296,21 +553,31 @@ struct Rec {
     long long launches = 0;
 };
 
-static FineArgs fine_args(mg_ctx* c, const Rec& rc) {
+static FineArgs fine_args(mg_ctx* c, const Slab& s, const Rec& rc) {
     FineArgs a{};
-    a.g = G0(c); a.E = c->E; a.mask = c->lv[0].mask; a.omega = c->opts.omega;
+    a.g = s.lv[0].g; a.E = s.E; a.mask = s.lv[0].mask; a.omega = c->opts.omega;
     a.active = rc.active; a.done = rc.done; a.R = rc.R; a.nu_paper = c->nu_paper ? 1 : 0;
+    a.so0 = s.lv[0].o0; a.so1 = s.lv[0].o1; a.pstride = c->pst;
+    return a;
+}
+
+static March2Args march_args(mg_ctx* c, const Slab& s, const Rec& rc) {
+    March2Args a{};
+    a.g = s.lv[0].g;
+    if (c->L > 1) { a.gc = s.lv[1].g; a.maskc = s.lv[1].mask; }
+    a.pd = s.pd; a.E = s.Epad; a.mask = s.maskpad; a.Dinv = s.Dinvpad; a.omega = c->opts.omega;
+    a.alpha = c->ctl.alpha; a.beta = c->ctl.beta; a.xalpha = c->ctl.xalpha;
+    a.active = rc.active; a.done = rc.done; a.R = rc.R;
+    a.so0 = s.lv[0].o0; a.so1 = s.lv[0].o1; a.off0 = s.gl; a.pstride = c->pst;
     return a;
 }
 
 // Level-0 operator application: 2D through the padded march kernels, 3D through fine_ops.
-static int level0_apply(mg_ctx* c, int op, const FineArgs& f) {
+static int level0_apply(mg_ctx* c, const Slab& s, int op, const FineArgs& f) {
     if (c->dim != 2) return fine_apply(op, f, c->stream);
-    March2Args m{};
-    m.g = G0(c);
-    if (c->L > 1) { m.gc = c->lv[1].g; m.maskc = c->lv[1].mask; }
-    m.pd = c->pd; m.E = c->Epad; m.mask = c->maskpad; m.Dinv = c->Dinvpad;
-    m.omega = f.omega; m.active = f.active; m.done = f.done; m.partial = f.partial; m.R = f.R;
+    Rec rc{c, f.R, f.active, f.done};
+    March2Args m = march_args(c, s, rc);
+    m.omega = f.omega; m.partial = f.partial;
     int mop;
     switch (op) {
         case FOP_MATVEC: mop = M2_MATVEC; m.x = f.x; m.y = f.y; break;
@@ -324,168 +591,256 @@ static int level0_apply(mg_ctx* c, int op, const FineArgs& f) {
     return march2_apply(mop, m, c->nu_paper, c->stream);
 }
 
-static void level_smooth(Rec& rc, int l, const double* r, const double* z, double* w, double* partial) {
+// owned entries [d0, d1) of a level-0 vector (for dots)
+static void fine_own_range(mg_ctx* c, const Slab& s, long long* d0, long long* d1) {
+    const Level& v = s.lv[0];
+    if (c->dim == 2) {
+        *d0 = 2 * (s.pd.org + (long long)v.o0 * s.pd.pitch);
+        *d1 = 2 * (s.pd.org + (long long)v.o1 * s.pd.pitch);
+    } else {
+        *d0 = v.o0 * v.pn * 3;
+        *d1 = v.o1 * v.pn * 3;
+    }
+}
+
+// consume the dot partials (items per RHS, stride c->pst) with a scalar CG step; across ranks
+// the per-RHS sums are all-reduced first
+static mg_status finish_dots(mg_ctx* c, int mode, int R, long long items, int aux = 0, double tol = 0.0) {
+    if (c->comm.nranks > 1) {
+        reduce_partials(R, c->partial, (int)items, c->pst, c->sums, c->stream);
+        COMM(comm_allreduce_sum(c->comm, c->sums, R, c->stream));
+        cg_scalars(mode, R, c->sums, 1, c->ctl, tol, c->stream, aux, 1);
+        c->launches += 2;
+    } else {
+        cg_scalars(mode, R, c->partial, (int)items, c->ctl, tol, c->stream, aux, c->pst);
+        c->launches++;
+    }
+    return MG_OK;
+}
+
+static void level_smooth(Rec& rc, Slab& s, int l, const double* r, const double* z, double* w, double* partial) {
     mg_ctx* c = rc.c;
     if (l == 0 && c->L > 1) {
-        FineArgs a = fine_args(c, rc);
-        a.x = z; a.b = r; a.Dinv = c->lv[0].Dinv; a.y = w; a.partial = partial;
-        level0_apply(c, FOP_JACOBI, a);
+        FineArgs a = fine_args(c, s, rc);
+        a.x = z; a.b = r; a.Dinv = s.lv[0].Dinv; a.y = w; a.partial = partial;
+        level0_apply(c, s, FOP_JACOBI, a);
     } else {
         CoarseArgs a{};
-        a.g = c->lv[l].g; a.st = c->lv[l].st; a.x = z; a.b = r; a.Dinv = c->lv[l].Dinv; a.y = w;
+        a.g = s.lv[l].g; a.st = s.lv[l].st; a.x = z; a.b = r; a.Dinv = s.lv[l].Dinv; a.y = w;
         a.omega = c->opts.omega; a.active = rc.active; a.done = rc.done; a.R = rc.R;
         coarse_apply(COP_JACOBI, a, c->stream);
     }
     rc.launches++;
 }
 
-static void level_resid(Rec& rc, int l, const double* r, const double* z, double* w) {
+static void level_resid(Rec& rc, Slab& s, int l, const double* r, const double* z, double* w) {
     mg_ctx* c = rc.c;
     if (l == 0) {
-        FineArgs a = fine_args(c, rc);
+        FineArgs a = fine_args(c, s, rc);
         a.x = z; a.b = r; a.y = w;
-        level0_apply(c, FOP_RESID, a);
+        level0_apply(c, s, FOP_RESID, a);
     } else {
         CoarseArgs a{};
-        a.g = c->lv[l].g; a.st = c->lv[l].st; a.x = z; a.b = r; a.y = w;
+        a.g = s.lv[l].g; a.st = s.lv[l].st; a.x = z; a.b = r; a.y = w;
         a.active = rc.active; a.done = rc.done; a.R = rc.R;
         coarse_apply(COP_RESID, a, c->stream);
     }
     rc.launches++;
 }
 
-// Symmetric V(nu_pre, nu_post)-cycle on level l (generic kernels): z ~ A_l^-1 r.  Returns
-// the buffer holding z (z or w).  Used for levels >= 1 in the solve and for mg_vcycle.
-static double* vcycle(Rec& rc, int l, const double* r, double* z, double* w) {
+// Symmetric V(nu_pre, nu_post)-cycle on level l >= 1 of every slab: z ~ A_l^-1 r, with r
+// owned-valid on entry (ghosts exchanged here) and z valid on all local planes on exit.
+// Per slab the result is in z or w (same choice on every slab); returns 0 for z, 1 for w.
+static mg_status vcycle(Rec& rc, int l, int* which) {
     mg_ctx* c = rc.c;
-    const Level& lv = c->lv[l];
     const int R = rc.R;
     if (l == c->L - 1) {
-        dense_apply(c->Ainv, c->npad, c->nL, r, z, R, rc.active, rc.done, c->stream);
+        TRY(coarsest_solve(c, R, rc.active, rc.done, [&](Slab& s) { return s.lv[l].r; },
+                           [&](Slab& s) { return s.lv[l].z; }));
         rc.launches++;
-        return z;
+        *which = 0;
+        return MG_OK;
     }
-    cg_pointwise_jacobi(lv.g.ndof, R, r, lv.Dinv, c->opts.omega, z, rc.active, rc.done, c->stream);
-    rc.launches++;
-    for (int s = 1; s < c->opts.nu_pre; ++s) {
-        level_smooth(rc, l, r, z, w, nullptr);
-        std::swap(z, w);
+    TRY(xchg(c, [&](const Slab& s) { return vec_field(c, s, l, s.lv[l].r, R); }));
+    int zi = 0;   // 0: z holds the iterate, 1: w
+    auto zb = [&](Slab& s) { return zi ? s.lv[l].w : s.lv[l].z; };
+    auto wb = [&](Slab& s) { return zi ? s.lv[l].z : s.lv[l].w; };
+    for (Slab& s : c->sl) {
+        cg_pointwise_jacobi(s.lv[l].g.ndof, R, s.lv[l].r, s.lv[l].Dinv, c->opts.omega, s.lv[l].z, rc.active, rc.done,
+                            c->stream);
+        rc.launches++;
     }
-    level_resid(rc, l, r, z, w);
-    const Level& nx = c->lv[l + 1];
-    restrict_apply(lv.g, nx.g, lv.mask, nx.mask, w, nx.r, R, rc.active, rc.done, c->stream);
-    rc.launches++;
-    double* zc = vcycle(rc, l + 1, nx.r, nx.z, nx.w);
-    prolong_add(lv.g, nx.g, lv.mask, nx.mask, zc, z, R, rc.active, rc.done, true, c->stream);
-    rc.launches++;
-    for (int s = 0; s < c->opts.nu_post; ++s) {
-        level_smooth(rc, l, r, z, w, nullptr);
-        std::swap(z, w);
+    for (int it = 1; it < c->opts.nu_pre; ++it) {
+        TRY(xchg(c, [&](const Slab& s) { return vec_field(c, s, l, zi ? s.lv[l].w : s.lv[l].z, R); }));
+        for (Slab& s : c->sl) level_smooth(rc, s, l, s.lv[l].r, zb(s), wb(s), nullptr);
+        zi ^= 1;
     }
-    return z;
+    if (c->opts.nu_pre > 1)
+        TRY(xchg(c, [&](const Slab& s) { return vec_field(c, s, l, zi ? s.lv[l].w : s.lv[l].z, R); }));
+    for (Slab& s : c->sl) {
+        level_resid(rc, s, l, s.lv[l].r, zb(s), wb(s));
+        Level& f = s.lv[l];
+        Level& nx = s.lv[l + 1];
+        restrict_apply(f.g, nx.g, f.mask, nx.mask, wb(s), nx.r, R, rc.active, rc.done, c->stream, s.gl, f.o0, f.o1);
+        rc.launches++;
+    }
+    TRY(xchg_add(c, [&](const Slab& s) { return vec_field(c, s, l + 1, s.lv[l + 1].r, R); }));
+    int cw = 0;
+    TRY(vcycle(rc, l + 1, &cw));
+    for (Slab& s : c->sl) {
+        Level& f = s.lv[l];
+        Level& nx = s.lv[l + 1];
+        prolong_add(f.g, nx.g, f.mask, nx.mask, cw ? nx.w : nx.z, zb(s), R, rc.active, rc.done, true, c->stream, s.gl);
+        rc.launches++;
+    }
+    for (int it = 0; it < c->opts.nu_post; ++it) {
+        if (it > 0) TRY(xchg(c, [&](const Slab& s) { return vec_field(c, s, l, zi ? s.lv[l].w : s.lv[l].z, R); }));
+        for (Slab& s : c->sl) level_smooth(rc, s, l, s.lv[l].r, zb(s), wb(s), nullptr);
+        zi ^= 1;
+    }
+    if (c->opts.nu_post > 0)
+        TRY(xchg(c, [&](const Slab& s) { return vec_field(c, s, l, zi ? s.lv[l].w : s.lv[l].z, R); }));
+    *which = zi;
+    return MG_OK;
 }
 
 // ---- fine-level blocks of one CG iteration (fused kernels in 2D, composed kernels otherwise)
-static March2Args march_args(mg_ctx* c, const Rec& rc) {
-    March2Args a{};
-    a.g = G0(c);
-    if (c->L > 1) { a.gc = c->lv[1].g; a.maskc = c->lv[1].mask; }
-    a.pd = c->pd; a.E = c->Epad; a.mask = c->maskpad; a.Dinv = c->Dinvpad; a.omega = c->opts.omega;
-    a.alpha = c->ctl.alpha; a.beta = c->ctl.beta; a.xalpha = c->ctl.xalpha;
-    a.active = rc.active; a.done = rc.done; a.R = rc.R;
-    return a;
-}
-
-// p_out = zf + beta p_in ; q = K p_out ; partial p.q ; x += xalpha p_in.  Returns partial items.
-static int blk_cgp(Rec& rc, const double* pin, double* pout) {
+// p_out = zf + beta p_in ; q = K p_out ; partial p.q ; x += xalpha p_in.  Then q ghosts.
+static mg_status blk_cgp(Rec& rc, double* Slab::*pin, double* Slab::*pout, long long* items) {
     mg_ctx* c = rc.c;
-    rc.launches++;
-    FineArgs a = fine_args(c, rc);
-    a.z = c->zf; a.pin = pin; a.pout = pout; a.y = c->q; a.beta = c->ctl.beta;
-    a.xv = c->x; a.xalpha = c->ctl.xalpha; a.partial = c->partial;
-    return level0_apply(c, FOP_CGP, a);
+    long long off = 0;
+    for (Slab& s : c->sl) {
+        FineArgs a = fine_args(c, s, rc);
+        a.z = s.zf; a.pin = s.*pin; a.pout = s.*pout; a.y = s.q; a.beta = c->ctl.beta;
+        a.xv = s.x; a.xalpha = c->ctl.xalpha; a.partial = c->partial + off;
+        off += level0_apply(c, s, FOP_CGP, a);
+        rc.launches++;
+    }
+    *items = off;
+    return MG_OK;
 }
 
 // r_out = r_in - alpha q ; partial r.r ; pre-smooth z1 = omega D^-1 r_out ; r_1 = P^T (r_out - K z1)
-static int blk_restrict(Rec& rc, const double* rin, double* rout) {
+static mg_status blk_restrict(Rec& rc, double* Slab::*rin, double* Slab::*rout, long long* items) {
     mg_ctx* c = rc.c;
-    const long long n = c->vs;
+    const int R = rc.R;
+    TRY(xchg(c, [&](const Slab& s) { return fine_field(c, s, s.q, R); }));
+    long long off = 0;
     if (c->fused2d) {
-        March2Args a = march_args(c, rc);
-        a.x = rin; a.x2 = c->q; a.y2 = rout; a.coarse = c->lv[1].r; a.partial = c->partial;
+        for (Slab& s : c->sl) {
+            March2Args a = march_args(c, s, rc);
+            a.x = s.*rin; a.x2 = s.q; a.y2 = s.*rout; a.coarse = s.lv[1].r; a.partial = c->partial + off;
+            off += march2_apply(M2_RESTRICT, a, c->nu_paper, c->stream);
+            rc.launches++;
+        }
+        *items = off;
+        return xchg_add(c, [&](const Slab& s) { return vec_field(c, s, 1, s.lv[1].r, R); });
+    }
+    for (Slab& s : c->sl) {
+        long long d0, d1;
+        fine_own_range(c, s, &d0, &d1);
+        off += cg_rupdate(s.vs, R, c->ctl.alpha, s.*rin, s.q, s.*rout, c->dim == 2 ? s.Dinvpad : s.lv[0].Dinv,
+                          c->opts.omega, c->L > 1 ? s.z : nullptr, c->partial + off, c->pst, d0, d1, rc.active,
+                          rc.done, c->stream);
         rc.launches++;
-        return march2_apply(M2_RESTRICT, a, c->nu_paper, c->stream);
     }
-    cg_rupdate(n, rc.R, c->ctl.alpha, rin, c->q, rout, c->dim == 2 ? c->Dinvpad : c->lv[0].Dinv, c->opts.omega,
-               c->L > 1 ? c->z : nullptr,
-               c->partial, rc.active, rc.done, c->stream);
-    rc.launches++;
-    const int items = vec_blocks(n);
-    if (c->L == 1) return items;
-    double *z = c->z, *w = c->t;
-    for (int s = 1; s < c->opts.nu_pre; ++s) {
-        level_smooth(rc, 0, rout, z, w, nullptr);
-        std::swap(z, w);
+    *items = off;
+    if (c->L == 1) return MG_OK;
+    int zi = 0;
+    for (int it = 1; it < c->opts.nu_pre; ++it) {
+        TRY(xchg(c, [&](const Slab& s) { return fine_field(c, s, zi ? s.t : s.z, R); }));
+        for (Slab& s : c->sl) level_smooth(rc, s, 0, s.*rout, zi ? s.t : s.z, zi ? s.z : s.t, nullptr);
+        zi ^= 1;
     }
-    level_resid(rc, 0, rout, z, w);
-    restrict_apply(G0(c), c->lv[1].g, c->lv[0].mask, c->lv[1].mask, w, c->lv[1].r, rc.R, rc.active, rc.done,
-                   c->stream);
-    rc.launches++;
-    c->zpre = z;
-    return items;
+    if (c->opts.nu_pre > 1) TRY(xchg(c, [&](const Slab& s) { return fine_field(c, s, zi ? s.t : s.z, R); }));
+    for (Slab& s : c->sl) {
+        double* z = zi ? s.t : s.z;
+        double* w = zi ? s.z : s.t;
+        level_resid(rc, s, 0, s.*rout, z, w);
+        restrict_apply(s.lv[0].g, s.lv[1].g, s.lv[0].mask, s.lv[1].mask, w, s.lv[1].r, R, rc.active, rc.done,
+                       c->stream, s.gl, s.lv[0].o0, s.lv[0].o1);
+        rc.launches++;
+        s.zpre = z;
+    }
+    return xchg_add(c, [&](const Slab& s) { return vec_field(c, s, 1, s.lv[1].r, R); });
 }
 
-// levels 1..L-1 of the V-cycle on lv[1].r; returns the level-1 correction buffer
-static double* coarse_cycle(Rec& rc) {
-    mg_ctx* c = rc.c;
-    if (c->L == 1) return nullptr;
-    return vcycle(rc, 1, c->lv[1].r, c->lv[1].z, c->lv[1].w);
+// levels 1..L-1 of the V-cycle on lv[1].r; *which: 0 -> lv[1].z, 1 -> lv[1].w
+static mg_status coarse_cycle(Rec& rc, int* which) {
+    *which = 0;
+    if (rc.c->L == 1) return MG_OK;
+    return vcycle(rc, 1, which);
 }
 
-// zf = post-smoothed (z1 + P ec) ; partial r.zf.  Returns partial items.
-static int blk_post(Rec& rc, const double* r, const double* ec) {
+// zf = post-smoothed (z1 + P ec) ; partial r.zf ; then zf ghosts.
+static mg_status blk_post(Rec& rc, double* Slab::*r, int cw, long long* items) {
     mg_ctx* c = rc.c;
-    const long long n = c->vs;
-    if (c->L == 1) {
-        if (c->dim == 2) {   // dense solve on the compact layout
-            unpad2_vectors(G0(c), c->pd, rc.R, r, c->stage, c->stream);
-            dense_apply(c->Ainv, c->npad, c->nL, c->stage, c->stage2, rc.R, rc.active, rc.done, c->stream);
-            pad2_vectors(G0(c), c->pd, rc.R, nullptr, c->stage2, c->zf, c->stream);
+    const int R = rc.R;
+    long long off = 0;
+    if (c->L == 1) {   // single slab: dense solve on the compact layout
+        Slab& s = c->sl[0];
+        if (c->dim == 2) {
+            unpad2_vectors(s.lv[0].g, s.pd, R, s.*r, c->stage, c->stream);
+            dense_apply(c->Ainv, c->npad, c->nL, c->stage, c->stage2, R, rc.active, rc.done, c->stream);
+            pad2_vectors(s.lv[0].g, s.pd, R, nullptr, c->stage2, s.zf, c->stream);
             rc.launches += 2;
         } else {
-            dense_apply(c->Ainv, c->npad, c->nL, r, c->zf, rc.R, rc.active, rc.done, c->stream);
+            dense_apply(c->Ainv, c->npad, c->nL, s.*r, s.zf, R, rc.active, rc.done, c->stream);
         }
-        vec_dot(n, rc.R, r, c->zf, c->partial, rc.active, rc.done, c->stream);
+        off = vec_dot_range(s.vs, 0, s.vs, R, s.*r, s.zf, c->partial, c->pst, rc.active, rc.done, c->stream);
         rc.launches += 2;
-        return vec_blocks(n);
+        *items = off;
+        return MG_OK;
     }
     if (c->fused2d) {
-        March2Args a = march_args(c, rc);
-        a.x = r; a.ec = ec; a.y = c->zf; a.partial = c->partial;
-        rc.launches++;
-        return march2_apply(M2_POST, a, c->nu_paper, c->stream);
+        for (Slab& s : c->sl) {
+            March2Args a = march_args(c, s, rc);
+            a.x = s.*r; a.ec = cw ? s.lv[1].w : s.lv[1].z; a.y = s.zf; a.partial = c->partial + off;
+            off += march2_apply(M2_POST, a, c->nu_paper, c->stream);
+            rc.launches++;
+        }
+        *items = off;
+        return xchg(c, [&](const Slab& s) { return fine_field(c, s, s.zf, R); });
     }
-    prolong_add(G0(c), c->lv[1].g, c->lv[0].mask, c->lv[1].mask, ec, c->zpre, rc.R, rc.active, rc.done, true,
-                c->stream);
-    rc.launches++;
-    double* src = c->zpre;
-    int items = vec_blocks(n);
+    for (Slab& s : c->sl) {
+        prolong_add(s.lv[0].g, s.lv[1].g, s.lv[0].mask, s.lv[1].mask, cw ? s.lv[1].w : s.lv[1].z, s.zpre, R,
+                    rc.active, rc.done, true, c->stream, s.gl);
+        rc.launches++;
+    }
     if (c->opts.nu_post == 0) {
-        cudaMemcpyAsync(c->zf, src, sizeof(double) * n * rc.R, cudaMemcpyDeviceToDevice, c->stream);
-        vec_dot(n, rc.R, r, c->zf, c->partial, rc.active, rc.done, c->stream);
-        rc.launches++;
-        return items;
+        for (Slab& s : c->sl) {
+            CU(cudaMemcpyAsync(s.zf, s.zpre, sizeof(double) * s.vs * R, cudaMemcpyDeviceToDevice, c->stream));
+            long long d0, d1;
+            fine_own_range(c, s, &d0, &d1);
+            off += vec_dot_range(s.vs, d0, d1, R, s.*r, s.zf, c->partial + off, c->pst, rc.active, rc.done, c->stream);
+            rc.launches++;
+        }
+        *items = off;
+        return MG_OK;   // zf = zpre is ghost-valid (prolongation is local)
     }
-    for (int s = 0; s < c->opts.nu_post; ++s) {
-        const bool last = s == c->opts.nu_post - 1;
-        double* dst = last ? c->zf : (src == c->z ? c->t : c->z);
-        FineArgs a = fine_args(c, rc);
-        a.x = src; a.b = r; a.Dinv = c->lv[0].Dinv; a.y = dst; a.partial = last ? c->partial : nullptr;
-        items = level0_apply(c, FOP_JACOBI, a);
-        rc.launches++;
-        src = dst;
+    // post sweeps: src -> dst, the last one into zf with the r.zf dot
+    std::vector<double*> src(nslab(c));
+    for (int k = 0; k < nslab(c); ++k) src[k] = c->sl[k].zpre;
+    for (int it = 0; it < c->opts.nu_post; ++it) {
+        const bool last = it == c->opts.nu_post - 1;
+        if (it > 0) {
+            std::vector<PlaneField> f;
+            for (int k = 0; k < nslab(c); ++k) f.push_back(fine_field(c, c->sl[k], src[k], R));
+            if (multi(c)) COMM(halo_forward(c->comm, f.data(), nslab(c), c->stream));
+        }
+        off = 0;
+        for (int k = 0; k < nslab(c); ++k) {
+            Slab& s = c->sl[k];
+            double* dst = last ? s.zf : (src[k] == s.z ? s.t : s.z);
+            FineArgs a = fine_args(c, s, rc);
+            a.x = src[k]; a.b = s.*r; a.Dinv = s.lv[0].Dinv; a.y = dst; a.partial = last ? c->partial + off : nullptr;
+            off += level0_apply(c, s, FOP_JACOBI, a);
+            rc.launches++;
+            src[k] = dst;
+        }
     }
-    return items;
+    *items = off;
+    return xchg(c, [&](const Slab& s) { return fine_field(c, s, s.zf, R); });
 }
 
 static mg_status capture_begin(mg_ctx* c) {
@@ -504,65 +859,277 @@ static mg_status capture_end(mg_ctx* c, cudaGraphExec_t* exec, long long* nodes)
     return MG_OK;
 }
 
+// abort an open capture on error so the stream stays usable
+static mg_status captured(mg_ctx* c, mg_status st) {
+    if (st != MG_OK) {
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(c->stream, &g);
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+    }
+    return st;
+}
+
+// b.b over owned entries (all slabs) -> SM_BB
+static mg_status dot_finish(mg_ctx* c, int R, double* Slab::*a, double* Slab::*b, int mode) {
+    long long off = 0;
+    for (Slab& s : c->sl) {
+        long long d0, d1;
+        fine_own_range(c, s, &d0, &d1);
+        off += vec_dot_range(s.vs, d0, d1, R, s.*a, s.*b, c->partial + off, c->pst, nullptr, nullptr, c->stream);
+        c->launches++;
+    }
+    return finish_dots(c, mode, R, off);
+}
+
 // Graphs (captured once per (R, tol)):
 //   init    : b.b, x = 0, p0 = 0, q = 0, r1 = b
 //   restart : z = B r (r1 -> r0, alpha = 0), r.z            (start and true-residual restarts)
 //   iter    : two CG iterations (p and r ping-pong buffers)
 //   true    : flush deferred x update, t = b - K x, t.t
+static mg_status record_restart(mg_ctx* c, int R) {
+    Rec rc{c, R, c->ctl.active, c->ctl.done};
+    long long k;
+    TRY(blk_restrict(rc, &Slab::r1, &Slab::r0, &k));
+    int cw;
+    TRY(coarse_cycle(rc, &cw));
+    TRY(blk_post(rc, &Slab::r0, cw, &k));
+    return finish_dots(c, SM_RZ0, R, k);
+}
+
+static mg_status record_iter(mg_ctx* c, int R, double tol) {
+    Rec rc{c, R, c->ctl.active, c->ctl.done};
+    for (int it = 0; it < 2; ++it) {
+        double* Slab::*pin = it == 0 ? &Slab::p0 : &Slab::p1;
+        double* Slab::*pout = it == 0 ? &Slab::p1 : &Slab::p0;
+        double* Slab::*rin = it == 0 ? &Slab::r0 : &Slab::r1;
+        double* Slab::*rout = it == 0 ? &Slab::r1 : &Slab::r0;
+        long long k;
+        TRY(blk_cgp(rc, pin, pout, &k));
+        TRY(finish_dots(c, SM_ALPHA, R, k, pout == &Slab::p1 ? 1 : 0));
+        TRY(blk_restrict(rc, rin, rout, &k));
+        TRY(finish_dots(c, SM_CONV, R, k, 0, tol));
+        int cw;
+        TRY(coarse_cycle(rc, &cw));
+        TRY(blk_post(rc, rout, cw, &k));
+        TRY(finish_dots(c, SM_BETA, R, k));
+    }
+    return MG_OK;
+}
+
+static mg_status record_true(mg_ctx* c, int R) {
+    for (Slab& s : c->sl) {
+        cg_flush_x(s.vs, R, c->ctl, s.p0, s.p1, s.x, c->stream);
+        c->launches++;
+    }
+    TRY(xchg(c, [&](const Slab& s) { return fine_field(c, s, s.x, R); }));
+    Rec all{c, R, nullptr, nullptr};
+    for (Slab& s : c->sl) {
+        FineArgs a = fine_args(c, s, all);
+        a.x = s.x; a.b = s.b; a.y = s.t;
+        level0_apply(c, s, FOP_RESID, a);
+        c->launches++;
+    }
+    return dot_finish(c, R, &Slab::t, &Slab::t, SM_TRUE);
+}
+
 static mg_status build_graphs(mg_ctx* c, int R, double tol) {
     for (cudaGraphExec_t* g : {&c->g_init, &c->g_restart, &c->g_iter, &c->g_true})
         if (*g) { cudaGraphExecDestroy(*g); *g = nullptr; }
-    const long long n = c->vs;
-    const int vb = vec_blocks(n);
-    Rec rc{c, R, c->ctl.active, c->ctl.done};
-    // ---- restart / initial preconditioning
     TRY(capture_begin(c));
-    {
-        blk_restrict(rc, c->r1, c->r0);
-        double* ec = coarse_cycle(rc);
-        const int k = blk_post(rc, c->r0, ec);
-        cg_scalars(SM_RZ0, R, c->partial, k, c->ctl, 0.0, c->stream);
-    }
+    TRY(captured(c, record_restart(c, R)));
     TRY(capture_end(c, &c->g_restart, &c->n_restart));
-    // ---- init
     TRY(capture_begin(c));
-    vec_dot(n, R, c->b, c->b, c->partial, nullptr, nullptr, c->stream);
-    cg_scalars(SM_BB, R, c->partial, vb, c->ctl, 0.0, c->stream);
-    CU(cudaMemsetAsync(c->x, 0, sizeof(double) * n * R, c->stream));
-    CU(cudaMemsetAsync(c->p0, 0, sizeof(double) * n * R, c->stream));
-    CU(cudaMemsetAsync(c->q, 0, sizeof(double) * n * R, c->stream));
-    CU(cudaMemcpyAsync(c->r1, c->b, sizeof(double) * n * R, cudaMemcpyDeviceToDevice, c->stream));
+    TRY(captured(c, [&]() -> mg_status {
+        TRY(dot_finish(c, R, &Slab::b, &Slab::b, SM_BB));
+        for (Slab& s : c->sl) {
+            CU(cudaMemsetAsync(s.x, 0, sizeof(double) * s.vs * R, c->stream));
+            CU(cudaMemsetAsync(s.p0, 0, sizeof(double) * s.vs * R, c->stream));
+            CU(cudaMemsetAsync(s.q, 0, sizeof(double) * s.vs * R, c->stream));
+            CU(cudaMemcpyAsync(s.r1, s.b, sizeof(double) * s.vs * R, cudaMemcpyDeviceToDevice, c->stream));
+        }
+        return MG_OK;
+    }()));
     TRY(capture_end(c, &c->g_init, &c->n_init));
-    // ---- two CG iterations
     TRY(capture_begin(c));
-    for (int it = 0; it < 2; ++it) {
-        double* pin = it == 0 ? c->p0 : c->p1;
-        double* pout = it == 0 ? c->p1 : c->p0;
-        double* rin = it == 0 ? c->r0 : c->r1;
-        double* rout = it == 0 ? c->r1 : c->r0;
-        int k = blk_cgp(rc, pin, pout);
-        cg_scalars(SM_ALPHA, R, c->partial, k, c->ctl, 0.0, c->stream, pout == c->p1 ? 1 : 0);
-        k = blk_restrict(rc, rin, rout);
-        cg_scalars(SM_CONV, R, c->partial, k, c->ctl, tol, c->stream);
-        double* ec = coarse_cycle(rc);
-        k = blk_post(rc, rout, ec);
-        cg_scalars(SM_BETA, R, c->partial, k, c->ctl, 0.0, c->stream);
-    }
+    TRY(captured(c, record_iter(c, R, tol)));
     TRY(capture_end(c, &c->g_iter, &c->n_iter));
-    // ---- true residual
     TRY(capture_begin(c));
-    {
-        cg_flush_x(n, R, c->ctl, c->p0, c->p1, c->x, c->stream);
-        Rec all{c, R, nullptr, nullptr};
-        FineArgs a = fine_args(c, all);
-        a.x = c->x; a.b = c->b; a.y = c->t;
-        level0_apply(c, FOP_RESID, a);
-        vec_dot(n, R, c->t, c->t, c->partial, nullptr, nullptr, c->stream);
-        cg_scalars(SM_TRUE, R, c->partial, vb, c->ctl, 0.0, c->stream);
-    }
+    TRY(captured(c, record_true(c, R)));
     TRY(capture_end(c, &c->g_true, &c->n_true));
     c->graph_R = R;
     CHECK_LAUNCH();
+    return MG_OK;
+}
+
+// ---------------------------------------------------------------- setup
+static mg_status setup_impl(mg_ctx* c, const mg_grid* grid, const double* E_e, const uint8_t* fixed, int levels,
+                            const mg_opts* opts, const mg_dist* dist, void* stream) {
+    c->dim = grid->dim;
+    c->L = levels;
+    c->nu = grid->nu;
+    if (opts) c->opts = *opts;
+    c->user = (cudaStream_t)stream;
+    const int rank = dist ? dist->rank : 0, nranks = dist ? dist->nranks : 1;
+    const int nsl = dist ? dist->nslab : 1;
+    c->S = nranks * nsl;
+    CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
+    if (!comm_init(c->comm, rank, nranks, dist ? dist->nccl_id : nullptr))
+        return fail(MG_ERR_NCCL, std::string("NCCL init: ") + comm_last_error());
+    stream_enter(c);
+    cudaStream_t s = c->stream;
+    const int dim = c->dim;
+    int N[3] = {grid->nel[0], grid->nel[1], dim == 3 ? grid->nel[2] : 1};
+    for (int l = 0; l < levels; ++l) {
+        int Nl[3];
+        for (int k = 0; k < 3; ++k) Nl[k] = N[k] >> l;
+        c->G[l] = make_geom(dim, Nl);
+    }
+    c->pn0 = c->G[0].nnodes / c->G[0].nn[0];
+    // partition: rank q holds slabs [q*nsl, (q+1)*nsl)
+    c->rank_p0.assign(nranks, 0);
+    c->rank_p1.assign(nranks, 0);
+    for (int q = 0; q < nranks; ++q) {
+        int a, b, d;
+        partition(N[0], levels, c->S, q * nsl, &a, &d);
+        partition(N[0], levels, c->S, q * nsl + nsl - 1, &d, &b);
+        c->rank_p0[q] = a;
+        c->rank_p1[q] = b;
+    }
+    const int rp0 = c->rank_p0[rank], rp1 = c->rank_p1[rank];
+    const long long le0 = c->G[0].nelem / N[0];   // elements per fine layer
+    c->m_rank = (long long)(rp1 - rp0) * le0;
+    c->n_rank = (long long)(rp1 - rp0 + (rank == nranks - 1 ? 1 : 0)) * c->pn0 * dim;
+    c->sl.resize(nsl);
+    for (int k = 0; k < nsl; ++k) {
+        Slab& sl = c->sl[k];
+        sl.id = rank * nsl + k;
+        partition(N[0], levels, c->S, sl.id, &sl.e0, &sl.e1);
+        sl.gl = sl.id > 0 ? 1 : 0;
+        sl.gh = sl.id < c->S - 1 ? 1 : 0;
+        sl.uoff = (long long)(sl.e0 - rp0) * c->pn0;
+        for (int l = 0; l < levels; ++l) {
+            Level& v = sl.lv[l];
+            int Nl[3];
+            for (int q = 0; q < 3; ++q) Nl[q] = N[q] >> l;
+            const int own = (sl.e1 - sl.e0) >> l;
+            Nl[0] = own + sl.gl;
+            v.g = make_geom(dim, Nl);
+            v.pn = v.g.nnodes / v.g.nn[0];
+            v.o0 = sl.gl;
+            v.o1 = sl.gl + own + (sl.gh ? 0 : 1);
+            v.gp0 = (sl.e0 >> l) - sl.gl;
+        }
+    }
+    element_stiffness(dim, c->nu, c->K0);
+    c->nu_paper = (c->nu == MG_NU_PAPER);
+    c->fused2d = (dim == 2 && levels >= 2);
+    fine_set_constants(dim, c->K0.data(), s);
+    if (dim == 2) fine2d_set_constants(c->K0.data(), s);
+    galerkin_set_constants(dim, c->K0.data(), s);
+    stress_set_constants(dim, c->nu, s);
+    const int NL = dim * (1 << dim);
+    const bool edev = is_device_ptr(E_e), fdev = is_device_ptr(fixed);
+    uint8_t* dfix = nullptr;
+    const uint8_t* fsrc = fixed;
+    if (!fdev) {
+        CU(cudaMalloc(&dfix, c->n_rank));
+        CU(cudaMemcpyAsync(dfix, fixed, c->n_rank, cudaMemcpyHostToDevice, s));
+        fsrc = dfix;
+    }
+    for (Slab& sl : c->sl) {
+        const LevelGeom& g0 = sl.lv[0].g;
+        CU(cudaMalloc(&sl.E, sizeof(double) * g0.nelem + 64));   // +64: aligned tails
+        CU(cudaMemsetAsync(sl.E, 0, sizeof(double) * g0.nelem, s));
+        for (int l = 0; l < levels; ++l) {
+            Level& v = sl.lv[l];
+            CU(cudaMalloc(&v.mask, v.g.nnodes + 64));
+            CU(cudaMemsetAsync(v.mask, 0, v.g.nnodes, s));
+            CU(cudaMalloc(&v.Dinv, sizeof(double) * v.g.ndof));
+            CU(cudaMalloc(&v.D, sizeof(double) * v.g.ndof));
+            if (l >= 1 || levels == 1) {
+                const int ns = dim == 2 ? 9 : 27;
+                CU(cudaMalloc(&v.st, sizeof(double) * v.g.nnodes * ns * dim * dim));
+            }
+        }
+        // element-matrix ping-pong buffers (level 1 in A, level 2 in B, ...)
+        const long long nA = levels >= 2 ? sl.lv[1].g.nelem : (levels == 1 ? g0.nelem : 1);
+        const long long nB = levels >= 3 ? sl.lv[2].g.nelem : 1;
+        CU(cudaMalloc(&sl.elmA, sizeof(double) * nA * NL * NL));
+        CU(cudaMalloc(&sl.elmB, sizeof(double) * nB * NL * NL));
+        // owned fixed planes -> fine mask
+        const Level& v0 = sl.lv[0];
+        const long long cnt = (long long)(v0.o1 - v0.o0) * v0.pn;
+        fixed_to_mask_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(cnt, dim, fsrc, sl.uoff, v0.mask,
+                                                                            v0.o0 * v0.pn);
+        c->launches++;
+        CHECK_LAUNCH();
+    }
+    TRY(xchg(c, [&](const Slab& sl) { return node_field(sl, 0, sl.lv[0].mask, 1, 1, 0, 1); }));
+    for (int l = 1; l < levels; ++l) {
+        for (Slab& sl : c->sl) {
+            coarse_mask_kernel<<<(unsigned)((sl.lv[l].g.nnodes + 255) / 256), 256, 0, s>>>(
+                sl.lv[l - 1].g, sl.lv[l].g, sl.lv[l - 1].mask, sl.lv[l].mask, sl.gl);
+            c->launches++;
+        }
+        CHECK_LAUNCH();
+        TRY(xchg(c, [&](const Slab& sl) { return node_field(sl, l, sl.lv[l].mask, 1, 1, 0, 1); }));
+    }
+    if (dfix) CU(cudaFreeAsync(dfix, s));
+    for (Slab& sl : c->sl) {
+        const LevelGeom& g0 = sl.lv[0].g;
+        const long long le = g0.nelem / g0.N[0];
+        CU(cudaMemcpyAsync(sl.E + sl.gl * le, E_e + (long long)(sl.e0 - rp0) * le,
+                           sizeof(double) * (sl.e1 - sl.e0) * le,
+                           edev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+        if (dim == 2) {
+            sl.pd = pad2_layout(g0);
+            CU(cudaMalloc(&sl.Epad, sizeof(double) * sl.pd.elems));
+            CU(cudaMalloc(&sl.maskpad, sl.pd.nodes));
+            CU(cudaMalloc(&sl.Dinvpad, sizeof(double) * 2 * sl.pd.nodes));
+            sl.vs = sl.pd.vstride;
+        } else {
+            sl.vs = g0.ndof;
+        }
+    }
+    const LevelGeom& gL = c->G[levels - 1];
+    c->nL = gL.ndof;
+    c->npad = (c->nL + 31) / 32 * 32;
+    CU(cudaMalloc(&c->Ainv, sizeof(double) * c->npad * c->npad));
+    CU(cudaMalloc(&c->gj_work, sizeof(double) * (32 * 32 + 2 * c->npad * 32)));
+    if (multi(c)) {
+        const int ns = dim == 2 ? 9 : 27;
+        CU(cudaMalloc(&c->stg, sizeof(double) * gL.nnodes * ns * dim * dim));
+        if (nranks > 1) {
+            // per rank: at most (largest rank's coarsest planes) x plane x max(ns d^2, MG_MAX_RHS d)
+            int maxp = 0;
+            const int f = 1 << (levels - 1);
+            for (int q = 0; q < nranks; ++q) maxp = std::max(maxp, (c->rank_p1[q] - c->rank_p0[q]) / f + 1);
+            const long long pnL = gL.nnodes / gL.nn[0];
+            c->cpack_cap = (long long)maxp * pnL * std::max(ns * dim * dim, MG_MAX_RHS * dim);
+            CU(cudaMalloc(&c->cpack, sizeof(double) * c->cpack_cap));
+            CU(cudaMalloc(&c->cgath, sizeof(double) * c->cpack_cap * nranks));
+            CU(cudaMalloc(&c->sums, sizeof(double) * MG_MAX_RHS));
+        }
+    }
+    // control block
+    const int MR = MG_MAX_RHS;
+    size_t bytes = sizeof(double) * 8 * MR + sizeof(int) * (4 * MR + 4);
+    CU(cudaMalloc(&c->ctl_mem, bytes));
+    CU(cudaMemsetAsync(c->ctl_mem, 0, bytes, s));
+    double* dp = (double*)c->ctl_mem;
+    c->ctl.alpha = dp; c->ctl.beta = dp + MR; c->ctl.rz = dp + 2 * MR; c->ctl.rr = dp + 3 * MR;
+    c->ctl.bb = dp + 4 * MR; c->ctl.pq = dp + 5 * MR; c->ctl.tt = dp + 6 * MR; c->ctl.xalpha = dp + 7 * MR;
+    int* ip = (int*)(dp + 8 * MR);
+    c->ctl.active = ip; c->ctl.iters = ip + MR; c->ctl.xbuf = ip + 2 * MR;
+    c->ctl.done = ip + 3 * MR; c->ctl.status = ip + 3 * MR + 1;
+    c->d_status = ip + 3 * MR + 2;
+    CU(cudaMallocHost(&c->h_pinned, sizeof(int) * (2 * MR + 4)));
+    CU(cudaMallocHost(&c->h_dbl, sizeof(double) * 4 * MR));
+    TRY(compute_operators(c));
+    stream_leave(c);
     return MG_OK;
 }
 
@@ -590,97 +1157,23 @@ const char* mg_last_error(void) { return g_last_error.c_str(); }
 
 long long mg_kernel_launches(mg_handle h) { return h ? h->launches : -1; }
 
-static mg_status setup_impl(mg_ctx* c, const mg_grid* grid, const double* E_e, const uint8_t* fixed, int levels,
-                            const mg_opts* opts, void* stream) {
-    c->dim = grid->dim;
-    c->L = levels;
-    c->nu = grid->nu;
-    if (opts) c->opts = *opts;
-    c->user = (cudaStream_t)stream;
-    CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    CU(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
-    CU(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
-    stream_enter(c);
-    cudaStream_t s = c->stream;
-    int N[3] = {grid->nel[0], grid->nel[1], grid->dim == 3 ? grid->nel[2] : 1};
-    for (int l = 0; l < levels; ++l) {
-        int Nl[3];
-        for (int k = 0; k < 3; ++k) Nl[k] = N[k] >> l;
-        c->lv[l].g = make_geom(c->dim, Nl);
-    }
-    element_stiffness(c->dim, c->nu, c->K0);
-    c->nu_paper = (c->nu == MG_NU_PAPER);
-    c->fused2d = (c->dim == 2 && levels >= 2);
-    fine_set_constants(c->dim, c->K0.data(), s);
-    if (c->dim == 2) fine2d_set_constants(c->K0.data(), s);
-    galerkin_set_constants(c->dim, c->K0.data(), s);
-    stress_set_constants(c->dim, c->nu, s);
-    const LevelGeom& g0 = G0(c);
-    CU(cudaMalloc(&c->E, sizeof(double) * g0.nelem + 64));   // +64: aligned bulk-copy tails
-    CU(cudaMemcpyAsync(c->E, E_e, sizeof(double) * g0.nelem,
-                       is_device_ptr(E_e) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
-    for (int l = 0; l < levels; ++l) {
-        Level& v = c->lv[l];
-        CU(cudaMalloc(&v.mask, v.g.nnodes + 64));
-        CU(cudaMalloc(&v.Dinv, sizeof(double) * v.g.ndof));
-        CU(cudaMalloc(&v.D, sizeof(double) * v.g.ndof));
-        if (l >= 1 || levels == 1) {
-            const int ns = c->dim == 2 ? 9 : 27;
-            CU(cudaMalloc(&v.st, sizeof(double) * v.g.nnodes * ns * c->dim * c->dim));
-        }
-    }
-    {
-        uint8_t* dfix = nullptr;
-        const uint8_t* fsrc = fixed;
-        if (!is_device_ptr(fixed)) {
-            CU(cudaMallocAsync(&dfix, g0.ndof, s));
-            CU(cudaMemcpyAsync(dfix, fixed, g0.ndof, cudaMemcpyHostToDevice, s));
-            fsrc = dfix;
-        }
-        fixed_to_mask_kernel<<<(unsigned)((g0.nnodes + 255) / 256), 256, 0, s>>>(g0.nnodes, c->dim, fsrc,
-                                                                                 c->lv[0].mask);
-        CHECK_LAUNCH();
-        if (dfix) CU(cudaFreeAsync(dfix, s));
-    }
-    for (int l = 1; l < levels; ++l) {
-        coarse_mask_kernel<<<(unsigned)((c->lv[l].g.nnodes + 255) / 256), 256, 0, s>>>(
-            c->lv[l - 1].g, c->lv[l].g, c->lv[l - 1].mask, c->lv[l].mask);
-        CHECK_LAUNCH();
-    }
-    c->launches += levels;
-    if (c->dim == 2) {
-        c->pd = pad2_layout(g0);
-        CU(cudaMalloc(&c->Epad, sizeof(double) * c->pd.elems));
-        CU(cudaMalloc(&c->maskpad, c->pd.nodes));
-        CU(cudaMalloc(&c->Dinvpad, sizeof(double) * 2 * c->pd.nodes));
-        c->vs = c->pd.vstride;
-    } else {
-        c->vs = g0.ndof;
-    }
-    c->nL = c->lv[levels - 1].g.ndof;
-    c->npad = (c->nL + 31) / 32 * 32;
-    CU(cudaMalloc(&c->Ainv, sizeof(double) * c->npad * c->npad));
-    // control block
-    const int MR = MG_MAX_RHS;
-    size_t bytes = sizeof(double) * 8 * MR + sizeof(int) * (4 * MR + 4);
-    CU(cudaMalloc(&c->ctl_mem, bytes));
-    CU(cudaMemsetAsync(c->ctl_mem, 0, bytes, s));
-    double* dp = (double*)c->ctl_mem;
-    c->ctl.alpha = dp; c->ctl.beta = dp + MR; c->ctl.rz = dp + 2 * MR; c->ctl.rr = dp + 3 * MR;
-    c->ctl.bb = dp + 4 * MR; c->ctl.pq = dp + 5 * MR; c->ctl.tt = dp + 6 * MR; c->ctl.xalpha = dp + 7 * MR;
-    int* ip = (int*)(dp + 8 * MR);
-    c->ctl.active = ip; c->ctl.iters = ip + MR; c->ctl.xbuf = ip + 2 * MR;
-    c->ctl.done = ip + 3 * MR; c->ctl.status = ip + 3 * MR + 1;
-    c->d_status = ip + 3 * MR + 2;
-    CU(cudaMallocHost(&c->h_pinned, sizeof(int) * (2 * MR + 4)));
-    CU(cudaMallocHost(&c->h_dbl, sizeof(double) * 4 * MR));
-    TRY(compute_operators(c));
-    stream_leave(c);
+mg_status mg_partition(const mg_grid* grid, int levels, int nparts, int part, int* e_begin, int* e_end) {
+    if (!grid || !e_begin || !e_end) return fail(MG_ERR_ARG, "NULL argument");
+    if (levels < 1 || levels > MG_MAX_LEVELS) return fail(MG_ERR_ARG, "levels out of range");
+    if (grid->nel[0] % (1 << (levels - 1))) return fail(MG_ERR_NONDIVISIBLE, "nel[0] not divisible by 2^(levels-1)");
+    if (!partition(grid->nel[0], levels, nparts, part, e_begin, e_end))
+        return fail(MG_ERR_DIM, "need 0 <= part < nparts <= coarsest-level element layers");
     return MG_OK;
 }
 
-mg_status mg_setup(const mg_grid* grid, const double* E_e, const uint8_t* fixed, int levels, const mg_opts* opts,
-                   void* stream, mg_handle* out) {
+mg_status mg_nccl_unique_id(void* out128) {
+    if (!out128) return fail(MG_ERR_ARG, "NULL argument");
+    if (!comm_nccl_unique_id(out128)) return fail(MG_ERR_NCCL, comm_last_error());
+    return MG_OK;
+}
+
+mg_status mg_setup_dist(const mg_grid* grid, const double* E_e, const uint8_t* fixed, int levels, const mg_opts* opts,
+                        const mg_dist* dist, void* stream, mg_handle* out) {
     if (!grid || !E_e || !fixed || !out) return fail(MG_ERR_ARG, "NULL argument");
     if (grid->dim != 2 && grid->dim != 3) return fail(MG_ERR_ARG, "dim must be 2 or 3");
     if (levels < 1 || levels > MG_MAX_LEVELS) return fail(MG_ERR_ARG, "levels out of range");
@@ -689,6 +1182,12 @@ mg_status mg_setup(const mg_grid* grid, const double* E_e, const uint8_t* fixed,
         return fail(MG_ERR_ARG, "invalid mg_opts");
     if (opts && grid->dim == 2 && (opts->nu_pre != 1 || opts->nu_post != 1))
         return fail(MG_ERR_ARG, "2D path implements the fused V(1,1) cycle only (nu_pre = nu_post = 1)");
+    if (dist) {
+        if (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks || dist->nslab < 1)
+            return fail(MG_ERR_ARG, "invalid mg_dist");
+        if (dist->nranks > 1 && !dist->nccl_id) return fail(MG_ERR_ARG, "mg_dist.nccl_id required for nranks > 1");
+        if (dist->nranks * dist->nslab > 1 && levels < 2) return fail(MG_ERR_ARG, "slab decomposition needs levels >= 2");
+    }
     const int f = 1 << (levels - 1);
     long long nodes = 1;
     for (int k = 0; k < grid->dim; ++k) {
@@ -700,8 +1199,10 @@ mg_status mg_setup(const mg_grid* grid, const double* E_e, const uint8_t* fixed,
     long long ncoarse = grid->dim;
     for (int k = 0; k < grid->dim; ++k) ncoarse *= grid->nel[k] / f + 1;
     if (ncoarse > 20000) return fail(MG_ERR_DIM, "coarsest level too large for the dense direct solve; add levels");
+    if (dist && grid->nel[0] / f < dist->nranks * dist->nslab)
+        return fail(MG_ERR_DIM, "more slabs than coarsest-level element layers along axis 0");
     mg_ctx* c = new mg_ctx();
-    mg_status st = setup_impl(c, grid, E_e, fixed, levels, opts, stream);
+    mg_status st = setup_impl(c, grid, E_e, fixed, levels, opts, dist, stream);
     if (st != MG_OK) {
         std::string keep = g_last_error;
         mg_destroy(c);
@@ -712,11 +1213,32 @@ mg_status mg_setup(const mg_grid* grid, const double* E_e, const uint8_t* fixed,
     return MG_OK;
 }
 
+mg_status mg_setup(const mg_grid* grid, const double* E_e, const uint8_t* fixed, int levels, const mg_opts* opts,
+                   void* stream, mg_handle* out) {
+    return mg_setup_dist(grid, E_e, fixed, levels, opts, nullptr, stream, out);
+}
+
+mg_status mg_local_info(mg_handle c, long long* ndof_local, long long* nelem_local, int* e_begin, int* e_end) {
+    if (!c) return fail(MG_ERR_ARG, "NULL handle");
+    if (ndof_local) *ndof_local = c->n_rank;
+    if (nelem_local) *nelem_local = c->m_rank;
+    if (e_begin) *e_begin = c->rank_p0[c->comm.rank];
+    if (e_end) *e_end = c->rank_p1[c->comm.rank];
+    return MG_OK;
+}
+
 mg_status mg_update_modulus(mg_handle c, const double* E_e) {
     if (!c || !E_e) return fail(MG_ERR_ARG, "NULL argument");
     stream_enter(c);
-    CU(cudaMemcpyAsync(c->E, E_e, sizeof(double) * G0(c).nelem,
-                       is_device_ptr(E_e) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+    const bool edev = is_device_ptr(E_e);
+    const int rp0 = c->rank_p0[c->comm.rank];
+    for (Slab& sl : c->sl) {
+        const LevelGeom& g0 = sl.lv[0].g;
+        const long long le = g0.nelem / g0.N[0];
+        CU(cudaMemcpyAsync(sl.E + sl.gl * le, E_e + (long long)(sl.e0 - rp0) * le,
+                           sizeof(double) * (sl.e1 - sl.e0) * le,
+                           edev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+    }
     // E changes the stencils but not the masks; the masks of coarse levels may have been
     // augmented by zero-diagonal DOFs, which stay valid for the same BCs.
     TRY(compute_operators(c));
@@ -728,8 +1250,7 @@ mg_status mgcg_solve(mg_handle c, const double* rhs, int nrhs, double tol, doubl
     if (!c || !rhs || !x) return fail(MG_ERR_ARG, "NULL argument");
     if (nrhs < 1 || nrhs > MG_MAX_RHS) return fail(MG_ERR_ARG, "nrhs out of range");
     if (!(tol > 0.0) || !(tol < 1.0)) return fail(MG_ERR_ARG, "tol must be in (0,1)");
-    const LevelGeom& g0 = G0(c);
-    const long long n = g0.ndof;
+    const long long n = c->n_rank;
     cudaStream_t s = c->stream;
     stream_enter(c);
     cudaEvent_t e0, e1;
@@ -747,9 +1268,7 @@ mg_status mgcg_solve(mg_handle c, const double* rhs, int nrhs, double tol, doubl
         CU(cudaMemcpyAsync(c->stage, rhs, sizeof(double) * n * nrhs, cudaMemcpyHostToDevice, s));
         rsrc = c->stage;
     }
-    if (c->dim == 2) pad2_vectors(g0, c->pd, nrhs, c->lv[0].mask, rsrc, c->b, s);
-    else vec_mask_copy(g0.nnodes, c->dim, nrhs, c->lv[0].mask, rsrc, c->b, s);
-    c->launches += 1;
+    TRY(scatter_fine(c, rsrc, nrhs, true, &Slab::b));
     CU(cudaMemsetAsync(c->ctl.status, 0, sizeof(int), s));
     CU(cudaGraphLaunch(c->g_init, s));
     CU(cudaGraphLaunch(c->g_restart, s));
@@ -794,27 +1313,19 @@ mg_status mgcg_solve(mg_handle c, const double* rhs, int nrhs, double tol, doubl
         ++restarts;
         int* d_restart = c->ctl.active;   // active := restart flags, then r1 = t for them
         CU(cudaMemcpyAsync(d_restart, restart.data(), sizeof(int) * MG_MAX_RHS, cudaMemcpyHostToDevice, s));
-        vec_axpy_masked_restart(c->vs, nrhs, c->t, c->r1, d_restart, s);
+        for (Slab& sl : c->sl) vec_axpy_masked_restart(sl.vs, nrhs, sl.t, sl.r1, d_restart, s);
+        TRY(xchg(c, [&](const Slab& sl) { return fine_field(c, sl, sl.r1, nrhs); }));
         CU(cudaMemsetAsync(c->ctl.alpha, 0, sizeof(double) * MG_MAX_RHS, s));
         int zero = 0;
         CU(cudaMemcpyAsync(c->ctl.done, &zero, sizeof(int), cudaMemcpyHostToDevice, s));
         CU(cudaGraphLaunch(c->g_restart, s));
         ++glaunch;
-        klaunch += c->n_restart + 1;
+        klaunch += c->n_restart + nslab(c);
     }
     // copy x out
-    if (c->dim == 2) {
-        if (xdev) {
-            unpad2_vectors(g0, c->pd, nrhs, c->x, x, s);
-        } else {
-            unpad2_vectors(g0, c->pd, nrhs, c->x, c->stage, s);
-            CU(cudaMemcpyAsync(x, c->stage, sizeof(double) * n * nrhs, cudaMemcpyDeviceToHost, s));
-        }
-    } else if (xdev) {
-        CU(cudaMemcpyAsync(x, c->x, sizeof(double) * n * nrhs, cudaMemcpyDeviceToDevice, s));
-    } else {
-        CU(cudaMemcpyAsync(x, c->x, sizeof(double) * n * nrhs, cudaMemcpyDeviceToHost, s));
-    }
+    double* xdst = xdev ? x : c->stage;
+    TRY(gather_fine(c, &Slab::x, nrhs, xdst));
+    if (!xdev) CU(cudaMemcpyAsync(x, c->stage, sizeof(double) * n * nrhs, cudaMemcpyDeviceToHost, s));
     CU(cudaEventRecord(e1, s));
     CU(cudaStreamSynchronize(s));
     float ms = 0.f;
@@ -855,64 +1366,119 @@ mg_status stress_stiffness_apply(mg_handle c, const double* Es_e, const double* 
                                  double* y) {
     if (!c || !Es_e || !u || !phi || !y) return fail(MG_ERR_ARG, "NULL argument");
     if (nphi < 1) return fail(MG_ERR_ARG, "nphi must be >= 1");
-    const LevelGeom& g0 = G0(c);
     cudaStream_t s = c->stream;
+    const int dim = c->dim;
+    const int nv = dim == 2 ? 3 : 6;
     stream_enter(c);
-    const int nv = c->dim == 2 ? 3 : 6;
-    if (!c->sig) CU(cudaMalloc(&c->sig, sizeof(double) * g0.nelem * nv));
     const bool dev = is_device_ptr(phi) && is_device_ptr(y) && is_device_ptr(u) && is_device_ptr(Es_e);
-    const long long n = g0.ndof;
-    if (dev) {
-        stress_sigma(g0, Es_e, u, c->sig, s);
-        stress_apply(g0, c->sig, c->lv[0].mask, phi, y, nphi, s);
+    if (!multi(c) && dev) {   // one slab, device buffers: direct
+        Slab& sl = c->sl[0];
+        const LevelGeom& g0 = sl.lv[0].g;
+        if (!sl.sig) CU(cudaMalloc(&sl.sig, sizeof(double) * g0.nelem * nv));
+        stress_sigma(g0, Es_e, u, sl.sig, s);
+        stress_apply(g0, sl.sig, sl.lv[0].mask, phi, y, nphi, s);
         c->launches += 2;
         CHECK_LAUNCH();
         stream_leave(c);
         return MG_OK;
     }
-    // host buffers: stage through device temporaries (synchronous)
+    // general path: this rank's owned planes -> slab-local compact arrays (+ ghosts) -> kernels
+    // -> owned planes back.  Host buffers are staged (synchronous).
+    const long long n = c->n_rank, m = c->m_rank;
     double *dEs = nullptr, *du = nullptr, *dphi = nullptr, *dy = nullptr;
-    CU(cudaMallocAsync(&dEs, sizeof(double) * g0.nelem, s));
-    CU(cudaMallocAsync(&du, sizeof(double) * n, s));
-    CU(cudaMallocAsync(&dphi, sizeof(double) * n * nphi, s));
-    CU(cudaMallocAsync(&dy, sizeof(double) * n * nphi, s));
-    CU(cudaMemcpyAsync(dEs, Es_e, sizeof(double) * g0.nelem, cudaMemcpyDefault, s));
-    CU(cudaMemcpyAsync(du, u, sizeof(double) * n, cudaMemcpyDefault, s));
-    CU(cudaMemcpyAsync(dphi, phi, sizeof(double) * n * nphi, cudaMemcpyDefault, s));
-    stress_sigma(g0, dEs, du, c->sig, s);
-    stress_apply(g0, c->sig, c->lv[0].mask, dphi, dy, nphi, s);
-    c->launches += 2;
+    const double *Es_src = Es_e, *u_src = u, *phi_src = phi;
+    if (!dev) {
+        CU(cudaMallocAsync(&dEs, sizeof(double) * m, s));
+        CU(cudaMallocAsync(&du, sizeof(double) * n, s));
+        CU(cudaMallocAsync(&dphi, sizeof(double) * n * nphi, s));
+        CU(cudaMallocAsync(&dy, sizeof(double) * n * nphi, s));
+        CU(cudaMemcpyAsync(dEs, Es_e, sizeof(double) * m, cudaMemcpyDefault, s));
+        CU(cudaMemcpyAsync(du, u, sizeof(double) * n, cudaMemcpyDefault, s));
+        CU(cudaMemcpyAsync(dphi, phi, sizeof(double) * n * nphi, cudaMemcpyDefault, s));
+        Es_src = dEs; u_src = du; phi_src = dphi;
+    }
+    double* y_dst = dev ? y : dy;
+    const int rp0 = c->rank_p0[c->comm.rank];
+    for (Slab& sl : c->sl) {
+        const Level& v = sl.lv[0];
+        const long long nd = v.g.ndof;
+        if (!sl.sig) CU(cudaMalloc(&sl.sig, sizeof(double) * v.g.nelem * nv));
+        if (!sl.u) CU(cudaMalloc(&sl.u, sizeof(double) * nd));
+        if (sl.gphi_cap < nphi) {
+            if (sl.phi) cudaFree(sl.phi);
+            if (sl.gy) cudaFree(sl.gy);
+            CU(cudaMalloc(&sl.phi, sizeof(double) * nd * nphi));
+            CU(cudaMalloc(&sl.gy, sizeof(double) * nd * nphi));
+            sl.gphi_cap = nphi;
+        }
+        CU(cudaMemsetAsync(sl.u, 0, sizeof(double) * nd, s));
+        CU(cudaMemsetAsync(sl.phi, 0, sizeof(double) * nd * nphi, s));
+        const long long pl = v.pn * dim, np = v.o1 - v.o0;
+        CU(cudaMemcpyAsync(sl.u + v.o0 * pl, u_src + dim * sl.uoff, sizeof(double) * np * pl,
+                           cudaMemcpyDeviceToDevice, s));
+        CU(cudaMemcpy2DAsync(sl.phi + v.o0 * pl, nd * 8, phi_src + dim * sl.uoff, n * 8, np * pl * 8, nphi,
+                             cudaMemcpyDeviceToDevice, s));
+        // stress moduli of the owned element layers (ghost layer below by exchange)
+        const long long le = v.g.nelem / v.g.N[0];
+        if (!sl.Es) CU(cudaMalloc(&sl.Es, sizeof(double) * v.g.nelem));
+        CU(cudaMemsetAsync(sl.Es, 0, sizeof(double) * v.g.nelem, s));
+        CU(cudaMemcpyAsync(sl.Es + sl.gl * le, Es_src + (long long)(sl.e0 - rp0) * le,
+                           sizeof(double) * (sl.e1 - sl.e0) * le, cudaMemcpyDeviceToDevice, s));
+    }
+    TRY(xchg(c, [&](const Slab& sl) { return vec_field(c, sl, 0, sl.u, 1); }));
+    TRY(xchg(c, [&](const Slab& sl) { return vec_field(c, sl, 0, sl.phi, nphi); }));
+    TRY(xchg(c, [&](const Slab& sl) { return elem_field(sl, 0, sl.Es, 1); }));
+    for (Slab& sl : c->sl) {
+        const Level& v = sl.lv[0];
+        stress_sigma(v.g, sl.Es, sl.u, sl.sig, s);
+        stress_apply(v.g, sl.sig, v.mask, sl.phi, sl.gy, nphi, s);
+        c->launches += 2;
+        const long long pl = v.pn * dim, np = v.o1 - v.o0;
+        CU(cudaMemcpy2DAsync(y_dst + dim * sl.uoff, n * 8, sl.gy + v.o0 * pl, v.g.ndof * 8, np * pl * 8, nphi,
+                             cudaMemcpyDeviceToDevice, s));
+    }
     CHECK_LAUNCH();
-    CU(cudaMemcpyAsync(y, dy, sizeof(double) * n * nphi, cudaMemcpyDefault, s));
-    for (double* p : {dEs, du, dphi, dy}) CU(cudaFreeAsync(p, s));
-    CU(cudaStreamSynchronize(s));
+    if (!dev) {
+        CU(cudaMemcpyAsync(y, dy, sizeof(double) * n * nphi, cudaMemcpyDefault, s));
+        for (double* p : {dEs, du, dphi, dy}) CU(cudaFreeAsync(p, s));
+        CU(cudaStreamSynchronize(s));
+    }
     stream_leave(c);
     return MG_OK;
 }
 
 mg_status mg_matvec(mg_handle c, int level, const double* x, int nrhs, double* y) {
     if (!c || !x || !y) return fail(MG_ERR_ARG, "NULL argument");
-    if (level < 0 || level >= c->L || nrhs < 1) return fail(MG_ERR_ARG, "bad level / nrhs");
+    if (level < 0 || level >= c->L || nrhs < 1 || nrhs > MG_MAX_RHS) return fail(MG_ERR_ARG, "bad level / nrhs");
+    if (multi(c) && level > 0) return fail(MG_ERR_ARG, "coarse-level diagnostics need a single slab");
     stream_enter(c);
     if (level == 0) {
-        FineArgs a{};
-        a.g = G0(c); a.E = c->E; a.mask = c->lv[0].mask; a.x = x; a.y = y; a.R = nrhs;
-        a.nu_paper = c->nu_paper ? 1 : 0;
-        if (c->dim == 2) {   // compact <-> padded around the march kernel
+        if (c->dim == 2 || multi(c)) {   // rank layout <-> slab layout around the fine kernels
             TRY(ensure_vectors(c, nrhs));
-            pad2_vectors(G0(c), c->pd, nrhs, nullptr, x, c->t, c->stream);
-            a.x = c->t; a.y = c->q;
-            level0_apply(c, FOP_MATVEC, a);
-            unpad2_vectors(G0(c), c->pd, nrhs, c->q, y, c->stream);
+            TRY(scatter_fine(c, x, nrhs, false, &Slab::t));
+            Rec all{c, nrhs, nullptr, nullptr};
+            for (Slab& s : c->sl) {
+                FineArgs a = fine_args(c, s, all);
+                a.x = s.t; a.y = s.q;
+                level0_apply(c, s, FOP_MATVEC, a);
+                c->launches++;
+            }
+            TRY(gather_fine(c, &Slab::q, nrhs, y));
         } else {
+            Slab& s = c->sl[0];
+            Rec all{c, nrhs, nullptr, nullptr};
+            FineArgs a = fine_args(c, s, all);
+            a.x = x; a.y = y;
             fine_apply(FOP_MATVEC, a, c->stream);
+            c->launches++;
         }
     } else {
+        Slab& s = c->sl[0];
         CoarseArgs a{};
-        a.g = c->lv[level].g; a.st = c->lv[level].st; a.x = x; a.y = y; a.R = nrhs;
+        a.g = s.lv[level].g; a.st = s.lv[level].st; a.x = x; a.y = y; a.R = nrhs;
         coarse_apply(COP_MATVEC, a, c->stream);
+        c->launches++;
     }
-    c->launches++;
     CHECK_LAUNCH();
     stream_leave(c);
     return MG_OK;
@@ -923,18 +1489,17 @@ mg_status mg_vcycle(mg_handle c, const double* r, int nrhs, double* z) {
     if (nrhs < 1 || nrhs > MG_MAX_RHS) return fail(MG_ERR_ARG, "bad nrhs");
     TRY(ensure_vectors(c, nrhs));
     stream_enter(c);
-    const long long n = G0(c).ndof;
     // the preconditioner exactly as the solve applies it (same fine blocks, alpha = 0)
-    if (c->dim == 2) pad2_vectors(G0(c), c->pd, nrhs, c->lv[0].mask, r, c->r1, c->stream);
-    else CU(cudaMemcpyAsync(c->r1, r, sizeof(double) * n * nrhs, cudaMemcpyDeviceToDevice, c->stream));
+    TRY(scatter_fine(c, r, nrhs, true, &Slab::r1));
     CU(cudaMemsetAsync(c->ctl.alpha, 0, sizeof(double) * MG_MAX_RHS, c->stream));
-    CU(cudaMemsetAsync(c->q, 0, sizeof(double) * c->vs * nrhs, c->stream));
+    for (Slab& s : c->sl) CU(cudaMemsetAsync(s.q, 0, sizeof(double) * s.vs * nrhs, c->stream));
     Rec rc{c, nrhs, nullptr, nullptr};
-    blk_restrict(rc, c->r1, c->r0);
-    double* ec = coarse_cycle(rc);
-    blk_post(rc, c->r0, ec);
-    if (c->dim == 2) unpad2_vectors(G0(c), c->pd, nrhs, c->zf, z, c->stream);
-    else CU(cudaMemcpyAsync(z, c->zf, sizeof(double) * n * nrhs, cudaMemcpyDeviceToDevice, c->stream));
+    long long k;
+    TRY(blk_restrict(rc, &Slab::r1, &Slab::r0, &k));
+    int cw;
+    TRY(coarse_cycle(rc, &cw));
+    TRY(blk_post(rc, &Slab::r0, cw, &k));
+    TRY(gather_fine(c, &Slab::zf, nrhs, z));
     c->launches += rc.launches;
     CHECK_LAUNCH();
     stream_leave(c);
@@ -944,8 +1509,10 @@ mg_status mg_vcycle(mg_handle c, const double* r, int nrhs, double* z) {
 mg_status mg_restrict(mg_handle c, int level, const double* fine, int nrhs, double* coarse) {
     if (!c || !fine || !coarse) return fail(MG_ERR_ARG, "NULL argument");
     if (level < 0 || level >= c->L - 1 || nrhs < 1) return fail(MG_ERR_ARG, "bad level / nrhs");
+    if (multi(c)) return fail(MG_ERR_ARG, "level diagnostics need a single slab");
     stream_enter(c);
-    restrict_apply(c->lv[level].g, c->lv[level + 1].g, c->lv[level].mask, c->lv[level + 1].mask, fine, coarse, nrhs,
+    Slab& s = c->sl[0];
+    restrict_apply(s.lv[level].g, s.lv[level + 1].g, s.lv[level].mask, s.lv[level + 1].mask, fine, coarse, nrhs,
                    nullptr, nullptr, c->stream);
     c->launches++;
     CHECK_LAUNCH();
@@ -956,9 +1523,11 @@ mg_status mg_restrict(mg_handle c, int level, const double* fine, int nrhs, doub
 mg_status mg_prolong(mg_handle c, int level, const double* coarse, int nrhs, double* fine) {
     if (!c || !fine || !coarse) return fail(MG_ERR_ARG, "NULL argument");
     if (level < 0 || level >= c->L - 1 || nrhs < 1) return fail(MG_ERR_ARG, "bad level / nrhs");
+    if (multi(c)) return fail(MG_ERR_ARG, "level diagnostics need a single slab");
     stream_enter(c);
-    prolong_add(c->lv[level].g, c->lv[level + 1].g, c->lv[level].mask, c->lv[level + 1].mask, coarse, fine, nrhs,
-                nullptr, nullptr, false, c->stream);
+    Slab& s = c->sl[0];
+    prolong_add(s.lv[level].g, s.lv[level + 1].g, s.lv[level].mask, s.lv[level + 1].mask, coarse, fine, nrhs, nullptr,
+                nullptr, false, c->stream);
     c->launches++;
     CHECK_LAUNCH();
     stream_leave(c);
@@ -971,16 +1540,18 @@ mg_status mg_level_info(mg_handle c, int level, int* nel3, long long* ndof, int*
     if (level < 0) return MG_OK;
     if (level >= c->L) return fail(MG_ERR_ARG, "bad level");
     if (nel3)
-        for (int k = 0; k < 3; ++k) nel3[k] = k < c->dim ? c->lv[level].g.N[k] : 0;
-    if (ndof) *ndof = c->lv[level].g.ndof;
+        for (int k = 0; k < 3; ++k) nel3[k] = k < c->dim ? c->G[level].N[k] : 0;
+    if (ndof) *ndof = c->G[level].ndof;
     return MG_OK;
 }
 
 mg_status mg_get_diagonal(mg_handle c, int level, double* d) {
     if (!c || !d) return fail(MG_ERR_ARG, "NULL argument");
     if (level < 0 || level >= c->L) return fail(MG_ERR_ARG, "bad level");
+    if (multi(c)) return fail(MG_ERR_ARG, "level diagnostics need a single slab");
     stream_enter(c);
-    CU(cudaMemcpyAsync(d, c->lv[level].D, sizeof(double) * c->lv[level].g.ndof, cudaMemcpyDeviceToDevice, c->stream));
+    CU(cudaMemcpyAsync(d, c->sl[0].lv[level].D, sizeof(double) * c->G[level].ndof, cudaMemcpyDeviceToDevice,
+                       c->stream));
     stream_leave(c);
     return MG_OK;
 }
@@ -1005,21 +1576,24 @@ mg_status mg_profile_kernels(mg_handle c, int nrhs, int reps, double* ms) {
     CU(cudaEventCreate(&e0));
     CU(cudaEventCreate(&e1));
     for (int op = 0; op < 4; ++op) {
-        auto launch = [&]() {
+        auto launch = [&]() -> mg_status {
+            long long k;
             switch (op) {
-                case 0: blk_cgp(rc, c->p0, c->p1); break;
-                case 1: blk_restrict(rc, c->r0, c->r1); break;
-                case 2: blk_post(rc, c->r1, c->L > 1 ? c->lv[1].z : nullptr); break;
-                default: {
-                    FineArgs a = fine_args(c, rc);
-                    a.x = c->p0; a.y = c->q;
-                    level0_apply(c, FOP_MATVEC, a);
-                }
+                case 0: return blk_cgp(rc, &Slab::p0, &Slab::p1, &k);
+                case 1: return blk_restrict(rc, &Slab::r0, &Slab::r1, &k);
+                case 2: return blk_post(rc, &Slab::r1, 0, &k);
+                default:
+                    for (Slab& sl : c->sl) {
+                        FineArgs a = fine_args(c, sl, rc);
+                        a.x = sl.p0; a.y = sl.q;
+                        level0_apply(c, sl, FOP_MATVEC, a);
+                    }
+                    return MG_OK;
             }
         };
-        launch();
+        TRY(launch());
         CU(cudaEventRecord(e0, s));
-        for (int k = 0; k < reps; ++k) launch();
+        for (int k = 0; k < reps; ++k) TRY(launch());
         CU(cudaEventRecord(e1, s));
         CU(cudaEventSynchronize(e1));
         float t = 0.f;
@@ -1037,24 +1611,26 @@ mg_status mg_destroy(mg_handle c) {
     if (!c) return MG_OK;
     if (c->stream) cudaStreamSynchronize(c->stream);
     free_vectors(c);
-    for (int l = 0; l < MG_MAX_LEVELS; ++l) {
-        Level& v = c->lv[l];
-        if (v.mask) cudaFree(v.mask);
-        if (v.Dinv) cudaFree(v.Dinv);
-        if (v.D) cudaFree(v.D);
-        if (v.st) cudaFree(v.st);
+    for (Slab& s : c->sl) {
+        for (int l = 0; l < MG_MAX_LEVELS; ++l) {
+            Level& v = s.lv[l];
+            if (v.mask) cudaFree(v.mask);
+            if (v.Dinv) cudaFree(v.Dinv);
+            if (v.D) cudaFree(v.D);
+            if (v.st) cudaFree(v.st);
+        }
+        for (double* p : {s.E, s.elmA, s.elmB, s.Epad, s.Dinvpad, s.u, s.phi, s.gy, s.sig, s.Es})
+            if (p) cudaFree(p);
+        if (s.maskpad) cudaFree(s.maskpad);
     }
-    if (c->E) cudaFree(c->E);
-    if (c->Epad) cudaFree(c->Epad);
-    if (c->maskpad) cudaFree(c->maskpad);
-    if (c->Dinvpad) cudaFree(c->Dinvpad);
-    if (c->Ainv) cudaFree(c->Ainv);
+    for (double* p : {c->Ainv, c->stg, c->cpack, c->cgath, c->gj_work, c->sums})
+        if (p) cudaFree(p);
     if (c->ctl_mem) cudaFree(c->ctl_mem);
-    if (c->sig) cudaFree(c->sig);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
     if (c->h_dbl) cudaFreeHost(c->h_dbl);
     if (c->ev_in) cudaEventDestroy(c->ev_in);
     if (c->ev_out) cudaEventDestroy(c->ev_out);
+    comm_destroy(c->comm);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
     return MG_OK;

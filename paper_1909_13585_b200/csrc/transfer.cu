@@ -6,10 +6,14 @@
 #include "kernels.h"
 
 // coarse(I,k) = free_c(I,k) * sum_{delta in {-1,0,1}^d} w(delta) free_f(2I+delta,k) fine(2I+delta,k)
+// Slabs: fine local plane f is coincident with coarse local plane I when f = 2I - off0, and only
+// fine planes in [fo0, fo1) (slab-owned) contribute; the coarse ghost plane above then holds a
+// partial sum that the owner adds in (reverse halo exchange).
 template <int DIM>
 __global__ void restrict_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* __restrict__ mf,
                                 const uint8_t* __restrict__ mc, const double* __restrict__ fine,
-                                double* __restrict__ coarse, int R, const int* active, const int* done) {
+                                double* __restrict__ coarse, int R, const int* active, const int* done, int off0,
+                                int fo0, int fo1) {
     long long I = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (I >= gc.nnodes) return;
     if (done && *done) return;
@@ -30,8 +34,9 @@ __global__ void restrict_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* __res
         int dl[3];
         for (int k = DIM - 1; k >= 0; --k) { dl[k] = ss % 3 - 1; ss /= 3; }
         for (int k = 0; k < DIM; ++k) {
-            int f = 2 * ci[k] + dl[k];
+            int f = 2 * ci[k] + dl[k] - (k == 0 ? off0 : 0);
             if (f < 0 || f >= gf.nn[k]) ok = false;
+            if (k == 0 && (f < fo0 || f >= fo1)) ok = false;
             q = q * gf.nn[k] + f;
             if (dl[k] != 0) w *= 0.5;
         }
@@ -59,13 +64,15 @@ __global__ void restrict_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* __res
 }
 
 void restrict_apply(const LevelGeom& gf, const LevelGeom& gc, const uint8_t* mf, const uint8_t* mc,
-                    const double* fine, double* coarse, int R, const int* active, const int* done, cudaStream_t s) {
+                    const double* fine, double* coarse, int R, const int* active, const int* done, cudaStream_t s,
+                    int off0, int fo0, int fo1) {
+    if (fo1 < 0) fo1 = gf.nn[0];
     int th = 128;
     unsigned bl = (unsigned)((gc.nnodes + th - 1) / th);
     if (gf.dim == 2)
-        restrict_kernel<2><<<bl, th, 0, s>>>(gf, gc, mf, mc, fine, coarse, R, active, done);
+        restrict_kernel<2><<<bl, th, 0, s>>>(gf, gc, mf, mc, fine, coarse, R, active, done, off0, fo0, fo1);
     else
-        restrict_kernel<3><<<bl, th, 0, s>>>(gf, gc, mf, mc, fine, coarse, R, active, done);
+        restrict_kernel<3><<<bl, th, 0, s>>>(gf, gc, mf, mc, fine, coarse, R, active, done, off0, fo0, fo1);
 }
 
 // fine(i,k) (+)= free_f(i,k) * sum_I w free_c(I,k) coarse(I,k): along each axis an even
@@ -73,13 +80,15 @@ void restrict_apply(const LevelGeom& gf, const LevelGeom& gc, const uint8_t* mf,
 template <int DIM>
 __global__ void prolong_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* __restrict__ mf,
                                const uint8_t* __restrict__ mc, const double* __restrict__ coarse,
-                               double* __restrict__ fine, int R, const int* active, const int* done, bool accumulate) {
+                               double* __restrict__ fine, int R, const int* active, const int* done, bool accumulate,
+                               int off0) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= gf.nnodes) return;
     if (done && *done) return;
     int fi[3] = {0, 0, 0};
     long long t = i;
     for (int k = DIM - 1; k >= 0; --k) { fi[k] = (int)(t % gf.nn[k]); t /= gf.nn[k]; }
+    fi[0] += off0;   // shifted so that coarse plane I is coincident with fi[0] = 2I
     const int mfb = mf[i];
     constexpr int NC = 1 << DIM;
     long long cn[NC];
@@ -121,11 +130,11 @@ __global__ void prolong_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* __rest
 
 void prolong_add(const LevelGeom& gf, const LevelGeom& gc, const uint8_t* mf, const uint8_t* mc,
                  const double* coarse, double* fine, int R, const int* active, const int* done, bool accumulate,
-                 cudaStream_t s) {
+                 cudaStream_t s, int off0) {
     int th = 128;
     unsigned bl = (unsigned)((gf.nnodes + th - 1) / th);
     if (gf.dim == 2)
-        prolong_kernel<2><<<bl, th, 0, s>>>(gf, gc, mf, mc, coarse, fine, R, active, done, accumulate);
+        prolong_kernel<2><<<bl, th, 0, s>>>(gf, gc, mf, mc, coarse, fine, R, active, done, accumulate, off0);
     else
-        prolong_kernel<3><<<bl, th, 0, s>>>(gf, gc, mf, mc, coarse, fine, R, active, done, accumulate);
+        prolong_kernel<3><<<bl, th, 0, s>>>(gf, gc, mf, mc, coarse, fine, R, active, done, accumulate, off0);
 }
