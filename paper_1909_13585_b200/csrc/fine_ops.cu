@@ -16,6 +16,8 @@
 // warp also reads rows j-1, j+1 (served by L1/L2).  The RHS index is the fastest
 // grid dimension so that the R warps working on one tile run together and E_e is
 // read from HBM once per tile.
+#include <cstdlib>
+
 #include "kernels.h"
 
 __constant__ double c_K0[576];
@@ -29,8 +31,9 @@ static constexpr int COLS_PER_WARP = 30;
 static constexpr int CHUNK2 = 32;
 static constexpr int CHUNK3 = 16;
 
-int fine_items(const LevelGeom& g) {
+int fine_items(const LevelGeom& g, int R) {
     if (g.dim == 2) return march2_items(M2_MATVEC, g, nullptr);
+    if (!getenv("MG_DENSE_H8")) return h8_items(g, R);
     int ncols = g.nn[g.dim - 1];
     int nct = (ncols + COLS_PER_WARP - 1) / COLS_PER_WARP;
     int chunk = g.dim == 2 ? CHUNK2 : CHUNK3;
@@ -216,20 +219,21 @@ static void launch_fine(const FineArgs& a, cudaStream_t s) {
     int nct = (ncols + COLS_PER_WARP - 1) / COLS_PER_WARP;
     int chunk = g.dim == 2 ? CHUNK2 : CHUNK3;
     int nch = (g.nn[0] + chunk - 1) / chunk;
-    long long warps = (long long)a.R * fine_items(g);
+    long long warps = (long long)a.R * fine_items(g, a.R);
     int wpb = 4;
     long long blocks = (warps + wpb - 1) / wpb;
     fine3d_kernel<OP><<<(unsigned)blocks, 32 * wpb, 0, s>>>(a, nct, nch);
 }
 
 int fine_apply(int op, const FineArgs& a, cudaStream_t s) {
+    if (a.g.dim == 3 && !getenv("MG_DENSE_H8")) return h8_apply(op, a, s);
     switch (op) {
         case FOP_MATVEC: launch_fine<FOP_MATVEC>(a, s); break;
         case FOP_RESID: launch_fine<FOP_RESID>(a, s); break;
         case FOP_JACOBI: launch_fine<FOP_JACOBI>(a, s); break;
         default: launch_fine<FOP_CGP>(a, s); break;
     }
-    return fine_items(a.g);
+    return fine_items(a.g, a.R);
 }
 
 // D = diag(K): sum over adjacent elements E_e K0[(a,k),(a,k)]; 1 at fixed DOFs (identity rows).

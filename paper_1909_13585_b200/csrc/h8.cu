@@ -1,0 +1,362 @@
+// 3D (H8) fine level: matrix-free element-by-element K = sum_e E_e A_e^T K0 A_e (PAPER.md:99
+// "K_e = E_kappa(x_e) K_e0"), Dirichlet rows/cols identity (reading r11),
+// fused with its consumer in the CG iteration / smoother exactly like the former dense kernel:
+//   FOP_MATVEC  y = K x
+//   FOP_RESID   y = b - K x
+//   FOP_JACOBI  y = x + omega D^-1 (b - K x), dot(b, y)
+//   FOP_CGP     p = z + beta p_in ; q = K p ; dot(p, q) ; x += xalpha p_in
+//
+// Why not dense: 24x24 per element is 576 DFMA per element x RHS, ~4x over the fp64 ridge
+// of B200 (the fine matvec moves ~50 B per element x RHS).  Here every element is applied
+// once, in the sum/difference basis of the trilinear shape functions: per axis the nodal
+// pair (v0, v1) becomes (m = v0 + v1, d = v1 - v0), in which the 1-D mass and stiffness
+// matrices are diagonal and the mixed one has a single entry, so the element matrix
+// K^ = T^-T K0 T^-1 has 45 nonzeros instead of 576 (SURVEY 7 "Hard parts" 1; closed form
+// below, pinned against K0 in tests).  The transform is separable and shared between
+// neighbouring elements: edges along axis 2 by a warp shuffle, faces along axis 1 through
+// shared memory, the axis-0 stage in registers while marching -- ~171 fp64 instructions per
+// element x RHS instead of 576.  The transposed transform scatters the element result back
+// to its 8 nodes through the same stages (no atomics, deterministic).
+//
+// Work decomposition: a CTA is a tile of 8 node rows (axis 1) x 32 node columns (axis 2),
+// one warp per row, marching along axis 0 over a chunk of node planes.  Thread (r, lane)
+// computes element (j, c) = (row, col) of each layer; owned outputs are rows 1..6 and lanes
+// 1..30 of the tile (the outer ring only feeds neighbours).  RHS index is the fastest grid
+// coordinate so the R CTAs of a tile run together and share E in L2.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+
+#include "element.cuh"
+#include "kernels.h"
+
+__constant__ double c_Kh[576];
+
+// ---------------------------------------------------------------- K^ in closed form
+// 1-D factors in the (m, d) basis (t = 0: m, t = 1: d) of the integrals of element.cuh:
+// M^ = diag(1/4, 1/12), D^ = diag(0, 1), C^[d][m] = 1/2 (derivative on the test function),
+// C^T[m][d] = 1/2.  K^[(s,i),(t,j)] = lam S^_ij + mu S^_ji + mu delta_ij sum_k S^_kk.
+__host__ __device__ constexpr double f1h(int kind, int ta, int tb) {
+    return kind == 0 ? (ta == tb ? (ta == 0 ? 0.25 : 1.0 / 12.0) : 0.0)
+         : kind == 1 ? ((ta == 1 && tb == 1) ? 1.0 : 0.0)
+         : kind == 2 ? ((ta == 1 && tb == 0) ? 0.5 : 0.0)
+                     : ((ta == 0 && tb == 1) ? 0.5 : 0.0);
+}
+
+__host__ __device__ constexpr double sh3(int i, int j, int s, int t) {
+    double v = 1.0;
+    for (int k = 0; k < 3; ++k) {
+        const int ta = (s >> (2 - k)) & 1, tb = (t >> (2 - k)) & 1;
+        const int kind = (k == i && k == j) ? 1 : (k == i ? 2 : (k == j ? 3 : 0));
+        v *= f1h(kind, ta, tb);
+    }
+    return v;
+}
+
+__host__ __device__ constexpr double khat(double nu, int row, int col) {
+    const int s = row / 3, i = row % 3, t = col / 3, j = col % 3;
+    const double mu = 1.0 / (2.0 * (1.0 + nu));
+    const double lam = nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
+    double v = lam * sh3(i, j, s, t) + mu * sh3(j, i, s, t);
+    if (i == j)
+        for (int k = 0; k < 3; ++k) v += mu * sh3(k, k, s, t);
+    return v;
+}
+
+void h8_set_constants(double nu, cudaStream_t s) {
+    static double Kh[576];
+    for (int r = 0; r < 24; ++r)
+        for (int c = 0; c < 24; ++c) Kh[r * 24 + c] = khat(nu, r, c);
+    cudaMemcpyToSymbolAsync(c_Kh, Kh, sizeof(Kh), 0, cudaMemcpyHostToDevice, s);
+}
+
+// the sparsity pattern is nu-independent; values are immediates for nu = 0.3
+template <bool C03>
+__device__ __forceinline__ double KH(int r, int c) {
+    if (C03) return khat(MG_NU_PAPER, r, c);
+    return c_Kh[r * 24 + c];
+}
+
+static constexpr int TR = 8;        // node rows per CTA (warps)
+static constexpr int TOWN_R = 6;    // owned rows
+static constexpr int TOWN_C = 30;   // owned columns
+static constexpr int HCH = 32;      // node planes per chunk
+
+struct H8Plane {              // per-thread data of one node plane
+    double raw[3];            // unmasked operator input (identity rows / dots)
+    double aux[3];            // RESID/JACOBI: b ; CGP: unused
+    double dinv[3];           // JACOBI
+    double xo[3];             // CGP: x (deferred update x += xalpha p_in)
+    double E;                 // element (P, j, c)
+    int m;                    // fixed bits
+};
+
+template <int OP, bool C03, int MINB>
+__global__ void __launch_bounds__(32 * TR, MINB) h8_kernel(FineArgs a, int ntc, int ntr, int nch, int hch) {
+    __shared__ double s_fwd[TR][6][32];   // edge (m, d) x 3 comps of plane P, per row
+    __shared__ double s_inv[TR][6][32];   // inverse edge contributions for row + 1
+    const int lane = threadIdx.x & 31, row = threadIdx.x >> 5;
+    const int nt = ntc * ntr;
+    const int bid = blockIdx.x;
+    const int R = a.R;
+    const int r = bid % R;
+    const int tile = bid / R;
+    if (tile >= nt * nch) return;
+    if (a.done && *a.done) return;
+    if (a.active && !a.active[r]) return;
+    const int tc = tile % ntc, tr = (tile / ntc) % ntr, ch = tile / nt;
+    const int n0 = a.g.nn[0], n1 = a.g.nn[1], n2 = a.g.nn[2];
+    const int N0 = a.g.N[0], N1 = a.g.N[1], N2 = a.g.N[2];
+    const int j = tr * TOWN_R - 1 + row;
+    const int c = tc * TOWN_C - 1 + lane;
+    const bool node_ok = j >= 0 && j < n1 && c >= 0 && c < n2;
+    const bool elem_jc = j >= 0 && j < N1 && c >= 0 && c < N2 && row < TR - 1 && lane < 31;
+    const bool own = node_ok && row >= 1 && row <= TOWN_R && lane >= 1 && lane <= TOWN_C;
+    const int i0 = ch * hch, i1 = min(i0 + hch, n0);
+    const long long vbase = (long long)r * a.g.ndof;
+    const long long col = (long long)j * n2 + c;          // node offset within a plane
+    const long long ecol = (long long)j * N2 + c;         // element offset within a layer
+    const long long pstride = (long long)n1 * n2, estride = (long long)N1 * N2;
+    const double beta = (OP == FOP_CGP) ? a.beta[r] : 0.0;
+    const double xal = (OP == FOP_CGP && a.xv) ? a.xalpha[r] : 0.0;
+
+    auto load = [&](H8Plane& q, int P) {
+        q.E = 0.0;
+        if (elem_jc && P >= 0 && P < N0) q.E = a.E[(long long)P * estride + ecol];
+        if (!(node_ok && P >= 0 && P < n0)) {
+            q.m = 7;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) q.raw[k] = q.aux[k] = q.dinv[k] = 0.0;
+            return;
+        }
+        const long long nd = (long long)P * pstride + col;
+        const long long o = vbase + 3 * nd;
+        q.m = a.mask[nd];
+        if (OP == FOP_CGP) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const double pin = a.pin[o + k];
+                q.raw[k] = fma(beta, pin, a.z[o + k]);
+                q.aux[k] = pin;
+                if (a.xv) q.xo[k] = a.xv[o + k];
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) q.raw[k] = a.x[o + k];
+        }
+        if (OP == FOP_RESID || OP == FOP_JACOBI) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) q.aux[k] = a.b[o + k];
+        }
+        if (OP == FOP_JACOBI) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) q.dinv[k] = a.Dinv[3 * nd + k];
+        }
+    };
+
+    // forward stages of plane P: edges along axis 2 (shuffle), faces along axis 1 (smem)
+    auto forward = [&](const H8Plane& q, double (&F)[3][4]) {
+        double em[3], ed[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const double u = ((q.m >> k) & 1) ? 0.0 : q.raw[k];
+            const double un = __shfl_down_sync(MGK_FULL, u, 1);
+            em[k] = u + un;
+            ed[k] = un - u;
+            s_fwd[row][k][lane] = em[k];
+            s_fwd[row][3 + k][lane] = ed[k];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const double em1 = row < TR - 1 ? s_fwd[row + 1][k][lane] : 0.0;
+            const double ed1 = row < TR - 1 ? s_fwd[row + 1][3 + k][lane] : 0.0;
+            F[k][0] = em[k] + em1;   // (m_j, m_c)
+            F[k][1] = ed[k] + ed1;   // (m_j, d_c)
+            F[k][2] = em1 - em[k];   // (d_j, m_c)
+            F[k][3] = ed1 - ed[k];   // (d_j, d_c)
+        }
+    };
+
+    double FL[3][4], CY[3][4];
+    H8Plane cur, nxt;
+    double dot = 0.0;
+    // prologue: plane i0-1 (its face; element layer i0-1 is added in the first step)
+    load(cur, i0 - 1);
+    forward(cur, FL);
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int f = 0; f < 4; ++f) CY[k][f] = 0.0;
+    load(nxt, i0);
+    for (int L = i0 - 1; L < i1; ++L) {
+        const int P = L + 1;
+        H8Plane pl = nxt;                       // plane P
+        H8Plane lo = cur;                       // plane L
+        if (P + 1 <= i1) load(nxt, P + 1);      // prefetch
+        if (OP == FOP_CGP && own && P >= i0 && P < i1) {
+            const long long o = vbase + 3 * ((long long)P * pstride + col);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                a.pout[o + k] = pl.raw[k];
+                if (a.xv) a.xv[o + k] = fma(xal, pl.aux[k], pl.xo[k]);   // deferred x += alpha p_in
+            }
+        }
+        // (no barrier needed here: every thread passed the previous step's second barrier,
+        // so all reads of s_fwd of that step are complete)
+        double FP[3][4];
+        forward(pl, FP);
+        // element (L, j, c): u^ = E * (T u) ; y^ = K^ u^ ; back to the two faces
+        double GL[3][4];
+        if (row == TR - 1) {   // top halo row: feeds row TR-2's faces only (warp-uniform)
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+#pragma unroll
+                for (int f = 0; f < 4; ++f) GL[k][f] = 0.0;
+        } else {
+            const double Ee = lo.E;   // E of element layer L, loaded with plane L
+            double uh[24], yh[24];
+#pragma unroll
+            for (int f = 0; f < 4; ++f)
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    uh[3 * f + k] = Ee * (FL[k][f] + FP[k][f]);          // t0 = m
+                    uh[3 * (4 + f) + k] = Ee * (FP[k][f] - FL[k][f]);    // t0 = d
+                }
+#pragma unroll
+            for (int rr = 0; rr < 24; ++rr) {
+                double acc = 0.0;
+#pragma unroll
+                for (int cc = 0; cc < 24; ++cc)
+                    if (khat(MG_NU_PAPER, rr, cc) != 0.0) acc = fma(KH<C03>(rr, cc), uh[cc], acc);
+                yh[rr] = acc;
+            }
+#pragma unroll
+            for (int f = 0; f < 4; ++f)
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const double ym = yh[3 * f + k], yd = yh[3 * (4 + f) + k];
+                    GL[k][f] = CY[k][f] + (ym - yd);   // face L total
+                    CY[k][f] = ym + yd;                // carried to face P
+                }
+        }
+        // face L -> edges of rows j (own) and j+1 (neighbour) -> nodes
+        double eo[3][2];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int t2 = 0; t2 < 2; ++t2) {
+                const double fm = GL[k][t2], fd = GL[k][2 + t2];
+                eo[k][t2] = fm - fd;
+                s_inv[row][2 * k + t2][lane] = fm + fd;
+            }
+        __syncthreads();
+        double y[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const double em = eo[k][0] + (row > 0 ? s_inv[row - 1][2 * k][lane] : 0.0);
+            const double ed = eo[k][1] + (row > 0 ? s_inv[row - 1][2 * k + 1][lane] : 0.0);
+            const double up = __shfl_up_sync(MGK_FULL, em + ed, 1);   // node c+1 part of lane-1
+            y[k] = (em - ed) + up;
+        }
+        if (own && L >= i0) {
+            const long long nd = (long long)L * pstride + col;
+            const long long o = vbase + 3 * nd;
+            const bool sdot = L >= a.so0 && L < a.so1;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const double ax = ((lo.m >> k) & 1) ? lo.raw[k] : y[k];
+                double out;
+                if (OP == FOP_MATVEC || OP == FOP_CGP) out = ax;
+                else if (OP == FOP_RESID) out = lo.aux[k] - ax;
+                else out = fma(a.omega * lo.dinv[k], lo.aux[k] - ax, lo.raw[k]);
+                if (OP == FOP_JACOBI && sdot) dot = fma(lo.aux[k], out, dot);
+                if (OP == FOP_CGP && sdot) dot = fma(lo.raw[k], ax, dot);
+                a.y[o + k] = out;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int f = 0; f < 4; ++f) FL[k][f] = FP[k][f];
+        cur = pl;
+    }
+    if (a.partial) {
+        dot = warp_sum(dot);
+        __shared__ double s_dot[TR];
+        if (lane == 0) s_dot[row] = dot;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+#pragma unroll
+            for (int w = 0; w < TR; ++w) t += s_dot[w];
+            a.partial[(long long)r * a.pstride + tile] = t;
+        }
+    }
+}
+
+static int h8_minb() {
+    static int v = [] {
+        const char* e = getenv("MG_H8_MINB");
+        return e && atoi(e) == 2 ? 2 : 1;
+    }();
+    return v;
+}
+
+// Chunking along axis 0: between HCH/2 and 2 HCH planes per chunk, picked so that the CTA
+// count fills the resident slots (148 SMs x CTAs per SM) with the smallest tail wave.
+static void h8_chunks(const LevelGeom& g, int R, int* nch_out, int* hch_out) {
+    const int ntc = (g.nn[2] + TOWN_C - 1) / TOWN_C;
+    const int ntr = (g.nn[1] + TOWN_R - 1) / TOWN_R;
+    const long long slots = 148LL * h8_minb();
+    const int n0 = g.nn[0];
+    int best = (n0 + HCH - 1) / HCH;
+    double best_eff = -1.0;
+    for (int nch = std::max(1, n0 / (2 * HCH)); nch <= std::max(1, 2 * n0 / HCH); ++nch) {
+        const int hch = (n0 + nch - 1) / nch;
+        const int nc = (n0 + hch - 1) / hch;
+        const long long ctas = (long long)ntc * ntr * nc * R;
+        const double waves = (double)ctas / slots;
+        const double fill = waves / std::ceil(waves);
+        const double eff = fill * hch / (hch + 1.0);   // + one prologue plane per chunk
+        if (eff > best_eff + 1e-9) { best_eff = eff; best = nc; }
+    }
+    *nch_out = best;
+    *hch_out = (n0 + best - 1) / best;
+}
+
+int h8_items(const LevelGeom& g, int R) {
+    const int ntc = (g.nn[2] + TOWN_C - 1) / TOWN_C;
+    const int ntr = (g.nn[1] + TOWN_R - 1) / TOWN_R;
+    int nch, hch;
+    h8_chunks(g, R, &nch, &hch);
+    return ntc * ntr * nch;
+}
+
+template <int OP>
+static void launch_h8(const FineArgs& a, cudaStream_t s) {
+    const LevelGeom& g = a.g;
+    const int ntc = (g.nn[2] + TOWN_C - 1) / TOWN_C;
+    const int ntr = (g.nn[1] + TOWN_R - 1) / TOWN_R;
+    int nch, hch;
+    h8_chunks(g, a.R, &nch, &hch);
+    const long long blocks = (long long)ntc * ntr * nch * a.R;
+    const unsigned nb = (unsigned)blocks;
+    if (h8_minb() == 1) {
+        if (a.nu_paper) h8_kernel<OP, true, 1><<<nb, 32 * TR, 0, s>>>(a, ntc, ntr, nch, hch);
+        else h8_kernel<OP, false, 1><<<nb, 32 * TR, 0, s>>>(a, ntc, ntr, nch, hch);
+    } else {
+        if (a.nu_paper) h8_kernel<OP, true, 2><<<nb, 32 * TR, 0, s>>>(a, ntc, ntr, nch, hch);
+        else h8_kernel<OP, false, 2><<<nb, 32 * TR, 0, s>>>(a, ntc, ntr, nch, hch);
+    }
+}
+
+int h8_apply(int op, const FineArgs& a, cudaStream_t s) {
+    switch (op) {
+        case FOP_MATVEC: launch_h8<FOP_MATVEC>(a, s); break;
+        case FOP_RESID: launch_h8<FOP_RESID>(a, s); break;
+        case FOP_JACOBI: launch_h8<FOP_JACOBI>(a, s); break;
+        default: launch_h8<FOP_CGP>(a, s); break;
+    }
+    return h8_items(a.g, a.R);
+}

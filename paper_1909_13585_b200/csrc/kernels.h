@@ -34,8 +34,12 @@ struct FineArgs {
 void fine_set_constants(int dim, const double* K0, cudaStream_t s);
 // Launch one fine-level layer-march kernel; returns number of dot partial items per RHS.
 int fine_apply(int op, const FineArgs& a, cudaStream_t s);
-int fine_items(const LevelGeom& g);
+int fine_items(const LevelGeom& g, int R);
 void fine_diag(const LevelGeom& g, const double* E, const uint8_t* mask, double* Dinv, double* D, cudaStream_t s);
+// 3D structured (sum/difference basis) fine operator (h8.cu); fine_apply routes 3D here
+void h8_set_constants(double nu, cudaStream_t s);
+int h8_apply(int op, const FineArgs& a, cudaStream_t s);
+int h8_items(const LevelGeom& g, int R);
 
 // ---------------------------------------------------------------- 2D fused march kernels (fine2d.cu)
 enum March2Op { M2_MATVEC = 0, M2_RESID = 1, M2_JACOBI = 2, M2_CGP = 3, M2_RESTRICT = 4, M2_POST = 5 };

@@ -485,7 +485,7 @@ static mg_status ensure_vectors(mg_ctx* c, int R) {
             CU(cudaMemset(s.lv[l].w, 0, sizeof(double) * nl * R));
             xplane = std::max(xplane, s.lv[l].pn * c->dim);
         }
-        long long items = fine_items(s.lv[0].g);
+        long long items = fine_items(s.lv[0].g, R);
         if (c->dim == 2) {
             for (int op : {M2_CGP, M2_RESTRICT, M2_POST, M2_RESID, M2_JACOBI}) {
                 long long it = march2_items(op, s.lv[0].g, c->L > 1 ? &s.lv[1].g : &s.lv[0].g);
@@ -1027,6 +1027,7 @@ static mg_status setup_impl(mg_ctx* c, const mg_grid* grid, const double* E_e, c
     c->nu_paper = (c->nu == MG_NU_PAPER);
     c->fused2d = (dim == 2 && levels >= 2);
     fine_set_constants(dim, c->K0.data(), s);
+    if (dim == 3) h8_set_constants(c->nu, s);
     if (dim == 2) fine2d_set_constants(c->K0.data(), s);
     galerkin_set_constants(dim, c->K0.data(), s);
     stress_set_constants(dim, c->nu, s);
