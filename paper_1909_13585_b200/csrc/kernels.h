@@ -128,6 +128,14 @@ void stencil_from_elements(const LevelGeom& g, const double* elm, uint8_t* mask,
 void stencil_diag(const LevelGeom& g, const double* st, uint8_t* mask, double* st_rw, double* Dinv, double* D,
                   cudaStream_t s);
 
+// 2D fused coarse-level V(1,1) halves (coarse2d.cu)
+void coarse2d_down(const LevelGeom& g, const LevelGeom& gc, const double* st, const double* Dinv,
+                   const uint8_t* mask, const uint8_t* maskc, const double* r, double* rc, int R, double omega,
+                   int off0, int fo0, int fo1, const int* active, const int* done, cudaStream_t s);
+void coarse2d_up(const LevelGeom& g, const LevelGeom& gc, const double* st, const double* Dinv, const uint8_t* mask,
+                 const uint8_t* maskc, const double* r, const double* ec, double* z, int R, double omega, int off0,
+                 const int* active, const int* done, cudaStream_t s);
+
 // ---------------------------------------------------------------- transfers
 // off0: 1 if the slab's local plane 0 is an (odd-global) ghost plane; [fo0, fo1): slab-owned fine
 // planes that contribute to the restriction (fo1 < 0: all).

@@ -145,6 +145,7 @@ struct mg_ctx {
     double nu = 0.3;
     bool nu_paper = true;     // nu == 0.3: compile-time K0 in the fine kernels
     bool fused2d = false;     // 2D, L >= 2, V(1,1): fused RESTRICT / POST fine kernels
+    bool unfused_coarse = false;   // MG_UNFUSED_COARSE=1: generic coarse-level kernels (A/B checks)
     mg_opts opts{0.6, 1, 1, 1000};
     cudaStream_t user = nullptr, stream = nullptr;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
@@ -662,6 +663,29 @@ static mg_status vcycle(Rec& rc, int l, int* which) {
         return MG_OK;
     }
     TRY(xchg(c, [&](const Slab& s) { return vec_field(c, s, l, s.lv[l].r, R); }));
+    if (c->dim == 2 && c->opts.nu_pre == 1 && c->opts.nu_post == 1 && !c->unfused_coarse) {
+        // fused V(1,1) halves (coarse2d.cu)
+        for (Slab& s : c->sl) {
+            Level& f = s.lv[l];
+            Level& nx = s.lv[l + 1];
+            coarse2d_down(f.g, nx.g, f.st, f.Dinv, f.mask, nx.mask, f.r, nx.r, R, c->opts.omega, s.gl, f.o0, f.o1,
+                          rc.active, rc.done, c->stream);
+            rc.launches++;
+        }
+        TRY(xchg_add(c, [&](const Slab& s) { return vec_field(c, s, l + 1, s.lv[l + 1].r, R); }));
+        int cw = 0;
+        TRY(vcycle(rc, l + 1, &cw));
+        for (Slab& s : c->sl) {
+            Level& f = s.lv[l];
+            Level& nx = s.lv[l + 1];
+            coarse2d_up(f.g, nx.g, f.st, f.Dinv, f.mask, nx.mask, f.r, cw ? nx.w : nx.z, f.z, R, c->opts.omega, s.gl,
+                        rc.active, rc.done, c->stream);
+            rc.launches++;
+        }
+        TRY(xchg(c, [&](const Slab& s) { return vec_field(c, s, l, s.lv[l].z, R); }));
+        *which = 0;
+        return MG_OK;
+    }
     int zi = 0;   // 0: z holds the iterate, 1: w
     auto zb = [&](Slab& s) { return zi ? s.lv[l].w : s.lv[l].z; };
     auto wb = [&](Slab& s) { return zi ? s.lv[l].z : s.lv[l].w; };
@@ -1026,6 +1050,7 @@ static mg_status setup_impl(mg_ctx* c, const mg_grid* grid, const double* E_e, c
     element_stiffness(dim, c->nu, c->K0);
     c->nu_paper = (c->nu == MG_NU_PAPER);
     c->fused2d = (dim == 2 && levels >= 2);
+    c->unfused_coarse = getenv("MG_UNFUSED_COARSE") && atoi(getenv("MG_UNFUSED_COARSE")) == 1;
     fine_set_constants(dim, c->K0.data(), s);
     if (dim == 3) h8_set_constants(c->nu, s);
     if (dim == 2) fine2d_set_constants(c->K0.data(), s);
