@@ -8,8 +8,9 @@ metric: fine-grid DOF*RHS*iter/s = n * sum_k iters_k / t_step  (plus MGCG solves
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl reference]
 
-N > 1 is launched by torchrun (one process per GPU); round 1 runs independent
-replicas per rank (weak scaling, no data-path collective), see DESIGN.md.
+N > 1 is launched by torchrun (one process per GPU): the global grid is cut into N axis-0
+slabs (mg_setup_dist; NCCL halo exchange + allreduce inside libmgcg), strong scaling,
+device time = max over ranks.
 """
 
 from __future__ import annotations
@@ -112,16 +113,20 @@ def traffic_from_profiles(cfg_name):
 def run_ours(args, cfg):
     import torch
     import paper_1909_13585_b200 as mg
+    from paper_1909_13585_b200.dist import bootstrap_nccl_id, local_inputs, rank_part
 
     ws, rank, local = dist_env()
-    if ws > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    # replicas: each rank its own seeded design of the same config (weak scaling)
-    inp = generate(cfg if rank == 0 else get_config(cfg.name, seed=cfg.seed + 100 * rank))
-    n = n_dofs(cfg.nel)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    # N > 1: one global problem cut into ws axis-0 slabs (strong scaling, NCCL halos + allreduce)
+    inp_g = generate(cfg)
+    part = rank_part(cfg.nel, cfg.levels, ws, rank)
+    inp = local_inputs(inp_g, part) if ws > 1 else inp_g
+    n_glob = n_dofs(cfg.nel)
+    n = inp["rhs"].shape[1]
     R = cfg.nrhs
     nphi = max(cfg.nphi, 0)
     E = torch.from_numpy(inp["E"]).to(dev)
@@ -133,7 +138,11 @@ def run_ours(args, cfg):
     y = torch.empty((nphi, n), dtype=torch.float64, device=dev) if nphi else None
     stream = torch.cuda.current_stream()
     t0 = time.time()
-    h = mg.mg_setup(cfg.nel, E, fixed, cfg.levels)
+    if ws > 1:
+        nid = bootstrap_nccl_id(rank, ws)
+        h = mg.mg_setup_dist(cfg.nel, E, fixed, cfg.levels, rank=rank, nranks=ws, nslab=1, nccl_id=nid)
+    else:
+        h = mg.mg_setup(cfg.nel, E, fixed, cfg.levels)
     torch.cuda.synchronize()
     setup_first_s = time.time() - t0
 
@@ -172,17 +181,13 @@ def run_ours(args, cfg):
     launches = mg.mg_kernel_launches(h) - l0
     ms_total = start.elapsed_time(end)
     phases = np.array([[e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3])] for e in evs])
-    dofiters = [n * sum(r["iters"]) for r in reps]
+    # units processed by the whole job: global DOFs x sum of per-RHS iterations (identical on all ranks)
+    total_dofiters = float(sum(n_glob * sum(r["iters"]) for r in reps))
     if ws > 1:
         import torch.distributed as dist
         t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
-        d = torch.tensor([float(sum(dofiters))], dtype=torch.float64, device=dev)
-        dist.all_reduce(d, op=dist.ReduceOp.SUM)
-        total_dofiters = float(d.item())
-    else:
-        total_dofiters = float(sum(dofiters))
     clocks = clk.stop()
     ms_step = ms_total / args.steps
     value = total_dofiters / (ms_total / 1e3)
@@ -191,7 +196,7 @@ def run_ours(args, cfg):
     # configuration as in the solve graph) with CUDA events on the handle's stream.
     hbm, peak_kind = peaks()
     kms = mg.mg_profile_kernels(h, R, reps=10)
-    m = int(np.prod(cfg.nel))
+    m = int(inp["E"].size)
     nR = float(n) * R
     coarse = 1.0 / (2 ** cfg.dim)
     # algorithmic bytes per launch (what each kernel must move)
@@ -224,13 +229,19 @@ def run_ours(args, cfg):
 
         e2e_step()
         torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
         t1 = time.perf_counter()
         its = 0
         for _ in range(max(1, min(args.steps, 3))):
             rep = e2e_step()
-            its += n * sum(rep["iters"])
+            its += n_glob * sum(rep["iters"])
         torch.cuda.synchronize()
         dt = time.perf_counter() - t1
+        if ws > 1:
+            tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            dt = float(tt.item())
         nst = max(1, min(args.steps, 3))
         h2d = 8 * (inp["E"].size + R * n + (inp["Es"].size + n + nphi * n if nphi else 0))
         d2h = 8 * (R * n + nphi * n)
@@ -239,12 +250,13 @@ def run_ours(args, cfg):
 
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong" if ws > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE recipe)",
         "config": {"workload": f"{cfg.name}: {'Q4' if cfg.dim == 2 else 'H8'} {'x'.join(map(str, cfg.nel))}, "
                                f"{R} RHS, {cfg.levels} levels, G(u)phi x{nphi}",
-                   "ndof": n, "nrhs": R, "levels": cfg.levels, "tol": cfg.tol,
-                   "parallelism": "replicas" if ws > 1 else "single",
+                   "ndof": n_glob, "nrhs": R, "levels": cfg.levels, "tol": cfg.tol,
+                   "parallelism": f"slabs{ws} (axis-0, NCCL halo + allreduce)" if ws > 1 else "single",
                    "l2": "inputs larger than L2 (fine R-vector %.0f MB)" % (8 * n * R / 1e6)},
         "solves_per_s": 1e3 / ms_step,
         "phase_ms": {"setup": float(phases[:, 0].mean()), "solve": float(phases[:, 1].mean()),

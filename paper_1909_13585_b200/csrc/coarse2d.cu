@@ -72,15 +72,13 @@ __global__ void __launch_bounds__(CT_I * CT_J, 1) coarse2d_down_kernel(LevelGeom
     const bool cok = cown && Ic < gc.nn[0] && Jc < gc.nn[1];
     const long long cnode = (long long)Ic * gc.nn[1] + Jc;
     const int mc = cok ? maskc[cnode] : 3;
+    // software pipeline over the RHS: r of RHS k+1 is in flight while RHS k is processed
+    double2 rn = make_double2(0.0, 0.0);
+    if (ok) rn = *reinterpret_cast<const double2*>(r + 2 * node);
     for (int k = 0; k < R; ++k) {
+        const double rx = rn.x, ry = rn.y;
+        if (ok && k + 1 < R) rn = *reinterpret_cast<const double2*>(r + (long long)(k + 1) * g.ndof + 2 * node);
         if (active && !active[k]) continue;
-        const double* rv = r + (long long)k * g.ndof;
-        double rx = 0.0, ry = 0.0;
-        if (ok) {
-            const double2 v = *reinterpret_cast<const double2*>(rv + 2 * node);
-            rx = v.x;
-            ry = v.y;
-        }
         s_z[ti][tj] = make_double2(omega * dx * rx, omega * dy * ry);
         __syncthreads();
         if (wreg) {
@@ -139,28 +137,27 @@ __global__ void __launch_bounds__(CT_I * CT_J, 1) coarse2d_up_kernel(LevelGeom g
     const int fsi = fi + off0;
     const int li0 = (fsi >> 1) - ci0, li1 = ((fsi + 1) >> 1) - ci0;
     const int lj0 = (fj >> 1) - cj0, lj1 = ((fj + 1) >> 1) - cj0;
+    static_assert(CI * CJ <= CT_I * CT_J, "one coarse tile entry per thread");
+    // this thread's coarse tile entry (if any)
+    const int ea = threadIdx.x / CJ, eb = threadIdx.x % CJ;
+    const int eI = ci0 + ea, eJ = cj0 + eb;
+    const bool eok = threadIdx.x < CI * CJ && eI >= 0 && eI < gc.nn[0] && eJ >= 0 && eJ < gc.nn[1];
+    const long long ecn = eok ? (long long)eI * gc.nn[1] + eJ : 0;
+    const int emc = eok ? maskc[ecn] : 3;
+    // software pipeline over the RHS: e and r of RHS k+1 are in flight while RHS k is processed
+    double2 en = make_double2(0.0, 0.0), rn = make_double2(0.0, 0.0);
+    if (eok) en = *reinterpret_cast<const double2*>(ec + 2 * ecn);
+    if (ok) rn = *reinterpret_cast<const double2*>(r + 2 * node);
     for (int k = 0; k < R; ++k) {
+        const double2 ev = en;
+        const double rx = rn.x, ry = rn.y;
+        if (k + 1 < R) {
+            if (eok) en = *reinterpret_cast<const double2*>(ec + (long long)(k + 1) * gc.ndof + 2 * ecn);
+            if (ok) rn = *reinterpret_cast<const double2*>(r + (long long)(k + 1) * g.ndof + 2 * node);
+        }
         if (active && !active[k]) continue;
-        const double* ev = ec + (long long)k * gc.ndof;
-        for (int q = threadIdx.x; q < CI * CJ; q += CT_I * CT_J) {
-            const int a = q / CJ, b = q % CJ;
-            const int I = ci0 + a, J = cj0 + b;
-            double2 v = make_double2(0.0, 0.0);
-            if (I >= 0 && I < gc.nn[0] && J >= 0 && J < gc.nn[1]) {
-                const long long cn = (long long)I * gc.nn[1] + J;
-                const int mc = maskc[cn];
-                v = *reinterpret_cast<const double2*>(ev + 2 * cn);
-                if (mc & 1) v.x = 0.0;
-                if (mc & 2) v.y = 0.0;
-            }
-            s_e[a][b] = v;
-        }
-        double rx = 0.0, ry = 0.0;
-        if (ok) {
-            const double2 v = *reinterpret_cast<const double2*>(r + (long long)k * g.ndof + 2 * node);
-            rx = v.x;
-            ry = v.y;
-        }
+        if (threadIdx.x < CI * CJ)
+            s_e[ea][eb] = make_double2((emc & 1) ? 0.0 : ev.x, (emc & 2) ? 0.0 : ev.y);
         __syncthreads();
         double zx = 0.0, zy = 0.0;
         if (ok) {

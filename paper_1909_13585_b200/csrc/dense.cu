@@ -188,9 +188,11 @@ void dense_spd_inverse(double* A, long long npad, double* work, int* d_status, c
     }
 }
 
-// z[r][i] = sum_j Ainv[i][j] rvec[r][j]; one warp per row, RB vectors per pass.
+// z[r][i] = sum_j Ainv[i][j] rvec[r][j]; one warp per row (4 rows per CTA so the grid
+// covers all SMs), up to RB vectors per pass, column loop unrolled for memory-level
+// parallelism (Ainv and the vectors are L2-resident: n_L <= ~4k).
 template <int RB>
-__global__ void __launch_bounds__(256) dense_apply_kernel(const double* __restrict__ Ainv, long long ld, long long n,
+__global__ void __launch_bounds__(128) dense_apply_kernel(const double* __restrict__ Ainv, long long ld, long long n,
                                                           const double* __restrict__ rv, double* __restrict__ z, int R,
                                                           int r0, const int* active, const int* done) {
     const int lane = threadIdx.x & 31;
@@ -205,11 +207,12 @@ __global__ void __launch_bounds__(256) dense_apply_kernel(const double* __restri
 #pragma unroll
     for (int q = 0; q < RB; ++q) acc[q] = 0.0;
     const double* row = Ainv + i * ld;
+#pragma unroll 4
     for (long long j = lane; j < n; j += 32) {
         const double a = row[j];
 #pragma unroll
         for (int q = 0; q < RB; ++q)
-            if (act[q]) acc[q] = fma(a, rv[(long long)(r0 + q) * n + j], acc[q]);
+            if (act[q]) acc[q] = fma(a, __ldg(rv + (long long)(r0 + q) * n + j), acc[q]);
     }
 #pragma unroll
     for (int q = 0; q < RB; ++q) {
@@ -220,11 +223,12 @@ __global__ void __launch_bounds__(256) dense_apply_kernel(const double* __restri
 
 void dense_apply(const double* Ainv, long long ld, long long n, const double* r, double* z, int R, const int* active,
                  const int* done, cudaStream_t s) {
-    unsigned bl = (unsigned)((n + 7) / 8);
+    unsigned bl = (unsigned)((n + 3) / 4);
     for (int r0 = 0; r0 < R;) {
         int rem = R - r0;
-        if (rem > 4) { dense_apply_kernel<8><<<bl, 256, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); r0 += 8; }
-        else if (rem > 1) { dense_apply_kernel<4><<<bl, 256, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); r0 += 4; }
-        else { dense_apply_kernel<1><<<bl, 256, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); r0 += 1; }
+        if (rem > 8) { dense_apply_kernel<16><<<bl, 128, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); r0 += 16; }
+        else if (rem > 4) { dense_apply_kernel<8><<<bl, 128, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); r0 += 8; }
+        else if (rem > 1) { dense_apply_kernel<4><<<bl, 128, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); r0 += 4; }
+        else { dense_apply_kernel<1><<<bl, 128, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); r0 += 1; }
     }
 }

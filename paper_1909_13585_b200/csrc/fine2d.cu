@@ -42,6 +42,9 @@ static constexpr int PD = 2;      // register prefetch depth (node planes in fli
 static constexpr int CH = 64;     // node planes per chunk
 static constexpr int CCH = 32;    // coarse rows per chunk (M2_RESTRICT)
 static constexpr int WPB = 4;     // warps per CTA (independent)
+// cap at 170 registers so 3 CTAs (12 warps) fit per SM (POST would otherwise take 185)
+static constexpr int march_minb(int op) { return op >= 0 ? 3 : 1; }
+
 
 __device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 __device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
@@ -170,7 +173,7 @@ struct Ops {
 };
 
 template <int OP, bool C03>
-__global__ void __launch_bounds__(32 * WPB) march2_kernel(March2Args a, int nct, int nch) {
+__global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2Args a, int nct, int nch) {
     constexpr int CS = (OP == M2_RESTRICT) ? 28 : 30;      // owned columns per warp
     constexpr int LOFF = (OP == M2_RESTRICT) ? 2 : 1;      // lane of the first owned column
     const int lane = threadIdx.x & 31;
