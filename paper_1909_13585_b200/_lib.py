@@ -11,7 +11,7 @@ import ctypes
 import os
 
 MG_MAX_RHS = 64
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libmgcg.so")
+LIB_PATH = os.environ.get("MG_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libmgcg.so")
 
 STATUS = {
     0: "MG_OK", 1: "MG_ERR_ARG", 2: "MG_ERR_NONDIVISIBLE", 3: "MG_ERR_DIM", 4: "MG_ERR_MODULUS",

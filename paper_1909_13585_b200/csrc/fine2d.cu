@@ -38,12 +38,36 @@ __device__ __forceinline__ double K2(int r, int c) {
     return c_K2[r * 8 + c];
 }
 
-static constexpr int PD = 2;      // register prefetch depth (node planes in flight per warp)
+// register prefetch depth (node planes in flight per warp) and CTAs per SM (register cap)
+// per kernel: tuned on B200 with ncu / bench A/B
+#ifndef MG_PD_CGP
+#define MG_PD_CGP 2
+#endif
+#ifndef MG_PD_RESTRICT
+#define MG_PD_RESTRICT 1
+#endif
+#ifndef MG_PD_POST
+#define MG_PD_POST 1
+#endif
+#ifndef MG_MB_CGP
+#define MG_MB_CGP 3
+#endif
+#ifndef MG_MB_RESTRICT
+#define MG_MB_RESTRICT 4
+#endif
+#ifndef MG_MB_POST
+#define MG_MB_POST 4
+#endif
+static constexpr int prefetch_depth(int op) {
+    return op == M2_POST ? MG_PD_POST : op == M2_RESTRICT ? MG_PD_RESTRICT : op == M2_CGP ? MG_PD_CGP : 2;
+}
 static constexpr int CH = 64;     // node planes per chunk
 static constexpr int CCH = 32;    // coarse rows per chunk (M2_RESTRICT)
 static constexpr int WPB = 4;     // warps per CTA (independent)
 // cap at 170 registers so 3 CTAs (12 warps) fit per SM (POST would otherwise take 185)
-static constexpr int march_minb(int op) { return op >= 0 ? 3 : 1; }
+static constexpr int march_minb(int op) {
+    return op == M2_POST ? MG_MB_POST : op == M2_RESTRICT ? MG_MB_RESTRICT : op == M2_CGP ? MG_MB_CGP : 3;
+}
 
 
 __device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
@@ -172,7 +196,8 @@ struct Ops {
     static constexpr bool DI = OP == M2_RESTRICT || OP == M2_POST || OP == M2_JACOBI;
 };
 
-template <int OP, bool C03>
+// SLAB = false: single slab (off0 = 0, every plane owned) -- the slab checks compile away
+template <int OP, bool C03, bool SLAB>
 __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2Args a, int nct, int nch) {
     constexpr int CS = (OP == M2_RESTRICT) ? 28 : 30;      // owned columns per warp
     constexpr int LOFF = (OP == M2_RESTRICT) ? 2 : 1;      // lane of the first owned column
@@ -191,7 +216,7 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
     const bool own_col = cin && lane >= LOFF && lane < LOFF + CS;
     // off0 = 1 when the slab's local plane 0 is a ghost plane at an odd global index:
     // coarse row I is coincident with local fine plane 2I - off0 (parities use P + off0).
-    const int off0 = a.off0;
+    const int off0 = SLAB ? a.off0 : 0;
     int i0, i1, own0, own1, I0 = 0, I1 = 0;
     if (OP == M2_RESTRICT) {
         const int nc0 = a.gc.nn[0];
@@ -279,7 +304,7 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
                       double& k2y) {
         const bool fx = s.m & 1, fy = s.m & 2;
         const bool own_plane = P >= own0 && P < own1;
-        const bool slab_plane = P >= a.so0 && P < a.so1;   // dots: slab-owned planes only
+        const bool slab_plane = !SLAB || (P >= a.so0 && P < a.so1);   // dots: slab-owned planes only
         if (OP == M2_CGP) {
             ux = fma(beta, s.v1x, s.v0x);
             uy = fma(beta, s.v1y, s.v0y);
@@ -324,6 +349,7 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
     };
 
     // ---- prologue: plane i0-1 and the prefetch ring
+    constexpr int PD = prefetch_depth(OP);
     Slot ring[PD];
     {
         Slot s0;
@@ -386,7 +412,7 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
             if (L >= i0) {
                 const double Axx = (mA & 1) ? urx : lox, Axy = (mA & 2) ? ury : loy;
                 const bool own = own_col && L >= own0 && L < own1;
-                const bool sdot = own && L >= a.so0 && L < a.so1;   // slab-owned: counts in dots
+                const bool sdot = own && (!SLAB || (L >= a.so0 && L < a.so1));   // slab-owned: counts in dots
                 const long long o = 2 * (pd.org + (long long)L * pd.pitch + c);
                 if (OP == M2_MATVEC) {
                     if (own) st2(yb + o, Axx, Axy);
@@ -415,7 +441,7 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
                     // t = r - K z1 (lanes 1..30 valid), then P^T: columns by shuffles, planes by carry
                     // t counts only on slab-owned planes: the coarse ghost row above gets a
                     // partial sum that the upper neighbour adds in (reverse halo exchange)
-                    const bool tv = cin && lane >= 1 && lane <= 30 && L >= a.so0 && L < a.so1;
+                    const bool tv = cin && lane >= 1 && lane <= 30 && (!SLAB || (L >= a.so0 && L < a.so1));
                     const double tx = (tv && !(mA & 1)) ? auxx - Axx : 0.0;
                     const double ty = (tv && !(mA & 2)) ? auxy - Axy : 0.0;
                     const double tlx = shfl_up1(tx), tly = shfl_up1(ty);
@@ -478,8 +504,14 @@ static void launch2(const March2Args& a, bool c03, cudaStream_t s) {
     }
     const long long warps = (long long)a.R * nct * nch;
     const unsigned blocks = (unsigned)((warps + WPB - 1) / WPB);
-    if (c03) march2_kernel<OP, true><<<blocks, 32 * WPB, 0, s>>>(a, nct, nch);
-    else march2_kernel<OP, false><<<blocks, 32 * WPB, 0, s>>>(a, nct, nch);
+    const bool slab = a.off0 != 0 || a.so0 != 0 || a.so1 != a.g.nn[0];
+    if (slab) {
+        if (c03) march2_kernel<OP, true, true><<<blocks, 32 * WPB, 0, s>>>(a, nct, nch);
+        else march2_kernel<OP, false, true><<<blocks, 32 * WPB, 0, s>>>(a, nct, nch);
+    } else {
+        if (c03) march2_kernel<OP, true, false><<<blocks, 32 * WPB, 0, s>>>(a, nct, nch);
+        else march2_kernel<OP, false, false><<<blocks, 32 * WPB, 0, s>>>(a, nct, nch);
+    }
 }
 
 int march2_apply(int op, const March2Args& a, bool c03, cudaStream_t s) {

@@ -1,0 +1,6 @@
+#!/bin/bash
+# A/B of library variants in paper_1909_13585_b200/_libvar on one config. usage: bash tools/gpu_ab.sh <tag> <config>
+O=gpurun_out/$1; mkdir -p $O; C=${2:-C3}
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1 || exit 1
+timeout 600 python bench.py --config $C --no-cpu --no-e2e --steps 5 > $O/bench_default.json 2>&1
+for f in paper_1909_13585_b200/_libvar/*.so; do n=$(basename $f .so); MG_LIB=$PWD/$f timeout 600 python bench.py --config $C --no-cpu --no-e2e --steps 5 > $O/bench_$n.json 2>&1; done
