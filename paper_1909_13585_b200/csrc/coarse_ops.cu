@@ -72,10 +72,14 @@ void elements_from_E(const LevelGeom& g, const double* E, const uint8_t* mask, d
 }
 
 // One CTA per coarse element; thread (row, col) owns one entry of K_E.
+// Level 1 from E: when none of the 3^d fine nodes of the coarse element is fixed, every
+// child matrix is E_c K0 and K_E = sum_c E_c M_c with the constant M_c = Q_c^T K0 Q_c
+// (c_M, set once per handle) -- one FMA per child instead of two small matrix products.
 template <int DIM, bool FROM_E>
 __global__ void galerkin_kernel(LevelGeom gc, LevelGeom gf, const double* __restrict__ E,
                                 const double* __restrict__ elm_f, const uint8_t* __restrict__ mask_f,
-                                const uint8_t* __restrict__ mask_c, double* __restrict__ elm_c, int off0) {
+                                const uint8_t* __restrict__ mask_c, double* __restrict__ elm_c, int off0,
+                                const double* __restrict__ Mc) {
     constexpr int NA = 1 << DIM, NL = DIM * NA;
     __shared__ double Kc[NL * NL];
     __shared__ double T[NL * NL];
@@ -89,6 +93,33 @@ __global__ void galerkin_kernel(LevelGeom gc, LevelGeom gf, const double* __rest
     // slab ghost element layer (children not local): filled by the halo exchange instead
     if (ci[0] < off0) return;
     double acc = 0.0;
+    bool fast = false;
+    if (FROM_E && Mc) {
+        constexpr int NF = DIM == 2 ? 9 : 27;   // fine nodes of the coarse element
+        int fixed_here = 0;
+        if (t < NF) {
+            int q = t, node = 0;
+            int fc[3];
+            for (int k = DIM - 1; k >= 0; --k) { fc[k] = 2 * ci[k] + q % 3 - (k == 0 ? off0 : 0); q /= 3; }
+            bool inside = true;
+            for (int k = 0; k < DIM; ++k) inside = inside && fc[k] >= 0 && fc[k] < gf.nn[k];
+            if (inside) {
+                for (int k = 0; k < DIM; ++k) node = node * gf.nn[k] + fc[k];
+                fixed_here = mask_f[node] != 0;
+            } else {
+                fixed_here = 1;
+            }
+        }
+        fast = !__syncthreads_or(fixed_here);
+    }
+    if (fast) {
+        for (int ch = 0; ch < NA; ++ch) {
+            long long fe = 0;
+            for (int k = 0; k < DIM; ++k)
+                fe = fe * gf.N[k] + 2 * ci[k] + ((ch >> (DIM - 1 - k)) & 1) - (k == 0 ? off0 : 0);
+            acc = fma(E[fe], Mc[ch * NL * NL + t], acc);
+        }
+    } else
     for (int ch = 0; ch < NA; ++ch) {
         int fi[3];
         for (int k = 0; k < DIM; ++k) fi[k] = 2 * ci[k] + ((ch >> (DIM - 1 - k)) & 1) - (k == 0 ? off0 : 0);
@@ -134,15 +165,39 @@ __global__ void galerkin_kernel(LevelGeom gc, LevelGeom gf, const double* __rest
 }
 
 void galerkin_elements(const LevelGeom& gc, const LevelGeom& gf, const double* E, const double* elm_f,
-                       const uint8_t* mask_f, const uint8_t* mask_c, double* elm_c, cudaStream_t s, int off0) {
+                       const uint8_t* mask_f, const uint8_t* mask_c, double* elm_c, cudaStream_t s, int off0,
+                       const double* Mc) {
     unsigned bl = (unsigned)gc.nelem;
     if (gc.dim == 2) {
-        if (E) galerkin_kernel<2, true><<<bl, 64, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0);
-        else galerkin_kernel<2, false><<<bl, 64, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0);
+        if (E) galerkin_kernel<2, true><<<bl, 64, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, Mc);
+        else galerkin_kernel<2, false><<<bl, 64, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, nullptr);
     } else {
-        if (E) galerkin_kernel<3, true><<<bl, 576, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0);
-        else galerkin_kernel<3, false><<<bl, 576, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0);
+        if (E) galerkin_kernel<3, true><<<bl, 576, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, Mc);
+        else galerkin_kernel<3, false><<<bl, 576, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, nullptr);
     }
+}
+
+// M_c = Q_c^T K0 Q_c for the 2^d children (host, once per handle); layout [child][NL*NL]
+void galerkin_child_matrices(int dim, const double* K0, double* Mc_host) {
+    const int na = 1 << dim, nl = dim * na;
+    for (int c = 0; c < na; ++c)
+        for (int r = 0; r < nl; ++r)
+            for (int q = 0; q < nl; ++q) {
+                const int b = r / dim, i = r % dim, b2 = q / dim, j = q % dim;
+                double v = 0.0;
+                for (int a = 0; a < na; ++a)
+                    for (int a2 = 0; a2 < na; ++a2) {
+                        double w1 = 1.0, w2 = 1.0;
+                        for (int k = 0; k < dim; ++k) {
+                            const int sh = dim - 1 - k;
+                            const int p1 = ((c >> sh) & 1) + ((a >> sh) & 1), p2 = ((c >> sh) & 1) + ((a2 >> sh) & 1);
+                            w1 *= (p1 == 1) ? 0.5 : (p1 == 2 * ((b >> sh) & 1) ? 1.0 : 0.0);
+                            w2 *= (p2 == 1) ? 0.5 : (p2 == 2 * ((b2 >> sh) & 1) ? 1.0 : 0.0);
+                        }
+                        if (w1 != 0.0 && w2 != 0.0) v += w1 * K0[(a * dim + i) * nl + a2 * dim + j] * w2;
+                    }
+                Mc_host[(c * nl + r) * nl + q] = v;
+            }
 }
 
 // ---------------------------------------------------------------- stencil assembly

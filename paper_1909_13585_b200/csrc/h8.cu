@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(32 * TR, MINB) h8_kernel(FineArgs a, int ntc, 
     const long long ecol = (long long)j * N2 + c;         // element offset within a layer
     const long long pstride = (long long)n1 * n2, estride = (long long)N1 * N2;
     const double beta = (OP == FOP_CGP) ? a.beta[r] : 0.0;
+    const double alpha = (OP == FOP_RESTR3) ? a.alpha[r] : 0.0;
     const double xal = (OP == FOP_CGP && a.xv) ? a.xalpha[r] : 0.0;
 
     auto load = [&](H8Plane& q, int P) {
@@ -132,7 +133,38 @@ __global__ void __launch_bounds__(32 * TR, MINB) h8_kernel(FineArgs a, int ntc, 
         const long long nd = (long long)P * pstride + col;
         const long long o = vbase + 3 * nd;
         q.m = a.mask[nd];
-        if (OP == FOP_CGP) {
+        if (OP == FOP_RESTR3) {
+            // r = rin - alpha q (kept in aux, stored by the caller loop), input omega D^-1 r
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const double rv = fma(-alpha, a.q[o + k], a.rin[o + k]);
+                q.aux[k] = rv;
+                q.raw[k] = a.omega * a.Dinv[3 * nd + k] * rv;
+            }
+        } else if (OP == FOP_POST3) {
+            // input z2 = omega D^-1 b + P ec (trilinear prolongation, coarse-masked)
+            const int Ps = P + a.off0;
+            const int I0 = Ps >> 1, I1 = (Ps + 1) >> 1, J0 = j >> 1, J1 = (j + 1) >> 1, C0 = c >> 1,
+                      C1 = (c + 1) >> 1;
+            const int cn1 = a.gc.nn[1], cn2 = a.gc.nn[2];
+            const double* ev = a.ec + (long long)r * a.gc.ndof;
+            double pe[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+            for (int s8 = 0; s8 < 8; ++s8) {
+                const int I = (s8 & 4) ? I1 : I0, J = (s8 & 2) ? J1 : J0, C = (s8 & 1) ? C1 : C0;
+                const long long cn = ((long long)I * cn1 + J) * cn2 + C;
+                const int mc = a.maskc[cn];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) pe[k] += ((mc >> k) & 1) ? 0.0 : ev[3 * cn + k];
+            }
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const double bv = a.b[o + k];
+                q.aux[k] = bv;
+                q.dinv[k] = a.Dinv[3 * nd + k];
+                q.raw[k] = ((q.m >> k) & 1) ? 0.0 : fma(a.omega * q.dinv[k], bv, 0.125 * pe[k]);
+            }
+        } else if (OP == FOP_CGP) {
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
                 const double pin = a.pin[o + k];
@@ -140,7 +172,7 @@ __global__ void __launch_bounds__(32 * TR, MINB) h8_kernel(FineArgs a, int ntc, 
                 q.aux[k] = pin;
                 if (a.xv) q.xo[k] = a.xv[o + k];
             }
-        } else {
+        } else if (OP != FOP_RESTR3 && OP != FOP_POST3) {
 #pragma unroll
             for (int k = 0; k < 3; ++k) q.raw[k] = a.x[o + k];
         }
@@ -194,6 +226,15 @@ __global__ void __launch_bounds__(32 * TR, MINB) h8_kernel(FineArgs a, int ntc, 
         H8Plane pl = nxt;                       // plane P
         H8Plane lo = cur;                       // plane L
         if (P + 1 <= i1) load(nxt, P + 1);      // prefetch
+        if (OP == FOP_RESTR3 && own && P >= i0 && P < i1) {
+            const long long o = vbase + 3 * ((long long)P * pstride + col);
+            const bool sd = P >= a.so0 && P < a.so1;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                a.rout[o + k] = pl.aux[k];
+                if (sd) dot = fma(pl.aux[k], pl.aux[k], dot);
+            }
+        }
         if (OP == FOP_CGP && own && P >= i0 && P < i1) {
             const long long o = vbase + 3 * ((long long)P * pstride + col);
 #pragma unroll
@@ -268,9 +309,9 @@ __global__ void __launch_bounds__(32 * TR, MINB) h8_kernel(FineArgs a, int ntc, 
                 const double ax = ((lo.m >> k) & 1) ? lo.raw[k] : y[k];
                 double out;
                 if (OP == FOP_MATVEC || OP == FOP_CGP) out = ax;
-                else if (OP == FOP_RESID) out = lo.aux[k] - ax;
+                else if (OP == FOP_RESID || OP == FOP_RESTR3) out = lo.aux[k] - ax;
                 else out = fma(a.omega * lo.dinv[k], lo.aux[k] - ax, lo.raw[k]);
-                if (OP == FOP_JACOBI && sdot) dot = fma(lo.aux[k], out, dot);
+                if ((OP == FOP_JACOBI || OP == FOP_POST3) && sdot) dot = fma(lo.aux[k], out, dot);
                 if (OP == FOP_CGP && sdot) dot = fma(lo.raw[k], ax, dot);
                 a.y[o + k] = out;
             }
@@ -356,6 +397,8 @@ int h8_apply(int op, const FineArgs& a, cudaStream_t s) {
         case FOP_MATVEC: launch_h8<FOP_MATVEC>(a, s); break;
         case FOP_RESID: launch_h8<FOP_RESID>(a, s); break;
         case FOP_JACOBI: launch_h8<FOP_JACOBI>(a, s); break;
+        case FOP_RESTR3: launch_h8<FOP_RESTR3>(a, s); break;
+        case FOP_POST3: launch_h8<FOP_POST3>(a, s); break;
         default: launch_h8<FOP_CGP>(a, s); break;
     }
     return h8_items(a.g, a.R);

@@ -5,7 +5,8 @@
 #include "common.cuh"
 
 // ---------------------------------------------------------------- fine level (matrix-free)
-enum FineOp { FOP_MATVEC = 0, FOP_RESID = 1, FOP_JACOBI = 2, FOP_CGP = 3 };
+// FOP_RESTR3 / FOP_POST3: 3D fused halves of the fine V(1,1) level (h8.cu), see there
+enum FineOp { FOP_MATVEC = 0, FOP_RESID = 1, FOP_JACOBI = 2, FOP_CGP = 3, FOP_RESTR3 = 4, FOP_POST3 = 5 };
 
 struct FineArgs {
     LevelGeom g;
@@ -29,6 +30,16 @@ struct FineArgs {
     int R;
     int nu_paper;           // 1: nu == 0.3 -> compile-time K0
     int so0, so1;           // slab-owned local node planes (dots)
+    // FOP_RESTR3: r = rin - alpha q (stored to rout), operator input omega D^-1 r, y = r - K(.)
+    const double* rin;
+    const double* q;
+    double* rout;
+    const double* alpha;
+    // FOP_POST3: operator input z2 = omega D^-1 b + P ec, y = z2 + omega D^-1 (b - K z2)
+    const double* ec;
+    LevelGeom gc;
+    const uint8_t* maskc;
+    int off0;
 };
 
 void fine_set_constants(int dim, const double* K0, cudaStream_t s);
@@ -122,7 +133,8 @@ void coarse_apply(int op, const CoarseArgs& a, cudaStream_t s);
 void galerkin_set_constants(int dim, const double* K0, cudaStream_t s);
 void galerkin_elements(const LevelGeom& gc, const LevelGeom& gf, const double* E /*if from_E*/,
                        const double* elm_f, const uint8_t* mask_f, const uint8_t* mask_c,
-                       double* elm_c, cudaStream_t s, int off0 = 0);
+                       double* elm_c, cudaStream_t s, int off0 = 0, const double* Mc = nullptr);
+void galerkin_child_matrices(int dim, const double* K0, double* Mc_host);
 void elements_from_E(const LevelGeom& g, const double* E, const uint8_t* mask, double* elm, cudaStream_t s);
 void stencil_from_elements(const LevelGeom& g, const double* elm, uint8_t* mask, double* st, cudaStream_t s);
 void stencil_diag(const LevelGeom& g, const double* st, uint8_t* mask, double* st_rw, double* Dinv, double* D,

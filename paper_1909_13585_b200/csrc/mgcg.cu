@@ -146,6 +146,7 @@ struct mg_ctx {
     bool nu_paper = true;     // nu == 0.3: compile-time K0 in the fine kernels
     bool fused2d = false;     // 2D, L >= 2, V(1,1): fused RESTRICT / POST fine kernels
     bool unfused_coarse = false;   // MG_UNFUSED_COARSE=1: generic coarse-level kernels (A/B checks)
+    bool fused3d = false;     // 3D, L >= 2, V(1,1): fused h8 RESTR3 / POST3 fine kernels
     mg_opts opts{0.6, 1, 1, 1000};
     cudaStream_t user = nullptr, stream = nullptr;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
@@ -165,6 +166,7 @@ struct mg_ctx {
     double *cpack = nullptr, *cgath = nullptr;   // cross-rank gather staging
     long long cpack_cap = 0;
     double* gj_work = nullptr;
+    double* Mc = nullptr;                        // Galerkin child matrices Q_c^T K0 Q_c
     double* xtmp = nullptr;                      // NCCL reverse-add receive buffer
     long long xtmp_cap = 0;
     // shared solve state
@@ -401,7 +403,7 @@ static mg_status compute_operators(mg_ctx* c) {
             Level& g = sl.lv[l];
             double* elm = (l & 1) ? sl.elmA : sl.elmB;
             double* elm_prev = (l & 1) ? sl.elmB : sl.elmA;
-            galerkin_elements(g.g, f.g, l == 1 ? sl.E : nullptr, elm_prev, f.mask, g.mask, elm, s, sl.gl);
+            galerkin_elements(g.g, f.g, l == 1 ? sl.E : nullptr, elm_prev, f.mask, g.mask, elm, s, sl.gl, c->Mc);
             c->launches++;
         }
         CHECK_LAUNCH();
@@ -760,6 +762,23 @@ static mg_status blk_restrict(Rec& rc, double* Slab::*rin, double* Slab::*rout, 
         *items = off;
         return xchg_add(c, [&](const Slab& s) { return vec_field(c, s, 1, s.lv[1].r, R); });
     }
+    if (c->fused3d) {
+        // 3D: r = rin - alpha q, r.r, t = r - K (omega D^-1 r) in one h8 kernel, then P^T t
+        for (Slab& s : c->sl) {
+            FineArgs a = fine_args(c, s, rc);
+            a.rin = s.*rin; a.q = s.q; a.rout = s.*rout; a.alpha = c->ctl.alpha; a.Dinv = s.lv[0].Dinv;
+            a.y = s.t; a.partial = c->partial + off;
+            off += fine_apply(FOP_RESTR3, a, c->stream);
+            rc.launches++;
+        }
+        *items = off;
+        for (Slab& s : c->sl) {
+            restrict_apply(s.lv[0].g, s.lv[1].g, s.lv[0].mask, s.lv[1].mask, s.t, s.lv[1].r, R, rc.active, rc.done,
+                           c->stream, s.gl, s.lv[0].o0, s.lv[0].o1);
+            rc.launches++;
+        }
+        return xchg_add(c, [&](const Slab& s) { return vec_field(c, s, 1, s.lv[1].r, R); });
+    }
     for (Slab& s : c->sl) {
         long long d0, d1;
         fine_own_range(c, s, &d0, &d1);
@@ -821,6 +840,18 @@ static mg_status blk_post(Rec& rc, double* Slab::*r, int cw, long long* items) {
             March2Args a = march_args(c, s, rc);
             a.x = s.*r; a.ec = cw ? s.lv[1].w : s.lv[1].z; a.y = s.zf; a.partial = c->partial + off;
             off += march2_apply(M2_POST, a, c->nu_paper, c->stream);
+            rc.launches++;
+        }
+        *items = off;
+        return xchg(c, [&](const Slab& s) { return fine_field(c, s, s.zf, R); });
+    }
+    if (c->fused3d) {
+        // 3D: z2 = omega D^-1 r + P e, zf = z2 + omega D^-1 (r - K z2), r.zf in one h8 kernel
+        for (Slab& s : c->sl) {
+            FineArgs a = fine_args(c, s, rc);
+            a.b = s.*r; a.Dinv = s.lv[0].Dinv; a.ec = cw ? s.lv[1].w : s.lv[1].z; a.gc = s.lv[1].g;
+            a.maskc = s.lv[1].mask; a.off0 = s.gl; a.y = s.zf; a.partial = c->partial + off;
+            off += fine_apply(FOP_POST3, a, c->stream);
             rc.launches++;
         }
         *items = off;
@@ -1051,10 +1082,21 @@ static mg_status setup_impl(mg_ctx* c, const mg_grid* grid, const double* E_e, c
     c->nu_paper = (c->nu == MG_NU_PAPER);
     c->fused2d = (dim == 2 && levels >= 2);
     c->unfused_coarse = getenv("MG_UNFUSED_COARSE") && atoi(getenv("MG_UNFUSED_COARSE")) == 1;
+    // (measured slower than the composed kernels on B200 -- more registers in a latency-bound
+    // kernel -- so opt-in with MG_FUSED3D=1; parity-tested either way)
+    c->fused3d = dim == 3 && levels >= 2 && c->opts.nu_pre == 1 && c->opts.nu_post == 1 && !c->unfused_coarse &&
+                 !getenv("MG_DENSE_H8") && getenv("MG_FUSED3D") && atoi(getenv("MG_FUSED3D")) == 1;
     fine_set_constants(dim, c->K0.data(), s);
     if (dim == 3) h8_set_constants(c->nu, s);
     if (dim == 2) fine2d_set_constants(c->K0.data(), s);
     galerkin_set_constants(dim, c->K0.data(), s);
+    {
+        const int na = 1 << dim, nl = dim * na;
+        std::vector<double> Mh((size_t)na * nl * nl);
+        galerkin_child_matrices(dim, c->K0.data(), Mh.data());
+        CU(cudaMalloc(&c->Mc, sizeof(double) * Mh.size()));
+        CU(cudaMemcpy(c->Mc, Mh.data(), sizeof(double) * Mh.size(), cudaMemcpyHostToDevice));
+    }
     stress_set_constants(dim, c->nu, s);
     const int NL = dim * (1 << dim);
     const bool edev = is_device_ptr(E_e), fdev = is_device_ptr(fixed);
@@ -1649,7 +1691,7 @@ mg_status mg_destroy(mg_handle c) {
             if (p) cudaFree(p);
         if (s.maskpad) cudaFree(s.maskpad);
     }
-    for (double* p : {c->Ainv, c->stg, c->cpack, c->cgath, c->gj_work, c->sums})
+    for (double* p : {c->Ainv, c->stg, c->cpack, c->cgath, c->gj_work, c->sums, c->Mc})
         if (p) cudaFree(p);
     if (c->ctl_mem) cudaFree(c->ctl_mem);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
