@@ -14,6 +14,8 @@
 // all R right-hand sides, so the stencil is read once per kernel.  Neighbour values (z1, w,
 // z2, e) go through shared memory.  Slabs: off0 shifts axis-0 parities (coarse plane I is
 // fine plane 2I - off0); restriction sources are the slab-owned fine planes [fo0, fo1) only.
+#include <algorithm>
+
 #include "kernels.h"
 
 static constexpr int CT_I = 16, CT_J = 32;   // thread tile (level-l nodes)
@@ -48,13 +50,15 @@ __global__ void __launch_bounds__(CT_I * CT_J, 1) coarse2d_down_kernel(LevelGeom
                                                                        const uint8_t* __restrict__ maskc,
                                                                        const double* __restrict__ r, double* rc,
                                                                        int R, double omega, int off0, int fo0, int fo1,
-                                                                       int nbj, const int* active, const int* done) {
+                                                                       int nbj, int rg, const int* active,
+                                                                       const int* done) {
     __shared__ double2 s_z[CT_I][CT_J];
     __shared__ double2 s_w[CT_I][CT_J];
     if (done && *done) return;
     const int ti = threadIdx.x / CT_J, tj = threadIdx.x % CT_J;
     const int bI = blockIdx.x / nbj, bJ = blockIdx.x % nbj;
     const int I0 = bI * DN_CI, J0 = bJ * DN_CJ;
+    const int k0 = blockIdx.y * rg, k1 = min(R, k0 + rg);   // this CTA's right-hand sides
     const int fi = 2 * I0 - off0 - 2 + ti, fj = 2 * J0 - 2 + tj;
     const int n0 = g.nn[0], n1 = g.nn[1];
     const bool ok = fi >= 0 && fi < n0 && fj >= 0 && fj < n1;
@@ -74,10 +78,10 @@ __global__ void __launch_bounds__(CT_I * CT_J, 1) coarse2d_down_kernel(LevelGeom
     const int mc = cok ? maskc[cnode] : 3;
     // software pipeline over the RHS: r of RHS k+1 is in flight while RHS k is processed
     double2 rn = make_double2(0.0, 0.0);
-    if (ok) rn = *reinterpret_cast<const double2*>(r + 2 * node);
-    for (int k = 0; k < R; ++k) {
+    if (ok) rn = *reinterpret_cast<const double2*>(r + (long long)k0 * g.ndof + 2 * node);
+    for (int k = k0; k < k1; ++k) {
         const double rx = rn.x, ry = rn.y;
-        if (ok && k + 1 < R) rn = *reinterpret_cast<const double2*>(r + (long long)(k + 1) * g.ndof + 2 * node);
+        if (ok && k + 1 < k1) rn = *reinterpret_cast<const double2*>(r + (long long)(k + 1) * g.ndof + 2 * node);
         if (active && !active[k]) continue;
         s_z[ti][tj] = make_double2(omega * dx * rx, omega * dy * ry);
         __syncthreads();
@@ -114,7 +118,7 @@ __global__ void __launch_bounds__(CT_I * CT_J, 1) coarse2d_up_kernel(LevelGeom g
                                                                      const uint8_t* __restrict__ maskc,
                                                                      const double* __restrict__ r,
                                                                      const double* __restrict__ ec, double* z, int R,
-                                                                     double omega, int off0, int nbj,
+                                                                     double omega, int off0, int nbj, int rg,
                                                                      const int* active, const int* done) {
     constexpr int CI = CT_I / 2 + 2, CJ = CT_J / 2 + 2;
     __shared__ double2 s_z[CT_I][CT_J];
@@ -123,6 +127,7 @@ __global__ void __launch_bounds__(CT_I * CT_J, 1) coarse2d_up_kernel(LevelGeom g
     const int ti = threadIdx.x / CT_J, tj = threadIdx.x % CT_J;
     const int bI = blockIdx.x / nbj, bJ = blockIdx.x % nbj;
     const int fi0 = bI * UP_OI - 1, fj0 = bJ * UP_OJ - 1;
+    const int k0 = blockIdx.y * rg, k1 = min(R, k0 + rg);   // this CTA's right-hand sides
     const int fi = fi0 + ti, fj = fj0 + tj;
     const int n0 = g.nn[0], n1 = g.nn[1];
     const bool ok = fi >= 0 && fi < n0 && fj >= 0 && fj < n1;
@@ -146,12 +151,12 @@ __global__ void __launch_bounds__(CT_I * CT_J, 1) coarse2d_up_kernel(LevelGeom g
     const int emc = eok ? maskc[ecn] : 3;
     // software pipeline over the RHS: e and r of RHS k+1 are in flight while RHS k is processed
     double2 en = make_double2(0.0, 0.0), rn = make_double2(0.0, 0.0);
-    if (eok) en = *reinterpret_cast<const double2*>(ec + 2 * ecn);
-    if (ok) rn = *reinterpret_cast<const double2*>(r + 2 * node);
-    for (int k = 0; k < R; ++k) {
+    if (eok) en = *reinterpret_cast<const double2*>(ec + (long long)k0 * gc.ndof + 2 * ecn);
+    if (ok) rn = *reinterpret_cast<const double2*>(r + (long long)k0 * g.ndof + 2 * node);
+    for (int k = k0; k < k1; ++k) {
         const double2 ev = en;
         const double rx = rn.x, ry = rn.y;
-        if (k + 1 < R) {
+        if (k + 1 < k1) {
             if (eok) en = *reinterpret_cast<const double2*>(ec + (long long)(k + 1) * gc.ndof + 2 * ecn);
             if (ok) rn = *reinterpret_cast<const double2*>(r + (long long)(k + 1) * g.ndof + 2 * node);
         }
@@ -180,18 +185,31 @@ __global__ void __launch_bounds__(CT_I * CT_J, 1) coarse2d_up_kernel(LevelGeom g
     }
 }
 
+// RHS per CTA: all of them on large levels (stencil read once); on small levels the RHS are
+// spread over CTAs so the grid still covers the SMs (the stencil then comes from L2)
+static int rhs_group(int tiles, int R) {
+    const int want = 2 * 148;
+    if (tiles >= want) return R;
+    const int groups = std::min(R, (want + tiles - 1) / tiles);
+    return (R + groups - 1) / groups;
+}
+
 void coarse2d_down(const LevelGeom& g, const LevelGeom& gc, const double* st, const double* Dinv,
                    const uint8_t* mask, const uint8_t* maskc, const double* r, double* rc, int R, double omega,
                    int off0, int fo0, int fo1, const int* active, const int* done, cudaStream_t s) {
     const int nbi = (gc.nn[0] + DN_CI - 1) / DN_CI, nbj = (gc.nn[1] + DN_CJ - 1) / DN_CJ;
-    coarse2d_down_kernel<<<nbi * nbj, CT_I * CT_J, 0, s>>>(g, gc, st, Dinv, mask, maskc, r, rc, R, omega, off0, fo0,
-                                                         fo1, nbj, active, done);
+    const int rg = rhs_group(nbi * nbj, R);
+    dim3 grid(nbi * nbj, (R + rg - 1) / rg);
+    coarse2d_down_kernel<<<grid, CT_I * CT_J, 0, s>>>(g, gc, st, Dinv, mask, maskc, r, rc, R, omega, off0, fo0, fo1,
+                                                    nbj, rg, active, done);
 }
 
 void coarse2d_up(const LevelGeom& g, const LevelGeom& gc, const double* st, const double* Dinv, const uint8_t* mask,
                  const uint8_t* maskc, const double* r, const double* ec, double* z, int R, double omega, int off0,
                  const int* active, const int* done, cudaStream_t s) {
     const int nbi = (g.nn[0] + UP_OI - 1) / UP_OI, nbj = (g.nn[1] + UP_OJ - 1) / UP_OJ;
-    coarse2d_up_kernel<<<nbi * nbj, CT_I * CT_J, 0, s>>>(g, gc, st, Dinv, mask, maskc, r, ec, z, R, omega, off0, nbj,
-                                                       active, done);
+    const int rg = rhs_group(nbi * nbj, R);
+    dim3 grid(nbi * nbj, (R + rg - 1) / rg);
+    coarse2d_up_kernel<<<grid, CT_I * CT_J, 0, s>>>(g, gc, st, Dinv, mask, maskc, r, ec, z, R, omega, off0, nbj, rg,
+                                                  active, done);
 }

@@ -259,3 +259,16 @@ def test_profile_kernels_leaves_solver_state_valid(name):
     x2 = torch.empty_like(rhs)
     mg.mgcg_solve(h, rhs, 1e-10, x2)
     assert torch.equal(x1, x2)
+
+
+@pytest.mark.parametrize("name", ["T3b", "T3c"])
+def test_fused3d_variant_parity(name, monkeypatch):
+    """The opt-in fused 3D fine V-cycle halves (MG_FUSED3D=1) give the same solution."""
+    import paper_1909_13585_b200 as mg
+    monkeypatch.setenv("MG_FUSED3D", "1")
+    cfg, inp, K = case(name)
+    U = direct(name)
+    h = handle(name)
+    x = torch.empty((cfg.nrhs, U.shape[1]), dtype=torch.float64, device=DEV)
+    rep = mg.mgcg_solve(h, to_dev(inp["rhs"]), cfg.tol, x)
+    assert rel(x.cpu().numpy(), U).max() < 1e-8, rep
