@@ -188,47 +188,57 @@ void dense_spd_inverse(double* A, long long npad, double* work, int* d_status, c
     }
 }
 
-// z[r][i] = sum_j Ainv[i][j] rvec[r][j]; one warp per row (4 rows per CTA so the grid
-// covers all SMs), up to RB vectors per pass, column loop unrolled for memory-level
-// parallelism (Ainv and the vectors are L2-resident: n_L <= ~4k).
+// z[r][i] = sum_j Ainv[i][j] rvec[r][j]: 4 rows per CTA (one warp each), the RB right-hand
+// sides staged through shared memory in column chunks so every Ainv row is streamed once and
+// the vectors come from shared memory (Ainv and the vectors are L2-resident, n_L <= ~4k).
+static constexpr int DA_ROWS = 4, DA_CHK = 256;
+
 template <int RB>
-__global__ void __launch_bounds__(128) dense_apply_kernel(const double* __restrict__ Ainv, long long ld, long long n,
-                                                          const double* __restrict__ rv, double* __restrict__ z, int R,
-                                                          int r0, const int* active, const int* done) {
-    const int lane = threadIdx.x & 31;
-    long long i = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (i >= n) return;
+__global__ void __launch_bounds__(32 * DA_ROWS) dense_apply_kernel(const double* __restrict__ Ainv, long long ld,
+                                                                   long long n, const double* __restrict__ rv,
+                                                                   double* __restrict__ z, int R, int r0,
+                                                                   const int* active, const int* done) {
+    __shared__ double s_r[RB][DA_CHK];
     if (done && *done) return;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const long long i = (long long)blockIdx.x * DA_ROWS + w;
     const int nr = min(RB, R - r0);
-    bool act[RB];
-#pragma unroll
-    for (int q = 0; q < RB; ++q) act[q] = q < nr && (!active || active[r0 + q]);
     double acc[RB];
 #pragma unroll
     for (int q = 0; q < RB; ++q) acc[q] = 0.0;
-    const double* row = Ainv + i * ld;
-#pragma unroll 4
-    for (long long j = lane; j < n; j += 32) {
-        const double a = row[j];
+    const double* row = Ainv + (i < n ? i : 0) * ld;
+    for (long long j0 = 0; j0 < n; j0 += DA_CHK) {
+        const int len = (int)(n - j0 < DA_CHK ? n - j0 : DA_CHK);
+        for (int e = threadIdx.x; e < RB * DA_CHK; e += 32 * DA_ROWS) {
+            const int q = e / DA_CHK, jj = e % DA_CHK;
+            s_r[q][jj] = (q < nr && jj < len) ? rv[(long long)(r0 + q) * n + j0 + jj] : 0.0;
+        }
+        __syncthreads();
+        if (i < n) {
+            for (int jj = lane; jj < len; jj += 32) {
+                const double a = row[j0 + jj];
 #pragma unroll
-        for (int q = 0; q < RB; ++q)
-            if (act[q]) acc[q] = fma(a, __ldg(rv + (long long)(r0 + q) * n + j), acc[q]);
+                for (int q = 0; q < RB; ++q) acc[q] = fma(a, s_r[q][jj], acc[q]);
+            }
+        }
+        __syncthreads();
     }
+    if (i >= n) return;
 #pragma unroll
     for (int q = 0; q < RB; ++q) {
-        double v = warp_sum(acc[q]);
-        if (lane == 0 && act[q]) z[(long long)(r0 + q) * n + i] = v;
+        const double v = warp_sum(acc[q]);
+        if (lane == 0 && q < nr && (!active || active[r0 + q])) z[(long long)(r0 + q) * n + i] = v;
     }
 }
 
 void dense_apply(const double* Ainv, long long ld, long long n, const double* r, double* z, int R, const int* active,
                  const int* done, cudaStream_t s) {
-    unsigned bl = (unsigned)((n + 3) / 4);
+    unsigned bl = (unsigned)((n + DA_ROWS - 1) / DA_ROWS);
     for (int r0 = 0; r0 < R;) {
         int rem = R - r0;
-        if (rem > 8) { dense_apply_kernel<16><<<bl, 128, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); r0 += 16; }
-        else if (rem > 4) { dense_apply_kernel<8><<<bl, 128, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); r0 += 8; }
-        else if (rem > 1) { dense_apply_kernel<4><<<bl, 128, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); r0 += 4; }
-        else { dense_apply_kernel<1><<<bl, 128, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); r0 += 1; }
+        if (rem > 8) { dense_apply_kernel<16><<<bl, 32 * DA_ROWS, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); r0 += 16; }
+        else if (rem > 4) { dense_apply_kernel<8><<<bl, 32 * DA_ROWS, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); r0 += 8; }
+        else if (rem > 1) { dense_apply_kernel<4><<<bl, 32 * DA_ROWS, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); r0 += 4; }
+        else { dense_apply_kernel<1><<<bl, 32 * DA_ROWS, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); r0 += 1; }
     }
 }
