@@ -61,8 +61,7 @@ __device__ __forceinline__ double K2(int r, int c) {
 static constexpr int prefetch_depth(int op) {
     return op == M2_POST ? MG_PD_POST : op == M2_RESTRICT ? MG_PD_RESTRICT : op == M2_CGP ? MG_PD_CGP : 2;
 }
-static constexpr int CH = 64;     // node planes per chunk
-static constexpr int CCH = 32;    // coarse rows per chunk (M2_RESTRICT)
+static constexpr int CH_MAX = 64; // node planes per chunk (halved on small grids, see march2_chunk)
 static constexpr int WPB = 4;     // warps per CTA (independent)
 // cap at 170 registers so 3 CTAs (12 warps) fit per SM (POST would otherwise take 185)
 static constexpr int march_minb(int op) {
@@ -198,7 +197,7 @@ struct Ops {
 
 // SLAB = false: single slab (off0 = 0, every plane owned) -- the slab checks compile away
 template <int OP, bool C03, bool SLAB>
-__global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2Args a, int nct, int nch) {
+__global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2Args a, int nct, int nch, int chl) {
     constexpr int CS = (OP == M2_RESTRICT) ? 28 : 30;      // owned columns per warp
     constexpr int LOFF = (OP == M2_RESTRICT) ? 2 : 1;      // lane of the first owned column
     const int lane = threadIdx.x & 31;
@@ -220,15 +219,15 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
     int i0, i1, own0, own1, I0 = 0, I1 = 0;
     if (OP == M2_RESTRICT) {
         const int nc0 = a.gc.nn[0];
-        I0 = ch * CCH;
-        I1 = min(I0 + CCH, nc0);
+        I0 = ch * (chl / 2);
+        I1 = min(I0 + chl / 2, nc0);
         i0 = max(0, 2 * I0 - 1 - off0);
         i1 = min(2 * I1 - off0, n0);
         own0 = max(0, 2 * I0 - off0);
         own1 = i1;
     } else {
-        i0 = ch * CH;
-        i1 = min(i0 + CH, n0);
+        i0 = ch * chl;
+        i1 = min(i0 + chl, n0);
         own0 = i0;
         own1 = i1;
     }
@@ -481,36 +480,41 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
     }
 }
 
-int march2_items(int op, const LevelGeom& g, const LevelGeom* gc) {
-    if (op == M2_RESTRICT) {
-        const int nct = (g.nn[1] + 27) / 28;
-        const int nch = (gc->nn[0] + CCH - 1) / CCH;
-        return nct * nch;
+// Chunk length along axis 0 (planes; RESTRICT: coarse rows = chl / 2): CH_MAX unless the
+// grid then has too few warps to fill the SMs (small levels / configs), down to 4 planes.
+static int march2_chunk(int op, const LevelGeom& g, const LevelGeom* gc, int R, int* nct_out, int* nch_out) {
+    const int nct = op == M2_RESTRICT ? (g.nn[1] + 27) / 28 : (g.nn[1] + 29) / 30;
+    const long long want = 3LL * 148 * WPB;   // resident warps at 3 CTAs / SM
+    int chl = CH_MAX, nch = 0;
+    for (;;) {
+        nch = op == M2_RESTRICT ? (gc->nn[0] + chl / 2 - 1) / (chl / 2) : (g.nn[0] + chl - 1) / chl;
+        if (chl <= 4 || (long long)R * nct * nch >= want) break;
+        chl /= 2;
     }
-    const int nct = (g.nn[1] + 29) / 30;
-    const int nch = (g.nn[0] + CH - 1) / CH;
+    *nct_out = nct;
+    *nch_out = nch;
+    return chl;
+}
+
+int march2_items(int op, const LevelGeom& g, const LevelGeom* gc, int R) {
+    int nct, nch;
+    march2_chunk(op, g, gc, R, &nct, &nch);
     return nct * nch;
 }
 
 template <int OP>
 static void launch2(const March2Args& a, bool c03, cudaStream_t s) {
     int nct, nch;
-    if (OP == M2_RESTRICT) {
-        nct = (a.g.nn[1] + 27) / 28;
-        nch = (a.gc.nn[0] + CCH - 1) / CCH;
-    } else {
-        nct = (a.g.nn[1] + 29) / 30;
-        nch = (a.g.nn[0] + CH - 1) / CH;
-    }
+    const int chl = march2_chunk(OP, a.g, &a.gc, a.R, &nct, &nch);
     const long long warps = (long long)a.R * nct * nch;
     const unsigned blocks = (unsigned)((warps + WPB - 1) / WPB);
     const bool slab = a.off0 != 0 || a.so0 != 0 || a.so1 != a.g.nn[0];
     if (slab) {
-        if (c03) march2_kernel<OP, true, true><<<blocks, 32 * WPB, 0, s>>>(a, nct, nch);
-        else march2_kernel<OP, false, true><<<blocks, 32 * WPB, 0, s>>>(a, nct, nch);
+        if (c03) march2_kernel<OP, true, true><<<blocks, 32 * WPB, 0, s>>>(a, nct, nch, chl);
+        else march2_kernel<OP, false, true><<<blocks, 32 * WPB, 0, s>>>(a, nct, nch, chl);
     } else {
-        if (c03) march2_kernel<OP, true, false><<<blocks, 32 * WPB, 0, s>>>(a, nct, nch);
-        else march2_kernel<OP, false, false><<<blocks, 32 * WPB, 0, s>>>(a, nct, nch);
+        if (c03) march2_kernel<OP, true, false><<<blocks, 32 * WPB, 0, s>>>(a, nct, nch, chl);
+        else march2_kernel<OP, false, false><<<blocks, 32 * WPB, 0, s>>>(a, nct, nch, chl);
     }
 }
 
@@ -523,5 +527,5 @@ int march2_apply(int op, const March2Args& a, bool c03, cudaStream_t s) {
         case M2_RESTRICT: launch2<M2_RESTRICT>(a, c03, s); break;
         default: launch2<M2_POST>(a, c03, s); break;
     }
-    return march2_items(op, a.g, &a.gc);
+    return march2_items(op, a.g, &a.gc, a.R);
 }

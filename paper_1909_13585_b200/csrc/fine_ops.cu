@@ -32,7 +32,7 @@ static constexpr int CHUNK2 = 32;
 static constexpr int CHUNK3 = 16;
 
 int fine_items(const LevelGeom& g, int R) {
-    if (g.dim == 2) return march2_items(M2_MATVEC, g, nullptr);
+    if (g.dim == 2) return march2_items(M2_MATVEC, g, nullptr, R);
     if (!getenv("MG_DENSE_H8")) return h8_items(g, R);
     int ncols = g.nn[g.dim - 1];
     int nct = (ncols + COLS_PER_WARP - 1) / COLS_PER_WARP;

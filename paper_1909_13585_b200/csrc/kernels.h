@@ -109,7 +109,7 @@ void pad2_vectors_planes(const LevelGeom& g, const Pad2& p, int R, const uint8_t
 void unpad2_vectors_planes(const LevelGeom& g, const Pad2& p, int R, int p0, int nplanes, const double* src,
                            double* dst, long long dst_ndof, cudaStream_t s);
 int march2_apply(int op, const March2Args& a, bool nu_paper, cudaStream_t s);
-int march2_items(int op, const LevelGeom& g, const LevelGeom* gc);
+int march2_items(int op, const LevelGeom& g, const LevelGeom* gc, int R);
 
 // ---------------------------------------------------------------- coarse levels (assembled stencils)
 enum CoarseOp { COP_MATVEC = 0, COP_RESID = 1, COP_JACOBI = 2 };

@@ -181,6 +181,7 @@ struct mg_ctx {
     double* h_dbl = nullptr;     // bb, rr, tt [64] each
     int* d_status = nullptr;
     cudaGraphExec_t g_init = nullptr, g_restart = nullptr, g_iter = nullptr, g_true = nullptr;
+    cudaGraphExec_t g_loop = nullptr;   // device-side CG loop (conditional WHILE node around g_iter's body)
     long long n_init = 0, n_restart = 0, n_iter = 0, n_true = 0;
     int graph_R = -1;
     double graph_tol = -1.0;
@@ -459,7 +460,7 @@ static void free_vectors(mg_ctx* c) {
     double** cv[] = {&c->partial, &c->stage, &c->stage2, &c->cr, &c->cz, &c->xtmp};
     for (auto p : cv)
         if (*p) { cudaFree(*p); *p = nullptr; }
-    cudaGraphExec_t* gs[] = {&c->g_init, &c->g_restart, &c->g_iter, &c->g_true};
+    cudaGraphExec_t* gs[] = {&c->g_init, &c->g_restart, &c->g_iter, &c->g_true, &c->g_loop};
     for (auto g : gs)
         if (*g) { cudaGraphExecDestroy(*g); *g = nullptr; }
     c->graph_R = -1;
@@ -491,7 +492,7 @@ static mg_status ensure_vectors(mg_ctx* c, int R) {
         long long items = fine_items(s.lv[0].g, R);
         if (c->dim == 2) {
             for (int op : {M2_CGP, M2_RESTRICT, M2_POST, M2_RESID, M2_JACOBI}) {
-                long long it = march2_items(op, s.lv[0].g, c->L > 1 ? &s.lv[1].g : &s.lv[0].g);
+                long long it = march2_items(op, s.lv[0].g, c->L > 1 ? &s.lv[1].g : &s.lv[0].g, R);
                 items = std::max(items, it);
             }
         }
@@ -988,8 +989,52 @@ static mg_status record_true(mg_ctx* c, int R) {
     return dot_finish(c, R, &Slab::t, &Slab::t, SM_TRUE);
 }
 
+// WHILE condition of the device-side loop: continue while some RHS is active, no breakdown
+// and no RHS has reached max_iter (the host loop's test, evaluated on the device).
+__global__ void loop_cond_kernel(cudaGraphConditionalHandle h, const int* done, const int* status,
+                                 const int* iters, int R, int maxit) {
+    int go = !*done && !*status;
+    for (int r = 0; go && r < R; ++r) go = iters[r] < maxit;
+    cudaGraphSetConditional(h, go ? 1u : 0u);
+}
+
+// g_loop = [cond] -> WHILE(cond) { two CG iterations ; cond }: the whole iteration runs
+// without host round trips (CUDA 12.4+ conditional graph nodes).  Single rank only (NCCL
+// calls stay in host-driven graphs).
+static mg_status build_loop_graph(mg_ctx* c, int R, double tol) {
+    cudaGraph_t g = nullptr;
+    CU(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h;
+    CU(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
+    const int maxit = c->opts.max_iter;
+    CU(cudaStreamBeginCaptureToGraph(c->stream, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    loop_cond_kernel<<<1, 1, 0, c->stream>>>(h, c->ctl.done, c->ctl.status, c->ctl.iters, R, maxit);
+    cudaGraph_t gc = nullptr;
+    CU(cudaStreamEndCapture(c->stream, &gc));
+    cudaGraphNode_t first = nullptr;
+    size_t nn = 1;
+    CU(cudaGraphGetNodes(g, &first, &nn));
+    cudaGraphNodeParams np{};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t wn = nullptr;
+    CU(cudaGraphAddNode(&wn, g, &first, 1, &np));
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    CU(cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    mg_status st = record_iter(c, R, tol);
+    loop_cond_kernel<<<1, 1, 0, c->stream>>>(h, c->ctl.done, c->ctl.status, c->ctl.iters, R, maxit);
+    cudaGraph_t bc = nullptr;
+    CU(cudaStreamEndCapture(c->stream, &bc));
+    TRY(st);
+    CU(cudaGraphInstantiate(&c->g_loop, g, 0));
+    CU(cudaGraphDestroy(g));
+    return MG_OK;
+}
+
 static mg_status build_graphs(mg_ctx* c, int R, double tol) {
-    for (cudaGraphExec_t* g : {&c->g_init, &c->g_restart, &c->g_iter, &c->g_true})
+    for (cudaGraphExec_t* g : {&c->g_init, &c->g_restart, &c->g_iter, &c->g_true, &c->g_loop})
         if (*g) { cudaGraphExecDestroy(*g); *g = nullptr; }
     TRY(capture_begin(c));
     TRY(captured(c, record_restart(c, R)));
@@ -1012,6 +1057,15 @@ static mg_status build_graphs(mg_ctx* c, int R, double tol) {
     TRY(capture_begin(c));
     TRY(captured(c, record_true(c, R)));
     TRY(capture_end(c, &c->g_true, &c->n_true));
+    if (c->comm.nranks == 1 && !getenv("MG_HOST_LOOP")) {
+        if (build_loop_graph(c, R, tol) != MG_OK) {   // fall back to the host-driven loop
+            cudaGraph_t g = nullptr;
+            cudaStreamEndCapture(c->stream, &g);
+            if (g) cudaGraphDestroy(g);
+            cudaGetLastError();
+            if (c->g_loop) { cudaGraphExecDestroy(c->g_loop); c->g_loop = nullptr; }
+        }
+    }
     c->graph_R = R;
     CHECK_LAUNCH();
     return MG_OK;
@@ -1346,9 +1400,22 @@ mg_status mgcg_solve(mg_handle c, const double* rhs, int nrhs, double tol, doubl
     double* hd = c->h_dbl;    // bb[64] rr[64] tt[64]
     const int maxit = c->opts.max_iter;
     int restarts = 0;
+    int host_mx = 0;   // largest per-RHS iteration count seen by the host (launch accounting)
     mg_status result = MG_OK;
     for (;;) {
         // iterate until all RHS converged (recursive residual) or the cap
+        if (c->g_loop) {
+            const int mx0 = host_mx;
+            CU(cudaGraphLaunch(c->g_loop, s));
+            ++glaunch;
+            CU(cudaMemcpyAsync(hp, c->ctl.done, sizeof(int) * 2, cudaMemcpyDeviceToHost, s));
+            CU(cudaMemcpyAsync(hp + 2, c->ctl.iters, sizeof(int) * nrhs, cudaMemcpyDeviceToHost, s));
+            CU(cudaStreamSynchronize(s));
+            int mx1 = 0;
+            for (int k = 0; k < nrhs; ++k) mx1 = hp[2 + k] > mx1 ? hp[2 + k] : mx1;
+            klaunch += 1 + (long long)((mx1 - mx0 + 1) / 2) * (c->n_iter + 1);
+            host_mx = mx1;
+        } else
         for (;;) {
             CU(cudaMemcpyAsync(hp, c->ctl.done, sizeof(int) * 2, cudaMemcpyDeviceToHost, s));
             CU(cudaMemcpyAsync(hp + 2, c->ctl.iters, sizeof(int) * nrhs, cudaMemcpyDeviceToHost, s));
