@@ -77,8 +77,6 @@ __device__ __forceinline__ double KH(int r, int c) {
     return c_Kh[r * 24 + c];
 }
 
-static constexpr int TR = 8;        // node rows per CTA (warps)
-static constexpr int TOWN_R = 6;    // owned rows
 static constexpr int TOWN_C = 30;   // owned columns
 static constexpr int HCH = 32;      // node planes per chunk
 
@@ -91,10 +89,13 @@ struct H8Plane {              // per-thread data of one node plane
     int m;                    // fixed bits
 };
 
-template <int OP, bool C03, int MINB>
+// TR node rows per CTA (one warp each), TR - 2 owned; MINB CTAs per SM (register cap)
+template <int OP, bool C03, int TR, int MINB>
 __global__ void __launch_bounds__(32 * TR, MINB) h8_kernel(FineArgs a, int ntc, int ntr, int nch, int hch) {
-    __shared__ double s_fwd[TR][6][32];   // edge (m, d) x 3 comps of plane P, per row
-    __shared__ double s_inv[TR][6][32];   // inverse edge contributions for row + 1
+    constexpr int TOWN_R = TR - 2;
+    extern __shared__ double h8_smem[];
+    double (*s_fwd)[6][32] = reinterpret_cast<double (*)[6][32]>(h8_smem);             // edge (m, d) x 3 comps, per row
+    double (*s_inv)[6][32] = reinterpret_cast<double (*)[6][32]>(h8_smem + TR * 6 * 32); // inverse edges for row + 1
     const int lane = threadIdx.x & 31, row = threadIdx.x >> 5;
     const int nt = ntc * ntr;
     const int bid = blockIdx.x;
@@ -336,20 +337,28 @@ __global__ void __launch_bounds__(32 * TR, MINB) h8_kernel(FineArgs a, int ntc, 
     }
 }
 
-static int h8_minb() {
+// variant: 8 rows x 1 CTA/SM (default), 16 rows x 1 CTA/SM (128-register cap), or 8 rows x
+// 2 CTAs/SM (128-register cap); MG_H8_VARIANT = 0 / 1 / 2
+// Default per op from B200 A/B (C4/C5): CGP 16 rows (better row efficiency outweighs the
+// spills of the 128-register cap), the other ops 8 rows x 1 CTA/SM.
+static int h8_variant(int op) {
     static int v = [] {
-        const char* e = getenv("MG_H8_MINB");
-        return e && atoi(e) == 2 ? 2 : 1;
+        const char* e = getenv("MG_H8_VARIANT");
+        return e ? atoi(e) : -1;
     }();
-    return v;
+    if (v >= 0) return v;
+    return op == FOP_CGP ? 1 : 0;
 }
+static int h8_rows(int op) { return h8_variant(op) == 1 ? 16 : 8; }
+static int h8_slots(int op) { return 148 * (h8_variant(op) == 2 ? 2 : 1); }
 
 // Chunking along axis 0: between HCH/2 and 2 HCH planes per chunk, picked so that the CTA
 // count fills the resident slots (148 SMs x CTAs per SM) with the smallest tail wave.
-static void h8_chunks(const LevelGeom& g, int R, int* nch_out, int* hch_out) {
+static void h8_chunks(int op, const LevelGeom& g, int R, int* nch_out, int* hch_out) {
+    const int town_r = h8_rows(op) - 2;
     const int ntc = (g.nn[2] + TOWN_C - 1) / TOWN_C;
-    const int ntr = (g.nn[1] + TOWN_R - 1) / TOWN_R;
-    const long long slots = 148LL * h8_minb();
+    const int ntr = (g.nn[1] + town_r - 1) / town_r;
+    const long long slots = h8_slots(op);
     const int n0 = g.nn[0];
     int best = (n0 + HCH - 1) / HCH;
     double best_eff = -1.0;
@@ -366,29 +375,48 @@ static void h8_chunks(const LevelGeom& g, int R, int* nch_out, int* hch_out) {
     *hch_out = (n0 + best - 1) / best;
 }
 
-int h8_items(const LevelGeom& g, int R) {
+static int h8_items_op(int op, const LevelGeom& g, int R) {
+    const int town_r = h8_rows(op) - 2;
     const int ntc = (g.nn[2] + TOWN_C - 1) / TOWN_C;
-    const int ntr = (g.nn[1] + TOWN_R - 1) / TOWN_R;
+    const int ntr = (g.nn[1] + town_r - 1) / town_r;
     int nch, hch;
-    h8_chunks(g, R, &nch, &hch);
+    h8_chunks(op, g, R, &nch, &hch);
     return ntc * ntr * nch;
+}
+
+// partial items: the largest over the ops (buffers are sized with this)
+int h8_items(const LevelGeom& g, int R) {
+    int m = 0;
+    for (int op = 0; op <= FOP_POST3; ++op) m = std::max(m, h8_items_op(op, g, R));
+    return m;
+}
+
+template <int OP, int TR, int MINB>
+static void launch_h8_v(const FineArgs& a, int ntc, int ntr, int nch, int hch, unsigned nb, cudaStream_t s) {
+    const size_t smem = sizeof(double) * 2 * TR * 6 * 32;
+    static bool attr = [&] {
+        cudaFuncSetAttribute(h8_kernel<OP, true, TR, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(h8_kernel<OP, false, TR, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        return true;
+    }();
+    (void)attr;
+    if (a.nu_paper) h8_kernel<OP, true, TR, MINB><<<nb, 32 * TR, smem, s>>>(a, ntc, ntr, nch, hch);
+    else h8_kernel<OP, false, TR, MINB><<<nb, 32 * TR, smem, s>>>(a, ntc, ntr, nch, hch);
 }
 
 template <int OP>
 static void launch_h8(const FineArgs& a, cudaStream_t s) {
     const LevelGeom& g = a.g;
+    const int town_r = h8_rows(OP) - 2;
     const int ntc = (g.nn[2] + TOWN_C - 1) / TOWN_C;
-    const int ntr = (g.nn[1] + TOWN_R - 1) / TOWN_R;
+    const int ntr = (g.nn[1] + town_r - 1) / town_r;
     int nch, hch;
-    h8_chunks(g, a.R, &nch, &hch);
-    const long long blocks = (long long)ntc * ntr * nch * a.R;
-    const unsigned nb = (unsigned)blocks;
-    if (h8_minb() == 1) {
-        if (a.nu_paper) h8_kernel<OP, true, 1><<<nb, 32 * TR, 0, s>>>(a, ntc, ntr, nch, hch);
-        else h8_kernel<OP, false, 1><<<nb, 32 * TR, 0, s>>>(a, ntc, ntr, nch, hch);
-    } else {
-        if (a.nu_paper) h8_kernel<OP, true, 2><<<nb, 32 * TR, 0, s>>>(a, ntc, ntr, nch, hch);
-        else h8_kernel<OP, false, 2><<<nb, 32 * TR, 0, s>>>(a, ntc, ntr, nch, hch);
+    h8_chunks(OP, g, a.R, &nch, &hch);
+    const unsigned nb = (unsigned)((long long)ntc * ntr * nch * a.R);
+    switch (h8_variant(OP)) {
+        case 1: launch_h8_v<OP, 16, 1>(a, ntc, ntr, nch, hch, nb, s); break;
+        case 2: launch_h8_v<OP, 8, 2>(a, ntc, ntr, nch, hch, nb, s); break;
+        default: launch_h8_v<OP, 8, 1>(a, ntc, ntr, nch, hch, nb, s); break;
     }
 }
 
@@ -401,5 +429,5 @@ int h8_apply(int op, const FineArgs& a, cudaStream_t s) {
         case FOP_POST3: launch_h8<FOP_POST3>(a, s); break;
         default: launch_h8<FOP_CGP>(a, s); break;
     }
-    return h8_items(a.g, a.R);
+    return h8_items_op(op, a.g, a.R);
 }
