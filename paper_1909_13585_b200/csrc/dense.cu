@@ -108,6 +108,15 @@ __global__ void __launch_bounds__(256) gj_update_kernel(double* A, long long ld,
     __shared__ double Rs[GJ_NB][64 + 1];
     const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
     const long long i0 = (long long)blockIdx.y * 64, j0 = (long long)blockIdx.x * 64;
+    // the A tile is read up front so its latency overlaps the panel loads and the product
+    double aold[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const long long i = i0 + ty + 16 * a, j = j0 + tx + 16 * b;
+            aold[a][b] = (i < n && j < n) ? A[i * ld + j] : 0.0;
+        }
     for (int e = threadIdx.x; e < 64 * GJ_NB; e += 256) {
         int r = e / GJ_NB, t = e % GJ_NB;
         long long i = i0 + r;
@@ -141,7 +150,7 @@ __global__ void __launch_bounds__(256) gj_update_kernel(double* A, long long ld,
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
             long long j = j0 + tx + 16 * b;
-            if (j < n) A[i * ld + j] -= acc[a][b];
+            if (j < n) A[i * ld + j] = aold[a][b] - acc[a][b];
         }
     }
 }
