@@ -220,15 +220,24 @@ def run_ours(args, cfg):
         hx = torch.empty((R, n), dtype=torch.float64).pin_memory().numpy()
         hy = torch.empty((max(nphi, 1), n), dtype=torch.float64).pin_memory().numpy()
 
+        e2e_ph = np.zeros(3)
+
         def e2e_step():
+            t_a = time.perf_counter()
             mg.mg_update_modulus(h, hE)
+            torch.cuda.synchronize()
+            t_b = time.perf_counter()
             rep = mg.mgcg_solve(h, hrhs, cfg.tol, hx)
+            t_c = time.perf_counter()
             if nphi:
                 mg.stress_stiffness_apply(h, hEs, np.ascontiguousarray(hx[0]), hphi, hy[:nphi])
+            t_d = time.perf_counter()
+            e2e_ph[:] += (t_b - t_a, t_c - t_b, t_d - t_c)
             return rep
 
         e2e_step()
         torch.cuda.synchronize()
+        e2e_ph[:] = 0.0
         if ws > 1:
             torch.distributed.barrier()
         t1 = time.perf_counter()
@@ -246,7 +255,9 @@ def run_ours(args, cfg):
         h2d = 8 * (inp["E"].size + R * n + (inp["Es"].size + n + nphi * n if nphi else 0))
         d2h = 8 * (R * n + nphi * n)
         e2e = {"value": its / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": 1e3 * dt / nst}
+               "ms_per_step": 1e3 * dt / nst,
+               "phase_ms": {"setup": 1e3 * e2e_ph[0] / nst, "solve": 1e3 * e2e_ph[1] / nst,
+                            "stress_apply": 1e3 * e2e_ph[2] / nst}}
 
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,

@@ -167,6 +167,8 @@ struct mg_ctx {
     long long cpack_cap = 0;
     double* gj_work = nullptr;
     double* Mc = nullptr;                        // Galerkin child matrices Q_c^T K0 Q_c
+    double* gstage = nullptr;                    // G(u) phi host-path staging
+    long long gstage_cap = 0;
     double* xtmp = nullptr;                      // NCCL reverse-add receive buffer
     long long xtmp_cap = 0;
     // shared solve state
@@ -1523,10 +1525,18 @@ mg_status stress_stiffness_apply(mg_handle c, const double* Es_e, const double* 
     double *dEs = nullptr, *du = nullptr, *dphi = nullptr, *dy = nullptr;
     const double *Es_src = Es_e, *u_src = u, *phi_src = phi;
     if (!dev) {
-        CU(cudaMallocAsync(&dEs, sizeof(double) * m, s));
-        CU(cudaMallocAsync(&du, sizeof(double) * n, s));
-        CU(cudaMallocAsync(&dphi, sizeof(double) * n * nphi, s));
-        CU(cudaMallocAsync(&dy, sizeof(double) * n * nphi, s));
+        // persistent staging (grown on demand): Es | u | phi | y
+        const long long need = m + n + 2 * n * nphi;
+        if (need > c->gstage_cap) {
+            if (c->gstage) cudaFree(c->gstage);
+            c->gstage = nullptr;
+            CU(cudaMalloc(&c->gstage, sizeof(double) * need));
+            c->gstage_cap = need;
+        }
+        dEs = c->gstage;
+        du = dEs + m;
+        dphi = du + n;
+        dy = dphi + n * nphi;
         CU(cudaMemcpyAsync(dEs, Es_e, sizeof(double) * m, cudaMemcpyDefault, s));
         CU(cudaMemcpyAsync(du, u, sizeof(double) * n, cudaMemcpyDefault, s));
         CU(cudaMemcpyAsync(dphi, phi, sizeof(double) * n * nphi, cudaMemcpyDefault, s));
@@ -1575,7 +1585,6 @@ mg_status stress_stiffness_apply(mg_handle c, const double* Es_e, const double* 
     CHECK_LAUNCH();
     if (!dev) {
         CU(cudaMemcpyAsync(y, dy, sizeof(double) * n * nphi, cudaMemcpyDefault, s));
-        for (double* p : {dEs, du, dphi, dy}) CU(cudaFreeAsync(p, s));
         CU(cudaStreamSynchronize(s));
     }
     stream_leave(c);
@@ -1758,7 +1767,7 @@ mg_status mg_destroy(mg_handle c) {
             if (p) cudaFree(p);
         if (s.maskpad) cudaFree(s.maskpad);
     }
-    for (double* p : {c->Ainv, c->stg, c->cpack, c->cgath, c->gj_work, c->sums, c->Mc})
+    for (double* p : {c->Ainv, c->stg, c->cpack, c->cgath, c->gj_work, c->sums, c->Mc, c->gstage})
         if (p) cudaFree(p);
     if (c->ctl_mem) cudaFree(c->ctl_mem);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
