@@ -165,6 +165,25 @@ mg_status mgcg_solve(mg_handle h, const double* rhs, int nrhs, double tol, doubl
 mg_status stress_stiffness_apply(mg_handle h, const double* Es_e, const double* u,
                                  const double* phi, int nphi, double* y);
 
+/* NEXT-1: adjoint right-hand sides of Eq. 5,
+ *   b_i = phi_i^T (grad_u G) phi_i,  i < nphi,
+ * i.e. b_i[k] = d(phi_i^T G(u) phi_i)/du_k; G is linear in u so b does not depend on u.
+ *   Es_e  device, nelem fp64 stress moduli (Eq. 2 :106);  phi (nphi, ndof) device;
+ *   b     (nphi, ndof) device output, zero on fixed DOFs (ready for mgcg_solve).
+ * Single slab (mg_setup) only this round.  Asynchronous. */
+mg_status mg_adjoint_rhs(mg_handle h, const double* Es_e, const double* phi, int nphi, double* b);
+/* NEXT-1: element sensitivities of simple buckling load factors, Eq. 4:
+ *   out[i][e] = dEk_e (phi_ie^T K_e0 phi_ie - lambda_i z_ie^T K_e0 u_e)
+ *             + lambda_i dEs_e phi_ie^T G_e0[u_e] phi_ie
+ * with dEk = dE_kappa/dx, dEs = dE_sigma/dx (Eq. 2, caller-supplied), u the state, phi_i the
+ * modes, z_i the adjoint solutions (K z_i = mg_adjoint_rhs(phi_i)).  phi, z (and u in the K
+ * term) are taken on the free DOFs.  Reading: this is d lambda_i / d x_e for modes
+ * normalised by phi^T (-G) phi = 1; for phi^T K phi = 1 multiply by lambda_i.
+ *   dEk, dEs (nelem), u (ndof), phi, z (nphi, ndof): device;  lambda: nphi values, host or
+ *   device;  out (nphi, nelem) device.  1 <= nphi <= MG_MAX_RHS.  Single slab.  Synchronous. */
+mg_status mg_eigen_sensitivity(mg_handle h, const double* dEk, const double* dEs, const double* u, const double* phi,
+                               const double* z, const double* lambda, int nphi, double* out);
+
 /* Diagnostics (used by the parity tests; all device pointers, asynchronous):
  * y = A_level x for nrhs vectors (level 0 = fine matrix-free K; level >= 1 =
  * Galerkin operator incl. identity rows at fixed DOFs). */

@@ -17,7 +17,7 @@ from ._lib import MgDist, MgError, MgGrid, MgOpts, MgReport, check, lib
 
 __all__ = [
     "Handle", "MgError", "mg_setup", "mg_setup_dist", "mg_partition", "mg_nccl_unique_id", "mg_local_info",
-    "mg_update_modulus", "mgcg_solve", "stress_stiffness_apply",
+    "mg_update_modulus", "mg_adjoint_rhs", "mg_eigen_sensitivity", "mgcg_solve", "stress_stiffness_apply",
     "mg_matvec", "mg_vcycle", "mg_restrict", "mg_prolong", "mg_level_info", "mg_get_diagonal",
     "mg_get_coarse_inverse", "mg_kernel_launches", "mg_profile_kernels", "mg_destroy", "lib_path",
 ]
@@ -156,6 +156,19 @@ def mgcg_solve(h, rhs, tol, x, raise_on_error=True):
 def stress_stiffness_apply(h, Es, u, phi, y):
     check(lib.stress_stiffness_apply(h.raw, _ptr(Es, np.float64), _ptr(u, np.float64), _ptr(phi, np.float64),
                                      phi.shape[0], _ptr(y, np.float64)))
+
+
+def mg_adjoint_rhs(h, Es, phi, b):
+    """b_i = phi_i^T (grad_u G) phi_i (Eq. 5 right-hand sides), device tensors."""
+    check(lib.mg_adjoint_rhs(h.raw, _ptr(Es, np.float64), _ptr(phi, np.float64), phi.shape[0], _ptr(b, np.float64)))
+
+
+def mg_eigen_sensitivity(h, dEk, dEs, u, phi, z, lam, out):
+    """Eq. 4 element sensitivities for nphi modes (device tensors; lam: sequence of nphi floats)."""
+    lam_arr = np.ascontiguousarray(np.asarray(lam, dtype=np.float64))
+    check(lib.mg_eigen_sensitivity(h.raw, _ptr(dEk, np.float64), _ptr(dEs, np.float64), _ptr(u, np.float64),
+                                   _ptr(phi, np.float64), _ptr(z, np.float64), _ptr(lam_arr, np.float64),
+                                   phi.shape[0], _ptr(out, np.float64)))
 
 
 def mg_matvec(h, level, x, y):

@@ -197,3 +197,11 @@ void stress_set_constants(int dim, double nu, cudaStream_t s);
 void stress_sigma(const LevelGeom& g, const double* Es, const double* u, double* sig, cudaStream_t s);
 void stress_apply(const LevelGeom& g, const double* sig, const uint8_t* mask, const double* phi, double* y,
                   int nphi, cudaStream_t s);
+
+// ---------------------------------------------------------------- NEXT-1: adjoint RHS, sensitivities (sens.cu)
+void sens_set_constants(int dim, const double* K0, double nu, cudaStream_t s);
+void adjoint_rhs_apply(const LevelGeom& g, const double* Es, const uint8_t* mask, const double* phi, int nphi,
+                       double* w, double* b, cudaStream_t s);
+void eigen_sensitivity_apply(const LevelGeom& g, const double* dEk, const double* dEs, const uint8_t* mask,
+                             const double* u, const double* phi, const double* z, const double* lam, int nphi,
+                             double* out, cudaStream_t s);

@@ -169,6 +169,9 @@ struct mg_ctx {
     double* Mc = nullptr;                        // Galerkin child matrices Q_c^T K0 Q_c
     double* gstage = nullptr;                    // G(u) phi host-path staging
     long long gstage_cap = 0;
+    double* wbuf = nullptr;                      // adjoint RHS element terms (nphi x m x nv)
+    long long wbuf_cap = 0;
+    double* dlam = nullptr;                      // eigenvalues for mg_eigen_sensitivity (MG_MAX_RHS)
     double* xtmp = nullptr;                      // NCCL reverse-add receive buffer
     long long xtmp_cap = 0;
     // shared solve state
@@ -1154,6 +1157,7 @@ static mg_status setup_impl(mg_ctx* c, const mg_grid* grid, const double* E_e, c
         CU(cudaMemcpy(c->Mc, Mh.data(), sizeof(double) * Mh.size(), cudaMemcpyHostToDevice));
     }
     stress_set_constants(dim, c->nu, s);
+    sens_set_constants(dim, c->K0.data(), c->nu, s);
     const int NL = dim * (1 << dim);
     const bool edev = is_device_ptr(E_e), fdev = is_device_ptr(fixed);
     uint8_t* dfix = nullptr;
@@ -1591,6 +1595,49 @@ mg_status stress_stiffness_apply(mg_handle c, const double* Es_e, const double* 
     return MG_OK;
 }
 
+mg_status mg_adjoint_rhs(mg_handle c, const double* Es_e, const double* phi, int nphi, double* b) {
+    if (!c || !Es_e || !phi || !b) return fail(MG_ERR_ARG, "NULL argument");
+    if (nphi < 1) return fail(MG_ERR_ARG, "nphi must be >= 1");
+    if (multi(c)) return fail(MG_ERR_ARG, "mg_adjoint_rhs: single slab only (this round)");
+    if (!is_device_ptr(Es_e) || !is_device_ptr(phi) || !is_device_ptr(b))
+        return fail(MG_ERR_ARG, "mg_adjoint_rhs: device pointers required");
+    stream_enter(c);
+    const LevelGeom& g = c->G[0];
+    const long long need = (long long)nphi * g.nelem * (c->dim == 2 ? 3 : 6);
+    if (need > c->wbuf_cap) {
+        CU(cudaStreamSynchronize(c->stream));
+        if (c->wbuf) cudaFree(c->wbuf);
+        c->wbuf = nullptr;
+        CU(cudaMalloc(&c->wbuf, sizeof(double) * need));
+        c->wbuf_cap = need;
+    }
+    adjoint_rhs_apply(g, Es_e, c->sl[0].lv[0].mask, phi, nphi, c->wbuf, b, c->stream);
+    c->launches += 2;
+    CHECK_LAUNCH();
+    stream_leave(c);
+    return MG_OK;
+}
+
+mg_status mg_eigen_sensitivity(mg_handle c, const double* dEk, const double* dEs, const double* u, const double* phi,
+                               const double* z, const double* lambda, int nphi, double* out) {
+    if (!c || !dEk || !dEs || !u || !phi || !z || !lambda || !out) return fail(MG_ERR_ARG, "NULL argument");
+    if (nphi < 1 || nphi > MG_MAX_RHS) return fail(MG_ERR_ARG, "nphi out of range");
+    if (multi(c)) return fail(MG_ERR_ARG, "mg_eigen_sensitivity: single slab only (this round)");
+    for (const void* p : {(const void*)dEk, (const void*)dEs, (const void*)u, (const void*)phi, (const void*)z,
+                          (const void*)out})
+        if (!is_device_ptr(p)) return fail(MG_ERR_ARG, "mg_eigen_sensitivity: device pointers required");
+    stream_enter(c);
+    if (!c->dlam) CU(cudaMalloc(&c->dlam, sizeof(double) * MG_MAX_RHS));
+    CU(cudaMemcpyAsync(c->dlam, lambda, sizeof(double) * nphi,
+                       is_device_ptr(lambda) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+    eigen_sensitivity_apply(c->G[0], dEk, dEs, c->sl[0].lv[0].mask, u, phi, z, c->dlam, nphi, out, c->stream);
+    c->launches++;
+    CHECK_LAUNCH();
+    CU(cudaStreamSynchronize(c->stream));   // lambda may be a host temporary
+    stream_leave(c);
+    return MG_OK;
+}
+
 mg_status mg_matvec(mg_handle c, int level, const double* x, int nrhs, double* y) {
     if (!c || !x || !y) return fail(MG_ERR_ARG, "NULL argument");
     if (level < 0 || level >= c->L || nrhs < 1 || nrhs > MG_MAX_RHS) return fail(MG_ERR_ARG, "bad level / nrhs");
@@ -1767,7 +1814,7 @@ mg_status mg_destroy(mg_handle c) {
             if (p) cudaFree(p);
         if (s.maskpad) cudaFree(s.maskpad);
     }
-    for (double* p : {c->Ainv, c->stg, c->cpack, c->cgath, c->gj_work, c->sums, c->Mc, c->gstage})
+    for (double* p : {c->Ainv, c->stg, c->cpack, c->cgath, c->gj_work, c->sums, c->Mc, c->gstage, c->wbuf, c->dlam})
         if (p) cudaFree(p);
     if (c->ctl_mem) cudaFree(c->ctl_mem);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
