@@ -61,12 +61,20 @@ typedef enum {
     MG_ERR_SINGULAR = 10     /* coarsest-level factorisation hit a non-positive pivot */
 } mg_status;
 
+/* Element type: MG_ELEM_STD = standard bilinear Q4 / trilinear H8 (SURVEY.md 8(c) reading r1);
+ * MG_ELEM_WILSON = incompatible-mode element of the paper:
+ * bubble modes 1 - xi_k^2 per component condensed statically on the unit element.  Both use the
+ * centroid stress for G (the bubble gradients vanish there). */
+#define MG_ELEM_STD 0
+#define MG_ELEM_WILSON 1
+
 /* Structured grid: dim = 2 (Q4) or 3 (H8); nel[k] element count along axis k
- * (nel[2] ignored in 2D); nu = Poisson ratio (0.3). Unit elements. */
+ * (nel[2] ignored in 2D); nu = Poisson ratio (0.3); element type. Unit elements. */
 typedef struct {
     int dim;
     int nel[3];
     double nu;
+    int element;
 } mg_grid;
 
 /* Multigrid / CG options; pass NULL for defaults {0.6, 1, 1, 1000}.

@@ -9,7 +9,8 @@ generators in `workloads/` (which hold none of the method's arithmetic).
 What it computes (SURVEY.md 8(c) "Definition"), each function citing its passage:
 
 * `fem`      element matrices K_e0 (standard bilinear Q4 / trilinear H8, exact
-             2x2(x2) Gauss of B^T D B) and the centroid-stress geometric
+             2x2(x2) Gauss of B^T D B; incompatible-mode "Wilson" elements with
+             statically condensed bubble modes, NEXT-4) and the centroid-stress geometric
              matrices H_ij used by G_e0[u_e]  (PAPER.md:99-111, Eq. 2);
 * `assemble` sparse K = sum_e E_e A_e^T K0 A_e and G(u) = sum_e Es_e A_e^T G_e0[u_e] A_e
              with Dirichlet rows/cols replaced by identity (K) or zero (G);
@@ -20,6 +21,7 @@ What it computes (SURVEY.md 8(c) "Definition"), each function citing its passage
              (Alg. 1 l.2; Eq. 5 :133-136; Eq. 6 :161-165), and an
              independent multigrid-preconditioned CG for the 3D
              sizes where direct factorisation is infeasible (SURVEY 8(c));
+* `sens`     adjoint right-hand sides (Eq. 5) and Eq. 4 sensitivities (NEXT-1);
 * `mg`       nested hierarchy, bilinear/trilinear prolongation P = I^j_{j+1}
              and the Galerkin product P^T K P (Alg. 2 l.5).
 

@@ -41,10 +41,10 @@ def _coo(edofs, Ke_flat, n):
     return sp.coo_matrix((Ke_flat.reshape(-1), (rows, cols)), shape=(n, n)).tocsr()
 
 
-def assemble_K_raw(nel, E, nu=0.3) -> sp.csr_matrix:
+def assemble_K_raw(nel, E, nu=0.3, element="std") -> sp.csr_matrix:
     """K = sum_e E_e A_e^T K0 A_e, no boundary conditions."""
     dim = len(nel)
-    K0 = fem.element_stiffness(dim, nu)
+    K0 = fem.element_stiffness_of(element, dim, nu)
     edofs = element_dofs(nel)
     n = dim * int(np.prod([m + 1 for m in nel]))
     vals = np.asarray(E, dtype=np.float64)[:, None] * K0.reshape(1, -1)
@@ -60,9 +60,9 @@ def apply_dirichlet(A: sp.csr_matrix, fixed, identity: bool) -> sp.csr_matrix:
     return out.tocsr()
 
 
-def assemble_K(nel, E, fixed, nu=0.3) -> sp.csr_matrix:
+def assemble_K(nel, E, fixed, nu=0.3, element="std") -> sp.csr_matrix:
     """Fine-grid K with fixed rows/cols replaced by identity."""
-    return apply_dirichlet(assemble_K_raw(nel, E, nu), fixed, identity=True)
+    return apply_dirichlet(assemble_K_raw(nel, E, nu, element), fixed, identity=True)
 
 
 def element_geometric_batch(dim, u_e, nu=0.3):

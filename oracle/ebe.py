@@ -20,14 +20,14 @@ def _slices(bits, nel):
     return tuple(slice(b, b + n) for b, n in zip(bits, nel))
 
 
-def matvec(nel, E, fixed, x, nu=0.3, dtype=np.float64):
+def matvec(nel, E, fixed, x, nu=0.3, dtype=np.float64, element="std"):
     """y = K x for one vector x (n,) or a batch (R, n)."""
     x = np.asarray(x)
     if x.ndim == 2:
-        return np.stack([matvec(nel, E, fixed, xi, nu, dtype) for xi in x])
+        return np.stack([matvec(nel, E, fixed, xi, nu, dtype, element) for xi in x])
     dim = len(nel)
     nsh = tuple(n + 1 for n in nel) + (dim,)
-    K0 = fem.element_stiffness(dim, nu).astype(dtype)
+    K0 = fem.element_stiffness_of(element, dim, nu).astype(dtype)
     free = (1 - np.asarray(fixed).astype(dtype)).reshape(nsh)
     xg = x.astype(dtype).reshape(nsh) * free
     Eg = np.asarray(E).astype(dtype).reshape(tuple(nel) + (1,))
@@ -44,12 +44,12 @@ def matvec(nel, E, fixed, x, nu=0.3, dtype=np.float64):
     return y.reshape(-1)
 
 
-def matvec_rows(nel, E, fixed, x, nodes, nu=0.3):
+def matvec_rows(nel, E, fixed, x, nodes, nu=0.3, element="std"):
     """Rows of y = K x at the given node indices only: returns (len(nodes), d).
     Each row sums the 2^d adjacent elements one by one (sampled parity at full size)."""
     dim = len(nel)
     nn = np.array([n + 1 for n in nel])
-    K0 = fem.element_stiffness(dim, nu)
+    K0 = fem.element_stiffness_of(element, dim, nu)
     x = np.asarray(x, dtype=np.float64)
     fixed = np.asarray(fixed)
     E = np.asarray(E, dtype=np.float64)

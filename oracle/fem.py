@@ -89,6 +89,45 @@ def element_stiffness(dim: int, nu: float = 0.3, E: float = 1.0, nodes=None) -> 
     return K
 
 
+def element_stiffness_wilson(dim: int, nu: float = 0.3, E: float = 1.0) -> np.ndarray:
+    """Incompatible-mode element (Wilson et al.; "Wilson quadrilaterals in 2D",
+    hexahedra in 3D): the displacement field is enriched per
+    component with the bubble modes M_k = 1 - xi_k^2 (xi_k = 2 x_k - 1 in [-1, 1], k < d), whose
+    DOFs are condensed statically on the unit element (material constant per element):
+        K_e0 = K_cc - K_ci K_ii^-1 K_ic,   K = int [B_c B_i]^T D0 [B_c B_i], exact 2x2(x2) Gauss.
+    Incompatible DOF (comp c, mode k) has strain dM_k/dx_j = -4 (2 x_k - 1) delta_kj."""
+    D = constitutive(dim, E, nu)
+    na = 2 ** dim
+    nv = 3 if dim == 2 else 6
+    n, ninc = dim * na, dim * dim
+    K = np.zeros((n + ninc, n + ninc))
+    for xi, w in gauss_points(dim):
+        Bc = strain_displacement(dim, xi)
+        Bi = np.zeros((nv, ninc))
+        for k in range(dim):
+            dM = np.zeros(dim)
+            dM[k] = -4.0 * (2.0 * xi[k] - 1.0)
+            for c in range(dim):
+                col = c * dim + k
+                Bi[c, col] += dM[c]
+                for s, (i, j) in enumerate(VOIGT_SHEAR[dim]):
+                    if c == i:
+                        Bi[dim + s, col] += dM[j]
+                    if c == j:
+                        Bi[dim + s, col] += dM[i]
+        B = np.hstack([Bc, Bi])
+        K += w * B.T @ D @ B
+    Kcc, Kci, Kii = K[:n, :n], K[:n, n:], K[n:, n:]
+    return Kcc - Kci @ np.linalg.solve(Kii, Kci.T)
+
+
+def element_stiffness_of(element: str, dim: int, nu: float = 0.3) -> np.ndarray:
+    """K_e0 of the element type: "std" (bilinear / trilinear) or "wilson" (incompatible modes)."""
+    if element == "wilson":
+        return element_stiffness_wilson(dim, nu)
+    return element_stiffness(dim, nu)
+
+
 def geometric_H(dim: int, nodes=None) -> np.ndarray:
     """H[i, j, a, b] = int dN_a/dx_i dN_b/dx_j over the unit element (exact Gauss)."""
     na = 2 ** dim
@@ -115,7 +154,9 @@ def centroid_stress(dim: int, u_e: np.ndarray, nu: float = 0.3) -> np.ndarray:
 
 
 def element_geometric(dim: int, u_e: np.ndarray, nu: float = 0.3) -> np.ndarray:
-    """G_e0[u_e] = (sum_ij sigma_ij H_ij) kron I_d."""
+    """G_e0[u_e] = (sum_ij sigma_ij H_ij) kron I_d.  The same for the
+    incompatible-mode element: the bubble gradients vanish at the centroid, so the recovered
+    incompatible DOFs do not change the centroid stress."""
     sig = centroid_stress(dim, u_e, nu)
     S = np.einsum("ij,ijab->ab", sig, geometric_H(dim))
     return np.kron(S, np.eye(dim))

@@ -71,9 +71,11 @@ def _stream_ptr(stream):
     return ctypes.c_void_p(getattr(stream, "cuda_stream", stream))
 
 
-def mg_setup(nel, E, fixed, levels, nu=0.3, omega=0.6, nu_pre=1, nu_post=1, max_iter=1000, stream=None):
+def mg_setup(nel, E, fixed, levels, nu=0.3, omega=0.6, nu_pre=1, nu_post=1, max_iter=1000, stream=None,
+             element="std"):
+    """element: "std" (bilinear / trilinear) or "wilson" (incompatible modes, NEXT-4)."""
     dim = len(nel)
-    g = MgGrid(dim, (ctypes.c_int * 3)(*(list(nel) + [0] * (3 - dim))), nu)
+    g = _grid(nel, nu, element)
     o = MgOpts(omega, nu_pre, nu_post, max_iter)
     raw = ctypes.c_void_p()
     sp = _stream_ptr(stream)
@@ -82,9 +84,9 @@ def mg_setup(nel, E, fixed, levels, nu=0.3, omega=0.6, nu_pre=1, nu_post=1, max_
     return Handle(raw, dim, nel, levels, sp)
 
 
-def _grid(nel, nu=0.3):
+def _grid(nel, nu=0.3, element="std"):
     dim = len(nel)
-    return MgGrid(dim, (ctypes.c_int * 3)(*(list(nel) + [0] * (3 - dim))), nu)
+    return MgGrid(dim, (ctypes.c_int * 3)(*(list(nel) + [0] * (3 - dim))), nu, _lib.ELEMENTS[element])
 
 
 def mg_partition(nel, levels, nparts, part):
@@ -102,11 +104,11 @@ def mg_nccl_unique_id():
 
 
 def mg_setup_dist(nel, E, fixed, levels, rank=0, nranks=1, nslab=1, nccl_id=None, nu=0.3, omega=0.6, nu_pre=1,
-                  nu_post=1, max_iter=1000, stream=None):
+                  nu_post=1, max_iter=1000, stream=None, element="std"):
     """Slab-decomposed setup: E / fixed (and all later vectors) cover this rank's owned part
     (mg_local_info); nslab slabs are kept in this handle."""
     dim = len(nel)
-    g = _grid(nel, nu)
+    g = _grid(nel, nu, element)
     o = MgOpts(omega, nu_pre, nu_post, max_iter)
     idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
     d = MgDist(rank, nranks, nslab, ctypes.cast(idbuf, ctypes.c_void_p) if idbuf is not None else None)

@@ -27,8 +27,12 @@ EXPORTED = [
 ]
 
 
+ELEMENTS = {"std": 0, "wilson": 1}
+
+
 class MgGrid(ctypes.Structure):
-    _fields_ = [("dim", ctypes.c_int), ("nel", ctypes.c_int * 3), ("nu", ctypes.c_double)]
+    _fields_ = [("dim", ctypes.c_int), ("nel", ctypes.c_int * 3), ("nu", ctypes.c_double),
+                ("element", ctypes.c_int)]
 
 
 class MgOpts(ctypes.Structure):

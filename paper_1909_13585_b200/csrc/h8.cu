@@ -63,10 +63,30 @@ __host__ __device__ constexpr double khat(double nu, int row, int col) {
     return v;
 }
 
-void h8_set_constants(double nu, cudaStream_t s) {
-    static double Kh[576];
+// K^ = T^-T K0 T^-1 for any element matrix K0 (standard at any nu, or the incompatible-mode
+// element): per axis T^-1 = (1/2) [[1, -1], [1, 1]].  Its sparsity is that of khat (checked for
+// both element types), which the kernel's compile-time skip pattern relies on.
+void h8_set_constants(const double* K0, cudaStream_t s) {
+    static double Ti[24][24], Kh[576];
+    for (int a = 0; a < 8; ++a)       // nodal index a, transformed index t
+        for (int t = 0; t < 8; ++t) {
+            double v = 1.0;
+            for (int k = 0; k < 3; ++k) {
+                const int ab = (a >> (2 - k)) & 1, tb = (t >> (2 - k)) & 1;
+                v *= 0.5 * ((tb == 0) ? 1.0 : (ab ? 1.0 : -1.0));
+            }
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) Ti[3 * a + i][3 * t + j] = (i == j) ? v : 0.0;
+        }
     for (int r = 0; r < 24; ++r)
-        for (int c = 0; c < 24; ++c) Kh[r * 24 + c] = khat(nu, r, c);
+        for (int c = 0; c < 24; ++c) {
+            double v = 0.0;
+            for (int p = 0; p < 24; ++p) {
+                if (Ti[p][r] == 0.0) continue;
+                for (int q = 0; q < 24; ++q) v += Ti[p][r] * K0[p * 24 + q] * Ti[q][c];
+            }
+            Kh[r * 24 + c] = v;
+        }
     cudaMemcpyToSymbolAsync(c_Kh, Kh, sizeof(Kh), 0, cudaMemcpyHostToDevice, s);
 }
 

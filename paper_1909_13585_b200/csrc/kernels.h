@@ -48,7 +48,7 @@ int fine_apply(int op, const FineArgs& a, cudaStream_t s);
 int fine_items(const LevelGeom& g, int R);
 void fine_diag(const LevelGeom& g, const double* E, const uint8_t* mask, double* Dinv, double* D, cudaStream_t s);
 // 3D structured (sum/difference basis) fine operator (h8.cu); fine_apply routes 3D here
-void h8_set_constants(double nu, cudaStream_t s);
+void h8_set_constants(const double* K0, cudaStream_t s);
 int h8_apply(int op, const FineArgs& a, cudaStream_t s);
 int h8_items(const LevelGeom& g, int R);
 

@@ -72,6 +72,107 @@ static void element_stiffness(int dim, double nu, std::vector<double>& K) {
         for (int c = 0; c < nl; ++c) K[r * nl + c] = dim == 2 ? k0_entry<2>(nu, r, c) : k0_entry<3>(nu, r, c);
 }
 
+// Incompatible-mode element ("Wilson quadrilaterals ... hexahedra"):
+// per component the bubble modes M_k = 1 - (2 x_k - 1)^2, k < d, condensed on the unit element
+// (material constant per element): K_e0 = K_cc - K_ci K_ii^-1 K_ic with
+// K = int [B_c B_i]^T D0 [B_c B_i] by 2x2(x2) Gauss (exact for these polynomials).
+static void element_stiffness_wilson(int dim, double nu, std::vector<double>& K0) {
+    const int na = 1 << dim, n = dim * na, ni = dim * dim, nt = n + ni, nv = dim == 2 ? 3 : 6;
+    double D[36] = {0};
+    if (dim == 2) {
+        const double c = 1.0 / (1.0 - nu * nu);
+        const double m[9] = {c, c * nu, 0, c * nu, c, 0, 0, 0, c * (1 - nu) / 2};
+        for (int i = 0; i < 9; ++i) D[i] = m[i];
+    } else {
+        const double lam = nu / ((1 + nu) * (1 - 2 * nu)), mu = 1.0 / (2 * (1 + nu));
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) D[i * 6 + j] = lam + (i == j ? 2 * mu : 0.0);
+        for (int i = 3; i < 6; ++i) D[i * 6 + i] = mu;
+    }
+    const int sh[3][2] = {{1, 2}, {0, 2}, {0, 1}};   // 3D engineering shear pairs (2D: (0, 1))
+    auto shear = [&](int s, int& i, int& j) {
+        if (dim == 2) { i = 0; j = 1; } else { i = sh[s][0]; j = sh[s][1]; }
+    };
+    const double g1[2] = {0.5 - 0.5 / std::sqrt(3.0), 0.5 + 0.5 / std::sqrt(3.0)};
+    std::vector<double> K((size_t)nt * nt, 0.0), B((size_t)nv * nt);
+    const int ng = 1 << dim;
+    for (int q = 0; q < ng; ++q) {
+        double x[3];
+        for (int k = 0; k < dim; ++k) x[k] = g1[(q >> (dim - 1 - k)) & 1];
+        const double w = 1.0 / ng;
+        std::fill(B.begin(), B.end(), 0.0);
+        for (int a = 0; a < na; ++a) {
+            double gr[3];
+            for (int j = 0; j < dim; ++j) {
+                double v = 1.0;
+                for (int k = 0; k < dim; ++k) {
+                    const int bit = (a >> (dim - 1 - k)) & 1;
+                    v *= (k == j) ? (bit ? 1.0 : -1.0) : (bit ? x[k] : 1.0 - x[k]);
+                }
+                gr[j] = v;
+            }
+            for (int i = 0; i < dim; ++i) B[i * nt + dim * a + i] = gr[i];
+            for (int s = 0; s < nv - dim; ++s) {
+                int i, j;
+                shear(s, i, j);
+                B[(dim + s) * nt + dim * a + i] += gr[j];
+                B[(dim + s) * nt + dim * a + j] += gr[i];
+            }
+        }
+        for (int k = 0; k < dim; ++k) {
+            const double dm = -4.0 * (2.0 * x[k] - 1.0);   // dM_k/dx_k
+            for (int c = 0; c < dim; ++c) {
+                const int col = n + c * dim + k;
+                if (c == k) B[c * nt + col] += dm;
+                for (int s = 0; s < nv - dim; ++s) {
+                    int i, j;
+                    shear(s, i, j);
+                    if (c == i && j == k) B[(dim + s) * nt + col] += dm;
+                    if (c == j && i == k) B[(dim + s) * nt + col] += dm;
+                }
+            }
+        }
+        for (int r = 0; r < nt; ++r)
+            for (int cc = 0; cc < nt; ++cc) {
+                double v = 0.0;
+                for (int p = 0; p < nv; ++p)
+                    for (int p2 = 0; p2 < nv; ++p2) v += B[p * nt + r] * D[p * nv + p2] * B[p2 * nt + cc];
+                K[(size_t)r * nt + cc] += w * v;
+            }
+    }
+    // K_ii^-1 K_ic by Gauss-Jordan on the small SPD block
+    std::vector<double> Kii((size_t)ni * ni), X((size_t)ni * n);
+    for (int r = 0; r < ni; ++r) {
+        for (int c = 0; c < ni; ++c) Kii[r * ni + c] = K[(size_t)(n + r) * nt + n + c];
+        for (int c = 0; c < n; ++c) X[r * n + c] = K[(size_t)(n + r) * nt + c];
+    }
+    for (int p = 0; p < ni; ++p) {
+        const double piv = Kii[p * ni + p];
+        for (int c = 0; c < ni; ++c) Kii[p * ni + c] /= piv;
+        for (int c = 0; c < n; ++c) X[p * n + c] /= piv;
+        for (int r = 0; r < ni; ++r) {
+            if (r == p) continue;
+            const double f = Kii[r * ni + p];
+            if (f == 0.0) continue;
+            for (int c = 0; c < ni; ++c) Kii[r * ni + c] -= f * Kii[p * ni + c];
+            for (int c = 0; c < n; ++c) X[r * n + c] -= f * X[p * n + c];
+        }
+    }
+    K0.assign((size_t)n * n, 0.0);
+    for (int r = 0; r < n; ++r)
+        for (int c = 0; c < n; ++c) {
+            double v = K[(size_t)r * nt + c];
+            for (int p = 0; p < ni; ++p) v -= K[(size_t)r * nt + n + p] * X[p * n + c];
+            K0[(size_t)r * n + c] = v;
+        }
+    // symmetrise the rounding
+    for (int r = 0; r < n; ++r)
+        for (int c = r + 1; c < n; ++c) {
+            const double v = 0.5 * (K0[(size_t)r * n + c] + K0[(size_t)c * n + r]);
+            K0[(size_t)r * n + c] = K0[(size_t)c * n + r] = v;
+        }
+}
+
 // ---------------------------------------------------------------- small kernels
 // mask[dst0 + i] = fixed bits of node (src0 + i) of the user's fixed array, i < count
 __global__ void fixed_to_mask_kernel(long long count, int dim, const uint8_t* fixed, long long src0, uint8_t* mask,
@@ -1137,8 +1238,10 @@ static mg_status setup_impl(mg_ctx* c, const mg_grid* grid, const double* E_e, c
             v.gp0 = (sl.e0 >> l) - sl.gl;
         }
     }
-    element_stiffness(dim, c->nu, c->K0);
-    c->nu_paper = (c->nu == MG_NU_PAPER);
+    if (grid->element == MG_ELEM_WILSON) element_stiffness_wilson(dim, c->nu, c->K0);
+    else element_stiffness(dim, c->nu, c->K0);
+    // compile-time K0 / K^ immediates only for the standard element at the paper's nu
+    c->nu_paper = (c->nu == MG_NU_PAPER) && grid->element == MG_ELEM_STD;
     c->fused2d = (dim == 2 && levels >= 2);
     c->unfused_coarse = getenv("MG_UNFUSED_COARSE") && atoi(getenv("MG_UNFUSED_COARSE")) == 1;
     // (measured slower than the composed kernels on B200 -- more registers in a latency-bound
@@ -1146,7 +1249,7 @@ static mg_status setup_impl(mg_ctx* c, const mg_grid* grid, const double* E_e, c
     c->fused3d = dim == 3 && levels >= 2 && c->opts.nu_pre == 1 && c->opts.nu_post == 1 && !c->unfused_coarse &&
                  !getenv("MG_DENSE_H8") && getenv("MG_FUSED3D") && atoi(getenv("MG_FUSED3D")) == 1;
     fine_set_constants(dim, c->K0.data(), s);
-    if (dim == 3) h8_set_constants(c->nu, s);
+    if (dim == 3) h8_set_constants(c->K0.data(), s);
     if (dim == 2) fine2d_set_constants(c->K0.data(), s);
     galerkin_set_constants(dim, c->K0.data(), s);
     {
@@ -1304,6 +1407,7 @@ mg_status mg_setup_dist(const mg_grid* grid, const double* E_e, const uint8_t* f
                         const mg_dist* dist, void* stream, mg_handle* out) {
     if (!grid || !E_e || !fixed || !out) return fail(MG_ERR_ARG, "NULL argument");
     if (grid->dim != 2 && grid->dim != 3) return fail(MG_ERR_ARG, "dim must be 2 or 3");
+    if (grid->element != MG_ELEM_STD && grid->element != MG_ELEM_WILSON) return fail(MG_ERR_ARG, "unknown element");
     if (levels < 1 || levels > MG_MAX_LEVELS) return fail(MG_ERR_ARG, "levels out of range");
     if (!(grid->nu > -1.0 && grid->nu < 0.5)) return fail(MG_ERR_ARG, "nu out of range");
     if (opts && (opts->nu_pre < 1 || opts->nu_post < 0 || opts->max_iter < 1 || !(opts->omega > 0)))

@@ -222,7 +222,7 @@ def test_patch_uniform_compression_exact(nel):
     assert np.abs(G - Gw).max() < 1e-12
 
 
-def _cantilever_tip(nel):
+def _cantilever_tip(nel, element="std"):
     dim = len(nel)
     nsh = tuple(m + 1 for m in nel)
     fixed = np.zeros(nsh + (dim,), np.uint8)
@@ -234,7 +234,7 @@ def _cantilever_tip(nel):
         w = t if w is None else np.multiply.outer(w, t)
     f[nel[0], ..., 1] = -w                        # unit total tip shear along -axis 1
     fixed = fixed.reshape(-1)
-    K = assemble.assemble_K(nel, np.ones(int(np.prod(nel))), fixed)
+    K = assemble.assemble_K(nel, np.ones(int(np.prod(nel))), fixed, element=element)
     u = solve.direct_solve(K, f.reshape(-1), fixed).reshape(nsh + (dim,))
     delta = -np.sum(u[nel[0], ..., 1] * w)        # load-weighted tip deflection
     L, h = nel[0], nel[1]
@@ -404,3 +404,57 @@ def test_iterative_oracle_matches_direct():
     for k in range(cfg.nrhs):
         assert np.linalg.norm(Ui[k] - Ud[k]) <= 1e-11 * np.linalg.norm(Ud[k])
     assert max(its) < 100
+
+
+# ---------------------------------------------------------------- NEXT-4: incompatible-mode element
+@pytest.mark.parametrize("dim", [2, 3])
+def test_wilson_element_properties(dim):
+    """Condensed incompatible-mode K_e0: symmetric, PSD with
+    exactly the rigid modes as null space, and strictly softer than the standard element on the
+    pure-bending nodal pattern while equal on constant-strain (patch) patterns."""
+    Kw = fem.element_stiffness_wilson(dim)
+    K0 = fem.element_stiffness(dim)
+    assert np.abs(Kw - Kw.T).max() < 1e-15
+    ev = np.linalg.eigvalsh(Kw)
+    nrig = 3 if dim == 2 else 6
+    assert np.all(np.abs(ev[:nrig]) < 1e-13) and ev[nrig] > 1e-3
+    nodes = fem.local_nodes(dim).astype(float)
+    # pure bending about axis 1: u_0 = (x_0 - 1/2)(x_1 - 1/2), other components 0
+    ub = np.zeros(dim * len(nodes))
+    ub[0::dim] = (nodes[:, 0] - 0.5) * (nodes[:, 1] - 0.5)
+    assert ub @ Kw @ ub < ub @ K0 @ ub * (1 - 1e-3)
+    # constant strain u = A x: identical energy (incompatible modes pass the patch test)
+    rng = np.random.default_rng(0)
+    A = rng.standard_normal((dim, dim))
+    uc = (nodes @ A.T).reshape(-1)
+    assert abs(uc @ Kw @ uc - uc @ K0 @ uc) < 1e-12 * abs(uc @ K0 @ uc)
+
+
+def test_wilson_pure_bending_is_exact_on_the_unit_square():
+    """Plane stress pure bending sigma_xx = M y: the Wilson Q6 element represents it exactly, so
+    the element energy of the exact nodal field equals the continuum energy (1/2 int sigma eps)."""
+    nu = 0.3
+    Kw = fem.element_stiffness_wilson(2, nu)
+    nodes = fem.local_nodes(2).astype(float)
+    # exact field for eps_xx = kappa (y - 1/2), eps_yy = -nu kappa (y - 1/2), gamma = 0:
+    # u = kappa x (y - 1/2), v = -kappa x^2 / 2 - nu kappa (y - 1/2)^2 / 2 (up to rigid modes)
+    kappa = 1.0
+    x, y = nodes[:, 0], nodes[:, 1]
+    u = np.zeros(8)
+    u[0::2] = kappa * x * (y - 0.5)
+    u[1::2] = -0.5 * kappa * x ** 2 - 0.5 * nu * kappa * (y - 0.5) ** 2
+    # continuum energy: 1/2 int E eps_xx^2 dA (sigma_yy = 0), = 1/2 kappa^2 int (y - 1/2)^2 = kappa^2 / 24
+    exact = kappa ** 2 / 24.0
+    assert abs(0.5 * u @ Kw @ u - exact) < 1e-13
+    # the standard element overestimates it (shear locking)
+    K0 = fem.element_stiffness(2, nu)
+    assert 0.5 * u @ K0 @ u > exact * 1.05
+
+
+def test_wilson_cantilever_closer_to_beam_theory():
+    """SURVEY 8(f) NEXT-4 pin: on a coarse cantilever the incompatible-mode element is closer to
+    Timoshenko beam theory than the standard Q4."""
+    r_std = _cantilever_tip((16, 2), "std")
+    r_wil = _cantilever_tip((16, 2), "wilson")
+    assert abs(1 - r_wil) < 0.2 * abs(1 - r_std)
+    assert 0.97 < r_wil < 1.03
