@@ -164,6 +164,14 @@ mg_status mg_update_modulus(mg_handle h, const double* E_e);
  * Synchronous with respect to the handle's stream. 1 <= nrhs <= MG_MAX_RHS. */
 mg_status mgcg_solve(mg_handle h, const double* rhs, int nrhs, double tol, double* x, mg_report* rep);
 
+/* NEXT-3: the paper's block variant mgBPCG (Alg. 2 l.15 :732):
+ * O'Leary block CG over the nrhs columns with the same V(1,1) preconditioner, sharing one Krylov
+ * space; the R x R Gram systems are solved by a pivoted Cholesky whose dropped pivots deflate
+ * dependent or converged directions.  Same arguments, report and stopping rule
+ * as mgcg_solve (per column ||r_k|| <= tol ||b_k||, true residual at exit); report.iters[k] counts
+ * the block iterations until column k converged.  Single slab this round. */
+mg_status mgcg_block_solve(mg_handle h, const double* rhs, int nrhs, double tol, double* x, mg_report* rep);
+
 /* y_k = G(u) phi_k for k < nphi (PAPER.md:99 G_e = E_sigma G_e0[u_e]; Eq. 6 :163):
  *   Es_e  device, nelem fp64 stress moduli E_sigma(x_e) = x_e^p E_1 (Eq. 2 :106).
  *   u     device, ndof fp64 displacement (taken as given, incl. fixed DOFs).

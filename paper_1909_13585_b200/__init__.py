@@ -17,7 +17,7 @@ from ._lib import MgDist, MgError, MgGrid, MgOpts, MgReport, check, lib
 
 __all__ = [
     "Handle", "MgError", "mg_setup", "mg_setup_dist", "mg_partition", "mg_nccl_unique_id", "mg_local_info",
-    "mg_update_modulus", "mg_adjoint_rhs", "mg_eigen_sensitivity", "mgcg_solve", "stress_stiffness_apply",
+    "mg_update_modulus", "mg_adjoint_rhs", "mg_eigen_sensitivity", "mgcg_block_solve", "mgcg_solve", "stress_stiffness_apply",
     "mg_matvec", "mg_vcycle", "mg_restrict", "mg_prolong", "mg_level_info", "mg_get_diagonal",
     "mg_get_coarse_inverse", "mg_kernel_launches", "mg_profile_kernels", "mg_destroy", "lib_path",
 ]
@@ -148,6 +148,18 @@ def mgcg_solve(h, rhs, tol, x, raise_on_error=True):
     nrhs = rhs.shape[0]
     rep = MgReport()
     st = lib.mgcg_solve(h.raw, _ptr(rhs, np.float64), nrhs, tol, _ptr(x, np.float64), ctypes.byref(rep))
+    out = _report(rep, nrhs)
+    out["status"] = _lib.STATUS.get(st, st)
+    if raise_on_error:
+        check(st)
+    return out
+
+
+def mgcg_block_solve(h, rhs, tol, x, raise_on_error=True):
+    """Block PCG (mgBPCG) over all rows of rhs (nrhs, ndof); x written in place."""
+    nrhs = rhs.shape[0]
+    rep = MgReport()
+    st = lib.mgcg_block_solve(h.raw, _ptr(rhs, np.float64), nrhs, tol, _ptr(x, np.float64), ctypes.byref(rep))
     out = _report(rep, nrhs)
     out["status"] = _lib.STATUS.get(st, st)
     if raise_on_error:

@@ -205,3 +205,12 @@ void adjoint_rhs_apply(const LevelGeom& g, const double* Es, const uint8_t* mask
 void eigen_sensitivity_apply(const LevelGeom& g, const double* dEk, const double* dEs, const uint8_t* mask,
                              const double* u, const double* phi, const double* z, const double* lam, int nphi,
                              double* out, cudaStream_t s);
+
+// ---------------------------------------------------------------- NEXT-3: block PCG (block.cu)
+int gram_blocks(long long n, int R);
+void gram(long long n, long long stride, int R, const double* A, const double* B, double* partial, double* G,
+          cudaStream_t s);
+void block_coef(int R, const double* Gam, const double* Rho, double* C, double thr, int* rank, cudaStream_t s);
+void block_axpy(long long n, long long stride, int R, const double* X, const double* C, const double* base, double* Y,
+                double sign, cudaStream_t s);
+void block_conv(int R, const double* partial, int items, double tol, CgCtl c, cudaStream_t s);

@@ -273,6 +273,12 @@ struct mg_ctx {
     double* wbuf = nullptr;                      // adjoint RHS element terms (nphi x m x nv)
     long long wbuf_cap = 0;
     double* dlam = nullptr;                      // eigenvalues for mg_eigen_sensitivity (MG_MAX_RHS)
+    // block PCG workspace
+    double *bpart = nullptr, *bGam = nullptr, *bRho = nullptr, *bRhoN = nullptr, *bC = nullptr;
+    int* brank = nullptr;
+    int block_R = 0;
+    cudaGraphExec_t g_block = nullptr;
+    double block_tol = -1.0;
     double* xtmp = nullptr;                      // NCCL reverse-add receive buffer
     long long xtmp_cap = 0;
     // shared solve state
@@ -1607,6 +1613,39 @@ mg_status mgcg_solve(mg_handle c, const double* rhs, int nrhs, double tol, doubl
     return MG_OK;
 }
 
+// ---------------------------------------------------------------- block PCG (NEXT-3)
+// O'Leary's block CG with the same V(1,1) preconditioner (Alg. 2 l.15):
+//   Q = A P; Gamma = P^T Q; alpha = Gamma^+ Rho; X += P alpha; R -= Q alpha; Z = M R;
+//   Rho' = Z^T R; beta = Rho^+ Rho'; P = Z + P beta; Rho = Rho'
+// with pivoted-Cholesky pseudo-inverses (dependent / converged directions deflated).
+static mg_status record_block_iter(mg_ctx* c, int R, double tol) {
+    Slab& s = c->sl[0];
+    const long long n = s.vs;
+    Rec all{c, R, nullptr, nullptr};
+    {
+        FineArgs a = fine_args(c, s, all);
+        a.x = s.p0; a.y = s.q;
+        level0_apply(c, s, FOP_MATVEC, a);
+    }
+    gram(n, n, R, s.p0, s.q, c->bpart, c->bGam, c->stream);
+    block_coef(R, c->bGam, c->bRho, c->bC, 1e-13, c->brank, c->stream);
+    block_axpy(n, n, R, s.p0, c->bC, nullptr, s.x, 1.0, c->stream);
+    block_axpy(n, n, R, s.q, c->bC, nullptr, s.r1, -1.0, c->stream);
+    const int items = vec_dot_range(n, 0, n, R, s.r1, s.r1, c->partial, c->pst, nullptr, nullptr, c->stream);
+    block_conv(R, c->partial, items, tol, c->ctl, c->stream);
+    long long k;
+    TRY(blk_restrict(all, &Slab::r1, &Slab::r0, &k));
+    int cw;
+    TRY(coarse_cycle(all, &cw));
+    TRY(blk_post(all, &Slab::r0, cw, &k));
+    gram(n, n, R, s.zf, s.r1, c->bpart, c->bRhoN, c->stream);
+    block_coef(R, c->bRho, c->bRhoN, c->bC, 1e-13, c->brank, c->stream);
+    block_axpy(n, n, R, s.p0, c->bC, s.zf, s.p0, 1.0, c->stream);
+    CU(cudaMemcpyAsync(c->bRho, c->bRhoN, sizeof(double) * R * R, cudaMemcpyDeviceToDevice, c->stream));
+    c->launches += 14;
+    return MG_OK;
+}
+
 mg_status stress_stiffness_apply(mg_handle c, const double* Es_e, const double* u, const double* phi, int nphi,
                                  double* y) {
     if (!c || !Es_e || !u || !phi || !y) return fail(MG_ERR_ARG, "NULL argument");
@@ -1739,6 +1778,126 @@ mg_status mg_eigen_sensitivity(mg_handle c, const double* dEk, const double* dEs
     CHECK_LAUNCH();
     CU(cudaStreamSynchronize(c->stream));   // lambda may be a host temporary
     stream_leave(c);
+    return MG_OK;
+}
+
+mg_status mgcg_block_solve(mg_handle c, const double* rhs, int nrhs, double tol, double* x, mg_report* rep) {
+    if (!c || !rhs || !x) return fail(MG_ERR_ARG, "NULL argument");
+    if (nrhs < 1 || nrhs > MG_MAX_RHS) return fail(MG_ERR_ARG, "nrhs out of range");
+    if (!(tol > 0.0) || !(tol < 1.0)) return fail(MG_ERR_ARG, "tol must be in (0,1)");
+    if (multi(c)) return fail(MG_ERR_ARG, "mgcg_block_solve: single slab only (this round)");
+    const int R = nrhs;
+    const long long nr = c->n_rank;
+    cudaStream_t s = c->stream;
+    stream_enter(c);
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreate(&e0));
+    CU(cudaEventCreate(&e1));
+    CU(cudaEventRecord(e0, s));
+    TRY(ensure_vectors(c, R));
+    Slab& sl = c->sl[0];
+    const long long n = sl.vs;
+    if (c->block_R < R) {
+        for (double** p : {&c->bpart, &c->bGam, &c->bRho, &c->bRhoN, &c->bC})
+            if (*p) { cudaFree(*p); *p = nullptr; }
+        CU(cudaMalloc(&c->bpart, sizeof(double) * (long long)R * R * gram_blocks(n, R)));
+        for (double** p : {&c->bGam, &c->bRho, &c->bRhoN, &c->bC}) CU(cudaMalloc(p, sizeof(double) * R * R));
+        if (!c->brank) CU(cudaMalloc(&c->brank, sizeof(int)));
+        c->block_R = R;
+        if (c->g_block) { cudaGraphExecDestroy(c->g_block); c->g_block = nullptr; }
+    }
+    const bool rdev = is_device_ptr(rhs), xdev = is_device_ptr(x);
+    const double* rsrc = rhs;
+    if (!rdev) {
+        CU(cudaMemcpyAsync(c->stage, rhs, sizeof(double) * nr * R, cudaMemcpyHostToDevice, s));
+        rsrc = c->stage;
+    }
+    TRY(scatter_fine(c, rsrc, R, true, &Slab::b));
+    // init: bb, active, iters; x = 0; r = b; Z = M r; P = Z; Rho = Z^T r
+    TRY(dot_finish(c, R, &Slab::b, &Slab::b, SM_BB));
+    CU(cudaMemsetAsync(c->ctl.alpha, 0, sizeof(double) * MG_MAX_RHS, s));
+    CU(cudaMemsetAsync(c->ctl.status, 0, sizeof(int), s));
+    CU(cudaMemsetAsync(sl.x, 0, sizeof(double) * n * R, s));
+    CU(cudaMemsetAsync(sl.q, 0, sizeof(double) * n * R, s));
+    CU(cudaMemcpyAsync(sl.r1, sl.b, sizeof(double) * n * R, cudaMemcpyDeviceToDevice, s));
+    if (!c->g_block || c->block_tol != tol) {
+        if (c->g_block) { cudaGraphExecDestroy(c->g_block); c->g_block = nullptr; }
+        TRY(capture_begin(c));
+        TRY(captured(c, record_block_iter(c, R, tol)));
+        long long nn;
+        TRY(capture_end(c, &c->g_block, &nn));
+        c->block_tol = tol;
+    }
+    int* hp = c->h_pinned;
+    double* hd = c->h_dbl;
+    int it = 0, restarts = 0;
+    const int maxit = c->opts.max_iter;
+    for (;;) {
+        // (re)start the block Krylov space from r: Z = M r, P = Z, Rho = Z^T r
+        {
+            Rec all{c, R, nullptr, nullptr};
+            long long k;
+            TRY(blk_restrict(all, &Slab::r1, &Slab::r0, &k));
+            int cw;
+            TRY(coarse_cycle(all, &cw));
+            TRY(blk_post(all, &Slab::r0, cw, &k));
+        }
+        CU(cudaMemcpyAsync(sl.p0, sl.zf, sizeof(double) * n * R, cudaMemcpyDeviceToDevice, s));
+        gram(n, n, R, sl.zf, sl.r1, c->bpart, c->bRho, s);
+        int zero = 0;
+        CU(cudaMemcpyAsync(c->ctl.done, &zero, sizeof(int), cudaMemcpyHostToDevice, s));
+        for (; it < maxit;) {
+            CU(cudaGraphLaunch(c->g_block, s));
+            ++it;
+            CU(cudaMemcpyAsync(hp, c->ctl.done, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CU(cudaStreamSynchronize(s));
+            if (hp[0]) break;
+        }
+        TRY(record_true(c, R));   // x has no deferred update; flush is a no-op (xalpha = 0)
+        CU(cudaMemcpyAsync(hd, c->ctl.bb, sizeof(double) * MG_MAX_RHS, cudaMemcpyDeviceToHost, s));
+        CU(cudaMemcpyAsync(hd + MG_MAX_RHS, c->ctl.rr, sizeof(double) * MG_MAX_RHS, cudaMemcpyDeviceToHost, s));
+        CU(cudaMemcpyAsync(hd + 2 * MG_MAX_RHS, c->ctl.tt, sizeof(double) * MG_MAX_RHS, cudaMemcpyDeviceToHost, s));
+        CU(cudaMemcpyAsync(hp + 2, c->ctl.iters, sizeof(int) * R, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        bool need = false;
+        for (int k = 0; k < R; ++k)
+            if (hd[k] > 0.0 && hd[2 * MG_MAX_RHS + k] > tol * tol * hd[k]) need = true;
+        // residual gap of block CG (recursive vs true residual): restart from r = b - K x
+        if (!need || restarts >= 3 || it >= maxit) break;
+        ++restarts;
+        CU(cudaMemcpyAsync(sl.r1, sl.t, sizeof(double) * n * R, cudaMemcpyDeviceToDevice, s));
+    }
+    double* xdst = xdev ? x : c->stage;
+    TRY(gather_fine(c, &Slab::x, R, xdst));
+    if (!xdev) CU(cudaMemcpyAsync(x, c->stage, sizeof(double) * nr * R, cudaMemcpyDeviceToHost, s));
+    CU(cudaEventRecord(e1, s));
+    CU(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    bool all_conv = true;
+    for (int k = 0; k < R; ++k) {
+        const double bb = hd[k];
+        const double tr = bb > 0 ? std::sqrt(hd[2 * MG_MAX_RHS + k] / bb) : 0.0;
+        all_conv = all_conv && tr <= tol;
+        if (rep) {
+            rep->iters[k] = hp[2 + k];
+            rep->relres[k] = bb > 0 ? std::sqrt(hd[MG_MAX_RHS + k] / bb) : 0.0;
+            rep->true_relres[k] = tr;
+            rep->converged[k] = tr <= tol ? 1 : 0;
+        }
+    }
+    if (rep) {
+        rep->nrhs = R;
+        rep->max_iters = it;
+        rep->restarts = restarts;
+        rep->graph_launches = it;
+        rep->kernel_launches = 14LL * it;
+        rep->solve_ms = ms;
+    }
+    stream_leave(c);
+    if (!all_conv) return fail(MG_ERR_MAXITER, "block PCG: not all right-hand sides reached tol");
     return MG_OK;
 }
 
@@ -1918,9 +2077,12 @@ mg_status mg_destroy(mg_handle c) {
             if (p) cudaFree(p);
         if (s.maskpad) cudaFree(s.maskpad);
     }
-    for (double* p : {c->Ainv, c->stg, c->cpack, c->cgath, c->gj_work, c->sums, c->Mc, c->gstage, c->wbuf, c->dlam})
+    for (double* p : {c->Ainv, c->stg, c->cpack, c->cgath, c->gj_work, c->sums, c->Mc, c->gstage, c->wbuf, c->dlam,
+                      c->bpart, c->bGam, c->bRho, c->bRhoN, c->bC})
         if (p) cudaFree(p);
     if (c->ctl_mem) cudaFree(c->ctl_mem);
+    if (c->brank) cudaFree(c->brank);
+    if (c->g_block) cudaGraphExecDestroy(c->g_block);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
     if (c->h_dbl) cudaFreeHost(c->h_dbl);
     if (c->ev_in) cudaEventDestroy(c->ev_in);

@@ -1,0 +1,81 @@
+"""NEXT-3 on the GPU: block PCG (mgBPCG) reaches the same
+solutions as the direct oracle and as batched PCG; block size one is PCG; duplicate columns
+deflate."""
+
+import functools
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import assemble, solve  # noqa: E402
+from workloads import generate, get_config  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def to_dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+@functools.lru_cache(maxsize=None)
+def case(name):
+    cfg = get_config(name)
+    inp = generate(cfg)
+    K = assemble.assemble_K(cfg.nel, inp["E"], inp["fixed"])
+    return cfg, inp, K
+
+
+def handle(name):
+    import paper_1909_13585_b200 as mg
+    cfg, inp, _ = case(name)
+    return mg.mg_setup(cfg.nel, to_dev(inp["E"]), to_dev(inp["fixed"]), cfg.levels)
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b, axis=-1) / np.linalg.norm(b, axis=-1)
+
+
+@pytest.mark.parametrize("name", ["T2a", "T2b", "T2c", "C2", "T3a", "T3b"])
+def test_block_solve_parity_and_iterations(name):
+    import paper_1909_13585_b200 as mg
+    cfg, inp, K = case(name)
+    U = solve.direct_solve(K, inp["rhs"], inp["fixed"])
+    h = handle(name)
+    xb = torch.empty((cfg.nrhs, U.shape[1]), dtype=torch.float64, device=DEV)
+    rep = mg.mgcg_block_solve(h, to_dev(inp["rhs"]), cfg.tol, xb)
+    assert rel(xb.cpu().numpy(), U).max() < 1e-8, rep
+    assert max(rep["true_relres"]) <= cfg.tol
+    x = torch.empty_like(xb)
+    rb = mg.mgcg_solve(h, to_dev(inp["rhs"]), cfg.tol, x)
+    assert rel(xb.cpu().numpy(), x.cpu().numpy()).max() < 1e-8
+    # a shared Krylov space never needs more iterations than the slowest independent solve
+    assert max(rep["iters"]) <= max(rb["iters"]) + 1
+
+
+def test_block_size_one_is_pcg():
+    import paper_1909_13585_b200 as mg
+    cfg, inp, K = case("T2b")
+    h = handle("T2b")
+    b = to_dev(inp["rhs"][:1])
+    xb = torch.empty_like(b)
+    x = torch.empty_like(b)
+    rb = mg.mgcg_block_solve(h, b, 1e-10, xb)
+    rp = mg.mgcg_solve(h, b, 1e-10, x)
+    assert abs(rb["iters"][0] - rp["iters"][0]) <= 1
+    assert rel(xb.cpu().numpy(), x.cpu().numpy()).max() < 1e-9
+
+
+def test_block_duplicate_columns_deflate():
+    import paper_1909_13585_b200 as mg
+    cfg, inp, K = case("T2a")
+    h = handle("T2a")
+    F = np.stack([inp["rhs"][1], inp["rhs"][1], inp["rhs"][2]])
+    U = solve.direct_solve(K, F, inp["fixed"])
+    xb = torch.empty((3, F.shape[1]), dtype=torch.float64, device=DEV)
+    rep = mg.mgcg_block_solve(h, to_dev(F), 1e-10, xb)
+    X = xb.cpu().numpy()
+    assert rel(X, U).max() < 1e-8, rep
+    assert np.abs(X[0] - X[1]).max() <= 1e-12 * np.abs(X[0]).max()
