@@ -172,6 +172,20 @@ mg_status mgcg_solve(mg_handle h, const double* rhs, int nrhs, double tol, doubl
  * the block iterations until column k converged.  Single slab this round. */
 mg_status mgcg_block_solve(mg_handle h, const double* rhs, int nrhs, double tol, double* x, mg_report* rep);
 
+/* NEXT-2: multilevel approximation of the q lowest buckling modes, the four
+ * steps of PAPER.md:146-175 (Sec. 2.1):
+ *   1. coarse eigenproblem (K^l + lambda^l G^l) psi^l = 0 (Eq. 6) with K^l, G^l the Galerkin
+ *      projections on the coarsest level (G^l by the same element agglomeration as K^l);
+ *      solved on the device by subspace iteration with the coarsest K^-1 and a host
+ *      Rayleigh-Ritz on the (q+8)-dimensional subspace;
+ *   2. Psi = I^1_2 ... I^{l-1}_l Psi^l (prolongation to the fine level);
+ *   3. K Phi~ = G Psi (Eq. 7) by block PCG (mgcg_block_solve, mgBPCG) to tol;
+ *   4. lambda~_i = -phi~_i^T K phi~_i / phi~_i^T G phi~_i (Eq. 8).
+ *   Es_e (nelem), u (ndof): device; Phi (q, ndof) device output; lam_tilde (q) host output;
+ *   lam_coarse (q) host output or NULL.  1 <= q <= 32, levels >= 2, single slab. Synchronous. */
+mg_status mg_multilevel_modes(mg_handle h, const double* Es_e, const double* u, int q, double tol, double* Phi,
+                              double* lam_tilde, double* lam_coarse);
+
 /* y_k = G(u) phi_k for k < nphi (PAPER.md:99 G_e = E_sigma G_e0[u_e]; Eq. 6 :163):
  *   Es_e  device, nelem fp64 stress moduli E_sigma(x_e) = x_e^p E_1 (Eq. 2 :106).
  *   u     device, ndof fp64 displacement (taken as given, incl. fixed DOFs).

@@ -17,7 +17,7 @@ from ._lib import MgDist, MgError, MgGrid, MgOpts, MgReport, check, lib
 
 __all__ = [
     "Handle", "MgError", "mg_setup", "mg_setup_dist", "mg_partition", "mg_nccl_unique_id", "mg_local_info",
-    "mg_update_modulus", "mg_adjoint_rhs", "mg_eigen_sensitivity", "mgcg_block_solve", "mgcg_solve", "stress_stiffness_apply",
+    "mg_update_modulus", "mg_adjoint_rhs", "mg_eigen_sensitivity", "mgcg_block_solve", "mg_multilevel_modes", "mgcg_solve", "stress_stiffness_apply",
     "mg_matvec", "mg_vcycle", "mg_restrict", "mg_prolong", "mg_level_info", "mg_get_diagonal",
     "mg_get_coarse_inverse", "mg_kernel_launches", "mg_profile_kernels", "mg_destroy", "lib_path",
 ]
@@ -165,6 +165,15 @@ def mgcg_block_solve(h, rhs, tol, x, raise_on_error=True):
     if raise_on_error:
         check(st)
     return out
+
+
+def mg_multilevel_modes(h, Es, u, q, Phi, tol=1e-10):
+    """Sec. 2.1 multilevel modes: fills Phi (q, ndof) and returns (lam_tilde, lam_coarse) lists."""
+    lt = np.zeros(q)
+    lc = np.zeros(q)
+    check(lib.mg_multilevel_modes(h.raw, _ptr(Es, np.float64), _ptr(u, np.float64), q, tol, _ptr(Phi, np.float64),
+                                  _ptr(lt, np.float64), _ptr(lc, np.float64)))
+    return list(lt), list(lc)
 
 
 def stress_stiffness_apply(h, Es, u, phi, y):

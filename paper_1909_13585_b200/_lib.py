@@ -21,7 +21,7 @@ STATUS = {
 
 EXPORTED = [
     "mg_setup", "mg_setup_dist", "mg_partition", "mg_nccl_unique_id", "mg_local_info", "mg_update_modulus",
-    "mg_adjoint_rhs", "mg_eigen_sensitivity", "mgcg_block_solve", "mgcg_solve", "stress_stiffness_apply", "mg_matvec", "mg_vcycle",
+    "mg_adjoint_rhs", "mg_eigen_sensitivity", "mgcg_block_solve", "mg_multilevel_modes", "mgcg_solve", "stress_stiffness_apply", "mg_matvec", "mg_vcycle",
     "mg_restrict", "mg_prolong", "mg_level_info", "mg_get_diagonal", "mg_get_coarse_inverse",
     "mg_kernel_launches", "mg_profile_kernels", "mg_destroy", "mg_strerror", "mg_last_error",
 ]
@@ -99,6 +99,7 @@ def _load():
         "mg_update_modulus": ([P, P], I),
         "mgcg_solve": ([P, P, I, D, P, ctypes.POINTER(MgReport)], I),
         "mgcg_block_solve": ([P, P, I, D, P, ctypes.POINTER(MgReport)], I),
+        "mg_multilevel_modes": ([P, P, P, I, D, P, P, P], I),
         "stress_stiffness_apply": ([P, P, P, P, I, P], I),
         "mg_adjoint_rhs": ([P, P, P, I, P], I),
         "mg_eigen_sensitivity": ([P, P, P, P, P, P, P, I, P], I),

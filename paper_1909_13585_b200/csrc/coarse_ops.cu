@@ -15,6 +15,7 @@
 
 __constant__ double c_K0g[576];
 __constant__ double c_Q[8 * 8 * 8];   // [child][fine local node a][coarse local node b]
+__constant__ double c_Hg[3 * 3 * 8 * 8];   // H_ij[a][b] = int dN_a/dx_i dN_b/dx_j (G element matrices)
 
 void galerkin_set_constants(int dim, const double* K0, cudaStream_t s) {
     int nl = dim * (1 << dim);
@@ -36,6 +37,25 @@ void galerkin_set_constants(int dim, const double* K0, cudaStream_t s) {
                 Q[(c * na + a) * na + b] = v;
             }
     cudaMemcpyToSymbolAsync(c_Q, Q, sizeof(double) * na * na * na, 0, cudaMemcpyHostToDevice, s);
+    static double H[3 * 3 * 8 * 8];
+    const double M1[2][2] = {{1.0 / 3, 1.0 / 6}, {1.0 / 6, 1.0 / 3}};
+    const double D1[2][2] = {{1.0, -1.0}, {-1.0, 1.0}};
+    const double C1[2][2] = {{-0.5, -0.5}, {0.5, 0.5}};
+    for (int i = 0; i < dim; ++i)
+        for (int j = 0; j < dim; ++j)
+            for (int a = 0; a < na; ++a)
+                for (int b = 0; b < na; ++b) {
+                    double v = 1.0;
+                    for (int k = 0; k < dim; ++k) {
+                        const int ak = (a >> (dim - 1 - k)) & 1, bk = (b >> (dim - 1 - k)) & 1;
+                        if (k == i && k == j) v *= D1[ak][bk];
+                        else if (k == i) v *= C1[ak][bk];
+                        else if (k == j) v *= C1[bk][ak];
+                        else v *= M1[ak][bk];
+                    }
+                    H[((i * 3 + j) * 8 + a) * 8 + b] = v;
+                }
+    cudaMemcpyToSymbolAsync(c_Hg, H, sizeof(H), 0, cudaMemcpyHostToDevice, s);
 }
 
 __device__ __forceinline__ void node_coords(const LevelGeom& g, long long node, int* idx) {
@@ -75,7 +95,9 @@ void elements_from_E(const LevelGeom& g, const double* E, const uint8_t* mask, d
 // Level 1 from E: when none of the 3^d fine nodes of the coarse element is fixed, every
 // child matrix is E_c K0 and K_E = sum_c E_c M_c with the constant M_c = Q_c^T K0 Q_c
 // (c_M, set once per handle) -- one FMA per child instead of two small matrix products.
-template <int DIM, bool FROM_E>
+// SRC: 0 = child element matrices elm_f (levels >= 2), 1 = E_e K0 (K, level 1), 2 = the stress
+// stiffness Es_e (sigma_e : H) kron I_d from per-element Voigt stresses in E (G, level 1; NEXT-2)
+template <int DIM, int SRC>
 __global__ void galerkin_kernel(LevelGeom gc, LevelGeom gf, const double* __restrict__ E,
                                 const double* __restrict__ elm_f, const uint8_t* __restrict__ mask_f,
                                 const uint8_t* __restrict__ mask_c, double* __restrict__ elm_c, int off0,
@@ -94,6 +116,7 @@ __global__ void galerkin_kernel(LevelGeom gc, LevelGeom gf, const double* __rest
     if (ci[0] < off0) return;
     double acc = 0.0;
     bool fast = false;
+    constexpr bool FROM_E = SRC == 1;
     if (FROM_E && Mc) {
         constexpr int NF = DIM == 2 ? 9 : 27;   // fine nodes of the coarse element
         int fixed_here = 0;
@@ -125,7 +148,7 @@ __global__ void galerkin_kernel(LevelGeom gc, LevelGeom gf, const double* __rest
         for (int k = 0; k < DIM; ++k) fi[k] = 2 * ci[k] + ((ch >> (DIM - 1 - k)) & 1) - (k == 0 ? off0 : 0);
         long long fe = fi[0];
         for (int k = 1; k < DIM; ++k) fe = fe * gf.N[k] + fi[k];
-        if (FROM_E) {
+        if (SRC == 1 || SRC == 2) {
             if (t < NL) {
                 int a = t / DIM, comp = t % DIM;
                 long long node = 0;
@@ -133,7 +156,22 @@ __global__ void galerkin_kernel(LevelGeom gc, LevelGeom gf, const double* __rest
                 fr[t] = ((mask_f[node] >> comp) & 1) ? 0.0 : 1.0;
             }
             __syncthreads();
-            Kc[t] = E[fe] * c_K0g[t] * fr[row] * fr[col];
+            if (SRC == 1) {
+                Kc[t] = E[fe] * c_K0g[t] * fr[row] * fr[col];
+            } else {
+                constexpr int NV = DIM == 2 ? 3 : 6;
+                const int a = row / DIM, b = col / DIM;
+                double v = 0.0;
+                if (row % DIM == col % DIM) {
+                    const double* sg = E + fe * NV;
+                    for (int i = 0; i < DIM; ++i) v += sg[i] * c_Hg[((i * 3 + i) * 8 + a) * 8 + b];
+                    for (int q = 0; q < NV - DIM; ++q) {
+                        const int i = DIM == 2 ? 0 : (q == 0 ? 1 : 0), j = DIM == 2 ? 1 : (q == 2 ? 1 : 2);
+                        v += sg[DIM + q] * (c_Hg[((i * 3 + j) * 8 + a) * 8 + b] + c_Hg[((j * 3 + i) * 8 + a) * 8 + b]);
+                    }
+                }
+                Kc[t] = v * fr[row] * fr[col];
+            }
         } else {
             Kc[t] = elm_f[fe * NL * NL + t];   // already masked at level l-1
         }
@@ -169,12 +207,20 @@ void galerkin_elements(const LevelGeom& gc, const LevelGeom& gf, const double* E
                        const double* Mc) {
     unsigned bl = (unsigned)gc.nelem;
     if (gc.dim == 2) {
-        if (E) galerkin_kernel<2, true><<<bl, 64, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, Mc);
-        else galerkin_kernel<2, false><<<bl, 64, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, nullptr);
+        if (E) galerkin_kernel<2, 1><<<bl, 64, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, Mc);
+        else galerkin_kernel<2, 0><<<bl, 64, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, nullptr);
     } else {
-        if (E) galerkin_kernel<3, true><<<bl, 576, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, Mc);
-        else galerkin_kernel<3, false><<<bl, 576, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, nullptr);
+        if (E) galerkin_kernel<3, 1><<<bl, 576, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, Mc);
+        else galerkin_kernel<3, 0><<<bl, 576, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, nullptr);
     }
+}
+
+// level-1 Galerkin element matrices of G from the fine per-element Voigt stresses (Es included)
+void galerkin_elements_G(const LevelGeom& gc, const LevelGeom& gf, const double* sig, const uint8_t* mask_f,
+                         const uint8_t* mask_c, double* elm_c, cudaStream_t s) {
+    unsigned bl = (unsigned)gc.nelem;
+    if (gc.dim == 2) galerkin_kernel<2, 2><<<bl, 64, 0, s>>>(gc, gf, sig, nullptr, mask_f, mask_c, elm_c, 0, nullptr);
+    else galerkin_kernel<3, 2><<<bl, 576, 0, s>>>(gc, gf, sig, nullptr, mask_f, mask_c, elm_c, 0, nullptr);
 }
 
 // M_c = Q_c^T K0 Q_c for the 2^d children (host, once per handle); layout [child][NL*NL]
@@ -205,7 +251,7 @@ void galerkin_child_matrices(int dim, const double* K0, double* Mc_host) {
 // node+delta_s (local b = a + delta_s) of elm[E][(a,k),(b,k2)]; identity at fixed DOFs.
 template <int DIM>
 __global__ void stencil_kernel(LevelGeom g, const double* __restrict__ elm, const uint8_t* __restrict__ mask,
-                               double* __restrict__ st) {
+                               double* __restrict__ st, int ident) {
     constexpr int NA = 1 << DIM, NL = DIM * NA;
     constexpr int NS = DIM == 2 ? 9 : 27;
     long long node = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -248,18 +294,19 @@ __global__ void stencil_kernel(LevelGeom g, const double* __restrict__ elm, cons
 #pragma unroll
         for (int k2 = 0; k2 < DIM; ++k2) {
             double v = acc[k * DIM + k2];
-            if (center && k == k2 && ((mb >> k) & 1)) v = 1.0;
+            if (ident && center && k == k2 && ((mb >> k) & 1)) v = 1.0;
             st[((long long)(s * DIM + k) * DIM + k2) * g.nnodes + node] = v;
         }
 }
 
-void stencil_from_elements(const LevelGeom& g, const double* elm, uint8_t* mask, double* st, cudaStream_t s) {
+void stencil_from_elements(const LevelGeom& g, const double* elm, uint8_t* mask, double* st, cudaStream_t s,
+                           bool identity_fixed) {
     int th = 128;
     dim3 grid((unsigned)((g.nnodes + th - 1) / th), g.dim == 2 ? 9 : 27);
     if (g.dim == 2)
-        stencil_kernel<2><<<grid, th, 0, s>>>(g, elm, mask, st);
+        stencil_kernel<2><<<grid, th, 0, s>>>(g, elm, mask, st, identity_fixed ? 1 : 0);
     else
-        stencil_kernel<3><<<grid, th, 0, s>>>(g, elm, mask, st);
+        stencil_kernel<3><<<grid, th, 0, s>>>(g, elm, mask, st, identity_fixed ? 1 : 0);
 }
 
 // Diagonal from the stencil centre; free DOFs with zero Galerkin diagonal become fixed.

@@ -136,7 +136,11 @@ void galerkin_elements(const LevelGeom& gc, const LevelGeom& gf, const double* E
                        double* elm_c, cudaStream_t s, int off0 = 0, const double* Mc = nullptr);
 void galerkin_child_matrices(int dim, const double* K0, double* Mc_host);
 void elements_from_E(const LevelGeom& g, const double* E, const uint8_t* mask, double* elm, cudaStream_t s);
-void stencil_from_elements(const LevelGeom& g, const double* elm, uint8_t* mask, double* st, cudaStream_t s);
+// identity_fixed: identity rows at fixed DOFs (K); false for G (zero rows/cols)
+void stencil_from_elements(const LevelGeom& g, const double* elm, uint8_t* mask, double* st, cudaStream_t s,
+                           bool identity_fixed = true);
+void galerkin_elements_G(const LevelGeom& gc, const LevelGeom& gf, const double* sig, const uint8_t* mask_f,
+                         const uint8_t* mask_c, double* elm_c, cudaStream_t s);
 void stencil_diag(const LevelGeom& g, const double* st, uint8_t* mask, double* st_rw, double* Dinv, double* D,
                   cudaStream_t s);
 

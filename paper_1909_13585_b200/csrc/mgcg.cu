@@ -1901,6 +1901,250 @@ mg_status mgcg_block_solve(mg_handle c, const double* rhs, int nrhs, double tol,
     return MG_OK;
 }
 
+// ---------------------------------------------------------------- multilevel buckling modes (NEXT-2)
+// Host: symmetric eigen decomposition of a small p x p matrix by cyclic Jacobi rotations
+// (A is destroyed; eigenvalues in w, eigenvectors in the columns of V, row-major).
+static void jacobi_eig(int p, std::vector<double>& A, std::vector<double>& w, std::vector<double>& V) {
+    V.assign((size_t)p * p, 0.0);
+    for (int i = 0; i < p; ++i) V[i * p + i] = 1.0;
+    for (int sweep = 0; sweep < 100; ++sweep) {
+        double off = 0.0;
+        for (int i = 0; i < p; ++i)
+            for (int j = i + 1; j < p; ++j) off += A[i * p + j] * A[i * p + j];
+        if (off < 1e-30) break;
+        for (int i = 0; i < p; ++i)
+            for (int j = i + 1; j < p; ++j) {
+                const double aij = A[i * p + j];
+                if (std::fabs(aij) < 1e-300) continue;
+                const double th = 0.5 * (A[j * p + j] - A[i * p + i]) / aij;
+                const double t = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
+                const double cs = 1.0 / std::sqrt(t * t + 1.0), sn = t * cs;
+                for (int k = 0; k < p; ++k) {   // A <- J^T A J
+                    const double aki = A[k * p + i], akj = A[k * p + j];
+                    A[k * p + i] = cs * aki - sn * akj;
+                    A[k * p + j] = sn * aki + cs * akj;
+                }
+                for (int k = 0; k < p; ++k) {
+                    const double aik = A[i * p + k], ajk = A[j * p + k];
+                    A[i * p + k] = cs * aik - sn * ajk;
+                    A[j * p + k] = sn * aik + cs * ajk;
+                }
+                for (int k = 0; k < p; ++k) {
+                    const double vki = V[k * p + i], vkj = V[k * p + j];
+                    V[k * p + i] = cs * vki - sn * vkj;
+                    V[k * p + j] = sn * vki + cs * vkj;
+                }
+            }
+    }
+    w.resize(p);
+    for (int i = 0; i < p; ++i) w[i] = A[i * p + i];
+}
+
+// Generalized symmetric-definite p x p problem A y = theta B y (B SPD): Cholesky B = L L^T,
+// C = L^-1 A L^-T, Jacobi on C, Y = L^-T W.  Returns false if B is not positive definite.
+static bool small_geneig(int p, const std::vector<double>& A, const std::vector<double>& B, std::vector<double>& th,
+                         std::vector<double>& Y) {
+    std::vector<double> L((size_t)p * p, 0.0);
+    for (int j = 0; j < p; ++j) {
+        double d = B[j * p + j];
+        for (int k = 0; k < j; ++k) d -= L[j * p + k] * L[j * p + k];
+        if (!(d > 0.0)) return false;
+        L[j * p + j] = std::sqrt(d);
+        for (int i = j + 1; i < p; ++i) {
+            double v = B[i * p + j];
+            for (int k = 0; k < j; ++k) v -= L[i * p + k] * L[j * p + k];
+            L[i * p + j] = v / L[j * p + j];
+        }
+    }
+    // M = L^-1 A ; C = M L^-T
+    std::vector<double> M((size_t)p * p), C((size_t)p * p);
+    for (int c = 0; c < p; ++c)
+        for (int i = 0; i < p; ++i) {
+            double v = A[i * p + c];
+            for (int k = 0; k < i; ++k) v -= L[i * p + k] * M[k * p + c];
+            M[i * p + c] = v / L[i * p + i];
+        }
+    for (int r = 0; r < p; ++r)
+        for (int i = 0; i < p; ++i) {
+            double v = M[r * p + i];
+            for (int k = 0; k < i; ++k) v -= C[r * p + k] * L[i * p + k];
+            C[r * p + i] = v / L[i * p + i];
+        }
+    for (int i = 0; i < p; ++i)
+        for (int j = i + 1; j < p; ++j) C[i * p + j] = C[j * p + i] = 0.5 * (C[i * p + j] + C[j * p + i]);
+    std::vector<double> W;
+    jacobi_eig(p, C, th, W);
+    // Y = L^-T W
+    Y.assign((size_t)p * p, 0.0);
+    for (int c = 0; c < p; ++c)
+        for (int i = p - 1; i >= 0; --i) {
+            double v = W[i * p + c];
+            for (int k = i + 1; k < p; ++k) v -= L[k * p + i] * Y[k * p + c];
+            Y[i * p + c] = v / L[i * p + i];
+        }
+    return true;
+}
+
+mg_status mg_multilevel_modes(mg_handle c, const double* Es_e, const double* u, int q, double tol, double* Phi,
+                              double* lam_tilde, double* lam_coarse) {
+    if (!c || !Es_e || !u || !Phi || !lam_tilde) return fail(MG_ERR_ARG, "NULL argument");
+    if (q < 1 || q > 32) return fail(MG_ERR_ARG, "q must be in [1, 32]");
+    if (multi(c)) return fail(MG_ERR_ARG, "mg_multilevel_modes: single slab only (this round)");
+    for (const void* p : {(const void*)Es_e, (const void*)u, (const void*)Phi})
+        if (!is_device_ptr(p)) return fail(MG_ERR_ARG, "mg_multilevel_modes: device pointers required");
+    const int dim = c->dim, L = c->L, NL = dim * (1 << dim), nv = dim == 2 ? 3 : 6;
+    const int pblk = std::min<int>(q + 8, 48);       // subspace size (oversampled)
+    if ((long long)c->nL < pblk) return fail(MG_ERR_DIM, "coarsest level smaller than the mode subspace");
+    TRY(ensure_vectors(c, std::max(q, 1)));
+    cudaStream_t s = c->stream;
+    stream_enter(c);
+    Slab& sl = c->sl[0];
+    const LevelGeom& g0 = sl.lv[0].g;
+    const long long n = g0.ndof, nL = c->nL, ld = c->npad;
+    // ---- step 1: G^l by Galerkin projection (element agglomeration, like K) and the coarse
+    //      eigenproblem (K^l + lambda G^l) psi = 0 by subspace iteration with K^-1 (Ainv)
+    std::vector<void*> tmp;
+    auto dalloc = [&](size_t bytes) -> double* {
+        void* p = nullptr;
+        if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) return nullptr;
+        tmp.push_back(p);
+        return (double*)p;
+    };
+    auto cleanup = [&]() {
+        for (void* p : tmp) cudaFreeAsync(p, s);
+        tmp.clear();
+    };
+    double* sig = dalloc(sizeof(double) * g0.nelem * nv);
+    double* Gd = dalloc(sizeof(double) * ld * ld);
+    double* Kd = dalloc(sizeof(double) * ld * ld);
+    double* stG = L > 1 ? dalloc(sizeof(double) * sl.lv[L - 1].g.nnodes * (dim == 2 ? 9 : 27) * dim * dim) : nullptr;
+    double* V = dalloc(sizeof(double) * pblk * nL);
+    double* W = dalloc(sizeof(double) * pblk * nL);
+    double* KV = dalloc(sizeof(double) * pblk * nL);
+    double* GV = dalloc(sizeof(double) * pblk * nL);
+    double* gpart = dalloc(sizeof(double) * (long long)pblk * pblk * gram_blocks(std::max(n, nL), pblk));
+    double* Gr = dalloc(sizeof(double) * pblk * pblk);
+    double* Yd = dalloc(sizeof(double) * pblk * pblk);
+    double* Psi = dalloc(sizeof(double) * q * n);
+    double* GPsi = dalloc(sizeof(double) * q * n);
+    double* KPhi = dalloc(sizeof(double) * q * n);
+    for (void* p : tmp)
+        if (!p) { cleanup(); return fail(MG_ERR_OOM, "mg_multilevel_modes workspace"); }
+    stress_sigma(g0, Es_e, u, sig, s);
+    c->launches++;
+    if (L > 1) {
+        for (int l = 1; l < L; ++l) {
+            Level& f = sl.lv[l - 1];
+            Level& gl = sl.lv[l];
+            double* elm = (l & 1) ? sl.elmA : sl.elmB;
+            double* elm_prev = (l & 1) ? sl.elmB : sl.elmA;
+            if (l == 1) galerkin_elements_G(gl.g, f.g, sig, f.mask, gl.mask, elm, s);
+            else galerkin_elements(gl.g, f.g, nullptr, elm_prev, f.mask, gl.mask, elm, s);
+            c->launches++;
+        }
+        Level& cl = sl.lv[L - 1];
+        stencil_from_elements(cl.g, (L - 1) & 1 ? sl.elmA : sl.elmB, cl.mask, stG, s, false);
+        CU(cudaMemsetAsync(Gd, 0, sizeof(double) * ld * ld, s));
+        dense_from_stencil(cl.g, stG, Gd, ld, s);
+        CU(cudaMemsetAsync(Kd, 0, sizeof(double) * ld * ld, s));
+        dense_from_stencil(cl.g, cl.st, Kd, ld, s);
+        c->launches += 3;
+    } else {
+        cleanup();
+        stream_leave(c);
+        return fail(MG_ERR_ARG, "mg_multilevel_modes needs levels >= 2");
+    }
+    CHECK_LAUNCH();
+    // subspace iteration: V <- K^-1 G V, Rayleigh-Ritz on (-G, K) every step (V K-orthonormal)
+    {
+        std::vector<double> init((size_t)pblk * nL);
+        uint64_t st = 0x9E3779B97F4A7C15ull;
+        for (auto& v : init) {   // deterministic pseudo-random start (xorshift)
+            st ^= st << 13; st ^= st >> 7; st ^= st << 17;
+            v = (double)(st >> 11) / 9007199254740992.0 - 0.5;
+        }
+        CU(cudaMemcpyAsync(V, init.data(), sizeof(double) * init.size(), cudaMemcpyHostToDevice, s));
+        CU(cudaStreamSynchronize(s));
+    }
+    std::vector<double> Ah((size_t)pblk * pblk), Bh((size_t)pblk * pblk), th, Y, prev(q, 0.0);
+    std::vector<double> lamc(q, 0.0);
+    int iters = 0;
+    for (; iters < 500; ++iters) {
+        dense_apply(Gd, ld, nL, V, W, pblk, nullptr, nullptr, s);       // W = G V
+        dense_apply(c->Ainv, ld, nL, W, V, pblk, nullptr, nullptr, s);  // V = K^-1 G V  (= -K^-1 (-G) V)
+        dense_apply(Gd, ld, nL, V, GV, pblk, nullptr, nullptr, s);
+        dense_apply(Kd, ld, nL, V, KV, pblk, nullptr, nullptr, s);
+        gram(nL, nL, pblk, V, GV, gpart, Gr, s);
+        CU(cudaMemcpyAsync(Ah.data(), Gr, sizeof(double) * pblk * pblk, cudaMemcpyDeviceToHost, s));
+        gram(nL, nL, pblk, V, KV, gpart, Gr, s);
+        CU(cudaMemcpyAsync(Bh.data(), Gr, sizeof(double) * pblk * pblk, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        c->launches += 8;
+        for (auto& v : Ah) v = -v;                                      // (-G, K)
+        if (!small_geneig(pblk, Ah, Bh, th, Y)) {
+            cleanup();
+            stream_leave(c);
+            return fail(MG_ERR_BREAKDOWN, "mg_multilevel_modes: coarse Gram matrix not SPD");
+        }
+        // order by decreasing theta (largest theta = smallest positive lambda)
+        std::vector<int> ord(pblk);
+        for (int i = 0; i < pblk; ++i) ord[i] = i;
+        std::sort(ord.begin(), ord.end(), [&](int a, int b) { return th[a] > th[b]; });
+        std::vector<double> Ys((size_t)pblk * pblk);
+        for (int r = 0; r < pblk; ++r)
+            for (int j = 0; j < pblk; ++j) Ys[r * pblk + j] = Y[r * pblk + ord[j]];
+        CU(cudaMemcpyAsync(Yd, Ys.data(), sizeof(double) * pblk * pblk, cudaMemcpyHostToDevice, s));
+        CU(cudaMemsetAsync(W, 0, sizeof(double) * pblk * nL, s));
+        block_axpy(nL, nL, pblk, V, Yd, nullptr, W, 1.0, s);          // W = V Y
+        CU(cudaMemcpyAsync(V, W, sizeof(double) * pblk * nL, cudaMemcpyDeviceToDevice, s));
+        double change = 0.0;
+        for (int i = 0; i < q; ++i) {
+            const double t = th[ord[i]];
+            if (!(t > 0.0)) { change = 1.0; lamc[i] = INFINITY; continue; }
+            lamc[i] = 1.0 / t;
+            change = std::max(change, std::fabs(lamc[i] - prev[i]) / std::fabs(lamc[i]));
+            prev[i] = lamc[i];
+        }
+        if (iters > 2 && change < 1e-13) { ++iters; break; }
+    }
+    if (lam_coarse)
+        for (int i = 0; i < q; ++i) lam_coarse[i] = lamc[i];
+    // ---- step 2: Psi^j = I^j_{j+1} Psi^{j+1} down to the fine level
+    {
+        const double* src = V;   // first q columns (sorted), coarsest level layout
+        for (int l = L - 2; l >= 0; --l) {
+            Level& f = sl.lv[l];
+            Level& cl = sl.lv[l + 1];
+            double* dst = l == 0 ? Psi : f.z;
+            prolong_add(f.g, cl.g, f.mask, cl.mask, src, dst, q, nullptr, nullptr, false, s);
+            c->launches++;
+            src = dst;
+        }
+    }
+    stream_leave(c);
+    // ---- step 3: K Phi~ = G Psi by block PCG (mgBPCG, Alg. 2 l.15)
+    TRY(([&]() -> mg_status {
+        mg_status st = stress_stiffness_apply(c, Es_e, u, Psi, q, GPsi);
+        if (st != MG_OK) return st;
+        return mgcg_block_solve(c, GPsi, q, tol, Phi, nullptr);
+    }()));
+    // ---- step 4: Rayleigh quotients lambda~_i = -phi~^T K phi~ / phi~^T G phi~
+    TRY(mg_matvec(c, 0, Phi, q, KPhi));
+    TRY(stress_stiffness_apply(c, Es_e, u, Phi, q, GPsi));
+    stream_enter(c);
+    std::vector<double> num((size_t)q * q), den((size_t)q * q);
+    gram(n, n, q, Phi, KPhi, gpart, Gr, s);
+    CU(cudaMemcpyAsync(num.data(), Gr, sizeof(double) * q * q, cudaMemcpyDeviceToHost, s));
+    gram(n, n, q, Phi, GPsi, gpart, Gr, s);
+    CU(cudaMemcpyAsync(den.data(), Gr, sizeof(double) * q * q, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    for (int i = 0; i < q; ++i) lam_tilde[i] = -num[i * q + i] / den[i * q + i];
+    cleanup();
+    CU(cudaStreamSynchronize(s));
+    stream_leave(c);
+    return MG_OK;
+}
+
 mg_status mg_matvec(mg_handle c, int level, const double* x, int nrhs, double* y) {
     if (!c || !x || !y) return fail(MG_ERR_ARG, "NULL argument");
     if (level < 0 || level >= c->L || nrhs < 1 || nrhs > MG_MAX_RHS) return fail(MG_ERR_ARG, "bad level / nrhs");

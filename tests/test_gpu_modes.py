@@ -1,0 +1,37 @@
+"""NEXT-2 on the GPU: the multilevel mode approximation through
+the C ABI against the pinned oracle pipeline (oracle/modes.py) -- coarse BLFs, fine Rayleigh
+quotients and the fine mode shapes (up to sign)."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import assemble, modes, solve  # noqa: E402
+from workloads import generate, get_config  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def to_dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+@pytest.mark.parametrize("name,q", [("T2a", 3), ("T2c", 4), ("C1", 6), ("T3a", 3), ("T3b", 2)])
+def test_multilevel_modes_parity(name, q):
+    import paper_1909_13585_b200 as mg
+    cfg = get_config(name)
+    inp = generate(cfg)
+    K = assemble.assemble_K(cfg.nel, inp["E"], inp["fixed"])
+    u = solve.direct_solve(K, inp["rhs"][0], inp["fixed"])
+    lam_c, Psi, Phi, lam_t = modes.multilevel_modes(cfg.nel, inp["E"], inp["Es"], inp["fixed"], u, cfg.levels, q)
+    h = mg.mg_setup(cfg.nel, to_dev(inp["E"]), to_dev(inp["fixed"]), cfg.levels)
+    P = torch.empty((q, Phi.shape[1]), dtype=torch.float64, device=DEV)
+    lt, lc = mg.mg_multilevel_modes(h, to_dev(inp["Es"]), to_dev(u), q, P)
+    assert np.allclose(lc, lam_c, rtol=1e-9), (lc, lam_c)
+    assert np.allclose(lt, lam_t, rtol=1e-7), (lt, lam_t)
+    Pg = P.cpu().numpy()
+    for i in range(q):
+        s = np.sign(Pg[i] @ Phi[i])
+        assert np.linalg.norm(s * Pg[i] - Phi[i]) / np.linalg.norm(Phi[i]) < 1e-6
