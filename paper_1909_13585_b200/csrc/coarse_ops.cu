@@ -342,15 +342,25 @@ void stencil_diag(const LevelGeom& g, const double* /*st*/, uint8_t* mask, doubl
 
 // ---------------------------------------------------------------- stencil operator kernels
 // Thread per node; all R vectors (chunks of RB) accumulated in registers so the
-// stencil (3^d d^2 doubles per node) is read once per chunk.
+// stencil (3^d d^2 doubles per node) is read once per chunk.  The 3^d neighbour loop is
+// unrolled (compile-time offsets, no local-memory index arrays).
 template <int DIM, int OP, int RB>
 __global__ void __launch_bounds__(128) coarse_kernel(CoarseArgs a, int r0) {
     constexpr int NS = DIM == 2 ? 9 : 27;
     long long node = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (node >= a.g.nnodes) return;
     if (a.done && *a.done) return;
-    int idx[3] = {0, 0, 0};
-    node_coords(a.g, node, idx);
+    const int n1 = a.g.nn[1], n2 = DIM == 3 ? a.g.nn[2] : 1;
+    int i0, i1, i2 = 0;
+    if (DIM == 3) {
+        i2 = (int)(node % n2);
+        const long long t = node / n2;
+        i1 = (int)(t % n1);
+        i0 = (int)(t / n1);
+    } else {
+        i1 = (int)(node % n1);
+        i0 = (int)(node / n1);
+    }
     const int nr = min(RB, a.R - r0);
     bool act[RB];
 #pragma unroll
@@ -361,19 +371,15 @@ __global__ void __launch_bounds__(128) coarse_kernel(CoarseArgs a, int r0) {
 #pragma unroll
         for (int k = 0; k < DIM; ++k) acc[q][k] = 0.0;
     const long long nn = a.g.nnodes;
-#pragma unroll 1
+#pragma unroll
     for (int s = 0; s < NS; ++s) {
-        int dl[3] = {0, 0, 0};
-        int ss = s;
-        for (int k = DIM - 1; k >= 0; --k) { dl[k] = ss % 3 - 1; ss /= 3; }
-        bool ok = true;
-        long long q = 0;
-        for (int k = 0; k < DIM; ++k) {
-            int c = idx[k] + dl[k];
-            if (c < 0 || c >= a.g.nn[k]) ok = false;
-            q = q * a.g.nn[k] + c;
-        }
+        const int d0 = DIM == 3 ? s / 9 - 1 : s / 3 - 1;
+        const int d1 = DIM == 3 ? (s / 3) % 3 - 1 : s % 3 - 1;
+        const int d2 = DIM == 3 ? s % 3 - 1 : 0;
+        const bool ok = i0 + d0 >= 0 && i0 + d0 < a.g.nn[0] && i1 + d1 >= 0 && i1 + d1 < n1 &&
+                        (DIM == 2 || (i2 + d2 >= 0 && i2 + d2 < n2));
         if (!ok) continue;
+        const long long q = node + ((long long)d0 * n1 + d1) * n2 + d2;
         double blk[DIM * DIM];
 #pragma unroll
         for (int e = 0; e < DIM * DIM; ++e) blk[e] = a.st[(long long)(s * DIM * DIM + e) * nn + node];

@@ -8,42 +8,28 @@
 // coarse(I,k) = free_c(I,k) * sum_{delta in {-1,0,1}^d} w(delta) free_f(2I+delta,k) fine(2I+delta,k)
 // Slabs: fine local plane f is coincident with coarse local plane I when f = 2I - off0, and only
 // fine planes in [fo0, fo1) (slab-owned) contribute; the coarse ghost plane above then holds a
-// partial sum that the owner adds in (reverse halo exchange).
+// partial sum that the owner adds in (reverse halo exchange).  The 3^d neighbour loop is
+// unrolled with compile-time weights (no per-thread index arrays).
 template <int DIM>
 __global__ void restrict_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* __restrict__ mf,
                                 const uint8_t* __restrict__ mc, const double* __restrict__ fine,
                                 double* __restrict__ coarse, int R, const int* active, const int* done, int off0,
                                 int fo0, int fo1) {
+    constexpr int NS = DIM == 2 ? 9 : 27;
     long long I = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (I >= gc.nnodes) return;
     if (done && *done) return;
     int ci[3] = {0, 0, 0};
-    long long t = I;
-    for (int k = DIM - 1; k >= 0; --k) { ci[k] = (int)(t % gc.nn[k]); t /= gc.nn[k]; }
-    const int mcb = mc[I];
-    constexpr int NS = DIM == 2 ? 9 : 27;
-    long long fnode[NS];
-    double wgt[NS];
-    int fm[NS];
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-        int ss = s;
-        long long q = 0;
-        double w = 1.0;
-        bool ok = true;
-        int dl[3];
-        for (int k = DIM - 1; k >= 0; --k) { dl[k] = ss % 3 - 1; ss /= 3; }
-        for (int k = 0; k < DIM; ++k) {
-            int f = 2 * ci[k] + dl[k] - (k == 0 ? off0 : 0);
-            if (f < 0 || f >= gf.nn[k]) ok = false;
-            if (k == 0 && (f < fo0 || f >= fo1)) ok = false;
-            q = q * gf.nn[k] + f;
-            if (dl[k] != 0) w *= 0.5;
-        }
-        fnode[s] = ok ? q : -1;
-        wgt[s] = w;
-        fm[s] = ok ? mf[q] : 0xff;
+    {
+        long long t = I;
+        if (DIM == 3) { ci[2] = (int)(t % gc.nn[2]); t /= gc.nn[2]; }
+        ci[1] = (int)(t % gc.nn[1]);
+        ci[0] = (int)(t / gc.nn[1]);
     }
+    const int f0 = 2 * ci[0] - off0, f1 = 2 * ci[1], f2 = DIM == 3 ? 2 * ci[2] : 0;
+    const int n1 = gf.nn[1], n2 = DIM == 3 ? gf.nn[2] : 1;
+    const long long fbase = ((long long)f0 * n1 + f1) * n2 + f2;
+    const int mcb = mc[I];
     for (int r = 0; r < R; ++r) {
         if (active && !active[r]) continue;
         const double* fv = fine + (long long)r * gf.ndof;
@@ -52,10 +38,19 @@ __global__ void restrict_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* __res
         for (int k = 0; k < DIM; ++k) acc[k] = 0.0;
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
-            if (fnode[s] < 0) continue;
+            const int d0 = DIM == 3 ? s / 9 - 1 : s / 3 - 1;
+            const int d1 = DIM == 3 ? (s / 3) % 3 - 1 : s % 3 - 1;
+            const int d2 = DIM == 3 ? s % 3 - 1 : 0;
+            const double w = (d0 ? 0.5 : 1.0) * (d1 ? 0.5 : 1.0) * (d2 ? 0.5 : 1.0);
+            const int g0 = f0 + d0;
+            const bool ok = g0 >= 0 && g0 < gf.nn[0] && g0 >= fo0 && g0 < fo1 && f1 + d1 >= 0 && f1 + d1 < n1 &&
+                            (DIM == 2 || (f2 + d2 >= 0 && f2 + d2 < n2));
+            if (!ok) continue;
+            const long long q = fbase + ((long long)d0 * n1 + d1) * n2 + d2;
+            const int fm = mf[q];
 #pragma unroll
             for (int k = 0; k < DIM; ++k)
-                if (!((fm[s] >> k) & 1)) acc[k] = fma(wgt[s], fv[DIM * fnode[s] + k], acc[k]);
+                if (!((fm >> k) & 1)) acc[k] = fma(w, fv[DIM * q + k], acc[k]);
         }
         double* cv = coarse + (long long)r * gc.ndof + DIM * I;
 #pragma unroll
