@@ -30,8 +30,9 @@ __global__ void restrict_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* __res
     const int n1 = gf.nn[1], n2 = DIM == 3 ? gf.nn[2] : 1;
     const long long fbase = ((long long)f0 * n1 + f1) * n2 + f2;
     const int mcb = mc[I];
-    for (int r = 0; r < R; ++r) {
-        if (active && !active[r]) continue;
+    {   // one RHS per thread (grid.y): enough independent loads in flight on small levels
+        const int r = blockIdx.y;
+        if (active && !active[r]) return;
         const double* fv = fine + (long long)r * gf.ndof;
         double acc[DIM];
 #pragma unroll
@@ -63,7 +64,7 @@ void restrict_apply(const LevelGeom& gf, const LevelGeom& gc, const uint8_t* mf,
                     int off0, int fo0, int fo1) {
     if (fo1 < 0) fo1 = gf.nn[0];
     int th = 128;
-    unsigned bl = (unsigned)((gc.nnodes + th - 1) / th);
+    dim3 bl((unsigned)((gc.nnodes + th - 1) / th), R);
     if (gf.dim == 2)
         restrict_kernel<2><<<bl, th, 0, s>>>(gf, gc, mf, mc, fine, coarse, R, active, done, off0, fo0, fo1);
     else
@@ -103,8 +104,9 @@ __global__ void prolong_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* __rest
         }
         cn[s] = ok ? q : 0; wgt[s] = ok ? w : 0.0; cm[s] = ok ? mc[q] : 0xff;
     }
-    for (int r = 0; r < R; ++r) {
-        if (active && !active[r]) continue;
+    {   // one RHS per thread (grid.y)
+        const int r = blockIdx.y;
+        if (active && !active[r]) return;
         const double* cv = coarse + (long long)r * gc.ndof;
         double acc[DIM];
 #pragma unroll
@@ -127,7 +129,7 @@ void prolong_add(const LevelGeom& gf, const LevelGeom& gc, const uint8_t* mf, co
                  const double* coarse, double* fine, int R, const int* active, const int* done, bool accumulate,
                  cudaStream_t s, int off0) {
     int th = 128;
-    unsigned bl = (unsigned)((gf.nnodes + th - 1) / th);
+    dim3 bl((unsigned)((gf.nnodes + th - 1) / th), R);
     if (gf.dim == 2)
         prolong_kernel<2><<<bl, th, 0, s>>>(gf, gc, mf, mc, coarse, fine, R, active, done, accumulate, off0);
     else
