@@ -347,6 +347,7 @@ void stencil_diag(const LevelGeom& g, const double* /*st*/, uint8_t* mask, doubl
 template <int DIM, int OP, int RB>
 __global__ void __launch_bounds__(128) coarse_kernel(CoarseArgs a, int r0) {
     constexpr int NS = DIM == 2 ? 9 : 27;
+    r0 += blockIdx.y * RB;   // small levels: RHS groups spread over grid.y
     long long node = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (node >= a.g.nnodes) return;
     if (a.done && *a.done) return;
@@ -415,6 +416,10 @@ template <int DIM, int OP>
 static void launch_coarse_dim(const CoarseArgs& a, cudaStream_t s) {
     int th = 128;
     unsigned bl = (unsigned)((a.g.nnodes + th - 1) / th);
+    if (bl < 2 * 148) {   // small level: one RHS per thread, RHS over grid.y (stencil from L2)
+        coarse_kernel<DIM, OP, 1><<<dim3(bl, a.R), th, 0, s>>>(a, 0);
+        return;
+    }
     for (int r0 = 0; r0 < a.R;) {
         int rem = a.R - r0;
         if (rem > 8) {
