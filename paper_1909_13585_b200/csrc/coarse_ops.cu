@@ -106,14 +106,15 @@ __global__ void galerkin_kernel(LevelGeom gc, LevelGeom gf, const double* __rest
     __shared__ double Kc[NL * NL];
     __shared__ double T[NL * NL];
     __shared__ double fr[NL];
-    const long long Ec = blockIdx.x;
     const int t = threadIdx.x;
     const int row = t / NL, col = t % NL;
+    // grid-stride over coarse elements: a few waves of CTAs instead of one CTA per element
+    for (long long Ec = blockIdx.x; Ec < gc.nelem; Ec += gridDim.x) {
     int ci[3] = {0, 0, 0};
     long long tt = Ec;
     for (int k = DIM - 1; k >= 0; --k) { ci[k] = (int)(tt % gc.N[k]); tt /= gc.N[k]; }
     // slab ghost element layer (children not local): filled by the halo exchange instead
-    if (ci[0] < off0) return;
+    if (ci[0] < off0) continue;
     double acc = 0.0;
     bool fast = false;
     constexpr bool FROM_E = SRC == 1;
@@ -200,12 +201,19 @@ __global__ void galerkin_kernel(LevelGeom gc, LevelGeom gf, const double* __rest
         return ((mask_c[node] >> comp) & 1) ? 0.0 : 1.0;
     };
     elm_c[Ec * NL * NL + t] = acc * cfree(row) * cfree(col);
+    __syncthreads();   // shared Kc / T / fr are rewritten for the next element
+    }
+}
+
+static unsigned galerkin_grid(const LevelGeom& gc) {
+    const long long cap = 148LL * 16;
+    return (unsigned)(gc.nelem < cap ? gc.nelem : cap);
 }
 
 void galerkin_elements(const LevelGeom& gc, const LevelGeom& gf, const double* E, const double* elm_f,
                        const uint8_t* mask_f, const uint8_t* mask_c, double* elm_c, cudaStream_t s, int off0,
                        const double* Mc) {
-    unsigned bl = (unsigned)gc.nelem;
+    unsigned bl = galerkin_grid(gc);
     if (gc.dim == 2) {
         if (E) galerkin_kernel<2, 1><<<bl, 64, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, Mc);
         else galerkin_kernel<2, 0><<<bl, 64, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, nullptr);
@@ -218,7 +226,7 @@ void galerkin_elements(const LevelGeom& gc, const LevelGeom& gf, const double* E
 // level-1 Galerkin element matrices of G from the fine per-element Voigt stresses (Es included)
 void galerkin_elements_G(const LevelGeom& gc, const LevelGeom& gf, const double* sig, const uint8_t* mask_f,
                          const uint8_t* mask_c, double* elm_c, cudaStream_t s) {
-    unsigned bl = (unsigned)gc.nelem;
+    unsigned bl = galerkin_grid(gc);
     if (gc.dim == 2) galerkin_kernel<2, 2><<<bl, 64, 0, s>>>(gc, gf, sig, nullptr, mask_f, mask_c, elm_c, 0, nullptr);
     else galerkin_kernel<3, 2><<<bl, 576, 0, s>>>(gc, gf, sig, nullptr, mask_f, mask_c, elm_c, 0, nullptr);
 }
