@@ -27,15 +27,74 @@
 #include "kernels.h"
 
 __constant__ double c_K2[64];
+__constant__ double c_Kh2[64];
+
+#ifndef MG_2D_TRANSFORM
+#define MG_2D_TRANSFORM 1   // element operator in the sum/difference basis (10 nonzeros, see below)
+#endif
+
+// K^ = T^-T K0 T^-1 in the per-axis (m = v0 + v1, d = v1 - v0) basis (see h8.cu): closed form from
+// the 1-D factors M^ = diag(1/4, 1/12), D^ = diag(0, 1), C^[d][m] = C^T[m][d] = 1/2; plane stress.
+__host__ __device__ constexpr double f1h2(int kind, int ta, int tb) {
+    return kind == 0 ? (ta == tb ? (ta == 0 ? 0.25 : 1.0 / 12.0) : 0.0)
+         : kind == 1 ? ((ta == 1 && tb == 1) ? 1.0 : 0.0)
+         : kind == 2 ? ((ta == 1 && tb == 0) ? 0.5 : 0.0)
+                     : ((ta == 0 && tb == 1) ? 0.5 : 0.0);
+}
+__host__ __device__ constexpr double sh2(int i, int j, int s, int t) {
+    double v = 1.0;
+    for (int k = 0; k < 2; ++k) {
+        const int ta = (s >> (1 - k)) & 1, tb = (t >> (1 - k)) & 1;
+        const int kind = (k == i && k == j) ? 1 : (k == i ? 2 : (k == j ? 3 : 0));
+        v *= f1h2(kind, ta, tb);
+    }
+    return v;
+}
+__host__ __device__ constexpr double khat2(double nu, int row, int col) {
+    const int s = row / 2, i = row % 2, t = col / 2, j = col % 2;
+    const double mu = 1.0 / (2.0 * (1.0 + nu));
+    const double lam = nu / (1.0 - nu * nu);
+    double v = lam * sh2(i, j, s, t) + mu * sh2(j, i, s, t);
+    if (i == j)
+        for (int k = 0; k < 2; ++k) v += mu * sh2(k, k, s, t);
+    return v;
+}
 
 void fine2d_set_constants(const double* K0, cudaStream_t s) {
     cudaMemcpyToSymbolAsync(c_K2, K0, sizeof(double) * 64, 0, cudaMemcpyHostToDevice, s);
+    // K^ from K0 (any element / nu): per axis T^-1 = (1/2) [[1, -1], [1, 1]]
+    static double Ti[8][8], Kh[64];
+    for (int a = 0; a < 4; ++a)
+        for (int t = 0; t < 4; ++t) {
+            double v = 1.0;
+            for (int k = 0; k < 2; ++k) {
+                const int ab = (a >> (1 - k)) & 1, tb = (t >> (1 - k)) & 1;
+                v *= 0.5 * ((tb == 0) ? 1.0 : (ab ? 1.0 : -1.0));
+            }
+            for (int i = 0; i < 2; ++i)
+                for (int j = 0; j < 2; ++j) Ti[2 * a + i][2 * t + j] = (i == j) ? v : 0.0;
+        }
+    for (int r = 0; r < 8; ++r)
+        for (int c = 0; c < 8; ++c) {
+            double v = 0.0;
+            for (int p = 0; p < 8; ++p)
+                for (int q = 0; q < 8; ++q) v += Ti[p][r] * K0[p * 8 + q] * Ti[q][c];
+            Kh[r * 8 + c] = v;
+        }
+    cudaMemcpyToSymbolAsync(c_Kh2, Kh, sizeof(Kh), 0, cudaMemcpyHostToDevice, s);
 }
 
 template <bool C03>
 __device__ __forceinline__ double K2(int r, int c) {
     if (C03) return k0_entry<2>(MG_NU_PAPER, r, c);
     return c_K2[r * 8 + c];
+}
+// transformed element matrix: the sparsity (10 nonzeros) is that of the standard element at
+// nu = 0.3, shared by every nu and by the incompatible-mode element
+template <bool C03>
+__device__ __forceinline__ double KH2(int r, int c) {
+    if (C03) return khat2(MG_NU_PAPER, r, c);
+    return c_Kh2[r * 8 + c];
 }
 
 // register prefetch depth (node planes in flight per warp) and CTAs per SM (register cap)
@@ -256,7 +315,9 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
         if (Ops<OP>::XV) { const double2 v2 = ld2(xvb + 2 * no); s.xx = v2.x; s.xy = v2.y; }
         if (Ops<OP>::DI) { const double2 d = ldg2(a.Dinv + 2 * no); s.dx = d.x; s.dy = d.y; }
         s.e = __ldg(a.E + eo);
+#if !MG_2D_TRANSFORM
         s.el = __ldg(a.E + eo - 1);
+#endif
         s.m = __ldg(a.mask + no);
         if (OP == M2_POST) {
             s.cx0 = s.cy0 = s.cx1 = s.cy1 = 0.0;
@@ -280,7 +341,12 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
     };
 
     // plane state
+#if MG_2D_TRANSFORM
+    double eAmx, eAdx, eAmy, eAdy;              // edge (c, c+1) of plane L in the (m, d) basis
+    double cymx = 0.0, cydx = 0.0, cymy = 0.0, cydy = 0.0;   // element layer L-1's plane-L edge part
+#else
     double A0x, A0y, A1x, A1y, A2x, A2y;      // masked input at c-1, c, c+1 of plane L
+#endif
     double urx, ury, auxx = 0, auxy = 0, aux2x = 0, aux2y = 0, dax = 1, day = 1;
     double ex, exl;                           // E of layer L at c, c-1
     int mA;
@@ -361,10 +427,16 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
         urx = ux; ury = uy;
         dax = s0.dx; day = s0.dy;
         const double mx = (mA & 1) ? 0.0 : ux, my = (mA & 2) ? 0.0 : uy;
+#if MG_2D_TRANSFORM
+        const double nx0 = shfl_dn1(mx), ny0 = shfl_dn1(my);
+        eAmx = mx + nx0; eAdx = nx0 - mx; eAmy = my + ny0; eAdy = ny0 - my;
+        ex = s0.e;
+#else
         A1x = mx; A1y = my;
         A0x = shfl_up1(mx); A0y = shfl_up1(my);
         A2x = shfl_dn1(mx); A2y = shfl_dn1(my);
         ex = s0.e; exl = s0.el;
+#endif
     }
 
     for (int L0 = i0 - 1; L0 < i1; L0 += PD) {
@@ -378,9 +450,45 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
             double ux, uy, kx, ky, k2x, k2y;
             derive(s, P, ux, uy, kx, ky, k2x, k2y);
             const double mx = (s.m & 1) ? 0.0 : ux, my = (s.m & 2) ? 0.0 : uy;
+#if !MG_2D_TRANSFORM
             const double B1x = mx, B1y = my;
             const double B0x = shfl_up1(mx), B0y = shfl_up1(my);
             const double B2x = shfl_dn1(mx), B2y = shfl_dn1(my);
+#endif
+#if MG_2D_TRANSFORM
+            // element (L, c) in the sum/difference basis: edge (c, c+1) of plane L+1 by a shuffle,
+            // the axis-0 combination with the carried edge of plane L, K^ (10 nonzeros), and back:
+            // the edge of plane L is completed with the carry, its node-c+1 half shuffled up.
+            double lox, loy;
+            {
+                const double nxB = shfl_dn1(mx), nyB = shfl_dn1(my);
+                const double eBmx = mx + nxB, eBdx = nxB - mx, eBmy = my + nyB, eBdy = nyB - my;
+                // uh[2 s + k], s = 2 t0 + t1 (t0: axis 0, t1: axis 1), scaled by E(L, c)
+                double uh[8];
+                uh[0] = 0.0; uh[1] = 0.0;                             // translations (zero rows/cols)
+                uh[2] = ex * (eAdx + eBdx); uh[3] = ex * (eAdy + eBdy);   // s = 1: (m, d)
+                uh[4] = ex * (eBmx - eAmx); uh[5] = ex * (eBmy - eAmy);   // s = 2: (d, m)
+                uh[6] = ex * (eBdx - eAdx); uh[7] = ex * (eBdy - eAdy);   // s = 3: (d, d)
+                double yh[8];
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int q = 2; q < 8; ++q)
+                        if (khat2(MG_NU_PAPER, r, q) != 0.0) acc = fma(KH2<C03>(r, q), uh[q], acc);
+                    yh[r] = acc;
+                }
+                // lower edge (plane L) = s(0,t1) - s(1,t1) ; upper (plane L+1) = sum
+                const double gmx = cymx + (yh[0] - yh[4]), gmy = cymy + (yh[1] - yh[5]);
+                const double gdx = cydx + (yh[2] - yh[6]), gdy = cydy + (yh[3] - yh[7]);
+                cymx = yh[0] + yh[4]; cymy = yh[1] + yh[5];
+                cydx = yh[2] + yh[6]; cydy = yh[3] + yh[7];
+                const double upx = shfl_up1(gmx + gdx), upy = shfl_up1(gmy + gdy);
+                lox = (gmx - gdx) + upx;
+                loy = (gmy - gdy) + upy;
+                eAmx = eBmx; eAdx = eBdx; eAmy = eBmy; eAdy = eBdy;
+            }
+#else
             // element layer L: e=0 -> element column c-1, e=1 -> column c
             double lox = carx, loy = cary, hix = 0.0, hiy = 0.0;
 #pragma unroll
@@ -407,6 +515,7 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
                 lox = fma(Ee, tlx, lox); loy = fma(Ee, tly, loy);
                 hix = fma(Ee, thx, hix); hiy = fma(Ee, thy, hiy);
             }
+#endif
             // ---- finish node plane L
             if (L >= i0) {
                 const double Axx = (mA & 1) ? urx : lox, Axy = (mA & 2) ? ury : loy;
@@ -466,12 +575,18 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
                 }
             }
             // ---- shift plane L+1 -> L
+#if !MG_2D_TRANSFORM
             carx = hix; cary = hiy;
             A0x = B0x; A0y = B0y; A1x = B1x; A1y = B1y; A2x = B2x; A2y = B2y;
+#endif
             urx = ux; ury = uy; mA = s.m;
             auxx = kx; auxy = ky; aux2x = k2x; aux2y = k2y;
             dax = s.dx; day = s.dy;
+#if MG_2D_TRANSFORM
+            ex = s.e;
+#else
             ex = s.e; exl = s.el;
+#endif
         }
     }
     if (a.partial) {
