@@ -254,6 +254,41 @@ struct Ops {
     static constexpr bool DI = OP == M2_RESTRICT || OP == M2_POST || OP == M2_JACOBI;
 };
 
+#ifndef MG_ASYNC_RING
+#define MG_ASYNC_RING 1   // POST / RESTRICT: cp.async shared-memory prefetch ring (see below)
+#endif
+static constexpr int NSTAGE = 4;   // planes in flight per warp in the async ring
+
+// cp.async (LDGSTS): per-lane asynchronous global -> shared copies; a false predicate zero-fills
+__device__ __forceinline__ void cpa16(void* dst, const void* src, bool pred) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(pred ? 16 : 0));
+}
+__device__ __forceinline__ void cpa8(void* dst, const void* src, bool pred) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(pred ? 8 : 0));
+}
+__device__ __forceinline__ void cpa4(void* dst, const void* src, bool pred) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src), "r"(pred ? 4 : 0));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Per-warp ring of NSTAGE planes (struct of arrays over the 32 lanes); unused fields have size 1.
+template <int OP>
+struct ARing {
+    static constexpr bool POST = OP == M2_POST, RESTR = OP == M2_RESTRICT;
+    double2 v0[NSTAGE][32];
+    double2 v1[RESTR ? NSTAGE : 1][32];
+    double2 d[NSTAGE][32];
+    double e[NSTAGE][32];
+    unsigned m[NSTAGE][32];                 // aligned 4-byte word holding the mask byte
+    double2 c0[POST ? NSTAGE : 1][32], c1[POST ? NSTAGE : 1][32];
+    unsigned cm0[NSTAGE][32], cm1[POST ? NSTAGE : 1][32];
+};
+
 // SLAB = false: single slab (off0 = 0, every plane owned) -- the slab checks compile away
 template <int OP, bool C03, bool SLAB>
 __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2Args a, int nct, int nch, int chl) {
@@ -340,6 +375,68 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
         }
     };
 
+    // async ring (POST / RESTRICT): issue(P) copies plane P's lane data into stage st; fetch(s, P)
+    // rebuilds the same Slot as load() from shared memory (after cpa_wait)
+    constexpr bool ASYNC = MG_ASYNC_RING && (OP == M2_POST || OP == M2_RESTRICT);
+    __shared__ ARing<OP> ring_sm[ASYNC ? WPB : 1];
+    ARing<OP>& AR = ring_sm[ASYNC ? (threadIdx.x >> 5) : 0];
+    auto issue = [&](int P, int st) {
+        const long long no = pd.org + (long long)P * pd.pitch + c;
+        const long long eo = pd.orgE + (long long)P * pd.pitchE + c;
+        cpa16(&AR.v0[st][lane], x0b + 2 * no, true);
+        if (OP == M2_RESTRICT) cpa16(&AR.v1[st][lane], x1b + 2 * no, true);
+        cpa16(&AR.d[st][lane], a.Dinv + 2 * no, true);
+        cpa8(&AR.e[st][lane], a.E + eo, true);
+        cpa4(&AR.m[st][lane], reinterpret_cast<const uint8_t*>((uintptr_t)(a.mask + no) & ~(uintptr_t)3), true);
+        const int Ps = P + off0;
+        if (OP == M2_POST) {
+            const int I = (Ps + 1) >> 1;
+            const bool pr = (Ps & 1) && cin && I < a.gc.nn[0];
+            const long long row = (long long)(pr ? I : 0) * nc1;
+            const long long j0 = pr ? J0 : 0, j1 = pr ? J1 : 0;
+            cpa16(&AR.c0[st][lane], a.ec + vbc + 2 * (row + j0), pr);
+            cpa16(&AR.c1[st][lane], a.ec + vbc + 2 * (row + j1), pr);
+            cpa4(&AR.cm0[st][lane], reinterpret_cast<const uint8_t*>((uintptr_t)(a.maskc + row + j0) & ~(uintptr_t)3), pr);
+            cpa4(&AR.cm1[st][lane], reinterpret_cast<const uint8_t*>((uintptr_t)(a.maskc + row + j1) & ~(uintptr_t)3), pr);
+        }
+        if (OP == M2_RESTRICT) {
+            const int I = (Ps - 1) >> 1;
+            const bool pr = Ps >= 1 && cin && !(c & 1) && I < a.gc.nn[0];
+            const long long ci = pr ? (long long)I * nc1 + J0 : 0;
+            cpa4(&AR.cm0[st][lane], reinterpret_cast<const uint8_t*>((uintptr_t)(a.maskc + ci) & ~(uintptr_t)3), pr);
+        }
+    };
+    auto byte_of = [](unsigned word, const void* addr) { return (int)((word >> (8 * ((uintptr_t)addr & 3))) & 0xff); };
+    auto fetch = [&](Slot& s, int P, int st) {
+        const long long no = pd.org + (long long)P * pd.pitch + c;
+        const double2 v0 = AR.v0[st][lane];
+        s.v0x = v0.x; s.v0y = v0.y;
+        if (OP == M2_RESTRICT) { const double2 v1 = AR.v1[st][lane]; s.v1x = v1.x; s.v1y = v1.y; }
+        const double2 d = AR.d[st][lane];
+        s.dx = d.x; s.dy = d.y;
+        s.e = AR.e[st][lane];
+        s.m = byte_of(AR.m[st][lane], a.mask + no);
+        const int Ps = P + off0;
+        if (OP == M2_POST) {
+            const int I = (Ps + 1) >> 1;
+            const bool pr = (Ps & 1) && cin && I < a.gc.nn[0];
+            s.cx0 = s.cy0 = s.cx1 = s.cy1 = 0.0;
+            if (pr) {
+                const long long row = (long long)I * nc1;
+                const int m0 = byte_of(AR.cm0[st][lane], a.maskc + row + J0);
+                const int m1 = byte_of(AR.cm1[st][lane], a.maskc + row + J1);
+                const double2 e0 = AR.c0[st][lane], e1 = AR.c1[st][lane];
+                s.cx0 = (m0 & 1) ? 0.0 : e0.x; s.cy0 = (m0 & 2) ? 0.0 : e0.y;
+                s.cx1 = (m1 & 1) ? 0.0 : e1.x; s.cy1 = (m1 & 2) ? 0.0 : e1.y;
+            }
+        }
+        if (OP == M2_RESTRICT) {
+            const int I = (Ps - 1) >> 1;
+            const bool pr = Ps >= 1 && cin && !(c & 1) && I < a.gc.nn[0];
+            s.cm = pr ? byte_of(AR.cm0[st][lane], a.maskc + (long long)I * nc1 + J0) : 3;
+        }
+    };
+
     // plane state
 #if MG_2D_TRANSFORM
     double eAmx, eAdx, eAmy, eAdy;              // edge (c, c+1) of plane L in the (m, d) basis
@@ -413,14 +510,8 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
         }
     };
 
-    // ---- prologue: plane i0-1 and the prefetch ring
-    constexpr int PD = prefetch_depth(OP);
-    Slot ring[PD];
-    {
-        Slot s0;
-        load(s0, i0 - 1);
-#pragma unroll
-        for (int u = 0; u < PD; ++u) load(ring[u], min(i0 + u, i1));
+    // ---- one march step: element layer L, finishing node plane L, with plane P = L + 1's slot
+    auto prologue = [&](const Slot& s0) {
         double ux, uy;
         derive(s0, i0 - 1, ux, uy, auxx, auxy, aux2x, aux2y);
         mA = s0.m;
@@ -437,157 +528,194 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
         A2x = shfl_dn1(mx); A2y = shfl_dn1(my);
         ex = s0.e; exl = s0.el;
 #endif
-    }
-
-    for (int L0 = i0 - 1; L0 < i1; L0 += PD) {
-#pragma unroll
-        for (int u = 0; u < PD; ++u) {
-            const int L = L0 + u;
-            if (L >= i1) break;
-            const Slot s = ring[u];
-            if (L + 1 + PD <= i1) load(ring[u], L + 1 + PD);
+    };
+    auto step = [&](const Slot& s, int L) {
             const int P = L + 1;
-            double ux, uy, kx, ky, k2x, k2y;
-            derive(s, P, ux, uy, kx, ky, k2x, k2y);
-            const double mx = (s.m & 1) ? 0.0 : ux, my = (s.m & 2) ? 0.0 : uy;
+        double ux, uy, kx, ky, k2x, k2y;
+        derive(s, P, ux, uy, kx, ky, k2x, k2y);
+        const double mx = (s.m & 1) ? 0.0 : ux, my = (s.m & 2) ? 0.0 : uy;
 #if !MG_2D_TRANSFORM
-            const double B1x = mx, B1y = my;
-            const double B0x = shfl_up1(mx), B0y = shfl_up1(my);
-            const double B2x = shfl_dn1(mx), B2y = shfl_dn1(my);
+        const double B1x = mx, B1y = my;
+        const double B0x = shfl_up1(mx), B0y = shfl_up1(my);
+        const double B2x = shfl_dn1(mx), B2y = shfl_dn1(my);
 #endif
 #if MG_2D_TRANSFORM
-            // element (L, c) in the sum/difference basis: edge (c, c+1) of plane L+1 by a shuffle,
-            // the axis-0 combination with the carried edge of plane L, K^ (10 nonzeros), and back:
-            // the edge of plane L is completed with the carry, its node-c+1 half shuffled up.
-            double lox, loy;
-            {
-                const double nxB = shfl_dn1(mx), nyB = shfl_dn1(my);
-                const double eBmx = mx + nxB, eBdx = nxB - mx, eBmy = my + nyB, eBdy = nyB - my;
-                // uh[2 s + k], s = 2 t0 + t1 (t0: axis 0, t1: axis 1), scaled by E(L, c)
-                double uh[8];
-                uh[0] = 0.0; uh[1] = 0.0;                             // translations (zero rows/cols)
-                uh[2] = ex * (eAdx + eBdx); uh[3] = ex * (eAdy + eBdy);   // s = 1: (m, d)
-                uh[4] = ex * (eBmx - eAmx); uh[5] = ex * (eBmy - eAmy);   // s = 2: (d, m)
-                uh[6] = ex * (eBdx - eAdx); uh[7] = ex * (eBdy - eAdy);   // s = 3: (d, d)
-                double yh[8];
+        // element (L, c) in the sum/difference basis: edge (c, c+1) of plane L+1 by a shuffle,
+        // the axis-0 combination with the carried edge of plane L, K^ (10 nonzeros), and back:
+        // the edge of plane L is completed with the carry, its node-c+1 half shuffled up.
+        double lox, loy;
+        {
+            const double nxB = shfl_dn1(mx), nyB = shfl_dn1(my);
+            const double eBmx = mx + nxB, eBdx = nxB - mx, eBmy = my + nyB, eBdy = nyB - my;
+            // uh[2 s + k], s = 2 t0 + t1 (t0: axis 0, t1: axis 1), scaled by E(L, c)
+            double uh[8];
+            uh[0] = 0.0; uh[1] = 0.0;                             // translations (zero rows/cols)
+            uh[2] = ex * (eAdx + eBdx); uh[3] = ex * (eAdy + eBdy);   // s = 1: (m, d)
+            uh[4] = ex * (eBmx - eAmx); uh[5] = ex * (eBmy - eAmy);   // s = 2: (d, m)
+            uh[6] = ex * (eBdx - eAdx); uh[7] = ex * (eBdy - eAdy);   // s = 3: (d, d)
+            double yh[8];
 #pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    double acc = 0.0;
+            for (int r = 0; r < 8; ++r) {
+                double acc = 0.0;
 #pragma unroll
-                    for (int q = 2; q < 8; ++q)
-                        if (khat2(MG_NU_PAPER, r, q) != 0.0) acc = fma(KH2<C03>(r, q), uh[q], acc);
-                    yh[r] = acc;
-                }
-                // lower edge (plane L) = s(0,t1) - s(1,t1) ; upper (plane L+1) = sum
-                const double gmx = cymx + (yh[0] - yh[4]), gmy = cymy + (yh[1] - yh[5]);
-                const double gdx = cydx + (yh[2] - yh[6]), gdy = cydy + (yh[3] - yh[7]);
-                cymx = yh[0] + yh[4]; cymy = yh[1] + yh[5];
-                cydx = yh[2] + yh[6]; cydy = yh[3] + yh[7];
-                const double upx = shfl_up1(gmx + gdx), upy = shfl_up1(gmy + gdy);
-                lox = (gmx - gdx) + upx;
-                loy = (gmy - gdy) + upy;
-                eAmx = eBmx; eAdx = eBdx; eAmy = eBmy; eAdy = eBdy;
+                for (int q = 2; q < 8; ++q)
+                    if (khat2(MG_NU_PAPER, r, q) != 0.0) acc = fma(KH2<C03>(r, q), uh[q], acc);
+                yh[r] = acc;
             }
-#else
-            // element layer L: e=0 -> element column c-1, e=1 -> column c
-            double lox = carx, loy = cary, hix = 0.0, hiy = 0.0;
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const double Ee = e ? ex : exl;
-                const int a1 = 1 - e;
-                double tlx = 0, tly = 0, thx = 0, thy = 0;
-#pragma unroll
-                for (int b0 = 0; b0 < 2; ++b0)
-#pragma unroll
-                    for (int b1 = 0; b1 < 2; ++b1)
-#pragma unroll
-                        for (int k2 = 0; k2 < 2; ++k2) {
-                            const int q = e + b1;
-                            const double xv = b0 ? (q == 0 ? (k2 ? B0y : B0x) : q == 1 ? (k2 ? B1y : B1x) : (k2 ? B2y : B2x))
-                                                 : (q == 0 ? (k2 ? A0y : A0x) : q == 1 ? (k2 ? A1y : A1x) : (k2 ? A2y : A2x));
-                            const int col = (b0 * 2 + b1) * 2 + k2;
-                            const int rl = (0 * 2 + a1) * 2, rh = (1 * 2 + a1) * 2;
-                            if (!C03 || K2<C03>(rl + 0, col) != 0.0) tlx = fma(K2<C03>(rl + 0, col), xv, tlx);
-                            if (!C03 || K2<C03>(rl + 1, col) != 0.0) tly = fma(K2<C03>(rl + 1, col), xv, tly);
-                            if (!C03 || K2<C03>(rh + 0, col) != 0.0) thx = fma(K2<C03>(rh + 0, col), xv, thx);
-                            if (!C03 || K2<C03>(rh + 1, col) != 0.0) thy = fma(K2<C03>(rh + 1, col), xv, thy);
-                        }
-                lox = fma(Ee, tlx, lox); loy = fma(Ee, tly, loy);
-                hix = fma(Ee, thx, hix); hiy = fma(Ee, thy, hiy);
-            }
-#endif
-            // ---- finish node plane L
-            if (L >= i0) {
-                const double Axx = (mA & 1) ? urx : lox, Axy = (mA & 2) ? ury : loy;
-                const bool own = own_col && L >= own0 && L < own1;
-                const bool sdot = own && (!SLAB || (L >= a.so0 && L < a.so1));   // slab-owned: counts in dots
-                const long long o = 2 * (pd.org + (long long)L * pd.pitch + c);
-                if (OP == M2_MATVEC) {
-                    if (own) st2(yb + o, Axx, Axy);
-                } else if (OP == M2_RESID) {
-                    if (own) st2(yb + o, auxx - Axx, auxy - Axy);
-                } else if (OP == M2_JACOBI || OP == M2_POST) {
-                    const double zx = fma(omega * dax, auxx - Axx, urx);
-                    const double zy = fma(omega * day, auxy - Axy, ury);
-                    if (own) {
-                        st2(yb + o, zx, zy);
-                        if (sdot) {
-                            dot = fma(auxx, zx, dot);
-                            dot = fma(auxy, zy, dot);
-                        }
-                    }
-                } else if (OP == M2_CGP) {
-                    if (own) {
-                        st2(yb + o, Axx, Axy);
-                        if (sdot) {
-                            dot = fma(urx, Axx, dot);
-                            dot = fma(ury, Axy, dot);
-                        }
-                        st2(xvb + o, fma(xalpha, auxx, aux2x), fma(xalpha, auxy, aux2y));
-                    }
-                } else if (OP == M2_RESTRICT) {
-                    // t = r - K z1 (lanes 1..30 valid), then P^T: columns by shuffles, planes by carry
-                    // t counts only on slab-owned planes: the coarse ghost row above gets a
-                    // partial sum that the upper neighbour adds in (reverse halo exchange)
-                    const bool tv = cin && lane >= 1 && lane <= 30 && (!SLAB || (L >= a.so0 && L < a.so1));
-                    const double tx = (tv && !(mA & 1)) ? auxx - Axx : 0.0;
-                    const double ty = (tv && !(mA & 2)) ? auxy - Axy : 0.0;
-                    const double tlx = shfl_up1(tx), tly = shfl_up1(ty);
-                    const double trx = shfl_dn1(tx), try_ = shfl_dn1(ty);
-                    const double hx = fma(0.5, tlx + trx, tx), hy = fma(0.5, tly + try_, ty);
-                    const bool cown = cin && !(c & 1) && lane >= 2 && lane <= 28;
-                    const int cm = (int)k2x;     // coarse mask of row (P-1)>>1 = the row output below
-                    const int Ls = L + off0;
-                    if (Ls & 1) {
-                        accx = fma(0.5, hx, accx); accy = fma(0.5, hy, accy);
-                        const int I = (Ls - 1) >> 1;
-                        if (cown && I >= I0 && I < I1)
-                            st2(a.coarse + vbc + 2 * ((long long)I * nc1 + J0), (cm & 1) ? 0.0 : accx,
-                                (cm & 2) ? 0.0 : accy);
-                        accx = 0.5 * hx; accy = 0.5 * hy;
-                    } else {
-                        accx += hx; accy += hy;
-                        const int I = Ls >> 1;
-                        if (L == n0 - 1 && cown && I >= I0 && I < I1)
-                            st2(a.coarse + vbc + 2 * ((long long)I * nc1 + J0), (cm & 1) ? 0.0 : accx,
-                                (cm & 2) ? 0.0 : accy);
-                    }
-                }
-            }
-            // ---- shift plane L+1 -> L
-#if !MG_2D_TRANSFORM
-            carx = hix; cary = hiy;
-            A0x = B0x; A0y = B0y; A1x = B1x; A1y = B1y; A2x = B2x; A2y = B2y;
-#endif
-            urx = ux; ury = uy; mA = s.m;
-            auxx = kx; auxy = ky; aux2x = k2x; aux2y = k2y;
-            dax = s.dx; day = s.dy;
-#if MG_2D_TRANSFORM
-            ex = s.e;
-#else
-            ex = s.e; exl = s.el;
-#endif
+            // lower edge (plane L) = s(0,t1) - s(1,t1) ; upper (plane L+1) = sum
+            const double gmx = cymx + (yh[0] - yh[4]), gmy = cymy + (yh[1] - yh[5]);
+            const double gdx = cydx + (yh[2] - yh[6]), gdy = cydy + (yh[3] - yh[7]);
+            cymx = yh[0] + yh[4]; cymy = yh[1] + yh[5];
+            cydx = yh[2] + yh[6]; cydy = yh[3] + yh[7];
+            const double upx = shfl_up1(gmx + gdx), upy = shfl_up1(gmy + gdy);
+            lox = (gmx - gdx) + upx;
+            loy = (gmy - gdy) + upy;
+            eAmx = eBmx; eAdx = eBdx; eAmy = eBmy; eAdy = eBdy;
         }
+#else
+        // element layer L: e=0 -> element column c-1, e=1 -> column c
+        double lox = carx, loy = cary, hix = 0.0, hiy = 0.0;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const double Ee = e ? ex : exl;
+            const int a1 = 1 - e;
+            double tlx = 0, tly = 0, thx = 0, thy = 0;
+#pragma unroll
+            for (int b0 = 0; b0 < 2; ++b0)
+#pragma unroll
+                for (int b1 = 0; b1 < 2; ++b1)
+#pragma unroll
+                    for (int k2 = 0; k2 < 2; ++k2) {
+                        const int q = e + b1;
+                        const double xv = b0 ? (q == 0 ? (k2 ? B0y : B0x) : q == 1 ? (k2 ? B1y : B1x) : (k2 ? B2y : B2x))
+                                             : (q == 0 ? (k2 ? A0y : A0x) : q == 1 ? (k2 ? A1y : A1x) : (k2 ? A2y : A2x));
+                        const int col = (b0 * 2 + b1) * 2 + k2;
+                        const int rl = (0 * 2 + a1) * 2, rh = (1 * 2 + a1) * 2;
+                        if (!C03 || K2<C03>(rl + 0, col) != 0.0) tlx = fma(K2<C03>(rl + 0, col), xv, tlx);
+                        if (!C03 || K2<C03>(rl + 1, col) != 0.0) tly = fma(K2<C03>(rl + 1, col), xv, tly);
+                        if (!C03 || K2<C03>(rh + 0, col) != 0.0) thx = fma(K2<C03>(rh + 0, col), xv, thx);
+                        if (!C03 || K2<C03>(rh + 1, col) != 0.0) thy = fma(K2<C03>(rh + 1, col), xv, thy);
+                    }
+            lox = fma(Ee, tlx, lox); loy = fma(Ee, tly, loy);
+            hix = fma(Ee, thx, hix); hiy = fma(Ee, thy, hiy);
+        }
+#endif
+        // ---- finish node plane L
+        if (L >= i0) {
+            const double Axx = (mA & 1) ? urx : lox, Axy = (mA & 2) ? ury : loy;
+            const bool own = own_col && L >= own0 && L < own1;
+            const bool sdot = own && (!SLAB || (L >= a.so0 && L < a.so1));   // slab-owned: counts in dots
+            const long long o = 2 * (pd.org + (long long)L * pd.pitch + c);
+            if (OP == M2_MATVEC) {
+                if (own) st2(yb + o, Axx, Axy);
+            } else if (OP == M2_RESID) {
+                if (own) st2(yb + o, auxx - Axx, auxy - Axy);
+            } else if (OP == M2_JACOBI || OP == M2_POST) {
+                const double zx = fma(omega * dax, auxx - Axx, urx);
+                const double zy = fma(omega * day, auxy - Axy, ury);
+                if (own) {
+                    st2(yb + o, zx, zy);
+                    if (sdot) {
+                        dot = fma(auxx, zx, dot);
+                        dot = fma(auxy, zy, dot);
+                    }
+                }
+            } else if (OP == M2_CGP) {
+                if (own) {
+                    st2(yb + o, Axx, Axy);
+                    if (sdot) {
+                        dot = fma(urx, Axx, dot);
+                        dot = fma(ury, Axy, dot);
+                    }
+                    st2(xvb + o, fma(xalpha, auxx, aux2x), fma(xalpha, auxy, aux2y));
+                }
+            } else if (OP == M2_RESTRICT) {
+                // t = r - K z1 (lanes 1..30 valid), then P^T: columns by shuffles, planes by carry
+                // t counts only on slab-owned planes: the coarse ghost row above gets a
+                // partial sum that the upper neighbour adds in (reverse halo exchange)
+                const bool tv = cin && lane >= 1 && lane <= 30 && (!SLAB || (L >= a.so0 && L < a.so1));
+                const double tx = (tv && !(mA & 1)) ? auxx - Axx : 0.0;
+                const double ty = (tv && !(mA & 2)) ? auxy - Axy : 0.0;
+                const double tlx = shfl_up1(tx), tly = shfl_up1(ty);
+                const double trx = shfl_dn1(tx), try_ = shfl_dn1(ty);
+                const double hx = fma(0.5, tlx + trx, tx), hy = fma(0.5, tly + try_, ty);
+                const bool cown = cin && !(c & 1) && lane >= 2 && lane <= 28;
+                const int cm = (int)k2x;     // coarse mask of row (P-1)>>1 = the row output below
+                const int Ls = L + off0;
+                if (Ls & 1) {
+                    accx = fma(0.5, hx, accx); accy = fma(0.5, hy, accy);
+                    const int I = (Ls - 1) >> 1;
+                    if (cown && I >= I0 && I < I1)
+                        st2(a.coarse + vbc + 2 * ((long long)I * nc1 + J0), (cm & 1) ? 0.0 : accx,
+                            (cm & 2) ? 0.0 : accy);
+                    accx = 0.5 * hx; accy = 0.5 * hy;
+                } else {
+                    accx += hx; accy += hy;
+                    const int I = Ls >> 1;
+                    if (L == n0 - 1 && cown && I >= I0 && I < I1)
+                        st2(a.coarse + vbc + 2 * ((long long)I * nc1 + J0), (cm & 1) ? 0.0 : accx,
+                            (cm & 2) ? 0.0 : accy);
+                }
+            }
+        }
+        // ---- shift plane L+1 -> L
+#if !MG_2D_TRANSFORM
+        carx = hix; cary = hiy;
+        A0x = B0x; A0y = B0y; A1x = B1x; A1y = B1y; A2x = B2x; A2y = B2y;
+#endif
+        urx = ux; ury = uy; mA = s.m;
+        auxx = kx; auxy = ky; aux2x = k2x; aux2y = k2y;
+        dax = s.dx; day = s.dy;
+#if MG_2D_TRANSFORM
+        ex = s.e;
+#else
+        ex = s.e; exl = s.el;
+#endif
+    };
+
+    if constexpr (!ASYNC) {
+        // register prefetch ring of PD planes
+        constexpr int PD = prefetch_depth(OP);
+        Slot ring[PD];
+        Slot s0;
+        load(s0, i0 - 1);
+#pragma unroll
+        for (int u = 0; u < PD; ++u) load(ring[u], min(i0 + u, i1));
+        prologue(s0);
+        for (int L0 = i0 - 1; L0 < i1; L0 += PD) {
+#pragma unroll
+            for (int u = 0; u < PD; ++u) {
+                const int L = L0 + u;
+                if (L >= i1) break;
+                const Slot s = ring[u];
+                if (L + 1 + PD <= i1) load(ring[u], L + 1 + PD);
+                step(s, L);
+            }
+        }
+    } else {
+        // cp.async ring: NSTAGE planes in flight, one commit group per plane (empty groups keep
+        // the count uniform), plane p in stage (p - i0 + 1) % NSTAGE
+        auto stage = [&](int p) { return (p - i0 + 1) % NSTAGE; };
+#pragma unroll
+        for (int k = 0; k < NSTAGE; ++k) {
+            issue(min(i0 - 1 + k, i1), k);
+            cpa_commit();
+        }
+        cpa_wait<NSTAGE - 1>();
+        Slot s0;
+        fetch(s0, i0 - 1, 0);
+        prologue(s0);
+        for (int L = i0 - 1; L < i1; ++L) {
+            const int P = L + 1;
+            const int pn = P + NSTAGE - 1;
+            if (pn <= i1) issue(pn, stage(pn));
+            cpa_commit();
+            cpa_wait<NSTAGE - 1>();
+            Slot s;
+            fetch(s, P, stage(P));
+            step(s, L);
+        }
+        cpa_wait<0>();
     }
     if (a.partial) {
         dot = warp_sum(dot);
