@@ -257,7 +257,13 @@ struct Ops {
 #ifndef MG_ASYNC_RING
 #define MG_ASYNC_RING 1   // POST / RESTRICT: cp.async shared-memory prefetch ring (see below)
 #endif
-static constexpr int NSTAGE = 4;   // planes in flight per warp in the async ring
+#ifndef MG_ASYNC_CGP
+#define MG_ASYNC_CGP 1    // CGP through the same ring
+#endif
+#ifndef MG_NSTAGE
+#define MG_NSTAGE 4
+#endif
+static constexpr int NSTAGE = MG_NSTAGE;   // planes in flight per warp in the async ring
 
 // cp.async (LDGSTS): per-lane asynchronous global -> shared copies; a false predicate zero-fills
 __device__ __forceinline__ void cpa16(void* dst, const void* src, bool pred) {
@@ -279,14 +285,15 @@ __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %
 // Per-warp ring of NSTAGE planes (struct of arrays over the 32 lanes); unused fields have size 1.
 template <int OP>
 struct ARing {
-    static constexpr bool POST = OP == M2_POST, RESTR = OP == M2_RESTRICT;
+    static constexpr bool POST = OP == M2_POST, RESTR = OP == M2_RESTRICT, CGP = OP == M2_CGP;
     double2 v0[NSTAGE][32];
-    double2 v1[RESTR ? NSTAGE : 1][32];
-    double2 d[NSTAGE][32];
+    double2 v1[(RESTR || CGP) ? NSTAGE : 1][32];
+    double2 xv[CGP ? NSTAGE : 1][32];
+    double2 d[CGP ? 1 : NSTAGE][32];
     double e[NSTAGE][32];
     unsigned m[NSTAGE][32];                 // aligned 4-byte word holding the mask byte
     double2 c0[POST ? NSTAGE : 1][32], c1[POST ? NSTAGE : 1][32];
-    unsigned cm0[NSTAGE][32], cm1[POST ? NSTAGE : 1][32];
+    unsigned cm0[CGP ? 1 : NSTAGE][32], cm1[POST ? NSTAGE : 1][32];
 };
 
 // SLAB = false: single slab (off0 = 0, every plane owned) -- the slab checks compile away
@@ -377,15 +384,16 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
 
     // async ring (POST / RESTRICT): issue(P) copies plane P's lane data into stage st; fetch(s, P)
     // rebuilds the same Slot as load() from shared memory (after cpa_wait)
-    constexpr bool ASYNC = MG_ASYNC_RING && (OP == M2_POST || OP == M2_RESTRICT);
+    constexpr bool ASYNC = MG_ASYNC_RING && (OP == M2_POST || OP == M2_RESTRICT || (MG_ASYNC_CGP && OP == M2_CGP));
     __shared__ ARing<OP> ring_sm[ASYNC ? WPB : 1];
     ARing<OP>& AR = ring_sm[ASYNC ? (threadIdx.x >> 5) : 0];
     auto issue = [&](int P, int st) {
         const long long no = pd.org + (long long)P * pd.pitch + c;
         const long long eo = pd.orgE + (long long)P * pd.pitchE + c;
         cpa16(&AR.v0[st][lane], x0b + 2 * no, true);
-        if (OP == M2_RESTRICT) cpa16(&AR.v1[st][lane], x1b + 2 * no, true);
-        cpa16(&AR.d[st][lane], a.Dinv + 2 * no, true);
+        if (OP == M2_RESTRICT || OP == M2_CGP) cpa16(&AR.v1[st][lane], x1b + 2 * no, true);
+        if (OP == M2_CGP) cpa16(&AR.xv[st][lane], xvb + 2 * no, true);
+        if (OP != M2_CGP) cpa16(&AR.d[st][lane], a.Dinv + 2 * no, true);
         cpa8(&AR.e[st][lane], a.E + eo, true);
         cpa4(&AR.m[st][lane], reinterpret_cast<const uint8_t*>((uintptr_t)(a.mask + no) & ~(uintptr_t)3), true);
         const int Ps = P + off0;
@@ -411,9 +419,9 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
         const long long no = pd.org + (long long)P * pd.pitch + c;
         const double2 v0 = AR.v0[st][lane];
         s.v0x = v0.x; s.v0y = v0.y;
-        if (OP == M2_RESTRICT) { const double2 v1 = AR.v1[st][lane]; s.v1x = v1.x; s.v1y = v1.y; }
-        const double2 d = AR.d[st][lane];
-        s.dx = d.x; s.dy = d.y;
+        if (OP == M2_RESTRICT || OP == M2_CGP) { const double2 v1 = AR.v1[st][lane]; s.v1x = v1.x; s.v1y = v1.y; }
+        if (OP == M2_CGP) { const double2 x2 = AR.xv[st][lane]; s.xx = x2.x; s.xy = x2.y; }
+        if (OP != M2_CGP) { const double2 d = AR.d[st][lane]; s.dx = d.x; s.dy = d.y; }
         s.e = AR.e[st][lane];
         s.m = byte_of(AR.m[st][lane], a.mask + no);
         const int Ps = P + off0;
