@@ -19,6 +19,15 @@
 #include "kernels.h"
 
 static constexpr int CT_I = 16, CT_J = 32;   // thread tile (level-l nodes)
+static constexpr int NSR = 3;                // right-hand sides in flight (cp.async ring)
+
+__device__ __forceinline__ void cpa16c(void* dst, const void* src, bool pred) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(pred ? 16 : 0));
+}
+__device__ __forceinline__ void cpa_commit_c() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cpa_wait_c() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NSR - 1)); }
+__device__ __forceinline__ void cpa_wait_all_c() { asm volatile("cp.async.wait_group 0;\n" ::); }
 static constexpr int DN_CI = 6, DN_CJ = 14;  // coarse nodes owned by a down CTA
 static constexpr int UP_OI = 14, UP_OJ = 30; // level-l nodes owned by an up CTA
 
@@ -54,6 +63,7 @@ __global__ void __launch_bounds__(CT_I * CT_J, 1) coarse2d_down_kernel(LevelGeom
                                                                        const int* done) {
     __shared__ double2 s_z[CT_I][CT_J];
     __shared__ double2 s_w[CT_I][CT_J];
+    __shared__ double2 s_r[NSR][CT_I * CT_J];   // r of the next RHS, per thread
     if (done && *done) return;
     const int ti = threadIdx.x / CT_J, tj = threadIdx.x % CT_J;
     const int bI = blockIdx.x / nbj, bJ = blockIdx.x % nbj;
@@ -76,12 +86,22 @@ __global__ void __launch_bounds__(CT_I * CT_J, 1) coarse2d_down_kernel(LevelGeom
     const bool cok = cown && Ic < gc.nn[0] && Jc < gc.nn[1];
     const long long cnode = (long long)Ic * gc.nn[1] + Jc;
     const int mc = cok ? maskc[cnode] : 3;
-    // software pipeline over the RHS: r of RHS k+1 is in flight while RHS k is processed
-    double2 rn = make_double2(0.0, 0.0);
-    if (ok) rn = *reinterpret_cast<const double2*>(r + (long long)k0 * g.ndof + 2 * node);
+    // software pipeline over the RHS: r of the next NSR - 1 RHS is in flight (cp.async ring, one
+    // commit group per RHS; a thread reads only its own slots)
+    const int tid = threadIdx.x;
+    const double* rnode = r + 2 * node;
+#pragma unroll
+    for (int q = 0; q < NSR; ++q) {
+        if (k0 + q < k1) cpa16c(&s_r[q][tid], rnode + (long long)(k0 + q) * g.ndof, ok);
+        cpa_commit_c();
+    }
     for (int k = k0; k < k1; ++k) {
-        const double rx = rn.x, ry = rn.y;
-        if (ok && k + 1 < k1) rn = *reinterpret_cast<const double2*>(r + (long long)(k + 1) * g.ndof + 2 * node);
+        const int st = (k - k0) % NSR;
+        cpa_wait_c();
+        const double2 rv = s_r[st][tid];
+        const double rx = rv.x, ry = rv.y;
+        if (k + NSR < k1) cpa16c(&s_r[st][tid], rnode + (long long)(k + NSR) * g.ndof, ok);
+        cpa_commit_c();
         if (active && !active[k]) continue;
         s_z[ti][tj] = make_double2(omega * dx * rx, omega * dy * ry);
         __syncthreads();
@@ -109,6 +129,7 @@ __global__ void __launch_bounds__(CT_I * CT_J, 1) coarse2d_down_kernel(LevelGeom
         // next RHS overwrites s_z only after every thread has passed the second barrier,
         // i.e. finished reading s_z; s_w is rewritten after the next first barrier
     }
+    cpa_wait_all_c();
 }
 
 __global__ void __launch_bounds__(CT_I * CT_J, 1) coarse2d_up_kernel(LevelGeom g, LevelGeom gc,
@@ -123,6 +144,8 @@ __global__ void __launch_bounds__(CT_I * CT_J, 1) coarse2d_up_kernel(LevelGeom g
     constexpr int CI = CT_I / 2 + 2, CJ = CT_J / 2 + 2;
     __shared__ double2 s_z[CT_I][CT_J];
     __shared__ double2 s_e[CI][CJ];
+    __shared__ double2 s_r[NSR][CT_I * CT_J];   // r of the next RHS, per thread
+    __shared__ double2 s_en[NSR][CI * CJ];      // coarse tile entry of the next RHS
     if (done && *done) return;
     const int ti = threadIdx.x / CT_J, tj = threadIdx.x % CT_J;
     const int bI = blockIdx.x / nbj, bJ = blockIdx.x % nbj;
@@ -149,17 +172,30 @@ __global__ void __launch_bounds__(CT_I * CT_J, 1) coarse2d_up_kernel(LevelGeom g
     const bool eok = threadIdx.x < CI * CJ && eI >= 0 && eI < gc.nn[0] && eJ >= 0 && eJ < gc.nn[1];
     const long long ecn = eok ? (long long)eI * gc.nn[1] + eJ : 0;
     const int emc = eok ? maskc[ecn] : 3;
-    // software pipeline over the RHS: e and r of RHS k+1 are in flight while RHS k is processed
-    double2 en = make_double2(0.0, 0.0), rn = make_double2(0.0, 0.0);
-    if (eok) en = *reinterpret_cast<const double2*>(ec + (long long)k0 * gc.ndof + 2 * ecn);
-    if (ok) rn = *reinterpret_cast<const double2*>(r + (long long)k0 * g.ndof + 2 * node);
-    for (int k = k0; k < k1; ++k) {
-        const double2 ev = en;
-        const double rx = rn.x, ry = rn.y;
-        if (k + 1 < k1) {
-            if (eok) en = *reinterpret_cast<const double2*>(ec + (long long)(k + 1) * gc.ndof + 2 * ecn);
-            if (ok) rn = *reinterpret_cast<const double2*>(r + (long long)(k + 1) * g.ndof + 2 * node);
+    // software pipeline over the RHS: e and r of the next NSR - 1 RHS are in flight (cp.async ring)
+    const int tid = threadIdx.x;
+    const bool has_e = tid < CI * CJ;
+    const double* rnode = r + 2 * node;
+    const double* enode = ec + 2 * ecn;
+#pragma unroll
+    for (int q = 0; q < NSR; ++q) {
+        if (k0 + q < k1) {
+            cpa16c(&s_r[q][tid], rnode + (long long)(k0 + q) * g.ndof, ok);
+            if (has_e) cpa16c(&s_en[q][tid], enode + (long long)(k0 + q) * gc.ndof, eok);
         }
+        cpa_commit_c();
+    }
+    for (int k = k0; k < k1; ++k) {
+        const int st = (k - k0) % NSR;
+        cpa_wait_c();
+        const double2 rv = s_r[st][tid];
+        const double2 ev = has_e ? s_en[st][tid] : make_double2(0.0, 0.0);
+        const double rx = rv.x, ry = rv.y;
+        if (k + NSR < k1) {
+            cpa16c(&s_r[st][tid], rnode + (long long)(k + NSR) * g.ndof, ok);
+            if (has_e) cpa16c(&s_en[st][tid], enode + (long long)(k + NSR) * gc.ndof, eok);
+        }
+        cpa_commit_c();
         if (active && !active[k]) continue;
         if (threadIdx.x < CI * CJ)
             s_e[ea][eb] = make_double2((emc & 1) ? 0.0 : ev.x, (emc & 2) ? 0.0 : ev.y);
@@ -183,6 +219,7 @@ __global__ void __launch_bounds__(CT_I * CT_J, 1) coarse2d_up_kernel(LevelGeom g
         // s_e is rewritten by the next RHS only after every thread passed the second barrier
         // (all s_e reads done); s_z only after the next first barrier (all s_z reads done)
     }
+    cpa_wait_all_c();
 }
 
 // RHS per CTA: all of them on large levels (stencil read once); on small levels the RHS are
