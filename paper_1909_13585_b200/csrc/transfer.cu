@@ -104,9 +104,11 @@ __global__ void prolong_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* __rest
         }
         cn[s] = ok ? q : 0; wgt[s] = ok ? w : 0.0; cm[s] = ok ? mc[q] : 0xff;
     }
-    {   // one RHS per thread (grid.y)
-        const int r = blockIdx.y;
-        if (active && !active[r]) return;
+    // RHS group of this thread: grid.y = R on small levels, all RHS per thread on large ones
+    const int rg = (R + gridDim.y - 1) / gridDim.y;
+    const int rb = blockIdx.y * rg, re = min(R, rb + rg);
+    for (int r = rb; r < re; ++r) {
+        if (active && !active[r]) continue;
         const double* cv = coarse + (long long)r * gc.ndof;
         double acc[DIM];
 #pragma unroll
@@ -129,7 +131,8 @@ void prolong_add(const LevelGeom& gf, const LevelGeom& gc, const uint8_t* mf, co
                  const double* coarse, double* fine, int R, const int* active, const int* done, bool accumulate,
                  cudaStream_t s, int off0) {
     int th = 128;
-    dim3 bl((unsigned)((gf.nnodes + th - 1) / th), R);
+    const long long blocks = (gf.nnodes + th - 1) / th;
+    dim3 bl((unsigned)blocks, blocks >= 148 * 16 ? 1 : R);
     if (gf.dim == 2)
         prolong_kernel<2><<<bl, th, 0, s>>>(gf, gc, mf, mc, coarse, fine, R, active, done, accumulate, off0);
     else
