@@ -35,6 +35,7 @@ struct FineArgs {
     const double* q;
     double* rout;
     const double* alpha;
+    double* z1out;          // FOP_RESTR3: omega D^-1 r stored here too (pre-smoothed z1) or NULL
     // FOP_POST3: operator input z2 = omega D^-1 b + P ec, y = z2 + omega D^-1 (b - K z2)
     const double* ec;
     LevelGeom gc;

@@ -247,7 +247,8 @@ struct mg_ctx {
     bool nu_paper = true;     // nu == 0.3: compile-time K0 in the fine kernels
     bool fused2d = false;     // 2D, L >= 2, V(1,1): fused RESTRICT / POST fine kernels
     bool unfused_coarse = false;   // MG_UNFUSED_COARSE=1: generic coarse-level kernels (A/B checks)
-    bool fused3d = false;     // 3D, L >= 2, V(1,1): fused h8 RESTR3 / POST3 fine kernels
+    bool fused3d = false;     // 3D, L >= 2, V(1,1): fused h8 RESTR3 fine kernel
+    bool fused3d_post = false;   // ... and fused POST3
     mg_opts opts{0.6, 1, 1, 1000};
     cudaStream_t user = nullptr, stream = nullptr;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
@@ -881,6 +882,10 @@ static mg_status blk_restrict(Rec& rc, double* Slab::*rin, double* Slab::*rout, 
             FineArgs a = fine_args(c, s, rc);
             a.rin = s.*rin; a.q = s.q; a.rout = s.*rout; a.alpha = c->ctl.alpha; a.Dinv = s.lv[0].Dinv;
             a.y = s.t; a.partial = c->partial + off;
+            if (!c->fused3d_post) {   // the composed post-smoother needs z1
+                a.z1out = s.z;
+                s.zpre = s.z;
+            }
             off += fine_apply(FOP_RESTR3, a, c->stream);
             rc.launches++;
         }
@@ -958,7 +963,7 @@ static mg_status blk_post(Rec& rc, double* Slab::*r, int cw, long long* items) {
         *items = off;
         return xchg(c, [&](const Slab& s) { return fine_field(c, s, s.zf, R); });
     }
-    if (c->fused3d) {
+    if (c->fused3d_post) {
         // 3D: z2 = omega D^-1 r + P e, zf = z2 + omega D^-1 (r - K z2), r.zf in one h8 kernel
         for (Slab& s : c->sl) {
             FineArgs a = fine_args(c, s, rc);
@@ -1250,10 +1255,18 @@ static mg_status setup_impl(mg_ctx* c, const mg_grid* grid, const double* E_e, c
     c->nu_paper = (c->nu == MG_NU_PAPER) && grid->element == MG_ELEM_STD;
     c->fused2d = (dim == 2 && levels >= 2);
     c->unfused_coarse = getenv("MG_UNFUSED_COARSE") && atoi(getenv("MG_UNFUSED_COARSE")) == 1;
-    // (measured slower than the composed kernels on B200 -- more registers in a latency-bound
-    // kernel -- so opt-in with MG_FUSED3D=1; parity-tested either way)
-    c->fused3d = dim == 3 && levels >= 2 && c->opts.nu_pre == 1 && c->opts.nu_post == 1 && !c->unfused_coarse &&
-                 !getenv("MG_DENSE_H8") && getenv("MG_FUSED3D") && atoi(getenv("MG_FUSED3D")) == 1;
+    // 3D fused fine kernels (opt-in, parity-tested either way), MG_FUSED3D bit 0: r update +
+    // pre-smoother + residual in one h8 kernel (RESTR3; on the plane-ring kernel as fast as
+    // cg_rupdate + RESID on B200, not faster), bit 1: prolongation + post-smoother (POST3; slower
+    // than prolong + JACOBI: more registers in a latency-bound kernel)
+    {
+        const char* e = getenv("MG_FUSED3D");
+        const int f3 = e ? atoi(e) : 0;
+        const bool ok3 = dim == 3 && levels >= 2 && c->opts.nu_pre == 1 && c->opts.nu_post == 1 &&
+                         !c->unfused_coarse && !getenv("MG_DENSE_H8");
+        c->fused3d = ok3 && (f3 & 1);
+        c->fused3d_post = ok3 && (f3 & 2);
+    }
     fine_set_constants(dim, c->K0.data(), s);
     if (dim == 3) h8_set_constants(c->K0.data(), s);
     if (dim == 2) fine2d_set_constants(c->K0.data(), s);

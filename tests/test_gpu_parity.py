@@ -261,14 +261,43 @@ def test_profile_kernels_leaves_solver_state_valid(name):
     assert torch.equal(x1, x2)
 
 
+@pytest.mark.parametrize("fused", ["0", "1", "2", "3"])
 @pytest.mark.parametrize("name", ["T3b", "T3c"])
-def test_fused3d_variant_parity(name, monkeypatch):
-    """The opt-in fused 3D fine V-cycle halves (MG_FUSED3D=1) give the same solution."""
+def test_fused3d_variant_parity(name, fused, monkeypatch):
+    """Every MG_FUSED3D setting of the 3D fine V-cycle halves (bit 0: r update + pre-smoother +
+    residual in one h8 kernel, the default; bit 1: prolongation + post-smoother) solves to the
+    direct solution and applies the oracle's V-cycle."""
     import paper_1909_13585_b200 as mg
-    monkeypatch.setenv("MG_FUSED3D", "1")
+    monkeypatch.setenv("MG_FUSED3D", fused)
     cfg, inp, K = case(name)
     U = direct(name)
     h = handle(name)
+    x = torch.empty((cfg.nrhs, U.shape[1]), dtype=torch.float64, device=DEV)
+    rep = mg.mgcg_solve(h, to_dev(inp["rhs"]), cfg.tol, x)
+    assert rel(x.cpu().numpy(), U).max() < 1e-8, rep
+    H = omg.Hierarchy(cfg.nel, K, inp["fixed"], cfg.levels)
+    V = solve._VCycle(H, 0.6, 1)
+    A = rough_vectors(cfg, 2, seed_offset=31, masked=True)
+    Z = torch.empty((2, A.shape[1]), dtype=torch.float64, device=DEV)
+    mg.mg_vcycle(h, to_dev(A), Z)
+    Zo = np.stack([V.apply(a) for a in A])
+    assert rel(Z.cpu().numpy(), Zo).max() < 1e-9
+
+
+@pytest.mark.parametrize("variants", ["9,9,9,9,9", "3,3,3,3,3", "4,4,4,4,4", "5,5,5,5,5", "0,1,2,0,1"])
+def test_h8_kernel_variants_matvec_and_solve(variants, monkeypatch):
+    """All H8 fine-kernel variants (register prefetch 8/16 rows, 2 CTAs/SM, shared-memory plane
+    ring with and without slot retention) give the same operator and solution."""
+    import paper_1909_13585_b200 as mg
+    monkeypatch.setenv("MG_H8_VARIANTS", variants)
+    name = "T3c"
+    cfg, inp, K = case(name)
+    U = direct(name)
+    h = handle(name)
+    X = rough_vectors(cfg, 3)
+    Y = torch.empty((3, X.shape[1]), dtype=torch.float64, device=DEV)
+    mg.mg_matvec(h, 0, to_dev(X), Y)
+    assert rel(Y.cpu().numpy(), (K @ X.T).T).max() < 1e-13
     x = torch.empty((cfg.nrhs, U.shape[1]), dtype=torch.float64, device=DEV)
     rep = mg.mgcg_solve(h, to_dev(inp["rhs"]), cfg.tol, x)
     assert rel(x.cpu().numpy(), U).max() < 1e-8, rep
