@@ -257,6 +257,9 @@ struct Ops {
 #ifndef MG_ASYNC_RING
 #define MG_ASYNC_RING 1   // POST / RESTRICT: cp.async shared-memory prefetch ring (see below)
 #endif
+#ifndef MG_2D_UNROLL
+#define MG_2D_UNROLL 3    // async ring loop unrolled by NSTAGE: bit 0 CGP, bit 1 RESTRICT, bit 2 POST (B200 A/B: POST slower)
+#endif
 #ifndef MG_ASYNC_CGP
 #define MG_ASYNC_CGP 1    // CGP through the same ring
 #endif
@@ -713,6 +716,26 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
         Slot s0;
         fetch(s0, i0 - 1, 0);
         prologue(s0);
+        constexpr bool UNR = (MG_2D_UNROLL >> (OP == M2_CGP ? 0 : OP == M2_RESTRICT ? 1 : 2)) & 1;
+        if constexpr (UNR) {
+        // unrolled by NSTAGE: stage indices are compile-time and the plane-state shift becomes
+        // register renaming (no moves)
+        for (int L0 = i0 - 1; L0 < i1; L0 += NSTAGE) {
+#pragma unroll
+            for (int u = 0; u < NSTAGE; ++u) {
+                const int L = L0 + u;
+                if (L >= i1) break;
+                const int P = L + 1;
+                const int pn = P + NSTAGE - 1;
+                if (pn <= i1) issue(pn, u);
+                cpa_commit();
+                cpa_wait<NSTAGE - 1>();
+                Slot s;
+                fetch(s, P, (u + 1) % NSTAGE);
+                step(s, L);
+            }
+        }
+        } else {
         for (int L = i0 - 1; L < i1; ++L) {
             const int P = L + 1;
             const int pn = P + NSTAGE - 1;
@@ -722,6 +745,7 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
             Slot s;
             fetch(s, P, stage(P));
             step(s, L);
+        }
         }
         cpa_wait<0>();
     }
