@@ -136,8 +136,8 @@ __device__ __forceinline__ void st2(double* p, double a, double b) { *reinterpre
 Pad2 pad2_layout(const LevelGeom& g) {
     Pad2 p{};
     const int n0 = g.nn[0], n1 = g.nn[1], N0 = g.N[0], N1 = g.N[1];
-    p.pitch = n1 + 2;
-    p.org = 16 + p.pitch + 2;                    // front slack: lanes reach column -2 of row -1
+    p.pitch = (n1 + 2 + 3) & ~3;                 // multiple of 4: a lane's mask byte offset is fixed
+    p.org = 16 + p.pitch + 5;                    // front slack (lanes reach column -3 of row -1); org % 4 == 1
     p.nodes = p.org + (long long)(n0 + 1) * p.pitch + 64;
     p.pitchE = N1 + 2;
     p.orgE = 16 + p.pitchE + 4;
@@ -303,7 +303,9 @@ struct ARing {
 template <int OP, bool C03, bool SLAB>
 __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2Args a, int nct, int nch, int chl) {
     constexpr int CS = (OP == M2_RESTRICT) ? 28 : 30;      // owned columns per warp
-    constexpr int LOFF = (OP == M2_RESTRICT) ? 2 : 1;      // lane of the first owned column
+    // lane of the first owned column; lane 0 sits at an odd column for every op, which with
+    // pad2_layout's odd org and pitch % 4 == 0 makes each warp's 512-byte plane row 32-byte aligned
+    constexpr int LOFF = (OP == M2_RESTRICT) ? 3 : 1;
     const int lane = threadIdx.x & 31;
     const long long w = (long long)blockIdx.x * WPB + (threadIdx.x >> 5);
     const int items = nct * nch;
@@ -417,7 +419,9 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
             cpa4(&AR.cm0[st][lane], reinterpret_cast<const uint8_t*>((uintptr_t)(a.maskc + ci) & ~(uintptr_t)3), pr);
         }
     };
-    auto byte_of = [](unsigned word, const void* addr) { return (int)((word >> (8 * ((uintptr_t)addr & 3))) & 0xff); };
+    const int msh = 8 * (int)((unsigned)(pd.org + c) & 3u);   // pitch % 4 == 0 (pad2_layout)
+    // byte i of a mask array (4-byte aligned base) from the aligned word holding it
+    auto byte_of = [](unsigned word, unsigned i) { return (int)((word >> (8 * (i & 3u))) & 0xffu); };
     auto fetch = [&](Slot& s, int P, int st) {
         const long long no = pd.org + (long long)P * pd.pitch + c;
         const double2 v0 = AR.v0[st][lane];
@@ -426,7 +430,7 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
         if (OP == M2_CGP) { const double2 x2 = AR.xv[st][lane]; s.xx = x2.x; s.xy = x2.y; }
         if (OP != M2_CGP) { const double2 d = AR.d[st][lane]; s.dx = d.x; s.dy = d.y; }
         s.e = AR.e[st][lane];
-        s.m = byte_of(AR.m[st][lane], a.mask + no);
+        s.m = (int)((AR.m[st][lane] >> msh) & 0xffu);
         const int Ps = P + off0;
         if (OP == M2_POST) {
             const int I = (Ps + 1) >> 1;
@@ -434,8 +438,9 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
             s.cx0 = s.cy0 = s.cx1 = s.cy1 = 0.0;
             if (pr) {
                 const long long row = (long long)I * nc1;
-                const int m0 = byte_of(AR.cm0[st][lane], a.maskc + row + J0);
-                const int m1 = byte_of(AR.cm1[st][lane], a.maskc + row + J1);
+                const unsigned rowu = (unsigned)I * (unsigned)nc1;
+                const int m0 = byte_of(AR.cm0[st][lane], rowu + J0);
+                const int m1 = byte_of(AR.cm1[st][lane], rowu + J1);
                 const double2 e0 = AR.c0[st][lane], e1 = AR.c1[st][lane];
                 s.cx0 = (m0 & 1) ? 0.0 : e0.x; s.cy0 = (m0 & 2) ? 0.0 : e0.y;
                 s.cx1 = (m1 & 1) ? 0.0 : e1.x; s.cy1 = (m1 & 2) ? 0.0 : e1.y;
@@ -444,7 +449,7 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
         if (OP == M2_RESTRICT) {
             const int I = (Ps - 1) >> 1;
             const bool pr = Ps >= 1 && cin && !(c & 1) && I < a.gc.nn[0];
-            s.cm = pr ? byte_of(AR.cm0[st][lane], a.maskc + (long long)I * nc1 + J0) : 3;
+            s.cm = pr ? byte_of(AR.cm0[st][lane], (unsigned)I * (unsigned)nc1 + J0) : 3;
         }
     };
 
@@ -650,7 +655,7 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
                 const double tlx = shfl_up1(tx), tly = shfl_up1(ty);
                 const double trx = shfl_dn1(tx), try_ = shfl_dn1(ty);
                 const double hx = fma(0.5, tlx + trx, tx), hy = fma(0.5, tly + try_, ty);
-                const bool cown = cin && !(c & 1) && lane >= 2 && lane <= 28;
+                const bool cown = cin && !(c & 1) && lane >= LOFF && lane <= LOFF + CS - 2;
                 const int cm = (int)k2x;     // coarse mask of row (P-1)>>1 = the row output below
                 const int Ls = L + off0;
                 if (Ls & 1) {
@@ -706,7 +711,7 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
     } else {
         // cp.async ring: NSTAGE planes in flight, one commit group per plane (empty groups keep
         // the count uniform), plane p in stage (p - i0 + 1) % NSTAGE
-        auto stage = [&](int p) { return (p - i0 + 1) % NSTAGE; };
+        auto stage = [&](int p) { return (int)((unsigned)(p - i0 + 1) % NSTAGE); };
 #pragma unroll
         for (int k = 0; k < NSTAGE; ++k) {
             issue(min(i0 - 1 + k, i1), k);
