@@ -200,54 +200,79 @@ void dense_spd_inverse(double* A, long long npad, double* work, int* d_status, c
 // z[r][i] = sum_j Ainv[i][j] rvec[r][j]: 4 rows per CTA (one warp each), the RB right-hand
 // sides staged through shared memory in column chunks so every Ainv row is streamed once and
 // the vectors come from shared memory (Ainv and the vectors are L2-resident, n_L <= ~4k).
-static constexpr int DA_ROWS = 4, DA_CHK = 256;
+// z[q][i] = sum_j Ainv[i][j] r[q][j] for the RB right-hand sides q of this chunk.  A CTA owns
+// RW = 32 / RB rows; its 8 warps split the columns, every lane accumulates RW x RB = 32 partial
+// sums (one A load per row and one r load per RHS per column: RW RB FMAs per RW + RB loads).
+// The 32 per-lane values are reduced across the warp by a transposing butterfly (31 shuffles,
+// lane l ends with value l), then across the 8 warps through shared memory.
+static constexpr int DA_WARPS = 8;
 
 template <int RB>
-__global__ void __launch_bounds__(32 * DA_ROWS) dense_apply_kernel(const double* __restrict__ Ainv, long long ld,
-                                                                   long long n, const double* __restrict__ rv,
-                                                                   double* __restrict__ z, int R, int r0,
-                                                                   const int* active, const int* done) {
-    __shared__ double s_r[RB][DA_CHK];
+__global__ void __launch_bounds__(32 * DA_WARPS) dense_apply_kernel(const double* __restrict__ Ainv, long long ld,
+                                                                    long long n, const double* __restrict__ rv,
+                                                                    double* __restrict__ z, int R, int r0,
+                                                                    const int* active, const int* done) {
+    constexpr int RW = 32 / RB;
+    __shared__ double red[DA_WARPS][32];
     if (done && *done) return;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const long long i = (long long)blockIdx.x * DA_ROWS + w;
+    const long long i0 = (long long)blockIdx.x * RW;
     const int nr = min(RB, R - r0);
-    double acc[RB];
+    double v[32];
 #pragma unroll
-    for (int q = 0; q < RB; ++q) acc[q] = 0.0;
-    const double* row = Ainv + (i < n ? i : 0) * ld;
-    for (long long j0 = 0; j0 < n; j0 += DA_CHK) {
-        const int len = (int)(n - j0 < DA_CHK ? n - j0 : DA_CHK);
-        for (int e = threadIdx.x; e < RB * DA_CHK; e += 32 * DA_ROWS) {
-            const int q = e / DA_CHK, jj = e % DA_CHK;
-            s_r[q][jj] = (q < nr && jj < len) ? rv[(long long)(r0 + q) * n + j0 + jj] : 0.0;
-        }
-        __syncthreads();
-        if (i < n) {
-            for (int jj = lane; jj < len; jj += 32) {
-                const double a = row[j0 + jj];
+    for (int t = 0; t < 32; ++t) v[t] = 0.0;
+    const long long seg = ((n + 32 * DA_WARPS - 1) / (32 * DA_WARPS)) * 32;
+    const long long jb = w * seg, je = min(n, jb + seg);
+    const int nrow = (int)(n - i0 < RW ? n - i0 : RW);
+    const double* row0 = Ainv + i0 * ld;
+    for (long long j = jb + lane; j < je; j += 32) {
+        double a[RW];
 #pragma unroll
-                for (int q = 0; q < RB; ++q) acc[q] = fma(a, s_r[q][jj], acc[q]);
-            }
+        for (int rr = 0; rr < RW; ++rr) a[rr] = rr < nrow ? __ldg(row0 + rr * ld + j) : 0.0;
+#pragma unroll
+        for (int q = 0; q < RB; ++q) {
+            const double x = q < nr ? __ldg(rv + (long long)(r0 + q) * n + j) : 0.0;
+#pragma unroll
+            for (int rr = 0; rr < RW; ++rr) v[rr * RB + q] = fma(a[rr], x, v[rr * RB + q]);
         }
-        __syncthreads();
     }
-    if (i >= n) return;
+    // transposing butterfly: after the step with offset o, a lane keeps the half of its values
+    // selected by its bit o; lane l finishes with the warp sum of value l
 #pragma unroll
-    for (int q = 0; q < RB; ++q) {
-        const double v = warp_sum(acc[q]);
-        if (lane == 0 && q < nr && (!active || active[r0 + q])) z[(long long)(r0 + q) * n + i] = v;
+    for (int o = 16, cnt = 32; o >= 1; o >>= 1, cnt >>= 1) {
+        const bool up = lane & o;
+#pragma unroll
+        for (int k = 0; k < cnt / 2; ++k) {
+            const double send = up ? v[k] : v[k + cnt / 2];
+            const double keep = up ? v[k + cnt / 2] : v[k];
+            v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    red[w][lane] = v[0];
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int t = threadIdx.x, rr = t / RB, q = t % RB;
+        double sum = 0.0;
+#pragma unroll
+        for (int ww = 0; ww < DA_WARPS; ++ww) sum += red[ww][t];
+        const long long i = i0 + rr;
+        if (i < n && q < nr && (!active || active[r0 + q])) z[(long long)(r0 + q) * n + i] = sum;
     }
 }
 
 void dense_apply(const double* Ainv, long long ld, long long n, const double* r, double* z, int R, const int* active,
                  const int* done, cudaStream_t s) {
-    unsigned bl = (unsigned)((n + DA_ROWS - 1) / DA_ROWS);
     for (int r0 = 0; r0 < R;) {
-        int rem = R - r0;
-        if (rem > 8) { dense_apply_kernel<16><<<bl, 32 * DA_ROWS, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); r0 += 16; }
-        else if (rem > 4) { dense_apply_kernel<8><<<bl, 32 * DA_ROWS, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); r0 += 8; }
-        else if (rem > 1) { dense_apply_kernel<4><<<bl, 32 * DA_ROWS, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); r0 += 4; }
-        else { dense_apply_kernel<1><<<bl, 32 * DA_ROWS, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); r0 += 1; }
+        const int rem = R - r0;
+        const int rb = rem > 16 ? 32 : rem > 8 ? 16 : rem > 4 ? 8 : rem > 1 ? 4 : 1;
+        const unsigned bl = (unsigned)((n + 32 / rb - 1) / (32 / rb));
+        switch (rb) {
+            case 32: dense_apply_kernel<32><<<bl, 32 * DA_WARPS, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); break;
+            case 16: dense_apply_kernel<16><<<bl, 32 * DA_WARPS, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); break;
+            case 8: dense_apply_kernel<8><<<bl, 32 * DA_WARPS, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); break;
+            case 4: dense_apply_kernel<4><<<bl, 32 * DA_WARPS, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); break;
+            default: dense_apply_kernel<1><<<bl, 32 * DA_WARPS, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); break;
+        }
+        r0 += rb;
     }
 }
