@@ -5,6 +5,8 @@
 // block 32).  Per V-cycle: z = A^-1 r for all R vectors, one warp per row, so the
 // solve is a bandwidth-bound dense product instead of a latency-bound triangular
 // sweep.
+#include <cstdlib>
+
 #include "kernels.h"
 
 static constexpr int GJ_NB = 32;
@@ -51,30 +53,8 @@ void dense_pad_identity(double* A, long long n, long long npad, cudaStream_t s) 
     if (npad > n) pad_identity_kernel<<<1, GJ_NB, 0, s>>>(A, n, npad);
 }
 
-// In-place Gauss-Jordan inverse of the NB x NB diagonal block k (one CTA, NB*NB threads).
-__global__ void gj_diag_kernel(double* A, long long ld, int k0, double* P, int* status) {
-    __shared__ double S[GJ_NB][GJ_NB + 1];
-    const int i = threadIdx.y, j = threadIdx.x;
-    S[i][j] = A[(k0 + i) * ld + k0 + j];
-    __syncthreads();
-    for (int p = 0; p < GJ_NB; ++p) {
-        const double piv = S[p][p];
-        const double sip = S[i][p], spj = S[p][j], sij = S[i][j];
-        __syncthreads();
-        if (!(piv > 0.0)) {
-            if (i == 0 && j == 0) atomicOr(status, 2);
-        }
-        const double ip = 1.0 / piv;
-        double v;
-        if (i == p && j == p) v = ip;
-        else if (i == p) v = spj * ip;
-        else if (j == p) v = -sip * ip;
-        else v = sij - sip * spj * ip;
-        S[i][j] = v;
-        __syncthreads();
-    }
-    P[i * GJ_NB + j] = S[i][j];
-}
+// panel / fix-up kernels split the NB panel rows over GJ_TQ CTAs (grid.y) for parallelism
+static constexpr int GJ_TQ = 4;
 
 // Rrow[t][j] = sum_s P[t][s] A[k0+s][j]   (new row panel), Ccol[i][t] = A[i][k0+t] (old column panel)
 __global__ void gj_panels_kernel(const double* A, long long ld, long long n, int k0, const double* P, double* Rrow,
@@ -85,11 +65,13 @@ __global__ void gj_panels_kernel(const double* A, long long ld, long long n, int
     __syncthreads();
     long long j = (long long)blockIdx.x * blockDim.x + tid;
     if (j >= n) return;
+    const int tb = blockIdx.y * (GJ_NB / GJ_TQ);   // this CTA's rows t of the panels
     double col[GJ_NB];
 #pragma unroll
     for (int s = 0; s < GJ_NB; ++s) col[s] = A[(k0 + s) * ld + j];
-#pragma unroll 4
-    for (int t = 0; t < GJ_NB; ++t) {
+#pragma unroll
+    for (int tt = 0; tt < GJ_NB / GJ_TQ; ++tt) {
+        const int t = tb + tt;
         double acc = 0.0;
 #pragma unroll
         for (int s = 0; s < GJ_NB; ++s) acc = fma(Ps[t][s], col[s], acc);
@@ -98,7 +80,7 @@ __global__ void gj_panels_kernel(const double* A, long long ld, long long n, int
     // column panel: row j of A's column block (A symmetric in exact arithmetic, but
     // read the column explicitly to stay exact for the unsymmetric rounding)
 #pragma unroll
-    for (int t = 0; t < GJ_NB; ++t) Ccol[j * GJ_NB + t] = A[j * ld + k0 + t];
+    for (int tt = 0; tt < GJ_NB / GJ_TQ; ++tt) Ccol[j * GJ_NB + tb + tt] = A[j * ld + k0 + tb + tt];
 }
 
 // A[i][j] -= sum_t Ccol[i][t] Rrow[t][j] for all i, j (64x64 tile per CTA, 4x4 per thread).
@@ -155,18 +137,173 @@ __global__ void __launch_bounds__(256) gj_update_kernel(double* A, long long ld,
     }
 }
 
-// Overwrite the pivot column panel: A[i][k] = -Ccol[i] P for rows i outside the pivot block.
-__global__ void gj_fix_cols_kernel(double* A, long long ld, long long n, int k0, const double* P, const double* Ccol) {
+// Same update on the fp64 tensor-core path (DMMA, mma.sync m8n8k4 f64): 64x64 tile per CTA,
+// 4 warps of 32x32 (4x4 m8n8 tiles each); per k-step of 4 a warp loads 4 A and 4 B fragments
+// (one double per lane each) for 16 MMAs instead of 8 shared loads per 16 FMAs per thread.
+// Shared-memory leading dimensions = 4 (mod 16) doubles: conflict-free fragment loads.
+static constexpr int GU_LDC = GJ_NB + 4, GU_LDR = 64 + 4;
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// kn >= 0: the CTA whose tile holds the next diagonal block (kn..kn+31)^2 -- scheduled first --
+// also inverts it after its update (Gauss-Jordan in shared memory) into Pn, so the next block
+// step needs no separate diagonal kernel.
+// Gauss-Jordan inverse of the 32x32 SPD block S in shared memory by NT threads (1024 / NT entries
+// each, two barriers per pivot).  Scalar pivots: the blocked (4x4-pivot) variant measured slower
+// on B200 (the redundant pivot-block inverses cost more than the barriers they save).
+template <int NT>
+__device__ __forceinline__ void gj_block_inverse_smem(double (*S)[GJ_NB + 1], int tid, int* status) {
+    constexpr int PE = GJ_NB * GJ_NB / NT;
+    for (int p = 0; p < GJ_NB; ++p) {
+        const double piv = S[p][p];
+        const double ip = 1.0 / piv;
+        double v[PE];
+#pragma unroll
+        for (int q = 0; q < PE; ++q) {
+            const int e = tid + q * NT, i = e / GJ_NB, j = e % GJ_NB;
+            if (i == p && j == p) v[q] = ip;
+            else if (i == p) v[q] = S[p][j] * ip;
+            else if (j == p) v[q] = -S[i][p] * ip;
+            else v[q] = S[i][j] - S[i][p] * S[p][j] * ip;
+        }
+        if (!(piv > 0.0) && tid == 0) atomicOr(status, 2);
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < PE; ++q) {
+            const int e = tid + q * NT;
+            S[e / GJ_NB][e % GJ_NB] = v[q];
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(1024) gj_diag_kernel(const double* A, long long ld, int k0, double* P, int* status) {
+    __shared__ double S[GJ_NB][GJ_NB + 1];
+    const int e = threadIdx.x;
+    S[e / GJ_NB][e % GJ_NB] = A[(k0 + e / GJ_NB) * ld + k0 + e % GJ_NB];
+    __syncthreads();
+    gj_block_inverse_smem<1024>(S, threadIdx.x, status);
+    P[e] = S[e / GJ_NB][e % GJ_NB];
+}
+
+__global__ void __launch_bounds__(128) gj_update_mma_kernel(double* A, long long ld, long long n, const double* Ccol,
+                                                            const double* Rrow, long long kn, double* Pn,
+                                                            int* status) {
+    __shared__ __align__(16) double Cs[64 * GU_LDC];
+    __shared__ __align__(16) double Rs[GJ_NB * GU_LDR];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm = warp >> 1, wn = warp & 1;
+    // tile order: the next diagonal block's tile first, the others shifted up (CTA 0 starts first)
+    const long long nt = gridDim.x;
+    long long tile = (long long)blockIdx.y * nt + blockIdx.x;
+    const long long td = kn >= 0 ? (kn / 64) * nt + kn / 64 : -1;
+    if (td >= 0) tile = tile == 0 ? td : (tile <= td ? tile - 1 : tile);
+    const long long i0 = (tile / nt) * 64, j0 = (tile % nt) * 64;
+    const int gr = lane >> 2, gc = lane & 3;
+    // old A values at this thread's accumulator positions (latency overlaps the panel loads)
+    double2 aold[4][4];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+            const long long i = i0 + wm * 32 + mi * 8 + gr, j = j0 + wn * 32 + ni * 8 + 2 * gc;
+            aold[mi][ni] = (i < n && j < n) ? *reinterpret_cast<const double2*>(A + i * ld + j) : make_double2(0.0, 0.0);
+        }
+    // panels by cp.async (16-byte pairs, zero-filled outside the matrix): all 16 copies of a
+    // thread in flight at once instead of a load -> store dependency per element
+#pragma unroll
+    for (int q = 0; q < 64 * GJ_NB / 2 / 128; ++q) {
+        const int e = 2 * (threadIdx.x + q * 128);
+        const int r = e / GJ_NB, t = e % GJ_NB;
+        const long long i = i0 + r;
+        const unsigned dc = (unsigned)__cvta_generic_to_shared(&Cs[r * GU_LDC + t]);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dc),
+                     "l"(Ccol + (i < n ? i : 0) * GJ_NB + t), "r"(i < n ? 16 : 0));
+        const int t2 = e / 64, c = e % 64;
+        const long long j = j0 + c;
+        const unsigned dr = (unsigned)__cvta_generic_to_shared(&Rs[t2 * GU_LDR + c]);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dr),
+                     "l"(Rrow + t2 * n + (j < n ? j : 0)), "r"(j < n ? 16 : 0));
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
+    __syncthreads();
+    double acc[4][4][2];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+#pragma unroll
+    for (int k0 = 0; k0 < GJ_NB; k0 += 4) {
+        double af[4], bf[4];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) af[mi] = Cs[(wm * 32 + mi * 8 + gr) * GU_LDC + k0 + gc];
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) bf[ni] = Rs[(k0 + gc) * GU_LDR + wn * 32 + ni * 8 + gr];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af[mi], bf[ni]);
+    }
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+        const long long i = i0 + wm * 32 + mi * 8 + gr;
+        if (i >= n) continue;
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+            const long long j = j0 + wn * 32 + ni * 8 + 2 * gc;
+            if (j < n)
+                *reinterpret_cast<double2*>(A + i * ld + j) =
+                    make_double2(aold[mi][ni].x - acc[mi][ni][0], aold[mi][ni].y - acc[mi][ni][1]);
+        }
+    }
+    if (td < 0 || tile != td) return;
+    // the next diagonal block is warp (q, q)'s 32x32 sub-tile
+    const int q = (int)((kn / 32) & 1);
+    __syncthreads();   // Cs is reused as the block
+    double(*S)[GJ_NB + 1] = reinterpret_cast<double(*)[GJ_NB + 1]>(Cs);
+    if (wm == q && wn == q) {
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) {
+                S[mi * 8 + gr][ni * 8 + 2 * gc] = aold[mi][ni].x - acc[mi][ni][0];
+                S[mi * 8 + gr][ni * 8 + 2 * gc + 1] = aold[mi][ni].y - acc[mi][ni][1];
+            }
+    }
+    __syncthreads();
+    gj_block_inverse_smem<128>(S, threadIdx.x, status);
+    for (int e = threadIdx.x; e < GJ_NB * GJ_NB; e += 128) Pn[e] = S[e / GJ_NB][e % GJ_NB];
+}
+
+// Both fix-ups in one launch (disjoint parts of A): grid.y < GJ_TQ -> pivot columns (rows outside
+// the block, NB / GJ_TQ columns per CTA row), grid.y >= GJ_TQ -> pivot rows.
+__global__ void __launch_bounds__(128) gj_fix_kernel(double* A, long long ld, long long n, int k0, const double* P,
+                                                     const double* Ccol, const double* Rrow) {
     __shared__ double Ps[GJ_NB][GJ_NB];
+    if (blockIdx.y >= GJ_TQ) {
+        const long long j = (long long)blockIdx.x * 128 + threadIdx.x;
+        if (j >= n) return;
+#pragma unroll
+        for (int tt = 0; tt < GJ_NB / GJ_TQ; ++tt) {
+            const int t = (blockIdx.y - GJ_TQ) * (GJ_NB / GJ_TQ) + tt;
+            A[(k0 + t) * ld + j] = (j >= k0 && j < k0 + GJ_NB) ? P[t * GJ_NB + (j - k0)] : Rrow[t * n + j];
+        }
+        return;
+    }
     for (int e = threadIdx.x; e < GJ_NB * GJ_NB; e += blockDim.x) Ps[e / GJ_NB][e % GJ_NB] = P[e];
     __syncthreads();
-    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    long long i = (long long)blockIdx.x * 128 + threadIdx.x;
     if (i >= n || (i >= k0 && i < k0 + GJ_NB)) return;
     double c[GJ_NB];
 #pragma unroll
     for (int s = 0; s < GJ_NB; ++s) c[s] = Ccol[i * GJ_NB + s];
-#pragma unroll 4
-    for (int t = 0; t < GJ_NB; ++t) {
+#pragma unroll
+    for (int tt = 0; tt < GJ_NB / GJ_TQ; ++tt) {
+        const int t = blockIdx.y * (GJ_NB / GJ_TQ) + tt;
         double acc = 0.0;
 #pragma unroll
         for (int s = 0; s < GJ_NB; ++s) acc = fma(c[s], Ps[s][t], acc);
@@ -174,26 +311,37 @@ __global__ void gj_fix_cols_kernel(double* A, long long ld, long long n, int k0,
     }
 }
 
-// Overwrite the pivot row panel: A[k][j] = Rrow (j outside the block), A[k][k] = P.
-__global__ void gj_fix_rows_kernel(double* A, long long ld, long long n, int k0, const double* P, const double* Rrow) {
-    const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const int t = blockIdx.y;
-    if (j >= n) return;
-    A[(k0 + t) * ld + j] = (j >= k0 && j < k0 + GJ_NB) ? P[t * GJ_NB + (j - k0)] : Rrow[t * n + j];
+// MG_GJ_MMA=0 selects the DFMA update kernel
+static bool gj_mma() {
+    static bool v = [] {
+        const char* e = getenv("MG_GJ_MMA");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return v;
 }
 
+static constexpr long long GJ_FOLD_N = 3072;
+
 void dense_spd_inverse(double* A, long long npad, double* work, int* d_status, cudaStream_t s) {
-    double* P = work;
-    double* Rrow = work + GJ_NB * GJ_NB;
+    double* Pb[2] = {work, work + GJ_NB * GJ_NB};   // ping-pong: block k's inverse, next block's
+    double* Rrow = work + 2 * GJ_NB * GJ_NB;
     double* Ccol = Rrow + npad * GJ_NB;
     const long long n = npad;
-    for (long long k0 = 0; k0 < n; k0 += GJ_NB) {
-        gj_diag_kernel<<<1, dim3(GJ_NB, GJ_NB), 0, s>>>(A, n, (int)k0, P, d_status);
-        gj_panels_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(A, n, n, (int)k0, P, Rrow, Ccol);
+    const bool mma = gj_mma();
+    const unsigned nb = (unsigned)((n + 127) / 128);
+    for (long long k0 = 0, it = 0; k0 < n; k0 += GJ_NB, ++it) {
+        double* P = Pb[it & 1];
+        double* Pn = Pb[(it + 1) & 1];
+        // the next diagonal block is inverted inside the update kernel when that kernel is long
+        // enough to hide it (large coarsest levels), else by its own kernel
+        const bool fold = mma && n >= GJ_FOLD_N;
+        if (!fold || k0 == 0) gj_diag_kernel<<<1, 1024, 0, s>>>(A, n, (int)k0, P, d_status);
+        gj_panels_kernel<<<dim3(nb, GJ_TQ), 128, 0, s>>>(A, n, n, (int)k0, P, Rrow, Ccol);
         dim3 g((unsigned)((n + 63) / 64), (unsigned)((n + 63) / 64));
-        gj_update_kernel<<<g, 256, 0, s>>>(A, n, n, Ccol, Rrow);
-        gj_fix_cols_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(A, n, n, (int)k0, P, Ccol);
-        gj_fix_rows_kernel<<<dim3((unsigned)((n + 255) / 256), GJ_NB), 256, 0, s>>>(A, n, n, (int)k0, P, Rrow);
+        const long long kn = (fold && k0 + GJ_NB < n) ? k0 + GJ_NB : -1;
+        if (mma) gj_update_mma_kernel<<<g, 128, 0, s>>>(A, n, n, Ccol, Rrow, kn, Pn, d_status);
+        else gj_update_kernel<<<g, 256, 0, s>>>(A, n, n, Ccol, Rrow);
+        gj_fix_kernel<<<dim3(nb, 2 * GJ_TQ), 128, 0, s>>>(A, n, n, (int)k0, P, Ccol, Rrow);
     }
 }
 

@@ -547,7 +547,7 @@ static mg_status compute_operators(mg_ctx* c) {
     CU(cudaMemsetAsync(c->Ainv, 0, sizeof(double) * c->npad * c->npad, s));
     dense_from_stencil(gL, stc, c->Ainv, c->npad, s);
     dense_pad_identity(c->Ainv, c->nL, c->npad, s);
-    CU(cudaMemsetAsync(c->gj_work, 0, sizeof(double) * (32 * 32 + 2 * c->npad * 32), s));
+    CU(cudaMemsetAsync(c->gj_work, 0, sizeof(double) * (2 * 32 * 32 + 2 * c->npad * 32), s));
     dense_spd_inverse(c->Ainv, c->npad, c->gj_work, c->d_status, s);
     c->launches += 2 + 5 * (c->npad / 32);
     CHECK_LAUNCH();
@@ -1348,7 +1348,7 @@ static mg_status setup_impl(mg_ctx* c, const mg_grid* grid, const double* E_e, c
     c->nL = gL.ndof;
     c->npad = (c->nL + 31) / 32 * 32;
     CU(cudaMalloc(&c->Ainv, sizeof(double) * c->npad * c->npad));
-    CU(cudaMalloc(&c->gj_work, sizeof(double) * (32 * 32 + 2 * c->npad * 32)));
+    CU(cudaMalloc(&c->gj_work, sizeof(double) * (2 * 32 * 32 + 2 * c->npad * 32)));
     if (multi(c)) {
         const int ns = dim == 2 ? 9 : 27;
         CU(cudaMalloc(&c->stg, sizeof(double) * gL.nnodes * ns * dim * dim));
