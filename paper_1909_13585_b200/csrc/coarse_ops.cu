@@ -97,32 +97,40 @@ void elements_from_E(const LevelGeom& g, const double* E, const uint8_t* mask, d
 // (c_M, set once per handle) -- one FMA per child instead of two small matrix products.
 // SRC: 0 = child element matrices elm_f (levels >= 2), 1 = E_e K0 (K, level 1), 2 = the stress
 // stiffness Es_e (sigma_e : H) kron I_d from per-element Voigt stresses in E (G, level 1; NEXT-2)
-template <int DIM, int SRC>
-__global__ void galerkin_kernel(LevelGeom gc, LevelGeom gf, const double* __restrict__ E,
-                                const double* __restrict__ elm_f, const uint8_t* __restrict__ mask_f,
-                                const uint8_t* __restrict__ mask_c, double* __restrict__ elm_c, int off0,
-                                const double* __restrict__ Mc) {
+// NT threads per coarse element, EPT = NL^2 / NT matrix entries per thread (3D: 192 threads x 3
+// entries, so ~8 elements are in flight per SM instead of 3 -- the per-element mask check and
+// child loads are latency, not bandwidth).
+template <int DIM, int SRC, int NT>
+__global__ void __launch_bounds__(NT) galerkin_kernel(LevelGeom gc, LevelGeom gf, const double* __restrict__ E,
+                                                      const double* __restrict__ elm_f,
+                                                      const uint8_t* __restrict__ mask_f,
+                                                      const uint8_t* __restrict__ mask_c, double* __restrict__ elm_c,
+                                                      int off0, const double* __restrict__ Mc) {
     constexpr int NA = 1 << DIM, NL = DIM * NA;
+    constexpr int EPT = NL * NL / NT;
+    static_assert(EPT * NT == NL * NL, "NT divides NL^2");
     __shared__ double Kc[NL * NL];
     __shared__ double T[NL * NL];
     __shared__ double fr[NL];
-    const int t = threadIdx.x;
-    const int row = t / NL, col = t % NL;
-    // grid-stride over coarse elements: a few waves of CTAs instead of one CTA per element
+    const int t0 = threadIdx.x;
+    // grid-stride over coarse elements
     for (long long Ec = blockIdx.x; Ec < gc.nelem; Ec += gridDim.x) {
     int ci[3] = {0, 0, 0};
     long long tt = Ec;
     for (int k = DIM - 1; k >= 0; --k) { ci[k] = (int)(tt % gc.N[k]); tt /= gc.N[k]; }
     // slab ghost element layer (children not local): filled by the halo exchange instead
     if (ci[0] < off0) continue;
-    double acc = 0.0;
+    double acc[EPT];
+#pragma unroll
+    for (int u = 0; u < EPT; ++u) acc[u] = 0.0;
     bool fast = false;
     constexpr bool FROM_E = SRC == 1;
     if (FROM_E && Mc) {
         constexpr int NF = DIM == 2 ? 9 : 27;   // fine nodes of the coarse element
+        static_assert(NF <= NT, "one fine node per thread");
         int fixed_here = 0;
-        if (t < NF) {
-            int q = t, node = 0;
+        if (t0 < NF) {
+            int q = t0, node = 0;
             int fc[3];
             for (int k = DIM - 1; k >= 0; --k) { fc[k] = 2 * ci[k] + q % 3 - (k == 0 ? off0 : 0); q /= 3; }
             bool inside = true;
@@ -137,12 +145,18 @@ __global__ void galerkin_kernel(LevelGeom gc, LevelGeom gf, const double* __rest
         fast = !__syncthreads_or(fixed_here);
     }
     if (fast) {
+        double ev[NA];
+#pragma unroll
         for (int ch = 0; ch < NA; ++ch) {
             long long fe = 0;
             for (int k = 0; k < DIM; ++k)
                 fe = fe * gf.N[k] + 2 * ci[k] + ((ch >> (DIM - 1 - k)) & 1) - (k == 0 ? off0 : 0);
-            acc = fma(E[fe], Mc[ch * NL * NL + t], acc);
+            ev[ch] = E[fe];
         }
+#pragma unroll
+        for (int ch = 0; ch < NA; ++ch)
+#pragma unroll
+            for (int u = 0; u < EPT; ++u) acc[u] = fma(ev[ch], Mc[ch * NL * NL + t0 + u * NT], acc[u]);
     } else
     for (int ch = 0; ch < NA; ++ch) {
         int fi[3];
@@ -150,46 +164,55 @@ __global__ void galerkin_kernel(LevelGeom gc, LevelGeom gf, const double* __rest
         long long fe = fi[0];
         for (int k = 1; k < DIM; ++k) fe = fe * gf.N[k] + fi[k];
         if (SRC == 1 || SRC == 2) {
-            if (t < NL) {
-                int a = t / DIM, comp = t % DIM;
+            if (t0 < NL) {
+                int a = t0 / DIM, comp = t0 % DIM;
                 long long node = 0;
                 for (int k = 0; k < DIM; ++k) node = node * gf.nn[k] + fi[k] + ((a >> (DIM - 1 - k)) & 1);
-                fr[t] = ((mask_f[node] >> comp) & 1) ? 0.0 : 1.0;
+                fr[t0] = ((mask_f[node] >> comp) & 1) ? 0.0 : 1.0;
             }
             __syncthreads();
-            if (SRC == 1) {
-                Kc[t] = E[fe] * c_K0g[t] * fr[row] * fr[col];
-            } else {
-                constexpr int NV = DIM == 2 ? 3 : 6;
-                const int a = row / DIM, b = col / DIM;
-                double v = 0.0;
-                if (row % DIM == col % DIM) {
-                    const double* sg = E + fe * NV;
-                    for (int i = 0; i < DIM; ++i) v += sg[i] * c_Hg[((i * 3 + i) * 8 + a) * 8 + b];
-                    for (int q = 0; q < NV - DIM; ++q) {
-                        const int i = DIM == 2 ? 0 : (q == 0 ? 1 : 0), j = DIM == 2 ? 1 : (q == 2 ? 1 : 2);
-                        v += sg[DIM + q] * (c_Hg[((i * 3 + j) * 8 + a) * 8 + b] + c_Hg[((j * 3 + i) * 8 + a) * 8 + b]);
+#pragma unroll
+            for (int u = 0; u < EPT; ++u) {
+                const int t = t0 + u * NT, row = t / NL, col = t % NL;
+                if (SRC == 1) {
+                    Kc[t] = E[fe] * c_K0g[t] * fr[row] * fr[col];
+                } else {
+                    constexpr int NV = DIM == 2 ? 3 : 6;
+                    const int a = row / DIM, b = col / DIM;
+                    double v = 0.0;
+                    if (row % DIM == col % DIM) {
+                        const double* sg = E + fe * NV;
+                        for (int i = 0; i < DIM; ++i) v += sg[i] * c_Hg[((i * 3 + i) * 8 + a) * 8 + b];
+                        for (int q = 0; q < NV - DIM; ++q) {
+                            const int i = DIM == 2 ? 0 : (q == 0 ? 1 : 0), j = DIM == 2 ? 1 : (q == 2 ? 1 : 2);
+                            v += sg[DIM + q] * (c_Hg[((i * 3 + j) * 8 + a) * 8 + b] + c_Hg[((j * 3 + i) * 8 + a) * 8 + b]);
+                        }
                     }
+                    Kc[t] = v * fr[row] * fr[col];
                 }
-                Kc[t] = v * fr[row] * fr[col];
             }
         } else {
-            Kc[t] = elm_f[fe * NL * NL + t];   // already masked at level l-1
+#pragma unroll
+            for (int u = 0; u < EPT; ++u) Kc[t0 + u * NT] = elm_f[fe * NL * NL + t0 + u * NT];   // masked at l-1
         }
         __syncthreads();
         // T[(a,k),(b2,k2)] = sum_a2 Kc[(a,k),(a2,k2)] Q[a2][b2]
-        {
-            const int b2 = col / DIM, k2 = col % DIM;
-            double s = 0.0;
 #pragma unroll
-            for (int a2 = 0; a2 < NA; ++a2) s = fma(Kc[row * NL + a2 * DIM + k2], c_Q[(ch * NA + a2) * NA + b2], s);
-            T[t] = s;
+        for (int u = 0; u < EPT; ++u) {
+            const int t = t0 + u * NT, row = t / NL, col = t % NL;
+            const int b2 = col / DIM, k2 = col % DIM;
+            double sacc = 0.0;
+#pragma unroll
+            for (int a2 = 0; a2 < NA; ++a2) sacc = fma(Kc[row * NL + a2 * DIM + k2], c_Q[(ch * NA + a2) * NA + b2], sacc);
+            T[t] = sacc;
         }
         __syncthreads();
-        {
+#pragma unroll
+        for (int u = 0; u < EPT; ++u) {
+            const int t = t0 + u * NT, row = t / NL, col = t % NL;
             const int b = row / DIM, k = row % DIM;
 #pragma unroll
-            for (int a = 0; a < NA; ++a) acc = fma(c_Q[(ch * NA + a) * NA + b], T[(a * DIM + k) * NL + col], acc);
+            for (int a = 0; a < NA; ++a) acc[u] = fma(c_Q[(ch * NA + a) * NA + b], T[(a * DIM + k) * NL + col], acc[u]);
         }
         __syncthreads();
     }
@@ -200,13 +223,22 @@ __global__ void galerkin_kernel(LevelGeom gc, LevelGeom gf, const double* __rest
         for (int k = 0; k < DIM; ++k) node = node * gc.nn[k] + ci[k] + ((a >> (DIM - 1 - k)) & 1);
         return ((mask_c[node] >> comp) & 1) ? 0.0 : 1.0;
     };
-    elm_c[Ec * NL * NL + t] = acc * cfree(row) * cfree(col);
+#pragma unroll
+    for (int u = 0; u < EPT; ++u) {
+        const int t = t0 + u * NT, row = t / NL, col = t % NL;
+        elm_c[Ec * NL * NL + t] = acc[u] * cfree(row) * cfree(col);
+    }
     __syncthreads();   // shared Kc / T / fr are rewritten for the next element
     }
 }
 
+#ifndef MG_GAL3_NT
+#define MG_GAL3_NT 192   // B200 A/B (C4/C5 setup): 192 < 64 < 576 (ms)
+#endif
+static constexpr int GAL3_NT = MG_GAL3_NT;   // threads per coarse element (3D)
+
 static unsigned galerkin_grid(const LevelGeom& gc) {
-    const long long cap = 148LL * 16;
+    const long long cap = 148LL * 32;
     return (unsigned)(gc.nelem < cap ? gc.nelem : cap);
 }
 
@@ -215,11 +247,11 @@ void galerkin_elements(const LevelGeom& gc, const LevelGeom& gf, const double* E
                        const double* Mc) {
     unsigned bl = galerkin_grid(gc);
     if (gc.dim == 2) {
-        if (E) galerkin_kernel<2, 1><<<bl, 64, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, Mc);
-        else galerkin_kernel<2, 0><<<bl, 64, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, nullptr);
+        if (E) galerkin_kernel<2, 1, 64><<<bl, 64, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, Mc);
+        else galerkin_kernel<2, 0, 64><<<bl, 64, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, nullptr);
     } else {
-        if (E) galerkin_kernel<3, 1><<<bl, 576, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, Mc);
-        else galerkin_kernel<3, 0><<<bl, 576, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, nullptr);
+        if (E) galerkin_kernel<3, 1, GAL3_NT><<<bl, GAL3_NT, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, Mc);
+        else galerkin_kernel<3, 0, GAL3_NT><<<bl, GAL3_NT, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, nullptr);
     }
 }
 
@@ -227,8 +259,8 @@ void galerkin_elements(const LevelGeom& gc, const LevelGeom& gf, const double* E
 void galerkin_elements_G(const LevelGeom& gc, const LevelGeom& gf, const double* sig, const uint8_t* mask_f,
                          const uint8_t* mask_c, double* elm_c, cudaStream_t s) {
     unsigned bl = galerkin_grid(gc);
-    if (gc.dim == 2) galerkin_kernel<2, 2><<<bl, 64, 0, s>>>(gc, gf, sig, nullptr, mask_f, mask_c, elm_c, 0, nullptr);
-    else galerkin_kernel<3, 2><<<bl, 576, 0, s>>>(gc, gf, sig, nullptr, mask_f, mask_c, elm_c, 0, nullptr);
+    if (gc.dim == 2) galerkin_kernel<2, 2, 64><<<bl, 64, 0, s>>>(gc, gf, sig, nullptr, mask_f, mask_c, elm_c, 0, nullptr);
+    else galerkin_kernel<3, 2, GAL3_NT><<<bl, GAL3_NT, 0, s>>>(gc, gf, sig, nullptr, mask_f, mask_c, elm_c, 0, nullptr);
 }
 
 // M_c = Q_c^T K0 Q_c for the 2^d children (host, once per handle); layout [child][NL*NL]
