@@ -11,6 +11,8 @@
 // assembled into a per-node stencil of 3^d blocks (d x d); a coarse DOF whose
 // Galerkin diagonal is exactly 0 (P column zero on the free fine DOFs) is marked
 // fixed, which leaves the preconditioner unchanged.
+#include <cstdlib>
+
 #include "kernels.h"
 
 __constant__ double c_K0g[576];
@@ -452,12 +454,84 @@ __global__ void __launch_bounds__(128) coarse_kernel(CoarseArgs a, int r0) {
     }
 }
 
+// Small levels: one warp per (32 nodes, output component k) -- a CTA is DIM warps over the same
+// 32 nodes -- and all RB right-hand sides per thread.  Each thread reads its row k of the node's
+// 3^d blocks once (the stencil leaves HBM once instead of once per RHS) and the neighbour
+// vectors from L1; DIM x more threads than node-per-thread at the same stencil traffic.
+template <int DIM, int OP, int RB>
+__global__ void __launch_bounds__(32 * DIM) coarse_comp_kernel(CoarseArgs a, int r0) {
+    constexpr int NS = DIM == 2 ? 9 : 27;
+    const int k = threadIdx.x >> 5;
+    const long long node = (long long)blockIdx.x * 32 + (threadIdx.x & 31);
+    if (node >= a.g.nnodes) return;
+    if (a.done && *a.done) return;
+    const int n1 = a.g.nn[1], n2 = DIM == 3 ? a.g.nn[2] : 1;
+    int i0, i1, i2 = 0;
+    if (DIM == 3) {
+        i2 = (int)(node % n2);
+        const long long t = node / n2;
+        i1 = (int)(t % n1);
+        i0 = (int)(t / n1);
+    } else {
+        i1 = (int)(node % n1);
+        i0 = (int)(node / n1);
+    }
+    const int nr = min(RB, a.R - r0);
+    bool act[RB];
+#pragma unroll
+    for (int q = 0; q < RB; ++q) act[q] = (q < nr) && (!a.active || a.active[r0 + q]);
+    double acc[RB];
+#pragma unroll
+    for (int q = 0; q < RB; ++q) acc[q] = 0.0;
+    const long long nn = a.g.nnodes;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        const int d0 = DIM == 3 ? s / 9 - 1 : s / 3 - 1;
+        const int d1 = DIM == 3 ? (s / 3) % 3 - 1 : s % 3 - 1;
+        const int d2 = DIM == 3 ? s % 3 - 1 : 0;
+        const bool ok = i0 + d0 >= 0 && i0 + d0 < a.g.nn[0] && i1 + d1 >= 0 && i1 + d1 < n1 &&
+                        (DIM == 2 || (i2 + d2 >= 0 && i2 + d2 < n2));
+        if (!ok) continue;
+        const long long q = node + ((long long)d0 * n1 + d1) * n2 + d2;
+        double blk[DIM];
+#pragma unroll
+        for (int k2 = 0; k2 < DIM; ++k2) blk[k2] = a.st[(long long)((s * DIM + k) * DIM + k2) * nn + node];
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr) {
+            if (!act[rr]) continue;
+            const double* xv = a.x + (long long)(r0 + rr) * a.g.ndof + (long long)DIM * q;
+#pragma unroll
+            for (int k2 = 0; k2 < DIM; ++k2) acc[rr] = fma(blk[k2], __ldg(xv + k2), acc[rr]);
+        }
+    }
+#pragma unroll
+    for (int rr = 0; rr < RB; ++rr) {
+        if (!act[rr]) continue;
+        const long long o = (long long)(r0 + rr) * a.g.ndof + (long long)DIM * node + k;
+        double v;
+        if (OP == COP_MATVEC) v = acc[rr];
+        else if (OP == COP_RESID) v = a.b[o] - acc[rr];
+        else v = a.x[o] + a.omega * a.Dinv[(long long)DIM * node + k] * (a.b[o] - acc[rr]);
+        a.y[o] = v;
+    }
+}
+
 template <int DIM, int OP>
 static void launch_coarse_dim(const CoarseArgs& a, cudaStream_t s) {
     int th = 128;
     unsigned bl = (unsigned)((a.g.nnodes + th - 1) / th);
-    if (bl < 2 * 148) {   // small level: one RHS per thread, RHS over grid.y (stencil from L2)
-        coarse_kernel<DIM, OP, 1><<<dim3(bl, a.R), th, 0, s>>>(a, 0);
+    if (bl < 2 * 148) {   // small level: warp per (32 nodes, component), all RHS per thread
+        static const bool comp = !getenv("MG_COARSE_COMP") || atoi(getenv("MG_COARSE_COMP")) != 0;
+        if (!comp) {   // former path: one RHS per thread, RHS over grid.y (stencil from L2)
+            coarse_kernel<DIM, OP, 1><<<dim3(bl, a.R), th, 0, s>>>(a, 0);
+            return;
+        }
+        const unsigned bc = (unsigned)((a.g.nnodes + 31) / 32);
+        for (int r0 = 0; r0 < a.R; r0 += 8) {
+            if (a.R - r0 > 4) coarse_comp_kernel<DIM, OP, 8><<<bc, 32 * DIM, 0, s>>>(a, r0);
+            else if (a.R - r0 > 1) coarse_comp_kernel<DIM, OP, 4><<<bc, 32 * DIM, 0, s>>>(a, r0);
+            else coarse_comp_kernel<DIM, OP, 1><<<bc, 32 * DIM, 0, s>>>(a, r0);
+        }
         return;
     }
     for (int r0 = 0; r0 < a.R;) {
