@@ -143,6 +143,37 @@ def test_galerkin_levels_match_triple_product(name):
     assert np.abs(Ai.cpu().numpy() - ref).max() < 1e-9 * np.abs(ref).max()
 
 
+def test_coarse_inverse_large_level():
+    """Coarsest level as large as C5's (4131 DOFs, padded 4160): the Gauss-Jordan path that folds
+    the next diagonal block into the DMMA update kernel, against numpy's inverse."""
+    import paper_1909_13585_b200 as mg
+    name = "T3e"
+    cfg, inp, K = case(name)
+    H = omg.Hierarchy(cfg.nel, K, inp["fixed"], cfg.levels)
+    h = handle(name)
+    nL = H.A[-1].shape[0]
+    assert nL >= 3072
+    Ai = torch.empty((nL, nL), dtype=torch.float64, device=DEV)
+    mg.mg_get_coarse_inverse(h, Ai)
+    ref = np.linalg.inv(H.A[-1].toarray())
+    assert np.abs(Ai.cpu().numpy() - ref).max() < 1e-9 * np.abs(ref).max()
+
+
+def test_vcycle_many_rhs_matches_oracle():
+    """40 right-hand sides (> 32: the dense coarsest apply runs in two RHS chunks)."""
+    import paper_1909_13585_b200 as mg
+    name = "T3a"
+    cfg, inp, K = case(name)
+    H = omg.Hierarchy(cfg.nel, K, inp["fixed"], cfg.levels)
+    V = solve._VCycle(H, 0.6, 1)
+    h = handle(name)
+    A = rough_vectors(cfg, 40, seed_offset=41, masked=True)
+    Z = torch.empty((40, A.shape[1]), dtype=torch.float64, device=DEV)
+    mg.mg_vcycle(h, to_dev(A), Z)
+    Zo = np.stack([V.apply(a) for a in A])
+    assert rel(Z.cpu().numpy(), Zo).max() < 1e-9
+
+
 @pytest.mark.parametrize("name", ["T2b", "T3a"])
 def test_vcycle_symmetric_positive(name):
     import paper_1909_13585_b200 as mg

@@ -56,6 +56,8 @@ CONFIGS = {
     "T3b": Config("T3b", (24, 12, 12), 3, 3, load="edge", nphi=2, seed=3002),
     "T3c": Config("T3c", (40, 24, 16), 2, 3, nphi=2, seed=3003),       # ragged tiles
     "T3d": Config("T3d", (48, 24, 24), 7, 4, load="edge", nphi=2, seed=3004),
+    # coarsest level of C5's size (n_L = 4131 -> padded 4160): the large-level Gauss-Jordan path
+    "T3e": Config("T3e", (32, 16, 16), 2, 2, seed=3005),
 }
 
 
