@@ -18,7 +18,11 @@
 
 #include "kernels.h"
 
-static constexpr int CT_I = 16, CT_J = 32;   // thread tile (level-l nodes)
+#ifndef MG_C2D_TJ
+#define MG_C2D_TJ 32   // thread tile 16 x TJ level-l nodes (TJ = 32: 1 CTA/SM, 16: 2 CTAs/SM)
+#endif
+static constexpr int CT_I = 16, CT_J = MG_C2D_TJ;   // thread tile (level-l nodes)
+static constexpr int C2D_MINB = CT_J == 32 ? 1 : 2;
 static constexpr int NSR = 3;                // right-hand sides in flight (cp.async ring)
 
 __device__ __forceinline__ void cpa16c(void* dst, const void* src, bool pred) {
@@ -28,8 +32,8 @@ __device__ __forceinline__ void cpa16c(void* dst, const void* src, bool pred) {
 __device__ __forceinline__ void cpa_commit_c() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cpa_wait_c() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NSR - 1)); }
 __device__ __forceinline__ void cpa_wait_all_c() { asm volatile("cp.async.wait_group 0;\n" ::); }
-static constexpr int DN_CI = 6, DN_CJ = 14;  // coarse nodes owned by a down CTA
-static constexpr int UP_OI = 14, UP_OJ = 30; // level-l nodes owned by an up CTA
+static constexpr int DN_CI = CT_I / 2 - 2, DN_CJ = CT_J / 2 - 2;  // coarse nodes owned by a down CTA
+static constexpr int UP_OI = CT_I - 2, UP_OJ = CT_J - 2;          // level-l nodes owned by an up CTA
 
 __device__ __forceinline__ void load_stencil(const double* __restrict__ st, long long nn, long long node, bool ok,
                                              double (&A)[36]) {
@@ -52,7 +56,7 @@ __device__ __forceinline__ void apply_stencil(const double (&A)[36], const doubl
     }
 }
 
-__global__ void __launch_bounds__(CT_I * CT_J, 1) coarse2d_down_kernel(LevelGeom g, LevelGeom gc,
+__global__ void __launch_bounds__(CT_I * CT_J, C2D_MINB) coarse2d_down_kernel(LevelGeom g, LevelGeom gc,
                                                                        const double* __restrict__ st,
                                                                        const double* __restrict__ Dinv,
                                                                        const uint8_t* __restrict__ mask,
@@ -132,7 +136,7 @@ __global__ void __launch_bounds__(CT_I * CT_J, 1) coarse2d_down_kernel(LevelGeom
     cpa_wait_all_c();
 }
 
-__global__ void __launch_bounds__(CT_I * CT_J, 1) coarse2d_up_kernel(LevelGeom g, LevelGeom gc,
+__global__ void __launch_bounds__(CT_I * CT_J, C2D_MINB) coarse2d_up_kernel(LevelGeom g, LevelGeom gc,
                                                                      const double* __restrict__ st,
                                                                      const double* __restrict__ Dinv,
                                                                      const uint8_t* __restrict__ mask,
