@@ -160,7 +160,7 @@ __device__ __forceinline__ void gj_block_inverse_smem(double (*S)[GJ_NB + 1], in
     constexpr int PE = GJ_NB * GJ_NB / NT;
     for (int p = 0; p < GJ_NB; ++p) {
         const double piv = S[p][p];
-        const double ip = 1.0 / piv;
+        const double ip = __drcp_rn(piv);   // correctly rounded reciprocal, no division slow path
         double v[PE];
 #pragma unroll
         for (int q = 0; q < PE; ++q) {
@@ -181,13 +181,40 @@ __device__ __forceinline__ void gj_block_inverse_smem(double (*S)[GJ_NB + 1], in
     }
 }
 
+// The standalone pivot-block inverse (1024 threads, one entry each) pivots on 2x2 blocks: half the
+// barrier pairs of the scalar sweep; the 2x2 pivot inverse is closed-form in every thread.
 __global__ void __launch_bounds__(1024) gj_diag_kernel(const double* A, long long ld, int k0, double* P, int* status) {
     __shared__ double S[GJ_NB][GJ_NB + 1];
-    const int e = threadIdx.x;
-    S[e / GJ_NB][e % GJ_NB] = A[(k0 + e / GJ_NB) * ld + k0 + e % GJ_NB];
+    const int e = threadIdx.x, i = e / GJ_NB, j = e % GJ_NB;
+    S[i][j] = A[(k0 + i) * ld + k0 + j];
     __syncthreads();
-    gj_block_inverse_smem<1024>(S, threadIdx.x, status);
-    P[e] = S[e / GJ_NB][e % GJ_NB];
+    for (int b = 0; b < GJ_NB; b += 2) {
+        const double a00 = S[b][b], a01 = S[b][b + 1], a10 = S[b + 1][b], a11 = S[b + 1][b + 1];
+        const double det = a00 * a11 - a01 * a10;
+        if (e == 0 && !(a00 > 0.0 && det > 0.0)) atomicOr(status, 2);
+        const double id = __drcp_rn(det);
+        const double q00 = a11 * id, q01 = -a01 * id, q10 = -a10 * id, q11 = a00 * id;
+        const int ri = i - b, rj = j - b;
+        const bool ip = ri == 0 || ri == 1, jp = rj == 0 || rj == 1;
+        double v;
+        if (ip && jp) {
+            v = ri == 0 ? (rj == 0 ? q00 : q01) : (rj == 0 ? q10 : q11);
+        } else if (ip) {
+            const double s0 = S[b][j], s1 = S[b + 1][j];
+            v = ri == 0 ? fma(q00, s0, q01 * s1) : fma(q10, s0, q11 * s1);
+        } else if (jp) {
+            const double s0 = S[i][b], s1 = S[i][b + 1];
+            v = rj == 0 ? -fma(s0, q00, s1 * q10) : -fma(s0, q01, s1 * q11);
+        } else {
+            const double c0 = S[i][b], c1 = S[i][b + 1], r0 = S[b][j], r1 = S[b + 1][j];
+            const double u0 = fma(q00, r0, q01 * r1), u1 = fma(q10, r0, q11 * r1);
+            v = S[i][j] - fma(c0, u0, c1 * u1);
+        }
+        __syncthreads();
+        S[i][j] = v;
+        __syncthreads();
+    }
+    P[e] = S[i][j];
 }
 
 __global__ void __launch_bounds__(128) gj_update_mma_kernel(double* A, long long ld, long long n, const double* Ccol,
@@ -322,6 +349,12 @@ static bool gj_mma() {
 
 static constexpr long long GJ_FOLD_N = 3072;
 
+int dense_spd_inverse_launches(long long npad) {
+    const long long steps = npad / GJ_NB;
+    const bool fold = gj_mma() && npad >= GJ_FOLD_N;
+    return (int)(fold ? 3 * steps + 1 : 4 * steps);
+}
+
 void dense_spd_inverse(double* A, long long npad, double* work, int* d_status, cudaStream_t s) {
     double* Pb[2] = {work, work + GJ_NB * GJ_NB};   // ping-pong: block k's inverse, next block's
     double* Rrow = work + 2 * GJ_NB * GJ_NB;
@@ -345,9 +378,6 @@ void dense_spd_inverse(double* A, long long npad, double* work, int* d_status, c
     }
 }
 
-// z[r][i] = sum_j Ainv[i][j] rvec[r][j]: 4 rows per CTA (one warp each), the RB right-hand
-// sides staged through shared memory in column chunks so every Ainv row is streamed once and
-// the vectors come from shared memory (Ainv and the vectors are L2-resident, n_L <= ~4k).
 // z[q][i] = sum_j Ainv[i][j] r[q][j] for the RB right-hand sides q of this chunk.  A CTA owns
 // RW = 32 / RB rows; its 8 warps split the columns, every lane accumulates RW x RB = 32 partial
 // sums (one A load per row and one r load per RHS per column: RW RB FMAs per RW + RB loads).

@@ -169,6 +169,7 @@ void dense_pad_identity(double* A, long long n, long long npad, cudaStream_t s);
 // In-place SPD inverse by blocked Gauss-Jordan (block 32). Work buffers sized npad*32*2 + 32*32.
 // Returns via *d_status (device int) nonzero if a non-positive pivot is met.
 void dense_spd_inverse(double* A, long long npad, double* work, int* d_status, cudaStream_t s);
+int dense_spd_inverse_launches(long long npad);   // kernels dense_spd_inverse launches
 void dense_apply(const double* Ainv, long long ld, long long n, const double* r, double* z, int R,
                  const int* active, const int* done, cudaStream_t s);
 

@@ -279,6 +279,7 @@ struct mg_ctx {
     int* brank = nullptr;
     int block_R = 0;
     cudaGraphExec_t g_block = nullptr;
+    cudaGraphExec_t g_gj = nullptr;   // coarsest assembly + Gauss-Jordan inverse (fixed shapes per handle)
     double block_tol = -1.0;
     double* xtmp = nullptr;                      // NCCL reverse-add receive buffer
     long long xtmp_cap = 0;
@@ -544,12 +545,22 @@ static mg_status compute_operators(mg_ctx* c) {
                             ns * dim * dim, c->stg, gL.nnodes));
         stc = c->stg;
     }
-    CU(cudaMemsetAsync(c->Ainv, 0, sizeof(double) * c->npad * c->npad, s));
-    dense_from_stencil(gL, stc, c->Ainv, c->npad, s);
-    dense_pad_identity(c->Ainv, c->nL, c->npad, s);
-    CU(cudaMemsetAsync(c->gj_work, 0, sizeof(double) * (2 * 32 * 32 + 2 * c->npad * 32), s));
-    dense_spd_inverse(c->Ainv, c->npad, c->gj_work, c->d_status, s);
-    c->launches += 2 + 5 * (c->npad / 32);
+    // ~4 launches per 32-column block step: captured once into a graph (the shapes and buffers are
+    // fixed for the handle) so a setup pays graph-node rather than stream-launch overhead
+    if (!c->g_gj) {
+        CU(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        cudaMemsetAsync(c->Ainv, 0, sizeof(double) * c->npad * c->npad, s);
+        dense_from_stencil(gL, stc, c->Ainv, c->npad, s);
+        dense_pad_identity(c->Ainv, c->nL, c->npad, s);
+        cudaMemsetAsync(c->gj_work, 0, sizeof(double) * (2 * 32 * 32 + 2 * c->npad * 32), s);
+        dense_spd_inverse(c->Ainv, c->npad, c->gj_work, c->d_status, s);
+        cudaGraph_t gg = nullptr;
+        CU(cudaStreamEndCapture(s, &gg));
+        CU(cudaGraphInstantiate(&c->g_gj, gg, 0));
+        CU(cudaGraphDestroy(gg));
+    }
+    CU(cudaGraphLaunch(c->g_gj, s));
+    c->launches += (c->npad > c->nL ? 2 : 1) + dense_spd_inverse_launches(c->npad);
     CHECK_LAUNCH();
     int st[1] = {0};
     CU(cudaMemcpyAsync(st, c->d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -2340,6 +2351,7 @@ mg_status mg_destroy(mg_handle c) {
     if (c->ctl_mem) cudaFree(c->ctl_mem);
     if (c->brank) cudaFree(c->brank);
     if (c->g_block) cudaGraphExecDestroy(c->g_block);
+    if (c->g_gj) cudaGraphExecDestroy(c->g_gj);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
     if (c->h_dbl) cudaFreeHost(c->h_dbl);
     if (c->ev_in) cudaEventDestroy(c->ev_in);

@@ -1,5 +1,5 @@
 #!/bin/bash
-O=gpurun_out/h8ab; mkdir -p $O
+O=gpurun_out/h8ab2; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1 || exit 1
 timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "h8 or 3d or fused3d or T3" > $O/tests.log 2>&1; echo "rc=$?" >> $O/tests.log
 for C in C4 C5; do timeout 300 python bench.py --config $C --no-cpu --no-e2e --steps 5 > $O/${C}_default.json 2>&1
