@@ -295,8 +295,8 @@ struct ARing {
     double2 d[CGP ? 1 : NSTAGE][32];
     double e[NSTAGE][32];
     unsigned m[NSTAGE][32];                 // aligned 4-byte word holding the mask byte
-    double2 c0[POST ? NSTAGE : 1][32], c1[POST ? NSTAGE : 1][32];
-    unsigned cm0[CGP ? 1 : NSTAGE][32], cm1[POST ? NSTAGE : 1][32];
+    double2 c0[POST ? NSTAGE : 1][32];       // coarse node J0 = c >> 1 (J1's value comes from lane + 1)
+    unsigned cm0[CGP ? 1 : NSTAGE][32];
 };
 
 // SLAB = false: single slab (off0 = 0, every plane owned) -- the slab checks compile away
@@ -406,11 +406,9 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
             const int I = (Ps + 1) >> 1;
             const bool pr = (Ps & 1) && cin && I < a.gc.nn[0];
             const long long row = (long long)(pr ? I : 0) * nc1;
-            const long long j0 = pr ? J0 : 0, j1 = pr ? J1 : 0;
+            const long long j0 = pr ? J0 : 0;
             cpa16(&AR.c0[st][lane], a.ec + vbc + 2 * (row + j0), pr);
-            cpa16(&AR.c1[st][lane], a.ec + vbc + 2 * (row + j1), pr);
             cpa4(&AR.cm0[st][lane], reinterpret_cast<const uint8_t*>((uintptr_t)(a.maskc + row + j0) & ~(uintptr_t)3), pr);
-            cpa4(&AR.cm1[st][lane], reinterpret_cast<const uint8_t*>((uintptr_t)(a.maskc + row + j1) & ~(uintptr_t)3), pr);
         }
         if (OP == M2_RESTRICT) {
             const int I = (Ps - 1) >> 1;
@@ -435,16 +433,16 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
         if (OP == M2_POST) {
             const int I = (Ps + 1) >> 1;
             const bool pr = (Ps & 1) && cin && I < a.gc.nn[0];
-            s.cx0 = s.cy0 = s.cx1 = s.cy1 = 0.0;
+            s.cx0 = s.cy0 = 0.0;
             if (pr) {
-                const long long row = (long long)I * nc1;
-                const unsigned rowu = (unsigned)I * (unsigned)nc1;
-                const int m0 = byte_of(AR.cm0[st][lane], rowu + J0);
-                const int m1 = byte_of(AR.cm1[st][lane], rowu + J1);
-                const double2 e0 = AR.c0[st][lane], e1 = AR.c1[st][lane];
+                const int m0 = byte_of(AR.cm0[st][lane], (unsigned)I * (unsigned)nc1 + J0);
+                const double2 e0 = AR.c0[st][lane];
                 s.cx0 = (m0 & 1) ? 0.0 : e0.x; s.cy0 = (m0 & 2) ? 0.0 : e0.y;
-                s.cx1 = (m1 & 1) ? 0.0 : e1.x; s.cy1 = (m1 & 2) ? 0.0 : e1.y;
             }
+            // J1 = (c + 1) >> 1 is lane + 1's J0 when c is odd (c + 1 <= N1 is inside), else J0
+            const double nx = shfl_dn1(s.cx0), ny = shfl_dn1(s.cy0);
+            s.cx1 = (c & 1) ? nx : s.cx0;
+            s.cy1 = (c & 1) ? ny : s.cy0;
         }
         if (OP == M2_RESTRICT) {
             const int I = (Ps - 1) >> 1;
