@@ -77,11 +77,11 @@ __global__ void __launch_bounds__(CT_I * CT_J, C2D_MINB) coarse2d_down_kernel(Le
     const int n0 = g.nn[0], n1 = g.nn[1];
     const bool ok = fi >= 0 && fi < n0 && fj >= 0 && fj < n1;
     const long long node = (long long)fi * n1 + fj;
+    const bool wreg = ti >= 1 && ti < CT_I - 1 && tj >= 1 && tj < CT_J - 1;
     double A[36];
-    load_stencil(st, g.nnodes, node, ok, A);
+    load_stencil(st, g.nnodes, node, ok && wreg, A);   // the halo ring only supplies z1
     const int m = ok ? mask[node] : 3;
     const double dx = ok ? Dinv[2 * node] : 0.0, dy = ok ? Dinv[2 * node + 1] : 0.0;
-    const bool wreg = ti >= 1 && ti < CT_I - 1 && tj >= 1 && tj < CT_J - 1;
     // restriction source: slab-owned, free fine DOFs
     const bool src = ok && fi >= fo0 && fi < fo1;
     // coarse owner: ti = 2 + 2a, tj = 2 + 2b
@@ -159,11 +159,11 @@ __global__ void __launch_bounds__(CT_I * CT_J, C2D_MINB) coarse2d_up_kernel(Leve
     const int n0 = g.nn[0], n1 = g.nn[1];
     const bool ok = fi >= 0 && fi < n0 && fj >= 0 && fj < n1;
     const long long node = (long long)fi * n1 + fj;
+    const bool own = ok && ti >= 1 && ti < CT_I - 1 && tj >= 1 && tj < CT_J - 1;
     double A[36];
-    load_stencil(st, g.nnodes, node, ok, A);
+    load_stencil(st, g.nnodes, node, own, A);   // the halo ring only supplies z2
     const int m = ok ? mask[node] : 3;
     const double dx = ok ? Dinv[2 * node] : 0.0, dy = ok ? Dinv[2 * node + 1] : 0.0;
-    const bool own = ok && ti >= 1 && ti < CT_I - 1 && tj >= 1 && tj < CT_J - 1;
     // coarse tile: shifted fine index fs = f + off0 maps to coarse fs >> 1 (floor) .. (fs + 1) >> 1
     const int ci0 = (fi0 + off0) >> 1, cj0 = fj0 >> 1;
     const int fsi = fi + off0;
