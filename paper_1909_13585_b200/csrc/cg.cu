@@ -4,7 +4,17 @@
 //   ||r_k|| <= tol ||b_k|| ; beta_k = (r.z)_new / (r.z)_old ; p = z + beta p.
 // Dot products: per-warp shuffle reductions written to a partial array, then
 // summed in a fixed order by `cg_scalars` (deterministic, no atomics).
+#include <cstdlib>
+
 #include "kernels.h"
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("MG_PDL");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return on;
+}
 
 #define MG_MAX_RHS_DEV 64
 
@@ -33,6 +43,7 @@ __device__ __forceinline__ void block_partial(double v, double* partial, long lo
 // z = omega Dinv r
 __global__ void jacobi0_kernel(long long n, const double* __restrict__ r, const double* __restrict__ Dinv,
                                double omega, double* __restrict__ z, const int* active, const int* done) {
+    pdl_begin();
     const int rr = blockIdx.y;
     if (done && *done) return;
     if (active && !active[rr]) return;
@@ -44,7 +55,7 @@ __global__ void jacobi0_kernel(long long n, const double* __restrict__ r, const 
 void cg_pointwise_jacobi(long long n, int R, const double* r, const double* Dinv, double omega, double* z,
                          const int* active, const int* done, cudaStream_t s) {
     dim3 g(vec_blocks(n), R);
-    jacobi0_kernel<<<g, VEC_THREADS, 0, s>>>(n, r, Dinv, omega, z, active, done);
+    launch_kp(false, jacobi0_kernel, dim3(g), dim3(VEC_THREADS), 0, s, n, r, Dinv, omega, z, active, done);
 }
 
 // partial[rr * pstride + block] = sum over i in [d0, d1) of a[rr][i] b[rr][i]  (vectors of stride n)
@@ -113,6 +124,7 @@ void vec_axpy_masked_restart(long long n, int R, const double* t, double* r, con
 // the scalar CG logic runs per RHS.
 __global__ void __launch_bounds__(512) scalars_kernel(int mode, int R, const double* __restrict__ partial, int items,
                                                       long long pstride, CgCtl c, double tol, int aux) {
+    pdl_begin();
     __shared__ int any_active;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if (threadIdx.x == 0) any_active = 0;
@@ -182,7 +194,7 @@ __global__ void __launch_bounds__(512) scalars_kernel(int mode, int R, const dou
 
 void cg_scalars(int mode, int R, const double* partial, int items, CgCtl c, double tol, cudaStream_t s, int aux,
                 long long pstride) {
-    scalars_kernel<<<1, 512, 0, s>>>(mode, R, partial, items, pstride < 0 ? items : pstride, c, tol, aux);
+    launch_k(scalars_kernel, dim3(1), dim3(512), 0, s, mode, R, partial, items, pstride < 0 ? items : pstride, c, tol, aux);
 }
 
 // sums[r] = sum_i partial[r * pstride + i], i < items (fixed order; multi-rank dots are then
@@ -210,6 +222,7 @@ __global__ void __launch_bounds__(VEC_THREADS) rupdate_kernel(long long n, const
                                                               double* __restrict__ z1, double* partial,
                                                               long long pstride, long long d0, long long d1,
                                                               const int* active, const int* done) {
+    pdl_begin();
     const int rr = blockIdx.y;
     if (done && *done) return;
     if (active && !active[rr]) return;
@@ -230,7 +243,7 @@ int cg_rupdate(long long n, int R, const double* alpha, const double* rin, const
                long long d1, const int* active, const int* done, cudaStream_t s) {
     const int nb = vec_blocks(n);
     dim3 g(nb, R);
-    rupdate_kernel<<<g, VEC_THREADS, 0, s>>>(n, alpha, rin, q, rout, Dinv, omega, z1, partial, pstride, d0, d1,
+    launch_kp(false, rupdate_kernel, dim3(g), dim3(VEC_THREADS), 0, s, n, alpha, rin, q, rout, Dinv, omega, z1, partial, pstride, d0, d1,
                                               active, done);
     return nb;
 }

@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(CT_I * CT_J, C2D_MINB) coarse2d_down_kernel(Le
                                                                        int R, double omega, int off0, int fo0, int fo1,
                                                                        int nbj, int rg, const int* active,
                                                                        const int* done) {
+    pdl_begin();
     __shared__ double2 s_z[CT_I][CT_J];
     __shared__ double2 s_w[CT_I][CT_J];
     __shared__ double2 s_r[NSR][CT_I * CT_J];   // r of the next RHS, per thread
@@ -145,6 +146,7 @@ __global__ void __launch_bounds__(CT_I * CT_J, C2D_MINB) coarse2d_up_kernel(Leve
                                                                      const double* __restrict__ ec, double* z, int R,
                                                                      double omega, int off0, int nbj, int rg,
                                                                      const int* active, const int* done) {
+    pdl_begin();
     constexpr int CI = CT_I / 2 + 2, CJ = CT_J / 2 + 2;
     __shared__ double2 s_z[CT_I][CT_J];
     __shared__ double2 s_e[CI][CJ];
@@ -241,7 +243,7 @@ void coarse2d_down(const LevelGeom& g, const LevelGeom& gc, const double* st, co
     const int nbi = (gc.nn[0] + DN_CI - 1) / DN_CI, nbj = (gc.nn[1] + DN_CJ - 1) / DN_CJ;
     const int rg = rhs_group(nbi * nbj, R);
     dim3 grid(nbi * nbj, (R + rg - 1) / rg);
-    coarse2d_down_kernel<<<grid, CT_I * CT_J, 0, s>>>(g, gc, st, Dinv, mask, maskc, r, rc, R, omega, off0, fo0, fo1,
+    launch_k(coarse2d_down_kernel, dim3(grid), dim3(CT_I * CT_J), 0, s, g, gc, st, Dinv, mask, maskc, r, rc, R, omega, off0, fo0, fo1,
                                                     nbj, rg, active, done);
 }
 
@@ -251,6 +253,6 @@ void coarse2d_up(const LevelGeom& g, const LevelGeom& gc, const double* st, cons
     const int nbi = (g.nn[0] + UP_OI - 1) / UP_OI, nbj = (g.nn[1] + UP_OJ - 1) / UP_OJ;
     const int rg = rhs_group(nbi * nbj, R);
     dim3 grid(nbi * nbj, (R + rg - 1) / rg);
-    coarse2d_up_kernel<<<grid, CT_I * CT_J, 0, s>>>(g, gc, st, Dinv, mask, maskc, r, ec, z, R, omega, off0, nbj, rg,
+    launch_k(coarse2d_up_kernel, dim3(grid), dim3(CT_I * CT_J), 0, s, g, gc, st, Dinv, mask, maskc, r, ec, z, R, omega, off0, nbj, rg,
                                                   active, done);
 }

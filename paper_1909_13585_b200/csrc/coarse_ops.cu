@@ -388,6 +388,7 @@ void stencil_diag(const LevelGeom& g, const double* /*st*/, uint8_t* mask, doubl
 // unrolled (compile-time offsets, no local-memory index arrays).
 template <int DIM, int OP, int RB>
 __global__ void __launch_bounds__(128) coarse_kernel(CoarseArgs a, int r0) {
+    pdl_begin();
     constexpr int NS = DIM == 2 ? 9 : 27;
     r0 += blockIdx.y * RB;   // small levels: RHS groups spread over grid.y
     long long node = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -460,6 +461,7 @@ __global__ void __launch_bounds__(128) coarse_kernel(CoarseArgs a, int r0) {
 // vectors from L1; DIM x more threads than node-per-thread at the same stencil traffic.
 template <int DIM, int OP, int RB>
 __global__ void __launch_bounds__(32 * DIM) coarse_comp_kernel(CoarseArgs a, int r0) {
+    pdl_begin();
     constexpr int NS = DIM == 2 ? 9 : 27;
     const int k = threadIdx.x >> 5;
     const long long node = (long long)blockIdx.x * 32 + (threadIdx.x & 31);
@@ -523,30 +525,30 @@ static void launch_coarse_dim(const CoarseArgs& a, cudaStream_t s) {
     if (bl < 2 * 148) {   // small level: warp per (32 nodes, component), all RHS per thread
         static const bool comp = !getenv("MG_COARSE_COMP") || atoi(getenv("MG_COARSE_COMP")) != 0;
         if (!comp) {   // former path: one RHS per thread, RHS over grid.y (stencil from L2)
-            coarse_kernel<DIM, OP, 1><<<dim3(bl, a.R), th, 0, s>>>(a, 0);
+            launch_kp(false, coarse_kernel<DIM, OP, 1>, dim3(dim3(bl, a.R)), dim3(th), 0, s, a, 0);
             return;
         }
         const unsigned bc = (unsigned)((a.g.nnodes + 31) / 32);
         for (int r0 = 0; r0 < a.R; r0 += 8) {
-            if (a.R - r0 > 4) coarse_comp_kernel<DIM, OP, 8><<<bc, 32 * DIM, 0, s>>>(a, r0);
-            else if (a.R - r0 > 1) coarse_comp_kernel<DIM, OP, 4><<<bc, 32 * DIM, 0, s>>>(a, r0);
-            else coarse_comp_kernel<DIM, OP, 1><<<bc, 32 * DIM, 0, s>>>(a, r0);
+            if (a.R - r0 > 4) launch_kp(false, coarse_comp_kernel<DIM, OP, 8>, dim3(bc), dim3(32 * DIM), 0, s, a, r0);
+            else if (a.R - r0 > 1) launch_kp(false, coarse_comp_kernel<DIM, OP, 4>, dim3(bc), dim3(32 * DIM), 0, s, a, r0);
+            else launch_kp(false, coarse_comp_kernel<DIM, OP, 1>, dim3(bc), dim3(32 * DIM), 0, s, a, r0);
         }
         return;
     }
     for (int r0 = 0; r0 < a.R;) {
         int rem = a.R - r0;
         if (rem > 8) {
-            coarse_kernel<DIM, OP, 16><<<bl, th, 0, s>>>(a, r0);
+            launch_kp(false, coarse_kernel<DIM, OP, 16>, dim3(bl), dim3(th), 0, s, a, r0);
             r0 += 16;
         } else if (rem > 4) {
-            coarse_kernel<DIM, OP, 8><<<bl, th, 0, s>>>(a, r0);
+            launch_kp(false, coarse_kernel<DIM, OP, 8>, dim3(bl), dim3(th), 0, s, a, r0);
             r0 += 8;
         } else if (rem > 1) {
-            coarse_kernel<DIM, OP, 4><<<bl, th, 0, s>>>(a, r0);
+            launch_kp(false, coarse_kernel<DIM, OP, 4>, dim3(bl), dim3(th), 0, s, a, r0);
             r0 += 4;
         } else {
-            coarse_kernel<DIM, OP, 1><<<bl, th, 0, s>>>(a, r0);
+            launch_kp(false, coarse_kernel<DIM, OP, 1>, dim3(bl), dim3(th), 0, s, a, r0);
             r0 += 1;
         }
     }

@@ -40,3 +40,40 @@ __device__ __forceinline__ double warp_sum(double v) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(MGK_FULL, v, o);
     return v;
 }
+
+// ---- programmatic dependent launch (PDL) for the kernels of the CG iteration graphs.
+// A kernel launched with launch_k() may start while its predecessor in the stream is finishing:
+// its first statement is pdl_begin(), which waits until the predecessor grid has completed and
+// its memory is visible (griddepcontrol.wait), then lets the next dependent grid begin launching
+// (griddepcontrol.launch_dependents).  Launch latency overlaps the previous kernel's tail; the
+// data dependencies are unchanged.  Outside a PDL launch both instructions are no-ops.  Used for
+// the 2D iteration (march2, coarse2d) and the small scalar / dense kernels: B200 C1 -5%, C2 -3%;
+// the 3D kernels (H8, stencil, transfers, r update) launch without it -- early-resident dependents
+// of their large grids cost the 3D configs ~1%.
+__device__ __forceinline__ void pdl_begin() {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
+bool pdl_enabled();   // MG_PDL (default 1)
+
+template <typename... KArgs, typename... Args>
+inline void launch_kp(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                      Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = (pdl && pdl_enabled()) ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    launch_kp(true, kern, grid, block, smem, s, args...);
+}

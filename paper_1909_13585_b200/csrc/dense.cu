@@ -390,6 +390,7 @@ __global__ void __launch_bounds__(32 * DA_WARPS) dense_apply_kernel(const double
                                                                     long long n, const double* __restrict__ rv,
                                                                     double* __restrict__ z, int R, int r0,
                                                                     const int* active, const int* done) {
+    pdl_begin();
     constexpr int RW = 32 / RB;
     __shared__ double red[DA_WARPS][32];
     if (done && *done) return;
@@ -445,11 +446,11 @@ void dense_apply(const double* Ainv, long long ld, long long n, const double* r,
         const int rb = rem > 16 ? 32 : rem > 8 ? 16 : rem > 4 ? 8 : rem > 1 ? 4 : 1;
         const unsigned bl = (unsigned)((n + 32 / rb - 1) / (32 / rb));
         switch (rb) {
-            case 32: dense_apply_kernel<32><<<bl, 32 * DA_WARPS, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); break;
-            case 16: dense_apply_kernel<16><<<bl, 32 * DA_WARPS, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); break;
-            case 8: dense_apply_kernel<8><<<bl, 32 * DA_WARPS, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); break;
-            case 4: dense_apply_kernel<4><<<bl, 32 * DA_WARPS, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); break;
-            default: dense_apply_kernel<1><<<bl, 32 * DA_WARPS, 0, s>>>(Ainv, ld, n, r, z, R, r0, active, done); break;
+            case 32: launch_k(dense_apply_kernel<32>, dim3(bl), dim3(32 * DA_WARPS), 0, s, Ainv, ld, n, r, z, R, r0, active, done); break;
+            case 16: launch_k(dense_apply_kernel<16>, dim3(bl), dim3(32 * DA_WARPS), 0, s, Ainv, ld, n, r, z, R, r0, active, done); break;
+            case 8: launch_k(dense_apply_kernel<8>, dim3(bl), dim3(32 * DA_WARPS), 0, s, Ainv, ld, n, r, z, R, r0, active, done); break;
+            case 4: launch_k(dense_apply_kernel<4>, dim3(bl), dim3(32 * DA_WARPS), 0, s, Ainv, ld, n, r, z, R, r0, active, done); break;
+            default: launch_k(dense_apply_kernel<1>, dim3(bl), dim3(32 * DA_WARPS), 0, s, Ainv, ld, n, r, z, R, r0, active, done); break;
         }
         r0 += rb;
     }

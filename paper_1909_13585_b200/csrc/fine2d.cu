@@ -302,6 +302,7 @@ struct ARing {
 // SLAB = false: single slab (off0 = 0, every plane owned) -- the slab checks compile away
 template <int OP, bool C03, bool SLAB>
 __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2Args a, int nct, int nch, int chl) {
+    pdl_begin();
     constexpr int CS = (OP == M2_RESTRICT) ? 28 : 30;      // owned columns per warp
     // lane of the first owned column; lane 0 sits at an odd column for every op, which with
     // pad2_layout's odd org and pitch % 4 == 0 makes each warp's 512-byte plane row 32-byte aligned
@@ -788,11 +789,11 @@ static void launch2(const March2Args& a, bool c03, cudaStream_t s) {
     const unsigned blocks = (unsigned)((warps + WPB - 1) / WPB);
     const bool slab = a.off0 != 0 || a.so0 != 0 || a.so1 != a.g.nn[0];
     if (slab) {
-        if (c03) march2_kernel<OP, true, true><<<blocks, 32 * WPB, 0, s>>>(a, nct, nch, chl);
-        else march2_kernel<OP, false, true><<<blocks, 32 * WPB, 0, s>>>(a, nct, nch, chl);
+        if (c03) launch_k(march2_kernel<OP, true, true>, dim3(blocks), dim3(32 * WPB), 0, s, a, nct, nch, chl);
+        else launch_k(march2_kernel<OP, false, true>, dim3(blocks), dim3(32 * WPB), 0, s, a, nct, nch, chl);
     } else {
-        if (c03) march2_kernel<OP, true, false><<<blocks, 32 * WPB, 0, s>>>(a, nct, nch, chl);
-        else march2_kernel<OP, false, false><<<blocks, 32 * WPB, 0, s>>>(a, nct, nch, chl);
+        if (c03) launch_k(march2_kernel<OP, true, false>, dim3(blocks), dim3(32 * WPB), 0, s, a, nct, nch, chl);
+        else launch_k(march2_kernel<OP, false, false>, dim3(blocks), dim3(32 * WPB), 0, s, a, nct, nch, chl);
     }
 }
 

@@ -129,6 +129,7 @@ struct H8Plane {              // per-thread data of one node plane
 // TR node rows per CTA (one warp each), TR - 2 owned; MINB CTAs per SM (register cap)
 template <int OP, bool C03, int TR, int MINB>
 __global__ void __launch_bounds__(32 * TR, MINB) h8_kernel(FineArgs a, int ntc, int ntr, int nch, int hch) {
+    pdl_begin();
     constexpr int TOWN_R = TR - 2;
     extern __shared__ double h8_smem[];
     double (*s_fwd)[6][32] = reinterpret_cast<double (*)[6][32]>(h8_smem);             // edge (m, d) x 3 comps, per row
@@ -409,6 +410,7 @@ struct H8R {
 // memory instead of registers; one plane less in flight)
 template <int OP, bool C03, int TR, int MINB, int NS, bool KEEP>
 __global__ void __launch_bounds__(32 * TR, MINB) h8r_kernel(FineArgs a, int ntc, int ntr, int nch, int hch) {
+    pdl_begin();
     using F = H8R<OP>;
     constexpr int TOWN_R = TR - 2, NT = 32 * TR;
     extern __shared__ double h8_smem[];
@@ -734,8 +736,8 @@ static void launch_h8_v(const FineArgs& a, int ntc, int ntr, int nch, int hch, u
         return true;
     }();
     (void)attr;
-    if (a.nu_paper) h8_kernel<OP, true, TR, MINB><<<nb, 32 * TR, smem, s>>>(a, ntc, ntr, nch, hch);
-    else h8_kernel<OP, false, TR, MINB><<<nb, 32 * TR, smem, s>>>(a, ntc, ntr, nch, hch);
+    if (a.nu_paper) launch_kp(false, h8_kernel<OP, true, TR, MINB>, dim3(nb), dim3(32 * TR), smem, s, a, ntc, ntr, nch, hch);
+    else launch_kp(false, h8_kernel<OP, false, TR, MINB>, dim3(nb), dim3(32 * TR), smem, s, a, ntc, ntr, nch, hch);
 }
 
 static constexpr int H8_NS = 3;
@@ -752,8 +754,8 @@ static void launch_h8r(const FineArgs& a, int ntc, int ntr, int nch, int hch, un
             return true;
         }();
         (void)attr;
-        if (a.nu_paper) h8r_kernel<OP, true, TR, MINB, H8_NS, KEEP><<<nb, 32 * TR, smem, s>>>(a, ntc, ntr, nch, hch);
-        else h8r_kernel<OP, false, TR, MINB, H8_NS, KEEP><<<nb, 32 * TR, smem, s>>>(a, ntc, ntr, nch, hch);
+        if (a.nu_paper) launch_kp(false, h8r_kernel<OP, true, TR, MINB, H8_NS, KEEP>, dim3(nb), dim3(32 * TR), smem, s, a, ntc, ntr, nch, hch);
+        else launch_kp(false, h8r_kernel<OP, false, TR, MINB, H8_NS, KEEP>, dim3(nb), dim3(32 * TR), smem, s, a, ntc, ntr, nch, hch);
     }
 }
 

@@ -15,6 +15,7 @@ __global__ void restrict_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* __res
                                 const uint8_t* __restrict__ mc, const double* __restrict__ fine,
                                 double* __restrict__ coarse, int R, const int* active, const int* done, int off0,
                                 int fo0, int fo1) {
+    pdl_begin();
     constexpr int NS = DIM == 2 ? 9 : 27;
     long long I = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (I >= gc.nnodes) return;
@@ -66,9 +67,9 @@ void restrict_apply(const LevelGeom& gf, const LevelGeom& gc, const uint8_t* mf,
     int th = 128;
     dim3 bl((unsigned)((gc.nnodes + th - 1) / th), R);
     if (gf.dim == 2)
-        restrict_kernel<2><<<bl, th, 0, s>>>(gf, gc, mf, mc, fine, coarse, R, active, done, off0, fo0, fo1);
+        launch_kp(false, restrict_kernel<2>, dim3(bl), dim3(th), 0, s, gf, gc, mf, mc, fine, coarse, R, active, done, off0, fo0, fo1);
     else
-        restrict_kernel<3><<<bl, th, 0, s>>>(gf, gc, mf, mc, fine, coarse, R, active, done, off0, fo0, fo1);
+        launch_kp(false, restrict_kernel<3>, dim3(bl), dim3(th), 0, s, gf, gc, mf, mc, fine, coarse, R, active, done, off0, fo0, fo1);
 }
 
 // fine(i,k) (+)= free_f(i,k) * sum_I w free_c(I,k) coarse(I,k): along each axis an even
@@ -78,6 +79,7 @@ __global__ void prolong_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* __rest
                                const uint8_t* __restrict__ mc, const double* __restrict__ coarse,
                                double* __restrict__ fine, int R, const int* active, const int* done, bool accumulate,
                                int off0) {
+    pdl_begin();
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= gf.nnodes) return;
     if (done && *done) return;
@@ -134,7 +136,7 @@ void prolong_add(const LevelGeom& gf, const LevelGeom& gc, const uint8_t* mf, co
     const long long blocks = (gf.nnodes + th - 1) / th;
     dim3 bl((unsigned)blocks, blocks >= 148 * 16 ? 1 : R);
     if (gf.dim == 2)
-        prolong_kernel<2><<<bl, th, 0, s>>>(gf, gc, mf, mc, coarse, fine, R, active, done, accumulate, off0);
+        launch_kp(false, prolong_kernel<2>, dim3(bl), dim3(th), 0, s, gf, gc, mf, mc, coarse, fine, R, active, done, accumulate, off0);
     else
-        prolong_kernel<3><<<bl, th, 0, s>>>(gf, gc, mf, mc, coarse, fine, R, active, done, accumulate, off0);
+        launch_kp(false, prolong_kernel<3>, dim3(bl), dim3(th), 0, s, gf, gc, mf, mc, coarse, fine, R, active, done, accumulate, off0);
 }
