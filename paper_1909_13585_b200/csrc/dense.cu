@@ -471,6 +471,69 @@ __global__ void __launch_bounds__(256) dense_apply_rows_kernel(const double* __r
     }
 }
 
+// Tensor-core variant for small coarsest levels (n ~ 1k, the launch-latency regime): Z^T = Ainv X^T
+// with DMMA m8n8k4 tiles -- a CTA owns 8 rows, its 8 warps split the k range, each warp keeps one
+// (or two) 8x8 accumulator tiles of (rows x RHS); the partial tiles are summed across the warps in
+// shared memory.  ~1k warps in flight instead of RW-row CTAs looping over the columns.
+template <int NT>
+__global__ void __launch_bounds__(256) dense_apply_mma_kernel(const double* __restrict__ Ainv, long long ld, long long n,
+                                                              const double* __restrict__ rv, double* __restrict__ z,
+                                                              int R, int r0, const int* active, const int* done) {
+    pdl_begin();
+    __shared__ double red[8][NT][32][2];
+    if (done && *done) return;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const long long i0 = (long long)blockIdx.x * 8;   // i0 + 7 < npad (padded rows are valid memory)
+    const long long steps = (n + 3) / 4, per = (steps + 7) / 8;
+    const long long kb = w * per * 4, ke = min(n, (w + 1) * per * 4);
+    const int gr = lane >> 2, gc = lane & 3;
+    const double* arow = Ainv + (i0 + gr) * ld;
+    const int rend = min(R, r0 + 8 * NT);
+    double acc[NT][2];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
+#pragma unroll 2
+    for (long long k0 = kb; k0 < ke; k0 += 4) {
+        const long long kk = k0 + gc;
+        const bool kin = kk < n;
+        const double a = kin ? __ldg(arow + kk) : 0.0;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            const int q = r0 + t * 8 + gr;
+            const double b = (kin && q < rend) ? __ldg(rv + (long long)q * n + kk) : 0.0;
+            dmma(acc[t][0], acc[t][1], a, b);
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+        red[w][t][lane][0] = acc[t][0];
+        red[w][t][lane][1] = acc[t][1];
+    }
+    __syncthreads();
+    if (w >= NT) return;
+    // warp t sums n-tile t over the 8 k-segments; lane holds rows gr, RHS 2 gc + {0, 1}
+    const int t = w;
+    double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < 8; ++ww) {
+        v0 += red[ww][t][lane][0];
+        v1 += red[ww][t][lane][1];
+    }
+    const long long i = i0 + gr;
+    if (i >= n) return;
+    const int qa = r0 + t * 8 + 2 * gc, qb = qa + 1;
+    if (qa < rend && (!active || active[qa])) z[(long long)qa * n + i] = v0;
+    if (qb < rend && (!active || active[qb])) z[(long long)qb * n + i] = v1;
+}
+
+static bool dense_mma() {   // MG_DENSE_MMA=0: column-split DFMA kernel on small levels
+    static const bool v = [] {
+        const char* e = getenv("MG_DENSE_MMA");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return v;
+}
+
 static bool dense_rows() {
     static const bool v = [] {
         const char* e = getenv("MG_DENSE_ROWS");
@@ -491,6 +554,14 @@ void dense_apply(const double* Ainv, long long ld, long long n, const double* r,
             else if (rem > 4) { launch_k(dense_apply_rows_kernel<8>, dim3(bl), dim3(256), 0, s, Ainv, ld, n, r, z, R, r0, active, done); r0 += 8; }
             else if (rem > 1) { launch_k(dense_apply_rows_kernel<4>, dim3(bl), dim3(256), 0, s, Ainv, ld, n, r, z, R, r0, active, done); r0 += 4; }
             else { launch_k(dense_apply_rows_kernel<1>, dim3(bl), dim3(256), 0, s, Ainv, ld, n, r, z, R, r0, active, done); r0 += 1; }
+        }
+        return;
+    }
+    if (dense_mma()) {
+        const unsigned bl = (unsigned)((n + 7) / 8);
+        for (int r0 = 0; r0 < R;) {
+            if (R - r0 > 8) { launch_k(dense_apply_mma_kernel<2>, dim3(bl), dim3(256), 0, s, Ainv, ld, n, r, z, R, r0, active, done); r0 += 16; }
+            else { launch_k(dense_apply_mma_kernel<1>, dim3(bl), dim3(256), 0, s, Ainv, ld, n, r, z, R, r0, active, done); r0 += 8; }
         }
         return;
     }
