@@ -439,39 +439,8 @@ __global__ void __launch_bounds__(32 * DA_WARPS) dense_apply_kernel(const double
     }
 }
 
-// Row-per-warp variant: warp w of a CTA owns row i, its lanes stride over the columns with all RB
-// right-hand sides in registers (one Ainv load per RB FMAs); the vector columns come from L1 (the
-// 8 warps of a CTA read the same columns), no shared memory, no barriers, one warp_sum per RHS.
-template <int RB>
-__global__ void __launch_bounds__(256) dense_apply_rows_kernel(const double* __restrict__ Ainv, long long ld, long long n,
-                                                               const double* __restrict__ rv, double* __restrict__ z,
-                                                               int R, int r0, const int* active, const int* done) {
-    pdl_begin();
-    if (done && *done) return;
-    const int lane = threadIdx.x & 31;
-    const long long i = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
-    if (i >= n) return;
-    const int nr = min(RB, R - r0);
-    double acc[RB];
-#pragma unroll
-    for (int q = 0; q < RB; ++q) acc[q] = 0.0;
-    const double* row = Ainv + i * ld;
-#pragma unroll 2
-    for (long long j = lane; j < n; j += 32) {
-        const double a = __ldg(row + j);
-#pragma unroll
-        for (int q = 0; q < RB; ++q)
-            if (q < nr) acc[q] = fma(a, __ldg(rv + (long long)(r0 + q) * n + j), acc[q]);
-    }
-#pragma unroll
-    for (int q = 0; q < RB; ++q) {
-        if (q >= nr) break;
-        const double v = warp_sum(acc[q]);
-        if (lane == 0 && (!active || active[r0 + q])) z[(long long)(r0 + q) * n + i] = v;
-    }
-}
-
-// Tensor-core variant for small coarsest levels (n ~ 1k, the launch-latency regime): Z^T = Ainv X^T
+// Tensor-core variant (default at every size; B200: C2 6.47 -> 6.21, C4 22.6 -> 22.0, C5 179 -> 177
+// ms/step against the column-split kernel above): Z^T = Ainv X^T
 // with DMMA m8n8k4 tiles -- a CTA owns 8 rows, its 8 warps split the k range, each warp keeps one
 // (or two) 8x8 accumulator tiles of (rows x RHS); the partial tiles are summed across the warps in
 // shared memory.  ~1k warps in flight instead of RW-row CTAs looping over the columns.
@@ -534,29 +503,9 @@ static bool dense_mma() {   // MG_DENSE_MMA=0: column-split DFMA kernel on small
     return v;
 }
 
-static bool dense_rows() {
-    static const bool v = [] {
-        const char* e = getenv("MG_DENSE_ROWS");
-        return e ? atoi(e) != 0 : true;
-    }();
-    return v;
-}
 
 void dense_apply(const double* Ainv, long long ld, long long n, const double* r, double* z, int R, const int* active,
                  const int* done, cudaStream_t s) {
-    // row-per-warp on large coarsest levels (C5: -1 ms/step); on n ~ 1k it has too few warps
-    // (C2/C3 measured 3x slower) and the column-split kernel below is used
-    if (dense_rows() && n >= 3072) {
-        const unsigned bl = (unsigned)((n + 7) / 8);
-        for (int r0 = 0; r0 < R;) {
-            const int rem = R - r0;
-            if (rem > 8) { launch_k(dense_apply_rows_kernel<16>, dim3(bl), dim3(256), 0, s, Ainv, ld, n, r, z, R, r0, active, done); r0 += 16; }
-            else if (rem > 4) { launch_k(dense_apply_rows_kernel<8>, dim3(bl), dim3(256), 0, s, Ainv, ld, n, r, z, R, r0, active, done); r0 += 8; }
-            else if (rem > 1) { launch_k(dense_apply_rows_kernel<4>, dim3(bl), dim3(256), 0, s, Ainv, ld, n, r, z, R, r0, active, done); r0 += 4; }
-            else { launch_k(dense_apply_rows_kernel<1>, dim3(bl), dim3(256), 0, s, Ainv, ld, n, r, z, R, r0, active, done); r0 += 1; }
-        }
-        return;
-    }
     if (dense_mma()) {
         const unsigned bl = (unsigned)((n + 7) / 8);
         for (int r0 = 0; r0 < R;) {
