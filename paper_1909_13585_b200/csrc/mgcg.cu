@@ -271,6 +271,12 @@ struct mg_ctx {
     double* Mc = nullptr;                        // Galerkin child matrices Q_c^T K0 Q_c
     double* gstage = nullptr;                    // G(u) phi host-path staging
     long long gstage_cap = 0;
+    // G(u) phi with host buffers on one slab: phi chunks copied in / y chunks copied out on two
+    // copy streams while the previous chunk computes (duplex H2D / D2H overlapped with the kernel)
+    cudaStream_t cs_in = nullptr, cs_out = nullptr;
+    static constexpr int NCHUNK_EV = 8;
+    cudaEvent_t gev_in[NCHUNK_EV] = {}, gev_k[NCHUNK_EV] = {};
+    cudaEvent_t gev_sig = nullptr, gev_done = nullptr;
     double* wbuf = nullptr;                      // adjoint RHS element terms (nphi x m x nv)
     long long wbuf_cap = 0;
     double* dlam = nullptr;                      // eigenvalues for mg_eigen_sensitivity (MG_MAX_RHS)
@@ -1690,6 +1696,64 @@ mg_status stress_stiffness_apply(mg_handle c, const double* Es_e, const double* 
         stream_leave(c);
         return MG_OK;
     }
+    if (!multi(c) && !dev && nslab(c) == 1) {
+        // one slab, host buffers: Es and u in, sigma, then phi in chunks -- H2D of chunk k + 1 and
+        // D2H of chunk k - 1 overlap the kernel of chunk k (stream-ordered through events)
+        Slab& sl = c->sl[0];
+        const LevelGeom& g0 = sl.lv[0].g;
+        const long long n = g0.ndof, m = g0.nelem;
+        const long long need = m + n + 2 * n * nphi;
+        if (need > c->gstage_cap) {
+            CU(cudaStreamSynchronize(s));
+            if (c->gstage) cudaFree(c->gstage);
+            c->gstage = nullptr;
+            CU(cudaMalloc(&c->gstage, sizeof(double) * need));
+            c->gstage_cap = need;
+        }
+        if (!c->cs_in) {
+            CU(cudaStreamCreateWithFlags(&c->cs_in, cudaStreamNonBlocking));
+            CU(cudaStreamCreateWithFlags(&c->cs_out, cudaStreamNonBlocking));
+            for (int k = 0; k < mg_ctx::NCHUNK_EV; ++k) {
+                CU(cudaEventCreateWithFlags(&c->gev_in[k], cudaEventDisableTiming));
+                CU(cudaEventCreateWithFlags(&c->gev_k[k], cudaEventDisableTiming));
+            }
+            CU(cudaEventCreateWithFlags(&c->gev_sig, cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&c->gev_done, cudaEventDisableTiming));
+        }
+        double* dEs = c->gstage;
+        double* du = dEs + m;
+        double* dphi = du + n;
+        double* dy = dphi + n * nphi;
+        if (!sl.sig) CU(cudaMalloc(&sl.sig, sizeof(double) * m * nv));
+        // the copy streams must not overtake earlier work on the handle stream (staging reuse)
+        CU(cudaEventRecord(c->gev_sig, s));
+        CU(cudaStreamWaitEvent(c->cs_in, c->gev_sig, 0));
+        CU(cudaStreamWaitEvent(c->cs_out, c->gev_sig, 0));
+        CU(cudaMemcpyAsync(dEs, Es_e, sizeof(double) * m, cudaMemcpyDefault, s));
+        CU(cudaMemcpyAsync(du, u, sizeof(double) * n, cudaMemcpyDefault, s));
+        stress_sigma(g0, dEs, du, sl.sig, s);
+        c->launches++;
+        const int nch = std::min(mg_ctx::NCHUNK_EV, nphi);
+        const int per = (nphi + nch - 1) / nch;
+        for (int k = 0, k0 = 0; k0 < nphi; ++k, k0 += per) {
+            const int kc = std::min(per, nphi - k0);
+            const size_t bytes = sizeof(double) * n * kc;
+            CU(cudaMemcpyAsync(dphi + n * k0, phi + n * k0, bytes, cudaMemcpyDefault, c->cs_in));
+            CU(cudaEventRecord(c->gev_in[k], c->cs_in));
+            CU(cudaStreamWaitEvent(s, c->gev_in[k], 0));
+            stress_apply(g0, sl.sig, sl.lv[0].mask, dphi + n * k0, dy + n * k0, kc, s);
+            c->launches++;
+            CU(cudaEventRecord(c->gev_k[k], s));
+            CU(cudaStreamWaitEvent(c->cs_out, c->gev_k[k], 0));
+            CU(cudaMemcpyAsync(y + n * k0, dy + n * k0, bytes, cudaMemcpyDefault, c->cs_out));
+        }
+        CHECK_LAUNCH();
+        CU(cudaEventRecord(c->gev_done, c->cs_out));
+        CU(cudaStreamWaitEvent(s, c->gev_done, 0));
+        CU(cudaStreamSynchronize(s));
+        stream_leave(c);
+        return MG_OK;
+    }
     // general path: this rank's owned planes -> slab-local compact arrays (+ ghosts) -> kernels
     // -> owned planes back.  Host buffers are staged (synchronous).
     const long long n = c->n_rank, m = c->m_rank;
@@ -2356,6 +2420,14 @@ mg_status mg_destroy(mg_handle c) {
     if (c->h_dbl) cudaFreeHost(c->h_dbl);
     if (c->ev_in) cudaEventDestroy(c->ev_in);
     if (c->ev_out) cudaEventDestroy(c->ev_out);
+    for (int k = 0; k < mg_ctx::NCHUNK_EV; ++k) {
+        if (c->gev_in[k]) cudaEventDestroy(c->gev_in[k]);
+        if (c->gev_k[k]) cudaEventDestroy(c->gev_k[k]);
+    }
+    if (c->gev_sig) cudaEventDestroy(c->gev_sig);
+    if (c->gev_done) cudaEventDestroy(c->gev_done);
+    if (c->cs_in) cudaStreamDestroy(c->cs_in);
+    if (c->cs_out) cudaStreamDestroy(c->cs_out);
     comm_destroy(c->comm);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;

@@ -77,6 +77,29 @@ def test_stress_stiffness_parity(name):
     assert rel(y.cpu().numpy(), yo).max() < 1e-13
 
 
+@pytest.mark.parametrize("nphi", [1, 3, 7])
+@pytest.mark.parametrize("name", ["T2b", "T3a"])
+def test_stress_stiffness_host_buffers_bitwise(name, nphi):
+    """G(u) phi with host buffers (pageable, and pinned: the chunked copy-in / compute / copy-out
+    pipeline) equals the device-buffer result bit for bit."""
+    import paper_1909_13585_b200 as mg
+    cfg, inp, _ = case(name)
+    h = handle(name)
+    u = rough_vectors(cfg, 1, seed_offset=5)[0]
+    phi = rough_vectors(cfg, nphi, seed_offset=19)
+    yd = torch.empty((nphi, phi.shape[1]), dtype=torch.float64, device=DEV)
+    mg.stress_stiffness_apply(h, to_dev(inp["Es"]), to_dev(u), to_dev(phi), yd)
+    ref = yd.cpu().numpy()
+    yh = np.empty_like(phi)
+    mg.stress_stiffness_apply(h, np.ascontiguousarray(inp["Es"]), np.ascontiguousarray(u), np.ascontiguousarray(phi), yh)
+    assert np.array_equal(yh, ref)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    pEs, pu, pphi = pin(inp["Es"]), pin(u), pin(phi)
+    py = torch.empty(phi.shape, dtype=torch.float64).pin_memory()
+    mg.stress_stiffness_apply(h, pEs, pu, pphi, py)
+    assert np.array_equal(py.numpy(), ref)
+
+
 SOLVE_CASES = ["T2a", "T2b", "T2c", "C1", "C2", "T3a", "T3b", "T3c"]
 
 
