@@ -1,0 +1,46 @@
+"""Programmatic dependent launch (PDL) must not change results: the same solves and V-cycles with
+MG_PDL=1 (default) and MG_PDL=0 (plain launches) agree bit for bit.  The switch is read once per
+process, so each setting runs in its own interpreter."""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r"""
+import json, sys
+import numpy as np, torch
+sys.path.insert(0, %(root)r)
+import paper_1909_13585_b200 as mg
+from workloads import generate, get_config
+out = {}
+for name in %(names)r:
+    cfg = get_config(name)
+    inp = generate(cfg)
+    dev = torch.device("cuda:0")
+    h = mg.mg_setup(cfg.nel, torch.from_numpy(inp["E"]).to(dev), torch.from_numpy(inp["fixed"]).to(dev), cfg.levels)
+    rhs = torch.from_numpy(np.ascontiguousarray(inp["rhs"])).to(dev)
+    x = torch.empty_like(rhs)
+    for _ in range(3):   # repeated solves: the graphs are replayed
+        mg.mgcg_solve(h, rhs, 1e-10, x)
+    out[name] = x.cpu().numpy().tobytes().hex()
+print(json.dumps(out))
+"""
+
+
+@pytest.mark.gpu
+def test_pdl_on_off_bitwise():
+    names = ["T2b", "C1", "C2", "T3a"]
+    res = {}
+    for pdl in ("1", "0"):
+        env = dict(os.environ, MG_PDL=pdl)
+        p = subprocess.run([sys.executable, "-c", SCRIPT % {"root": ROOT, "names": names}], env=env,
+                           capture_output=True, text=True, timeout=600, cwd=ROOT)
+        assert p.returncode == 0, p.stderr[-2000:]
+        res[pdl] = json.loads(p.stdout.strip().splitlines()[-1])
+    for n in names:
+        assert res["1"][n] == res["0"][n], n
