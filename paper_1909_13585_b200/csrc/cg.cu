@@ -134,8 +134,18 @@ __global__ void __launch_bounds__(512) scalars_kernel(int mode, int R, const dou
         const bool act = c.active[r] != 0;
         double v = 0.0;
         if (mode == SM_BB || mode == SM_TRUE || act) {
-            for (int i = lane; i < items; i += 32) v += partial[(long long)r * pstride + i];
-            v = warp_sum(v);
+            // four independent chains (fixed order: deterministic, independent of R)
+            const double* pr = partial + (long long)r * pstride;
+            double v1 = 0.0, v2 = 0.0, v3 = 0.0;
+            int i = lane;
+            for (; i + 96 < items; i += 128) {
+                v += pr[i];
+                v1 += pr[i + 32];
+                v2 += pr[i + 64];
+                v3 += pr[i + 96];
+            }
+            for (; i < items; i += 32) v += pr[i];
+            v = warp_sum((v + v1) + (v2 + v3));
         }
         if (lane == 0) {
             switch (mode) {
