@@ -1,6 +1,6 @@
 #!/bin/bash
 # launch lists (host-driven loop so loop kernels are visible) for the given configs
-O=gpurun_out/launch3; mkdir -p $O
+O=gpurun_out/launch4; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1 || exit 1
 for C in "$@"; do
 CMD="python bench.py --config $C --steps 1 --warmup 3 --no-cpu --no-e2e"
