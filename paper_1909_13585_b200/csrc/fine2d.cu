@@ -422,7 +422,6 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
     // byte i of a mask array (4-byte aligned base) from the aligned word holding it
     auto byte_of = [](unsigned word, unsigned i) { return (int)((word >> (8 * (i & 3u))) & 0xffu); };
     auto fetch = [&](Slot& s, int P, int st) {
-        const long long no = pd.org + (long long)P * pd.pitch + c;
         const double2 v0 = AR.v0[st][lane];
         s.v0x = v0.x; s.v0y = v0.y;
         if (OP == M2_RESTRICT || OP == M2_CGP) { const double2 v1 = AR.v1[st][lane]; s.v1x = v1.x; s.v1y = v1.y; }
@@ -460,10 +459,15 @@ __global__ void __launch_bounds__(32 * WPB, march_minb(OP)) march2_kernel(March2
     double A0x, A0y, A1x, A1y, A2x, A2y;      // masked input at c-1, c, c+1 of plane L
 #endif
     double urx, ury, auxx = 0, auxy = 0, aux2x = 0, aux2y = 0, dax = 1, day = 1;
+#if MG_2D_TRANSFORM
+    double ex;                                // E of layer L at c
+#else
     double ex, exl;                           // E of layer L at c, c-1
+    double carx = 0.0, cary = 0.0;
+#endif
     int mA;
     double cev[4] = {0.0, 0.0, 0.0, 0.0};     // POST: coarse row of the last even plane
-    double carx = 0.0, cary = 0.0, dot = 0.0, accx = 0.0, accy = 0.0;
+    double dot = 0.0, accx = 0.0, accy = 0.0;
     if (OP == M2_POST) {
         const int rlo = (i0 - 1 + off0) >> 1;
         if (cin && rlo >= 0) {
