@@ -310,7 +310,6 @@ struct mg_ctx {
 
 static int nslab(const mg_ctx* c) { return (int)c->sl.size(); }
 static bool multi(const mg_ctx* c) { return c->S > 1; }
-static const LevelGeom& G0(mg_ctx* c) { return c->G[0]; }
 
 static LevelGeom make_geom(int dim, const int* N) {
     LevelGeom g{};
@@ -2080,7 +2079,7 @@ mg_status mg_multilevel_modes(mg_handle c, const double* Es_e, const double* u, 
     if (multi(c)) return fail(MG_ERR_ARG, "mg_multilevel_modes: single slab only (this round)");
     for (const void* p : {(const void*)Es_e, (const void*)u, (const void*)Phi})
         if (!is_device_ptr(p)) return fail(MG_ERR_ARG, "mg_multilevel_modes: device pointers required");
-    const int dim = c->dim, L = c->L, NL = dim * (1 << dim), nv = dim == 2 ? 3 : 6;
+    const int dim = c->dim, L = c->L, nv = dim == 2 ? 3 : 6;
     const int pblk = std::min<int>(q + 8, 48);       // subspace size (oversampled)
     if ((long long)c->nL < pblk) return fail(MG_ERR_DIM, "coarsest level smaller than the mode subspace");
     TRY(ensure_vectors(c, std::max(q, 1)));
