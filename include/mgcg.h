@@ -32,8 +32,17 @@
  *   - Ownership: mg_setup copies E_e and fixed; all other arrays are borrowed for
  *     the duration of the call.  The handle owns its device workspace.
  *   - Errors: every call returns mg_status; argument errors have no side
- *     effects; mg_last_error() gives a one-line description of the last failure
- *     on the calling thread.
+ *     effects (mg_update_modulus validates E before touching the handle);
+ *     mg_last_error() gives a one-line description of the last failure on the
+ *     calling thread.  On MG_ERR_BREAKDOWN x and the report describe the last
+ *     iterate (its true residual is evaluated).
+ *   - Handles and threads: several handles (any dim / nu / element) may be alive
+ *     and used from several threads.  Calls that launch work are serialised by a
+ *     process-wide lock.  The element constants (K0, K^, H, D0) sit in constant
+ *     memory shared by all handles: a call on a handle whose (dim, element, nu)
+ *     differs from the last one used first waits for all device work
+ *     (cudaDeviceSynchronize) and reloads them, so interleaving handles of
+ *     different element types is correct but synchronising.
  */
 #ifndef MGCG_H
 #define MGCG_H

@@ -51,6 +51,35 @@ def assemble_K_raw(nel, E, nu=0.3, element="std") -> sp.csr_matrix:
     return _coo(edofs, vals, n)
 
 
+def assemble_K_raw_slabs(nel, E, nu=0.3, element="std", planes=8) -> sp.csr_matrix:
+    """The same sum as `assemble_K_raw`, built one band of node planes (axis 0) at a time so that
+    the COO triplets of a 12.8M-DOF grid (C5: 2.4e9 of them) never exist at once.  Rows of node
+    planes [a, b) receive contributions only from element planes [a-1, b), so each band is
+    assembled from those elements' entries restricted to its own rows; the bands are stacked."""
+    dim = len(nel)
+    K0 = fem.element_stiffness_of(element, dim, nu)
+    E = np.asarray(E, dtype=np.float64).reshape(tuple(nel))
+    n = dim * int(np.prod([m + 1 for m in nel]))
+    plane = dim * int(np.prod([m + 1 for m in nel[1:]]))      # DOFs per node plane
+    eplane = int(np.prod(nel[1:]))                            # elements per element plane
+    edofs = element_dofs(nel)
+    nl = edofs.shape[1]
+    blocks = []
+    for a in range(0, nel[0] + 1, planes):
+        b = min(a + planes, nel[0] + 1)
+        e0, e1 = max(a - 1, 0), min(b, nel[0])
+        ed = edofs[e0 * eplane:e1 * eplane]
+        vals = E.reshape(-1)[e0 * eplane:e1 * eplane, None] * K0.reshape(1, -1)
+        rows = np.repeat(ed, nl, axis=1).reshape(-1)
+        cols = np.tile(ed, (1, nl)).reshape(-1)
+        keep = (rows >= a * plane) & (rows < b * plane)
+        blk = sp.coo_matrix((vals.reshape(-1)[keep], (rows[keep] - a * plane, cols[keep])),
+                            shape=((b - a) * plane, n)).tocsr()
+        del vals, rows, cols, keep
+        blocks.append(blk)
+    return sp.vstack(blocks, format="csr")
+
+
 def apply_dirichlet(A: sp.csr_matrix, fixed, identity: bool) -> sp.csr_matrix:
     free = 1.0 - np.asarray(fixed, dtype=np.float64)
     F = sp.diags(free)
@@ -60,9 +89,36 @@ def apply_dirichlet(A: sp.csr_matrix, fixed, identity: bool) -> sp.csr_matrix:
     return out.tocsr()
 
 
+def apply_dirichlet_inplace(A: sp.csr_matrix, fixed, identity: bool) -> sp.csr_matrix:
+    """`apply_dirichlet` for matrices too large to copy: the same F A F (+ I - F), formed by
+    scaling the stored entries by free[row] * free[col] in place and, for identity=True, setting
+    the (structurally present) diagonal of every fixed row to 1."""
+    free = 1.0 - np.asarray(fixed, dtype=np.float64)
+    n = A.shape[0]
+    step = 1 << 20
+    for r0 in range(0, n, step):
+        r1 = min(r0 + step, n)
+        s, e = A.indptr[r0], A.indptr[r1]
+        rows = np.repeat(np.arange(r0, r1), np.diff(A.indptr[r0:r1 + 1]))
+        A.data[s:e] *= free[rows] * free[A.indices[s:e]]
+    if identity:
+        for r in np.flatnonzero(free == 0.0):
+            s, e = A.indptr[r], A.indptr[r + 1]
+            j = s + np.flatnonzero(A.indices[s:e] == r)
+            if len(j) != 1:
+                raise ValueError("diagonal entry of a fixed row is not stored")
+            A.data[j] = 1.0
+    return A
+
+
 def assemble_K(nel, E, fixed, nu=0.3, element="std") -> sp.csr_matrix:
     """Fine-grid K with fixed rows/cols replaced by identity."""
     return apply_dirichlet(assemble_K_raw(nel, E, nu, element), fixed, identity=True)
+
+
+def assemble_K_large(nel, E, fixed, nu=0.3, element="std") -> sp.csr_matrix:
+    """`assemble_K` with the memory-light steps above (same entries; used at C5 size)."""
+    return apply_dirichlet_inplace(assemble_K_raw_slabs(nel, E, nu, element), fixed, identity=True)
 
 
 def element_geometric_batch(dim, u_e, nu=0.3):

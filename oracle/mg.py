@@ -57,15 +57,24 @@ def masked_prolongation(nel_c, fixed_f, fixed_c) -> sp.csr_matrix:
     return (sp.diags(1.0 - np.asarray(fixed_f, float)) @ P @ sp.diags(1.0 - np.asarray(fixed_c, float))).tocsr()
 
 
-def galerkin(A_f, Pm, fixed_c) -> sp.csr_matrix:
-    """A_c = Pm^T A_f Pm + (I - F_c)  (Alg. 2 l.5)."""
-    return (Pm.T @ A_f @ Pm + sp.diags(np.asarray(fixed_c, float))).tocsr()
+def galerkin(A_f, Pm, fixed_c, row_blocks=1) -> sp.csr_matrix:
+    """A_c = Pm^T A_f Pm + (I - F_c)  (Alg. 2 l.5).
+    row_blocks > 1 forms the same product as sum_b Pm[rows_b]^T (A_f[rows_b] Pm) over bands of
+    fine rows, so that the fine-by-coarse intermediate never exists whole (C5 size)."""
+    if row_blocks <= 1:
+        return (Pm.T @ A_f @ Pm + sp.diags(np.asarray(fixed_c, float))).tocsr()
+    n = A_f.shape[0]
+    Ac = sp.diags(np.asarray(fixed_c, float)).tocsr()
+    for b in range(row_blocks):
+        r0, r1 = b * n // row_blocks, (b + 1) * n // row_blocks
+        Ac = (Ac + Pm[r0:r1].T @ (A_f[r0:r1] @ Pm)).tocsr()
+    return Ac
 
 
 class Hierarchy:
     """All levels' operators for a K with Dirichlet identity rows (A_0 = K_bc)."""
 
-    def __init__(self, nel, K_bc, fixed, levels):
+    def __init__(self, nel, K_bc, fixed, levels, row_blocks=1):
         self.dims = level_dims(nel, levels)
         self.A = [K_bc.tocsr()]
         self.fixed = [np.asarray(fixed)]
@@ -75,4 +84,4 @@ class Hierarchy:
             Pm = masked_prolongation(self.dims[l], self.fixed[-1], fc)
             self.P.append(Pm)
             self.fixed.append(fc)
-            self.A.append(galerkin(self.A[-1], Pm, fc))
+            self.A.append(galerkin(self.A[-1], Pm, fc, row_blocks if l == 1 else 1))

@@ -87,11 +87,11 @@ def pcg(A, b, M, tol, maxit=2000):
     return x, maxit
 
 
-def mgpcg_solve(nel, K_bc, F, fixed, levels, tol=1e-13, omega=0.6, nu=1):
+def mgpcg_solve(nel, K_bc, F, fixed, levels, tol=1e-13, omega=0.6, nu=1, row_blocks=1):
     F = np.asarray(F, dtype=np.float64)
     single = F.ndim == 1
     F2 = F[None] if single else F
-    H = Hierarchy(nel, K_bc, fixed, levels)
+    H = Hierarchy(nel, K_bc, fixed, levels, row_blocks)
     V = _VCycle(H, omega, nu)
     U = np.zeros_like(F2)
     its = []

@@ -40,6 +40,37 @@ def _ptr(a, dtype):
     return ctypes.c_void_p(a.data_ptr())
 
 
+def _numel(a):
+    return int(a.size) if isinstance(a, np.ndarray) else int(a.numel())
+
+
+def _shape(a):
+    return tuple(a.shape)
+
+
+def _need_rows(a, n, name, nrows=None):
+    """a must be (nrows, n) -- or (n,) when nrows is 1 -- so the C side never reads or writes out
+    of bounds (it trusts the handle's sizes)."""
+    sh = _shape(a)
+    if len(sh) == 1 and (nrows in (None, 1)) and sh[0] == n:
+        return 1
+    if len(sh) != 2 or sh[1] != n or (nrows is not None and sh[0] != nrows):
+        want = f"({nrows if nrows is not None else 'k'}, {n})"
+        raise ValueError(f"{name}: expected shape {want}, got {sh}")
+    return sh[0]
+
+
+def _need_len(a, n, name):
+    if _numel(a) != n:
+        raise ValueError(f"{name}: expected {n} entries, got {_numel(a)}")
+
+
+def _level_ndof(h, level):
+    if level == 0:
+        return h.ndof
+    return mg_level_info(h, level)["ndof"]
+
+
 class Handle:
     """Owns an mg_handle (one design on one grid)."""
 
@@ -132,6 +163,7 @@ def mg_local_info(h):
 
 
 def mg_update_modulus(h, E):
+    _need_len(E, h.nelem, "E")
     check(lib.mg_update_modulus(h.raw, _ptr(E, np.float64)))
 
 
@@ -145,7 +177,8 @@ def _report(rep, nrhs):
 
 def mgcg_solve(h, rhs, tol, x, raise_on_error=True):
     """Solve K x_k = rhs_k for all rows of rhs (nrhs, ndof); x is written in place."""
-    nrhs = rhs.shape[0]
+    nrhs = _need_rows(rhs, h.ndof, "rhs")
+    _need_rows(x, h.ndof, "x", nrhs)
     rep = MgReport()
     st = lib.mgcg_solve(h.raw, _ptr(rhs, np.float64), nrhs, tol, _ptr(x, np.float64), ctypes.byref(rep))
     out = _report(rep, nrhs)
@@ -157,7 +190,8 @@ def mgcg_solve(h, rhs, tol, x, raise_on_error=True):
 
 def mgcg_block_solve(h, rhs, tol, x, raise_on_error=True):
     """Block PCG (mgBPCG) over all rows of rhs (nrhs, ndof); x written in place."""
-    nrhs = rhs.shape[0]
+    nrhs = _need_rows(rhs, h.ndof, "rhs")
+    _need_rows(x, h.ndof, "x", nrhs)
     rep = MgReport()
     st = lib.mgcg_block_solve(h.raw, _ptr(rhs, np.float64), nrhs, tol, _ptr(x, np.float64), ctypes.byref(rep))
     out = _report(rep, nrhs)
@@ -169,6 +203,9 @@ def mgcg_block_solve(h, rhs, tol, x, raise_on_error=True):
 
 def mg_multilevel_modes(h, Es, u, q, Phi, tol=1e-10):
     """Sec. 2.1 multilevel modes: fills Phi (q, ndof) and returns (lam_tilde, lam_coarse) lists."""
+    _need_len(Es, h.nelem, "Es")
+    _need_len(u, h.ndof, "u")
+    _need_rows(Phi, h.ndof, "Phi", q)
     lt = np.zeros(q)
     lc = np.zeros(q)
     check(lib.mg_multilevel_modes(h.raw, _ptr(Es, np.float64), _ptr(u, np.float64), q, tol, _ptr(Phi, np.float64),
@@ -177,36 +214,59 @@ def mg_multilevel_modes(h, Es, u, q, Phi, tol=1e-10):
 
 
 def stress_stiffness_apply(h, Es, u, phi, y):
+    _need_len(Es, h.nelem, "Es")
+    _need_len(u, h.ndof, "u")
+    nphi = _need_rows(phi, h.ndof, "phi")
+    _need_rows(y, h.ndof, "y", nphi)
     check(lib.stress_stiffness_apply(h.raw, _ptr(Es, np.float64), _ptr(u, np.float64), _ptr(phi, np.float64),
                                      phi.shape[0], _ptr(y, np.float64)))
 
 
 def mg_adjoint_rhs(h, Es, phi, b):
     """b_i = phi_i^T (grad_u G) phi_i (Eq. 5 right-hand sides), device tensors."""
+    _need_len(Es, h.nelem, "Es")
+    nphi = _need_rows(phi, h.ndof, "phi")
+    _need_rows(b, h.ndof, "b", nphi)
     check(lib.mg_adjoint_rhs(h.raw, _ptr(Es, np.float64), _ptr(phi, np.float64), phi.shape[0], _ptr(b, np.float64)))
 
 
 def mg_eigen_sensitivity(h, dEk, dEs, u, phi, z, lam, out):
     """Eq. 4 element sensitivities for nphi modes (device tensors; lam: sequence of nphi floats)."""
     lam_arr = np.ascontiguousarray(np.asarray(lam, dtype=np.float64))
+    _need_len(dEk, h.nelem, "dEk")
+    _need_len(dEs, h.nelem, "dEs")
+    _need_len(u, h.ndof, "u")
+    nphi = _need_rows(phi, h.ndof, "phi")
+    _need_rows(z, h.ndof, "z", nphi)
+    _need_len(lam_arr, nphi, "lam")
+    _need_len(out, nphi * h.nelem, "out")
     check(lib.mg_eigen_sensitivity(h.raw, _ptr(dEk, np.float64), _ptr(dEs, np.float64), _ptr(u, np.float64),
                                    _ptr(phi, np.float64), _ptr(z, np.float64), _ptr(lam_arr, np.float64),
                                    phi.shape[0], _ptr(out, np.float64)))
 
 
 def mg_matvec(h, level, x, y):
+    n = _level_ndof(h, level)
+    k = _need_rows(x, n, "x")
+    _need_rows(y, n, "y", k)
     check(lib.mg_matvec(h.raw, level, _ptr(x, np.float64), x.shape[0], _ptr(y, np.float64)))
 
 
 def mg_vcycle(h, r, z):
+    k = _need_rows(r, h.ndof, "r")
+    _need_rows(z, h.ndof, "z", k)
     check(lib.mg_vcycle(h.raw, _ptr(r, np.float64), r.shape[0], _ptr(z, np.float64)))
 
 
 def mg_restrict(h, level, fine, coarse):
+    k = _need_rows(fine, _level_ndof(h, level), "fine")
+    _need_rows(coarse, _level_ndof(h, level + 1), "coarse", k)
     check(lib.mg_restrict(h.raw, level, _ptr(fine, np.float64), fine.shape[0], _ptr(coarse, np.float64)))
 
 
 def mg_prolong(h, level, coarse, fine):
+    k = _need_rows(coarse, _level_ndof(h, level + 1), "coarse")
+    _need_rows(fine, _level_ndof(h, level), "fine", k)
     check(lib.mg_prolong(h.raw, level, _ptr(coarse, np.float64), coarse.shape[0], _ptr(fine, np.float64)))
 
 
@@ -219,6 +279,7 @@ def mg_level_info(h, level):
 
 
 def mg_get_diagonal(h, level, d):
+    _need_len(d, _level_ndof(h, level), "d")
     check(lib.mg_get_diagonal(h.raw, level, _ptr(d, np.float64)))
 
 

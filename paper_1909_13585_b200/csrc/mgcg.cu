@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -244,6 +245,7 @@ struct Slab {
 struct mg_ctx {
     int dim = 0, L = 0;
     double nu = 0.3;
+    int elem = 0;             // mg_grid.element
     bool nu_paper = true;     // nu == 0.3: compile-time K0 in the fine kernels
     bool fused2d = false;     // 2D, L >= 2, V(1,1): fused RESTRICT / POST fine kernels
     bool unfused_coarse = false;   // MG_UNFUSED_COARSE=1: generic coarse-level kernels (A/B checks)
@@ -342,6 +344,54 @@ static void stream_leave(mg_ctx* c) {
     cudaEventRecord(c->ev_out, c->stream);
     cudaStreamWaitEvent(c->user, c->ev_out, 0);
 }
+
+// ---------------------------------------------------------------- API scope
+// The element constants (K0, K^, Q, H, D0) live in __constant__ memory, shared by every handle of
+// the process.  Each entry point that launches work therefore (1) holds the process-wide API lock,
+// (2) makes the constants those of its own handle -- a handle with another (dim, element, nu) first
+// waits for ALL device work (no kernel of another handle may still be reading them), then uploads
+// and waits for the upload -- and (3) joins the handle stream to the caller's stream on entry and
+// the caller's stream back to the handle stream on every exit path (RAII).
+static std::recursive_mutex g_api_mu;
+static bool g_const_valid = false;
+static int g_const_dim = 0, g_const_elem = -1;
+static double g_const_nu = 0.0;
+
+static mg_status ensure_constants(mg_ctx* c) {
+    if (g_const_valid && g_const_dim == c->dim && g_const_elem == c->elem && g_const_nu == c->nu) return MG_OK;
+    if (g_const_valid) CU(cudaDeviceSynchronize());
+    g_const_valid = false;
+    cudaStream_t s = c->stream;
+    fine_set_constants(c->dim, c->K0.data(), s);
+    if (c->dim == 3) h8_set_constants(c->K0.data(), s);
+    if (c->dim == 2) fine2d_set_constants(c->K0.data(), s);
+    galerkin_set_constants(c->dim, c->K0.data(), s);
+    stress_set_constants(c->dim, c->nu, s);
+    sens_set_constants(c->dim, c->K0.data(), c->nu, s);
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(s));
+    g_const_valid = true;
+    g_const_dim = c->dim;
+    g_const_elem = c->elem;
+    g_const_nu = c->nu;
+    return MG_OK;
+}
+
+struct ApiScope {
+    mg_ctx* c;
+    std::lock_guard<std::recursive_mutex> lk;
+    mg_status status;
+    explicit ApiScope(mg_ctx* c_) : c(c_), lk(g_api_mu), status(MG_OK) {
+        stream_enter(c);
+        status = ensure_constants(c);
+    }
+    ~ApiScope() { stream_leave(c); }
+    ApiScope(const ApiScope&) = delete;
+    ApiScope& operator=(const ApiScope&) = delete;
+};
+#define API_SCOPE(c)          \
+    ApiScope api_scope_(c);   \
+    TRY(api_scope_.status)
 
 // ---------------------------------------------------------------- partition (host)
 // Slab k of S gets a contiguous run of coarsest-level element layers (sizes differ by at
@@ -589,10 +639,11 @@ static void free_vectors(mg_ctx* c) {
     double** cv[] = {&c->partial, &c->stage, &c->stage2, &c->cr, &c->cz, &c->xtmp};
     for (auto p : cv)
         if (*p) { cudaFree(*p); *p = nullptr; }
-    cudaGraphExec_t* gs[] = {&c->g_init, &c->g_restart, &c->g_iter, &c->g_true, &c->g_loop};
+    cudaGraphExec_t* gs[] = {&c->g_init, &c->g_restart, &c->g_iter, &c->g_true, &c->g_loop, &c->g_block};
     for (auto g : gs)
         if (*g) { cudaGraphExecDestroy(*g); *g = nullptr; }
     c->graph_R = -1;
+    c->block_tol = -1.0;   // the block-PCG graph referenced the freed vectors: recapture
     c->Ralloc = 0;
 }
 
@@ -1210,6 +1261,7 @@ static mg_status setup_impl(mg_ctx* c, const mg_grid* grid, const double* E_e, c
     c->dim = grid->dim;
     c->L = levels;
     c->nu = grid->nu;
+    c->elem = grid->element;
     if (opts) c->opts = *opts;
     c->user = (cudaStream_t)stream;
     const int rank = dist ? dist->rank : 0, nranks = dist ? dist->nranks : 1;
@@ -1283,10 +1335,7 @@ static mg_status setup_impl(mg_ctx* c, const mg_grid* grid, const double* E_e, c
         c->fused3d = ok3 && (f3 & 1);
         c->fused3d_post = ok3 && (f3 & 2);
     }
-    fine_set_constants(dim, c->K0.data(), s);
-    if (dim == 3) h8_set_constants(c->K0.data(), s);
-    if (dim == 2) fine2d_set_constants(c->K0.data(), s);
-    galerkin_set_constants(dim, c->K0.data(), s);
+    TRY(ensure_constants(c));
     {
         const int na = 1 << dim, nl = dim * na;
         std::vector<double> Mh((size_t)na * nl * nl);
@@ -1294,8 +1343,6 @@ static mg_status setup_impl(mg_ctx* c, const mg_grid* grid, const double* E_e, c
         CU(cudaMalloc(&c->Mc, sizeof(double) * Mh.size()));
         CU(cudaMemcpy(c->Mc, Mh.data(), sizeof(double) * Mh.size(), cudaMemcpyHostToDevice));
     }
-    stress_set_constants(dim, c->nu, s);
-    sens_set_constants(dim, c->K0.data(), c->nu, s);
     const int NL = dim * (1 << dim);
     const bool edev = is_device_ptr(E_e), fdev = is_device_ptr(fixed);
     uint8_t* dfix = nullptr;
@@ -1468,6 +1515,7 @@ mg_status mg_setup_dist(const mg_grid* grid, const double* E_e, const uint8_t* f
     if (ncoarse > 20000) return fail(MG_ERR_DIM, "coarsest level too large for the dense direct solve; add levels");
     if (dist && grid->nel[0] / f < dist->nranks * dist->nslab)
         return fail(MG_ERR_DIM, "more slabs than coarsest-level element layers along axis 0");
+    std::lock_guard<std::recursive_mutex> lk(g_api_mu);
     mg_ctx* c = new mg_ctx();
     mg_status st = setup_impl(c, grid, E_e, fixed, levels, opts, dist, stream);
     if (st != MG_OK) {
@@ -1496,21 +1544,59 @@ mg_status mg_local_info(mg_handle c, long long* ndof_local, long long* nelem_loc
 
 mg_status mg_update_modulus(mg_handle c, const double* E_e) {
     if (!c || !E_e) return fail(MG_ERR_ARG, "NULL argument");
-    stream_enter(c);
+    API_SCOPE(c);
+    cudaStream_t s = c->stream;
+    const long long m = c->m_rank;
+    // validate the new moduli BEFORE touching the handle (argument errors have no side effects):
+    // host input is staged on the device first and the slabs are then filled from the staging copy
     const bool edev = is_device_ptr(E_e);
+    double* stage = nullptr;
+    const double* src = E_e;
+    if (!edev) {
+        CU(cudaMallocAsync((void**)&stage, sizeof(double) * std::max<long long>(m, 1), s));
+        CU(cudaMemcpyAsync(stage, E_e, sizeof(double) * m, cudaMemcpyHostToDevice, s));
+        src = stage;
+    }
+    auto release = [&]() { if (stage) cudaFreeAsync(stage, s); };
+    int bad = 0;
+    if (cudaMemsetAsync(c->d_status, 0, sizeof(int), s) != cudaSuccess) { release(); return fail(MG_ERR_CUDA, "memset"); }
+    if (m > 0) check_modulus_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(m, src, c->d_status);
+    c->launches++;
+    if (cudaMemcpyAsync(c->h_pinned, c->d_status, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
+        release();
+        return fail(MG_ERR_CUDA, "mg_update_modulus: modulus check");
+    }
+    bad = c->h_pinned[0];
+    if (c->comm.nranks > 1) {   // every rank takes the same decision
+        double f = bad ? 1.0 : 0.0;
+        if (cudaMemcpyAsync(c->sums, &f, sizeof(double), cudaMemcpyHostToDevice, s) != cudaSuccess ||
+            !comm_allreduce_sum(c->comm, c->sums, 1, s) ||
+            cudaMemcpyAsync(&f, c->sums, sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess) {
+            release();
+            return fail(MG_ERR_NCCL, "mg_update_modulus: modulus check allreduce");
+        }
+        bad = f != 0.0;
+    }
+    if (bad) {
+        release();
+        return fail(MG_ERR_MODULUS, "E_e must be positive and finite (handle unchanged)");
+    }
     const int rp0 = c->rank_p0[c->comm.rank];
     for (Slab& sl : c->sl) {
         const LevelGeom& g0 = sl.lv[0].g;
         const long long le = g0.nelem / g0.N[0];
-        CU(cudaMemcpyAsync(sl.E + sl.gl * le, E_e + (long long)(sl.e0 - rp0) * le,
-                           sizeof(double) * (sl.e1 - sl.e0) * le,
-                           edev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+        if (cudaMemcpyAsync(sl.E + sl.gl * le, src + (long long)(sl.e0 - rp0) * le, sizeof(double) * (sl.e1 - sl.e0) * le,
+                            cudaMemcpyDeviceToDevice, s) != cudaSuccess) {
+            release();
+            return fail(MG_ERR_CUDA, "mg_update_modulus: copy");
+        }
     }
+    release();
     // E changes the stencils but not the masks; the masks of coarse levels may have been
     // augmented by zero-diagonal DOFs, which stay valid for the same BCs.
-    TRY(compute_operators(c));
-    stream_leave(c);
-    return MG_OK;
+    return compute_operators(c);
 }
 
 mg_status mgcg_solve(mg_handle c, const double* rhs, int nrhs, double tol, double* x, mg_report* rep) {
@@ -1519,7 +1605,7 @@ mg_status mgcg_solve(mg_handle c, const double* rhs, int nrhs, double tol, doubl
     if (!(tol > 0.0) || !(tol < 1.0)) return fail(MG_ERR_ARG, "tol must be in (0,1)");
     const long long n = c->n_rank;
     cudaStream_t s = c->stream;
-    stream_enter(c);
+    API_SCOPE(c);
     cudaEvent_t e0, e1;
     CU(cudaEventCreate(&e0));
     CU(cudaEventCreate(&e1));
@@ -1573,7 +1659,10 @@ mg_status mgcg_solve(mg_handle c, const double* rhs, int nrhs, double tol, doubl
             ++glaunch;
             klaunch += c->n_iter;
         }
-        if (hp[1]) { result = fail(MG_ERR_BREAKDOWN, "p.Kp <= 0 in CG"); break; }
+        // on breakdown the true residual is still evaluated (it also flushes the deferred x
+        // update), so x and the report describe the last iterate
+        const bool breakdown = hp[1] != 0;
+        if (breakdown) result = fail(MG_ERR_BREAKDOWN, "p.Kp <= 0 in CG");
         CU(cudaGraphLaunch(c->g_true, s));
         ++glaunch;
         klaunch += c->n_true;
@@ -1582,6 +1671,7 @@ mg_status mgcg_solve(mg_handle c, const double* rhs, int nrhs, double tol, doubl
         CU(cudaMemcpyAsync(hd + 2 * MG_MAX_RHS, c->ctl.tt, sizeof(double) * MG_MAX_RHS, cudaMemcpyDeviceToHost, s));
         CU(cudaMemcpyAsync(hp + 2, c->ctl.iters, sizeof(int) * nrhs, cudaMemcpyDeviceToHost, s));
         CU(cudaStreamSynchronize(s));
+        if (breakdown) break;
         // restart the RHS whose true residual exceeds tol (reading r12)
         std::vector<int> restart(MG_MAX_RHS, 0);
         int nre = 0;
@@ -1636,7 +1726,6 @@ mg_status mgcg_solve(mg_handle c, const double* rhs, int nrhs, double tol, doubl
         rep->kernel_launches = klaunch;
         rep->solve_ms = ms;
     }
-    stream_leave(c);
     if (result != MG_OK) return result;
     if (!all_conv) return fail(MG_ERR_MAXITER, "not all right-hand sides reached tol");
     return MG_OK;
@@ -1682,7 +1771,7 @@ mg_status stress_stiffness_apply(mg_handle c, const double* Es_e, const double* 
     cudaStream_t s = c->stream;
     const int dim = c->dim;
     const int nv = dim == 2 ? 3 : 6;
-    stream_enter(c);
+    API_SCOPE(c);
     const bool dev = is_device_ptr(phi) && is_device_ptr(y) && is_device_ptr(u) && is_device_ptr(Es_e);
     if (!multi(c) && dev) {   // one slab, device buffers: direct
         Slab& sl = c->sl[0];
@@ -1692,7 +1781,6 @@ mg_status stress_stiffness_apply(mg_handle c, const double* Es_e, const double* 
         stress_apply(g0, sl.sig, sl.lv[0].mask, phi, y, nphi, s);
         c->launches += 2;
         CHECK_LAUNCH();
-        stream_leave(c);
         return MG_OK;
     }
     if (!multi(c) && !dev && nslab(c) == 1) {
@@ -1750,7 +1838,6 @@ mg_status stress_stiffness_apply(mg_handle c, const double* Es_e, const double* 
         CU(cudaEventRecord(c->gev_done, c->cs_out));
         CU(cudaStreamWaitEvent(s, c->gev_done, 0));
         CU(cudaStreamSynchronize(s));
-        stream_leave(c);
         return MG_OK;
     }
     // general path: this rank's owned planes -> slab-local compact arrays (+ ghosts) -> kernels
@@ -1821,7 +1908,6 @@ mg_status stress_stiffness_apply(mg_handle c, const double* Es_e, const double* 
         CU(cudaMemcpyAsync(y, dy, sizeof(double) * n * nphi, cudaMemcpyDefault, s));
         CU(cudaStreamSynchronize(s));
     }
-    stream_leave(c);
     return MG_OK;
 }
 
@@ -1831,7 +1917,7 @@ mg_status mg_adjoint_rhs(mg_handle c, const double* Es_e, const double* phi, int
     if (multi(c)) return fail(MG_ERR_ARG, "mg_adjoint_rhs: single slab only (this round)");
     if (!is_device_ptr(Es_e) || !is_device_ptr(phi) || !is_device_ptr(b))
         return fail(MG_ERR_ARG, "mg_adjoint_rhs: device pointers required");
-    stream_enter(c);
+    API_SCOPE(c);
     const LevelGeom& g = c->G[0];
     const long long need = (long long)nphi * g.nelem * (c->dim == 2 ? 3 : 6);
     if (need > c->wbuf_cap) {
@@ -1844,7 +1930,6 @@ mg_status mg_adjoint_rhs(mg_handle c, const double* Es_e, const double* phi, int
     adjoint_rhs_apply(g, Es_e, c->sl[0].lv[0].mask, phi, nphi, c->wbuf, b, c->stream);
     c->launches += 2;
     CHECK_LAUNCH();
-    stream_leave(c);
     return MG_OK;
 }
 
@@ -1856,7 +1941,7 @@ mg_status mg_eigen_sensitivity(mg_handle c, const double* dEk, const double* dEs
     for (const void* p : {(const void*)dEk, (const void*)dEs, (const void*)u, (const void*)phi, (const void*)z,
                           (const void*)out})
         if (!is_device_ptr(p)) return fail(MG_ERR_ARG, "mg_eigen_sensitivity: device pointers required");
-    stream_enter(c);
+    API_SCOPE(c);
     if (!c->dlam) CU(cudaMalloc(&c->dlam, sizeof(double) * MG_MAX_RHS));
     CU(cudaMemcpyAsync(c->dlam, lambda, sizeof(double) * nphi,
                        is_device_ptr(lambda) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
@@ -1864,7 +1949,6 @@ mg_status mg_eigen_sensitivity(mg_handle c, const double* dEk, const double* dEs
     c->launches++;
     CHECK_LAUNCH();
     CU(cudaStreamSynchronize(c->stream));   // lambda may be a host temporary
-    stream_leave(c);
     return MG_OK;
 }
 
@@ -1876,7 +1960,7 @@ mg_status mgcg_block_solve(mg_handle c, const double* rhs, int nrhs, double tol,
     const int R = nrhs;
     const long long nr = c->n_rank;
     cudaStream_t s = c->stream;
-    stream_enter(c);
+    API_SCOPE(c);
     cudaEvent_t e0, e1;
     CU(cudaEventCreate(&e0));
     CU(cudaEventCreate(&e1));
@@ -1884,7 +1968,7 @@ mg_status mgcg_block_solve(mg_handle c, const double* rhs, int nrhs, double tol,
     TRY(ensure_vectors(c, R));
     Slab& sl = c->sl[0];
     const long long n = sl.vs;
-    if (c->block_R < R) {
+    if (c->block_R != R) {   // workspace and the captured iteration are both sized for R
         for (double** p : {&c->bpart, &c->bGam, &c->bRho, &c->bRhoN, &c->bC})
             if (*p) { cudaFree(*p); *p = nullptr; }
         CU(cudaMalloc(&c->bpart, sizeof(double) * (long long)R * R * gram_blocks(n, R)));
@@ -1983,7 +2067,6 @@ mg_status mgcg_block_solve(mg_handle c, const double* rhs, int nrhs, double tol,
         rep->kernel_launches = 14LL * it;
         rep->solve_ms = ms;
     }
-    stream_leave(c);
     if (!all_conv) return fail(MG_ERR_MAXITER, "block PCG: not all right-hand sides reached tol");
     return MG_OK;
 }
@@ -2084,7 +2167,7 @@ mg_status mg_multilevel_modes(mg_handle c, const double* Es_e, const double* u, 
     if ((long long)c->nL < pblk) return fail(MG_ERR_DIM, "coarsest level smaller than the mode subspace");
     TRY(ensure_vectors(c, std::max(q, 1)));
     cudaStream_t s = c->stream;
-    stream_enter(c);
+    API_SCOPE(c);
     Slab& sl = c->sl[0];
     const LevelGeom& g0 = sl.lv[0].g;
     const long long n = g0.ndof, nL = c->nL, ld = c->npad;
@@ -2138,7 +2221,6 @@ mg_status mg_multilevel_modes(mg_handle c, const double* Es_e, const double* u, 
         c->launches += 3;
     } else {
         cleanup();
-        stream_leave(c);
         return fail(MG_ERR_ARG, "mg_multilevel_modes needs levels >= 2");
     }
     CHECK_LAUNCH();
@@ -2170,7 +2252,6 @@ mg_status mg_multilevel_modes(mg_handle c, const double* Es_e, const double* u, 
         for (auto& v : Ah) v = -v;                                      // (-G, K)
         if (!small_geneig(pblk, Ah, Bh, th, Y)) {
             cleanup();
-            stream_leave(c);
             return fail(MG_ERR_BREAKDOWN, "mg_multilevel_modes: coarse Gram matrix not SPD");
         }
         // order by decreasing theta (largest theta = smallest positive lambda)
@@ -2208,7 +2289,6 @@ mg_status mg_multilevel_modes(mg_handle c, const double* Es_e, const double* u, 
             src = dst;
         }
     }
-    stream_leave(c);
     // ---- step 3: K Phi~ = G Psi by block PCG (mgBPCG, Alg. 2 l.15)
     TRY(([&]() -> mg_status {
         mg_status st = stress_stiffness_apply(c, Es_e, u, Psi, q, GPsi);
@@ -2218,7 +2298,6 @@ mg_status mg_multilevel_modes(mg_handle c, const double* Es_e, const double* u, 
     // ---- step 4: Rayleigh quotients lambda~_i = -phi~^T K phi~ / phi~^T G phi~
     TRY(mg_matvec(c, 0, Phi, q, KPhi));
     TRY(stress_stiffness_apply(c, Es_e, u, Phi, q, GPsi));
-    stream_enter(c);
     std::vector<double> num((size_t)q * q), den((size_t)q * q);
     gram(n, n, q, Phi, KPhi, gpart, Gr, s);
     CU(cudaMemcpyAsync(num.data(), Gr, sizeof(double) * q * q, cudaMemcpyDeviceToHost, s));
@@ -2228,7 +2307,6 @@ mg_status mg_multilevel_modes(mg_handle c, const double* Es_e, const double* u, 
     for (int i = 0; i < q; ++i) lam_tilde[i] = -num[i * q + i] / den[i * q + i];
     cleanup();
     CU(cudaStreamSynchronize(s));
-    stream_leave(c);
     return MG_OK;
 }
 
@@ -2236,7 +2314,7 @@ mg_status mg_matvec(mg_handle c, int level, const double* x, int nrhs, double* y
     if (!c || !x || !y) return fail(MG_ERR_ARG, "NULL argument");
     if (level < 0 || level >= c->L || nrhs < 1 || nrhs > MG_MAX_RHS) return fail(MG_ERR_ARG, "bad level / nrhs");
     if (multi(c) && level > 0) return fail(MG_ERR_ARG, "coarse-level diagnostics need a single slab");
-    stream_enter(c);
+    API_SCOPE(c);
     if (level == 0) {
         if (c->dim == 2 || multi(c)) {   // rank layout <-> slab layout around the fine kernels
             TRY(ensure_vectors(c, nrhs));
@@ -2265,7 +2343,6 @@ mg_status mg_matvec(mg_handle c, int level, const double* x, int nrhs, double* y
         c->launches++;
     }
     CHECK_LAUNCH();
-    stream_leave(c);
     return MG_OK;
 }
 
@@ -2273,7 +2350,7 @@ mg_status mg_vcycle(mg_handle c, const double* r, int nrhs, double* z) {
     if (!c || !r || !z) return fail(MG_ERR_ARG, "NULL argument");
     if (nrhs < 1 || nrhs > MG_MAX_RHS) return fail(MG_ERR_ARG, "bad nrhs");
     TRY(ensure_vectors(c, nrhs));
-    stream_enter(c);
+    API_SCOPE(c);
     // the preconditioner exactly as the solve applies it (same fine blocks, alpha = 0)
     TRY(scatter_fine(c, r, nrhs, true, &Slab::r1));
     CU(cudaMemsetAsync(c->ctl.alpha, 0, sizeof(double) * MG_MAX_RHS, c->stream));
@@ -2287,7 +2364,6 @@ mg_status mg_vcycle(mg_handle c, const double* r, int nrhs, double* z) {
     TRY(gather_fine(c, &Slab::zf, nrhs, z));
     c->launches += rc.launches;
     CHECK_LAUNCH();
-    stream_leave(c);
     return MG_OK;
 }
 
@@ -2295,13 +2371,12 @@ mg_status mg_restrict(mg_handle c, int level, const double* fine, int nrhs, doub
     if (!c || !fine || !coarse) return fail(MG_ERR_ARG, "NULL argument");
     if (level < 0 || level >= c->L - 1 || nrhs < 1) return fail(MG_ERR_ARG, "bad level / nrhs");
     if (multi(c)) return fail(MG_ERR_ARG, "level diagnostics need a single slab");
-    stream_enter(c);
+    API_SCOPE(c);
     Slab& s = c->sl[0];
     restrict_apply(s.lv[level].g, s.lv[level + 1].g, s.lv[level].mask, s.lv[level + 1].mask, fine, coarse, nrhs,
                    nullptr, nullptr, c->stream);
     c->launches++;
     CHECK_LAUNCH();
-    stream_leave(c);
     return MG_OK;
 }
 
@@ -2309,13 +2384,12 @@ mg_status mg_prolong(mg_handle c, int level, const double* coarse, int nrhs, dou
     if (!c || !fine || !coarse) return fail(MG_ERR_ARG, "NULL argument");
     if (level < 0 || level >= c->L - 1 || nrhs < 1) return fail(MG_ERR_ARG, "bad level / nrhs");
     if (multi(c)) return fail(MG_ERR_ARG, "level diagnostics need a single slab");
-    stream_enter(c);
+    API_SCOPE(c);
     Slab& s = c->sl[0];
     prolong_add(s.lv[level].g, s.lv[level + 1].g, s.lv[level].mask, s.lv[level + 1].mask, coarse, fine, nrhs, nullptr,
                 nullptr, false, c->stream);
     c->launches++;
     CHECK_LAUNCH();
-    stream_leave(c);
     return MG_OK;
 }
 
@@ -2334,19 +2408,17 @@ mg_status mg_get_diagonal(mg_handle c, int level, double* d) {
     if (!c || !d) return fail(MG_ERR_ARG, "NULL argument");
     if (level < 0 || level >= c->L) return fail(MG_ERR_ARG, "bad level");
     if (multi(c)) return fail(MG_ERR_ARG, "level diagnostics need a single slab");
-    stream_enter(c);
+    API_SCOPE(c);
     CU(cudaMemcpyAsync(d, c->sl[0].lv[level].D, sizeof(double) * c->G[level].ndof, cudaMemcpyDeviceToDevice,
                        c->stream));
-    stream_leave(c);
     return MG_OK;
 }
 
 mg_status mg_get_coarse_inverse(mg_handle c, double* Ainv) {
     if (!c || !Ainv) return fail(MG_ERR_ARG, "NULL argument");
-    stream_enter(c);
+    API_SCOPE(c);
     CU(cudaMemcpy2DAsync(Ainv, sizeof(double) * c->nL, c->Ainv, sizeof(double) * c->npad, sizeof(double) * c->nL,
                          c->nL, cudaMemcpyDeviceToDevice, c->stream));
-    stream_leave(c);
     return MG_OK;
 }
 
@@ -2354,7 +2426,7 @@ mg_status mg_profile_kernels(mg_handle c, int nrhs, int reps, double* ms) {
     if (!c || !ms) return fail(MG_ERR_ARG, "NULL argument");
     if (nrhs < 1 || nrhs > MG_MAX_RHS || reps < 1) return fail(MG_ERR_ARG, "bad nrhs / reps");
     TRY(ensure_vectors(c, nrhs));
-    stream_enter(c);
+    API_SCOPE(c);
     cudaStream_t s = c->stream;
     Rec rc{c, nrhs, nullptr, nullptr};
     cudaEvent_t e0, e1;
@@ -2388,12 +2460,12 @@ mg_status mg_profile_kernels(mg_handle c, int nrhs, int reps, double* ms) {
     CHECK_LAUNCH();
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    stream_leave(c);
     return MG_OK;
 }
 
 mg_status mg_destroy(mg_handle c) {
     if (!c) return MG_OK;
+    std::lock_guard<std::recursive_mutex> lk(g_api_mu);
     if (c->stream) cudaStreamSynchronize(c->stream);
     free_vectors(c);
     for (Slab& s : c->sl) {

@@ -64,3 +64,32 @@ def test_product_path_does_not_import_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle\b", src, flags=re.M), f
                 assert "oracle/" not in src.replace("oracle/`", ""), f
+
+
+def test_binding_rejects_wrong_shapes(libpath):
+    """The binding checks every array against the handle's sizes before calling into the library
+    (which trusts them); a wrong shape raises ValueError and never reaches the C side."""
+    import numpy as np
+    import paper_1909_13585_b200 as mg
+
+    h = mg.Handle.__new__(mg.Handle)   # a handle that was never set up: any C call would fail
+    h.raw, h.dim, h.nel, h.levels, h.stream = None, 2, (4, 2), 1, None
+    h.ndof, h.nelem = 30, 8
+    good = np.zeros((2, 30))
+    cases = [
+        lambda: mg.mgcg_solve(h, np.zeros((2, 29)), 1e-10, good),
+        lambda: mg.mgcg_solve(h, good, 1e-10, np.zeros((3, 30))),
+        lambda: mg.mgcg_block_solve(h, good, 1e-10, np.zeros((2, 31))),
+        lambda: mg.stress_stiffness_apply(h, np.zeros(8), np.zeros(30), good, np.zeros((1, 30))),
+        lambda: mg.stress_stiffness_apply(h, np.zeros(7), np.zeros(30), good, good),
+        lambda: mg.stress_stiffness_apply(h, np.zeros(8), np.zeros(29), good, good),
+        lambda: mg.mg_update_modulus(h, np.zeros(9)),
+        lambda: mg.mg_matvec(h, 0, np.zeros((2, 30)), np.zeros((2, 3))),
+        lambda: mg.mg_vcycle(h, np.zeros((1, 30)), np.zeros((2, 30))),
+        lambda: mg.mg_adjoint_rhs(h, np.zeros(8), good, np.zeros((2, 29))),
+        lambda: mg.mg_eigen_sensitivity(h, np.zeros(8), np.zeros(8), np.zeros(30), good, good, [1.0], np.zeros(16)),
+        lambda: mg.mg_get_diagonal(h, 0, np.zeros(29)),
+    ]
+    for i, fn in enumerate(cases):
+        with pytest.raises(ValueError):
+            fn()
