@@ -6,7 +6,7 @@ One step = one pass of the whole hot path for one desig
   + stress_stiffness_apply G(u) phi for the config's phi vectors (a8; u = state solution).
 metric: fine-grid DOF*RHS*iter/s = n * sum_k iters_k / t_step  (plus MGCG solves/s).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl reference]
 
 N > 1 is launched by torchrun (one process per GPU): the global grid is cut into N axis-0
 slabs (mg_setup_dist; NCCL halo exchange + allreduce inside libmgcg), strong scaling,
@@ -210,6 +210,16 @@ def run_ours(args, cfg):
                    "frac": alg[k] / (kms[k] / 1e3) / 1e9 / hbm} for k in alg}
     dom = "cgp"
     achieved = kernels[dom]["gbs"]
+    # ---- whole-solve roofline: algorithmic bytes of the fused V(1,1)-PCG iteration (SURVEY 8(d),
+    # DESIGN.md 6.6) summed over the iterations actually run, over the measured solve time:
+    #   per iteration and active RHS  8 n (16 + 2/2^d + 8/(2^d - 1))   (vectors, all levels)
+    #   per iteration                 8 n 2 + 24 m                      (D^-1 twice, E three times)
+    d = cfg.dim
+    per_rhs = 8.0 * n * (16 + 2.0 / 2 ** d + 8.0 / (2 ** d - 1))
+    rep_last = reps[-1]
+    solve_bytes = per_rhs * sum(rep_last["iters"]) + (16.0 * n + 24.0 * m) * max(rep_last["iters"])
+    solve_ms = float(phases[:, 1].mean())
+    solve_frac = solve_bytes / (solve_ms / 1e3) / 1e9 / hbm
 
     # ---- e2e: same step through the C ABI with pinned HOST buffers (H2D/D2H inside the timed region)
     e2e = None
@@ -278,13 +288,16 @@ def run_ours(args, cfg):
         "roofline": {"kernel": "CG direction + fine EbE matvec (march2_kernel<M2_CGP> 2D / h8r_kernel<FOP_CGP> 3D)",
                      "bound": "hbm", "achieved": achieved, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic_from_profiles(cfg.name),
-                     "alg_bytes_per_launch": alg[dom], "kernel_ms": kms[dom]},
+                     "alg_bytes_per_launch": alg[dom], "kernel_ms": kms[dom],
+                     "solve_frac": solve_frac, "solve_alg_bytes": solve_bytes,
+                     "solve_model": "8n(16+2/2^d+8/(2^d-1)) B per RHS-iteration + (16n+24m) B per iteration "
+                                    "(fused V(1,1)-PCG, SURVEY 8(d))"},
         "kernels": kernels,
         "clocks": clocks,
         "e2e": e2e,
     }
     if rank == 0 and ws == 1 and not args.no_cpu:
-        result["cpu_baseline"] = cpu_baseline(cfg, inp)
+        result["cpu_baseline"] = cpu_baseline(cfg)
     if ws > 1:
         torch.distributed.barrier()
     mg.mg_destroy(h)
@@ -292,17 +305,44 @@ def run_ours(args, cfg):
 
 
 # --------------------------------------------------------------------------- oracle (CPU) arm
-def oracle_sample(cfg, inp):
-    """Bounded sample of the same workload with the CPU oracle as it stands:
-    assemble K, build the scipy MG hierarchy, PCG-solve the state RHS (1 of R) to tol."""
+SAMPLE = {"C5": "C5s"}   # bounded CPU sample of a config (same recipe at reduced size), else itself
+
+
+def sample_config(cfg):
+    return get_config(SAMPLE.get(cfg.name, cfg.name))
+
+
+def oracle_phases(scfg, inp):
+    """The oracle as it stands, phase by phase, on one bounded sample: (i) assembly of K, (ii)
+    preconditioner setup (scipy Galerkin MG hierarchy + coarsest LU), (iii) PCG solve of all R RHS
+    to tol, (iv) one CSR SpMV with R columns, (v) G(u) assembly + apply to nphi vectors."""
     from oracle import assemble, mg as omg, solve
+    ph = {}
     t = time.perf_counter()
-    K = assemble.assemble_K(cfg.nel, inp["E"], inp["fixed"])
-    H = omg.Hierarchy(cfg.nel, K, inp["fixed"], cfg.levels)
+    K = assemble.assemble_K(scfg.nel, inp["E"], inp["fixed"])
+    ph["assembly_s"] = time.perf_counter() - t
+    t = time.perf_counter()
+    H = omg.Hierarchy(scfg.nel, K, inp["fixed"], scfg.levels)
     V = solve._VCycle(H, 0.6, 1)
-    _, it = solve.pcg(K, inp["rhs"][0], V.apply, cfg.tol)
-    dt = time.perf_counter() - t
-    return n_dofs(cfg.nel) * it / dt, dt, it
+    ph["precond_setup_s"] = time.perf_counter() - t
+    t = time.perf_counter()
+    its, U = [], []
+    for k in range(scfg.nrhs):
+        u, it = solve.pcg(K, inp["rhs"][k], V.apply, scfg.tol)
+        its.append(it)
+        U.append(u)
+    ph["solve_s"] = time.perf_counter() - t
+    t = time.perf_counter()
+    _ = K @ inp["rhs"].T
+    ph["spmv_R_s"] = time.perf_counter() - t
+    if scfg.nphi:
+        t = time.perf_counter()
+        G = assemble.assemble_G(scfg.nel, inp["Es"], U[0], inp["fixed"])
+        _ = G @ inp["phi"].T
+        ph["G_assembly_apply_s"] = time.perf_counter() - t
+    n = n_dofs(scfg.nel)
+    value = n * sum(its) / ph["solve_s"]
+    return value, ph, its
 
 
 def cpu_cores():
@@ -312,35 +352,70 @@ def cpu_cores():
         return os.cpu_count()
 
 
-def cpu_baseline(cfg, inp):
-    v, dt, it = oracle_sample(cfg, inp)
-    return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{cfg.name}: scipy assembly + Galerkin MG hierarchy + PCG of the state RHS (1 of {cfg.nrhs}) "
-                      f"to {cfg.tol:g}, {it} iterations, {dt:.1f} s (SpMV/SuperLU single-threaded; "
-                      f"{cpu_cores()} cores visible)"}
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(cfg):
+    scfg = sample_config(cfg)
+    inp = generate(scfg)
+    value, ph, its = oracle_phases(scfg, inp)
+    return {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{scfg.name}: {'x'.join(map(str, scfg.nel))} ({n_dofs(scfg.nel)} DOFs), {scfg.nrhs} RHS, "
+                      f"{scfg.levels} levels, same recipe as {cfg.name}; scipy PCG + Galerkin MG to {scfg.tol:g}, "
+                      f"iterations {its}; value = DOF*RHS*iter / solve phase",
+            "phases_s": {k: round(v, 3) for k, v in ph.items()},
+            "cpu": cpu_model(), "cores_visible": cpu_cores(),
+            "threads_note": "scipy SpMV / SuperLU single-threaded; numpy BLAS unused on this path"}
 
 
 def run_reference(args, cfg):
+    """--impl reference: the oracle as it stands on the host cores, rank 0 only; K timed steps
+    after W untimed ones, each step = one PCG solve of one of the R RHS (cycling) on the bounded
+    sample (the assembly and preconditioner setup are done once, outside the steps, and reported)."""
     ws, rank, local = dist_env()
     if rank != 0:
         return None
-    inp = generate(cfg)
-    for _ in range(args.warmup if args.warmup <= 1 else 1):
-        pass   # the oracle has no warm-up state; one sample per step
-    vals, dts = [], []
-    steps = max(1, min(args.steps, 3))
-    for _ in range(steps):
-        v, dt, it = oracle_sample(cfg, inp)
-        vals.append(v)
+    from oracle import assemble, mg as omg, solve
+    scfg = sample_config(cfg)
+    inp = generate(scfg)
+    t = time.perf_counter()
+    K = assemble.assemble_K(scfg.nel, inp["E"], inp["fixed"])
+    H = omg.Hierarchy(scfg.nel, K, inp["fixed"], scfg.levels)
+    V = solve._VCycle(H, 0.6, 1)
+    setup_s = time.perf_counter() - t
+    n = n_dofs(scfg.nel)
+
+    def step(i):   # one right-hand side per step, cycling through the R of the workload
+        t0 = time.perf_counter()
+        it = solve.pcg(K, inp["rhs"][i % scfg.nrhs], V.apply, scfg.tol)[1]
+        return time.perf_counter() - t0, it
+
+    for i in range(args.warmup):
+        step(i)
+    dts, units = [], 0.0
+    for i in range(args.steps):
+        dt, it = step(args.warmup + i)
         dts.append(dt)
-    value = float(np.median(vals))
+        units += n * it
+    total = float(sum(dts))
+    value = units / total
+    sample = (f"{scfg.name}: {'x'.join(map(str, scfg.nel))} ({n} DOFs), {scfg.nrhs} RHS, same recipe as {cfg.name}; "
+              f"one step = scipy PCG + Galerkin MG solve of one RHS (cycling over the {scfg.nrhs}) to {scfg.tol:g} "
+              f"(setup {setup_s:.1f} s once)")
     return {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * float(np.median(dts)), "higher_is_better": True,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE recipe)",
-        "config": {"workload": f"{cfg.name} (oracle sample: state RHS only)", "ndof": n_dofs(cfg.nel)},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"{cfg.name}: assembly + MG hierarchy + PCG of the state RHS to {cfg.tol:g}"},
+        "config": {"workload": f"{cfg.name} (oracle on the bounded sample {scfg.name})", "ndof": n},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                         "cpu": cpu_model(), "cores_visible": cpu_cores()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -350,7 +425,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C3")
+    ap.add_argument("--config", default="C5")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

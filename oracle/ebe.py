@@ -32,14 +32,14 @@ def matvec(nel, E, fixed, x, nu=0.3, dtype=np.float64, element="std"):
     xg = x.astype(dtype).reshape(nsh) * free
     Eg = np.asarray(E).astype(dtype).reshape(tuple(nel) + (1,))
     bits = fem.local_nodes(dim)
-    xa = [xg[_slices(bb, nel)] for bb in bits]
+    nl = dim * len(bits)
+    # element DOF vectors x_e (local DOF d*a + comp), element products y_e = E_e K0 x_e, then the
+    # gather-sum of y_e into the nodes of each element (K = sum_e E_e A_e^T K0 A_e)
+    xe = np.concatenate([xg[_slices(bb, nel)] for bb in bits], axis=-1)          # (*nel, nl)
+    ye = (xe.reshape(-1, nl) @ K0.T).reshape(xe.shape) * Eg
     y = np.zeros(nsh, dtype=dtype)
     for b, bb in enumerate(bits):
-        acc = np.zeros(tuple(nel) + (dim,), dtype=dtype)
-        for a in range(len(bits)):
-            blk = K0[b * dim:(b + 1) * dim, a * dim:(a + 1) * dim]
-            acc += np.einsum("...j,ij->...i", xa[a], blk)
-        y[_slices(bb, nel)] += Eg * acc
+        y[_slices(bb, nel)] += ye[..., b * dim:(b + 1) * dim]
     y = y * free + (1 - free) * x.astype(dtype).reshape(nsh)
     return y.reshape(-1)
 

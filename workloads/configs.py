@@ -45,9 +45,12 @@ CONFIGS = {
     # BASELINE.json:9 (also times G(u) phi for 12 phi)
     "C3": Config("C3", (1920, 960), 13, 7, nphi=12, seed=1003),
     # BASELINE.json:10 (cantilever: face x=0 clamped, line load on bottom edge of face x=end)
-    "C4": Config("C4", (96, 48, 48), 7, 4, load="edge", seed=1004),
+    # nphi: G(u) phi over the config's 6 adjoint fields (reading r16; full-size 3D G parity, bench step)
+    "C4": Config("C4", (96, 48, 48), 7, 4, load="edge", nphi=6, seed=1004),
     # BASELINE.json:11 (column: base clamped, uniform top pressure)
-    "C5": Config("C5", (256, 128, 128), 7, 5, seed=1005),
+    "C5": Config("C5", (256, 128, 128), 7, 5, nphi=6, seed=1005),
+    # bounded CPU-baseline sample of C5 (same recipe, BCs, load and 7 RHS at 1/64 of the elements)
+    "C5s": Config("C5s", (64, 32, 32), 7, 3, nphi=6, seed=1005),
     # small variants used by the parity tests (same recipes, oracle-friendly sizes)
     "T2a": Config("T2a", (32, 16), 3, 3, nphi=3, seed=2001),
     "T2b": Config("T2b", (40, 24), 5, 3, nphi=2, seed=2002),          # ragged tiles
