@@ -13,6 +13,8 @@ struct LevelGeom {
     long long nnodes;
     long long ndof;
     long long nelem;
+    int p2;          // node row pitch along axis 2 of the vectors (nn[2] compact; even on the padded 3D fine level)
+    long long vstr;  // doubles per RHS vector (ndof compact)
 };
 
 // Device-side CG control block (per RHS arrays of length MG_MAX_RHS).

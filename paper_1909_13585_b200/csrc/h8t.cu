@@ -1,0 +1,703 @@
+// 3D fine level (trilinear H8), TMA plane-ring march.  K = sum_e E_e A_e^T K0 A_e applied
+// matrix-free ("K_e = E_kappa K_e0", Eq. 2 :101-108), fused with the damped-Jacobi
+// smoother / residual / CG direction of the fine V(1,1)-PCG iteration.
+//
+// Element operator in the per-axis sum/difference basis (m = v0 + v1, d = v1 - v0): the 1-D mass
+// and stiffness matrices are diagonal there and the mixed one has one entry, so
+// K^ = T^-T K0 T^-1 has 45 nonzeros instead of 576 (closed form below; equal to K0 after the
+// transform for any nu and for the incompatible-mode element, whose K^ has the same pattern).
+//
+// Work decomposition.  A CTA owns a tile of TR - 1 node rows (axis 1) x 30 node columns (axis 2)
+// and marches along axis 0 over a chunk of node planes.  Warp w (0 <= w < TR) handles element
+// row j0 + w, lane l element column c0 + l (c0 = 30 tc - 1, j0 = (TR - 1) tr - 1); node rows
+// 1..TR-1 / lanes 1..30 of the tile are its outputs.  Per node plane, one thread issues TMA box
+// loads (cp.async.bulk.tensor, zero fill outside the grid) of every input field of the tile's
+// (TR + 1) x 32 nodes into a ring of NS plane slots (mbarrier complete_tx); the last warp to
+// release a slot refills it (smem counter), so no warp waits for a producer.  The only
+// cross-warp exchange per plane is row w's contribution to node row w + 1 (6 doubles per lane)
+// through a double-buffered shared array with point-to-point mbarriers (warp w -> warp w + 1):
+// no CTA-wide barrier inside the march.  Per thread the march carries the element's two forward
+// faces and the axis-0 carry of its element results in registers (the loop is unrolled by two
+// planes so the faces ping-pong between two register sets without moves).
+//
+// Layout (padded 3D fine level, mgcg.cu): vectors (R, n0, n1, p2, 3) with p2 = n2 rounded up to
+// even (TMA row strides are multiples of 16 bytes); D^-1 (n0, n1, p2, 3); masks (n0, n1, m2) bytes,
+// m2 = n2 rounded up to 16; E compact (N0, N1, N2) when N2 is even, else padded to even.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "element.cuh"
+#include "kernels.h"
+
+__constant__ double c_Kt[576];
+
+// ---------------------------------------------------------------- K^ in closed form
+// 1-D factors in the (m, d) basis (t = 0: m, t = 1: d): M^ = diag(1/4, 1/12), D^ = diag(0, 1),
+// C^[d][m] = 1/2 (derivative on the test function), C^T[m][d] = 1/2.
+// K^[(s,i),(t,j)] = lam S^_ij + mu S^_ji + mu delta_ij sum_k S^_kk.
+__host__ __device__ constexpr double t1h(int kind, int ta, int tb) {
+    return kind == 0 ? (ta == tb ? (ta == 0 ? 0.25 : 1.0 / 12.0) : 0.0)
+         : kind == 1 ? ((ta == 1 && tb == 1) ? 1.0 : 0.0)
+         : kind == 2 ? ((ta == 1 && tb == 0) ? 0.5 : 0.0)
+                     : ((ta == 0 && tb == 1) ? 0.5 : 0.0);
+}
+__host__ __device__ constexpr double tsh3(int i, int j, int s, int t) {
+    double v = 1.0;
+    for (int k = 0; k < 3; ++k) {
+        const int ta = (s >> (2 - k)) & 1, tb = (t >> (2 - k)) & 1;
+        const int kind = (k == i && k == j) ? 1 : (k == i ? 2 : (k == j ? 3 : 0));
+        v *= t1h(kind, ta, tb);
+    }
+    return v;
+}
+__host__ __device__ constexpr double tkhat(double nu, int row, int col) {
+    const int s = row / 3, i = row % 3, t = col / 3, j = col % 3;
+    const double mu = 1.0 / (2.0 * (1.0 + nu));
+    const double lam = nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
+    double v = lam * tsh3(i, j, s, t) + mu * tsh3(j, i, s, t);
+    if (i == j)
+        for (int k = 0; k < 3; ++k) v += mu * tsh3(k, k, s, t);
+    return v;
+}
+
+void h8t_set_constants(const double* K0, cudaStream_t s) {
+    static double Ti[24][24], Kh[576];
+    for (int a = 0; a < 8; ++a)
+        for (int t = 0; t < 8; ++t) {
+            double v = 1.0;
+            for (int k = 0; k < 3; ++k) {
+                const int ab = (a >> (2 - k)) & 1, tb = (t >> (2 - k)) & 1;
+                v *= 0.5 * ((tb == 0) ? 1.0 : (ab ? 1.0 : -1.0));
+            }
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) Ti[3 * a + i][3 * t + j] = (i == j) ? v : 0.0;
+        }
+    for (int r = 0; r < 24; ++r)
+        for (int c = 0; c < 24; ++c) {
+            double v = 0.0;
+            for (int p = 0; p < 24; ++p) {
+                if (Ti[p][r] == 0.0) continue;
+                for (int q = 0; q < 24; ++q) v += Ti[p][r] * K0[p * 24 + q] * Ti[q][c];
+            }
+            Kh[r * 24 + c] = v;
+        }
+    cudaMemcpyToSymbolAsync(c_Kt, Kh, sizeof(Kh), 0, cudaMemcpyHostToDevice, s);
+}
+
+template <bool C03>
+__device__ __forceinline__ double KT(int r, int c) {
+    if (C03) return tkhat(MG_NU_PAPER, r, c);
+    return c_Kt[r * 24 + c];
+}
+
+// connected components of the K^ pattern (rows = cols; the rigid-translation rows s = 0 are zero)
+static constexpr int T_NCOMP = 11;
+__device__ constexpr int T_COMP[T_NCOMP][3] = {{3, 14, -1}, {4, 8, -1},   {5, 7, 12},  {6, 13, -1},
+                                               {9, 16, 20}, {10, 15, -1}, {11, 18, -1}, {17, 19, -1},
+                                               {21, -1, -1}, {22, -1, -1}, {23, -1, -1}};
+// row rr = 3 s + k pairs with rr ^ 12 (s ^ 4: t0 flipped); "seen" = the partner was formed in an
+// earlier component (compile time)
+__host__ __device__ constexpr bool t_partner_seen(int ci, int q) {
+    const int rr = T_COMP[ci][q];
+    const int pr = ((rr / 3) ^ 4) * 3 + rr % 3;
+    for (int c2 = 0; c2 < ci; ++c2)
+        for (int q2 = 0; q2 < 3; ++q2)
+            if (T_COMP[c2][q2] == pr) return true;
+    for (int q2 = 0; q2 < q; ++q2)
+        if (T_COMP[ci][q2] == pr) return true;
+    return false;
+}
+
+// ---------------------------------------------------------------- PTX helpers (TMA, mbarrier)
+__device__ __forceinline__ unsigned t_smem(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void t_mbar_init(uint64_t* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(t_smem(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void t_mbar_expect_tx(uint64_t* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(t_smem(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void t_mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(t_smem(b)) : "memory");
+}
+__device__ __forceinline__ void t_mbar_wait(uint64_t* b, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "T_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra T_WAIT_%=;\n"
+        "}\n" ::"r"(t_smem(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void t_tma3(void* dst, const CUtensorMap* m, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+            t_smem(dst)),
+        "l"((unsigned long long)m), "r"(c0), "r"(c1), "r"(c2), "r"(t_smem(bar))
+        : "memory");
+}
+__device__ __forceinline__ void t_tma4(void* dst, const CUtensorMap* m, int c0, int c1, int c2, int c3, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(
+            t_smem(dst)),
+        "l"((unsigned long long)m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(t_smem(bar))
+        : "memory");
+}
+
+// ---------------------------------------------------------------- ring layout
+// fields per slot: A (vector), B (vector), C (vector or D^-1), E (element row box), M (mask box)
+//   MATVEC: A = x            RESID: A = x, B = b            JACOBI: A = x, B = b, C = D^-1
+//   CGP:    A = p_in, B = z, C = x (deferred update; optional)
+//   RESTR3: A = r_in, B = q, C = D^-1
+template <int OP, int TR>
+struct TL {
+    static constexpr int BR = TR + 1;                    // node rows per box
+    static constexpr bool HB = OP != FOP_MATVEC;
+    static constexpr bool HC = OP == FOP_JACOBI || OP == FOP_CGP || OP == FOP_RESTR3;
+    static constexpr int VB = BR * 96 * 8;               // vector box bytes (BR rows x 32 nodes x 3)
+    static constexpr int EB = TR * 32 * 8;               // E box bytes
+    static constexpr int MB = BR * 32;                   // mask box bytes
+    static constexpr int OA = 0;
+    static constexpr int OB = OA + VB;
+    static constexpr int OC = OB + (HB ? VB : 0);
+    static constexpr int OE = OC + (HC ? VB : 0);
+    static constexpr int OM = OE + EB;
+    static constexpr int SLOT = (OM + MB + 127) / 128 * 128;
+    static constexpr int SINV = 2 * TR * 6 * 32 * 8;    // double-buffered row -> row+1 exchange
+};
+
+template <int OP, int TR, int NS>
+static constexpr size_t h8t_smem_bytes() {
+    using T = TL<OP, TR>;
+    return (size_t)NS * T::SLOT + T::SINV + 8 * (NS + 4 * TR) + 4 * NS + 8 * TR + 128;
+}
+
+// per-slot expected TMA bytes (zero-filled out-of-range elements count too)
+template <int OP, int TR>
+__host__ __device__ constexpr unsigned h8t_tx_bytes(bool hasC) {
+    using T = TL<OP, TR>;
+    return (unsigned)(T::VB + (T::HB ? T::VB : 0) + ((T::HC && hasC) ? T::VB : 0) + T::EB + T::MB);
+}
+
+struct H8TMaps {
+    CUtensorMap A, B, C, E, M;
+};
+
+template <int OP, bool C03, int TR, int NS, int MINB>
+__global__ void __launch_bounds__(32 * TR, MINB)
+    h8t_kernel(const __grid_constant__ FineArgs a, const __grid_constant__ H8TMaps tm, int ntc, int ntr, int nch,
+               int hch, int hasC) {
+    pdl_begin();
+    using T = TL<OP, TR>;
+    constexpr int OWNR = TR - 1;
+    extern __shared__ __align__(128) unsigned char t_sm[];
+    unsigned char* ring = t_sm;
+    double* sinv = reinterpret_cast<double*>(t_sm + NS * T::SLOT);                       // [2][TR][6][32]
+    uint64_t* full = reinterpret_cast<uint64_t*>(t_sm + NS * T::SLOT + T::SINV);         // [NS]
+    uint64_t* sfull = full + NS;                                                         // [2][TR]
+    uint64_t* sempty = sfull + 2 * TR;                                                   // [2][TR]
+    int* cnt = reinterpret_cast<int*>(sempty + 2 * TR);                                  // [NS]
+    double* s_dot = reinterpret_cast<double*>(t_sm + NS * T::SLOT + T::SINV + 8 * (NS + 4 * TR) + 4 * NS + 8);
+
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int R = a.R;
+    const int r = blockIdx.x % R;
+    const int tile = blockIdx.x / R;
+    const int nt = ntc * ntr;
+    if (tile >= nt * nch) return;
+    if (a.done && *a.done) return;
+    if (a.active && !a.active[r]) return;
+    const int tc = tile % ntc, tr = (tile / ntc) % ntr, ch = tile / nt;
+    const int n0 = a.g.nn[0], n1 = a.g.nn[1], n2 = a.g.nn[2];
+    const int p2 = a.g.p2;
+    const int c0 = 30 * tc - 1, j0 = OWNR * tr - 1;
+    const int j = j0 + w, c = c0 + lane;
+    const bool own = w >= 1 && lane >= 1 && lane <= 30 && j < n1 && c < n2;
+    const int i0 = ch * hch, i1 = min(i0 + hch, n0);
+    const int nq = i1 - i0 + 2;   // planes i0-1 .. i1
+    const long long vbase = (long long)r * a.g.vstr;
+    const long long pstr = (long long)n1 * p2 * 3;          // doubles per node plane (padded)
+    const long long nodeoff = 3 * ((long long)j * p2 + c);  // within a plane
+    const double beta = OP == FOP_CGP ? a.beta[r] : 0.0;
+    const double xal = (OP == FOP_CGP && hasC) ? a.xalpha[r] : 0.0;
+    const double alpha = OP == FOP_RESTR3 ? a.alpha[r] : 0.0;
+    const double omega = a.omega;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) {
+            t_mbar_init(&full[s], 1);
+            cnt[s] = 0;
+        }
+        for (int b = 0; b < 2 * TR; ++b) {
+            t_mbar_init(&sfull[b], 1);
+            t_mbar_init(&sempty[b], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    const unsigned txb = h8t_tx_bytes<OP, TR>(hasC != 0);
+    auto issue = [&](int q) {   // plane Q = i0 - 1 + q into slot q % NS
+        const int s = q % NS, Q = i0 - 1 + q;
+        unsigned char* sl = ring + s * T::SLOT;
+        t_mbar_expect_tx(&full[s], txb);
+        t_tma4(sl + T::OA, &tm.A, 3 * c0, j0, Q, r, &full[s]);
+        if (T::HB) t_tma4(sl + T::OB, &tm.B, 3 * c0, j0, Q, r, &full[s]);
+        if (T::HC && hasC) {
+            if (OP == FOP_CGP) t_tma4(sl + T::OC, &tm.C, 3 * c0, j0, Q, r, &full[s]);
+            else t_tma3(sl + T::OC, &tm.C, 3 * c0, j0, Q, &full[s]);
+        }
+        t_tma3(sl + T::OE, &tm.E, c0, j0, Q, &full[s]);
+        t_tma3(sl + T::OM, &tm.M, c0, j0, Q, &full[s]);
+    };
+    if (threadIdx.x == 0)
+        for (int q = 0; q < NS && q < nq; ++q) issue(q);
+
+    auto fA = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OA) + row * 96 + 3 * lane; };
+    auto fB = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OB) + row * 96 + 3 * lane; };
+    auto fC = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OC) + row * 96 + 3 * lane; };
+    auto fE = [&](int s) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OE)[w * 32 + lane]; };
+    auto fM = [&](int s, int row) { return (int)(ring + s * T::SLOT + T::OM)[row * 32 + lane]; };
+
+    // operator input of box row `row` at slot s: raw (unmasked) and u (masked, fed to the element)
+    auto input = [&](int s, int row, double (&raw)[3], double (&u)[3], int& m) {
+        m = fM(s, row);
+        const double* A = fA(s, row);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            double v;
+            if (OP == FOP_CGP) v = fma(beta, A[k], fB(s, row)[k]);
+            else if (OP == FOP_RESTR3) v = omega * fC(s, row)[k] * fma(-alpha, fB(s, row)[k], A[k]);
+            else v = A[k];
+            raw[k] = v;
+            u[k] = ((m >> k) & 1) ? 0.0 : v;
+        }
+    };
+    // forward face (m/d along axes 1 and 2) of element (w, lane) from its two node rows
+    auto face = [&](const double (&u0)[3], const double (&u1)[3], double (&F)[3][4]) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const double a0 = u0[k], a1 = u1[k];
+            const double a0n = __shfl_down_sync(MGK_FULL, a0, 1), a1n = __shfl_down_sync(MGK_FULL, a1, 1);
+            const double em0 = a0 + a0n, ed0 = a0n - a0, em1 = a1 + a1n, ed1 = a1n - a1;
+            F[k][0] = em0 + em1;
+            F[k][1] = ed0 + ed1;
+            F[k][2] = em1 - em0;
+            F[k][3] = ed1 - ed0;
+        }
+    };
+
+    double dot = 0.0;
+    double CY[3][4];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int f = 0; f < 4; ++f) CY[k][f] = 0.0;
+
+    // one step: element layer L between node planes L (faces FL, own raw rawL / mask mL) and
+    // P = L + 1 (faces FP, rawP, mP computed here); outputs node plane L when L >= i0
+    auto step = [&](int L, const double (&FL)[3][4], double (&FP)[3][4], const double (&rawL)[3], double (&rawP)[3],
+                    int mL, int& mP) {
+        const int P = L + 1;
+        const int qP = P - (i0 - 1), qL = L - (i0 - 1);
+        const int sP = qP % NS, sL = qL % NS;
+        t_mbar_wait(&full[sP], (unsigned)((qP / NS) & 1));
+        {
+            double uo[3], uu[3], ru[3];
+            int mu;
+            input(sP, w, rawP, uo, mP);
+            input(sP, w + 1, ru, uu, mu);
+            if ((OP == FOP_CGP || OP == FOP_RESTR3) && own && P >= i0 && P < i1) {
+                const long long o = vbase + (long long)P * pstr + nodeoff;
+                if (OP == FOP_CGP) {
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) a.pout[o + k] = rawP[k];
+                    if (hasC) {
+                        const double* A = fA(sP, w);
+                        const double* C = fC(sP, w);
+#pragma unroll
+                        for (int k = 0; k < 3; ++k) a.xv[o + k] = fma(xal, A[k], C[k]);   // deferred x += alpha p_in
+                    }
+                } else {
+                    const double* A = fA(sP, w);
+                    const double* B = fB(sP, w);
+                    const bool sd = P >= a.so0 && P < a.so1;
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        const double rv = fma(-alpha, B[k], A[k]);
+                        a.rout[o + k] = rv;
+                        if (a.z1out) a.z1out[o + k] = rawP[k];
+                        if (sd) dot = fma(rv, rv, dot);
+                    }
+                }
+            }
+            face(uo, uu, FP);
+        }
+        // element (L, w, lane): u^ = E (T u), y^ = K^ u^, back to the faces of planes L (GL) and P (CY)
+        double GL[3][4];
+        {
+            const double Ee = fE(sL);
+#pragma unroll
+            for (int ci = 0; ci < T_NCOMP; ++ci) {
+                double u[3];
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const int cc = T_COMP[ci][q];
+                    if (cc < 0) continue;
+                    const int sc = cc / 3, kc = cc % 3, fc = sc & 3;
+                    u[q] = Ee * (sc < 4 ? FL[kc][fc] + FP[kc][fc] : FP[kc][fc] - FL[kc][fc]);
+                }
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const int rr = T_COMP[ci][q];
+                    if (rr < 0) continue;
+                    double acc = 0.0;
+                    bool first = true;
+#pragma unroll
+                    for (int q2 = 0; q2 < 3; ++q2) {
+                        const int cc = T_COMP[ci][q2];
+                        if (cc < 0 || tkhat(MG_NU_PAPER, rr, cc) == 0.0) continue;
+                        acc = first ? KT<C03>(rr, cc) * u[q2] : fma(KT<C03>(rr, cc), u[q2], acc);
+                        first = false;
+                    }
+                    const int sr = rr / 3, kr = rr % 3, fr = sr & 3;
+                    if (!t_partner_seen(ci, q)) {
+                        GL[kr][fr] = sr < 4 ? CY[kr][fr] + acc : CY[kr][fr] - acc;
+                        CY[kr][fr] = acc;
+                    } else {
+                        GL[kr][fr] = sr < 4 ? GL[kr][fr] + acc : GL[kr][fr] - acc;
+                        CY[kr][fr] += acc;
+                    }
+                }
+            }
+        }
+        if (L >= i0) {
+            // rows: own row w gets fm - fd, row w + 1 gets fm + fd (through the exchange)
+            const int o = L - i0;
+            const int bi = o & 1;
+            const unsigned ph = (unsigned)((o >> 1) & 1);
+            if (w < TR - 1) {
+                if (o >= 2) t_mbar_wait(&sempty[bi * TR + w], ph ^ 1u);
+                double* dst = sinv + ((bi * TR + w) * 6) * 32 + lane;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    dst[(2 * k) * 32] = GL[k][0] + GL[k][2];
+                    dst[(2 * k + 1) * 32] = GL[k][1] + GL[k][3];
+                }
+                __syncwarp();
+                if (lane == 0) t_mbar_arrive(&sfull[bi * TR + w]);
+            }
+            if (w >= 1) {
+                t_mbar_wait(&sfull[bi * TR + w - 1], ph);
+                const double* src = sinv + ((bi * TR + w - 1) * 6) * 32 + lane;
+                double y[3];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const double em = (GL[k][0] - GL[k][2]) + src[(2 * k) * 32];
+                    const double ed = (GL[k][1] - GL[k][3]) + src[(2 * k + 1) * 32];
+                    const double up = __shfl_up_sync(MGK_FULL, em + ed, 1);
+                    y[k] = (em - ed) + up;
+                }
+                __syncwarp();
+                if (lane == 0) t_mbar_arrive(&sempty[bi * TR + w - 1]);
+                if (own && L < i1) {
+                    const long long ob = vbase + (long long)L * pstr + nodeoff;
+                    const bool sdot = L >= a.so0 && L < a.so1;
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        const double ax = ((mL >> k) & 1) ? rawL[k] : y[k];
+                        double out;
+                        if (OP == FOP_MATVEC || OP == FOP_CGP) {
+                            out = ax;
+                            if (OP == FOP_CGP && sdot) dot = fma(rawL[k], ax, dot);
+                        } else if (OP == FOP_RESID) {
+                            out = fB(sL, w)[k] - ax;
+                        } else if (OP == FOP_RESTR3) {
+                            out = fma(-alpha, fB(sL, w)[k], fA(sL, w)[k]) - ax;
+                        } else {   // JACOBI
+                            const double bk = fB(sL, w)[k];
+                            out = fma(omega * fC(sL, w)[k], bk - ax, rawL[k]);
+                            if (sdot) dot = fma(bk, out, dot);
+                        }
+                        a.y[ob + k] = out;
+                    }
+                }
+            }
+        }
+        // release plane L's slot; the last warp refills it with plane L + NS
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence_block();
+            if (atomicAdd(&cnt[sL], 1) == TR - 1) {
+                cnt[sL] = 0;
+                if (qL + NS < nq) issue(qL + NS);
+            }
+        }
+    };
+
+    double FA[3][4], FB[3][4], rawA[3], rawB[3];
+    int mA = 7, mB = 7;
+    {   // prologue: plane i0 - 1 (q = 0)
+        t_mbar_wait(&full[0], 0u);
+        double uo[3], uu[3], ru[3];
+        int mu;
+        input(0, w, rawA, uo, mA);
+        input(0, w + 1, ru, uu, mu);
+        face(uo, uu, FA);
+    }
+    for (int L = i0 - 1; L < i1; L += 2) {
+        step(L, FA, FB, rawA, rawB, mA, mB);
+        if (L + 1 < i1) step(L + 1, FB, FA, rawB, rawA, mB, mA);
+    }
+    if (a.partial) {
+        dot = warp_sum(dot);
+        if (lane == 0) s_dot[w] = dot;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+#pragma unroll
+            for (int q = 0; q < TR; ++q) t += s_dot[q];
+            a.partial[(long long)r * a.pstride + tile] = t;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- host: tensor maps and launch
+static PFN_cuTensorMapEncodeTiled_v12000 t_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+static bool t_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base, const cuuint64_t* dims,
+                  const cuuint64_t* strides, const cuuint32_t* box) {
+    auto enc = t_encode();
+    if (!enc) return false;
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    CUresult e = enc(m, dt, (cuuint32_t)rank, const_cast<void*>(base), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (e != CUDA_SUCCESS) {
+        fprintf(stderr, "h8t: cuTensorMapEncodeTiled failed (%d)\n", (int)e);
+        return false;
+    }
+    return true;
+}
+
+// vectors (R, n0, n1, p2, 3) as a 4-D tensor {3 n2, n1, n0, R} (row pitch 3 p2)
+static bool t_map_vec(CUtensorMap* m, const FineArgs& a, const double* v, int BR, bool perR) {
+    const LevelGeom& g = a.g;
+    cuuint64_t dims[4] = {(cuuint64_t)3 * g.nn[2], (cuuint64_t)g.nn[1], (cuuint64_t)g.nn[0], (cuuint64_t)std::max(a.R, 1)};
+    cuuint64_t str[3] = {(cuuint64_t)3 * g.p2 * 8, (cuuint64_t)3 * g.p2 * g.nn[1] * 8, (cuuint64_t)g.vstr * 8};
+    cuuint32_t box[4] = {96, (cuuint32_t)BR, 1, 1};
+    return t_map(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, perR ? 4 : 3, v, dims, str, box);
+}
+
+template <int OP, int TR, int NS, int MINB>
+static bool launch_h8t_t(const FineArgs& a, cudaStream_t s) {
+    using T = TL<OP, TR>;
+    const LevelGeom& g = a.g;
+    const int ntc = (g.nn[2] + 29) / 30;
+    const int ntr = (g.nn[1] + TR - 2) / (TR - 1);
+    int nch, hch;
+    h8t_chunks(TR, MINB, g, a.R, &nch, &hch);
+    H8TMaps tm;
+    memset(&tm, 0, sizeof(tm));
+    const double* vA = OP == FOP_CGP ? a.pin : (OP == FOP_RESTR3 ? a.rin : a.x);
+    const double* vB = OP == FOP_CGP ? a.z : (OP == FOP_RESTR3 ? a.q : a.b);
+    const bool hasC = T::HC && (OP != FOP_CGP || a.xv != nullptr);
+    bool ok = t_map_vec(&tm.A, a, vA, T::BR, true);
+    if (T::HB) ok = ok && t_map_vec(&tm.B, a, vB, T::BR, true);
+    if (hasC) ok = ok && t_map_vec(&tm.C, a, OP == FOP_CGP ? a.xv : a.Dinv, T::BR, OP == FOP_CGP);
+    {
+        cuuint64_t dims[3] = {(cuuint64_t)g.N[2], (cuuint64_t)g.N[1], (cuuint64_t)g.N[0]};
+        cuuint64_t str[2] = {(cuuint64_t)a.ep2 * 8, (cuuint64_t)a.ep2 * g.N[1] * 8};
+        cuuint32_t box[3] = {32, (cuuint32_t)TR, 1};
+        ok = ok && t_map(&tm.E, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, a.E, dims, str, box);
+    }
+    {
+        cuuint64_t dims[3] = {(cuuint64_t)g.nn[2], (cuuint64_t)g.nn[1], (cuuint64_t)g.nn[0]};
+        cuuint64_t str[2] = {(cuuint64_t)a.m2, (cuuint64_t)a.m2 * g.nn[1]};
+        cuuint32_t box[3] = {32, (cuuint32_t)T::BR, 1};
+        ok = ok && t_map(&tm.M, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, a.mask, dims, str, box);
+    }
+    if (!ok) return false;
+    const size_t smem = h8t_smem_bytes<OP, TR, NS>();
+    auto k03 = h8t_kernel<OP, true, TR, NS, MINB>;
+    auto kgn = h8t_kernel<OP, false, TR, NS, MINB>;
+    static bool attr = [&] {
+        cudaFuncSetAttribute(k03, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(kgn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        return true;
+    }();
+    (void)attr;
+    const unsigned nb = (unsigned)((long long)ntc * ntr * nch * a.R);
+    if (a.nu_paper) launch_kp(false, k03, dim3(nb), dim3(32 * TR), smem, s, a, tm, ntc, ntr, nch, hch, hasC ? 1 : 0);
+    else launch_kp(false, kgn, dim3(nb), dim3(32 * TR), smem, s, a, tm, ntc, ntr, nch, hch, hasC ? 1 : 0);
+    return true;
+}
+
+// warps per CTA (TR) and ring depth; MG_H8T_TR = 8 (2 CTAs / SM) or 16 (1 CTA / SM)
+static int h8t_tr() {
+    static int tr = [] {
+        const char* e = getenv("MG_H8T_TR");
+        const int v = e ? atoi(e) : 16;
+        return v == 8 ? 8 : 16;
+    }();
+    return tr;
+}
+static constexpr int H8T_NS = 3;
+
+// chunking along axis 0: between 16 and 64 planes per chunk, picked so that the CTA count fills
+// the resident slots (148 SMs x CTAs per SM) with the smallest tail wave
+void h8t_chunks(int TR, int minb, const LevelGeom& g, int R, int* nch_out, int* hch_out) {
+    const int ntc = (g.nn[2] + 29) / 30;
+    const int ntr = (g.nn[1] + TR - 2) / (TR - 1);
+    const long long slots = 148LL * minb;
+    const int n0 = g.nn[0];
+    int best = 1;
+    double best_eff = -1.0;
+    for (int nch = 1; nch <= std::max(1, n0 / 8); ++nch) {
+        const int hch = (n0 + nch - 1) / nch;
+        const int nc = (n0 + hch - 1) / hch;
+        const long long ctas = (long long)ntc * ntr * nc * R;
+        const double waves = (double)ctas / slots;
+        const double fill = waves / std::ceil(waves);
+        const double eff = fill * hch / (hch + 1.0);   // + one prologue plane per chunk
+        if (eff > best_eff + 1e-9) { best_eff = eff; best = nc; }
+    }
+    *nch_out = best;
+    *hch_out = (n0 + best - 1) / best;
+}
+
+int h8t_items(const LevelGeom& g, int R) {
+    const int TR = h8t_tr();
+    const int ntc = (g.nn[2] + 29) / 30;
+    const int ntr = (g.nn[1] + TR - 2) / (TR - 1);
+    int nch, hch;
+    h8t_chunks(TR, TR == 8 ? 2 : 1, g, R, &nch, &hch);
+    return ntc * ntr * nch;
+}
+
+template <int OP>
+static bool launch_h8t_op(const FineArgs& a, cudaStream_t s) {
+    if (h8t_tr() == 8) return launch_h8t_t<OP, 8, H8T_NS, 2>(a, s);
+    return launch_h8t_t<OP, 16, H8T_NS, 1>(a, s);
+}
+
+int h8t_apply(int op, const FineArgs& a, cudaStream_t s) {
+    bool ok;
+    switch (op) {
+        case FOP_MATVEC: ok = launch_h8t_op<FOP_MATVEC>(a, s); break;
+        case FOP_RESID: ok = launch_h8t_op<FOP_RESID>(a, s); break;
+        case FOP_JACOBI: ok = launch_h8t_op<FOP_JACOBI>(a, s); break;
+        case FOP_RESTR3: ok = launch_h8t_op<FOP_RESTR3>(a, s); break;
+        default: ok = launch_h8t_op<FOP_CGP>(a, s); break;
+    }
+    return ok ? h8t_items(a.g, a.R) : -1;
+}
+
+// ---------------------------------------------------------------- padded 3D fine layout
+Pad3 pad3_layout(const LevelGeom& g) {
+    Pad3 p{};
+    p.p2 = g.nn[2] + (g.nn[2] & 1);
+    p.m2 = (g.nn[2] + 15) / 16 * 16;
+    p.ep2 = g.N[2] + (g.N[2] & 1);
+    p.vstride = 3LL * g.nn[0] * g.nn[1] * p.p2;
+    return p;
+}
+
+LevelGeom pad3_geom(const LevelGeom& g, const Pad3& p) {
+    LevelGeom q = g;
+    q.p2 = p.p2;
+    q.vstr = p.vstride;
+    return q;
+}
+
+// compact (R, planes, n1, n2, 3) -> padded; src planes [0, np) map to local planes [p0, p0 + np)
+__global__ void pad3_vec_kernel(LevelGeom g, Pad3 p, int R, const uint8_t* mask, int p0, int np, const double* src,
+                                long long src_ndof, double* dst) {
+    const long long per = (long long)np * g.nn[1] * g.nn[2];
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= per) return;
+    const int r = blockIdx.y;
+    const int c = (int)(i % g.nn[2]);
+    const long long t = i / g.nn[2];
+    const int j = (int)(t % g.nn[1]);
+    const int P = (int)(t / g.nn[1]) + p0;
+    const long long cn = ((long long)P * g.nn[1] + j) * g.nn[2] + c;   // compact local node
+    const int m = mask ? mask[cn] : 0;
+    const double* s = src + (long long)r * src_ndof + 3 * i;
+    double* d = dst + (long long)r * p.vstride + 3 * (((long long)P * g.nn[1] + j) * p.p2 + c);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) d[k] = ((m >> k) & 1) ? 0.0 : s[k];
+}
+
+__global__ void unpad3_vec_kernel(LevelGeom g, Pad3 p, int R, int p0, int np, const double* src, double* dst,
+                                  long long dst_ndof) {
+    const long long per = (long long)np * g.nn[1] * g.nn[2];
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= per) return;
+    const int r = blockIdx.y;
+    const int c = (int)(i % g.nn[2]);
+    const long long t = i / g.nn[2];
+    const int j = (int)(t % g.nn[1]);
+    const int P = (int)(t / g.nn[1]) + p0;
+    const double* s = src + (long long)r * p.vstride + 3 * (((long long)P * g.nn[1] + j) * p.p2 + c);
+    double* d = dst + (long long)r * dst_ndof + 3 * i;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) d[k] = s[k];
+}
+
+void pad3_vectors_planes(const LevelGeom& g, const Pad3& p, int R, const uint8_t* mask, int p0, int np,
+                         const double* src, long long src_ndof, double* dst, cudaStream_t s) {
+    const long long per = (long long)np * g.nn[1] * g.nn[2];
+    if (per <= 0) return;
+    pad3_vec_kernel<<<dim3((unsigned)((per + 255) / 256), R), 256, 0, s>>>(g, p, R, mask, p0, np, src, src_ndof, dst);
+}
+
+void unpad3_vectors_planes(const LevelGeom& g, const Pad3& p, int R, int p0, int np, const double* src, double* dst,
+                           long long dst_ndof, cudaStream_t s) {
+    const long long per = (long long)np * g.nn[1] * g.nn[2];
+    if (per <= 0) return;
+    unpad3_vec_kernel<<<dim3((unsigned)((per + 255) / 256), R), 256, 0, s>>>(g, p, R, p0, np, src, dst, dst_ndof);
+}
+
+// node arrays: masks (1 byte) -> pitch m2, D^-1 (3 doubles) -> pitch p2; E (N2) -> pitch ep2
+__global__ void pad3_nodes_kernel(LevelGeom g, Pad3 p, const uint8_t* mask, uint8_t* maskp, const double* dinv,
+                                  double* dinvp) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= g.nnodes) return;
+    const int c = (int)(i % g.nn[2]);
+    const long long row = i / g.nn[2];
+    maskp[row * p.m2 + c] = mask[i];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) dinvp[3 * (row * p.p2 + c) + k] = dinv[3 * i + k];
+}
+__global__ void pad3_elems_kernel(LevelGeom g, Pad3 p, const double* E, double* Ep) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= g.nelem) return;
+    const int c = (int)(i % g.N[2]);
+    const long long row = i / g.N[2];
+    Ep[row * p.ep2 + c] = E[i];
+}
+
+void pad3_nodes(const LevelGeom& g, const Pad3& p, const uint8_t* mask, uint8_t* maskp, const double* dinv,
+                double* dinvp, cudaStream_t s) {
+    pad3_nodes_kernel<<<(unsigned)((g.nnodes + 255) / 256), 256, 0, s>>>(g, p, mask, maskp, dinv, dinvp);
+}
+void pad3_elems(const LevelGeom& g, const Pad3& p, const double* E, double* Ep, cudaStream_t s) {
+    pad3_elems_kernel<<<(unsigned)((g.nelem + 255) / 256), 256, 0, s>>>(g, p, E, Ep);
+}

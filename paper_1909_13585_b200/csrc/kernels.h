@@ -41,6 +41,8 @@ struct FineArgs {
     LevelGeom gc;
     const uint8_t* maskc;
     int off0;
+    int ep2;                // 3D: E row pitch (elements along axis 2, even)
+    int m2;                 // 3D: mask row pitch (bytes, multiple of 16)
 };
 
 void fine_set_constants(int dim, const double* K0, cudaStream_t s);
@@ -48,10 +50,27 @@ void fine_set_constants(int dim, const double* K0, cudaStream_t s);
 int fine_apply(int op, const FineArgs& a, cudaStream_t s);
 int fine_items(const LevelGeom& g, int R);
 void fine_diag(const LevelGeom& g, const double* E, const uint8_t* mask, double* Dinv, double* D, cudaStream_t s);
-// 3D structured (sum/difference basis) fine operator (h8.cu); fine_apply routes 3D here
-void h8_set_constants(const double* K0, cudaStream_t s);
-int h8_apply(int op, const FineArgs& a, cudaStream_t s);
-int h8_items(const LevelGeom& g, int R);
+// 3D structured (sum/difference basis) fine operator, TMA plane-ring march (h8t.cu); fine_apply
+// routes 3D here.  Level-0 3D vectors, masks, D^-1 (and E when N2 is odd) use the padded layout:
+struct Pad3 {
+    int p2;               // nodes per vector row (n2 rounded up to even: 16-byte TMA row strides)
+    int m2;               // bytes per mask row (n2 rounded up to 16)
+    int ep2;              // elements per E row (N2 rounded up to even)
+    long long vstride;    // doubles per RHS vector: 3 n0 n1 p2
+};
+Pad3 pad3_layout(const LevelGeom& g);
+LevelGeom pad3_geom(const LevelGeom& g, const Pad3& p);   // g with p2 / vstr of the padded vectors
+void pad3_vectors_planes(const LevelGeom& g, const Pad3& p, int R, const uint8_t* mask, int p0, int np,
+                         const double* src, long long src_ndof, double* dst, cudaStream_t s);
+void unpad3_vectors_planes(const LevelGeom& g, const Pad3& p, int R, int p0, int np, const double* src, double* dst,
+                           long long dst_ndof, cudaStream_t s);
+void pad3_nodes(const LevelGeom& g, const Pad3& p, const uint8_t* mask, uint8_t* maskp, const double* dinv,
+                double* dinvp, cudaStream_t s);
+void pad3_elems(const LevelGeom& g, const Pad3& p, const double* E, double* Ep, cudaStream_t s);
+void h8t_set_constants(const double* K0, cudaStream_t s);
+int h8t_apply(int op, const FineArgs& a, cudaStream_t s);
+int h8t_items(const LevelGeom& g, int R);
+void h8t_chunks(int TR, int minb, const LevelGeom& g, int R, int* nch_out, int* hch_out);
 
 // ---------------------------------------------------------------- 2D fused march kernels (fine2d.cu)
 enum March2Op { M2_MATVEC = 0, M2_RESID = 1, M2_JACOBI = 2, M2_CGP = 3, M2_RESTRICT = 4, M2_POST = 5 };

@@ -231,6 +231,10 @@ struct Slab {
     double *elmA = nullptr, *elmB = nullptr;
     // 2D fine level: ghost-padded copies used by the march kernels (fine2d.cu)
     Pad2 pd{};
+    // 3D fine level: row-padded layout of the TMA march kernels (h8t.cu); g0p = level-0 geometry
+    // with the padded vector pitch (maskpad / Dinvpad / Epad below hold the padded copies)
+    Pad3 p3{};
+    LevelGeom g0p{};
     double* Epad = nullptr;
     uint8_t* maskpad = nullptr;
     double* Dinvpad = nullptr;
@@ -250,7 +254,6 @@ struct mg_ctx {
     bool fused2d = false;     // 2D, L >= 2, V(1,1): fused RESTRICT / POST fine kernels
     bool unfused_coarse = false;   // MG_UNFUSED_COARSE=1: generic coarse-level kernels (A/B checks)
     bool fused3d = false;     // 3D, L >= 2, V(1,1): fused h8 RESTR3 fine kernel
-    bool fused3d_post = false;   // ... and fused POST3
     mg_opts opts{0.6, 1, 1, 1000};
     cudaStream_t user = nullptr, stream = nullptr;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
@@ -324,6 +327,8 @@ static LevelGeom make_geom(int dim, const int* N) {
         if (k < dim) { g.nnodes *= g.nn[k]; g.nelem *= g.N[k]; }
     }
     g.ndof = g.nnodes * dim;
+    g.p2 = g.nn[2];
+    g.vstr = g.ndof;
     return g;
 }
 
@@ -363,7 +368,7 @@ static mg_status ensure_constants(mg_ctx* c) {
     g_const_valid = false;
     cudaStream_t s = c->stream;
     fine_set_constants(c->dim, c->K0.data(), s);
-    if (c->dim == 3) h8_set_constants(c->K0.data(), s);
+    if (c->dim == 3) h8t_set_constants(c->K0.data(), s);
     if (c->dim == 2) fine2d_set_constants(c->K0.data(), s);
     galerkin_set_constants(c->dim, c->K0.data(), s);
     stress_set_constants(c->dim, c->nu, s);
@@ -429,9 +434,13 @@ static PlaneField node_field(const Slab& s, int l, void* base, int esize, long l
 static PlaneField vec_field(mg_ctx* c, const Slab& s, int l, double* v, int R) {
     return node_field(s, l, v, 8, c->dim, s.lv[l].g.ndof, R);
 }
-// level-0 vectors: padded in 2D, compact in 3D
+// level-0 vectors: padded in 2D (ghost ring) and in 3D (row pitch)
 static PlaneField fine_field(mg_ctx* c, const Slab& s, double* v, int R) {
-    if (c->dim != 2) return vec_field(c, s, 0, v, R);
+    if (c->dim != 2) {
+        PlaneField f = node_field(s, 0, v, 8, 3, s.p3.vstride, R);
+        f.plane_len = 3LL * s.lv[0].g.nn[1] * s.p3.p2;
+        return f;
+    }
     PlaneField f = node_field(s, 0, v + 2 * s.pd.org, 8, 2, s.pd.vstride, R);
     f.plane_len = 2LL * s.pd.pitch;
     return f;
@@ -551,6 +560,13 @@ static mg_status compute_operators(mg_ctx* c) {
     c->launches += nslab(c);
     TRY(xchg(c, [&](const Slab& sl) { return node_field(sl, 0, sl.lv[0].Dinv, 8, dim, 0, 1); }));
     TRY(xchg(c, [&](const Slab& sl) { return node_field(sl, 0, sl.lv[0].D, 8, dim, 0, 1); }));
+    if (dim == 3) {
+        for (Slab& sl : c->sl) {
+            pad3_nodes(sl.lv[0].g, sl.p3, sl.lv[0].mask, sl.maskpad, sl.lv[0].Dinv, sl.Dinvpad, s);
+            if (sl.Epad) pad3_elems(sl.lv[0].g, sl.p3, sl.E, sl.Epad, s);
+            c->launches += sl.Epad ? 2 : 1;
+        }
+    }
     if (dim == 2) {
         for (Slab& sl : c->sl) {
             pad2_elems(sl.lv[0].g, sl.pd, sl.E, sl.Epad, s);
@@ -703,9 +719,8 @@ static mg_status scatter_fine(mg_ctx* c, const double* src, int R, bool masked, 
             pad2_vectors_planes(v.g, s.pd, R, masked ? v.mask : nullptr, v.o0, np, src + 2 * s.uoff, c->n_rank,
                                 s.*dst, c->stream);
         } else {
-            CU(cudaMemcpy2DAsync(s.*dst + v.o0 * v.pn * 3, v.g.ndof * 8, src + 3 * s.uoff, c->n_rank * 8,
-                                 np * v.pn * 3 * 8, R, cudaMemcpyDeviceToDevice, c->stream));
-            if (masked) vec_mask_copy(v.g.nnodes, 3, R, v.mask, s.*dst, s.*dst, c->stream);
+            pad3_vectors_planes(v.g, s.p3, R, masked ? v.mask : nullptr, v.o0, np, src + 3 * s.uoff, c->n_rank,
+                                s.*dst, c->stream);
         }
         c->launches++;
     }
@@ -721,8 +736,8 @@ static mg_status gather_fine(mg_ctx* c, double* Slab::*src, int R, double* dst) 
             unpad2_vectors_planes(v.g, s.pd, R, v.o0, np, s.*src, dst + 2 * s.uoff, c->n_rank, c->stream);
             c->launches++;
         } else {
-            CU(cudaMemcpy2DAsync(dst + 3 * s.uoff, c->n_rank * 8, s.*src + v.o0 * v.pn * 3, v.g.ndof * 8,
-                                 np * v.pn * 3 * 8, R, cudaMemcpyDeviceToDevice, c->stream));
+            unpad3_vectors_planes(v.g, s.p3, R, v.o0, np, s.*src, dst + 3 * s.uoff, c->n_rank, c->stream);
+            c->launches++;
         }
     }
     return MG_OK;
@@ -740,6 +755,10 @@ struct Rec {
 static FineArgs fine_args(mg_ctx* c, const Slab& s, const Rec& rc) {
     FineArgs a{};
     a.g = s.lv[0].g; a.E = s.E; a.mask = s.lv[0].mask; a.omega = c->opts.omega;
+    if (c->dim == 3) {   // padded 3D fine layout (h8t.cu)
+        a.g = s.g0p; a.E = s.Epad ? s.Epad : s.E; a.mask = s.maskpad; a.Dinv = s.Dinvpad;
+        a.ep2 = s.p3.ep2; a.m2 = s.p3.m2;
+    }
     a.active = rc.active; a.done = rc.done; a.R = rc.R; a.nu_paper = c->nu_paper ? 1 : 0;
     a.so0 = s.lv[0].o0; a.so1 = s.lv[0].o1; a.pstride = c->pst;
     return a;
@@ -782,8 +801,8 @@ static void fine_own_range(mg_ctx* c, const Slab& s, long long* d0, long long* d
         *d0 = 2 * (s.pd.org + (long long)v.o0 * s.pd.pitch);
         *d1 = 2 * (s.pd.org + (long long)v.o1 * s.pd.pitch);
     } else {
-        *d0 = v.o0 * v.pn * 3;
-        *d1 = v.o1 * v.pn * 3;
+        *d0 = 3LL * v.o0 * v.g.nn[1] * s.p3.p2;
+        *d1 = 3LL * v.o1 * v.g.nn[1] * s.p3.p2;
     }
 }
 
@@ -806,7 +825,7 @@ static void level_smooth(Rec& rc, Slab& s, int l, const double* r, const double*
     mg_ctx* c = rc.c;
     if (l == 0 && c->L > 1) {
         FineArgs a = fine_args(c, s, rc);
-        a.x = z; a.b = r; a.Dinv = s.lv[0].Dinv; a.y = w; a.partial = partial;
+        a.x = z; a.b = r; a.Dinv = s.Dinvpad; a.y = w; a.partial = partial;
         level0_apply(c, s, FOP_JACOBI, a);
     } else {
         CoarseArgs a{};
@@ -947,18 +966,16 @@ static mg_status blk_restrict(Rec& rc, double* Slab::*rin, double* Slab::*rout, 
         // 3D: r = rin - alpha q, r.r, t = r - K (omega D^-1 r) in one h8 kernel, then P^T t
         for (Slab& s : c->sl) {
             FineArgs a = fine_args(c, s, rc);
-            a.rin = s.*rin; a.q = s.q; a.rout = s.*rout; a.alpha = c->ctl.alpha; a.Dinv = s.lv[0].Dinv;
+            a.rin = s.*rin; a.q = s.q; a.rout = s.*rout; a.alpha = c->ctl.alpha; a.Dinv = s.Dinvpad;
             a.y = s.t; a.partial = c->partial + off;
-            if (!c->fused3d_post) {   // the composed post-smoother needs z1
-                a.z1out = s.z;
-                s.zpre = s.z;
-            }
+            a.z1out = s.z;   // the post-smoother starts from z1 + P e
+            s.zpre = s.z;
             off += fine_apply(FOP_RESTR3, a, c->stream);
             rc.launches++;
         }
         *items = off;
         for (Slab& s : c->sl) {
-            restrict_apply(s.lv[0].g, s.lv[1].g, s.lv[0].mask, s.lv[1].mask, s.t, s.lv[1].r, R, rc.active, rc.done,
+            restrict_apply(s.g0p, s.lv[1].g, s.lv[0].mask, s.lv[1].mask, s.t, s.lv[1].r, R, rc.active, rc.done,
                            c->stream, s.gl, s.lv[0].o0, s.lv[0].o1);
             rc.launches++;
         }
@@ -967,7 +984,7 @@ static mg_status blk_restrict(Rec& rc, double* Slab::*rin, double* Slab::*rout, 
     for (Slab& s : c->sl) {
         long long d0, d1;
         fine_own_range(c, s, &d0, &d1);
-        off += cg_rupdate(s.vs, R, c->ctl.alpha, s.*rin, s.q, s.*rout, c->dim == 2 ? s.Dinvpad : s.lv[0].Dinv,
+        off += cg_rupdate(s.vs, R, c->ctl.alpha, s.*rin, s.q, s.*rout, s.Dinvpad,
                           c->opts.omega, c->L > 1 ? s.z : nullptr, c->partial + off, c->pst, d0, d1, rc.active,
                           rc.done, c->stream);
         rc.launches++;
@@ -985,7 +1002,7 @@ static mg_status blk_restrict(Rec& rc, double* Slab::*rin, double* Slab::*rout, 
         double* z = zi ? s.t : s.z;
         double* w = zi ? s.z : s.t;
         level_resid(rc, s, 0, s.*rout, z, w);
-        restrict_apply(s.lv[0].g, s.lv[1].g, s.lv[0].mask, s.lv[1].mask, w, s.lv[1].r, R, rc.active, rc.done,
+        restrict_apply(c->dim == 3 ? s.g0p : s.lv[0].g, s.lv[1].g, s.lv[0].mask, s.lv[1].mask, w, s.lv[1].r, R, rc.active, rc.done,
                        c->stream, s.gl, s.lv[0].o0, s.lv[0].o1);
         rc.launches++;
         s.zpre = z;
@@ -1013,7 +1030,11 @@ static mg_status blk_post(Rec& rc, double* Slab::*r, int cw, long long* items) {
             pad2_vectors(s.lv[0].g, s.pd, R, nullptr, c->stage2, s.zf, c->stream);
             rc.launches += 2;
         } else {
-            dense_apply(c->Ainv, c->npad, c->nL, s.*r, s.zf, R, rc.active, rc.done, c->stream);
+            const LevelGeom& g0 = s.lv[0].g;
+            unpad3_vectors_planes(g0, s.p3, R, 0, g0.nn[0], s.*r, c->stage, g0.ndof, c->stream);
+            dense_apply(c->Ainv, c->npad, c->nL, c->stage, c->stage2, R, rc.active, rc.done, c->stream);
+            pad3_vectors_planes(g0, s.p3, R, nullptr, 0, g0.nn[0], c->stage2, g0.ndof, s.zf, c->stream);
+            rc.launches += 2;
         }
         off = vec_dot_range(s.vs, 0, s.vs, R, s.*r, s.zf, c->partial, c->pst, rc.active, rc.done, c->stream);
         rc.launches += 2;
@@ -1030,20 +1051,8 @@ static mg_status blk_post(Rec& rc, double* Slab::*r, int cw, long long* items) {
         *items = off;
         return xchg(c, [&](const Slab& s) { return fine_field(c, s, s.zf, R); });
     }
-    if (c->fused3d_post) {
-        // 3D: z2 = omega D^-1 r + P e, zf = z2 + omega D^-1 (r - K z2), r.zf in one h8 kernel
-        for (Slab& s : c->sl) {
-            FineArgs a = fine_args(c, s, rc);
-            a.b = s.*r; a.Dinv = s.lv[0].Dinv; a.ec = cw ? s.lv[1].w : s.lv[1].z; a.gc = s.lv[1].g;
-            a.maskc = s.lv[1].mask; a.off0 = s.gl; a.y = s.zf; a.partial = c->partial + off;
-            off += fine_apply(FOP_POST3, a, c->stream);
-            rc.launches++;
-        }
-        *items = off;
-        return xchg(c, [&](const Slab& s) { return fine_field(c, s, s.zf, R); });
-    }
     for (Slab& s : c->sl) {
-        prolong_add(s.lv[0].g, s.lv[1].g, s.lv[0].mask, s.lv[1].mask, cw ? s.lv[1].w : s.lv[1].z, s.zpre, R,
+        prolong_add(c->dim == 3 ? s.g0p : s.lv[0].g, s.lv[1].g, s.lv[0].mask, s.lv[1].mask, cw ? s.lv[1].w : s.lv[1].z, s.zpre, R,
                     rc.active, rc.done, true, c->stream, s.gl);
         rc.launches++;
     }
@@ -1073,7 +1082,7 @@ static mg_status blk_post(Rec& rc, double* Slab::*r, int cw, long long* items) {
             Slab& s = c->sl[k];
             double* dst = last ? s.zf : (src[k] == s.z ? s.t : s.z);
             FineArgs a = fine_args(c, s, rc);
-            a.x = src[k]; a.b = s.*r; a.Dinv = s.lv[0].Dinv; a.y = dst; a.partial = last ? c->partial + off : nullptr;
+            a.x = src[k]; a.b = s.*r; a.Dinv = s.Dinvpad; a.y = dst; a.partial = last ? c->partial + off : nullptr;
             off += level0_apply(c, s, FOP_JACOBI, a);
             rc.launches++;
             src[k] = dst;
@@ -1323,17 +1332,13 @@ static mg_status setup_impl(mg_ctx* c, const mg_grid* grid, const double* E_e, c
     c->nu_paper = (c->nu == MG_NU_PAPER) && grid->element == MG_ELEM_STD;
     c->fused2d = (dim == 2 && levels >= 2);
     c->unfused_coarse = getenv("MG_UNFUSED_COARSE") && atoi(getenv("MG_UNFUSED_COARSE")) == 1;
-    // 3D fused fine kernels (opt-in, parity-tested either way), MG_FUSED3D bit 0: r update +
-    // pre-smoother + residual in one h8 kernel (RESTR3; on the plane-ring kernel as fast as
-    // cg_rupdate + RESID on B200, not faster), bit 1: prolongation + post-smoother (POST3; slower
-    // than prolong + JACOBI: more registers in a latency-bound kernel)
+    // 3D: r update + pre-smoother + residual in one h8t kernel (RESTR3) instead of cg_rupdate +
+    // RESID; MG_FUSED3D=0/1 selects (both parity-tested)
     {
         const char* e = getenv("MG_FUSED3D");
         const int f3 = e ? atoi(e) : 0;
-        const bool ok3 = dim == 3 && levels >= 2 && c->opts.nu_pre == 1 && c->opts.nu_post == 1 &&
-                         !c->unfused_coarse && !getenv("MG_DENSE_H8");
+        const bool ok3 = dim == 3 && levels >= 2 && c->opts.nu_pre == 1 && c->opts.nu_post == 1 && !c->unfused_coarse;
         c->fused3d = ok3 && (f3 & 1);
-        c->fused3d_post = ok3 && (f3 & 2);
     }
     TRY(ensure_constants(c));
     {
@@ -1404,7 +1409,18 @@ static mg_status setup_impl(mg_ctx* c, const mg_grid* grid, const double* E_e, c
             CU(cudaMalloc(&sl.Dinvpad, sizeof(double) * 2 * sl.pd.nodes));
             sl.vs = sl.pd.vstride;
         } else {
-            sl.vs = g0.ndof;
+            sl.p3 = pad3_layout(g0);
+            sl.g0p = pad3_geom(g0, sl.p3);
+            sl.vs = sl.p3.vstride;
+            CU(cudaMalloc(&sl.maskpad, (size_t)g0.nn[0] * g0.nn[1] * sl.p3.m2 + 64));
+            CU(cudaMemsetAsync(sl.maskpad, 0, (size_t)g0.nn[0] * g0.nn[1] * sl.p3.m2, s));
+            CU(cudaMalloc(&sl.Dinvpad, sizeof(double) * sl.p3.vstride));
+            CU(cudaMemsetAsync(sl.Dinvpad, 0, sizeof(double) * sl.p3.vstride, s));
+            if (sl.p3.ep2 != g0.N[2]) {
+                const size_t ne = (size_t)g0.N[0] * g0.N[1] * sl.p3.ep2;
+                CU(cudaMalloc(&sl.Epad, sizeof(double) * ne));
+                CU(cudaMemsetAsync(sl.Epad, 0, sizeof(double) * ne, s));
+            }
         }
     }
     const LevelGeom& gL = c->G[levels - 1];
@@ -2316,7 +2332,7 @@ mg_status mg_matvec(mg_handle c, int level, const double* x, int nrhs, double* y
     if (multi(c) && level > 0) return fail(MG_ERR_ARG, "coarse-level diagnostics need a single slab");
     API_SCOPE(c);
     if (level == 0) {
-        if (c->dim == 2 || multi(c)) {   // rank layout <-> slab layout around the fine kernels
+        {   // rank layout <-> padded slab layout around the fine kernels
             TRY(ensure_vectors(c, nrhs));
             TRY(scatter_fine(c, x, nrhs, false, &Slab::t));
             Rec all{c, nrhs, nullptr, nullptr};
@@ -2327,13 +2343,6 @@ mg_status mg_matvec(mg_handle c, int level, const double* x, int nrhs, double* y
                 c->launches++;
             }
             TRY(gather_fine(c, &Slab::q, nrhs, y));
-        } else {
-            Slab& s = c->sl[0];
-            Rec all{c, nrhs, nullptr, nullptr};
-            FineArgs a = fine_args(c, s, all);
-            a.x = x; a.y = y;
-            fine_apply(FOP_MATVEC, a, c->stream);
-            c->launches++;
         }
     } else {
         Slab& s = c->sl[0];

@@ -29,12 +29,14 @@ __global__ void restrict_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* __res
     }
     const int f0 = 2 * ci[0] - off0, f1 = 2 * ci[1], f2 = DIM == 3 ? 2 * ci[2] : 0;
     const int n1 = gf.nn[1], n2 = DIM == 3 ? gf.nn[2] : 1;
+    const int p2 = DIM == 3 ? gf.p2 : 1;   // vector row pitch (padded 3D fine level) vs mask pitch n2
     const long long fbase = ((long long)f0 * n1 + f1) * n2 + f2;
+    const long long vfbase = ((long long)f0 * n1 + f1) * p2 + f2;
     const int mcb = mc[I];
     {   // one RHS per thread (grid.y): enough independent loads in flight on small levels
         const int r = blockIdx.y;
         if (active && !active[r]) return;
-        const double* fv = fine + (long long)r * gf.ndof;
+        const double* fv = fine + (long long)r * gf.vstr;
         double acc[DIM];
 #pragma unroll
         for (int k = 0; k < DIM; ++k) acc[k] = 0.0;
@@ -49,10 +51,11 @@ __global__ void restrict_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* __res
                             (DIM == 2 || (f2 + d2 >= 0 && f2 + d2 < n2));
             if (!ok) continue;
             const long long q = fbase + ((long long)d0 * n1 + d1) * n2 + d2;
+            const long long qv = vfbase + ((long long)d0 * n1 + d1) * p2 + d2;
             const int fm = mf[q];
 #pragma unroll
             for (int k = 0; k < DIM; ++k)
-                if (!((fm >> k) & 1)) acc[k] = fma(w, fv[DIM * q + k], acc[k]);
+                if (!((fm >> k) & 1)) acc[k] = fma(w, fv[DIM * qv + k], acc[k]);
         }
         double* cv = coarse + (long long)r * gc.ndof + DIM * I;
 #pragma unroll
@@ -86,6 +89,8 @@ __global__ void prolong_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* __rest
     int fi[3] = {0, 0, 0};
     long long t = i;
     for (int k = DIM - 1; k >= 0; --k) { fi[k] = (int)(t % gf.nn[k]); t /= gf.nn[k]; }
+    // vector index of fine node i (row pitch p2 on the padded 3D fine level; masks stay compact)
+    const long long iv = DIM == 3 ? ((long long)fi[0] * gf.nn[1] + fi[1]) * gf.p2 + fi[2] : i;
     fi[0] += off0;   // shifted so that coarse plane I is coincident with fi[0] = 2I
     const int mfb = mf[i];
     constexpr int NC = 1 << DIM;
@@ -120,7 +125,7 @@ __global__ void prolong_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* __rest
 #pragma unroll
             for (int k = 0; k < DIM; ++k)
                 if (!((cm[s] >> k) & 1)) acc[k] = fma(wgt[s], cv[DIM * cn[s] + k], acc[k]);
-        double* fv = fine + (long long)r * gf.ndof + DIM * i;
+        double* fv = fine + (long long)r * gf.vstr + DIM * iv;
 #pragma unroll
         for (int k = 0; k < DIM; ++k) {
             double v = ((mfb >> k) & 1) ? 0.0 : acc[k];
