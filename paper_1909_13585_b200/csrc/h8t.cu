@@ -156,27 +156,32 @@ __device__ __forceinline__ void t_tma4(void* dst, const CUtensorMap* m, int c0, 
 //   MATVEC: A = x            RESID: A = x, B = b            JACOBI: A = x, B = b, C = D^-1
 //   CGP:    A = p_in, B = z, C = x (deferred update; optional)
 //   RESTR3: A = r_in, B = q, C = D^-1
+// TMA requires the innermost box start to be 16-byte aligned, so the boxes start left of the
+// tile (c0 = 30 tc - 1 is odd): vectors at node c0 - 1 (100 doubles = 33 nodes + 1 per row), E at
+// element c0 - 1 (34 per row), masks at the 16-byte boundary at or below c0 - 1 (48 bytes per row).
+static constexpr int T_VW = 100, T_EW = 34, T_MW = 48;
+__host__ __device__ constexpr int t_r128(int b) { return (b + 127) / 128 * 128; }
 template <int OP, int TR>
 struct TL {
     static constexpr int BR = TR + 1;                    // node rows per box
     static constexpr bool HB = OP != FOP_MATVEC;
     static constexpr bool HC = OP == FOP_JACOBI || OP == FOP_CGP || OP == FOP_RESTR3;
-    static constexpr int VB = BR * 96 * 8;               // vector box bytes (BR rows x 32 nodes x 3)
-    static constexpr int EB = TR * 32 * 8;               // E box bytes
-    static constexpr int MB = BR * 32;                   // mask box bytes
+    static constexpr int VB = BR * T_VW * 8;             // vector box bytes
+    static constexpr int EB = TR * T_EW * 8;             // E box bytes
+    static constexpr int MB = BR * T_MW;                 // mask box bytes
     static constexpr int OA = 0;
-    static constexpr int OB = OA + VB;
-    static constexpr int OC = OB + (HB ? VB : 0);
-    static constexpr int OE = OC + (HC ? VB : 0);
-    static constexpr int OM = OE + EB;
-    static constexpr int SLOT = (OM + MB + 127) / 128 * 128;
+    static constexpr int OB = OA + t_r128(VB);
+    static constexpr int OC = OB + (HB ? t_r128(VB) : 0);
+    static constexpr int OE = OC + (HC ? t_r128(VB) : 0);
+    static constexpr int OM = OE + t_r128(EB);
+    static constexpr int SLOT = t_r128(OM + MB);
     static constexpr int SINV = 2 * TR * 6 * 32 * 8;    // double-buffered row -> row+1 exchange
 };
 
 template <int OP, int TR, int NS>
 static constexpr size_t h8t_smem_bytes() {
     using T = TL<OP, TR>;
-    return (size_t)NS * T::SLOT + T::SINV + 8 * (NS + 4 * TR) + 4 * NS + 8 * TR + 128;
+    return (size_t)NS * T::SLOT + T::SINV + 8 * (NS + 4 * TR) + 8 * NS + 8 * TR + 128;
 }
 
 // per-slot expected TMA bytes (zero-filled out-of-range elements count too)
@@ -204,7 +209,7 @@ __global__ void __launch_bounds__(32 * TR, MINB)
     uint64_t* sfull = full + NS;                                                         // [2][TR]
     uint64_t* sempty = sfull + 2 * TR;                                                   // [2][TR]
     int* cnt = reinterpret_cast<int*>(sempty + 2 * TR);                                  // [NS]
-    double* s_dot = reinterpret_cast<double*>(t_sm + NS * T::SLOT + T::SINV + 8 * (NS + 4 * TR) + 4 * NS + 8);
+    double* s_dot = reinterpret_cast<double*>(t_sm + NS * T::SLOT + T::SINV + 8 * (NS + 4 * TR) + 8 * NS);
 
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int R = a.R;
@@ -218,6 +223,8 @@ __global__ void __launch_bounds__(32 * TR, MINB)
     const int n0 = a.g.nn[0], n1 = a.g.nn[1], n2 = a.g.nn[2];
     const int p2 = a.g.p2;
     const int c0 = 30 * tc - 1, j0 = OWNR * tr - 1;
+    const int cm0 = (c0 - 1) & ~15;   // mask box start (16-byte aligned)
+    const int mlane = lane + (c0 - cm0);
     const int j = j0 + w, c = c0 + lane;
     const bool own = w >= 1 && lane >= 1 && lane <= 30 && j < n1 && c < n2;
     const int i0 = ch * hch, i1 = min(i0 + hch, n0);
@@ -247,23 +254,24 @@ __global__ void __launch_bounds__(32 * TR, MINB)
         const int s = q % NS, Q = i0 - 1 + q;
         unsigned char* sl = ring + s * T::SLOT;
         t_mbar_expect_tx(&full[s], txb);
-        t_tma4(sl + T::OA, &tm.A, 3 * c0, j0, Q, r, &full[s]);
-        if (T::HB) t_tma4(sl + T::OB, &tm.B, 3 * c0, j0, Q, r, &full[s]);
+        const int cv = 3 * (c0 - 1);
+        t_tma4(sl + T::OA, &tm.A, cv, j0, Q, r, &full[s]);
+        if (T::HB) t_tma4(sl + T::OB, &tm.B, cv, j0, Q, r, &full[s]);
         if (T::HC && hasC) {
-            if (OP == FOP_CGP) t_tma4(sl + T::OC, &tm.C, 3 * c0, j0, Q, r, &full[s]);
-            else t_tma3(sl + T::OC, &tm.C, 3 * c0, j0, Q, &full[s]);
+            if (OP == FOP_CGP) t_tma4(sl + T::OC, &tm.C, cv, j0, Q, r, &full[s]);
+            else t_tma3(sl + T::OC, &tm.C, cv, j0, Q, &full[s]);
         }
-        t_tma3(sl + T::OE, &tm.E, c0, j0, Q, &full[s]);
-        t_tma3(sl + T::OM, &tm.M, c0, j0, Q, &full[s]);
+        t_tma3(sl + T::OE, &tm.E, c0 - 1, j0, Q, &full[s]);
+        t_tma3(sl + T::OM, &tm.M, cm0, j0, Q, &full[s]);
     };
     if (threadIdx.x == 0)
         for (int q = 0; q < NS && q < nq; ++q) issue(q);
 
-    auto fA = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OA) + row * 96 + 3 * lane; };
-    auto fB = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OB) + row * 96 + 3 * lane; };
-    auto fC = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OC) + row * 96 + 3 * lane; };
-    auto fE = [&](int s) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OE)[w * 32 + lane]; };
-    auto fM = [&](int s, int row) { return (int)(ring + s * T::SLOT + T::OM)[row * 32 + lane]; };
+    auto fA = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OA) + row * T_VW + 3 * (lane + 1); };
+    auto fB = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OB) + row * T_VW + 3 * (lane + 1); };
+    auto fC = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OC) + row * T_VW + 3 * (lane + 1); };
+    auto fE = [&](int s) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OE)[w * T_EW + lane + 1]; };
+    auto fM = [&](int s, int row) { return (int)(ring + s * T::SLOT + T::OM)[row * T_MW + mlane]; };
 
     // operator input of box row `row` at slot s: raw (unmasked) and u (masked, fed to the element)
     auto input = [&](int s, int row, double (&raw)[3], double (&u)[3], int& m) {
@@ -501,7 +509,7 @@ static bool t_map_vec(CUtensorMap* m, const FineArgs& a, const double* v, int BR
     const LevelGeom& g = a.g;
     cuuint64_t dims[4] = {(cuuint64_t)3 * g.nn[2], (cuuint64_t)g.nn[1], (cuuint64_t)g.nn[0], (cuuint64_t)std::max(a.R, 1)};
     cuuint64_t str[3] = {(cuuint64_t)3 * g.p2 * 8, (cuuint64_t)3 * g.p2 * g.nn[1] * 8, (cuuint64_t)g.vstr * 8};
-    cuuint32_t box[4] = {96, (cuuint32_t)BR, 1, 1};
+    cuuint32_t box[4] = {(cuuint32_t)T_VW, (cuuint32_t)BR, 1, 1};
     return t_map(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, perR ? 4 : 3, v, dims, str, box);
 }
 
@@ -524,13 +532,13 @@ static bool launch_h8t_t(const FineArgs& a, cudaStream_t s) {
     {
         cuuint64_t dims[3] = {(cuuint64_t)g.N[2], (cuuint64_t)g.N[1], (cuuint64_t)g.N[0]};
         cuuint64_t str[2] = {(cuuint64_t)a.ep2 * 8, (cuuint64_t)a.ep2 * g.N[1] * 8};
-        cuuint32_t box[3] = {32, (cuuint32_t)TR, 1};
+        cuuint32_t box[3] = {(cuuint32_t)T_EW, (cuuint32_t)TR, 1};
         ok = ok && t_map(&tm.E, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, a.E, dims, str, box);
     }
     {
         cuuint64_t dims[3] = {(cuuint64_t)g.nn[2], (cuuint64_t)g.nn[1], (cuuint64_t)g.nn[0]};
         cuuint64_t str[2] = {(cuuint64_t)a.m2, (cuuint64_t)a.m2 * g.nn[1]};
-        cuuint32_t box[3] = {32, (cuuint32_t)T::BR, 1};
+        cuuint32_t box[3] = {(cuuint32_t)T_MW, (cuuint32_t)T::BR, 1};
         ok = ok && t_map(&tm.M, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, a.mask, dims, str, box);
     }
     if (!ok) return false;
