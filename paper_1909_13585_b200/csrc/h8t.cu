@@ -161,7 +161,7 @@ __device__ __forceinline__ void t_tma4(void* dst, const CUtensorMap* m, int c0, 
 // element c0 - 1 (34 per row), masks at the 16-byte boundary at or below c0 - 1 (48 bytes per row).
 static constexpr int T_VW = 100, T_EW = 34, T_MW = 48;
 __host__ __device__ constexpr int t_r128(int b) { return (b + 127) / 128 * 128; }
-template <int OP, int TR>
+template <int OP, int TR, int NB>
 struct TL {
     static constexpr int BR = TR + 1;                    // node rows per box
     static constexpr bool HB = OP != FOP_MATVEC;
@@ -175,19 +175,19 @@ struct TL {
     static constexpr int OE = OC + (HC ? t_r128(VB) : 0);
     static constexpr int OM = OE + t_r128(EB);
     static constexpr int SLOT = t_r128(OM + MB);
-    static constexpr int SINV = 2 * TR * 6 * 32 * 8;    // double-buffered row -> row+1 exchange
+    static constexpr int SINV = NB * TR * 6 * 32 * 8;   // row -> row+1 exchange, NB buffers
 };
 
-template <int OP, int TR, int NS>
+template <int OP, int TR, int NS, int NB>
 static constexpr size_t h8t_smem_bytes() {
-    using T = TL<OP, TR>;
-    return (size_t)NS * T::SLOT + T::SINV + 8 * (NS + 4 * TR) + 8 * NS + 8 * TR + 128;
+    using T = TL<OP, TR, NB>;
+    return (size_t)NS * T::SLOT + T::SINV + 8 * (NS + 2 * NB * TR) + 8 * NS + 8 * TR;
 }
 
 // per-slot expected TMA bytes (zero-filled out-of-range elements count too)
 template <int OP, int TR>
 __host__ __device__ constexpr unsigned h8t_tx_bytes(bool hasC) {
-    using T = TL<OP, TR>;
+    using T = TL<OP, TR, 1>;
     return (unsigned)(T::VB + (T::HB ? T::VB : 0) + ((T::HC && hasC) ? T::VB : 0) + T::EB + T::MB);
 }
 
@@ -195,21 +195,21 @@ struct H8TMaps {
     CUtensorMap A, B, C, E, M;
 };
 
-template <int OP, bool C03, int TR, int NS, int MINB>
+template <int OP, bool C03, int TR, int NS, int NB, int MINB>
 __global__ void __launch_bounds__(32 * TR, MINB)
     h8t_kernel(const __grid_constant__ FineArgs a, const __grid_constant__ H8TMaps tm, int ntc, int ntr, int nch,
                int hch, int hasC) {
     pdl_begin();
-    using T = TL<OP, TR>;
+    using T = TL<OP, TR, NB>;
     constexpr int OWNR = TR - 1;
     extern __shared__ __align__(128) unsigned char t_sm[];
     unsigned char* ring = t_sm;
-    double* sinv = reinterpret_cast<double*>(t_sm + NS * T::SLOT);                       // [2][TR][6][32]
+    double* sinv = reinterpret_cast<double*>(t_sm + NS * T::SLOT);                       // [NB][TR][6][32]
     uint64_t* full = reinterpret_cast<uint64_t*>(t_sm + NS * T::SLOT + T::SINV);         // [NS]
-    uint64_t* sfull = full + NS;                                                         // [2][TR]
-    uint64_t* sempty = sfull + 2 * TR;                                                   // [2][TR]
-    int* cnt = reinterpret_cast<int*>(sempty + 2 * TR);                                  // [NS]
-    double* s_dot = reinterpret_cast<double*>(t_sm + NS * T::SLOT + T::SINV + 8 * (NS + 4 * TR) + 8 * NS);
+    uint64_t* sfull = full + NS;                                                         // [NB][TR]
+    uint64_t* sempty = sfull + NB * TR;                                                  // [NB][TR]
+    int* cnt = reinterpret_cast<int*>(sempty + NB * TR);                                 // [NS]
+    double* s_dot = reinterpret_cast<double*>(t_sm + NS * T::SLOT + T::SINV + 8 * (NS + 2 * NB * TR) + 8 * NS);
 
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int R = a.R;
@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(32 * TR, MINB)
             t_mbar_init(&full[s], 1);
             cnt[s] = 0;
         }
-        for (int b = 0; b < 2 * TR; ++b) {
+        for (int b = 0; b < NB * TR; ++b) {
             t_mbar_init(&sfull[b], 1);
             t_mbar_init(&sempty[b], 1);
         }
@@ -388,10 +388,10 @@ __global__ void __launch_bounds__(32 * TR, MINB)
         if (L >= i0) {
             // rows: own row w gets fm - fd, row w + 1 gets fm + fd (through the exchange)
             const int o = L - i0;
-            const int bi = o & 1;
-            const unsigned ph = (unsigned)((o >> 1) & 1);
+            const int bi = o % NB;
+            const unsigned ph = (unsigned)((o / NB) & 1);
             if (w < TR - 1) {
-                if (o >= 2) t_mbar_wait(&sempty[bi * TR + w], ph ^ 1u);
+                if (o >= NB) t_mbar_wait(&sempty[bi * TR + w], ph ^ 1u);
                 double* dst = sinv + ((bi * TR + w) * 6) * 32 + lane;
 #pragma unroll
                 for (int k = 0; k < 3; ++k) {
@@ -513,9 +513,9 @@ static bool t_map_vec(CUtensorMap* m, const FineArgs& a, const double* v, int BR
     return t_map(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, perR ? 4 : 3, v, dims, str, box);
 }
 
-template <int OP, int TR, int NS, int MINB>
+template <int OP, int TR, int NS, int NB, int MINB>
 static bool launch_h8t_t(const FineArgs& a, cudaStream_t s) {
-    using T = TL<OP, TR>;
+    using T = TL<OP, TR, NB>;
     const LevelGeom& g = a.g;
     const int ntc = (g.nn[2] + 29) / 30;
     const int ntr = (g.nn[1] + TR - 2) / (TR - 1);
@@ -542,9 +542,9 @@ static bool launch_h8t_t(const FineArgs& a, cudaStream_t s) {
         ok = ok && t_map(&tm.M, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, a.mask, dims, str, box);
     }
     if (!ok) return false;
-    const size_t smem = h8t_smem_bytes<OP, TR, NS>();
-    auto k03 = h8t_kernel<OP, true, TR, NS, MINB>;
-    auto kgn = h8t_kernel<OP, false, TR, NS, MINB>;
+    const size_t smem = h8t_smem_bytes<OP, TR, NS, NB>();
+    auto k03 = h8t_kernel<OP, true, TR, NS, NB, MINB>;
+    auto kgn = h8t_kernel<OP, false, TR, NS, NB, MINB>;
     static bool attr = [&] {
         cudaFuncSetAttribute(k03, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(kgn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -566,7 +566,15 @@ static int h8t_tr() {
     }();
     return tr;
 }
-static constexpr int H8T_NS = 3;
+// ring depth / exchange buffers: MG_H8T_RING = 4 (4 plane slots, single row-exchange buffer) or 3
+// (3 slots, double buffer)
+static int h8t_ring() {
+    static int v = [] {
+        const char* e = getenv("MG_H8T_RING");
+        return (e && atoi(e) == 3) ? 3 : 4;
+    }();
+    return v;
+}
 
 // chunking along axis 0: between 16 and 64 planes per chunk, picked so that the CTA count fills
 // the resident slots (148 SMs x CTAs per SM) with the smallest tail wave
@@ -601,8 +609,9 @@ int h8t_items(const LevelGeom& g, int R) {
 
 template <int OP>
 static bool launch_h8t_op(const FineArgs& a, cudaStream_t s) {
-    if (h8t_tr() == 8) return launch_h8t_t<OP, 8, H8T_NS, 2>(a, s);
-    return launch_h8t_t<OP, 16, H8T_NS, 1>(a, s);
+    if (h8t_tr() == 8)
+        return h8t_ring() == 3 ? launch_h8t_t<OP, 8, 3, 2, 2>(a, s) : launch_h8t_t<OP, 8, 4, 1, 2>(a, s);
+    return h8t_ring() == 3 ? launch_h8t_t<OP, 16, 3, 2, 1>(a, s) : launch_h8t_t<OP, 16, 4, 1, 1>(a, s);
 }
 
 int h8t_apply(int op, const FineArgs& a, cudaStream_t s) {
