@@ -31,6 +31,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "element.cuh"
 #include "kernels.h"
@@ -130,7 +131,7 @@ __device__ __forceinline__ void t_mbar_wait(uint64_t* b, unsigned parity) {
         "{\n"
         ".reg .pred p;\n"
         "T_WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 0x989680;\n"
         "@!p bra T_WAIT_%=;\n"
         "}\n" ::"r"(t_smem(b)),
         "r"(parity)
@@ -310,11 +311,14 @@ __global__ void __launch_bounds__(32 * TR, MINB)
 
     // one step: element layer L between node planes L (faces FL, own raw rawL / mask mL) and
     // P = L + 1 (faces FP, rawP, mP computed here); outputs node plane L when L >= i0
-    auto step = [&](int L, const double (&FL)[3][4], double (&FP)[3][4], const double (&rawL)[3], double (&rawP)[3],
+    // KC = (L - (i0 - 1)) % NS when the march is unrolled by NS (slot offsets become immediates), or
+    // std::integral_constant<int, -1> for a runtime slot
+    auto step = [&](auto KC, int L, const double (&FL)[3][4], double (&FP)[3][4], const double (&rawL)[3], double (&rawP)[3],
                     int mL, int& mP) {
         const int P = L + 1;
         const int qP = P - (i0 - 1), qL = L - (i0 - 1);
-        const int sP = qP % NS, sL = qL % NS;
+        constexpr int KS = decltype(KC)::value;
+        const int sP = KS >= 0 ? (KS + 1) % NS : qP % NS, sL = KS >= 0 ? KS : qL % NS;
         t_mbar_wait(&full[sP], (unsigned)((qP / NS) & 1));
         {
             double uo[3], uu[3], ru[3];
@@ -459,9 +463,23 @@ __global__ void __launch_bounds__(32 * TR, MINB)
         input(0, w + 1, ru, uu, mu);
         face(uo, uu, FA);
     }
-    for (int L = i0 - 1; L < i1; L += 2) {
-        step(L, FA, FB, rawA, rawB, mA, mB);
-        if (L + 1 < i1) step(L + 1, FB, FA, rawB, rawA, mB, mA);
+    using I0 = std::integral_constant<int, 0>;
+    using I1 = std::integral_constant<int, 1>;
+    using I2 = std::integral_constant<int, 2>;
+    using I3 = std::integral_constant<int, 3>;
+    using IR = std::integral_constant<int, -1>;
+    if constexpr (NS == 4) {   // unrolled by the ring depth: every slot offset is a constant
+        for (int L = i0 - 1; L < i1; L += 4) {
+            step(I0{}, L, FA, FB, rawA, rawB, mA, mB);
+            if (L + 1 < i1) step(I1{}, L + 1, FB, FA, rawB, rawA, mB, mA);
+            if (L + 2 < i1) step(I2{}, L + 2, FA, FB, rawA, rawB, mA, mB);
+            if (L + 3 < i1) step(I3{}, L + 3, FB, FA, rawB, rawA, mB, mA);
+        }
+    } else {
+        for (int L = i0 - 1; L < i1; L += 2) {
+            step(IR{}, L, FA, FB, rawA, rawB, mA, mB);
+            if (L + 1 < i1) step(IR{}, L + 1, FB, FA, rawB, rawA, mB, mA);
+        }
     }
     if (a.partial) {
         dot = warp_sum(dot);
