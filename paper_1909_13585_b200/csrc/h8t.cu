@@ -575,21 +575,22 @@ static bool launch_h8t_t(const FineArgs& a, cudaStream_t s) {
     return true;
 }
 
-// warps per CTA (TR) and ring depth; MG_H8T_TR = 8 (2 CTAs / SM) or 16 (1 CTA / SM)
+// warps per CTA: MG_H8T_TR = 8 (2 CTAs / SM, default: B200 C5 A/B 147.8 vs 151.5 ms/step) or 16
+// (1 CTA / SM: less tile overlap, but a whole SM waits on one CTA's slowest warp)
 static int h8t_tr() {
     static int tr = [] {
         const char* e = getenv("MG_H8T_TR");
-        const int v = e ? atoi(e) : 16;
-        return v == 8 ? 8 : 16;
+        const int v = e ? atoi(e) : 8;
+        return v == 16 ? 16 : 8;
     }();
     return tr;
 }
-// ring depth / exchange buffers: MG_H8T_RING = 4 (4 plane slots, single row-exchange buffer) or 3
-// (3 slots, double buffer)
+// ring depth / exchange buffers: MG_H8T_RING = 3 (3 plane slots, double row-exchange buffer,
+// default) or 4 (4 slots, single buffer, march unrolled by 4: more spills, B200 C5 +7%)
 static int h8t_ring() {
     static int v = [] {
         const char* e = getenv("MG_H8T_RING");
-        return (e && atoi(e) == 3) ? 3 : 4;
+        return (e && atoi(e) == 4) ? 4 : 3;
     }();
     return v;
 }

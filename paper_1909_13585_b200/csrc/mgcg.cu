@@ -1332,11 +1332,11 @@ static mg_status setup_impl(mg_ctx* c, const mg_grid* grid, const double* E_e, c
     c->nu_paper = (c->nu == MG_NU_PAPER) && grid->element == MG_ELEM_STD;
     c->fused2d = (dim == 2 && levels >= 2);
     c->unfused_coarse = getenv("MG_UNFUSED_COARSE") && atoi(getenv("MG_UNFUSED_COARSE")) == 1;
-    // 3D: r update + pre-smoother + residual in one h8t kernel (RESTR3) instead of cg_rupdate +
-    // RESID; MG_FUSED3D=0/1 selects (both parity-tested)
+    // 3D: r update + pre-smoother + residual in one h8t kernel (RESTR3, default) instead of
+    // cg_rupdate + RESID (MG_FUSED3D=0); both parity-tested
     {
         const char* e = getenv("MG_FUSED3D");
-        const int f3 = e ? atoi(e) : 0;
+        const int f3 = e ? atoi(e) : 1;
         const bool ok3 = dim == 3 && levels >= 2 && c->opts.nu_pre == 1 && c->opts.nu_post == 1 && !c->unfused_coarse;
         c->fused3d = ok3 && (f3 & 1);
     }
