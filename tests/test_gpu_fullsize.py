@@ -159,7 +159,7 @@ def test_fullsize_C5_solution_vs_oracle_golden():
     assert len(g["rhs"]) == cfg.nrhs
     for e in g["rhs"]:
         k = e["k"]
-        assert e["relres"] <= 1e-12                      # the stored oracle solution itself
+        assert e["relres"] <= 1e-11   # the stored oracle solution itself (fp64 floor of a true residual)
         ref = np.array(e["values"])
         got = X[k][idx]
         assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-8, k
