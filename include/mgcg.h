@@ -189,11 +189,15 @@ mg_status mgcg_block_solve(mg_handle h, const double* rhs, int nrhs, double tol,
  *      Rayleigh-Ritz on the (q+8)-dimensional subspace;
  *   2. Psi = I^1_2 ... I^{l-1}_l Psi^l (prolongation to the fine level);
  *   3. K Phi~ = G Psi (Eq. 7) by block PCG (mgcg_block_solve, mgBPCG) to tol;
- *   4. lambda~_i = -phi~_i^T K phi~_i / phi~_i^T G phi~_i (Eq. 8).
+ *   4. lambda~_i = -phi~_i^T K phi~_i / phi~_i^T G phi~_i (Eq. 8); the returned modes are
+ *      K-normalised, phi~_i^T K phi~_i = 1, and the residual of the first pair,
+ *      y = (K + lambda~_1 G) phi~_1 (Eq. 7), is formed on request.
  *   Es_e (nelem), u (ndof): device; Phi (q, ndof) device output; lam_tilde (q) host output;
- *   lam_coarse (q) host output or NULL.  1 <= q <= 32, levels >= 2, single slab. Synchronous. */
+ *   lam_coarse (q) host output or NULL; y1 (ndof) device output or NULL; yres (2) host output or
+ *   NULL: ||y||_2 and ||y||_2 / ||K phi~_1||_2.  1 <= q <= 32, levels >= 2, single slab.
+ *   Synchronous. */
 mg_status mg_multilevel_modes(mg_handle h, const double* Es_e, const double* u, int q, double tol, double* Phi,
-                              double* lam_tilde, double* lam_coarse);
+                              double* lam_tilde, double* lam_coarse, double* y1, double* yres);
 
 /* y_k = G(u) phi_k for k < nphi (PAPER.md:99 G_e = E_sigma G_e0[u_e]; Eq. 6 :163):
  *   Es_e  device, nelem fp64 stress moduli E_sigma(x_e) = x_e^p E_1 (Eq. 2 :106).

@@ -5,7 +5,9 @@ SURVEY.md 8(f) NEXT-2; the four steps of PAPER.md:146-175 (Sec. 2.1, Eq. 6-8):
     the fine operators (Eq. 6, :153-157), q lowest positive lambda^l;
  2. Psi^j = I^j_{j+1} Psi^{j+1} down to the fine level (:160);
  3. fine BVP K Phi~ = G Psi (Eq. 7, :163-167);
- 4. Rayleigh quotients lambda~_i = -phi~_i^T K phi~_i / phi~_i^T G phi~_i (Eq. 8, :170-175).
+ 4. Rayleigh quotients lambda~_i = -phi~_i^T K phi~_i / phi~_i^T G phi~_i (Eq. 8, :170-175);
+    the modes are returned normalised as phi~_i^T K phi~_i = 1, and
+    `eigen_residual` gives y = (K + lambda~_1 G) phi~_1 (Eq. 7).
 
 K^l = P^T K P + (I - F_l) (identity on fixed coarse DOFs, like the multigrid hierarchy) and
 G^l = P^T G P with P the composition of the masked prolongations; the coarse
@@ -22,7 +24,7 @@ from .mg import Hierarchy
 
 
 def multilevel_modes(nel, E, Es, fixed, u, levels, q, nu=0.3, element="std"):
-    """Returns (lam_coarse (q,), Psi (q, n), Phi (q, n), lam_tilde (q,))."""
+    """Returns (lam_coarse (q,), Psi (q, n), Phi (q, n), lam_tilde (q,)); Phi K-normalised."""
     K = assemble.assemble_K(nel, E, fixed, nu, element)
     G = assemble.assemble_G(nel, Es, u, fixed, nu)
     H = Hierarchy(nel, K, fixed, levels)
@@ -46,4 +48,12 @@ def multilevel_modes(nel, E, Es, fixed, u, levels, q, nu=0.3, element="std"):
     Phi = solve.direct_solve(K, rhs, fixed)
     num = np.einsum("in,in->i", Phi, np.asarray((K @ Phi.T).T))
     den = np.einsum("in,in->i", Phi, np.asarray((G @ Phi.T).T))
+    Phi = Phi / np.sqrt(num)[:, None]            # phi~^T K phi~ = 1
     return lam_c, Psi, Phi, -num / den
+
+
+def eigen_residual(nel, E, Es, fixed, u, lam1, phi1, nu=0.3, element="std"):
+    """Eq. 7: y = (K[x] + lambda~_1 G[x, u]) phi~_1, with the assembled K and G."""
+    K = assemble.assemble_K(nel, E, fixed, nu, element)
+    G = assemble.assemble_G(nel, Es, u, fixed, nu)
+    return np.asarray(K @ phi1 + lam1 * (G @ phi1))

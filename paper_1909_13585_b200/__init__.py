@@ -201,15 +201,24 @@ def mgcg_block_solve(h, rhs, tol, x, raise_on_error=True):
     return out
 
 
-def mg_multilevel_modes(h, Es, u, q, Phi, tol=1e-10):
-    """Sec. 2.1 multilevel modes: fills Phi (q, ndof) and returns (lam_tilde, lam_coarse) lists."""
+def mg_multilevel_modes(h, Es, u, q, Phi, tol=1e-10, y1=None, with_residual=False):
+    """Sec. 2.1 multilevel modes: fills Phi (q, ndof) with K-normalised modes and returns
+    (lam_tilde, lam_coarse) lists, plus (||y||, ||y|| / ||K phi~_1||) of the Eq. 7 residual
+    y = (K + lam~_1 G) phi~_1 when with_residual (y1, if given, receives y)."""
     _need_len(Es, h.nelem, "Es")
     _need_len(u, h.ndof, "u")
     _need_rows(Phi, h.ndof, "Phi", q)
+    if y1 is not None:
+        _need_len(y1, h.ndof, "y1")
     lt = np.zeros(q)
     lc = np.zeros(q)
+    yr = np.zeros(2)
     check(lib.mg_multilevel_modes(h.raw, _ptr(Es, np.float64), _ptr(u, np.float64), q, tol, _ptr(Phi, np.float64),
-                                  _ptr(lt, np.float64), _ptr(lc, np.float64)))
+                                  _ptr(lt, np.float64), _ptr(lc, np.float64),
+                                  _ptr(y1, np.float64) if y1 is not None else None,
+                                  _ptr(yr, np.float64) if with_residual else None))
+    if with_residual:
+        return list(lt), list(lc), (float(yr[0]), float(yr[1]))
     return list(lt), list(lc)
 
 

@@ -99,7 +99,7 @@ def _load():
         "mg_update_modulus": ([P, P], I),
         "mgcg_solve": ([P, P, I, D, P, ctypes.POINTER(MgReport)], I),
         "mgcg_block_solve": ([P, P, I, D, P, ctypes.POINTER(MgReport)], I),
-        "mg_multilevel_modes": ([P, P, P, I, D, P, P, P], I),
+        "mg_multilevel_modes": ([P, P, P, I, D, P, P, P, P, P], I),
         "stress_stiffness_apply": ([P, P, P, P, I, P], I),
         "mg_adjoint_rhs": ([P, P, P, I, P], I),
         "mg_eigen_sensitivity": ([P, P, P, P, P, P, P, I, P], I),

@@ -196,3 +196,19 @@ __global__ void block_conv_kernel(int R, const double* __restrict__ partial, int
 void block_conv(int R, const double* partial, int items, double tol, CgCtl c, cudaStream_t s) {
     block_conv_kernel<<<1, 512, 0, s>>>(R, partial, items, tol, c);
 }
+
+// ---------------------------------------------------------------- NEXT-2 mode post-processing
+// Phi_i *= s_i (K normalisation) and, if y1, the Eq. 7 residual of the first pair
+// y1 = s_0 (K phi_0 + lambda_1 G phi_0) = (K + lambda~_1 G) phi~_1.
+__global__ void modes_finish_kernel(long long n, int q, double* Phi, const double* KPhi, const double* GPhi,
+                                    const double* sc, double lam1, double* y1) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int k = 0; k < q; ++k) Phi[(long long)k * n + i] *= sc[k];
+    if (y1) y1[i] = sc[0] * fma(lam1, GPhi[i], KPhi[i]);
+}
+
+void modes_finish(long long n, int q, double* Phi, const double* KPhi, const double* GPhi, const double* sc,
+                  double lam1, double* y1, cudaStream_t s) {
+    modes_finish_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, q, Phi, KPhi, GPhi, sc, lam1, y1);
+}

@@ -239,3 +239,5 @@ void block_coef(int R, const double* Gam, const double* Rho, double* C, double t
 void block_axpy(long long n, long long stride, int R, const double* X, const double* C, const double* base, double* Y,
                 double sign, cudaStream_t s);
 void block_conv(int R, const double* partial, int items, double tol, CgCtl c, cudaStream_t s);
+void modes_finish(long long n, int q, double* Phi, const double* KPhi, const double* GPhi, const double* sc,
+                  double lam1, double* y1, cudaStream_t s);

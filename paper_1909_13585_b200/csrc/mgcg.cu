@@ -2172,7 +2172,7 @@ static bool small_geneig(int p, const std::vector<double>& A, const std::vector<
 }
 
 mg_status mg_multilevel_modes(mg_handle c, const double* Es_e, const double* u, int q, double tol, double* Phi,
-                              double* lam_tilde, double* lam_coarse) {
+                              double* lam_tilde, double* lam_coarse, double* y1, double* yres) {
     if (!c || !Es_e || !u || !Phi || !lam_tilde) return fail(MG_ERR_ARG, "NULL argument");
     if (q < 1 || q > 32) return fail(MG_ERR_ARG, "q must be in [1, 32]");
     if (multi(c)) return fail(MG_ERR_ARG, "mg_multilevel_modes: single slab only (this round)");
@@ -2214,6 +2214,7 @@ mg_status mg_multilevel_modes(mg_handle c, const double* Es_e, const double* u, 
     double* Psi = dalloc(sizeof(double) * q * n);
     double* GPsi = dalloc(sizeof(double) * q * n);
     double* KPhi = dalloc(sizeof(double) * q * n);
+    double* Ysc = dalloc(sizeof(double) * n);        // Eq. 7 residual when the caller passes no y1
     for (void* p : tmp)
         if (!p) { cleanup(); return fail(MG_ERR_OOM, "mg_multilevel_modes workspace"); }
     stress_sigma(g0, Es_e, u, sig, s);
@@ -2321,6 +2322,30 @@ mg_status mg_multilevel_modes(mg_handle c, const double* Es_e, const double* u, 
     CU(cudaMemcpyAsync(den.data(), Gr, sizeof(double) * q * q, cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
     for (int i = 0; i < q; ++i) lam_tilde[i] = -num[i * q + i] / den[i * q + i];
+    // K normalisation phi~^T K phi~ = 1 and the Eq. 7 residual of the first pair,
+    // y = (K + lambda~_1 G) phi~_1, from K Phi and G Phi of step 4
+    {
+        std::vector<double> sc(q);
+        for (int i = 0; i < q; ++i) {
+            if (!(num[i * q + i] > 0.0)) { cleanup(); return fail(MG_ERR_BREAKDOWN, "mg_multilevel_modes: phi^T K phi <= 0"); }
+            sc[i] = 1.0 / std::sqrt(num[i * q + i]);
+        }
+        CU(cudaMemcpyAsync(Yd, sc.data(), sizeof(double) * q, cudaMemcpyHostToDevice, s));
+        double* yv = y1 ? y1 : (yres ? Ysc : nullptr);
+        modes_finish(n, q, Phi, KPhi, GPsi, Yd, lam_tilde[0], yv, s);
+        c->launches++;
+        CHECK_LAUNCH();
+        if (yres) {
+            double yy = 0.0, kk = 0.0;
+            gram(n, n, 1, yv, yv, gpart, Gr, s);
+            CU(cudaMemcpyAsync(&yy, Gr, sizeof(double), cudaMemcpyDeviceToHost, s));
+            gram(n, n, 1, KPhi, KPhi, gpart, Gr, s);
+            CU(cudaMemcpyAsync(&kk, Gr, sizeof(double), cudaMemcpyDeviceToHost, s));
+            CU(cudaStreamSynchronize(s));
+            yres[0] = std::sqrt(yy);
+            yres[1] = kk > 0.0 ? std::sqrt(yy) / (sc[0] * std::sqrt(kk)) : 0.0;
+        }
+    }
     cleanup();
     CU(cudaStreamSynchronize(s));
     return MG_OK;
