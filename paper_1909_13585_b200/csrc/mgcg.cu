@@ -2254,7 +2254,7 @@ mg_status mg_multilevel_modes(mg_handle c, const double* Es_e, const double* u, 
     }
     std::vector<double> Ah((size_t)pblk * pblk), Bh((size_t)pblk * pblk), th, Y, prev(q, 0.0);
     std::vector<double> lamc(q, 0.0);
-    int iters = 0;
+    int iters = 0, settled = -1;
     for (; iters < 500; ++iters) {
         dense_apply(Gd, ld, nL, V, W, pblk, nullptr, nullptr, s);       // W = G V
         dense_apply(c->Ainv, ld, nL, W, V, pblk, nullptr, nullptr, s);  // V = K^-1 G V  (= -K^-1 (-G) V)
@@ -2290,7 +2290,10 @@ mg_status mg_multilevel_modes(mg_handle c, const double* Es_e, const double* u, 
             change = std::max(change, std::fabs(lamc[i] - prev[i]) / std::fabs(lamc[i]));
             prev[i] = lamc[i];
         }
-        if (iters > 2 && change < 1e-13) { ++iters; break; }
+        // eigenvalues converge with the square of the eigenvector error: once they have settled at
+        // iteration N, run to 2N so the Ritz vectors (the prolongated modes) settle as well
+        if (iters > 2 && change < 1e-13 && settled < 0) settled = iters;
+        if (settled >= 0 && iters + 1 >= 2 * settled) { ++iters; break; }
     }
     if (lam_coarse)
         for (int i = 0; i < q; ++i) lam_coarse[i] = lamc[i];
