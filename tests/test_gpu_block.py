@@ -68,6 +68,25 @@ def test_block_size_one_is_pcg():
     assert rel(xb.cpu().numpy(), x.cpu().numpy()).max() < 1e-9
 
 
+@pytest.mark.parametrize("name,k", [("T2b", 3), ("T2b", 8), ("T3a", 3), ("T3a", 8)])
+def test_block_size_one_iterates_equal_pcg(name, k):
+    """q = 1 block CG is PCG algebraically: the k-th iterates of the two solvers agree
+    to rounding.  Not bitwise: the block path forms p.q and r.z with the Gram kernel and updates x
+    in a separate kernel, PCG fuses the dots into its march kernels (other summation order) and
+    defers the x update."""
+    import paper_1909_13585_b200 as mg
+    cfg, inp, K = case(name)
+    h = mg.mg_setup(cfg.nel, to_dev(inp["E"]), to_dev(inp["fixed"]), cfg.levels, max_iter=k)
+    b = to_dev(inp["rhs"][:1])
+    xb = torch.empty_like(b)
+    x = torch.empty_like(b)
+    rb = mg.mgcg_block_solve(h, b, 1e-14, xb, raise_on_error=False)
+    rp = mg.mgcg_solve(h, b, 1e-14, x, raise_on_error=False)
+    assert rb["status"] == rp["status"] == "MG_ERR_MAXITER"
+    assert rb["iters"][0] == rp["iters"][0] == k
+    assert rel(xb.cpu().numpy(), x.cpu().numpy()).max() < 1e-12
+
+
 def test_block_duplicate_columns_deflate():
     import paper_1909_13585_b200 as mg
     cfg, inp, K = case("T2a")
