@@ -153,9 +153,14 @@ def test_fullsize_C5_solution_vs_oracle_golden():
     cfg, inp, rep, X = solved("C5")
     g = _golden("C5")
     sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
-    assert g["inputs_sha256"] == dict(E=sha(inp["E"]), fixed=sha(inp["fixed"]), rhs=sha(inp["rhs"])), \
-        "regenerated C5 inputs differ from the ones the golden file was computed from"
+    assert g["inputs_sha256"] == dict(E=sha(inp["E"]), fixed=sha(inp["fixed"])), \
+        "regenerated C5 moduli / masks differ from the ones the golden file was computed from"
     idx = np.array(g["dofs"], dtype=np.int64)
+    # right-hand sides: FFT-filtered, equal to rounding across host CPUs (not bitwise)
+    for k in range(cfg.nrhs):
+        nb = np.linalg.norm(inp["rhs"][k])
+        assert abs(nb - g["rhs_norm2"][k]) <= 1e-13 * nb
+        assert np.abs(inp["rhs"][k][idx] - np.array(g["rhs_values"][k])).max() <= 1e-13 * np.abs(inp["rhs"][k]).max()
     assert len(g["rhs"]) == cfg.nrhs
     for e in g["rhs"]:
         k = e["k"]

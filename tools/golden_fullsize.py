@@ -8,7 +8,8 @@ per right-hand side: the solution at sampled DOFs, its 2-norm, the work f.u, the
 and the oracle's own relative residual; plus sha256 hashes of the generated inputs so a test can
 tell a regenerated-input mismatch apart from a solver mismatch.
 
-  python tools/golden_fullsize.py C5
+  python tools/golden_fullsize.py C5                 (oracle solve, ~25 min)
+  python tools/golden_fullsize.py C5 --inputs-only   (refresh the input fingerprint only)
 """
 
 import hashlib
@@ -47,6 +48,27 @@ def sample_dofs(cfg, count, seed):
     return np.array([cfg.dim * p + c for p in nodes for c in range(cfg.dim)], dtype=np.int64)
 
 
+def input_fingerprint(cfg, inp, idx):
+    """E and the masks hash exactly; the adjoint right-hand sides come from FFT filtering, whose last
+    bits depend on the host CPU, so they are fingerprinted by their norms and sampled values."""
+    return dict(inputs_sha256=dict(E=sha(inp["E"]), fixed=sha(inp["fixed"])),
+                rhs_norm2=[float(np.linalg.norm(b)) for b in inp["rhs"]],
+                rhs_values=[[float(v) for v in b[idx]] for b in inp["rhs"]])
+
+
+def refresh_inputs(name):
+    """Rewrite only the input fingerprint of an existing golden file (no oracle call)."""
+    cfg = get_config(name)
+    inp = generate(cfg, with_phi=False)
+    path = os.path.join(ROOT, "tests", "golden", f"fullsize_{name}_solution.json")
+    g = json.load(open(path))
+    g.pop("inputs_sha256", None)
+    g.update(input_fingerprint(cfg, inp, np.array(g["dofs"], dtype=np.int64)))
+    with open(path, "w") as f:
+        json.dump(g, f)
+    print("refreshed", path)
+
+
 def main(name):
     cfg = get_config(name)
     t0 = time.time()
@@ -71,8 +93,8 @@ def main(name):
         config=name, nel=list(cfg.nel), nrhs=cfg.nrhs, levels=cfg.levels,
         oracle="oracle.solve.mgpcg_solve (assembled K via assemble_K_large, Galerkin MG-PCG, tol 1e-13)",
         script="tools/golden_fullsize.py",
-        inputs_sha256=dict(E=sha(inp["E"]), fixed=sha(inp["fixed"]), rhs=sha(inp["rhs"])),
         dofs=[int(i) for i in idx], rhs=rhs_out, seconds=round(time.time() - t0, 1),
+        **input_fingerprint(cfg, inp, idx),
     )
     path = os.path.join(ROOT, "tests", "golden", f"fullsize_{name}_solution.json")
     with open(path, "w") as f:
@@ -81,4 +103,8 @@ def main(name):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "C5")
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    if "--inputs-only" in sys.argv:
+        refresh_inputs(args[0] if args else "C5")
+    else:
+        main(args[0] if args else "C5")
