@@ -37,6 +37,7 @@
 #include "kernels.h"
 
 __constant__ double c_Kt[576];
+__constant__ double c_Glm[2];   // lambda, mu of the centroid stress (E = 1) for G(u) phi
 
 // ---------------------------------------------------------------- K^ in closed form
 // 1-D factors in the (m, d) basis (t = 0: m, t = 1: d): M^ = diag(1/4, 1/12), D^ = diag(0, 1),
@@ -67,7 +68,11 @@ __host__ __device__ constexpr double tkhat(double nu, int row, int col) {
     return v;
 }
 
-void h8t_set_constants(const double* K0, cudaStream_t s) {
+void h8t_set_constants(const double* K0, double nu, cudaStream_t s) {
+    static double lm[2];
+    lm[0] = nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
+    lm[1] = 1.0 / (2.0 * (1.0 + nu));
+    cudaMemcpyToSymbolAsync(c_Glm, lm, sizeof(lm), 0, cudaMemcpyHostToDevice, s);
     static double Ti[24][24], Kh[576];
     for (int a = 0; a < 8; ++a)
         for (int t = 0; t < 8; ++t) {
@@ -137,6 +142,13 @@ __device__ __forceinline__ void t_mbar_wait(uint64_t* b, unsigned parity) {
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ void t_tma1(void* dst, const CUtensorMap* m, int c0, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.1d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2}], [%3];\n" ::"r"(
+            t_smem(dst)),
+        "l"((unsigned long long)m), "r"(c0), "r"(t_smem(bar))
+        : "memory");
+}
 __device__ __forceinline__ void t_tma3(void* dst, const CUtensorMap* m, int c0, int c1, int c2, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
@@ -161,13 +173,17 @@ __device__ __forceinline__ void t_tma4(void* dst, const CUtensorMap* m, int c0, 
 // tile (c0 = 30 tc - 1 is odd): vectors at node c0 - 1 (100 doubles = 33 nodes + 1 per row), E at
 // element c0 - 1 (34 per row), masks at the 16-byte boundary at or below c0 - 1 (48 bytes per row).
 static constexpr int T_VW = 100, T_EW = 34, T_MW = 48;
+// G(u) phi reads phi and u in the compact user layout, whose rows (odd node count) are not 16-byte
+// aligned: one 1-D box of 102 doubles per row, started at the even double at or below node c0 - 1
+// (row offset 0 / 1), rows 128-byte aligned in shared memory
+static constexpr int T_VWC = 112, T_RB = 102;
 __host__ __device__ constexpr int t_r128(int b) { return (b + 127) / 128 * 128; }
 template <int OP, int TR, int NB>
 struct TL {
     static constexpr int BR = TR + 1;                    // node rows per box
     static constexpr bool HB = OP != FOP_MATVEC;
     static constexpr bool HC = OP == FOP_JACOBI || OP == FOP_CGP || OP == FOP_RESTR3;
-    static constexpr int VB = BR * T_VW * 8;             // vector box bytes
+    static constexpr int VB = BR * (OP == FOP_GPHI ? T_VWC : T_VW) * 8;   // vector box bytes
     static constexpr int EB = TR * T_EW * 8;             // E box bytes
     static constexpr int MB = BR * T_MW;                 // mask box bytes
     static constexpr int OA = 0;
@@ -188,6 +204,7 @@ static constexpr size_t h8t_smem_bytes() {
 // per-slot expected TMA bytes (zero-filled out-of-range elements count too)
 template <int OP, int TR>
 __host__ __device__ constexpr unsigned h8t_tx_bytes(bool hasC) {
+    if (OP == FOP_GPHI) return (unsigned)(TR * T_EW * 8 + (TR + 1) * T_MW);   // + 2 T_RB * 8 per in-range row
     using T = TL<OP, TR, 1>;
     return (unsigned)(T::VB + (T::HB ? T::VB : 0) + ((T::HC && hasC) ? T::VB : 0) + T::EB + T::MB);
 }
@@ -230,7 +247,7 @@ __global__ void __launch_bounds__(32 * TR, MINB)
     const bool own = w >= 1 && lane >= 1 && lane <= 30 && j < n1 && c < n2;
     const int i0 = ch * hch, i1 = min(i0 + hch, n0);
     const int nq = i1 - i0 + 2;   // planes i0-1 .. i1
-    const long long vbase = (long long)r * a.g.vstr;
+    const long long vbase = (long long)r * a.g.vstr + (OP == FOP_GPHI ? a.goffA : 0);
     const long long pstr = (long long)n1 * p2 * 3;          // doubles per node plane (padded)
     const long long nodeoff = 3 * ((long long)j * p2 + c);  // within a plane
     const double beta = OP == FOP_CGP ? a.beta[r] : 0.0;
@@ -254,6 +271,25 @@ __global__ void __launch_bounds__(32 * TR, MINB)
     auto issue = [&](int q) {   // plane Q = i0 - 1 + q into slot q % NS
         const int s = q % NS, Q = i0 - 1 + q;
         unsigned char* sl = ring + s * T::SLOT;
+        if constexpr (OP == FOP_GPHI) {
+            // phi (RHS r) and u rows in range, one 1-D box per row; E and masks as 3-D boxes
+            unsigned bytes = txb;
+            for (int i = 0; i < T::BR; ++i) {
+                const int jj = j0 + i;
+                if (Q >= 0 && Q < n0 && jj >= 0 && jj < n1) bytes += 2 * T_RB * 8;
+            }
+            t_mbar_expect_tx(&full[s], bytes);
+            for (int i = 0; i < T::BR; ++i) {
+                const int jj = j0 + i;
+                if (!(Q >= 0 && Q < n0 && jj >= 0 && jj < n1)) continue;
+                const long long nd = 3 * (((long long)Q * n1 + jj) * n2 + c0 - 1);
+                t_tma1(sl + T::OA + i * T_VWC * 8, &tm.A, (int)((vbase + nd) & ~1LL), &full[s]);
+                t_tma1(sl + T::OB + i * T_VWC * 8, &tm.B, (int)((a.goffB + nd) & ~1LL), &full[s]);
+            }
+            t_tma3(sl + T::OE, &tm.E, c0 - 1, j0, Q, &full[s]);
+            t_tma3(sl + T::OM, &tm.M, cm0, j0, Q, &full[s]);
+            return;
+        }
         t_mbar_expect_tx(&full[s], txb);
         const int cv = 3 * (c0 - 1);
         t_tma4(sl + T::OA, &tm.A, cv, j0, Q, r, &full[s]);
@@ -274,9 +310,30 @@ __global__ void __launch_bounds__(32 * TR, MINB)
     auto fE = [&](int s) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OE)[w * T_EW + lane + 1]; };
     auto fM = [&](int s, int row) { return (int)(ring + s * T::SLOT + T::OM)[row * T_MW + mlane]; };
 
-    // operator input of box row `row` at slot s: raw (unmasked) and u (masked, fed to the element)
-    auto input = [&](int s, int row, double (&raw)[3], double (&u)[3], int& m) {
+    // G(u) phi: compact rows (row offset 0 / 1 double), rows outside the grid were not loaded
+    const bool colok = c >= 0 && c < n2;
+    auto rowok = [&](int Q, int row) {
+        const int jj = j0 + row;
+        return Q >= 0 && Q < n0 && jj >= 0 && jj < n1;
+    };
+    auto gvec = [&](int off, int s, int Q, int row, long long vb) {
+        const long long nd = vb + 3 * (((long long)Q * n1 + (j0 + row)) * n2 + c0 - 1);
+        return reinterpret_cast<const double*>(ring + s * T::SLOT + off) + row * T_VWC + (int)(nd & 1) + 3 * (lane + 1);
+    };
+    // operator input of box row `row` at slot s (plane Q): raw (unmasked) and u (masked, fed to
+    // the element)
+    auto input = [&](int s, int Q, int row, double (&raw)[3], double (&u)[3], int& m) {
         m = fM(s, row);
+        if constexpr (OP == FOP_GPHI) {
+            const bool ok = colok && rowok(Q, row);
+            const double* A = gvec(T::OA, s, Q, row, vbase);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                raw[k] = ok ? A[k] : 0.0;
+                u[k] = ((m >> k) & 1) ? 0.0 : raw[k];
+            }
+            return;
+        }
         const double* A = fA(s, row);
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
@@ -323,8 +380,8 @@ __global__ void __launch_bounds__(32 * TR, MINB)
         {
             double uo[3], uu[3], ru[3];
             int mu;
-            input(sP, w, rawP, uo, mP);
-            input(sP, w + 1, ru, uu, mu);
+            input(sP, P, w, rawP, uo, mP);
+            input(sP, P, w + 1, ru, uu, mu);
             if ((OP == FOP_CGP || OP == FOP_RESTR3) && own && P >= i0 && P < i1) {
                 const long long o = vbase + (long long)P * pstr + nodeoff;
                 if (OP == FOP_CGP) {
@@ -353,7 +410,93 @@ __global__ void __launch_bounds__(32 * TR, MINB)
         }
         // element (L, w, lane): u^ = E (T u), y^ = K^ u^, back to the faces of planes L (GL) and P (CY)
         double GL[3][4];
-        {
+        if constexpr (OP == FOP_GPHI) {
+            // centroid stress of element (L, w, lane) from u (PAPER.md:99 G_e0[u_e], reading r15):
+            // g[k][a] = 4 du_k/dx_a at the centroid, sigma = Es D0 eps
+            double g[3][3];
+            {
+                const double* uL0 = gvec(T::OB, sL, L, w, a.goffB);
+                const double* uL1 = gvec(T::OB, sL, L, w + 1, a.goffB);
+                const double* uP0 = gvec(T::OB, sP, P, w, a.goffB);
+                const double* uP1 = gvec(T::OB, sP, P, w + 1, a.goffB);
+                const bool oL0 = colok && rowok(L, w), oL1 = colok && rowok(L, w + 1);
+                const bool oP0 = colok && rowok(P, w), oP1 = colok && rowok(P, w + 1);
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const double a00 = oL0 ? uL0[k] : 0.0, a10 = oL1 ? uL1[k] : 0.0;
+                    const double b00 = oP0 ? uP0[k] : 0.0, b10 = oP1 ? uP1[k] : 0.0;
+                    const double a01 = __shfl_down_sync(MGK_FULL, a00, 1), a11 = __shfl_down_sync(MGK_FULL, a10, 1);
+                    const double b01 = __shfl_down_sync(MGK_FULL, b00, 1), b11 = __shfl_down_sync(MGK_FULL, b10, 1);
+                    const double sl0 = a00 + a01, sl1 = a10 + a11, sp0 = b00 + b01, sp1 = b10 + b11;
+                    g[k][0] = (sp0 + sp1) - (sl0 + sl1);
+                    g[k][1] = (sl1 - sl0) + (sp1 - sp0);
+                    g[k][2] = ((a01 - a00) + (a11 - a10)) + ((b01 - b00) + (b11 - b10));
+                }
+            }
+            const double Es4 = 0.25 * fE(sL);
+            const double lam = C03 ? MG_NU_PAPER / ((1.0 + MG_NU_PAPER) * (1.0 - 2.0 * MG_NU_PAPER)) : c_Glm[0];
+            const double mu = C03 ? 1.0 / (2.0 * (1.0 + MG_NU_PAPER)) : c_Glm[1];
+            const double tr = lam * (g[0][0] + g[1][1] + g[2][2]);
+            double sig[3][3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) sig[i][i] = Es4 * fma(2.0 * mu, g[i][i], tr);
+            sig[0][1] = sig[1][0] = Es4 * mu * (g[0][1] + g[1][0]);
+            sig[0][2] = sig[2][0] = Es4 * mu * (g[0][2] + g[2][0]);
+            sig[1][2] = sig[2][1] = Es4 * mu * (g[1][2] + g[2][1]);
+            // S^ = sum_ij sigma_ij H^_ij in the (m, d) basis (H^_ij = T^-T H_ij T^-1 has the same
+            // 1-D factors as the stiffness: 19 nonzeros, rows / cols s = 0 zero)
+            double S[8][8];
+#pragma unroll
+            for (int a = 1; a < 8; ++a)
+#pragma unroll
+                for (int b = 1; b < 8; ++b) {
+                    bool first = true;
+                    double v = 0.0;
+#pragma unroll
+                    for (int i = 0; i < 3; ++i)
+#pragma unroll
+                        for (int jx = 0; jx < 3; ++jx) {
+                            const double hv = tsh3(i, jx, a, b);
+                            if (hv == 0.0) continue;
+                            v = first ? sig[i][jx] * hv : fma(sig[i][jx], hv, v);
+                            first = false;
+                        }
+                    S[a][b] = v;
+                }
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                double uh[8], y[8];
+#pragma unroll
+                for (int t = 1; t < 8; ++t) {
+                    const int f = t & 3;
+                    uh[t] = t < 4 ? FL[k][f] + FP[k][f] : FP[k][f] - FL[k][f];
+                }
+#pragma unroll
+                for (int a = 1; a < 8; ++a) {
+                    bool first = true;
+                    double v = 0.0;
+#pragma unroll
+                    for (int b = 1; b < 8; ++b) {
+                        bool nz = false;
+#pragma unroll
+                        for (int i = 0; i < 3; ++i)
+#pragma unroll
+                            for (int jx = 0; jx < 3; ++jx) nz = nz || tsh3(i, jx, a, b) != 0.0;
+                        if (!nz) continue;
+                        v = first ? S[a][b] * uh[b] : fma(S[a][b], uh[b], v);
+                        first = false;
+                    }
+                    y[a] = v;
+                }
+                GL[k][0] = CY[k][0] - y[4];
+                CY[k][0] = y[4];
+#pragma unroll
+                for (int f = 1; f < 4; ++f) {
+                    GL[k][f] = CY[k][f] + (y[f] - y[4 + f]);
+                    CY[k][f] = y[f] + y[4 + f];
+                }
+            }
+        } else {
             const double Ee = fE(sL);
 #pragma unroll
             for (int ci = 0; ci < T_NCOMP; ++ci) {
@@ -418,7 +561,11 @@ __global__ void __launch_bounds__(32 * TR, MINB)
                 }
                 __syncwarp();
                 if (lane == 0) t_mbar_arrive(&sempty[bi * TR + w - 1]);
-                if (own && L < i1) {
+                if (OP == FOP_GPHI && own && L < i1) {   // F G F phi: fixed rows zero
+                    const long long ob = (long long)r * a.g.vstr + 3 * (((long long)L * n1 + j) * n2 + c);
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) a.y[ob + k] = ((mL >> k) & 1) ? 0.0 : y[k];
+                } else if (own && L < i1) {
                     const long long ob = vbase + (long long)L * pstr + nodeoff;
                     const bool sdot = L >= a.so0 && L < a.so1;
 #pragma unroll
@@ -459,8 +606,8 @@ __global__ void __launch_bounds__(32 * TR, MINB)
         t_mbar_wait(&full[0], 0u);
         double uo[3], uu[3], ru[3];
         int mu;
-        input(0, w, rawA, uo, mA);
-        input(0, w + 1, ru, uu, mu);
+        input(0, i0 - 1, w, rawA, uo, mA);
+        input(0, i0 - 1, w + 1, ru, uu, mu);
         face(uo, uu, FA);
     }
     using I0 = std::integral_constant<int, 0>;
@@ -544,9 +691,17 @@ static bool launch_h8t_t(const FineArgs& a, cudaStream_t s) {
     const double* vA = OP == FOP_CGP ? a.pin : (OP == FOP_RESTR3 ? a.rin : a.x);
     const double* vB = OP == FOP_CGP ? a.z : (OP == FOP_RESTR3 ? a.q : a.b);
     const bool hasC = T::HC && (OP != FOP_CGP || a.xv != nullptr);
-    bool ok = t_map_vec(&tm.A, a, vA, T::BR, true);
-    if (T::HB) ok = ok && t_map_vec(&tm.B, a, vB, T::BR, true);
-    if (hasC) ok = ok && t_map_vec(&tm.C, a, OP == FOP_CGP ? a.xv : a.Dinv, T::BR, OP == FOP_CGP);
+    bool ok;
+    if (OP == FOP_GPHI) {   // phi (R, ndof) and u (ndof) as 1-D tensors, one box per row
+        cuuint64_t dA[1] = {(cuuint64_t)g.ndof * a.R + a.goffA}, dB[1] = {(cuuint64_t)g.ndof + a.goffB};
+        cuuint32_t box[1] = {(cuuint32_t)T_RB};
+        ok = t_map(&tm.A, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 1, vA - a.goffA, dA, nullptr, box) &&
+             t_map(&tm.B, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 1, vB - a.goffB, dB, nullptr, box);
+    } else {
+        ok = t_map_vec(&tm.A, a, vA, T::BR, true);
+        if (T::HB) ok = ok && t_map_vec(&tm.B, a, vB, T::BR, true);
+        if (hasC) ok = ok && t_map_vec(&tm.C, a, OP == FOP_CGP ? a.xv : a.Dinv, T::BR, OP == FOP_CGP);
+    }
     {
         cuuint64_t dims[3] = {(cuuint64_t)g.N[2], (cuuint64_t)g.N[1], (cuuint64_t)g.N[0]};
         cuuint64_t str[2] = {(cuuint64_t)a.ep2 * 8, (cuuint64_t)a.ep2 * g.N[1] * 8};
@@ -636,6 +791,7 @@ static bool launch_h8t_op(const FineArgs& a, cudaStream_t s) {
 int h8t_apply(int op, const FineArgs& a, cudaStream_t s) {
     bool ok;
     switch (op) {
+        case FOP_GPHI: ok = launch_h8t_op<FOP_GPHI>(a, s); break;
         case FOP_MATVEC: ok = launch_h8t_op<FOP_MATVEC>(a, s); break;
         case FOP_RESID: ok = launch_h8t_op<FOP_RESID>(a, s); break;
         case FOP_JACOBI: ok = launch_h8t_op<FOP_JACOBI>(a, s); break;

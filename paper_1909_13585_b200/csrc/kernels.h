@@ -6,7 +6,8 @@
 
 // ---------------------------------------------------------------- fine level (matrix-free)
 // FOP_RESTR3 / FOP_POST3: 3D fused halves of the fine V(1,1) level (h8.cu), see there
-enum FineOp { FOP_MATVEC = 0, FOP_RESID = 1, FOP_JACOBI = 2, FOP_CGP = 3, FOP_RESTR3 = 4, FOP_POST3 = 5 };
+// FOP_GPHI: y = G(u) phi (stress stiffness) on the compact user layout (h8t.cu)
+enum FineOp { FOP_MATVEC = 0, FOP_RESID = 1, FOP_JACOBI = 2, FOP_CGP = 3, FOP_RESTR3 = 4, FOP_POST3 = 5, FOP_GPHI = 6 };
 
 struct FineArgs {
     LevelGeom g;
@@ -43,6 +44,7 @@ struct FineArgs {
     int off0;
     int ep2;                // 3D: E row pitch (elements along axis 2, even)
     int m2;                 // 3D: mask row pitch (bytes, multiple of 16)
+    int goffA, goffB;       // FOP_GPHI: x (phi) / b (u) start this many doubles after a 16-byte boundary
 };
 
 void fine_set_constants(int dim, const double* K0, cudaStream_t s);
@@ -67,7 +69,7 @@ void unpad3_vectors_planes(const LevelGeom& g, const Pad3& p, int R, int p0, int
 void pad3_nodes(const LevelGeom& g, const Pad3& p, const uint8_t* mask, uint8_t* maskp, const double* dinv,
                 double* dinvp, cudaStream_t s);
 void pad3_elems(const LevelGeom& g, const Pad3& p, const double* E, double* Ep, cudaStream_t s);
-void h8t_set_constants(const double* K0, cudaStream_t s);
+void h8t_set_constants(const double* K0, double nu, cudaStream_t s);
 int h8t_apply(int op, const FineArgs& a, cudaStream_t s);
 int h8t_items(const LevelGeom& g, int R);
 void h8t_chunks(int TR, int minb, const LevelGeom& g, int R, int* nch_out, int* hch_out);

@@ -368,7 +368,7 @@ static mg_status ensure_constants(mg_ctx* c) {
     g_const_valid = false;
     cudaStream_t s = c->stream;
     fine_set_constants(c->dim, c->K0.data(), s);
-    if (c->dim == 3) h8t_set_constants(c->K0.data(), s);
+    if (c->dim == 3) h8t_set_constants(c->K0.data(), c->nu, s);
     if (c->dim == 2) fine2d_set_constants(c->K0.data(), s);
     galerkin_set_constants(c->dim, c->K0.data(), s);
     stress_set_constants(c->dim, c->nu, s);
@@ -1780,6 +1780,34 @@ static mg_status record_block_iter(mg_ctx* c, int R, double tol) {
     return MG_OK;
 }
 
+// y = G(u) phi on one slab's compact device arrays (local geometry g).  3D with an even element
+// count along axis 2 and 8-byte aligned arrays: the TMA march kernel (h8t.cu, FOP_GPHI: centroid
+// stress formed in the kernel from u, the 19-nonzero stress matrix in the sum/difference basis);
+// otherwise centroid stresses (stress_sigma) + stress_apply.
+static void gphi_slab(mg_ctx* c, Slab& sl, const LevelGeom& g, const uint8_t* mask, const double* Es, const double* u,
+                      const double* phi, double* y, int nphi) {
+    cudaStream_t s = c->stream;
+    const int nv = c->dim == 2 ? 3 : 6;
+    auto a8 = [](const void* p) { return ((uintptr_t)p & 7) == 0; };
+    if (c->dim == 3 && g.N[2] % 2 == 0 && a8(Es) && a8(u) && a8(phi) && ((uintptr_t)Es & 15) == 0 &&
+        !getenv("MG_GPHI_LEGACY")) {
+        FineArgs a{};
+        a.g = g;   // compact vectors (p2 = n2, vstr = ndof)
+        a.E = Es; a.mask = sl.maskpad; a.m2 = sl.p3.m2; a.ep2 = g.N[2];
+        a.x = phi; a.b = u; a.y = y; a.R = nphi; a.nu_paper = c->nu_paper ? 1 : 0;
+        a.goffA = (int)(((uintptr_t)phi & 15) >> 3);
+        a.goffB = (int)(((uintptr_t)u & 15) >> 3);
+        if (fine_apply(FOP_GPHI, a, s) >= 0) {
+            c->launches++;
+            return;
+        }
+    }
+    if (!sl.sig) cudaMalloc(&sl.sig, sizeof(double) * g.nelem * nv);
+    stress_sigma(g, Es, u, sl.sig, s);
+    stress_apply(g, sl.sig, mask, phi, y, nphi, s);
+    c->launches += 2;
+}
+
 mg_status stress_stiffness_apply(mg_handle c, const double* Es_e, const double* u, const double* phi, int nphi,
                                  double* y) {
     if (!c || !Es_e || !u || !phi || !y) return fail(MG_ERR_ARG, "NULL argument");
@@ -1791,11 +1819,7 @@ mg_status stress_stiffness_apply(mg_handle c, const double* Es_e, const double* 
     const bool dev = is_device_ptr(phi) && is_device_ptr(y) && is_device_ptr(u) && is_device_ptr(Es_e);
     if (!multi(c) && dev) {   // one slab, device buffers: direct
         Slab& sl = c->sl[0];
-        const LevelGeom& g0 = sl.lv[0].g;
-        if (!sl.sig) CU(cudaMalloc(&sl.sig, sizeof(double) * g0.nelem * nv));
-        stress_sigma(g0, Es_e, u, sl.sig, s);
-        stress_apply(g0, sl.sig, sl.lv[0].mask, phi, y, nphi, s);
-        c->launches += 2;
+        gphi_slab(c, sl, sl.lv[0].g, sl.lv[0].mask, Es_e, u, phi, y, nphi);
         CHECK_LAUNCH();
         return MG_OK;
     }
@@ -1834,8 +1858,6 @@ mg_status stress_stiffness_apply(mg_handle c, const double* Es_e, const double* 
         CU(cudaStreamWaitEvent(c->cs_out, c->gev_sig, 0));
         CU(cudaMemcpyAsync(dEs, Es_e, sizeof(double) * m, cudaMemcpyDefault, s));
         CU(cudaMemcpyAsync(du, u, sizeof(double) * n, cudaMemcpyDefault, s));
-        stress_sigma(g0, dEs, du, sl.sig, s);
-        c->launches++;
         const int nch = std::min(mg_ctx::NCHUNK_EV, nphi);
         const int per = (nphi + nch - 1) / nch;
         for (int k = 0, k0 = 0; k0 < nphi; ++k, k0 += per) {
@@ -1844,8 +1866,7 @@ mg_status stress_stiffness_apply(mg_handle c, const double* Es_e, const double* 
             CU(cudaMemcpyAsync(dphi + n * k0, phi + n * k0, bytes, cudaMemcpyDefault, c->cs_in));
             CU(cudaEventRecord(c->gev_in[k], c->cs_in));
             CU(cudaStreamWaitEvent(s, c->gev_in[k], 0));
-            stress_apply(g0, sl.sig, sl.lv[0].mask, dphi + n * k0, dy + n * k0, kc, s);
-            c->launches++;
+            gphi_slab(c, sl, g0, sl.lv[0].mask, dEs, du, dphi + n * k0, dy + n * k0, kc);
             CU(cudaEventRecord(c->gev_k[k], s));
             CU(cudaStreamWaitEvent(c->cs_out, c->gev_k[k], 0));
             CU(cudaMemcpyAsync(y + n * k0, dy + n * k0, bytes, cudaMemcpyDefault, c->cs_out));
@@ -1912,9 +1933,7 @@ mg_status stress_stiffness_apply(mg_handle c, const double* Es_e, const double* 
     TRY(xchg(c, [&](const Slab& sl) { return elem_field(sl, 0, sl.Es, 1); }));
     for (Slab& sl : c->sl) {
         const Level& v = sl.lv[0];
-        stress_sigma(v.g, sl.Es, sl.u, sl.sig, s);
-        stress_apply(v.g, sl.sig, v.mask, sl.phi, sl.gy, nphi, s);
-        c->launches += 2;
+        gphi_slab(c, sl, v.g, v.mask, sl.Es, sl.u, sl.phi, sl.gy, nphi);
         const long long pl = v.pn * dim, np = v.o1 - v.o0;
         CU(cudaMemcpy2DAsync(y_dst + dim * sl.uoff, n * 8, sl.gy + v.o0 * pl, v.g.ndof * 8, np * pl * 8, nphi,
                              cudaMemcpyDeviceToDevice, s));
