@@ -68,12 +68,13 @@ def test_block_size_one_is_pcg():
     assert rel(xb.cpu().numpy(), x.cpu().numpy()).max() < 1e-9
 
 
-@pytest.mark.parametrize("name,k", [("T2b", 3), ("T2b", 8), ("T3a", 3), ("T3a", 8)])
+@pytest.mark.parametrize("name,k", [("T2b", 2), ("T2b", 8), ("T3a", 2), ("T3a", 8)])
 def test_block_size_one_iterates_equal_pcg(name, k):
     """q = 1 block CG is PCG algebraically: the k-th iterates of the two solvers agree
     to rounding.  Not bitwise: the block path forms p.q and r.z with the Gram kernel and updates x
     in a separate kernel, PCG fuses the dots into its march kernels (other summation order) and
-    defers the x update."""
+    defers the x update.  k even: the PCG graph body runs two CG iterations, so
+    max_iter is honoured to within one iteration."""
     import paper_1909_13585_b200 as mg
     cfg, inp, K = case(name)
     h = mg.mg_setup(cfg.nel, to_dev(inp["E"]), to_dev(inp["fixed"]), cfg.levels, max_iter=k)
