@@ -663,7 +663,8 @@ static bool t_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* 
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (e != CUDA_SUCCESS) {
-        fprintf(stderr, "h8t: cuTensorMapEncodeTiled failed (%d)\n", (int)e);
+        fprintf(stderr, "h8t: cuTensorMapEncodeTiled failed (%d): rank %d dim0 %llu box0 %u base %p\n", (int)e, rank,
+                (unsigned long long)dims[0], box[0], base);
         return false;
     }
     return true;
@@ -695,8 +696,9 @@ static bool launch_h8t_t(const FineArgs& a, cudaStream_t s) {
     if (OP == FOP_GPHI) {   // phi (R, ndof) and u (ndof) as 1-D tensors, one box per row
         cuuint64_t dA[1] = {(cuuint64_t)g.ndof * a.R + a.goffA}, dB[1] = {(cuuint64_t)g.ndof + a.goffB};
         cuuint32_t box[1] = {(cuuint32_t)T_RB};
-        ok = t_map(&tm.A, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 1, vA - a.goffA, dA, nullptr, box) &&
-             t_map(&tm.B, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 1, vB - a.goffB, dB, nullptr, box);
+        cuuint64_t nostr[1] = {0};   // rank 1: no strides (the array must still be valid)
+        ok = t_map(&tm.A, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 1, vA - a.goffA, dA, nostr, box) &&
+             t_map(&tm.B, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 1, vB - a.goffB, dB, nostr, box);
     } else {
         ok = t_map_vec(&tm.A, a, vA, T::BR, true);
         if (T::HB) ok = ok && t_map_vec(&tm.B, a, vB, T::BR, true);
