@@ -413,6 +413,18 @@ __global__ void __launch_bounds__(32 * TR, MINB)
         if constexpr (OP == FOP_GPHI) {
             // centroid stress of element (L, w, lane) from u (PAPER.md:99 G_e0[u_e], reading r15):
             // g[k][a] = 4 du_k/dx_a at the centroid, sigma = Es D0 eps
+            double sig[3][3];
+            if (a.sig) {   // precomputed (stress_sigma): Voigt [s00, s11, s22, s12, s02, s01], times Es
+                const bool eok = L >= 0 && L < a.g.N[0] && j >= 0 && j < a.g.N[1] && c >= 0 && c < a.g.N[2];
+                const double* sp = a.sig + 6 * (eok ? (((long long)L * a.g.N[1] + j) * a.g.N[2] + c) : 0);
+                double v[6];
+#pragma unroll
+                for (int q = 0; q < 6; ++q) v[q] = eok ? __ldg(sp + q) : 0.0;
+                sig[0][0] = v[0]; sig[1][1] = v[1]; sig[2][2] = v[2];
+                sig[1][2] = sig[2][1] = v[3];
+                sig[0][2] = sig[2][0] = v[4];
+                sig[0][1] = sig[1][0] = v[5];
+            } else {
             double g[3][3];
             {
                 const double* uL0 = gvec(T::OB, sL, L, w, a.goffB);
@@ -437,12 +449,12 @@ __global__ void __launch_bounds__(32 * TR, MINB)
             const double lam = C03 ? MG_NU_PAPER / ((1.0 + MG_NU_PAPER) * (1.0 - 2.0 * MG_NU_PAPER)) : c_Glm[0];
             const double mu = C03 ? 1.0 / (2.0 * (1.0 + MG_NU_PAPER)) : c_Glm[1];
             const double tr = lam * (g[0][0] + g[1][1] + g[2][2]);
-            double sig[3][3];
 #pragma unroll
             for (int i = 0; i < 3; ++i) sig[i][i] = Es4 * fma(2.0 * mu, g[i][i], tr);
             sig[0][1] = sig[1][0] = Es4 * mu * (g[0][1] + g[1][0]);
             sig[0][2] = sig[2][0] = Es4 * mu * (g[0][2] + g[2][0]);
             sig[1][2] = sig[2][1] = Es4 * mu * (g[1][2] + g[2][1]);
+            }
             // S^ = sum_ij sigma_ij H^_ij in the (m, d) basis (H^_ij = T^-T H_ij T^-1 has the same
             // 1-D factors as the stiffness: 19 nonzeros, rows / cols s = 0 zero)
             double S[8][8];

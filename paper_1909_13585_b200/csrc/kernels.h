@@ -45,6 +45,7 @@ struct FineArgs {
     int ep2;                // 3D: E row pitch (elements along axis 2, even)
     int m2;                 // 3D: mask row pitch (bytes, multiple of 16)
     int goffA, goffB;       // FOP_GPHI: x (phi) / b (u) start this many doubles after a 16-byte boundary
+    const double* sig;      // FOP_GPHI: element centroid stresses (nelem x 6, stress_sigma) or NULL (formed from u)
 };
 
 void fine_set_constants(int dim, const double* K0, cudaStream_t s);

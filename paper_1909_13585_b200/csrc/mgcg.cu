@@ -1797,8 +1797,17 @@ static void gphi_slab(mg_ctx* c, Slab& sl, const LevelGeom& g, const uint8_t* ma
         a.x = phi; a.b = u; a.y = y; a.R = nphi; a.nu_paper = c->nu_paper ? 1 : 0;
         a.goffA = (int)(((uintptr_t)phi & 15) >> 3);
         a.goffB = (int)(((uintptr_t)u & 15) >> 3);
+        // several phi: centroid stresses once per element (stress_sigma) instead of once per
+        // element and phi inside the kernel (MG_GPHI_SIGMA=0/1 forces either)
+        const char* e = getenv("MG_GPHI_SIGMA");
+        const bool pre = e ? atoi(e) != 0 : nphi > 1;
+        if (pre) {
+            if (!sl.sig) cudaMalloc(&sl.sig, sizeof(double) * g.nelem * nv);
+            stress_sigma(g, Es, u, sl.sig, s);
+            a.sig = sl.sig;
+        }
         if (fine_apply(FOP_GPHI, a, s) >= 0) {
-            c->launches++;
+            c->launches += pre ? 2 : 1;
             return;
         }
     }
