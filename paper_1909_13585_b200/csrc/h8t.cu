@@ -198,15 +198,7 @@ struct TL {
 template <int OP, int TR, int NS, int NB>
 static constexpr size_t h8t_smem_bytes() {
     using T = TL<OP, TR, NB>;
-    return (size_t)NS * T::SLOT + T::SINV + 8 * (NS + 2 * NB * TR) + 8 * NS + 8 * TR;
-}
-
-// per-slot expected TMA bytes (zero-filled out-of-range elements count too)
-template <int OP, int TR>
-__host__ __device__ constexpr unsigned h8t_tx_bytes(bool hasC) {
-    if (OP == FOP_GPHI) return (unsigned)(TR * T_EW * 8 + (TR + 1) * T_MW);   // + 2 T_RB * 8 per in-range row
-    using T = TL<OP, TR, 1>;
-    return (unsigned)(T::VB + (T::HB ? T::VB : 0) + ((T::HC && hasC) ? T::VB : 0) + T::EB + T::MB);
+    return (size_t)NS * T::SLOT + T::SINV + 8 * (NS * T::BR + 2 * NB * TR) + 8 * NS * T::BR + 8 * TR;
 }
 
 struct H8TMaps {
@@ -223,11 +215,14 @@ __global__ void __launch_bounds__(32 * TR, MINB)
     extern __shared__ __align__(128) unsigned char t_sm[];
     unsigned char* ring = t_sm;
     double* sinv = reinterpret_cast<double*>(t_sm + NS * T::SLOT);                       // [NB][TR][6][32]
-    uint64_t* full = reinterpret_cast<uint64_t*>(t_sm + NS * T::SLOT + T::SINV);         // [NS]
-    uint64_t* sfull = full + NS;                                                         // [NB][TR]
+    // the ring is kept per box row: row i of a slot is read by warps i - 1 (upper row of its
+    // elements) and i (own row) only, so it is released and refilled as soon as those two are done
+    uint64_t* full = reinterpret_cast<uint64_t*>(t_sm + NS * T::SLOT + T::SINV);         // [NS][BR]
+    uint64_t* sfull = full + NS * T::BR;                                                 // [NB][TR]
     uint64_t* sempty = sfull + NB * TR;                                                  // [NB][TR]
-    int* cnt = reinterpret_cast<int*>(sempty + NB * TR);                                 // [NS]
-    double* s_dot = reinterpret_cast<double*>(t_sm + NS * T::SLOT + T::SINV + 8 * (NS + 2 * NB * TR) + 8 * NS);
+    int* cnt = reinterpret_cast<int*>(sempty + NB * TR);                                 // [NS][BR]
+    double* s_dot = reinterpret_cast<double*>(t_sm + NS * T::SLOT + T::SINV + 8 * (NS * T::BR + 2 * NB * TR) +
+                                              8 * NS * T::BR);
 
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int R = a.R;
@@ -256,7 +251,7 @@ __global__ void __launch_bounds__(32 * TR, MINB)
     const double omega = a.omega;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < NS; ++s) {
+        for (int s = 0; s < NS * T::BR; ++s) {
             t_mbar_init(&full[s], 1);
             cnt[s] = 0;
         }
@@ -267,42 +262,43 @@ __global__ void __launch_bounds__(32 * TR, MINB)
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-    const unsigned txb = h8t_tx_bytes<OP, TR>(hasC != 0);
-    auto issue = [&](int q) {   // plane Q = i0 - 1 + q into slot q % NS
+    // row i of plane Q = i0 - 1 + q into slot q % NS: vector fields, E row i (i < TR), mask row i
+    const int nvf = 1 + (T::HB ? 1 : 0) + ((T::HC && hasC) ? 1 : 0);
+    auto issue_row = [&](int q, int i) {
         const int s = q % NS, Q = i0 - 1 + q;
         unsigned char* sl = ring + s * T::SLOT;
+        uint64_t* fb = &full[s * T::BR + i];
+        const int jj = j0 + i;
         if constexpr (OP == FOP_GPHI) {
-            // phi (RHS r) and u rows in range, one 1-D box per row; E and masks as 3-D boxes
-            unsigned bytes = txb;
-            for (int i = 0; i < T::BR; ++i) {
-                const int jj = j0 + i;
-                if (Q >= 0 && Q < n0 && jj >= 0 && jj < n1) bytes += 2 * T_RB * 8;
-            }
-            t_mbar_expect_tx(&full[s], bytes);
-            for (int i = 0; i < T::BR; ++i) {
-                const int jj = j0 + i;
-                if (!(Q >= 0 && Q < n0 && jj >= 0 && jj < n1)) continue;
+            const bool in = Q >= 0 && Q < n0 && jj >= 0 && jj < n1;
+            t_mbar_expect_tx(fb, (in ? 2 * T_RB * 8 : 0) + (i < TR ? T_EW * 8 : 0) + T_MW);
+            if (in) {   // phi (RHS r) and u rows: one 1-D box each
                 const long long nd = 3 * (((long long)Q * n1 + jj) * n2 + c0 - 1);
-                t_tma1(sl + T::OA + i * T_VWC * 8, &tm.A, (int)((vbase + nd) & ~1LL), &full[s]);
-                t_tma1(sl + T::OB + i * T_VWC * 8, &tm.B, (int)((a.goffB + nd) & ~1LL), &full[s]);
+                t_tma1(sl + T::OA + i * T_VWC * 8, &tm.A, (int)((vbase + nd) & ~1LL), fb);
+                t_tma1(sl + T::OB + i * T_VWC * 8, &tm.B, (int)((a.goffB + nd) & ~1LL), fb);
             }
-            t_tma3(sl + T::OE, &tm.E, c0 - 1, j0, Q, &full[s]);
-            t_tma3(sl + T::OM, &tm.M, cm0, j0, Q, &full[s]);
-            return;
+        } else {
+            t_mbar_expect_tx(fb, nvf * T_VW * 8 + (i < TR ? T_EW * 8 : 0) + T_MW);
+            const int cv = 3 * (c0 - 1);
+            t_tma4(sl + T::OA + i * T_VW * 8, &tm.A, cv, jj, Q, r, fb);
+            if (T::HB) t_tma4(sl + T::OB + i * T_VW * 8, &tm.B, cv, jj, Q, r, fb);
+            if (T::HC && hasC) {
+                if (OP == FOP_CGP) t_tma4(sl + T::OC + i * T_VW * 8, &tm.C, cv, jj, Q, r, fb);
+                else t_tma3(sl + T::OC + i * T_VW * 8, &tm.C, cv, jj, Q, fb);
+            }
         }
-        t_mbar_expect_tx(&full[s], txb);
-        const int cv = 3 * (c0 - 1);
-        t_tma4(sl + T::OA, &tm.A, cv, j0, Q, r, &full[s]);
-        if (T::HB) t_tma4(sl + T::OB, &tm.B, cv, j0, Q, r, &full[s]);
-        if (T::HC && hasC) {
-            if (OP == FOP_CGP) t_tma4(sl + T::OC, &tm.C, cv, j0, Q, r, &full[s]);
-            else t_tma3(sl + T::OC, &tm.C, cv, j0, Q, &full[s]);
-        }
-        t_tma3(sl + T::OE, &tm.E, c0 - 1, j0, Q, &full[s]);
-        t_tma3(sl + T::OM, &tm.M, cm0, j0, Q, &full[s]);
+        if (i < TR) t_tma3(sl + T::OE + i * T_EW * 8, &tm.E, c0 - 1, jj, Q, fb);
+        t_tma3(sl + T::OM + i * T_MW, &tm.M, cm0, jj, Q, fb);
     };
     if (threadIdx.x == 0)
-        for (int q = 0; q < NS && q < nq; ++q) issue(q);
+        for (int q = 0; q < NS && q < nq; ++q)
+            for (int i = 0; i < T::BR; ++i) issue_row(q, i);
+    // wait for rows w and w + 1 of slot s (fill index (q / NS))
+    auto wait_rows = [&](int s, int q) {
+        const unsigned ph = (unsigned)((q / NS) & 1);
+        t_mbar_wait(&full[s * T::BR + w], ph);
+        t_mbar_wait(&full[s * T::BR + w + 1], ph);
+    };
 
     auto fA = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OA) + row * T_VW + 3 * (lane + 1); };
     auto fB = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OB) + row * T_VW + 3 * (lane + 1); };
@@ -376,7 +372,7 @@ __global__ void __launch_bounds__(32 * TR, MINB)
         const int qP = P - (i0 - 1), qL = L - (i0 - 1);
         constexpr int KS = decltype(KC)::value;
         const int sP = KS >= 0 ? (KS + 1) % NS : qP % NS, sL = KS >= 0 ? KS : qL % NS;
-        t_mbar_wait(&full[sP], (unsigned)((qP / NS) & 1));
+        wait_rows(sP, qP);
         {
             double uo[3], uu[3], ru[3];
             int mu;
@@ -601,13 +597,19 @@ __global__ void __launch_bounds__(32 * TR, MINB)
                 }
             }
         }
-        // release plane L's slot; the last warp refills it with plane L + NS
+        // release rows w and w + 1 of plane L's slot; the last of a row's two readers refills it
+        // with that row of plane L + NS
         __syncwarp();
         if (lane == 0) {
             __threadfence_block();
-            if (atomicAdd(&cnt[sL], 1) == TR - 1) {
-                cnt[sL] = 0;
-                if (qL + NS < nq) issue(qL + NS);
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int row = w + i;
+                const int readers = (row == 0 || row == TR) ? 1 : 2;
+                if (atomicAdd(&cnt[sL * T::BR + row], 1) == readers - 1) {
+                    cnt[sL * T::BR + row] = 0;
+                    if (qL + NS < nq) issue_row(qL + NS, row);
+                }
             }
         }
     };
@@ -615,7 +617,7 @@ __global__ void __launch_bounds__(32 * TR, MINB)
     double FA[3][4], FB[3][4], rawA[3], rawB[3];
     int mA = 7, mB = 7;
     {   // prologue: plane i0 - 1 (q = 0)
-        t_mbar_wait(&full[0], 0u);
+        wait_rows(0, 0);
         double uo[3], uu[3], ru[3];
         int mu;
         input(0, i0 - 1, w, rawA, uo, mA);
@@ -712,20 +714,20 @@ static bool launch_h8t_t(const FineArgs& a, cudaStream_t s) {
         ok = t_map(&tm.A, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 1, vA - a.goffA, dA, nostr, box) &&
              t_map(&tm.B, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 1, vB - a.goffB, dB, nostr, box);
     } else {
-        ok = t_map_vec(&tm.A, a, vA, T::BR, true);
-        if (T::HB) ok = ok && t_map_vec(&tm.B, a, vB, T::BR, true);
-        if (hasC) ok = ok && t_map_vec(&tm.C, a, OP == FOP_CGP ? a.xv : a.Dinv, T::BR, OP == FOP_CGP);
+        ok = t_map_vec(&tm.A, a, vA, 1, true);   // one node row per box (per-row ring)
+        if (T::HB) ok = ok && t_map_vec(&tm.B, a, vB, 1, true);
+        if (hasC) ok = ok && t_map_vec(&tm.C, a, OP == FOP_CGP ? a.xv : a.Dinv, 1, OP == FOP_CGP);
     }
     {
         cuuint64_t dims[3] = {(cuuint64_t)g.N[2], (cuuint64_t)g.N[1], (cuuint64_t)g.N[0]};
         cuuint64_t str[2] = {(cuuint64_t)a.ep2 * 8, (cuuint64_t)a.ep2 * g.N[1] * 8};
-        cuuint32_t box[3] = {(cuuint32_t)T_EW, (cuuint32_t)TR, 1};
+        cuuint32_t box[3] = {(cuuint32_t)T_EW, 1, 1};
         ok = ok && t_map(&tm.E, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, a.E, dims, str, box);
     }
     {
         cuuint64_t dims[3] = {(cuuint64_t)g.nn[2], (cuuint64_t)g.nn[1], (cuuint64_t)g.nn[0]};
         cuuint64_t str[2] = {(cuuint64_t)a.m2, (cuuint64_t)a.m2 * g.nn[1]};
-        cuuint32_t box[3] = {(cuuint32_t)T_MW, (cuuint32_t)T::BR, 1};
+        cuuint32_t box[3] = {(cuuint32_t)T_MW, 1, 1};
         ok = ok && t_map(&tm.M, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, a.mask, dims, str, box);
     }
     if (!ok) return false;
