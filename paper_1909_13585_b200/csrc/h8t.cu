@@ -173,6 +173,8 @@ __device__ __forceinline__ void t_tma4(void* dst, const CUtensorMap* m, int c0, 
 // tile (c0 = 30 tc - 1 is odd): vectors at node c0 - 1 (100 doubles = 33 nodes + 1 per row), E at
 // element c0 - 1 (34 per row), masks at the 16-byte boundary at or below c0 - 1 (48 bytes per row).
 static constexpr int T_VW = 100, T_EW = 34, T_MW = 48;
+// shared-memory row pitches: every TMA destination (one box row each) 128-byte aligned
+static constexpr int T_VP = 112, T_EP = 48, T_MP = 128;
 // G(u) phi reads phi and u in the compact user layout, whose rows (odd node count) are not 16-byte
 // aligned: one 1-D box of 102 doubles per row, started at the even double at or below node c0 - 1
 // (row offset 0 / 1), rows 128-byte aligned in shared memory
@@ -183,9 +185,9 @@ struct TL {
     static constexpr int BR = TR + 1;                    // node rows per box
     static constexpr bool HB = OP != FOP_MATVEC;
     static constexpr bool HC = OP == FOP_JACOBI || OP == FOP_CGP || OP == FOP_RESTR3;
-    static constexpr int VB = BR * (OP == FOP_GPHI ? T_VWC : T_VW) * 8;   // vector box bytes
-    static constexpr int EB = TR * T_EW * 8;             // E box bytes
-    static constexpr int MB = BR * T_MW;                 // mask box bytes
+    static constexpr int VB = BR * T_VP * 8;             // vector rows
+    static constexpr int EB = TR * T_EP * 8;             // E rows
+    static constexpr int MB = BR * T_MP;                 // mask rows
     static constexpr int OA = 0;
     static constexpr int OB = OA + t_r128(VB);
     static constexpr int OC = OB + (HB ? t_r128(VB) : 0);
@@ -274,21 +276,21 @@ __global__ void __launch_bounds__(32 * TR, MINB)
             t_mbar_expect_tx(fb, (in ? 2 * T_RB * 8 : 0) + (i < TR ? T_EW * 8 : 0) + T_MW);
             if (in) {   // phi (RHS r) and u rows: one 1-D box each
                 const long long nd = 3 * (((long long)Q * n1 + jj) * n2 + c0 - 1);
-                t_tma1(sl + T::OA + i * T_VWC * 8, &tm.A, (int)((vbase + nd) & ~1LL), fb);
-                t_tma1(sl + T::OB + i * T_VWC * 8, &tm.B, (int)((a.goffB + nd) & ~1LL), fb);
+                t_tma1(sl + T::OA + i * T_VP * 8, &tm.A, (int)((vbase + nd) & ~1LL), fb);
+                t_tma1(sl + T::OB + i * T_VP * 8, &tm.B, (int)((a.goffB + nd) & ~1LL), fb);
             }
         } else {
             t_mbar_expect_tx(fb, nvf * T_VW * 8 + (i < TR ? T_EW * 8 : 0) + T_MW);
             const int cv = 3 * (c0 - 1);
-            t_tma4(sl + T::OA + i * T_VW * 8, &tm.A, cv, jj, Q, r, fb);
-            if (T::HB) t_tma4(sl + T::OB + i * T_VW * 8, &tm.B, cv, jj, Q, r, fb);
+            t_tma4(sl + T::OA + i * T_VP * 8, &tm.A, cv, jj, Q, r, fb);
+            if (T::HB) t_tma4(sl + T::OB + i * T_VP * 8, &tm.B, cv, jj, Q, r, fb);
             if (T::HC && hasC) {
-                if (OP == FOP_CGP) t_tma4(sl + T::OC + i * T_VW * 8, &tm.C, cv, jj, Q, r, fb);
-                else t_tma3(sl + T::OC + i * T_VW * 8, &tm.C, cv, jj, Q, fb);
+                if (OP == FOP_CGP) t_tma4(sl + T::OC + i * T_VP * 8, &tm.C, cv, jj, Q, r, fb);
+                else t_tma3(sl + T::OC + i * T_VP * 8, &tm.C, cv, jj, Q, fb);
             }
         }
-        if (i < TR) t_tma3(sl + T::OE + i * T_EW * 8, &tm.E, c0 - 1, jj, Q, fb);
-        t_tma3(sl + T::OM + i * T_MW, &tm.M, cm0, jj, Q, fb);
+        if (i < TR) t_tma3(sl + T::OE + i * T_EP * 8, &tm.E, c0 - 1, jj, Q, fb);
+        t_tma3(sl + T::OM + i * T_MP, &tm.M, cm0, jj, Q, fb);
     };
     if (threadIdx.x == 0)
         for (int q = 0; q < NS && q < nq; ++q)
@@ -300,11 +302,11 @@ __global__ void __launch_bounds__(32 * TR, MINB)
         t_mbar_wait(&full[s * T::BR + w + 1], ph);
     };
 
-    auto fA = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OA) + row * T_VW + 3 * (lane + 1); };
-    auto fB = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OB) + row * T_VW + 3 * (lane + 1); };
-    auto fC = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OC) + row * T_VW + 3 * (lane + 1); };
-    auto fE = [&](int s) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OE)[w * T_EW + lane + 1]; };
-    auto fM = [&](int s, int row) { return (int)(ring + s * T::SLOT + T::OM)[row * T_MW + mlane]; };
+    auto fA = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OA) + row * T_VP + 3 * (lane + 1); };
+    auto fB = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OB) + row * T_VP + 3 * (lane + 1); };
+    auto fC = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OC) + row * T_VP + 3 * (lane + 1); };
+    auto fE = [&](int s) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OE)[w * T_EP + lane + 1]; };
+    auto fM = [&](int s, int row) { return (int)(ring + s * T::SLOT + T::OM)[row * T_MP + mlane]; };
 
     // G(u) phi: compact rows (row offset 0 / 1 double), rows outside the grid were not loaded
     const bool colok = c >= 0 && c < n2;
@@ -314,7 +316,7 @@ __global__ void __launch_bounds__(32 * TR, MINB)
     };
     auto gvec = [&](int off, int s, int Q, int row, long long vb) {
         const long long nd = vb + 3 * (((long long)Q * n1 + (j0 + row)) * n2 + c0 - 1);
-        return reinterpret_cast<const double*>(ring + s * T::SLOT + off) + row * T_VWC + (int)(nd & 1) + 3 * (lane + 1);
+        return reinterpret_cast<const double*>(ring + s * T::SLOT + off) + row * T_VP + (int)(nd & 1) + 3 * (lane + 1);
     };
     // operator input of box row `row` at slot s (plane Q): raw (unmasked) and u (masked, fed to
     // the element)
