@@ -173,8 +173,6 @@ __device__ __forceinline__ void t_tma4(void* dst, const CUtensorMap* m, int c0, 
 // tile (c0 = 30 tc - 1 is odd): vectors at node c0 - 1 (100 doubles = 33 nodes + 1 per row), E at
 // element c0 - 1 (34 per row), masks at the 16-byte boundary at or below c0 - 1 (48 bytes per row).
 static constexpr int T_VW = 100, T_EW = 34, T_MW = 48;
-// shared-memory row pitches: every TMA destination (one box row each) 128-byte aligned
-static constexpr int T_VP = 112, T_EP = 48, T_MP = 128;
 // G(u) phi reads phi and u in the compact user layout, whose rows (odd node count) are not 16-byte
 // aligned: one 1-D box of 102 doubles per row, started at the even double at or below node c0 - 1
 // (row offset 0 / 1), rows 128-byte aligned in shared memory
@@ -185,9 +183,9 @@ struct TL {
     static constexpr int BR = TR + 1;                    // node rows per box
     static constexpr bool HB = OP != FOP_MATVEC;
     static constexpr bool HC = OP == FOP_JACOBI || OP == FOP_CGP || OP == FOP_RESTR3;
-    static constexpr int VB = BR * T_VP * 8;             // vector rows
-    static constexpr int EB = TR * T_EP * 8;             // E rows
-    static constexpr int MB = BR * T_MP;                 // mask rows
+    static constexpr int VB = BR * (OP == FOP_GPHI ? T_VWC : T_VW) * 8;   // vector box bytes
+    static constexpr int EB = TR * T_EW * 8;             // E box bytes
+    static constexpr int MB = BR * T_MW;                 // mask box bytes
     static constexpr int OA = 0;
     static constexpr int OB = OA + t_r128(VB);
     static constexpr int OC = OB + (HB ? t_r128(VB) : 0);
@@ -200,7 +198,15 @@ struct TL {
 template <int OP, int TR, int NS, int NB>
 static constexpr size_t h8t_smem_bytes() {
     using T = TL<OP, TR, NB>;
-    return (size_t)NS * T::SLOT + T::SINV + 8 * (NS * T::BR + 2 * NB * TR) + 8 * NS * T::BR + 8 * TR;
+    return (size_t)NS * T::SLOT + T::SINV + 8 * (NS + 2 * NB * TR) + 8 * NS + 8 * TR;
+}
+
+// per-slot expected TMA bytes (zero-filled out-of-range elements count too)
+template <int OP, int TR>
+__host__ __device__ constexpr unsigned h8t_tx_bytes(bool hasC) {
+    if (OP == FOP_GPHI) return (unsigned)(TR * T_EW * 8 + (TR + 1) * T_MW);   // + 2 T_RB * 8 per in-range row
+    using T = TL<OP, TR, 1>;
+    return (unsigned)(T::VB + (T::HB ? T::VB : 0) + ((T::HC && hasC) ? T::VB : 0) + T::EB + T::MB);
 }
 
 struct H8TMaps {
@@ -217,14 +223,11 @@ __global__ void __launch_bounds__(32 * TR, MINB)
     extern __shared__ __align__(128) unsigned char t_sm[];
     unsigned char* ring = t_sm;
     double* sinv = reinterpret_cast<double*>(t_sm + NS * T::SLOT);                       // [NB][TR][6][32]
-    // the ring is kept per box row: row i of a slot is read by warps i - 1 (upper row of its
-    // elements) and i (own row) only, so it is released and refilled as soon as those two are done
-    uint64_t* full = reinterpret_cast<uint64_t*>(t_sm + NS * T::SLOT + T::SINV);         // [NS][BR]
-    uint64_t* sfull = full + NS * T::BR;                                                 // [NB][TR]
+    uint64_t* full = reinterpret_cast<uint64_t*>(t_sm + NS * T::SLOT + T::SINV);         // [NS]
+    uint64_t* sfull = full + NS;                                                         // [NB][TR]
     uint64_t* sempty = sfull + NB * TR;                                                  // [NB][TR]
-    int* cnt = reinterpret_cast<int*>(sempty + NB * TR);                                 // [NS][BR]
-    double* s_dot = reinterpret_cast<double*>(t_sm + NS * T::SLOT + T::SINV + 8 * (NS * T::BR + 2 * NB * TR) +
-                                              8 * NS * T::BR);
+    int* cnt = reinterpret_cast<int*>(sempty + NB * TR);                                 // [NS]
+    double* s_dot = reinterpret_cast<double*>(t_sm + NS * T::SLOT + T::SINV + 8 * (NS + 2 * NB * TR) + 8 * NS);
 
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int R = a.R;
@@ -253,7 +256,7 @@ __global__ void __launch_bounds__(32 * TR, MINB)
     const double omega = a.omega;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < NS * T::BR; ++s) {
+        for (int s = 0; s < NS; ++s) {
             t_mbar_init(&full[s], 1);
             cnt[s] = 0;
         }
@@ -264,49 +267,48 @@ __global__ void __launch_bounds__(32 * TR, MINB)
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-    // row i of plane Q = i0 - 1 + q into slot q % NS: vector fields, E row i (i < TR), mask row i
-    const int nvf = 1 + (T::HB ? 1 : 0) + ((T::HC && hasC) ? 1 : 0);
-    auto issue_row = [&](int q, int i) {
+    const unsigned txb = h8t_tx_bytes<OP, TR>(hasC != 0);
+    auto issue = [&](int q) {   // plane Q = i0 - 1 + q into slot q % NS
         const int s = q % NS, Q = i0 - 1 + q;
         unsigned char* sl = ring + s * T::SLOT;
-        uint64_t* fb = &full[s * T::BR + i];
-        const int jj = j0 + i;
         if constexpr (OP == FOP_GPHI) {
-            const bool in = Q >= 0 && Q < n0 && jj >= 0 && jj < n1;
-            t_mbar_expect_tx(fb, (in ? 2 * T_RB * 8 : 0) + (i < TR ? T_EW * 8 : 0) + T_MW);
-            if (in) {   // phi (RHS r) and u rows: one 1-D box each
+            // phi (RHS r) and u rows in range, one 1-D box per row; E and masks as 3-D boxes
+            unsigned bytes = txb;
+            for (int i = 0; i < T::BR; ++i) {
+                const int jj = j0 + i;
+                if (Q >= 0 && Q < n0 && jj >= 0 && jj < n1) bytes += 2 * T_RB * 8;
+            }
+            t_mbar_expect_tx(&full[s], bytes);
+            for (int i = 0; i < T::BR; ++i) {
+                const int jj = j0 + i;
+                if (!(Q >= 0 && Q < n0 && jj >= 0 && jj < n1)) continue;
                 const long long nd = 3 * (((long long)Q * n1 + jj) * n2 + c0 - 1);
-                t_tma1(sl + T::OA + i * T_VP * 8, &tm.A, (int)((vbase + nd) & ~1LL), fb);
-                t_tma1(sl + T::OB + i * T_VP * 8, &tm.B, (int)((a.goffB + nd) & ~1LL), fb);
+                t_tma1(sl + T::OA + i * T_VWC * 8, &tm.A, (int)((vbase + nd) & ~1LL), &full[s]);
+                t_tma1(sl + T::OB + i * T_VWC * 8, &tm.B, (int)((a.goffB + nd) & ~1LL), &full[s]);
             }
-        } else {
-            t_mbar_expect_tx(fb, nvf * T_VW * 8 + (i < TR ? T_EW * 8 : 0) + T_MW);
-            const int cv = 3 * (c0 - 1);
-            t_tma4(sl + T::OA + i * T_VP * 8, &tm.A, cv, jj, Q, r, fb);
-            if (T::HB) t_tma4(sl + T::OB + i * T_VP * 8, &tm.B, cv, jj, Q, r, fb);
-            if (T::HC && hasC) {
-                if (OP == FOP_CGP) t_tma4(sl + T::OC + i * T_VP * 8, &tm.C, cv, jj, Q, r, fb);
-                else t_tma3(sl + T::OC + i * T_VP * 8, &tm.C, cv, jj, Q, fb);
-            }
+            t_tma3(sl + T::OE, &tm.E, c0 - 1, j0, Q, &full[s]);
+            t_tma3(sl + T::OM, &tm.M, cm0, j0, Q, &full[s]);
+            return;
         }
-        if (i < TR) t_tma3(sl + T::OE + i * T_EP * 8, &tm.E, c0 - 1, jj, Q, fb);
-        t_tma3(sl + T::OM + i * T_MP, &tm.M, cm0, jj, Q, fb);
+        t_mbar_expect_tx(&full[s], txb);
+        const int cv = 3 * (c0 - 1);
+        t_tma4(sl + T::OA, &tm.A, cv, j0, Q, r, &full[s]);
+        if (T::HB) t_tma4(sl + T::OB, &tm.B, cv, j0, Q, r, &full[s]);
+        if (T::HC && hasC) {
+            if (OP == FOP_CGP) t_tma4(sl + T::OC, &tm.C, cv, j0, Q, r, &full[s]);
+            else t_tma3(sl + T::OC, &tm.C, cv, j0, Q, &full[s]);
+        }
+        t_tma3(sl + T::OE, &tm.E, c0 - 1, j0, Q, &full[s]);
+        t_tma3(sl + T::OM, &tm.M, cm0, j0, Q, &full[s]);
     };
     if (threadIdx.x == 0)
-        for (int q = 0; q < NS && q < nq; ++q)
-            for (int i = 0; i < T::BR; ++i) issue_row(q, i);
-    // wait for rows w and w + 1 of slot s (fill index (q / NS))
-    auto wait_rows = [&](int s, int q) {
-        const unsigned ph = (unsigned)((q / NS) & 1);
-        t_mbar_wait(&full[s * T::BR + w], ph);
-        t_mbar_wait(&full[s * T::BR + w + 1], ph);
-    };
+        for (int q = 0; q < NS && q < nq; ++q) issue(q);
 
-    auto fA = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OA) + row * T_VP + 3 * (lane + 1); };
-    auto fB = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OB) + row * T_VP + 3 * (lane + 1); };
-    auto fC = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OC) + row * T_VP + 3 * (lane + 1); };
-    auto fE = [&](int s) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OE)[w * T_EP + lane + 1]; };
-    auto fM = [&](int s, int row) { return (int)(ring + s * T::SLOT + T::OM)[row * T_MP + mlane]; };
+    auto fA = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OA) + row * T_VW + 3 * (lane + 1); };
+    auto fB = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OB) + row * T_VW + 3 * (lane + 1); };
+    auto fC = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OC) + row * T_VW + 3 * (lane + 1); };
+    auto fE = [&](int s) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OE)[w * T_EW + lane + 1]; };
+    auto fM = [&](int s, int row) { return (int)(ring + s * T::SLOT + T::OM)[row * T_MW + mlane]; };
 
     // G(u) phi: compact rows (row offset 0 / 1 double), rows outside the grid were not loaded
     const bool colok = c >= 0 && c < n2;
@@ -316,7 +318,7 @@ __global__ void __launch_bounds__(32 * TR, MINB)
     };
     auto gvec = [&](int off, int s, int Q, int row, long long vb) {
         const long long nd = vb + 3 * (((long long)Q * n1 + (j0 + row)) * n2 + c0 - 1);
-        return reinterpret_cast<const double*>(ring + s * T::SLOT + off) + row * T_VP + (int)(nd & 1) + 3 * (lane + 1);
+        return reinterpret_cast<const double*>(ring + s * T::SLOT + off) + row * T_VWC + (int)(nd & 1) + 3 * (lane + 1);
     };
     // operator input of box row `row` at slot s (plane Q): raw (unmasked) and u (masked, fed to
     // the element)
@@ -374,7 +376,7 @@ __global__ void __launch_bounds__(32 * TR, MINB)
         const int qP = P - (i0 - 1), qL = L - (i0 - 1);
         constexpr int KS = decltype(KC)::value;
         const int sP = KS >= 0 ? (KS + 1) % NS : qP % NS, sL = KS >= 0 ? KS : qL % NS;
-        wait_rows(sP, qP);
+        t_mbar_wait(&full[sP], (unsigned)((qP / NS) & 1));
         {
             double uo[3], uu[3], ru[3];
             int mu;
@@ -599,19 +601,13 @@ __global__ void __launch_bounds__(32 * TR, MINB)
                 }
             }
         }
-        // release rows w and w + 1 of plane L's slot; the last of a row's two readers refills it
-        // with that row of plane L + NS
+        // release plane L's slot; the last warp refills it with plane L + NS
         __syncwarp();
         if (lane == 0) {
             __threadfence_block();
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                const int row = w + i;
-                const int readers = (row == 0 || row == TR) ? 1 : 2;
-                if (atomicAdd(&cnt[sL * T::BR + row], 1) == readers - 1) {
-                    cnt[sL * T::BR + row] = 0;
-                    if (qL + NS < nq) issue_row(qL + NS, row);
-                }
+            if (atomicAdd(&cnt[sL], 1) == TR - 1) {
+                cnt[sL] = 0;
+                if (qL + NS < nq) issue(qL + NS);
             }
         }
     };
@@ -619,7 +615,7 @@ __global__ void __launch_bounds__(32 * TR, MINB)
     double FA[3][4], FB[3][4], rawA[3], rawB[3];
     int mA = 7, mB = 7;
     {   // prologue: plane i0 - 1 (q = 0)
-        wait_rows(0, 0);
+        t_mbar_wait(&full[0], 0u);
         double uo[3], uu[3], ru[3];
         int mu;
         input(0, i0 - 1, w, rawA, uo, mA);
@@ -716,20 +712,20 @@ static bool launch_h8t_t(const FineArgs& a, cudaStream_t s) {
         ok = t_map(&tm.A, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 1, vA - a.goffA, dA, nostr, box) &&
              t_map(&tm.B, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 1, vB - a.goffB, dB, nostr, box);
     } else {
-        ok = t_map_vec(&tm.A, a, vA, 1, true);   // one node row per box (per-row ring)
-        if (T::HB) ok = ok && t_map_vec(&tm.B, a, vB, 1, true);
-        if (hasC) ok = ok && t_map_vec(&tm.C, a, OP == FOP_CGP ? a.xv : a.Dinv, 1, OP == FOP_CGP);
+        ok = t_map_vec(&tm.A, a, vA, T::BR, true);
+        if (T::HB) ok = ok && t_map_vec(&tm.B, a, vB, T::BR, true);
+        if (hasC) ok = ok && t_map_vec(&tm.C, a, OP == FOP_CGP ? a.xv : a.Dinv, T::BR, OP == FOP_CGP);
     }
     {
         cuuint64_t dims[3] = {(cuuint64_t)g.N[2], (cuuint64_t)g.N[1], (cuuint64_t)g.N[0]};
         cuuint64_t str[2] = {(cuuint64_t)a.ep2 * 8, (cuuint64_t)a.ep2 * g.N[1] * 8};
-        cuuint32_t box[3] = {(cuuint32_t)T_EW, 1, 1};
+        cuuint32_t box[3] = {(cuuint32_t)T_EW, (cuuint32_t)TR, 1};
         ok = ok && t_map(&tm.E, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, a.E, dims, str, box);
     }
     {
         cuuint64_t dims[3] = {(cuuint64_t)g.nn[2], (cuuint64_t)g.nn[1], (cuuint64_t)g.nn[0]};
         cuuint64_t str[2] = {(cuuint64_t)a.m2, (cuuint64_t)a.m2 * g.nn[1]};
-        cuuint32_t box[3] = {(cuuint32_t)T_MW, 1, 1};
+        cuuint32_t box[3] = {(cuuint32_t)T_MW, (cuuint32_t)T::BR, 1};
         ok = ok && t_map(&tm.M, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, a.mask, dims, str, box);
     }
     if (!ok) return false;

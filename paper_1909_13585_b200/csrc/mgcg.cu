@@ -1781,11 +1781,12 @@ static mg_status record_block_iter(mg_ctx* c, int R, double tol) {
 }
 
 // y = G(u) phi on one slab's compact device arrays (local geometry g).  3D with an even element
-// count along axis 2 and 8-byte aligned arrays: the TMA march kernel (h8t.cu, FOP_GPHI: centroid
-// stress formed in the kernel from u, the 19-nonzero stress matrix in the sum/difference basis);
-// otherwise centroid stresses (stress_sigma) + stress_apply.
+// count along axis 2 and 8-byte aligned arrays: the TMA march kernel (h8t.cu, FOP_GPHI; the
+// stress matrix in the sum/difference basis), reading the centroid stresses `sig` (stress_sigma,
+// once per call when several phi share them) or forming them in the kernel from u (sig = NULL);
+// otherwise centroid stresses + stress_apply.
 static void gphi_slab(mg_ctx* c, Slab& sl, const LevelGeom& g, const uint8_t* mask, const double* Es, const double* u,
-                      const double* phi, double* y, int nphi) {
+                      const double* phi, double* y, int nphi, const double* sig) {
     cudaStream_t s = c->stream;
     const int nv = c->dim == 2 ? 3 : 6;
     auto a8 = [](const void* p) { return ((uintptr_t)p & 7) == 0; };
@@ -1797,24 +1798,33 @@ static void gphi_slab(mg_ctx* c, Slab& sl, const LevelGeom& g, const uint8_t* ma
         a.x = phi; a.b = u; a.y = y; a.R = nphi; a.nu_paper = c->nu_paper ? 1 : 0;
         a.goffA = (int)(((uintptr_t)phi & 15) >> 3);
         a.goffB = (int)(((uintptr_t)u & 15) >> 3);
-        // several phi: centroid stresses once per element (stress_sigma) instead of once per
-        // element and phi inside the kernel (MG_GPHI_SIGMA=0/1 forces either)
-        const char* e = getenv("MG_GPHI_SIGMA");
-        const bool pre = e ? atoi(e) != 0 : nphi > 1;
-        if (pre) {
-            if (!sl.sig) cudaMalloc(&sl.sig, sizeof(double) * g.nelem * nv);
-            stress_sigma(g, Es, u, sl.sig, s);
-            a.sig = sl.sig;
-        }
+        a.sig = sig;
         if (fine_apply(FOP_GPHI, a, s) >= 0) {
-            c->launches += pre ? 2 : 1;
+            c->launches++;
             return;
         }
     }
+    if (!sig) {
+        if (!sl.sig) cudaMalloc(&sl.sig, sizeof(double) * g.nelem * nv);
+        stress_sigma(g, Es, u, sl.sig, s);
+        c->launches++;
+        sig = sl.sig;
+    }
+    stress_apply(g, sig, mask, phi, y, nphi, s);
+    c->launches++;
+}
+
+// centroid stresses of one slab (3 or 6 per element) when several phi share them, else NULL
+// (MG_GPHI_SIGMA=0/1 forces either)
+static const double* gphi_sigma(mg_ctx* c, Slab& sl, const LevelGeom& g, const double* Es, const double* u, int nphi) {
+    const char* e = getenv("MG_GPHI_SIGMA");
+    const bool pre = e ? atoi(e) != 0 : (nphi > 1 || c->dim == 2);
+    if (!pre) return nullptr;
+    const int nv = c->dim == 2 ? 3 : 6;
     if (!sl.sig) cudaMalloc(&sl.sig, sizeof(double) * g.nelem * nv);
-    stress_sigma(g, Es, u, sl.sig, s);
-    stress_apply(g, sl.sig, mask, phi, y, nphi, s);
-    c->launches += 2;
+    stress_sigma(g, Es, u, sl.sig, c->stream);
+    c->launches++;
+    return sl.sig;
 }
 
 mg_status stress_stiffness_apply(mg_handle c, const double* Es_e, const double* u, const double* phi, int nphi,
@@ -1828,7 +1838,8 @@ mg_status stress_stiffness_apply(mg_handle c, const double* Es_e, const double* 
     const bool dev = is_device_ptr(phi) && is_device_ptr(y) && is_device_ptr(u) && is_device_ptr(Es_e);
     if (!multi(c) && dev) {   // one slab, device buffers: direct
         Slab& sl = c->sl[0];
-        gphi_slab(c, sl, sl.lv[0].g, sl.lv[0].mask, Es_e, u, phi, y, nphi);
+        const double* sig = gphi_sigma(c, sl, sl.lv[0].g, Es_e, u, nphi);
+        gphi_slab(c, sl, sl.lv[0].g, sl.lv[0].mask, Es_e, u, phi, y, nphi, sig);
         CHECK_LAUNCH();
         return MG_OK;
     }
@@ -1867,6 +1878,7 @@ mg_status stress_stiffness_apply(mg_handle c, const double* Es_e, const double* 
         CU(cudaStreamWaitEvent(c->cs_out, c->gev_sig, 0));
         CU(cudaMemcpyAsync(dEs, Es_e, sizeof(double) * m, cudaMemcpyDefault, s));
         CU(cudaMemcpyAsync(du, u, sizeof(double) * n, cudaMemcpyDefault, s));
+        const double* sig = gphi_sigma(c, sl, g0, dEs, du, nphi);   // once for all chunks
         const int nch = std::min(mg_ctx::NCHUNK_EV, nphi);
         const int per = (nphi + nch - 1) / nch;
         for (int k = 0, k0 = 0; k0 < nphi; ++k, k0 += per) {
@@ -1875,7 +1887,7 @@ mg_status stress_stiffness_apply(mg_handle c, const double* Es_e, const double* 
             CU(cudaMemcpyAsync(dphi + n * k0, phi + n * k0, bytes, cudaMemcpyDefault, c->cs_in));
             CU(cudaEventRecord(c->gev_in[k], c->cs_in));
             CU(cudaStreamWaitEvent(s, c->gev_in[k], 0));
-            gphi_slab(c, sl, g0, sl.lv[0].mask, dEs, du, dphi + n * k0, dy + n * k0, kc);
+            gphi_slab(c, sl, g0, sl.lv[0].mask, dEs, du, dphi + n * k0, dy + n * k0, kc, sig);
             CU(cudaEventRecord(c->gev_k[k], s));
             CU(cudaStreamWaitEvent(c->cs_out, c->gev_k[k], 0));
             CU(cudaMemcpyAsync(y + n * k0, dy + n * k0, bytes, cudaMemcpyDefault, c->cs_out));
@@ -1942,7 +1954,8 @@ mg_status stress_stiffness_apply(mg_handle c, const double* Es_e, const double* 
     TRY(xchg(c, [&](const Slab& sl) { return elem_field(sl, 0, sl.Es, 1); }));
     for (Slab& sl : c->sl) {
         const Level& v = sl.lv[0];
-        gphi_slab(c, sl, v.g, v.mask, sl.Es, sl.u, sl.phi, sl.gy, nphi);
+        const double* sig = gphi_sigma(c, sl, v.g, sl.Es, sl.u, nphi);
+        gphi_slab(c, sl, v.g, v.mask, sl.Es, sl.u, sl.phi, sl.gy, nphi, sig);
         const long long pl = v.pn * dim, np = v.o1 - v.o0;
         CU(cudaMemcpy2DAsync(y_dst + dim * sl.uoff, n * 8, sl.gy + v.o0 * pl, v.g.ndof * 8, np * pl * 8, nphi,
                              cudaMemcpyDeviceToDevice, s));
