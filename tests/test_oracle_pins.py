@@ -451,6 +451,38 @@ def test_wilson_pure_bending_is_exact_on_the_unit_square():
     assert 0.5 * u @ K0 @ u > exact * 1.05
 
 
+@pytest.mark.parametrize("nu", [0.0, 0.3, 0.45])
+def test_wilson_pure_bending_is_exact_on_the_unit_cube(nu):
+    """3D pure bending sigma_xx = E kappa (y - 1/2), all other stresses zero: the exact field
+    u = kappa x (y - 1/2), v = -kappa x^2 / 2 - nu kappa ((y - 1/2)^2 - (z - 1/2)^2) / 2,
+    w = -nu kappa (y - 1/2)(z - 1/2) lies in the trilinear + bubble space of the incompatible-mode
+    hexahedron, so the condensed element energy of its nodal values equals the
+    continuum energy 1/2 int sigma_xx eps_xx = kappa^2 / 24 on the unit cube (E = 1).  A wrong
+    strain assignment of the bubble modes (e.g. the shear rows of B_i) changes this energy."""
+    Kw = fem.element_stiffness_wilson(3, nu)
+    nodes = fem.local_nodes(3).astype(float)
+    kappa = 1.0
+    x, y, z = nodes[:, 0], nodes[:, 1], nodes[:, 2]
+    u = np.zeros(24)
+    u[0::3] = kappa * x * (y - 0.5)
+    u[1::3] = -0.5 * kappa * x ** 2 - 0.5 * nu * kappa * ((y - 0.5) ** 2 - (z - 0.5) ** 2)
+    u[2::3] = -nu * kappa * (y - 0.5) * (z - 0.5)
+    exact = kappa ** 2 / 24.0
+    assert abs(0.5 * u @ Kw @ u - exact) < 1e-13
+    # the same bending about the other axes (coordinate permutations) is exact too
+    for perm in ((1, 2, 0), (2, 0, 1)):
+        up = np.zeros(24)
+        X = nodes[:, list(perm)]
+        comp = np.array([[0, 1, 2]])[0][list(perm)]
+        up[comp[0]::3] = kappa * X[:, 0] * (X[:, 1] - 0.5)
+        up[comp[1]::3] = -0.5 * kappa * X[:, 0] ** 2 - 0.5 * nu * kappa * ((X[:, 1] - 0.5) ** 2 - (X[:, 2] - 0.5) ** 2)
+        up[comp[2]::3] = -nu * kappa * (X[:, 1] - 0.5) * (X[:, 2] - 0.5)
+        assert abs(0.5 * up @ Kw @ up - exact) < 1e-13
+    # the standard trilinear element overestimates it (parasitic shear)
+    K0 = fem.element_stiffness(3, nu)
+    assert 0.5 * u @ K0 @ u > exact * 1.05
+
+
 def test_wilson_cantilever_closer_to_beam_theory():
     """SURVEY 8(f) NEXT-4 pin: on a coarse cantilever the incompatible-mode element is closer to
     Timoshenko beam theory than the standard Q4."""
