@@ -160,14 +160,51 @@ __global__ void block_axpy_kernel(long long n, long long stride, int R, const do
     }
 }
 
+// R > 16: the row's X values are staged in shared memory instead of registers (no spills; Y may
+// still alias X: a thread reads its whole row before writing it)
+static constexpr int BAX_T = 128;
+__global__ void __launch_bounds__(BAX_T) block_axpy_smem_kernel(long long n, long long stride, int R,
+                                                                const double* __restrict__ X,
+                                                                const double* __restrict__ C, const double* base,
+                                                                double* Y, double sign) {
+    extern __shared__ double bax_sm[];
+    double* Cs = bax_sm;               // R x R
+    double* xs = bax_sm + R * R;       // R x BAX_T
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) Cs[e] = C[e];
+    __syncthreads();
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        for (int k = 0; k < R; ++k) xs[k * BAX_T + threadIdx.x] = X[(long long)k * stride + i];
+        for (int j = 0; j < R; ++j) {
+            double s0 = 0.0, s1 = 0.0;
+            int k = 0;
+            for (; k + 1 < R; k += 2) {
+                s0 = fma(xs[k * BAX_T + threadIdx.x], Cs[k * R + j], s0);
+                s1 = fma(xs[(k + 1) * BAX_T + threadIdx.x], Cs[(k + 1) * R + j], s1);
+            }
+            if (k < R) s0 = fma(xs[k * BAX_T + threadIdx.x], Cs[k * R + j], s0);
+            const long long o = (long long)j * stride + i;
+            Y[o] = fma(sign, s0 + s1, base ? base[o] : Y[o]);
+        }
+    }
+}
+
 void block_axpy(long long n, long long stride, int R, const double* X, const double* C, const double* base, double* Y,
                 double sign, cudaStream_t s) {
     long long bl = (n + 255) / 256;
     if (bl > 148 * 8) bl = 148 * 8;
     if (R <= 8) block_axpy_kernel<8><<<(unsigned)bl, 256, 0, s>>>(n, stride, R, X, C, base, Y, sign);
     else if (R <= 16) block_axpy_kernel<16><<<(unsigned)bl, 256, 0, s>>>(n, stride, R, X, C, base, Y, sign);
-    else if (R <= 32) block_axpy_kernel<32><<<(unsigned)bl, 256, 0, s>>>(n, stride, R, X, C, base, Y, sign);
-    else block_axpy_kernel<64><<<(unsigned)bl, 128, 0, s>>>(n, stride, R, X, C, base, Y, sign);
+    else {
+        const size_t smem = sizeof(double) * ((size_t)R * R + (size_t)R * BAX_T);
+        static bool attr = [] {
+            cudaFuncSetAttribute(block_axpy_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+            return true;
+        }();
+        (void)attr;
+        long long b2 = (n + BAX_T - 1) / BAX_T;
+        if (b2 > 148 * 4) b2 = 148 * 4;
+        block_axpy_smem_kernel<<<(unsigned)b2, BAX_T, smem, s>>>(n, stride, R, X, C, base, Y, sign);
+    }
 }
 
 // per-column convergence of the block solve: rr[k] <= tol^2 bb[k] for all k -> *done = 1;

@@ -2,9 +2,10 @@
 // factorization"; the paper's coarsest solve is unstated).
 // Setup: the coarsest Galerkin operator (n_L <= a few thousand DOFs) is assembled
 // dense and inverted in place by blocked Gauss-Jordan (SPD => no pivoting needed,
-// block 32).  Per V-cycle: z = A^-1 r for all R vectors, one warp per row, so the
-// solve is a bandwidth-bound dense product instead of a latency-bound triangular
-// sweep.
+// block 32; rank-32 updates on the fp64 tensor cores, DMMA).  Per V-cycle: z = A^-1 r
+// for all R vectors as a dense product on DMMA tiles (dense_apply_mma_kernel: a CTA owns
+// 8 rows, its warps split k), so the solve is a bandwidth-bound dense product instead of a
+// latency-bound triangular sweep.
 #include <cstdlib>
 
 #include "kernels.h"
@@ -13,6 +14,7 @@ static constexpr int GJ_NB = 32;
 
 template <int DIM>
 __global__ void dense_from_stencil_kernel(LevelGeom g, const double* __restrict__ st, double* A, long long ld) {
+    pdl_begin();
     constexpr int NS = DIM == 2 ? 9 : 27;
     long long node = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     int s = blockIdx.y;
@@ -45,6 +47,7 @@ void dense_from_stencil(const LevelGeom& g, const double* st, double* A, long lo
 }
 
 __global__ void pad_identity_kernel(double* A, long long n, long long npad) {
+    pdl_begin();
     long long i = n + blockIdx.x * blockDim.x + threadIdx.x;
     if (i < npad) A[i * npad + i] = 1.0;
 }
@@ -59,6 +62,7 @@ static constexpr int GJ_TQ = 4;
 // Rrow[t][j] = sum_s P[t][s] A[k0+s][j]   (new row panel), Ccol[i][t] = A[i][k0+t] (old column panel)
 __global__ void gj_panels_kernel(const double* A, long long ld, long long n, int k0, const double* P, double* Rrow,
                                  double* Ccol) {
+    pdl_begin();
     __shared__ double Ps[GJ_NB][GJ_NB];
     const int tid = threadIdx.x;
     for (int e = tid; e < GJ_NB * GJ_NB; e += blockDim.x) Ps[e / GJ_NB][e % GJ_NB] = P[e];
@@ -86,6 +90,7 @@ __global__ void gj_panels_kernel(const double* A, long long ld, long long n, int
 // A[i][j] -= sum_t Ccol[i][t] Rrow[t][j] for all i, j (64x64 tile per CTA, 4x4 per thread).
 __global__ void __launch_bounds__(256) gj_update_kernel(double* A, long long ld, long long n, const double* Ccol,
                                                         const double* Rrow) {
+    pdl_begin();
     __shared__ double Cs[64][GJ_NB + 1];
     __shared__ double Rs[GJ_NB][64 + 1];
     const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
@@ -184,6 +189,7 @@ __device__ __forceinline__ void gj_block_inverse_smem(double (*S)[GJ_NB + 1], in
 // The standalone pivot-block inverse (1024 threads, one entry each) pivots on 2x2 blocks: half the
 // barrier pairs of the scalar sweep; the 2x2 pivot inverse is closed-form in every thread.
 __global__ void __launch_bounds__(1024) gj_diag_kernel(const double* A, long long ld, int k0, double* P, int* status) {
+    pdl_begin();
     __shared__ double S[GJ_NB][GJ_NB + 1];
     const int e = threadIdx.x, i = e / GJ_NB, j = e % GJ_NB;
     S[i][j] = A[(k0 + i) * ld + k0 + j];
@@ -220,6 +226,7 @@ __global__ void __launch_bounds__(1024) gj_diag_kernel(const double* A, long lon
 __global__ void __launch_bounds__(128) gj_update_mma_kernel(double* A, long long ld, long long n, const double* Ccol,
                                                             const double* Rrow, long long kn, double* Pn,
                                                             int* status) {
+    pdl_begin();
     __shared__ __align__(16) double Cs[64 * GU_LDC];
     __shared__ __align__(16) double Rs[GJ_NB * GU_LDR];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -310,6 +317,7 @@ __global__ void __launch_bounds__(128) gj_update_mma_kernel(double* A, long long
 // the block, NB / GJ_TQ columns per CTA row), grid.y >= GJ_TQ -> pivot rows.
 __global__ void __launch_bounds__(128) gj_fix_kernel(double* A, long long ld, long long n, int k0, const double* P,
                                                      const double* Ccol, const double* Rrow) {
+    pdl_begin();
     __shared__ double Ps[GJ_NB][GJ_NB];
     if (blockIdx.y >= GJ_TQ) {
         const long long j = (long long)blockIdx.x * 128 + threadIdx.x;
@@ -355,6 +363,17 @@ int dense_spd_inverse_launches(long long npad) {
     return (int)(fold ? 3 * steps + 1 : 4 * steps);
 }
 
+// MG_GJ_PDL=1: the Gauss-Jordan block steps launched with programmatic dependent launch (every
+// kernel of the sequence starts with griddepcontrol.wait, so none reads its predecessors' output
+// early); default off (B200 A/B in DESIGN.md)
+static bool gj_pdl() {
+    static bool v = [] {
+        const char* e = getenv("MG_GJ_PDL");
+        return e ? atoi(e) != 0 : false;
+    }();
+    return v;
+}
+
 void dense_spd_inverse(double* A, long long npad, double* work, int* d_status, cudaStream_t s) {
     double* Pb[2] = {work, work + GJ_NB * GJ_NB};   // ping-pong: block k's inverse, next block's
     double* Rrow = work + 2 * GJ_NB * GJ_NB;
@@ -368,13 +387,15 @@ void dense_spd_inverse(double* A, long long npad, double* work, int* d_status, c
         // the next diagonal block is inverted inside the update kernel when that kernel is long
         // enough to hide it (large coarsest levels), else by its own kernel
         const bool fold = mma && n >= GJ_FOLD_N;
-        if (!fold || k0 == 0) gj_diag_kernel<<<1, 1024, 0, s>>>(A, n, (int)k0, P, d_status);
-        gj_panels_kernel<<<dim3(nb, GJ_TQ), 128, 0, s>>>(A, n, n, (int)k0, P, Rrow, Ccol);
+        const bool pdl = gj_pdl();
+        if (!fold || k0 == 0) launch_kp(pdl, gj_diag_kernel, dim3(1), dim3(1024), 0, s, A, n, (int)k0, P, d_status);
+        launch_kp(pdl, gj_panels_kernel, dim3(nb, GJ_TQ), dim3(128), 0, s, A, n, n, (int)k0, (const double*)P, Rrow, Ccol);
         dim3 g((unsigned)((n + 63) / 64), (unsigned)((n + 63) / 64));
         const long long kn = (fold && k0 + GJ_NB < n) ? k0 + GJ_NB : -1;
-        if (mma) gj_update_mma_kernel<<<g, 128, 0, s>>>(A, n, n, Ccol, Rrow, kn, Pn, d_status);
-        else gj_update_kernel<<<g, 256, 0, s>>>(A, n, n, Ccol, Rrow);
-        gj_fix_kernel<<<dim3(nb, 2 * GJ_TQ), 128, 0, s>>>(A, n, n, (int)k0, P, Ccol, Rrow);
+        if (mma) launch_kp(pdl, gj_update_mma_kernel, g, dim3(128), 0, s, A, n, n, (const double*)Ccol, (const double*)Rrow, kn, Pn, d_status);
+        else launch_kp(pdl, gj_update_kernel, g, dim3(256), 0, s, A, n, n, (const double*)Ccol, (const double*)Rrow);
+        launch_kp(pdl, gj_fix_kernel, dim3(nb, 2 * GJ_TQ), dim3(128), 0, s, A, n, n, (int)k0, (const double*)P,
+                  (const double*)Ccol, (const double*)Rrow);
     }
 }
 

@@ -14,12 +14,13 @@
 // Work decomposition (B200): a warp owns a strip of node columns along axis 1 (30,
 // or 28 for the restriction so every coarse node is complete inside one warp), lanes
 // = columns, and marches along axis 0 over a chunk of node planes.  Plane data
-// (vectors, E_e, masks, coarse rows) is prefetched PD planes ahead into registers
-// (the ghost-padded layout makes every load unconditional).  (An earlier version
-// staged planes through a TMA bulk-copy / mbarrier shared-memory ring; the register
-// ring was faster at this occupancy.)  Each step exchanges column neighbours by warp shuffles, adds the contribution of
-// one element layer to the two node planes it touches, and finishes the lower plane.  No atomics, no colouring: deterministic.  The RHS
-// index is the fastest grid coordinate so the R warps of a tile share E_e in L2.
+// (vectors, E_e, masks, coarse rows) is staged by per-lane cp.async (LDGSTS, zero-fill
+// predicates) into a per-warp shared-memory ring of NSTAGE planes, one commit group per
+// plane (MG_ASYNC_RING; a register prefetch ring is the fallback); the ghost-padded layout
+// makes every load unconditional.  Each step exchanges column neighbours by warp shuffles,
+// adds the contribution of one element layer to the two node planes it touches, and
+// finishes the lower plane.  No atomics, no colouring: deterministic.  The RHS index is
+// the fastest grid coordinate so the R warps of a tile share E_e in L2.
 // K0 entries for nu = 0.3 are compile-time constants (element.cuh).
 #include "element.cuh"
 #include <algorithm>

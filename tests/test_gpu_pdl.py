@@ -32,15 +32,31 @@ print(json.dumps(out))
 """
 
 
+def _run(names, **env):
+    e = dict(os.environ, **env)
+    p = subprocess.run([sys.executable, "-c", SCRIPT % {"root": ROOT, "names": names}], env=e,
+                       capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert p.returncode == 0, p.stderr[-2000:]
+    return json.loads(p.stdout.strip().splitlines()[-1])
+
+
 @pytest.mark.gpu
 def test_pdl_on_off_bitwise():
-    names = ["T2b", "C1", "C2", "T3a"]
-    res = {}
-    for pdl in ("1", "0"):
-        env = dict(os.environ, MG_PDL=pdl)
-        p = subprocess.run([sys.executable, "-c", SCRIPT % {"root": ROOT, "names": names}], env=env,
-                           capture_output=True, text=True, timeout=600, cwd=ROOT)
-        assert p.returncode == 0, p.stderr[-2000:]
-        res[pdl] = json.loads(p.stdout.strip().splitlines()[-1])
+    """Default (PDL on the 2D iteration and the scalar / dense kernels) vs plain launches, up to
+    BASELINE's C3 / C4 sizes."""
+    names = ["T2b", "C1", "C2", "C3", "T3a", "C4"]
+    on, off = _run(names, MG_PDL="1"), _run(names, MG_PDL="0")
     for n in names:
-        assert res["1"][n] == res["0"][n], n
+        assert on[n] == off[n], n
+
+
+@pytest.mark.gpu
+def test_gauss_jordan_pdl_bitwise():
+    """The coarsest Gauss-Jordan sequence with programmatic dependent launch (MG_GJ_PDL=1; every
+    kernel of it waits on griddepcontrol before touching memory) gives the same inverse, hence
+    bitwise the same solves, as plain launches -- small levels (C1, T2b) and the folded
+    large-level path (T3e, n >= 3072)."""
+    names = ["T2b", "C1", "C2", "T3e"]
+    on, off = _run(names, MG_GJ_PDL="1"), _run(names, MG_GJ_PDL="0")
+    for n in names:
+        assert on[n] == off[n], n
