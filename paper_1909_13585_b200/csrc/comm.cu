@@ -111,6 +111,7 @@ bool comm_init(Comm& c, int rank, int nranks, const void* id128) {
     c.rank = rank;
     c.nranks = nranks;
     c.nccl = nullptr;
+    c.stage_local = std::getenv("MG_COMM_STAGE") && std::atoi(std::getenv("MG_COMM_STAGE")) == 1;
     if (nranks <= 1) return true;
     if (!load_nccl()) return false;
     ncclUniqueId id;
@@ -124,7 +125,40 @@ bool comm_init(Comm& c, int rank, int nranks, const void* id128) {
 void comm_destroy(Comm& c) {
     if (c.nccl && g_nccl.loaded) g_nccl.CommDestroy(static_cast<ncclComm_t>(c.nccl));
     c.nccl = nullptr;
+    if (c.stage) cudaFree(c.stage);
+    c.stage = nullptr;
+    c.stage_cap = 0;
 }
+
+bool comm_reserve(Comm& c, size_t bytes) {
+    if (c.nranks <= 1 && !c.stage_local) return true;
+    bytes = (bytes + 255) / 256 * 256;
+    if (bytes <= c.stage_cap) return true;
+    if (c.stage) cudaFree(c.stage);
+    c.stage = nullptr;
+    c.stage_cap = 0;
+    if (cudaMalloc(&c.stage, 4 * bytes) != cudaSuccess) {
+        g_nccl_err = "comm_reserve: cudaMalloc of the halo staging failed";
+        return false;
+    }
+    c.stage_cap = bytes;
+    return true;
+}
+
+namespace {
+// all nvec vectors of one plane <-> a contiguous message (nvec x plane bytes)
+bool pack_plane(char* buf, const PlaneField& f, int plane, cudaStream_t s) {
+    const size_t w = (size_t)f.plane_len * f.esize;
+    return cudaMemcpy2DAsync(buf, w, plane_ptr(f, plane), (size_t)f.vec_stride * f.esize, w, f.nvec,
+                             cudaMemcpyDeviceToDevice, s) == cudaSuccess;
+}
+bool unpack_plane(const PlaneField& f, int plane, const char* buf, cudaStream_t s) {
+    const size_t w = (size_t)f.plane_len * f.esize;
+    return cudaMemcpy2DAsync(plane_ptr(f, plane), (size_t)f.vec_stride * f.esize, buf, w, w, f.nvec,
+                             cudaMemcpyDeviceToDevice, s) == cudaSuccess;
+}
+size_t msg_bytes(const PlaneField& f) { return (size_t)f.plane_len * f.esize * f.nvec; }
+}  // namespace
 
 // ---------------------------------------------------------------- exchanges
 // f[k]: the field on local slab k (slabs in axis-0 order).
@@ -138,6 +172,24 @@ bool halo_forward(const Comm& c, const PlaneField* f, int nslab, cudaStream_t s)
     for (int k = 0; k + 1 < nslab; ++k) {
         const PlaneField& lo = f[k];
         const PlaneField& up = f[k + 1];
+        if (c.stage_local && lo.nvec > 1 && msg_bytes(lo) <= c.stage_cap) {
+            // the packed-message path of the cross-rank exchange, with a device copy as transport
+            // (MG_COMM_STAGE=1: exercises the packing on one GPU)
+            char* sbuf = c.stage;
+            char* rbuf = c.stage + 2 * c.stage_cap;
+            const size_t mb = msg_bytes(lo);
+            if (lo.dirs & 1) {
+                if (!pack_plane(sbuf, lo, lo.last_own, s)) return false;
+                if (cudaMemcpyAsync(rbuf, sbuf, mb, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return false;
+                if (!unpack_plane(up, up.lo_ghost, rbuf, s)) return false;
+            }
+            if (lo.dirs & 2) {
+                if (!pack_plane(sbuf, up, up.first_own, s)) return false;
+                if (cudaMemcpyAsync(rbuf, sbuf, mb, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return false;
+                if (!unpack_plane(lo, lo.hi_ghost, rbuf, s)) return false;
+            }
+            continue;
+        }
         if ((lo.dirs & 1) && !copy_plane(up, up.lo_ghost, lo, lo.last_own)) return false;
         if ((lo.dirs & 2) && !copy_plane(lo, lo.hi_ghost, up, up.first_own)) return false;
     }
@@ -149,15 +201,39 @@ bool halo_forward(const Comm& c, const PlaneField* f, int nslab, cudaStream_t s)
     const ncclDataType_t ty = first.esize == 8 ? ncclFloat64 : ncclUint8;
     const size_t cnt = (size_t)first.plane_len;
     const int dirs = first.dirs;
+    const bool lower = c.rank > 0, upper = c.rank + 1 < c.nranks;
+    if (first.nvec > 1 && msg_bytes(first) <= c.stage_cap) {
+        // one message per neighbour and direction: the boundary plane of all nvec vectors packed
+        char* s_dn = c.stage;
+        char* s_up = c.stage + c.stage_cap;
+        char* r_dn = c.stage + 2 * c.stage_cap;
+        char* r_up = c.stage + 3 * c.stage_cap;
+        const size_t n_all = cnt * first.nvec;
+        if (lower && (dirs & 2) && !pack_plane(s_dn, first, first.first_own, s)) return false;
+        if (upper && (dirs & 1) && !pack_plane(s_up, last, last.last_own, s)) return false;
+        if (!nccl_ok(g_nccl.GroupStart(), "ncclGroupStart")) return false;
+        if (lower) {
+            if (dirs & 2) g_nccl.Send(s_dn, n_all, ty, c.rank - 1, comm, s);
+            if (dirs & 1) g_nccl.Recv(r_dn, n_all, ty, c.rank - 1, comm, s);
+        }
+        if (upper) {
+            if (dirs & 1) g_nccl.Send(s_up, n_all, ty, c.rank + 1, comm, s);
+            if (dirs & 2) g_nccl.Recv(r_up, n_all, ty, c.rank + 1, comm, s);
+        }
+        if (!nccl_ok(g_nccl.GroupEnd(), "ncclGroupEnd")) return false;
+        if (lower && (dirs & 1) && !unpack_plane(first, first.lo_ghost, r_dn, s)) return false;
+        if (upper && (dirs & 2) && !unpack_plane(last, last.hi_ghost, r_up, s)) return false;
+        return true;
+    }
     if (!nccl_ok(g_nccl.GroupStart(), "ncclGroupStart")) return false;
     for (int v = 0; v < first.nvec; ++v) {
         const long long ofl = (long long)v * first.vec_stride * first.esize;
         const long long oll = (long long)v * last.vec_stride * last.esize;
-        if (c.rank > 0) {
+        if (lower) {
             if (dirs & 2) g_nccl.Send(plane_ptr(first, first.first_own) + ofl, cnt, ty, c.rank - 1, comm, s);
             if (dirs & 1) g_nccl.Recv(plane_ptr(first, first.lo_ghost) + ofl, cnt, ty, c.rank - 1, comm, s);
         }
-        if (c.rank + 1 < c.nranks) {
+        if (upper) {
             if (dirs & 1) g_nccl.Send(plane_ptr(last, last.last_own) + oll, cnt, ty, c.rank + 1, comm, s);
             if (dirs & 2) g_nccl.Recv(plane_ptr(last, last.hi_ghost) + oll, cnt, ty, c.rank + 1, comm, s);
         }
@@ -179,13 +255,21 @@ bool halo_reverse_add(const Comm& c, const PlaneField* f, int nslab, double* tmp
     const PlaneField& first = f[0];
     const PlaneField& last = f[nslab - 1];
     ncclComm_t comm = static_cast<ncclComm_t>(c.nccl);
+    const bool packed = first.nvec > 1 && msg_bytes(last) <= c.stage_cap;
+    if (packed && c.rank + 1 < c.nranks && !pack_plane(c.stage + c.stage_cap, last, last.hi_ghost, s)) return false;
     if (!nccl_ok(g_nccl.GroupStart(), "ncclGroupStart")) return false;
-    for (int v = 0; v < first.nvec; ++v) {
+    if (packed) {   // one message: the upper ghost plane of all vectors; received contiguous into tmp
         if (c.rank + 1 < c.nranks)
-            g_nccl.Send(plane_ptr(last, last.hi_ghost) + (long long)v * last.vec_stride * 8, last.plane_len,
-                        ncclFloat64, c.rank + 1, comm, s);
-        if (c.rank > 0)
-            g_nccl.Recv(tmp + (long long)v * first.plane_len, first.plane_len, ncclFloat64, c.rank - 1, comm, s);
+            g_nccl.Send(c.stage + c.stage_cap, (size_t)last.plane_len * last.nvec, ncclFloat64, c.rank + 1, comm, s);
+        if (c.rank > 0) g_nccl.Recv(tmp, (size_t)first.plane_len * first.nvec, ncclFloat64, c.rank - 1, comm, s);
+    } else {
+        for (int v = 0; v < first.nvec; ++v) {
+            if (c.rank + 1 < c.nranks)
+                g_nccl.Send(plane_ptr(last, last.hi_ghost) + (long long)v * last.vec_stride * 8, last.plane_len,
+                            ncclFloat64, c.rank + 1, comm, s);
+            if (c.rank > 0)
+                g_nccl.Recv(tmp + (long long)v * first.plane_len, first.plane_len, ncclFloat64, c.rank - 1, comm, s);
+        }
     }
     if (!nccl_ok(g_nccl.GroupEnd(), "ncclGroupEnd")) return false;
     if (c.rank > 0)

@@ -7,6 +7,11 @@
 struct Comm {
     int rank = 0, nranks = 1;
     void* nccl = nullptr;   // ncclComm_t when nranks > 1
+    // staging for packed halo messages (all vectors of a boundary plane in one message):
+    // send-down, send-up, recv-down, recv-up, `stage_cap` bytes each (comm_reserve, outside capture)
+    char* stage = nullptr;
+    size_t stage_cap = 0;
+    bool stage_local = false;   // MG_COMM_STAGE=1: in-process neighbours through the staging path too
 };
 
 // One field (vector family, mask, diagonal, element matrices ...) on one slab: plane p of
@@ -24,6 +29,7 @@ struct PlaneField {
 };
 
 bool comm_init(Comm& c, int rank, int nranks, const void* id128);
+bool comm_reserve(Comm& c, size_t bytes_per_message);
 void comm_destroy(Comm& c);
 bool comm_nccl_unique_id(void* out128);
 const char* comm_last_error();

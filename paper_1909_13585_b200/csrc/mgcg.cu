@@ -704,6 +704,14 @@ static mg_status ensure_vectors(mg_ctx* c, int R) {
         CU(cudaMalloc(&c->cz, sizeof(double) * c->nL * R));
         c->xtmp_cap = xplane * R;
         CU(cudaMalloc(&c->xtmp, sizeof(double) * std::max<long long>(c->xtmp_cap, 1)));
+        // packed halo messages: the largest vector plane (level 0 included) times R
+        long long p0 = 0;
+        for (const Slab& s : c->sl) {
+            const LevelGeom& g0 = s.lv[0].g;
+            p0 = std::max(p0, c->dim == 2 ? 2LL * s.pd.pitch : 3LL * g0.nn[1] * s.p3.p2);
+        }
+        if (!comm_reserve(c->comm, sizeof(double) * std::max(p0, xplane) * R))
+            return fail(MG_ERR_OOM, comm_last_error());
     }
     c->Ralloc = R;
     return MG_OK;
@@ -1157,11 +1165,28 @@ static mg_status record_iter(mg_ctx* c, int R, double tol) {
         TRY(blk_cgp(rc, pin, pout, &k));
         TRY(finish_dots(c, SM_ALPHA, R, k, pout == &Slab::p1 ? 1 : 0));
         TRY(blk_restrict(rc, rin, rout, &k));
-        TRY(finish_dots(c, SM_CONV, R, k, 0, tol));
+        const bool merged = c->comm.nranks > 1;
+        if (merged) {   // r.r partials -> sums[0, R); all-reduced together with r.z below
+            reduce_partials(R, c->partial, (int)k, c->pst, c->sums, c->stream);
+            c->launches++;
+        } else {
+            TRY(finish_dots(c, SM_CONV, R, k, 0, tol));
+        }
         int cw;
         TRY(coarse_cycle(rc, &cw));
         TRY(blk_post(rc, rout, cw, &k));
-        TRY(finish_dots(c, SM_BETA, R, k));
+        if (merged) {
+            // one allreduce of [r.r | r.z] per iteration (plus alpha's): the convergence test and
+            // beta are taken together after the post-smoother; an RHS that converged in this
+            // iteration ran one V-cycle it did not need (its result is never used)
+            reduce_partials(R, c->partial, (int)k, c->pst, c->sums + R, c->stream);
+            COMM(comm_allreduce_sum(c->comm, c->sums, 2 * R, c->stream));
+            cg_scalars(SM_CONV, R, c->sums, 1, c->ctl, tol, c->stream, 0, 1);
+            cg_scalars(SM_BETA, R, c->sums + R, 1, c->ctl, 0.0, c->stream, 0, 1);
+            c->launches += 3;
+        } else {
+            TRY(finish_dots(c, SM_BETA, R, k));
+        }
     }
     return MG_OK;
 }
@@ -1440,7 +1465,7 @@ static mg_status setup_impl(mg_ctx* c, const mg_grid* grid, const double* E_e, c
             c->cpack_cap = (long long)maxp * pnL * std::max(ns * dim * dim, MG_MAX_RHS * dim);
             CU(cudaMalloc(&c->cpack, sizeof(double) * c->cpack_cap));
             CU(cudaMalloc(&c->cgath, sizeof(double) * c->cpack_cap * nranks));
-            CU(cudaMalloc(&c->sums, sizeof(double) * MG_MAX_RHS));
+            CU(cudaMalloc(&c->sums, sizeof(double) * 2 * MG_MAX_RHS));
         }
     }
     // control block

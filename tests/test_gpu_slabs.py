@@ -119,3 +119,44 @@ def test_slab_update_modulus_and_host_buffers():
     xh = np.empty_like(inp["rhs"])
     mg.mgcg_solve(h, np.ascontiguousarray(inp["rhs"]), 1e-10, xh)
     assert rel(xh, U).max() < 1e-8
+
+
+_STAGE_SCRIPT = r"""
+import json, sys
+import numpy as np, torch
+sys.path.insert(0, %(root)r)
+import paper_1909_13585_b200 as mg
+from workloads import generate, get_config
+out = {}
+for name, nslab in %(cases)r:
+    cfg = get_config(name)
+    inp = generate(cfg)
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    h = mg.mg_setup_dist(cfg.nel, d(inp["E"]), d(inp["fixed"]), cfg.levels, nslab=nslab)
+    x = torch.empty((cfg.nrhs, inp["rhs"].shape[1]), dtype=torch.float64, device="cuda")
+    mg.mgcg_solve(h, d(inp["rhs"]), 1e-10, x)
+    out[name + str(nslab)] = x.cpu().numpy().tobytes().hex()
+print(json.dumps(out))
+"""
+
+
+def test_packed_halo_messages_bitwise():
+    """MG_COMM_STAGE=1 routes the in-process neighbour exchanges through the packed-message path
+    of the cross-rank exchange (all vectors of a boundary plane packed into one contiguous
+    message, moved, unpacked); data movement only, so the solves are bitwise those of the direct
+    plane copies."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cases = [("T2b", 3), ("C2", 4), ("T3b", 3), ("T3d", 5)]
+    res = {}
+    for st in ("0", "1"):
+        p = subprocess.run([sys.executable, "-c", _STAGE_SCRIPT % {"root": root, "cases": cases}],
+                           env=dict(os.environ, MG_COMM_STAGE=st), capture_output=True, text=True, timeout=900,
+                           cwd=root)
+        assert p.returncode == 0, p.stderr[-2000:]
+        res[st] = json.loads(p.stdout.strip().splitlines()[-1])
+    for k in res["0"]:
+        assert res["0"][k] == res["1"][k], k
