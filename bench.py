@@ -296,6 +296,23 @@ def run_ours(args, cfg):
         "clocks": clocks,
         "e2e": e2e,
     }
+    if ws > 1:
+        # self-check of the decomposed solve: every rank's owned part of x gathered into the global
+        # vector, compared on rank 0 with the undecomposed single-GPU solve of the same inputs
+        from paper_1909_13585_b200.dist import gather_owned
+        mg.mgcg_solve(h, rhs, cfg.tol, x)
+        xg = gather_owned(x, part, n_glob)
+        if rank == 0:
+            dg = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+            h1 = mg.mg_setup(cfg.nel, dg(inp_g["E"]), dg(inp_g["fixed"]), cfg.levels)
+            rhs1 = dg(inp_g["rhs"])
+            x1 = torch.empty_like(rhs1)
+            r1 = mg.mgcg_solve(h1, rhs1, cfg.tol, x1)
+            err = (torch.linalg.vector_norm(xg - x1, dim=1) / torch.linalg.vector_norm(x1, dim=1)).max().item()
+            result["parity_vs_1gpu"] = {"max_rel_l2": err, "ok": bool(err < 1e-8), "iters_1gpu": r1["iters"],
+                                        "iters_ngpu": reps[-1]["iters"]}
+            mg.mg_destroy(h1)
+        torch.distributed.barrier()
     if rank == 0 and ws == 1 and not args.no_cpu:
         result["cpu_baseline"] = cpu_baseline(cfg)
     if ws > 1:

@@ -67,3 +67,23 @@ def bootstrap_nccl_id(rank: int, nranks: int) -> bytes | None:
         buf.copy_(torch.frombuffer(bytearray(mg_nccl_unique_id()), dtype=torch.uint8))
     dist.broadcast(buf, 0)
     return bytes(buf.cpu().numpy().tobytes())
+
+
+def gather_owned(x_local, part: RankPart, n_glob: int):
+    """All ranks' owned slices of an (R, n_local) torch tensor, reassembled into the global
+    (R, n_glob) vector on every rank (all_gather of slices padded to the largest; works with the
+    nccl backend on CUDA tensors and gloo on CPU tensors).  Used by bench.py's N > 1 self-check."""
+    import torch
+    import torch.distributed as dist
+    R = x_local.shape[0]
+    spans = [None] * part.nranks
+    dist.all_gather_object(spans, (part.dof0, part.dof1))
+    mx = max(b - a for a, b in spans)
+    buf = torch.zeros((R, mx), dtype=x_local.dtype, device=x_local.device)
+    buf[:, :x_local.shape[1]] = x_local
+    outs = [torch.empty_like(buf) for _ in range(part.nranks)]
+    dist.all_gather(outs, buf)
+    full = torch.empty((R, n_glob), dtype=x_local.dtype, device=x_local.device)
+    for (a, b), o in zip(spans, outs):
+        full[:, a:b] = o[:, :b - a]
+    return full

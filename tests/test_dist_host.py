@@ -80,7 +80,13 @@ def _worker(rank, world, port, out):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     units = torch.tensor([float(p.dof1 - p.dof0)], dtype=torch.float64)
     dist.all_reduce(units, op=dist.ReduceOp.SUM)
-    out.put((rank, ids, parts, float(t.item()), float(units.item())))
+    # bench.py's N > 1 self-check gathers every rank's owned slice of x into the global vector
+    from paper_1909_13585_b200.dist import gather_owned
+    n = 2 * (cfg.nel[0] + 1) * (cfg.nel[1] + 1)
+    glob = torch.arange(3 * n, dtype=torch.float64).reshape(3, n)
+    full = gather_owned(glob[:, p.dof0:p.dof1].clone(), p, n)
+    gathered_ok = bool(torch.equal(full, glob))
+    out.put((rank, ids, parts, float(t.item()), float(units.item()), gathered_ok))
     dist.destroy_process_group()
 
 
@@ -96,7 +102,8 @@ def test_two_rank_gloo_bootstrap():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    (_, ids0, parts0, t0, u0), (_, ids1, parts1, t1, u1) = res
+    (_, ids0, parts0, t0, u0, g0), (_, ids1, parts1, t1, u1, g1) = res
+    assert g0 and g1
     assert ids0 == ids1 and ids0[0] == ids0[1] and len(ids0[0]) == 128
     assert parts0 == parts1
     (a0, a1, d0, d1), (b0, b1, e0, e1) = parts0
