@@ -213,7 +213,8 @@ mg_status stress_stiffness_apply(mg_handle h, const double* Es_e, const double* 
  * i.e. b_i[k] = d(phi_i^T G(u) phi_i)/du_k; G is linear in u so b does not depend on u.
  *   Es_e  device, nelem fp64 stress moduli (Eq. 2 :106);  phi (nphi, ndof) device;
  *   b     (nphi, ndof) device output, zero on fixed DOFs (ready for mgcg_solve).
- * Single slab (mg_setup) only this round.  Asynchronous. */
+ * Any decomposition (arrays cover the calling rank's owned part, as for mgcg_solve).
+ * Asynchronous (single slab) / synchronous (slabs). */
 mg_status mg_adjoint_rhs(mg_handle h, const double* Es_e, const double* phi, int nphi, double* b);
 /* NEXT-1: element sensitivities of simple buckling load factors, Eq. 4:
  *   out[i][e] = dEk_e (phi_ie^T K_e0 phi_ie - lambda_i z_ie^T K_e0 u_e)
@@ -223,7 +224,8 @@ mg_status mg_adjoint_rhs(mg_handle h, const double* Es_e, const double* phi, int
  * term) are taken on the free DOFs.  Reading: this is d lambda_i / d x_e for modes
  * normalised by phi^T (-G) phi = 1; for phi^T K phi = 1 multiply by lambda_i.
  *   dEk, dEs (nelem), u (ndof), phi, z (nphi, ndof): device;  lambda: nphi values, host or
- *   device;  out (nphi, nelem) device.  1 <= nphi <= MG_MAX_RHS.  Single slab.  Synchronous. */
+ *   device;  out (nphi, nelem) device.  1 <= nphi <= MG_MAX_RHS.  Any decomposition (owned
+ *   elements / nodes of the calling rank).  Synchronous. */
 mg_status mg_eigen_sensitivity(mg_handle h, const double* dEk, const double* dEs, const double* u, const double* phi,
                                const double* z, const double* lambda, int nphi, double* out);
 

@@ -244,6 +244,11 @@ struct Slab {
     double* zpre = nullptr;
     double *u = nullptr, *phi = nullptr, *gy = nullptr, *sig = nullptr, *Es = nullptr;   // G(u) phi (slab mode)
     long long gphi_cap = 0;
+    // NEXT-1 in slab mode: slab-local compact node vectors / element arrays (incl. ghosts)
+    double* tn[4] = {nullptr, nullptr, nullptr, nullptr};
+    long long tn_cap[4] = {0, 0, 0, 0};
+    double* te[3] = {nullptr, nullptr, nullptr};
+    long long te_cap[3] = {0, 0, 0};
 };
 
 struct mg_ctx {
@@ -1993,13 +1998,88 @@ mg_status stress_stiffness_apply(mg_handle c, const double* Es_e, const double* 
     return MG_OK;
 }
 
+// ---- slab mode of the NEXT-1 calls: this rank's owned arrays <-> slab-local compact copies
+// (owned planes / element layers copied, ghosts by exchange), the kernels then run unchanged on
+// each slab's local grid (the ghost element layer below and the ghost node planes make every
+// owned node / element exact, as for the operator).
+static mg_status stage_nodes(mg_ctx* c, const double* src, int nv, int k) {
+    cudaStream_t s = c->stream;
+    for (Slab& sl : c->sl) {
+        const Level& v = sl.lv[0];
+        const long long nd = v.g.ndof, need = nd * nv;
+        if (sl.tn_cap[k] < need) {
+            if (sl.tn[k]) cudaFree(sl.tn[k]);
+            sl.tn[k] = nullptr;
+            CU(cudaMalloc(&sl.tn[k], sizeof(double) * need));
+            sl.tn_cap[k] = need;
+        }
+        CU(cudaMemsetAsync(sl.tn[k], 0, sizeof(double) * need, s));
+        const long long pl = v.pn * c->dim, np = v.o1 - v.o0;
+        CU(cudaMemcpy2DAsync(sl.tn[k] + v.o0 * pl, nd * 8, src + c->dim * sl.uoff, c->n_rank * 8, np * pl * 8, nv,
+                             cudaMemcpyDeviceToDevice, s));
+    }
+    return xchg(c, [&](const Slab& sl) { return vec_field(c, sl, 0, sl.tn[k], nv); });
+}
+static mg_status unstage_nodes(mg_ctx* c, int k, int nv, double* dst) {
+    for (Slab& sl : c->sl) {
+        const Level& v = sl.lv[0];
+        const long long pl = v.pn * c->dim, np = v.o1 - v.o0;
+        CU(cudaMemcpy2DAsync(dst + c->dim * sl.uoff, c->n_rank * 8, sl.tn[k] + v.o0 * pl, v.g.ndof * 8, np * pl * 8, nv,
+                             cudaMemcpyDeviceToDevice, c->stream));
+    }
+    return MG_OK;
+}
+static mg_status stage_elems(mg_ctx* c, const double* src, int k) {
+    cudaStream_t s = c->stream;
+    const int rp0 = c->rank_p0[c->comm.rank];
+    for (Slab& sl : c->sl) {
+        const LevelGeom& g = sl.lv[0].g;
+        if (sl.te_cap[k] < g.nelem) {
+            if (sl.te[k]) cudaFree(sl.te[k]);
+            sl.te[k] = nullptr;
+            CU(cudaMalloc(&sl.te[k], sizeof(double) * g.nelem));
+            sl.te_cap[k] = g.nelem;
+        }
+        const long long le = g.nelem / g.N[0];
+        CU(cudaMemsetAsync(sl.te[k], 0, sizeof(double) * g.nelem, s));
+        CU(cudaMemcpyAsync(sl.te[k] + sl.gl * le, src + (long long)(sl.e0 - rp0) * le,
+                           sizeof(double) * (sl.e1 - sl.e0) * le, cudaMemcpyDeviceToDevice, s));
+    }
+    return xchg(c, [&](const Slab& sl) { return elem_field(sl, 0, sl.te[k], 1); });
+}
+
 mg_status mg_adjoint_rhs(mg_handle c, const double* Es_e, const double* phi, int nphi, double* b) {
     if (!c || !Es_e || !phi || !b) return fail(MG_ERR_ARG, "NULL argument");
     if (nphi < 1) return fail(MG_ERR_ARG, "nphi must be >= 1");
-    if (multi(c)) return fail(MG_ERR_ARG, "mg_adjoint_rhs: single slab only (this round)");
     if (!is_device_ptr(Es_e) || !is_device_ptr(phi) || !is_device_ptr(b))
         return fail(MG_ERR_ARG, "mg_adjoint_rhs: device pointers required");
     API_SCOPE(c);
+    if (multi(c)) {   // slab-local copies, kernels per slab, owned planes back
+        TRY(stage_elems(c, Es_e, 0));
+        TRY(stage_nodes(c, phi, nphi, 0));
+        long long need = 0;
+        for (Slab& sl : c->sl) need = std::max(need, (long long)nphi * sl.lv[0].g.nelem * (c->dim == 2 ? 3 : 6));
+        if (need > c->wbuf_cap) {
+            CU(cudaStreamSynchronize(c->stream));
+            if (c->wbuf) cudaFree(c->wbuf);
+            c->wbuf = nullptr;
+            CU(cudaMalloc(&c->wbuf, sizeof(double) * need));
+            c->wbuf_cap = need;
+        }
+        for (Slab& sl : c->sl) {
+            const long long nd = sl.lv[0].g.ndof * nphi;
+            if (sl.tn_cap[1] < nd) {
+                if (sl.tn[1]) cudaFree(sl.tn[1]);
+                sl.tn[1] = nullptr;
+                CU(cudaMalloc(&sl.tn[1], sizeof(double) * nd));
+                sl.tn_cap[1] = nd;
+            }
+            adjoint_rhs_apply(sl.lv[0].g, sl.te[0], sl.lv[0].mask, sl.tn[0], nphi, c->wbuf, sl.tn[1], c->stream);
+            c->launches += 2;
+        }
+        CHECK_LAUNCH();
+        return unstage_nodes(c, 1, nphi, b);
+    }
     const LevelGeom& g = c->G[0];
     const long long need = (long long)nphi * g.nelem * (c->dim == 2 ? 3 : 6);
     if (need > c->wbuf_cap) {
@@ -2019,7 +2099,6 @@ mg_status mg_eigen_sensitivity(mg_handle c, const double* dEk, const double* dEs
                                const double* z, const double* lambda, int nphi, double* out) {
     if (!c || !dEk || !dEs || !u || !phi || !z || !lambda || !out) return fail(MG_ERR_ARG, "NULL argument");
     if (nphi < 1 || nphi > MG_MAX_RHS) return fail(MG_ERR_ARG, "nphi out of range");
-    if (multi(c)) return fail(MG_ERR_ARG, "mg_eigen_sensitivity: single slab only (this round)");
     for (const void* p : {(const void*)dEk, (const void*)dEs, (const void*)u, (const void*)phi, (const void*)z,
                           (const void*)out})
         if (!is_device_ptr(p)) return fail(MG_ERR_ARG, "mg_eigen_sensitivity: device pointers required");
@@ -2027,6 +2106,33 @@ mg_status mg_eigen_sensitivity(mg_handle c, const double* dEk, const double* dEs
     if (!c->dlam) CU(cudaMalloc(&c->dlam, sizeof(double) * MG_MAX_RHS));
     CU(cudaMemcpyAsync(c->dlam, lambda, sizeof(double) * nphi,
                        is_device_ptr(lambda) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+    if (multi(c)) {   // slab-local copies; per slab the owned element layers of out are copied back
+        TRY(stage_elems(c, dEk, 0));
+        TRY(stage_elems(c, dEs, 1));
+        TRY(stage_nodes(c, u, 1, 0));
+        TRY(stage_nodes(c, phi, nphi, 1));
+        TRY(stage_nodes(c, z, nphi, 2));
+        const int rp0 = c->rank_p0[c->comm.rank];
+        for (Slab& sl : c->sl) {
+            const LevelGeom& g = sl.lv[0].g;
+            const long long no = g.nelem * nphi;
+            if (sl.tn_cap[3] < no) {
+                if (sl.tn[3]) cudaFree(sl.tn[3]);
+                sl.tn[3] = nullptr;
+                CU(cudaMalloc(&sl.tn[3], sizeof(double) * no));
+                sl.tn_cap[3] = no;
+            }
+            eigen_sensitivity_apply(g, sl.te[0], sl.te[1], sl.lv[0].mask, sl.tn[0], sl.tn[1], sl.tn[2], c->dlam, nphi,
+                                    sl.tn[3], c->stream);
+            c->launches++;
+            const long long le = g.nelem / g.N[0];
+            CU(cudaMemcpy2DAsync(out + (long long)(sl.e0 - rp0) * le, c->m_rank * 8, sl.tn[3] + sl.gl * le, g.nelem * 8,
+                                 (sl.e1 - sl.e0) * le * 8, nphi, cudaMemcpyDeviceToDevice, c->stream));
+        }
+        CHECK_LAUNCH();
+        CU(cudaStreamSynchronize(c->stream));
+        return MG_OK;
+    }
     eigen_sensitivity_apply(c->G[0], dEk, dEs, c->sl[0].lv[0].mask, u, phi, z, c->dlam, nphi, out, c->stream);
     c->launches++;
     CHECK_LAUNCH();
@@ -2580,6 +2686,10 @@ mg_status mg_destroy(mg_handle c) {
             if (v.st) cudaFree(v.st);
         }
         for (double* p : {s.E, s.elmA, s.elmB, s.Epad, s.Dinvpad, s.u, s.phi, s.gy, s.sig, s.Es})
+            if (p) cudaFree(p);
+        for (double* p : s.tn)
+            if (p) cudaFree(p);
+        for (double* p : s.te)
             if (p) cudaFree(p);
         if (s.maskpad) cudaFree(s.maskpad);
     }

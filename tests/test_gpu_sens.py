@@ -82,3 +82,31 @@ def test_adjoint_pipeline_on_gpu_matches_oracle():
     for i in range(2):
         ref = sens.eigen_sensitivity(cfg.nel, inp["fixed"], u, phi[i], zo[i], lam[i], dEk, dEs)
         assert np.abs(out.cpu().numpy()[i] - ref).max() <= 1e-8 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("name,nslab", [("T2b", 3), ("T2c", 4), ("T3b", 3), ("T3d", 5)])
+def test_next1_on_slabs_parity(name, nslab):
+    """NEXT-1 on a slab decomposition (in-process slabs: the halo path NCCL ranks use): the
+    adjoint right-hand sides and the Eq. 4 element sensitivities against the oracle, same bars."""
+    import paper_1909_13585_b200 as mg
+    cfg, inp = case(name)
+    h = mg.mg_setup_dist(cfg.nel, to_dev(inp["E"]), to_dev(inp["fixed"]), cfg.levels, nslab=nslab)
+    phi = rough_vectors(cfg, 3, seed_offset=41)
+    b = torch.empty((3, phi.shape[1]), dtype=torch.float64, device=DEV)
+    mg.mg_adjoint_rhs(h, to_dev(inp["Es"]), to_dev(phi), b)
+    ref = sens.adjoint_rhs(cfg.nel, inp["Es"], inp["fixed"], phi)
+    got = b.cpu().numpy()
+    assert (np.linalg.norm(got - ref, axis=1) / np.linalg.norm(ref, axis=1)).max() < 1e-13
+    K = assemble.assemble_K(cfg.nel, inp["E"], inp["fixed"])
+    u = solve.direct_solve(K, inp["rhs"][0], inp["fixed"])
+    z = rough_vectors(cfg, 3, seed_offset=47)
+    lam = [0.37, 1.9, 0.8]
+    rng = np.random.default_rng(9)
+    dEk = rng.uniform(0.1, 3.0, len(inp["E"]))
+    dEs = rng.uniform(0.1, 3.0, len(inp["E"]))
+    out = torch.empty((3, len(inp["E"])), dtype=torch.float64, device=DEV)
+    mg.mg_eigen_sensitivity(h, to_dev(dEk), to_dev(dEs), to_dev(u), to_dev(phi), to_dev(z), lam, out)
+    got = out.cpu().numpy()
+    for i in range(3):
+        ref = sens.eigen_sensitivity(cfg.nel, inp["fixed"], u, phi[i], z[i], lam[i], dEk, dEs)
+        assert np.abs(got[i] - ref).max() <= 1e-13 * np.abs(ref).max()
