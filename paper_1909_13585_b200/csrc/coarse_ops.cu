@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(128) coarse_kernel(CoarseArgs a, int r0) {
         const long long q = node + ((long long)d0 * n1 + d1) * n2 + d2;
         double blk[DIM * DIM];
 #pragma unroll
-        for (int e = 0; e < DIM * DIM; ++e) blk[e] = a.st[(long long)(s * DIM * DIM + e) * nn + node];
+        for (int e = 0; e < DIM * DIM; ++e) blk[e] = __ldcs(a.st + (long long)(s * DIM * DIM + e) * nn + node);   // streamed once: keep L1 for x
 #pragma unroll
         for (int rr = 0; rr < RB; ++rr) {
             if (!act[rr]) continue;
@@ -497,7 +497,7 @@ __global__ void __launch_bounds__(32 * DIM) coarse_comp_kernel(CoarseArgs a, int
         const long long q = node + ((long long)d0 * n1 + d1) * n2 + d2;
         double blk[DIM];
 #pragma unroll
-        for (int k2 = 0; k2 < DIM; ++k2) blk[k2] = a.st[(long long)((s * DIM + k) * DIM + k2) * nn + node];
+        for (int k2 = 0; k2 < DIM; ++k2) blk[k2] = __ldcs(a.st + (long long)((s * DIM + k) * DIM + k2) * nn + node);
 #pragma unroll
         for (int rr = 0; rr < RB; ++rr) {
             if (!act[rr]) continue;
