@@ -3,6 +3,8 @@
 // P = bilinear / trilinear nodal interpolation (tensor product of the 1-D stencil
 // [1/2, 1, 1/2]), restriction R = P^T, both masked by the free-DOF masks of the
 // two levels (reading r11: P_m = M_f P M_c).
+#include <cstdlib>
+
 #include "kernels.h"
 
 // coarse(I,k) = free_c(I,k) * sum_{delta in {-1,0,1}^d} w(delta) free_f(2I+delta,k) fine(2I+delta,k)
@@ -139,7 +141,9 @@ void prolong_add(const LevelGeom& gf, const LevelGeom& gc, const uint8_t* mf, co
                  cudaStream_t s, int off0) {
     int th = 128;
     const long long blocks = (gf.nnodes + th - 1) / th;
-    dim3 bl((unsigned)blocks, blocks >= 148 * 16 ? 1 : R);
+    // RHS over grid.y (one RHS per thread) unless the level is large; MG_PROLONG_SPLIT=1 always splits
+    static const int split = getenv("MG_PROLONG_SPLIT") ? atoi(getenv("MG_PROLONG_SPLIT")) : 0;
+    dim3 bl((unsigned)blocks, (blocks >= 148 * 16 && !split) ? 1 : R);
     if (gf.dim == 2)
         launch_kp(false, prolong_kernel<2>, dim3(bl), dim3(th), 0, s, gf, gc, mf, mc, coarse, fine, R, active, done, accumulate, off0);
     else
