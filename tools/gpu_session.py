@@ -110,6 +110,12 @@ def evidence(tag):
     open(f"{d}/status.txt", "w").write("\n".join(f"{k} exit {v}" for k, v in st) + "\n")
     launches(tag, "C5")
     launches(tag, "C3")
+    # roofline kernels and the G(u) phi kernels, one ncu --set full capture each
+    ncu(tag, "C5", "h8t_kernel<\\(int\\)3,", "1", "3")
+    ncu(tag, "C5", "h8t_kernel<\\(int\\)6,", "1", "1")
+    ncu(tag, "C3", "march2_kernel<\\(int\\)3,", "1", "3")
+    ncu(tag, "C3", "stress_apply_kernel", "1", "1")
+    ncu(tag, "C5", "coarse_kernel<\\(int\\)3, \\(int\\)1, \\(int\\)8", "1", "3")
 
 
 if __name__ == "__main__":
