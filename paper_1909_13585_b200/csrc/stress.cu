@@ -9,6 +9,10 @@
 // per element from sigma_e (3 or 6 doubles) and applies them to all d components.
 // Layout and march are those of the fine matvec (fine_ops.cu): warp = 30 node
 // columns, march along axis 0, phi index fastest in the grid.
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+
 #include "kernels.h"
 
 __constant__ double c_D0[36];          // Voigt constitutive matrix, E = 1
@@ -250,8 +254,177 @@ __global__ void __launch_bounds__(128) stress_apply_kernel(LevelGeom g, const do
     }
 }
 
+// ---------------------------------------------------------------- 2D: sum/difference-basis march
+// y = G(u) phi in 2D with the element matrix in the per-axis (m, d) basis (as the Q4 stiffness in
+// fine2d.cu): S^ = sum_ij sigma_ij H^_ij has 5 nonzeros (rows / cols of the (m, m) mode are zero).
+// A warp owns 30 node columns (lanes 1..30) of one phi and marches along axis 0; the next PD
+// planes of phi (one 16-byte load per node), masks and the element stresses (3 per element) are
+// prefetched into registers; column neighbours by shuffles, the axis-0 half of each element
+// result carried to the next plane.  Reads phi and sigma once, writes y once.
+__host__ __device__ constexpr double s2f(int kind, int ta, int tb) {   // 1-D factors in the (m, d) basis
+    return kind == 0 ? (ta == tb ? (ta == 0 ? 0.25 : 1.0 / 12.0) : 0.0)
+         : kind == 1 ? ((ta == 1 && tb == 1) ? 1.0 : 0.0)
+         : kind == 2 ? ((ta == 1 && tb == 0) ? 0.5 : 0.0)
+                     : ((ta == 0 && tb == 1) ? 0.5 : 0.0);
+}
+__host__ __device__ constexpr double s2h(int i, int j, int s, int t) {   // H^_ij[s][t]
+    double v = 1.0;
+    for (int k = 0; k < 2; ++k) {
+        const int ta = (s >> (1 - k)) & 1, tb = (t >> (1 - k)) & 1;
+        const int kind = (k == i && k == j) ? 1 : (k == i ? 2 : (k == j ? 3 : 0));
+        v *= s2f(kind, ta, tb);
+    }
+    return v;
+}
+
+static constexpr int G2_PD = 3;    // planes prefetched
+static constexpr int G2_CH = 64;   // planes per chunk
+
+__global__ void __launch_bounds__(128) stress2_kernel(LevelGeom g, const double* __restrict__ sig,
+                                                      const uint8_t* __restrict__ mask, const double* __restrict__ phi,
+                                                      double* __restrict__ y, int nphi, int nct, int nch, int hch) {
+    const int lane = threadIdx.x & 31;
+    const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (w >= (long long)nphi * nct * nch) return;
+    const int r = (int)(w % nphi);
+    const int item = (int)(w / nphi);
+    const int ct = item % nct, ch = item / nct;
+    const int n0 = g.nn[0], n1 = g.nn[1], N0 = g.N[0], N1 = g.N[1];
+    const int c = 30 * ct + lane - 1;
+    const bool cin = c >= 0 && c < n1;
+    const bool own = cin && lane >= 1 && lane <= 30;
+    const bool ein = c >= 0 && c < N1 && lane < 31;
+    const int i0 = ch * hch, i1 = min(i0 + hch, n0);
+    const double2* ph = reinterpret_cast<const double2*>(phi + (long long)r * g.ndof);
+    // prefetch ring: phi of node (P, c), its mask, sigma of element (P, c)
+    double2 rp[G2_PD];
+    int rm[G2_PD];
+    double rs[G2_PD][3];
+    auto load = [&](int P, int q) {
+        const bool v = cin && P >= 0 && P < n0;
+        const long long nd = v ? (long long)P * n1 + c : 0;
+        rm[q] = v ? mask[nd] : 3;
+        rp[q] = v ? __ldg(ph + nd) : make_double2(0.0, 0.0);
+        const bool ve = ein && P >= 0 && P < N0;
+        const long long el = ve ? (long long)P * N1 + c : 0;
+#pragma unroll
+        for (int v3 = 0; v3 < 3; ++v3) rs[q][v3] = ve ? __ldg(sig + 3 * el + v3) : 0.0;
+    };
+#pragma unroll
+    for (int q = 0; q < G2_PD; ++q) load(i0 - 1 + q, q);
+    double FL[2][2], CY[2][2];   // [comp][t1]: face (m, d along axis 1) of plane L; carry to plane P
+    int mL;
+    {
+        const int m = rm[0];
+        const double u0 = (m & 1) ? 0.0 : rp[0].x, u1 = (m & 2) ? 0.0 : rp[0].y;
+        const double un0 = __shfl_down_sync(MGK_FULL, u0, 1), un1 = __shfl_down_sync(MGK_FULL, u1, 1);
+        FL[0][0] = u0 + un0; FL[0][1] = un0 - u0;
+        FL[1][0] = u1 + un1; FL[1][1] = un1 - u1;
+        mL = m;
+    }
+    CY[0][0] = CY[0][1] = CY[1][0] = CY[1][1] = 0.0;
+    double sgL[3] = {rs[0][0], rs[0][1], rs[0][2]};
+    for (int L = i0 - 1; L < i1; ++L) {
+        // rotate the ring: slot (L - i0 + 2) % PD holds plane L + 1
+        const int q1 = ((L - i0 + 2) % G2_PD + G2_PD) % G2_PD;
+        double2 pP = rp[0];
+        int mP = rm[0];
+        double sgP[3] = {rs[0][0], rs[0][1], rs[0][2]};
+#pragma unroll
+        for (int q = 0; q < G2_PD; ++q)
+            if (q == q1) { pP = rp[q]; mP = rm[q]; sgP[0] = rs[q][0]; sgP[1] = rs[q][1]; sgP[2] = rs[q][2]; }
+        // refill that slot with plane L + 1 + PD... (the slot of plane L is free: load L + PD)
+        const int q0 = ((L - i0 + 1) % G2_PD + G2_PD) % G2_PD;
+#pragma unroll
+        for (int q = 0; q < G2_PD; ++q)
+            if (q == q0) load(L + G2_PD, q);
+        double FP[2][2];
+        {
+            const double u0 = (mP & 1) ? 0.0 : pP.x, u1 = (mP & 2) ? 0.0 : pP.y;
+            const double un0 = __shfl_down_sync(MGK_FULL, u0, 1), un1 = __shfl_down_sync(MGK_FULL, u1, 1);
+            FP[0][0] = u0 + un0; FP[0][1] = un0 - u0;
+            FP[1][0] = u1 + un1; FP[1][1] = un1 - u1;
+        }
+        // element (L, c): S^ from sigma_L, u^ (s = 2 t0 + t1), y^ = S^ u^, per component
+        double S[4][4];
+#pragma unroll
+        for (int a = 1; a < 4; ++a)
+#pragma unroll
+            for (int b = 1; b < 4; ++b) {
+                double v = 0.0;
+                bool first = true;
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const double hv = s2h(i, j, a, b);
+                        if (hv == 0.0) continue;
+                        const double sv = (i == j) ? sgL[i] : sgL[2];
+                        v = first ? sv * hv : fma(sv, hv, v);
+                        first = false;
+                    }
+                S[a][b] = v;
+            }
+        double GL[2][2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            double uh[4], yh[4];
+            uh[1] = FL[k][1] + FP[k][1];   // (m, d)
+            uh[2] = FP[k][0] - FL[k][0];   // (d, m)
+            uh[3] = FP[k][1] - FL[k][1];   // (d, d)
+#pragma unroll
+            for (int a = 1; a < 4; ++a) {
+                double v = 0.0;
+                bool first = true;
+#pragma unroll
+                for (int b = 1; b < 4; ++b) {
+                    bool nz = false;
+#pragma unroll
+                    for (int i = 0; i < 2; ++i)
+#pragma unroll
+                        for (int j = 0; j < 2; ++j) nz = nz || s2h(i, j, a, b) != 0.0;
+                    if (!nz) continue;
+                    v = first ? S[a][b] * uh[b] : fma(S[a][b], uh[b], v);
+                    first = false;
+                }
+                yh[a] = v;
+            }
+            // axis 0: plane L gets ym - yd, plane P gets ym + yd (t1 = m: s = 0 / 2, t1 = d: s = 1 / 3)
+            GL[k][0] = CY[k][0] - yh[2];
+            CY[k][0] = yh[2];
+            GL[k][1] = CY[k][1] + (yh[1] - yh[3]);
+            CY[k][1] = yh[1] + yh[3];
+        }
+        // axis 1: node c gets fm - fd, node c + 1 gets fm + fd (from lane - 1)
+        if (L >= i0) {
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const double up = __shfl_up_sync(MGK_FULL, GL[k][0] + GL[k][1], 1);
+                const double v = (GL[k][0] - GL[k][1]) + (lane > 0 ? up : 0.0);
+                if (own && ((mL >> k) & 1) == 0) y[(long long)r * g.ndof + 2 * ((long long)L * n1 + c) + k] = v;
+                else if (own) y[(long long)r * g.ndof + 2 * ((long long)L * n1 + c) + k] = 0.0;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) { FL[k][0] = FP[k][0]; FL[k][1] = FP[k][1]; }
+        sgL[0] = sgP[0]; sgL[1] = sgP[1]; sgL[2] = sgP[2];
+        mL = mP;
+    }
+}
+
 void stress_apply(const LevelGeom& g, const double* sig, const uint8_t* mask, const double* phi, double* y, int nphi,
                   cudaStream_t s) {
+    if (g.dim == 2 && ((uintptr_t)phi & 15) == 0 && !getenv("MG_STRESS2_LEGACY")) {
+        const int nct = (g.nn[1] + 29) / 30;
+        int nch = std::max(1, (g.nn[0] + G2_CH - 1) / G2_CH);
+        // enough warps: at least ~8 per SM
+        while ((long long)nct * nch * nphi < 148LL * 16 && nch < g.nn[0] / 8) nch *= 2;
+        const int hch = (g.nn[0] + nch - 1) / nch;
+        nch = (g.nn[0] + hch - 1) / hch;
+        const long long warps = (long long)nphi * nct * nch;
+        stress2_kernel<<<(unsigned)((warps + 3) / 4), 128, 0, s>>>(g, sig, mask, phi, y, nphi, nct, nch, hch);
+        return;
+    }
     int ncols = g.nn[g.dim - 1];
     int nct = (ncols + SCOLS - 1) / SCOLS;
     int ch = g.dim == 2 ? SCH2 : SCH3;
