@@ -65,73 +65,11 @@ __global__ void restrict_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* __res
     }
 }
 
-// Large levels: a thread per coarse node handles RB right-hand sides, so the 27-neighbour index
-// arithmetic and the fine mask are formed once per node instead of once per node and RHS (the
-// one-RHS kernel above spends ~60 % of its instructions on them).
-template <int RB>
-__global__ void __launch_bounds__(128) restrict3_rb_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* __restrict__ mf,
-                                                           const uint8_t* __restrict__ mc,
-                                                           const double* __restrict__ fine,
-                                                           double* __restrict__ coarse, int R, const int* active,
-                                                           const int* done, int off0, int fo0, int fo1) {
-    pdl_begin();
-    const long long I = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (I >= gc.nnodes) return;
-    if (done && *done) return;
-    const int r0 = blockIdx.y * RB;
-    const int nr = min(RB, R - r0);
-    int ci2 = (int)(I % gc.nn[2]);
-    long long t = I / gc.nn[2];
-    const int ci1 = (int)(t % gc.nn[1]), ci0 = (int)(t / gc.nn[1]);
-    const int f0 = 2 * ci0 - off0, f1 = 2 * ci1, f2 = 2 * ci2;
-    const int n1 = gf.nn[1], n2 = gf.nn[2], p2 = gf.p2;
-    bool act[RB];
-#pragma unroll
-    for (int q = 0; q < RB; ++q) act[q] = q < nr && (!active || active[r0 + q]);
-    double acc[RB][3];
-#pragma unroll
-    for (int q = 0; q < RB; ++q) acc[q][0] = acc[q][1] = acc[q][2] = 0.0;
-    const double* fv0 = fine + (long long)r0 * gf.vstr;
-#pragma unroll
-    for (int sidx = 0; sidx < 27; ++sidx) {
-        const int d0 = sidx / 9 - 1, d1 = (sidx / 3) % 3 - 1, d2 = sidx % 3 - 1;
-        const double w = (d0 ? 0.5 : 1.0) * (d1 ? 0.5 : 1.0) * (d2 ? 0.5 : 1.0);
-        const int g0 = f0 + d0, g1 = f1 + d1, g2 = f2 + d2;
-        if (!(g0 >= 0 && g0 < gf.nn[0] && g0 >= fo0 && g0 < fo1 && g1 >= 0 && g1 < n1 && g2 >= 0 && g2 < n2)) continue;
-        const int fm = mf[((long long)g0 * n1 + g1) * n2 + g2];
-        const double* fp = fv0 + 3 * (((long long)g0 * n1 + g1) * p2 + g2);
-        const double w0 = (fm & 1) ? 0.0 : w, w1 = (fm & 2) ? 0.0 : w, w2 = (fm & 4) ? 0.0 : w;
-#pragma unroll
-        for (int q = 0; q < RB; ++q) {
-            if (q >= nr) break;
-            const double* v = fp + (long long)q * gf.vstr;
-            acc[q][0] = fma(w0, __ldg(v), acc[q][0]);
-            acc[q][1] = fma(w1, __ldg(v + 1), acc[q][1]);
-            acc[q][2] = fma(w2, __ldg(v + 2), acc[q][2]);
-        }
-    }
-    const int mcb = mc[I];
-#pragma unroll
-    for (int q = 0; q < RB; ++q) {
-        if (q >= nr || !act[q]) continue;
-        double* cv = coarse + (long long)(r0 + q) * gc.ndof + 3 * I;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) cv[k] = ((mcb >> k) & 1) ? 0.0 : acc[q][k];
-    }
-}
-
 void restrict_apply(const LevelGeom& gf, const LevelGeom& gc, const uint8_t* mf, const uint8_t* mc,
                     const double* fine, double* coarse, int R, const int* active, const int* done, cudaStream_t s,
                     int off0, int fo0, int fo1) {
     if (fo1 < 0) fo1 = gf.nn[0];
     int th = 128;
-    static const int rbk = getenv("MG_RESTRICT_RB") ? atoi(getenv("MG_RESTRICT_RB")) : 1;
-    if (gf.dim == 3 && rbk && gc.nnodes >= 148LL * 128 * 4) {   // large 3D level: RHS per thread
-        const unsigned bx = (unsigned)((gc.nnodes + th - 1) / th);
-        if (R > 4) launch_kp(false, restrict3_rb_kernel<8>, dim3(bx, (R + 7) / 8), dim3(th), 0, s, gf, gc, mf, mc, fine, coarse, R, active, done, off0, fo0, fo1);
-        else launch_kp(false, restrict3_rb_kernel<4>, dim3(bx, (R + 3) / 4), dim3(th), 0, s, gf, gc, mf, mc, fine, coarse, R, active, done, off0, fo0, fo1);
-        return;
-    }
     dim3 bl((unsigned)((gc.nnodes + th - 1) / th), R);
     if (gf.dim == 2)
         launch_kp(false, restrict_kernel<2>, dim3(bl), dim3(th), 0, s, gf, gc, mf, mc, fine, coarse, R, active, done, off0, fo0, fo1);
@@ -178,7 +116,6 @@ __global__ void prolong_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* __rest
     // RHS group of this thread: grid.y = R on small levels, all RHS per thread on large ones
     const int rg = (R + gridDim.y - 1) / gridDim.y;
     const int rb = blockIdx.y * rg, re = min(R, rb + rg);
-#pragma unroll 2
     for (int r = rb; r < re; ++r) {
         if (active && !active[r]) continue;
         const double* cv = coarse + (long long)r * gc.ndof;
@@ -189,7 +126,7 @@ __global__ void prolong_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* __rest
         for (int s = 0; s < NC; ++s)
 #pragma unroll
             for (int k = 0; k < DIM; ++k)
-                if (!((cm[s] >> k) & 1)) acc[k] = fma(wgt[s], __ldg(cv + DIM * cn[s] + k), acc[k]);
+                if (!((cm[s] >> k) & 1)) acc[k] = fma(wgt[s], cv[DIM * cn[s] + k], acc[k]);
         double* fv = fine + (long long)r * gf.vstr + DIM * iv;
 #pragma unroll
         for (int k = 0; k < DIM; ++k) {
