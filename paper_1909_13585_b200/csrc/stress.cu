@@ -278,7 +278,6 @@ __host__ __device__ constexpr double s2h(int i, int j, int s, int t) {   // H^_i
 }
 
 static constexpr int G2_PD = 3;    // planes prefetched
-static constexpr int G2_CH = 64;   // planes per chunk
 
 __global__ void __launch_bounds__(128) stress2_kernel(LevelGeom g, const double* __restrict__ sig,
                                                       const uint8_t* __restrict__ mask, const double* __restrict__ phi,
@@ -416,11 +415,24 @@ void stress_apply(const LevelGeom& g, const double* sig, const uint8_t* mask, co
                   cudaStream_t s) {
     if (g.dim == 2 && ((uintptr_t)phi & 15) == 0 && !getenv("MG_STRESS2_LEGACY")) {
         const int nct = (g.nn[1] + 29) / 30;
-        int nch = std::max(1, (g.nn[0] + G2_CH - 1) / G2_CH);
-        // enough warps: at least ~8 per SM
-        while ((long long)nct * nch * nphi < 148LL * 16 && nch < g.nn[0] / 8) nch *= 2;
+        // chunks along axis 0 so the warp count fills whole waves of the resident warps (the
+        // occupancy calculator's CTAs per SM x 4 warps x 148 SMs) with the least tail
+        static int per_sm = [] {
+            int nb = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, stress2_kernel, 128, 0);
+            return std::max(1, nb) * 4;
+        }();
+        const long long slots = 148LL * per_sm;
+        int nch = 1;
+        double best = -1.0;
+        for (int c = 1; c <= std::max(1, g.nn[0] / 16); ++c) {
+            const int h = (g.nn[0] + c - 1) / c;
+            const int cc = (g.nn[0] + h - 1) / h;
+            const double waves = (double)nct * cc * nphi / slots;
+            const double eff = waves / std::ceil(waves) * h / (h + 1.0);
+            if (eff > best + 1e-9) { best = eff; nch = cc; }
+        }
         const int hch = (g.nn[0] + nch - 1) / nch;
-        nch = (g.nn[0] + hch - 1) / hch;
         const long long warps = (long long)nphi * nct * nch;
         stress2_kernel<<<(unsigned)((warps + 3) / 4), 128, 0, s>>>(g, sig, mask, phi, y, nphi, nct, nch, hch);
         return;
