@@ -60,8 +60,11 @@ void dense_pad_identity(double* A, long long n, long long npad, cudaStream_t s) 
 static constexpr int GJ_TQ = 4;
 
 // Rrow[t][j] = sum_s P[t][s] A[k0+s][j]   (new row panel), Ccol[i][t] = A[i][k0+t] (old column panel)
+// sym: only the lower triangle of the state M is kept (M[i][j] = sigma M[j][i], sigma = -1 when
+// exactly one of i, j is a processed pivot index, see dense_spd_inverse): for j >= k0 + NB the row
+// panel is read as M[j][K] (j unprocessed: sigma = +1), for j < k0 the column panel as -M[K][j].
 __global__ void gj_panels_kernel(const double* A, long long ld, long long n, int k0, const double* P, double* Rrow,
-                                 double* Ccol) {
+                                 double* Ccol, int sym) {
     pdl_begin();
     __shared__ double Ps[GJ_NB][GJ_NB];
     const int tid = threadIdx.x;
@@ -71,8 +74,9 @@ __global__ void gj_panels_kernel(const double* A, long long ld, long long n, int
     if (j >= n) return;
     const int tb = blockIdx.y * (GJ_NB / GJ_TQ);   // this CTA's rows t of the panels
     double col[GJ_NB];
+    const bool up = sym && j >= k0 + GJ_NB;   // upper part: read row j of the lower triangle
 #pragma unroll
-    for (int s = 0; s < GJ_NB; ++s) col[s] = A[(k0 + s) * ld + j];
+    for (int s = 0; s < GJ_NB; ++s) col[s] = up ? A[j * ld + k0 + s] : A[(k0 + s) * ld + j];
 #pragma unroll
     for (int tt = 0; tt < GJ_NB / GJ_TQ; ++tt) {
         const int t = tb + tt;
@@ -81,20 +85,22 @@ __global__ void gj_panels_kernel(const double* A, long long ld, long long n, int
         for (int s = 0; s < GJ_NB; ++s) acc = fma(Ps[t][s], col[s], acc);
         Rrow[t * n + j] = acc;
     }
-    // column panel: row j of A's column block (A symmetric in exact arithmetic, but
-    // read the column explicitly to stay exact for the unsymmetric rounding)
+    // column panel: row j of A's column block (full storage: read explicitly to stay exact for the
+    // unsymmetric rounding; sym: M[j][K] = -M[K][j] for processed j < k0, stored for j >= k0)
 #pragma unroll
-    for (int tt = 0; tt < GJ_NB / GJ_TQ; ++tt) Ccol[j * GJ_NB + tb + tt] = A[j * ld + k0 + tb + tt];
+    for (int tt = 0; tt < GJ_NB / GJ_TQ; ++tt)
+        Ccol[j * GJ_NB + tb + tt] = (sym && j < k0) ? -col[tb + tt] : (up ? col[tb + tt] : A[j * ld + k0 + tb + tt]);
 }
 
 // A[i][j] -= sum_t Ccol[i][t] Rrow[t][j] for all i, j (64x64 tile per CTA, 4x4 per thread).
 __global__ void __launch_bounds__(256) gj_update_kernel(double* A, long long ld, long long n, const double* Ccol,
-                                                        const double* Rrow) {
+                                                        const double* Rrow, int sym) {
     pdl_begin();
     __shared__ double Cs[64][GJ_NB + 1];
     __shared__ double Rs[GJ_NB][64 + 1];
     const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
     const long long i0 = (long long)blockIdx.y * 64, j0 = (long long)blockIdx.x * 64;
+    if (sym && j0 > i0) return;   // lower-triangle storage: upper tiles are not kept
     // the A tile is read up front so its latency overlaps the panel loads and the product
     double aold[4][4];
 #pragma unroll
@@ -225,7 +231,7 @@ __global__ void __launch_bounds__(1024) gj_diag_kernel(const double* A, long lon
 
 __global__ void __launch_bounds__(128) gj_update_mma_kernel(double* A, long long ld, long long n, const double* Ccol,
                                                             const double* Rrow, long long kn, double* Pn,
-                                                            int* status) {
+                                                            int* status, int sym) {
     pdl_begin();
     __shared__ __align__(16) double Cs[64 * GU_LDC];
     __shared__ __align__(16) double Rs[GJ_NB * GU_LDR];
@@ -237,6 +243,7 @@ __global__ void __launch_bounds__(128) gj_update_mma_kernel(double* A, long long
     const long long td = kn >= 0 ? (kn / 64) * nt + kn / 64 : -1;
     if (td >= 0) tile = tile == 0 ? td : (tile <= td ? tile - 1 : tile);
     const long long i0 = (tile / nt) * 64, j0 = (tile % nt) * 64;
+    if (sym && j0 > i0) return;   // lower-triangle storage: upper tiles are not kept
     const int gr = lane >> 2, gc = lane & 3;
     // old A values at this thread's accumulator positions (latency overlaps the panel loads)
     double2 aold[4][4];
@@ -316,12 +323,12 @@ __global__ void __launch_bounds__(128) gj_update_mma_kernel(double* A, long long
 // Both fix-ups in one launch (disjoint parts of A): grid.y < GJ_TQ -> pivot columns (rows outside
 // the block, NB / GJ_TQ columns per CTA row), grid.y >= GJ_TQ -> pivot rows.
 __global__ void __launch_bounds__(128) gj_fix_kernel(double* A, long long ld, long long n, int k0, const double* P,
-                                                     const double* Ccol, const double* Rrow) {
+                                                     const double* Ccol, const double* Rrow, int sym) {
     pdl_begin();
     __shared__ double Ps[GJ_NB][GJ_NB];
     if (blockIdx.y >= GJ_TQ) {
         const long long j = (long long)blockIdx.x * 128 + threadIdx.x;
-        if (j >= n) return;
+        if (j >= n || (sym && j >= k0 + GJ_NB)) return;   // sym: pivot rows left of the block only
 #pragma unroll
         for (int tt = 0; tt < GJ_NB / GJ_TQ; ++tt) {
             const int t = (blockIdx.y - GJ_TQ) * (GJ_NB / GJ_TQ) + tt;
@@ -332,7 +339,7 @@ __global__ void __launch_bounds__(128) gj_fix_kernel(double* A, long long ld, lo
     for (int e = threadIdx.x; e < GJ_NB * GJ_NB; e += blockDim.x) Ps[e / GJ_NB][e % GJ_NB] = P[e];
     __syncthreads();
     long long i = (long long)blockIdx.x * 128 + threadIdx.x;
-    if (i >= n || (i >= k0 && i < k0 + GJ_NB)) return;
+    if (i >= n || (i >= k0 && i < k0 + GJ_NB) || (sym && i < k0)) return;   // sym: pivot columns below only
     double c[GJ_NB];
 #pragma unroll
     for (int s = 0; s < GJ_NB; ++s) c[s] = Ccol[i * GJ_NB + s];
@@ -357,10 +364,23 @@ static bool gj_mma() {
 
 static constexpr long long GJ_FOLD_N = 3072;
 
+// MG_GJ_SYM=0: full storage; default: the state is kept in its lower triangle.  Invariant of the
+// in-place Gauss-Jordan sweep on a symmetric matrix (processed pivot set S): M[S,S] and M[U,U]
+// symmetric, M[S,U] = -M[U,S]^T -- so the update needs only the lower tiles (half the traffic;
+// the 4160^2 C5 coarsest matrix then fits in L2), panels and fix-ups read / write the lower
+// counterparts, and a final mirror restores the full symmetric inverse.
+static bool gj_sym() {
+    static bool v = [] {
+        const char* e = getenv("MG_GJ_SYM");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return v;
+}
+
 int dense_spd_inverse_launches(long long npad) {
     const long long steps = npad / GJ_NB;
     const bool fold = gj_mma() && npad >= GJ_FOLD_N;
-    return (int)(fold ? 3 * steps + 1 : 4 * steps);
+    return (int)(fold ? 3 * steps + 1 : 4 * steps) + (gj_sym() ? 1 : 0);
 }
 
 // MG_GJ_PDL=1: the Gauss-Jordan block steps launched with programmatic dependent launch (every
@@ -372,6 +392,24 @@ static bool gj_pdl() {
         return e ? atoi(e) != 0 : false;
     }();
     return v;
+}
+
+// lower triangle -> upper (symmetric Gauss-Jordan: the final state is symmetric)
+__global__ void gj_mirror_kernel(double* A, long long n) {
+    pdl_begin();
+    __shared__ double T[32][33];
+    const long long bi = blockIdx.y, bj = blockIdx.x;   // tile (bi, bj) with bi > bj -> (bj, bi)
+    if (bj >= bi) return;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int r = ty; r < 32; r += blockDim.x >> 5) {
+        const long long i = bi * 32 + r, j = bj * 32 + tx;
+        T[r][tx] = (i < n && j < n) ? A[i * n + j] : 0.0;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += blockDim.x >> 5) {
+        const long long i = bj * 32 + r, j = bi * 32 + tx;
+        if (i < n && j < n) A[i * n + j] = T[tx][r];
+    }
 }
 
 void dense_spd_inverse(double* A, long long npad, double* work, int* d_status, cudaStream_t s) {
@@ -388,14 +426,20 @@ void dense_spd_inverse(double* A, long long npad, double* work, int* d_status, c
         // enough to hide it (large coarsest levels), else by its own kernel
         const bool fold = mma && n >= GJ_FOLD_N;
         const bool pdl = gj_pdl();
+        const int sym = gj_sym() ? 1 : 0;
         if (!fold || k0 == 0) launch_kp(pdl, gj_diag_kernel, dim3(1), dim3(1024), 0, s, A, n, (int)k0, P, d_status);
-        launch_kp(pdl, gj_panels_kernel, dim3(nb, GJ_TQ), dim3(128), 0, s, A, n, n, (int)k0, (const double*)P, Rrow, Ccol);
+        launch_kp(pdl, gj_panels_kernel, dim3(nb, GJ_TQ), dim3(128), 0, s, A, n, n, (int)k0, (const double*)P, Rrow, Ccol,
+                  sym);
         dim3 g((unsigned)((n + 63) / 64), (unsigned)((n + 63) / 64));
         const long long kn = (fold && k0 + GJ_NB < n) ? k0 + GJ_NB : -1;
-        if (mma) launch_kp(pdl, gj_update_mma_kernel, g, dim3(128), 0, s, A, n, n, (const double*)Ccol, (const double*)Rrow, kn, Pn, d_status);
-        else launch_kp(pdl, gj_update_kernel, g, dim3(256), 0, s, A, n, n, (const double*)Ccol, (const double*)Rrow);
+        if (mma) launch_kp(pdl, gj_update_mma_kernel, g, dim3(128), 0, s, A, n, n, (const double*)Ccol, (const double*)Rrow, kn, Pn, d_status, sym);
+        else launch_kp(pdl, gj_update_kernel, g, dim3(256), 0, s, A, n, n, (const double*)Ccol, (const double*)Rrow, sym);
         launch_kp(pdl, gj_fix_kernel, dim3(nb, 2 * GJ_TQ), dim3(128), 0, s, A, n, n, (int)k0, (const double*)P,
-                  (const double*)Ccol, (const double*)Rrow);
+                  (const double*)Ccol, (const double*)Rrow, sym);
+    }
+    if (gj_sym()) {
+        const unsigned nt = (unsigned)((n + 31) / 32);
+        launch_kp(gj_pdl(), gj_mirror_kernel, dim3(nt, nt), dim3(256), 0, s, A, n);
     }
 }
 
