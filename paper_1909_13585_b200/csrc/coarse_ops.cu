@@ -114,18 +114,7 @@ __global__ void __launch_bounds__(NT) galerkin_kernel(LevelGeom gc, LevelGeom gf
     __shared__ double Kc[NL * NL];
     __shared__ double T[NL * NL];
     __shared__ double fr[NL];
-    __shared__ double cf[NL];   // coarse free-DOF factors of the element
     const int t0 = threadIdx.x;
-    constexpr bool FROM_E = SRC == 1;
-    // level 1 from E: this thread's entries of the 2^d constant child matrices, kept in registers
-    // for all the elements of the grid-stride loop
-    double mcr[FROM_E ? NA : 1][EPT];
-    if (FROM_E && Mc) {
-#pragma unroll
-        for (int ch = 0; ch < (FROM_E ? NA : 1); ++ch)
-#pragma unroll
-            for (int u = 0; u < EPT; ++u) mcr[ch][u] = Mc[ch * NL * NL + t0 + u * NT];
-    }
     // grid-stride over coarse elements
     for (long long Ec = blockIdx.x; Ec < gc.nelem; Ec += gridDim.x) {
     int ci[3] = {0, 0, 0};
@@ -137,6 +126,7 @@ __global__ void __launch_bounds__(NT) galerkin_kernel(LevelGeom gc, LevelGeom gf
 #pragma unroll
     for (int u = 0; u < EPT; ++u) acc[u] = 0.0;
     bool fast = false;
+    constexpr bool FROM_E = SRC == 1;
     if (FROM_E && Mc) {
         constexpr int NF = DIM == 2 ? 9 : 27;   // fine nodes of the coarse element
         static_assert(NF <= NT, "one fine node per thread");
@@ -166,9 +156,9 @@ __global__ void __launch_bounds__(NT) galerkin_kernel(LevelGeom gc, LevelGeom gf
             ev[ch] = E[fe];
         }
 #pragma unroll
-        for (int ch = 0; ch < (FROM_E ? NA : 1); ++ch)
+        for (int ch = 0; ch < NA; ++ch)
 #pragma unroll
-            for (int u = 0; u < EPT; ++u) acc[u] = fma(ev[ch], mcr[ch][u], acc[u]);
+            for (int u = 0; u < EPT; ++u) acc[u] = fma(ev[ch], Mc[ch * NL * NL + t0 + u * NT], acc[u]);
     } else
     for (int ch = 0; ch < NA; ++ch) {
         int fi[3];
@@ -228,18 +218,17 @@ __global__ void __launch_bounds__(NT) galerkin_kernel(LevelGeom gc, LevelGeom gf
         }
         __syncthreads();
     }
-    // coarse masks: the NL free-DOF factors of the element once, then per entry from shared memory
-    if (t0 < NL) {
-        const int a = t0 / DIM, comp = t0 % DIM;
+    // coarse masks
+    auto cfree = [&](int ld) {
+        int a = ld / DIM, comp = ld % DIM;
         long long node = 0;
         for (int k = 0; k < DIM; ++k) node = node * gc.nn[k] + ci[k] + ((a >> (DIM - 1 - k)) & 1);
-        cf[t0] = ((mask_c[node] >> comp) & 1) ? 0.0 : 1.0;
-    }
-    __syncthreads();
+        return ((mask_c[node] >> comp) & 1) ? 0.0 : 1.0;
+    };
 #pragma unroll
     for (int u = 0; u < EPT; ++u) {
         const int t = t0 + u * NT, row = t / NL, col = t % NL;
-        elm_c[Ec * NL * NL + t] = acc[u] * cf[row] * cf[col];
+        elm_c[Ec * NL * NL + t] = acc[u] * cfree(row) * cfree(col);
     }
     __syncthreads();   // shared Kc / T / fr are rewritten for the next element
     }
