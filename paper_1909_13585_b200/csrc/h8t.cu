@@ -627,7 +627,7 @@ __global__ void __launch_bounds__(32 * TR, MINB)
     using I2 = std::integral_constant<int, 2>;
     using I3 = std::integral_constant<int, 3>;
     using IR = std::integral_constant<int, -1>;
-    if constexpr (NS == 4) {   // unrolled by the ring depth: every slot offset is a constant
+    if constexpr (NS == 4 && false) {   // unrolled by the ring depth (every slot offset a constant): spills, not used
         for (int L = i0 - 1; L < i1; L += 4) {
             step(I0{}, L, FA, FB, rawA, rawB, mA, mB);
             if (L + 1 < i1) step(I1{}, L + 1, FB, FA, rawB, rawA, mB, mA);
@@ -755,7 +755,7 @@ static int h8t_tr() {
     return tr;
 }
 // ring depth / exchange buffers: MG_H8T_RING = 3 (3 plane slots, double row-exchange buffer,
-// default) or 4 (4 slots, single buffer, march unrolled by 4: more spills, B200 C5 +7%)
+// default) or 4 (4 slots, single buffer)
 static int h8t_ring() {
     static int v = [] {
         const char* e = getenv("MG_H8T_RING");
