@@ -223,7 +223,7 @@ void prolong_add(const LevelGeom& gf, const LevelGeom& gc, const uint8_t* mf, co
         const int th = 128;
         const long long np = (long long)gf.nn[0] * gf.nn[1] * (gf.p2 >> 1);
         const long long blocks = (np + th - 1) / th;
-        dim3 bl((unsigned)blocks, blocks >= 148 * 16 ? 1 : R);
+        dim3 bl((unsigned)blocks, pair == 2 ? 1 : R);   // one RHS per thread (MG_PROLONG_PAIR=2: all)
         launch_kp(false, prolong3_pair_kernel, bl, dim3(th), 0, s, gf, gc, mf, mc, coarse, fine, R, active, done,
                   accumulate, off0);
         return;
