@@ -386,7 +386,7 @@ void stencil_diag(const LevelGeom& g, const double* /*st*/, uint8_t* mask, doubl
 // Thread per node; all R vectors (chunks of RB) accumulated in registers so the
 // stencil (3^d d^2 doubles per node) is read once per chunk.  The 3^d neighbour loop is
 // unrolled (compile-time offsets, no local-memory index arrays).
-template <int DIM, int OP, int RB>
+template <int DIM, int OP, int RB, bool SYMH>
 __global__ void __launch_bounds__(128) coarse_kernel(CoarseArgs a, int r0) {
     pdl_begin();
     constexpr int NS = DIM == 2 ? 9 : 27;
@@ -425,8 +425,19 @@ __global__ void __launch_bounds__(128) coarse_kernel(CoarseArgs a, int r0) {
         if (!ok) continue;
         const long long q = node + ((long long)d0 * n1 + d1) * n2 + d2;
         double blk[DIM * DIM];
+        if (SYMH && s < NS / 2) {
+            // lower half from the transposed upper block stored at the neighbour: A(i, q) = A(q, i)^T
+            // (the coarse operator is symmetric, P' K P); that block was (or will be) read by node q
+            // itself shortly, so the lower half of the stencil never leaves HBM
 #pragma unroll
-        for (int e = 0; e < DIM * DIM; ++e) blk[e] = __ldcs(a.st + (long long)(s * DIM * DIM + e) * nn + node);   // streamed once: keep L1 for x
+            for (int k = 0; k < DIM; ++k)
+#pragma unroll
+                for (int k2 = 0; k2 < DIM; ++k2)
+                    blk[k * DIM + k2] = __ldg(a.st + (long long)((NS - 1 - s) * DIM * DIM + k2 * DIM + k) * nn + q);
+        } else {
+#pragma unroll
+            for (int e = 0; e < DIM * DIM; ++e) blk[e] = __ldcs(a.st + (long long)(s * DIM * DIM + e) * nn + node);   // streamed once: keep L1 for x
+        }
 #pragma unroll
         for (int rr = 0; rr < RB; ++rr) {
             if (!act[rr]) continue;
@@ -518,6 +529,26 @@ __global__ void __launch_bounds__(32 * DIM) coarse_comp_kernel(CoarseArgs a, int
     }
 }
 
+template <int DIM, int OP, bool SYMH>
+static void launch_coarse_large(const CoarseArgs& a, unsigned bl, int th, cudaStream_t s) {
+    for (int r0 = 0; r0 < a.R;) {
+        int rem = a.R - r0;
+        if (rem > 8) {
+            launch_kp(false, coarse_kernel<DIM, OP, 16, SYMH>, dim3(bl), dim3(th), 0, s, a, r0);
+            r0 += 16;
+        } else if (rem > 4) {
+            launch_kp(false, coarse_kernel<DIM, OP, 8, SYMH>, dim3(bl), dim3(th), 0, s, a, r0);
+            r0 += 8;
+        } else if (rem > 1) {
+            launch_kp(false, coarse_kernel<DIM, OP, 4, SYMH>, dim3(bl), dim3(th), 0, s, a, r0);
+            r0 += 4;
+        } else {
+            launch_kp(false, coarse_kernel<DIM, OP, 1, SYMH>, dim3(bl), dim3(th), 0, s, a, r0);
+            r0 += 1;
+        }
+    }
+}
+
 template <int DIM, int OP>
 static void launch_coarse_dim(const CoarseArgs& a, cudaStream_t s) {
     int th = 128;
@@ -525,7 +556,7 @@ static void launch_coarse_dim(const CoarseArgs& a, cudaStream_t s) {
     if (bl < 2 * 148) {   // small level: warp per (32 nodes, component), all RHS per thread
         static const bool comp = !getenv("MG_COARSE_COMP") || atoi(getenv("MG_COARSE_COMP")) != 0;
         if (!comp) {   // former path: one RHS per thread, RHS over grid.y (stencil from L2)
-            launch_kp(false, coarse_kernel<DIM, OP, 1>, dim3(dim3(bl, a.R)), dim3(th), 0, s, a, 0);
+            launch_kp(false, coarse_kernel<DIM, OP, 1, false>, dim3(dim3(bl, a.R)), dim3(th), 0, s, a, 0);
             return;
         }
         const unsigned bc = (unsigned)((a.g.nnodes + 31) / 32);
@@ -536,22 +567,10 @@ static void launch_coarse_dim(const CoarseArgs& a, cudaStream_t s) {
         }
         return;
     }
-    for (int r0 = 0; r0 < a.R;) {
-        int rem = a.R - r0;
-        if (rem > 8) {
-            launch_kp(false, coarse_kernel<DIM, OP, 16>, dim3(bl), dim3(th), 0, s, a, r0);
-            r0 += 16;
-        } else if (rem > 4) {
-            launch_kp(false, coarse_kernel<DIM, OP, 8>, dim3(bl), dim3(th), 0, s, a, r0);
-            r0 += 8;
-        } else if (rem > 1) {
-            launch_kp(false, coarse_kernel<DIM, OP, 4>, dim3(bl), dim3(th), 0, s, a, r0);
-            r0 += 4;
-        } else {
-            launch_kp(false, coarse_kernel<DIM, OP, 1>, dim3(bl), dim3(th), 0, s, a, r0);
-            r0 += 1;
-        }
-    }
+    // large levels read the upper half of the stencil only (MG_COARSE_SYMH=0: the whole stencil)
+    static const bool symh = !getenv("MG_COARSE_SYMH") || atoi(getenv("MG_COARSE_SYMH")) != 0;
+    if (symh) launch_coarse_large<DIM, OP, true>(a, bl, th, s);
+    else launch_coarse_large<DIM, OP, false>(a, bl, th, s);
 }
 
 void coarse_apply(int op, const CoarseArgs& a, cudaStream_t s) {

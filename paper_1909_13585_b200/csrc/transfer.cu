@@ -139,95 +139,9 @@ __global__ void prolong_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* __rest
     }
 }
 
-// 3D fine level in the padded layout (p2 even): a thread takes the fine node pair (2m, 2m + 1) along
-// axis 2 -- both read the coarse columns m and m + 1 only, so the coarse gathers are shared (8 nodes
-// per pair instead of per node) and the pair's 6 doubles move as three 16-byte loads / stores.
-__global__ void __launch_bounds__(128) prolong3_pair_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* __restrict__ mf,
-                                                            const uint8_t* __restrict__ mc,
-                                                            const double* __restrict__ coarse, double* fine, int R,
-                                                            const int* active, const int* done, bool accumulate,
-                                                            int off0) {
-    pdl_begin();
-    const int hp = gf.p2 >> 1;   // pairs per fine row
-    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= (long long)gf.nn[0] * gf.nn[1] * hp) return;
-    if (done && *done) return;
-    const int m = (int)(t % hp);
-    const long long rowi = t / hp;
-    const int f1 = (int)(rowi % gf.nn[1]), f0 = (int)(rowi / gf.nn[1]);
-    const int c = 2 * m;
-    const bool has1 = c + 1 < gf.nn[2];
-    const int g0 = f0 + off0;   // coarse plane I coincident with g0 = 2I
-    // coarse planes / rows touched, weights
-    const int I0 = g0 >> 1, I1 = (g0 + 1) >> 1, J0 = f1 >> 1, J1 = (f1 + 1) >> 1;
-    const double w0 = (g0 & 1) ? 0.5 : 1.0, w1 = (f1 & 1) ? 0.5 : 1.0;
-    const int nI = (g0 & 1) ? 2 : 1, nJ = (f1 & 1) ? 2 : 1;
-    const int cn1 = gc.nn[1], cn2 = gc.nn[2];
-    const long long cidx[4] = {((long long)I0 * cn1 + J0) * cn2 + m, ((long long)I0 * cn1 + J1) * cn2 + m,
-                               ((long long)I1 * cn1 + J0) * cn2 + m, ((long long)I1 * cn1 + J1) * cn2 + m};
-    const long long fnode = rowi * gf.nn[2] + c;   // compact index (masks)
-    const int mf0 = mf[fnode], mf1 = has1 ? mf[fnode + 1] : 7;
-    const bool hasm1 = m + 1 < cn2;
-    int cm0[4], cm1[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const bool used = (q & 1 ? nJ == 2 : true) && (q & 2 ? nI == 2 : true);
-        cm0[q] = used ? mc[cidx[q]] : 7;
-        cm1[q] = (used && hasm1) ? mc[cidx[q] + 1] : 7;
-    }
-    const long long vo = 3 * (rowi * gf.p2 + c);
-    const int rg = (R + gridDim.y - 1) / gridDim.y;
-    const int rb = blockIdx.y * rg, re = min(R, rb + rg);
-    for (int r = rb; r < re; ++r) {
-        if (active && !active[r]) continue;
-        const double* cv = coarse + (long long)r * gc.ndof;
-        double a0[3] = {0.0, 0.0, 0.0}, a1[3] = {0.0, 0.0, 0.0};   // node 2m, node 2m + 1
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const bool used = (q & 1 ? nJ == 2 : true) && (q & 2 ? nI == 2 : true);
-            if (!used) continue;
-            const double w = w0 * w1;
-            const double* p = cv + 3 * cidx[q];
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                const double e0 = ((cm0[q] >> k) & 1) ? 0.0 : __ldg(p + k);
-                const double e1 = ((cm1[q] >> k) & 1) ? 0.0 : __ldg(p + 3 + k);
-                a0[k] = fma(w, e0, a0[k]);
-                a1[k] = fma(0.5 * w, e0 + e1, a1[k]);
-            }
-        }
-        double* fv = fine + (long long)r * gf.vstr + vo;
-        double2* f2 = reinterpret_cast<double2*>(fv);
-        double v[6];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            v[k] = ((mf0 >> k) & 1) ? 0.0 : a0[k];
-            v[3 + k] = ((mf1 >> k) & 1) ? 0.0 : a1[k];
-        }
-        if (accumulate) {
-            const double2 o0 = f2[0], o1 = f2[1], o2 = f2[2];
-            v[0] += o0.x; v[1] += o0.y; v[2] += o1.x; v[3] += o1.y; v[4] += o2.x; v[5] += o2.y;
-        }
-        if (!has1) v[3] = v[4] = v[5] = 0.0;   // padding column stays zero
-        f2[0] = make_double2(v[0], v[1]);
-        f2[1] = make_double2(v[2], v[3]);
-        f2[2] = make_double2(v[4], v[5]);
-    }
-}
-
 void prolong_add(const LevelGeom& gf, const LevelGeom& gc, const uint8_t* mf, const uint8_t* mc,
                  const double* coarse, double* fine, int R, const int* active, const int* done, bool accumulate,
                  cudaStream_t s, int off0) {
-    static const int pair = getenv("MG_PROLONG_PAIR") ? atoi(getenv("MG_PROLONG_PAIR")) : 1;
-    if (pair && gf.dim == 3 && gf.p2 != gf.nn[2] && (gf.p2 & 1) == 0 && ((uintptr_t)fine & 15) == 0) {
-        const int th = 128;
-        const long long np = (long long)gf.nn[0] * gf.nn[1] * (gf.p2 >> 1);
-        const long long blocks = (np + th - 1) / th;
-        dim3 bl((unsigned)blocks, pair == 2 ? 1 : R);   // one RHS per thread (MG_PROLONG_PAIR=2: all)
-        launch_kp(false, prolong3_pair_kernel, bl, dim3(th), 0, s, gf, gc, mf, mc, coarse, fine, R, active, done,
-                  accumulate, off0);
-        return;
-    }
     int th = 128;
     const long long blocks = (gf.nnodes + th - 1) / th;
     // RHS over grid.y (one RHS per thread) unless the level is large; MG_PROLONG_SPLIT=1 always splits
