@@ -529,6 +529,74 @@ __global__ void __launch_bounds__(32 * DIM) coarse_comp_kernel(CoarseArgs a, int
     }
 }
 
+// Small levels (latency-bound): a CTA takes 32 nodes; warp (k, p) = output component k and the
+// neighbour plane d0 = p - 1 (9 offsets), all RB right-hand sides per thread, branch-free loads (an
+// out-of-grid neighbour reads the node itself against the zero stencil block) so a thread's loads are
+// all in flight at once; the three plane partials are summed in shared memory in a fixed order.
+template <int OP, int RB>
+__global__ void __launch_bounds__(288) coarse_split_kernel(CoarseArgs a, int r0) {
+    pdl_begin();
+    __shared__ double part[3][3][RB][32];   // [k][p][rhs][lane]
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, k = w / 3, p = w % 3;
+    const long long node0 = (long long)blockIdx.x * 32 + lane;
+    if (a.done && *a.done) return;
+    const bool valid = node0 < a.g.nnodes;
+    const long long node = valid ? node0 : 0;
+    const int n1 = a.g.nn[1], n2 = a.g.nn[2];
+    const int i2 = (int)(node % n2);
+    const long long t = node / n2;
+    const int i1 = (int)(t % n1), i0 = (int)(t / n1);
+    const int nr = min(RB, a.R - r0);
+    const long long nn = a.g.nnodes;
+    double acc[RB];
+#pragma unroll
+    for (int q = 0; q < RB; ++q) acc[q] = 0.0;
+    const int d0 = p - 1;
+    const bool ok0 = i0 + d0 >= 0 && i0 + d0 < a.g.nn[0];
+#pragma unroll
+    for (int s9 = 0; s9 < 9; ++s9) {
+        const int s = p * 9 + s9;
+        const int d1 = s9 / 3 - 1, d2 = s9 % 3 - 1;
+        const bool ok = ok0 && i1 + d1 >= 0 && i1 + d1 < n1 && i2 + d2 >= 0 && i2 + d2 < n2;
+        const long long q = ok ? node + ((long long)d0 * n1 + d1) * n2 + d2 : node;
+        double blk[3];
+#pragma unroll
+        for (int k2 = 0; k2 < 3; ++k2) blk[k2] = __ldg(a.st + (long long)((s * 3 + k) * 3 + k2) * nn + node);
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr) {
+            if (rr >= nr) continue;   // uniform
+            const double* xv = a.x + (long long)(r0 + rr) * a.g.ndof + 3 * q;
+#pragma unroll
+            for (int k2 = 0; k2 < 3; ++k2) acc[rr] = fma(blk[k2], __ldg(xv + k2), acc[rr]);
+        }
+    }
+#pragma unroll
+    for (int rr = 0; rr < RB; ++rr) part[k][p][rr][lane] = acc[rr];
+    __syncthreads();
+    if (p != 0 || !valid) return;
+#pragma unroll
+    for (int rr = 0; rr < RB; ++rr) {
+        if (rr >= nr || (a.active && !a.active[r0 + rr])) continue;
+        const double v3 = (part[k][0][rr][lane] + part[k][1][rr][lane]) + part[k][2][rr][lane];
+        const long long o = (long long)(r0 + rr) * a.g.ndof + 3 * node + k;
+        double v;
+        if (OP == COP_MATVEC) v = v3;
+        else if (OP == COP_RESID) v = a.b[o] - v3;
+        else v = a.x[o] + a.omega * a.Dinv[3 * node + k] * (a.b[o] - v3);
+        a.y[o] = v;
+    }
+}
+
+template <int OP>
+static void launch_coarse_split(const CoarseArgs& a, cudaStream_t s) {
+    const unsigned bc = (unsigned)((a.g.nnodes + 31) / 32);
+    for (int r0 = 0; r0 < a.R; r0 += 8) {
+        if (a.R - r0 > 4) launch_kp(false, coarse_split_kernel<OP, 8>, dim3(bc), dim3(288), 0, s, a, r0);
+        else if (a.R - r0 > 1) launch_kp(false, coarse_split_kernel<OP, 4>, dim3(bc), dim3(288), 0, s, a, r0);
+        else launch_kp(false, coarse_split_kernel<OP, 1>, dim3(bc), dim3(288), 0, s, a, r0);
+    }
+}
+
 template <int DIM, int OP, bool SYMH>
 static void launch_coarse_large(const CoarseArgs& a, unsigned bl, int th, cudaStream_t s) {
     for (int r0 = 0; r0 < a.R;) {
@@ -553,6 +621,12 @@ template <int DIM, int OP>
 static void launch_coarse_dim(const CoarseArgs& a, cudaStream_t s) {
     int th = 128;
     unsigned bl = (unsigned)((a.g.nnodes + th - 1) / th);
+    // 3D levels below MG_COARSE_SPLIT nodes (default 40000): plane-split kernel
+    static const long long split = getenv("MG_COARSE_SPLIT") ? atoll(getenv("MG_COARSE_SPLIT")) : 40000;
+    if (DIM == 3 && a.g.nnodes < split) {
+        launch_coarse_split<OP>(a, s);
+        return;
+    }
     if (bl < 2 * 148) {   // small level: warp per (32 nodes, component), all RHS per thread
         static const bool comp = !getenv("MG_COARSE_COMP") || atoi(getenv("MG_COARSE_COMP")) != 0;
         if (!comp) {   // former path: one RHS per thread, RHS over grid.y (stencil from L2)
