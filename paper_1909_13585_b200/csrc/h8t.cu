@@ -36,6 +36,10 @@
 #include "element.cuh"
 #include "kernels.h"
 
+#ifndef H8T_RAWRE
+#define H8T_RAWRE 1
+#endif
+
 __constant__ double c_Kt[576];
 __constant__ double c_Glm[2];   // lambda, mu of the centroid stress (E = 1) for G(u) phi
 
@@ -573,27 +577,39 @@ __global__ void __launch_bounds__(32 * TR, MINB)
                 }
                 __syncwarp();
                 if (lane == 0) t_mbar_arrive(&sempty[bi * TR + w - 1]);
+                // H8T_RAWRE: the own row's raw input and mask of plane L re-read from its ring slot
+                // (still resident: released below) instead of carried in registers across the step
+                double rawR[3];
+                int mR;
+                if (H8T_RAWRE) {
+                    double uR[3];
+                    input(sL, L, w, rawR, uR, mR);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) rawR[k] = rawL[k];
+                    mR = mL;
+                }
                 if (OP == FOP_GPHI && own && L < i1) {   // F G F phi: fixed rows zero
                     const long long ob = (long long)r * a.g.vstr + 3 * (((long long)L * n1 + j) * n2 + c);
 #pragma unroll
-                    for (int k = 0; k < 3; ++k) a.y[ob + k] = ((mL >> k) & 1) ? 0.0 : y[k];
+                    for (int k = 0; k < 3; ++k) a.y[ob + k] = ((mR >> k) & 1) ? 0.0 : y[k];
                 } else if (own && L < i1) {
                     const long long ob = vbase + (long long)L * pstr + nodeoff;
                     const bool sdot = L >= a.so0 && L < a.so1;
 #pragma unroll
                     for (int k = 0; k < 3; ++k) {
-                        const double ax = ((mL >> k) & 1) ? rawL[k] : y[k];
+                        const double ax = ((mR >> k) & 1) ? rawR[k] : y[k];
                         double out;
                         if (OP == FOP_MATVEC || OP == FOP_CGP) {
                             out = ax;
-                            if (OP == FOP_CGP && sdot) dot = fma(rawL[k], ax, dot);
+                            if (OP == FOP_CGP && sdot) dot = fma(rawR[k], ax, dot);
                         } else if (OP == FOP_RESID) {
                             out = fB(sL, w)[k] - ax;
                         } else if (OP == FOP_RESTR3) {
                             out = fma(-alpha, fB(sL, w)[k], fA(sL, w)[k]) - ax;
                         } else {   // JACOBI
                             const double bk = fB(sL, w)[k];
-                            out = fma(omega * fC(sL, w)[k], bk - ax, rawL[k]);
+                            out = fma(omega * fC(sL, w)[k], bk - ax, rawR[k]);
                             if (sdot) dot = fma(bk, out, dot);
                         }
                         a.y[ob + k] = out;
