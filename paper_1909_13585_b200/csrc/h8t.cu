@@ -100,9 +100,38 @@ void h8t_set_constants(const double* K0, double nu, cudaStream_t s) {
     cudaMemcpyToSymbolAsync(c_Kt, Kh, sizeof(Kh), 0, cudaMemcpyHostToDevice, s);
 }
 
+// nu = 0.3 (C03): lambda / mu = 3/2 exactly, and with the 1-D factors scaled by 12 (M^ = diag(3, 1),
+// D^ = diag(0, 12), C^ = 6) every entry of K^ is (mu / 27) times a dyadic rational with a small
+// numerator (7 distinct values: 9/16 ... 189/32), so K~ = (27 / mu) K^ enters DFMA as a 32-bit
+// immediate instead of a 64-bit constant materialised in two registers per use; the element
+// modulus carries the factor mu / 27 (one DMUL per element).
+__host__ __device__ constexpr double t1i(int kind, int ta, int tb) {
+    return kind == 0 ? (ta == tb ? (ta == 0 ? 3.0 : 1.0) : 0.0)
+         : kind == 1 ? ((ta == 1 && tb == 1) ? 12.0 : 0.0)
+         : kind == 2 ? ((ta == 1 && tb == 0) ? 6.0 : 0.0)
+                     : ((ta == 0 && tb == 1) ? 6.0 : 0.0);
+}
+__host__ __device__ constexpr double tsh3i(int i, int j, int s, int t) {
+    double v = 1.0;
+    for (int k = 0; k < 3; ++k) {
+        const int ta = (s >> (2 - k)) & 1, tb = (t >> (2 - k)) & 1;
+        const int kind = (k == i && k == j) ? 1 : (k == i ? 2 : (k == j ? 3 : 0));
+        v *= t1i(kind, ta, tb);
+    }
+    return v;
+}
+__host__ __device__ constexpr double tkhat_dy(int row, int col) {   // (27 / mu) K^ at nu = 0.3: exact
+    const int s = row / 3, i = row % 3, t = col / 3, j = col % 3;
+    double v = 1.5 * tsh3i(i, j, s, t) + tsh3i(j, i, s, t);
+    if (i == j)
+        for (int k = 0; k < 3; ++k) v += tsh3i(k, k, s, t);
+    return v / 64.0;   // x 27 / 12^3
+}
+static constexpr double H8T_KSCALE = 1.0 / (2.0 * (1.0 + MG_NU_PAPER)) / 27.0;   // mu / 27 at nu = 0.3
+
 template <bool C03>
 __device__ __forceinline__ double KT(int r, int c) {
-    if (C03) return tkhat(MG_NU_PAPER, r, c);
+    if (C03) return tkhat_dy(r, c);
     return c_Kt[r * 24 + c];
 }
 
@@ -513,7 +542,7 @@ __global__ void __launch_bounds__(32 * TR, MINB)
                 }
             }
         } else {
-            const double Ee = fE(sL);
+            const double Ee = C03 ? fE(sL) * H8T_KSCALE : fE(sL);
 #pragma unroll
             for (int ci = 0; ci < T_NCOMP; ++ci) {
                 double u[3];
