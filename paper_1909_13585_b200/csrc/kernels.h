@@ -181,9 +181,13 @@ void coarse2d_up(const LevelGeom& g, const LevelGeom& gc, const double* st, cons
 void restrict_apply(const LevelGeom& gf, const LevelGeom& gc, const uint8_t* mf, const uint8_t* mc,
                     const double* fine, double* coarse, int R, const int* active, const int* done, cudaStream_t s,
                     int off0 = 0, int fo0 = 0, int fo1 = -1);
+// rb != NULL (padded 3D fine level, prolong_from_r_ok): fine = omega D^-1 rb + P coarse (the
+// pre-smoothed z1 of the fused V-cycle formed from r instead of stored)
 void prolong_add(const LevelGeom& gf, const LevelGeom& gc, const uint8_t* mf, const uint8_t* mc,
                  const double* coarse, double* fine, int R, const int* active, const int* done, bool accumulate,
-                 cudaStream_t s, int off0 = 0);
+                 cudaStream_t s, int off0 = 0, const double* rb = nullptr, const double* dinv = nullptr,
+                 double omega = 0.0);
+bool prolong_from_r_ok(const LevelGeom& gf, const LevelGeom& gc, const double* fine);
 
 // ---------------------------------------------------------------- dense coarsest
 void dense_from_stencil(const LevelGeom& g, const double* st, double* A, long long ld, cudaStream_t s);

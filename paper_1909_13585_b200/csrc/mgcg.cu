@@ -242,6 +242,7 @@ struct Slab {
     double *b = nullptr, *x = nullptr, *r0 = nullptr, *r1 = nullptr, *p0 = nullptr, *p1 = nullptr, *q = nullptr,
            *zf = nullptr, *z = nullptr, *t = nullptr;
     double* zpre = nullptr;
+    bool z1_from_r = false;   // fused 3D V-cycle: zpre is formed by the prolongation from r (not stored)
     double *u = nullptr, *phi = nullptr, *gy = nullptr, *sig = nullptr, *Es = nullptr;   // G(u) phi (slab mode)
     long long gphi_cap = 0;
     // NEXT-1 in slab mode: slab-local compact node vectors / element arrays (incl. ghosts)
@@ -959,6 +960,11 @@ static mg_status blk_cgp(Rec& rc, double* Slab::*pin, double* Slab::*pout, long 
     return MG_OK;
 }
 
+static bool z1_from_r() {
+    static const bool v = !getenv("MG_Z1_FROM_R") || atoi(getenv("MG_Z1_FROM_R")) != 0;
+    return v;
+}
+
 // r_out = r_in - alpha q ; partial r.r ; pre-smooth z1 = omega D^-1 r_out ; r_1 = P^T (r_out - K z1)
 static mg_status blk_restrict(Rec& rc, double* Slab::*rin, double* Slab::*rout, long long* items) {
     mg_ctx* c = rc.c;
@@ -981,7 +987,10 @@ static mg_status blk_restrict(Rec& rc, double* Slab::*rin, double* Slab::*rout, 
             FineArgs a = fine_args(c, s, rc);
             a.rin = s.*rin; a.q = s.q; a.rout = s.*rout; a.alpha = c->ctl.alpha; a.Dinv = s.Dinvpad;
             a.y = s.t; a.partial = c->partial + off;
-            a.z1out = s.z;   // the post-smoother starts from z1 + P e
+            // the post-smoother starts from z1 + P e; with the pair prolongation z1 = omega D^-1 r is
+            // formed there from r (MG_Z1_FROM_R=0: stored here)
+            s.z1_from_r = z1_from_r() && prolong_from_r_ok(s.g0p, s.lv[1].g, s.z);
+            a.z1out = s.z1_from_r ? nullptr : s.z;
             s.zpre = s.z;
             off += fine_apply(FOP_RESTR3, a, c->stream);
             rc.launches++;
@@ -1066,7 +1075,8 @@ static mg_status blk_post(Rec& rc, double* Slab::*r, int cw, long long* items) {
     }
     for (Slab& s : c->sl) {
         prolong_add(c->dim == 3 ? s.g0p : s.lv[0].g, s.lv[1].g, s.lv[0].mask, s.lv[1].mask, cw ? s.lv[1].w : s.lv[1].z, s.zpre, R,
-                    rc.active, rc.done, true, c->stream, s.gl);
+                    rc.active, rc.done, true, c->stream, s.gl, s.z1_from_r ? s.*r : nullptr, s.Dinvpad, c->opts.omega);
+        s.z1_from_r = false;
         rc.launches++;
     }
     if (c->opts.nu_post == 0) {

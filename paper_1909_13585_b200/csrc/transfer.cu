@@ -146,7 +146,8 @@ __global__ void __launch_bounds__(128) restrict3p_kernel(LevelGeom gf, LevelGeom
 __global__ void __launch_bounds__(128) prolong3p_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* __restrict__ mf,
                                                         const uint8_t* __restrict__ mc, const double* __restrict__ coarse,
                                                         double* fine, int R, const int* active, const int* done,
-                                                        bool accumulate, int off0) {
+                                                        bool accumulate, int off0, const double* __restrict__ rb,
+                                                        const double* __restrict__ dinv, double omega) {
     pdl_begin();
     if (done && *done) return;
     const long long I = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -227,7 +228,14 @@ __global__ void __launch_bounds__(128) prolong3p_kernel(LevelGeom gf, LevelGeom 
                 o[k] = tp_mask(fm[q], k, v[0][k]);
                 o[3 + k] = (c + 1 < n2) ? tp_mask(fm[q], 3 + k, v[1][k]) : 0.0;   // padding column stays zero
             }
-            if (accumulate) {
+            if (rb) {   // fine = omega D^-1 r + P e: the pre-smoothed z1 formed here from r (not stored)
+                const double2* rp = reinterpret_cast<const double2*>(rb + (long long)r * gf.vstr + fo[q]);
+                const double2* dp = reinterpret_cast<const double2*>(dinv + fo[q]);
+                const double2 r0 = rp[0], r1 = rp[1], r2 = rp[2], d0 = __ldg(dp), d1 = __ldg(dp + 1), d2 = __ldg(dp + 2);
+                const double rv[6] = {r0.x, r0.y, r1.x, r1.y, r2.x, r2.y}, dv[6] = {d0.x, d0.y, d1.x, d1.y, d2.x, d2.y};
+#pragma unroll
+                for (int u = 0; u < 6; ++u) o[u] += __dmul_rn(__dmul_rn(omega, dv[u]), rv[u]);
+            } else if (accumulate) {
                 const double2 u0 = p[0], u1 = p[1], u2 = p[2];
                 o[0] += u0.x; o[1] += u0.y; o[2] += u1.x; o[3] += u1.y; o[4] += u2.x; o[5] += u2.y;
             }
@@ -322,13 +330,15 @@ __global__ void prolong_kernel(LevelGeom gf, LevelGeom gc, const uint8_t* __rest
     }
 }
 
+bool prolong_from_r_ok(const LevelGeom& gf, const LevelGeom& gc, const double* fine) { return tp_ok(gf, gc, fine); }
+
 void prolong_add(const LevelGeom& gf, const LevelGeom& gc, const uint8_t* mf, const uint8_t* mc,
                  const double* coarse, double* fine, int R, const int* active, const int* done, bool accumulate,
-                 cudaStream_t s, int off0) {
+                 cudaStream_t s, int off0, const double* rb, const double* dinv, double omega) {
     if (tp_ok(gf, gc, fine)) {
         const unsigned nb = (unsigned)((gc.nnodes + 127) / 128);
         launch_kp(false, prolong3p_kernel, dim3(nb, nb >= 148 * 8 ? 1 : R), dim3(128), 0, s, gf, gc, mf, mc, coarse,
-                  fine, R, active, done, accumulate, off0);
+                  fine, R, active, done, accumulate, off0, rb, dinv, omega);
         return;
     }
     int th = 128;
