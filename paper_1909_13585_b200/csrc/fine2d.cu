@@ -34,7 +34,7 @@ __constant__ double c_Kh2[64];
 #define MG_2D_TRANSFORM 1   // element operator in the sum/difference basis (10 nonzeros, see below)
 #endif
 
-// K^ = T^-T K0 T^-1 in the per-axis (m = v0 + v1, d = v1 - v0) basis (see h8.cu): closed form from
+// K^ = T^-T K0 T^-1 in the per-axis (m = v0 + v1, d = v1 - v0) basis (see h8t.cu): closed form from
 // the 1-D factors M^ = diag(1/4, 1/12), D^ = diag(0, 1), C^[d][m] = C^T[m][d] = 1/2; plane stress.
 __host__ __device__ constexpr double f1h2(int kind, int ta, int tb) {
     return kind == 0 ? (ta == tb ? (ta == 0 ? 0.25 : 1.0 / 12.0) : 0.0)

@@ -5,9 +5,9 @@
 #include "common.cuh"
 
 // ---------------------------------------------------------------- fine level (matrix-free)
-// FOP_RESTR3 / FOP_POST3: 3D fused halves of the fine V(1,1) level (h8.cu), see there
+// FOP_RESTR3: 3D fused residual half of the fine V(1,1) level (h8t.cu), see there (5: retired)
 // FOP_GPHI: y = G(u) phi (stress stiffness) on the compact user layout (h8t.cu)
-enum FineOp { FOP_MATVEC = 0, FOP_RESID = 1, FOP_JACOBI = 2, FOP_CGP = 3, FOP_RESTR3 = 4, FOP_POST3 = 5, FOP_GPHI = 6 };
+enum FineOp { FOP_MATVEC = 0, FOP_RESID = 1, FOP_JACOBI = 2, FOP_CGP = 3, FOP_RESTR3 = 4, FOP_GPHI = 6 };
 
 struct FineArgs {
     LevelGeom g;
@@ -37,11 +37,6 @@ struct FineArgs {
     double* rout;
     const double* alpha;
     double* z1out;          // FOP_RESTR3: omega D^-1 r stored here too (pre-smoothed z1) or NULL
-    // FOP_POST3: operator input z2 = omega D^-1 b + P ec, y = z2 + omega D^-1 (b - K z2)
-    const double* ec;
-    LevelGeom gc;
-    const uint8_t* maskc;
-    int off0;
     int ep2;                // 3D: E row pitch (elements along axis 2, even)
     int m2;                 // 3D: mask row pitch (bytes, multiple of 16)
     int goffA, goffB;       // FOP_GPHI: x (phi) / b (u) start this many doubles after a 16-byte boundary
