@@ -799,14 +799,25 @@ static int h8t_tr() {
     }();
     return tr;
 }
-// ring depth / exchange buffers: MG_H8T_RING = 3 (3 plane slots, double row-exchange buffer,
-// default) or 4 (4 slots, single buffer)
+// ring depth / exchange buffers: MG_H8T_RING = 0 (default: per op, the deepest ring of 3..8 plane
+// slots that keeps two 8-warp CTAs per SM, single row-exchange buffer -- B200 C5 A/B: CGP 1.04 -> 0.91
+// ms with 4 slots instead of 3), 3 (3 slots, double exchange buffer) or 4 (4 slots, single buffer)
 static int h8t_ring() {
     static int v = [] {
         const char* e = getenv("MG_H8T_RING");
-        return (e && atoi(e) == 4) ? 4 : 3;
+        const int r = e ? atoi(e) : 0;
+        return (r == 3 || r == 4) ? r : 0;
     }();
     return v;
+}
+template <int OP, int TR, int NB, int MINB>
+constexpr int h8t_auto_ns() {
+    constexpr size_t budget = (size_t)(MINB == 2 ? 112 : 224) * 1024;
+    int ns = 3;
+    if (h8t_smem_bytes<OP, TR, 4, NB>() <= budget) ns = 4;
+    if (h8t_smem_bytes<OP, TR, 5, NB>() <= budget) ns = 5;
+    if (h8t_smem_bytes<OP, TR, 6, NB>() <= budget) ns = 6;
+    return ns;
 }
 
 // chunking along axis 0: between 16 and 64 planes per chunk, picked so that the CTA count fills
@@ -842,8 +853,11 @@ int h8t_items(const LevelGeom& g, int R) {
 
 template <int OP>
 static bool launch_h8t_op(const FineArgs& a, cudaStream_t s) {
-    if (h8t_tr() == 8)
-        return h8t_ring() == 3 ? launch_h8t_t<OP, 8, 3, 2, 2>(a, s) : launch_h8t_t<OP, 8, 4, 1, 2>(a, s);
+    if (h8t_tr() == 8) {
+        if (h8t_ring() == 3) return launch_h8t_t<OP, 8, 3, 2, 2>(a, s);
+        if (h8t_ring() == 4) return launch_h8t_t<OP, 8, 4, 1, 2>(a, s);
+        return launch_h8t_t<OP, 8, h8t_auto_ns<OP, 8, 1, 2>(), 1, 2>(a, s);
+    }
     return h8t_ring() == 3 ? launch_h8t_t<OP, 16, 3, 2, 1>(a, s) : launch_h8t_t<OP, 16, 4, 1, 1>(a, s);
 }
 
