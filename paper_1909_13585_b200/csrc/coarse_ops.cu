@@ -341,12 +341,72 @@ __global__ void stencil_kernel(LevelGeom g, const double* __restrict__ elm, cons
         }
 }
 
+// 3D: a CTA per 16 consecutive nodes, thread (node, s) with s fastest, so the threads reading one
+// element matrix (its node-a rows, one 3-column block per neighbour s) touch contiguous 192-byte row
+// segments and every element entry leaves HBM once; the 243 x 32 results go through shared memory
+// so the stencil arrays are written as coalesced 128-byte rows.  Same sums in the same order as
+// stencil_kernel (bitwise equal).
+__global__ void __launch_bounds__(432) stencil3_tile_kernel(LevelGeom g, const double* __restrict__ elm,
+                                                            const uint8_t* __restrict__ mask, double* __restrict__ st,
+                                                            int ident) {
+    constexpr int NA = 8, NL = 24, NS = 27;
+    __shared__ double tile[NS * 9][17];
+    const int nl = threadIdx.x / NS, s = threadIdx.x % NS;
+    const long long node = (long long)blockIdx.x * 16 + nl;
+    double acc[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) acc[q] = 0.0;
+    if (node < g.nnodes) {
+        const int i2 = (int)(node % g.nn[2]);
+        const long long t = node / g.nn[2];
+        const int idx[3] = {(int)(t / g.nn[1]), (int)(t % g.nn[1]), i2};
+        const int dlt[3] = {s / 9 - 1, (s / 3) % 3 - 1, s % 3 - 1};
+        for (int a = 0; a < NA; ++a) {
+            int b = 0;
+            bool ok = true;
+            long long el = 0;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const int ab = (a >> (2 - k)) & 1;
+                const int bb = ab + dlt[k];
+                if (bb < 0 || bb > 1) ok = false;
+                b = b * 2 + (bb & 1);
+                const int ek = idx[k] - ab;
+                if (ek < 0 || ek >= g.N[k]) ok = false;
+                el = el * g.N[k] + ek;
+            }
+            if (!ok) continue;
+            const double* m = elm + el * NL * NL;
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+#pragma unroll
+                for (int k2 = 0; k2 < 3; ++k2) acc[k * 3 + k2] += m[(a * 3 + k) * NL + b * 3 + k2];
+        }
+        const int mb = mask[node];
+        if (ident && s == NS / 2)
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                if ((mb >> k) & 1) acc[k * 3 + k] = 1.0;
+    }
+#pragma unroll
+    for (int e = 0; e < 9; ++e) tile[s * 9 + e][nl] = acc[e];
+    __syncthreads();
+    const long long n0 = (long long)blockIdx.x * 16;
+    for (int q = threadIdx.x; q < NS * 9 * 16; q += blockDim.x) {
+        const int arr = q >> 4, j = q & 15;
+        if (n0 + j < g.nnodes) st[(long long)arr * g.nnodes + n0 + j] = tile[arr][j];
+    }
+}
+
 void stencil_from_elements(const LevelGeom& g, const double* elm, uint8_t* mask, double* st, cudaStream_t s,
                            bool identity_fixed) {
     int th = 128;
     dim3 grid((unsigned)((g.nnodes + th - 1) / th), g.dim == 2 ? 9 : 27);
+    static const bool tiled = !getenv("MG_STENCIL_TILE") || atoi(getenv("MG_STENCIL_TILE")) != 0;
     if (g.dim == 2)
         stencil_kernel<2><<<grid, th, 0, s>>>(g, elm, mask, st, identity_fixed ? 1 : 0);
+    else if (tiled)
+        stencil3_tile_kernel<<<(unsigned)((g.nnodes + 15) / 16), 432, 0, s>>>(g, elm, mask, st, identity_fixed ? 1 : 0);
     else
         stencil_kernel<3><<<grid, th, 0, s>>>(g, elm, mask, st, identity_fixed ? 1 : 0);
 }

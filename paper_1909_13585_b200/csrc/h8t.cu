@@ -854,7 +854,8 @@ int h8t_items(const LevelGeom& g, int R) {
 template <int OP>
 static bool launch_h8t_op(const FineArgs& a, cudaStream_t s) {
     if (h8t_tr() == 8) {
-        if (h8t_ring() == 3) return launch_h8t_t<OP, 8, 3, 2, 2>(a, s);
+        // G(u) phi keeps 3 slots + double exchange buffer: its deeper-ring builds spill (C5 1.69 -> 2.03 ms)
+        if (h8t_ring() == 3 || OP == FOP_GPHI) return launch_h8t_t<OP, 8, 3, 2, 2>(a, s);
         if (h8t_ring() == 4) return launch_h8t_t<OP, 8, 4, 1, 2>(a, s);
         return launch_h8t_t<OP, 8, h8t_auto_ns<OP, 8, 1, 2>(), 1, 2>(a, s);
     }
