@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(NT) galerkin_kernel(LevelGeom gc, LevelGeom gf
     __shared__ double Kc[NL * NL];
     __shared__ double T[NL * NL];
     __shared__ double fr[NL];
+    __shared__ double frc[NL];   // coarse free-DOF factors of the current element
     const int t0 = threadIdx.x;
     // grid-stride over coarse elements
     for (long long Ec = blockIdx.x; Ec < gc.nelem; Ec += gridDim.x) {
@@ -125,6 +126,12 @@ __global__ void __launch_bounds__(NT) galerkin_kernel(LevelGeom gc, LevelGeom gf
     double acc[EPT];
 #pragma unroll
     for (int u = 0; u < EPT; ++u) acc[u] = 0.0;
+    if (t0 < NL) {   // read after the barriers below
+        const int a = t0 / DIM, comp = t0 % DIM;
+        long long node = 0;
+        for (int k = 0; k < DIM; ++k) node = node * gc.nn[k] + ci[k] + ((a >> (DIM - 1 - k)) & 1);
+        frc[t0] = ((mask_c[node] >> comp) & 1) ? 0.0 : 1.0;
+    }
     bool fast = false;
     constexpr bool FROM_E = SRC == 1;
     if (FROM_E && Mc) {
@@ -219,16 +226,11 @@ __global__ void __launch_bounds__(NT) galerkin_kernel(LevelGeom gc, LevelGeom gf
         __syncthreads();
     }
     // coarse masks
-    auto cfree = [&](int ld) {
-        int a = ld / DIM, comp = ld % DIM;
-        long long node = 0;
-        for (int k = 0; k < DIM; ++k) node = node * gc.nn[k] + ci[k] + ((a >> (DIM - 1 - k)) & 1);
-        return ((mask_c[node] >> comp) & 1) ? 0.0 : 1.0;
-    };
+    if (!FROM_E || !Mc || !fast) __syncthreads();   // fast path: frc visible through __syncthreads_or
 #pragma unroll
     for (int u = 0; u < EPT; ++u) {
         const int t = t0 + u * NT, row = t / NL, col = t % NL;
-        elm_c[Ec * NL * NL + t] = acc[u] * cfree(row) * cfree(col);
+        elm_c[Ec * NL * NL + t] = acc[u] * frc[row] * frc[col];
     }
     __syncthreads();   // shared Kc / T / fr are rewritten for the next element
     }
