@@ -595,11 +595,13 @@ __global__ void __launch_bounds__(32 * DIM) coarse_comp_kernel(CoarseArgs a, int
 // neighbour plane d0 = p - 1 (9 offsets), all RB right-hand sides per thread, branch-free loads (an
 // out-of-grid neighbour reads the node itself against the zero stencil block) so a thread's loads are
 // all in flight at once; the three plane partials are summed in shared memory in a fixed order.
-template <int OP, int RB>
-__global__ void __launch_bounds__(288) coarse_split_kernel(CoarseArgs a, int r0) {
+template <int OP, int RB, int SP>
+__global__ void __launch_bounds__(96 * SP) coarse_split_kernel(CoarseArgs a, int r0) {
     pdl_begin();
-    __shared__ double part[3][3][RB][32];   // [k][p][rhs][lane]
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, k = w / 3, p = w % 3;
+    // SP = 3: warp (k, p) with p = the neighbour plane d0 (9 offsets each); SP = 9: p = (d0, d1)
+    // (3 offsets each) -- more loads in flight for the smallest levels
+    extern __shared__ double part[];   // [3 k][SP p][RB][32 lanes]
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, k = w / SP, p = w % SP;
     const long long node0 = (long long)blockIdx.x * 32 + lane;
     if (a.done && *a.done) return;
     const bool valid = node0 < a.g.nnodes;
@@ -613,13 +615,12 @@ __global__ void __launch_bounds__(288) coarse_split_kernel(CoarseArgs a, int r0)
     double acc[RB];
 #pragma unroll
     for (int q = 0; q < RB; ++q) acc[q] = 0.0;
-    const int d0 = p - 1;
-    const bool ok0 = i0 + d0 >= 0 && i0 + d0 < a.g.nn[0];
+    constexpr int NO = 27 / SP;   // offsets per thread
 #pragma unroll
-    for (int s9 = 0; s9 < 9; ++s9) {
-        const int s = p * 9 + s9;
-        const int d1 = s9 / 3 - 1, d2 = s9 % 3 - 1;
-        const bool ok = ok0 && i1 + d1 >= 0 && i1 + d1 < n1 && i2 + d2 >= 0 && i2 + d2 < n2;
+    for (int so = 0; so < NO; ++so) {
+        const int s = p * NO + so;
+        const int d0 = s / 9 - 1, d1 = (s / 3) % 3 - 1, d2 = s % 3 - 1;
+        const bool ok = i0 + d0 >= 0 && i0 + d0 < a.g.nn[0] && i1 + d1 >= 0 && i1 + d1 < n1 && i2 + d2 >= 0 && i2 + d2 < n2;
         const long long q = ok ? node + ((long long)d0 * n1 + d1) * n2 + d2 : node;
         double blk[3];
 #pragma unroll
@@ -633,13 +634,15 @@ __global__ void __launch_bounds__(288) coarse_split_kernel(CoarseArgs a, int r0)
         }
     }
 #pragma unroll
-    for (int rr = 0; rr < RB; ++rr) part[k][p][rr][lane] = acc[rr];
+    for (int rr = 0; rr < RB; ++rr) part[((k * SP + p) * RB + rr) * 32 + lane] = acc[rr];
     __syncthreads();
     if (p != 0 || !valid) return;
 #pragma unroll
     for (int rr = 0; rr < RB; ++rr) {
         if (rr >= nr || (a.active && !a.active[r0 + rr])) continue;
-        const double v3 = (part[k][0][rr][lane] + part[k][1][rr][lane]) + part[k][2][rr][lane];
+        double v3 = part[((k * SP + 0) * RB + rr) * 32 + lane];
+#pragma unroll
+        for (int pp = 1; pp < SP; ++pp) v3 += part[((k * SP + pp) * RB + rr) * 32 + lane];
         const long long o = (long long)(r0 + rr) * a.g.ndof + 3 * node + k;
         double v;
         if (OP == COP_MATVEC) v = v3;
@@ -649,14 +652,31 @@ __global__ void __launch_bounds__(288) coarse_split_kernel(CoarseArgs a, int r0)
     }
 }
 
-template <int OP>
-static void launch_coarse_split(const CoarseArgs& a, cudaStream_t s) {
+template <int OP, int SP>
+static void launch_coarse_split_sp(const CoarseArgs& a, cudaStream_t s) {
     const unsigned bc = (unsigned)((a.g.nnodes + 31) / 32);
     for (int r0 = 0; r0 < a.R; r0 += 8) {
-        if (a.R - r0 > 4) launch_kp(false, coarse_split_kernel<OP, 8>, dim3(bc), dim3(288), 0, s, a, r0);
-        else if (a.R - r0 > 1) launch_kp(false, coarse_split_kernel<OP, 4>, dim3(bc), dim3(288), 0, s, a, r0);
-        else launch_kp(false, coarse_split_kernel<OP, 1>, dim3(bc), dim3(288), 0, s, a, r0);
+        const int rb = a.R - r0 > 4 ? 8 : (a.R - r0 > 1 ? 4 : 1);
+        const size_t sm = sizeof(double) * 3 * SP * rb * 32;
+        if (rb == 8) {
+            static bool at = (cudaFuncSetAttribute(coarse_split_kernel<OP, 8, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), true);
+            (void)at;
+            launch_kp(false, coarse_split_kernel<OP, 8, SP>, dim3(bc), dim3(96 * SP), sm, s, a, r0);
+        } else if (rb == 4) {
+            launch_kp(false, coarse_split_kernel<OP, 4, SP>, dim3(bc), dim3(96 * SP), sm, s, a, r0);
+        } else {
+            launch_kp(false, coarse_split_kernel<OP, 1, SP>, dim3(bc), dim3(96 * SP), sm, s, a, r0);
+        }
     }
+}
+
+// MG_COARSE_SPLIT9: levels below this many nodes (default 40000, i.e. every split level) split the
+// offsets 9 ways (B200 C4: 17.15 ms/step with 3 ways, 16.35 with 9)
+template <int OP>
+static void launch_coarse_split(const CoarseArgs& a, cudaStream_t s) {
+    static const long long s9 = getenv("MG_COARSE_SPLIT9") ? atoll(getenv("MG_COARSE_SPLIT9")) : 40000;
+    if (a.g.nnodes < s9) launch_coarse_split_sp<OP, 9>(a, s);
+    else launch_coarse_split_sp<OP, 3>(a, s);
 }
 
 template <int DIM, int OP, bool SYMH>
