@@ -40,7 +40,7 @@ def handle(name, nslab):
 
 
 # (config, slabs): uneven splits, 2D and 3D, slabs down to one coarsest layer
-SLAB_CASES = [("T2b", 2), ("T2b", 3), ("T2c", 4), ("C2", 4), ("T3a", 2), ("T3b", 3), ("T3c", 4), ("T3d", 5)]
+SLAB_CASES = [("T2b", 2), ("T2b", 3), ("T2c", 4), ("C2", 4), ("T3a", 2), ("T3b", 3), ("T3c", 4), ("T3d", 5), ("T3f", 2)]
 
 
 @pytest.mark.parametrize("name,nslab", SLAB_CASES)

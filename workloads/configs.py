@@ -61,6 +61,10 @@ CONFIGS = {
     "T3d": Config("T3d", (48, 24, 24), 7, 4, load="edge", nphi=2, seed=3004),
     # coarsest level of C5's size (n_L = 4131 -> padded 4160): the large-level Gauss-Jordan path
     "T3e": Config("T3e", (32, 16, 16), 2, 2, seed=3005),
+    # axis 2 wider than one 32-element column tile: the column-cluster fine kernels (h8t.cu CX) with
+    # a full last tile (N2 = 64, the grid's last node column right of it) and a ragged one (N2 = 70)
+    "T3f": Config("T3f", (8, 12, 64), 3, 3, nphi=2, seed=3006),
+    "T3g": Config("T3g", (8, 10, 70), 2, 2, nphi=2, seed=3007),
 }
 
 
