@@ -287,6 +287,7 @@ __global__ void __launch_bounds__(32 * TR, MINB)
     const double xal = (OP == FOP_CGP && hasC) ? a.xalpha[r] : 0.0;
     const double alpha = OP == FOP_RESTR3 ? a.alpha[r] : 0.0;
     const double omega = a.omega;
+    const bool z1r = OP == FOP_JACOBI && a.z1r;   // z2 = P e + omega D^-1 r formed here (blk_post)
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) {
@@ -373,6 +374,7 @@ __global__ void __launch_bounds__(32 * TR, MINB)
             double v;
             if (OP == FOP_CGP) v = fma(beta, A[k], fB(s, row)[k]);
             else if (OP == FOP_RESTR3) v = omega * fC(s, row)[k] * fma(-alpha, fB(s, row)[k], A[k]);
+            else if (OP == FOP_JACOBI && z1r) v = A[k] + __dmul_rn(__dmul_rn(omega, fC(s, row)[k]), fB(s, row)[k]);
             else v = A[k];
             raw[k] = v;
             u[k] = ((m >> k) & 1) ? 0.0 : v;

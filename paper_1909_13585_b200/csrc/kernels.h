@@ -41,6 +41,8 @@ struct FineArgs {
     int m2;                 // 3D: mask row pitch (bytes, multiple of 16)
     int goffA, goffB;       // FOP_GPHI: x (phi) / b (u) start this many doubles after a 16-byte boundary
     const double* sig;      // FOP_GPHI: element centroid stresses (nelem x 6, stress_sigma) or NULL (formed from u)
+    int z1r;                // FOP_JACOBI: x holds the coarse correction P e only; the sweep's input is
+                            // z2 = x + (omega D^-1) b, rounded as the prolongation formed it (MG_Z2_IN_POST)
 };
 
 void fine_set_constants(int dim, const double* K0, cudaStream_t s);

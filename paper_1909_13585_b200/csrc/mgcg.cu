@@ -960,6 +960,11 @@ static mg_status blk_cgp(Rec& rc, double* Slab::*pin, double* Slab::*pout, long 
     return MG_OK;
 }
 
+static bool z2_in_post() {
+    static const bool v = !getenv("MG_Z2_IN_POST") || atoi(getenv("MG_Z2_IN_POST")) != 0;
+    return v;
+}
+
 static bool z1_from_r() {
     static const bool v = !getenv("MG_Z1_FROM_R") || atoi(getenv("MG_Z1_FROM_R")) != 0;
     return v;
@@ -1073,9 +1078,16 @@ static mg_status blk_post(Rec& rc, double* Slab::*r, int cw, long long* items) {
         *items = off;
         return xchg(c, [&](const Slab& s) { return fine_field(c, s, s.zf, R); });
     }
+    // MG_Z2_IN_POST (default on): with z1 = omega D^-1 r not stored, the prolongation writes only the
+    // correction P e and the first post-smoothing sweep forms z2 = P e + omega D^-1 r from the r and
+    // D^-1 it reads anyway (the prolongation no longer reads them: one fine R-vector + D^-1 less)
+    bool z2post = false;
     for (Slab& s : c->sl) {
+        const bool zp = c->dim == 3 && s.z1_from_r && c->opts.nu_post > 0 && z2_in_post();
+        z2post = zp;   // same decision on every slab (same level-0 layout rules)
         prolong_add(c->dim == 3 ? s.g0p : s.lv[0].g, s.lv[1].g, s.lv[0].mask, s.lv[1].mask, cw ? s.lv[1].w : s.lv[1].z, s.zpre, R,
-                    rc.active, rc.done, true, c->stream, s.gl, s.z1_from_r ? s.*r : nullptr, s.Dinvpad, c->opts.omega);
+                    rc.active, rc.done, !zp, c->stream, s.gl, (s.z1_from_r && !zp) ? s.*r : nullptr, s.Dinvpad,
+                    c->opts.omega);
         s.z1_from_r = false;
         rc.launches++;
     }
@@ -1106,6 +1118,7 @@ static mg_status blk_post(Rec& rc, double* Slab::*r, int cw, long long* items) {
             double* dst = last ? s.zf : (src[k] == s.z ? s.t : s.z);
             FineArgs a = fine_args(c, s, rc);
             a.x = src[k]; a.b = s.*r; a.Dinv = s.Dinvpad; a.y = dst; a.partial = last ? c->partial + off : nullptr;
+            a.z1r = (it == 0 && z2post) ? 1 : 0;
             off += level0_apply(c, s, FOP_JACOBI, a);
             rc.launches++;
             src[k] = dst;

@@ -60,3 +60,14 @@ def test_gauss_jordan_pdl_bitwise():
     on, off = _run(names, MG_GJ_PDL="1"), _run(names, MG_GJ_PDL="0")
     for n in names:
         assert on[n] == off[n], n
+
+
+@pytest.mark.gpu
+def test_z2_in_post_bitwise():
+    """3D fused V-cycle: the prolongation writing only P e with the first post-smoothing sweep forming
+    z2 = P e + omega D^-1 r (MG_Z2_IN_POST=1, default) gives bit for bit the solves of the
+    prolongation forming z2 itself (=0): the same products, rounded the same way."""
+    names = ["T3a", "T3c", "T3f", "C4"]
+    on, off = _run(names, MG_Z2_IN_POST="1"), _run(names, MG_Z2_IN_POST="0")
+    for n in names:
+        assert on[n] == off[n], n
