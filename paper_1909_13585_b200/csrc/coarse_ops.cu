@@ -107,7 +107,8 @@ __global__ void __launch_bounds__(NT) galerkin_kernel(LevelGeom gc, LevelGeom gf
                                                       const double* __restrict__ elm_f,
                                                       const uint8_t* __restrict__ mask_f,
                                                       const uint8_t* __restrict__ mask_c, double* __restrict__ elm_c,
-                                                      int off0, const double* __restrict__ Mc) {
+                                                      int off0, const double* __restrict__ Mc,
+                                                      const int* __restrict__ list) {
     constexpr int NA = 1 << DIM, NL = DIM * NA;
     constexpr int EPT = NL * NL / NT;
     static_assert(EPT * NT == NL * NL, "NT divides NL^2");
@@ -115,9 +116,16 @@ __global__ void __launch_bounds__(NT) galerkin_kernel(LevelGeom gc, LevelGeom gf
     __shared__ double T[NL * NL];
     __shared__ double fr[NL];
     __shared__ double frc[NL];   // coarse free-DOF factors of the current element
+    // the prolongation stencils in shared memory: the lanes of a warp index different columns b2, which
+    // the constant cache would serve one address at a time
+    __shared__ double Qs[NA * NA * NA];
     const int t0 = threadIdx.x;
-    // grid-stride over coarse elements
-    for (long long Ec = blockIdx.x; Ec < gc.nelem; Ec += gridDim.x) {
+    for (int e = t0; e < NA * NA * NA; e += NT) Qs[e] = c_Q[e];
+    __syncthreads();
+    // grid-stride over coarse elements (list: count, then the element indices)
+    const long long ne = list ? (long long)list[0] : gc.nelem;
+    for (long long ie = blockIdx.x; ie < ne; ie += gridDim.x) {
+    const long long Ec = list ? (long long)list[1 + ie] : ie;
     int ci[3] = {0, 0, 0};
     long long tt = Ec;
     for (int k = DIM - 1; k >= 0; --k) { ci[k] = (int)(tt % gc.N[k]); tt /= gc.N[k]; }
@@ -212,7 +220,7 @@ __global__ void __launch_bounds__(NT) galerkin_kernel(LevelGeom gc, LevelGeom gf
             const int b2 = col / DIM, k2 = col % DIM;
             double sacc = 0.0;
 #pragma unroll
-            for (int a2 = 0; a2 < NA; ++a2) sacc = fma(Kc[row * NL + a2 * DIM + k2], c_Q[(ch * NA + a2) * NA + b2], sacc);
+            for (int a2 = 0; a2 < NA; ++a2) sacc = fma(Kc[row * NL + a2 * DIM + k2], Qs[(ch * NA + a2) * NA + b2], sacc);
             T[t] = sacc;
         }
         __syncthreads();
@@ -221,7 +229,7 @@ __global__ void __launch_bounds__(NT) galerkin_kernel(LevelGeom gc, LevelGeom gf
             const int t = t0 + u * NT, row = t / NL, col = t % NL;
             const int b = row / DIM, k = row % DIM;
 #pragma unroll
-            for (int a = 0; a < NA; ++a) acc[u] = fma(c_Q[(ch * NA + a) * NA + b], T[(a * DIM + k) * NL + col], acc[u]);
+            for (int a = 0; a < NA; ++a) acc[u] = fma(Qs[(ch * NA + a) * NA + b], T[(a * DIM + k) * NL + col], acc[u]);
         }
         __syncthreads();
     }
@@ -233,6 +241,66 @@ __global__ void __launch_bounds__(NT) galerkin_kernel(LevelGeom gc, LevelGeom gf
         elm_c[Ec * NL * NL + t] = acc[u] * frc[row] * frc[col];
     }
     __syncthreads();   // shared Kc / T / fr are rewritten for the next element
+    }
+}
+
+// 3D level 1 from E: a warp per coarse element.  Elements whose 27 fine nodes are all free have
+// K_E = sum_c E_c M_c (M_c = Q_c' K0 Q_c, staged in shared memory), formed entry by entry in the
+// children order of galerkin_kernel's fast path (bitwise the same matrices) and scaled by the coarse
+// free-DOF factors; the others are appended to `list` (list[0] = count) for galerkin_kernel.  No
+// CTA barrier per element: 8 warps per CTA keep 8 elements in flight each.
+static constexpr int GALW_WARPS = 8;
+__global__ void __launch_bounds__(32 * GALW_WARPS) galerkin_warp3_kernel(LevelGeom gc, LevelGeom gf,
+                                                                         const double* __restrict__ E,
+                                                                         const uint8_t* __restrict__ mask_f,
+                                                                         const uint8_t* __restrict__ mask_c,
+                                                                         double* __restrict__ elm_c, int off0,
+                                                                         const double* __restrict__ Mc, int* list) {
+    constexpr int NL = 24, NE = NL * NL;
+    extern __shared__ double Ms[];   // [8][576]
+    for (int e = threadIdx.x; e < 8 * NE; e += blockDim.x) Ms[e] = Mc[e];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (long long Ec = (long long)blockIdx.x * GALW_WARPS + warp; Ec < gc.nelem; Ec += (long long)gridDim.x * GALW_WARPS) {
+        int ci[3];
+        long long tt = Ec;
+        for (int k = 2; k >= 0; --k) { ci[k] = (int)(tt % gc.N[k]); tt /= gc.N[k]; }
+        if (ci[0] < off0) continue;   // slab ghost element layer: filled by the halo exchange
+        int fixed_here = 0;
+        if (lane < 27) {
+            int q = lane, fc[3];
+            for (int k = 2; k >= 0; --k) { fc[k] = 2 * ci[k] + q % 3 - (k == 0 ? off0 : 0); q /= 3; }
+            const bool inside = fc[0] >= 0 && fc[0] < gf.nn[0] && fc[1] < gf.nn[1] && fc[2] < gf.nn[2];
+            fixed_here = inside ? mask_f[((long long)fc[0] * gf.nn[1] + fc[1]) * gf.nn[2] + fc[2]] != 0 : 1;
+        }
+        if (__any_sync(0xffffffffu, fixed_here)) {
+            if (lane == 0) list[1 + atomicAdd(list, 1)] = (int)Ec;
+            continue;
+        }
+        double fr = 0.0, ev = 0.0;
+        if (lane < NL) {   // coarse free-DOF factor of local DOF lane
+            const int a = lane / 3, comp = lane % 3;
+            const long long node = ((long long)(ci[0] + (a >> 2)) * gc.nn[1] + ci[1] + ((a >> 1) & 1)) * gc.nn[2] + ci[2] + (a & 1);
+            fr = ((mask_c[node] >> comp) & 1) ? 0.0 : 1.0;
+        }
+        if (lane < 8) {    // child lane's modulus
+            const long long fe = ((long long)(2 * ci[0] + (lane >> 2) - off0) * gf.N[1] + 2 * ci[1] + ((lane >> 1) & 1)) * gf.N[2] +
+                                 2 * ci[2] + (lane & 1);
+            ev = E[fe];
+        }
+        double evc[8];
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) evc[ch] = __shfl_sync(0xffffffffu, ev, ch);
+        double* out = elm_c + Ec * NE;
+#pragma unroll 2
+        for (int u = 0; u < NE / 32; ++u) {
+            const int t = lane + 32 * u, row = t / NL, col = t % NL;
+            double acc = 0.0;
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) acc = fma(evc[ch], Ms[ch * NE + t], acc);
+            const double frow = __shfl_sync(0xffffffffu, fr, row), fcol = __shfl_sync(0xffffffffu, fr, col);
+            out[t] = acc * frow * fcol;
+        }
     }
 }
 
@@ -248,14 +316,25 @@ static unsigned galerkin_grid(const LevelGeom& gc) {
 
 void galerkin_elements(const LevelGeom& gc, const LevelGeom& gf, const double* E, const double* elm_f,
                        const uint8_t* mask_f, const uint8_t* mask_c, double* elm_c, cudaStream_t s, int off0,
-                       const double* Mc) {
+                       const double* Mc, int* slow_ws) {
     unsigned bl = galerkin_grid(gc);
+    if (gc.dim == 3 && E && Mc && slow_ws) {
+        const size_t sm = sizeof(double) * 8 * 576;
+        static bool at = (cudaFuncSetAttribute(galerkin_warp3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), true);
+        (void)at;
+        cudaMemsetAsync(slow_ws, 0, sizeof(int), s);
+        const long long nb = (gc.nelem + GALW_WARPS - 1) / GALW_WARPS;
+        const unsigned gw = (unsigned)(nb < 148LL * 48 ? nb : 148LL * 48);
+        galerkin_warp3_kernel<<<gw, 32 * GALW_WARPS, sm, s>>>(gc, gf, E, mask_f, mask_c, elm_c, off0, Mc, slow_ws);
+        galerkin_kernel<3, 1, GAL3_NT><<<bl, GAL3_NT, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, Mc, slow_ws);
+        return;
+    }
     if (gc.dim == 2) {
-        if (E) galerkin_kernel<2, 1, 64><<<bl, 64, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, Mc);
-        else galerkin_kernel<2, 0, 64><<<bl, 64, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, nullptr);
+        if (E) galerkin_kernel<2, 1, 64><<<bl, 64, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, Mc, nullptr);
+        else galerkin_kernel<2, 0, 64><<<bl, 64, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, nullptr, nullptr);
     } else {
-        if (E) galerkin_kernel<3, 1, GAL3_NT><<<bl, GAL3_NT, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, Mc);
-        else galerkin_kernel<3, 0, GAL3_NT><<<bl, GAL3_NT, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, nullptr);
+        if (E) galerkin_kernel<3, 1, GAL3_NT><<<bl, GAL3_NT, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, Mc, nullptr);
+        else galerkin_kernel<3, 0, GAL3_NT><<<bl, GAL3_NT, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, nullptr, nullptr);
     }
 }
 
@@ -263,8 +342,8 @@ void galerkin_elements(const LevelGeom& gc, const LevelGeom& gf, const double* E
 void galerkin_elements_G(const LevelGeom& gc, const LevelGeom& gf, const double* sig, const uint8_t* mask_f,
                          const uint8_t* mask_c, double* elm_c, cudaStream_t s) {
     unsigned bl = galerkin_grid(gc);
-    if (gc.dim == 2) galerkin_kernel<2, 2, 64><<<bl, 64, 0, s>>>(gc, gf, sig, nullptr, mask_f, mask_c, elm_c, 0, nullptr);
-    else galerkin_kernel<3, 2, GAL3_NT><<<bl, GAL3_NT, 0, s>>>(gc, gf, sig, nullptr, mask_f, mask_c, elm_c, 0, nullptr);
+    if (gc.dim == 2) galerkin_kernel<2, 2, 64><<<bl, 64, 0, s>>>(gc, gf, sig, nullptr, mask_f, mask_c, elm_c, 0, nullptr, nullptr);
+    else galerkin_kernel<3, 2, GAL3_NT><<<bl, GAL3_NT, 0, s>>>(gc, gf, sig, nullptr, mask_f, mask_c, elm_c, 0, nullptr, nullptr);
 }
 
 // M_c = Q_c^T K0 Q_c for the 2^d children (host, once per handle); layout [child][NL*NL]

@@ -153,7 +153,8 @@ void coarse_apply(int op, const CoarseArgs& a, cudaStream_t s);
 void galerkin_set_constants(int dim, const double* K0, cudaStream_t s);
 void galerkin_elements(const LevelGeom& gc, const LevelGeom& gf, const double* E /*if from_E*/,
                        const double* elm_f, const uint8_t* mask_f, const uint8_t* mask_c,
-                       double* elm_c, cudaStream_t s, int off0 = 0, const double* Mc = nullptr);
+                       double* elm_c, cudaStream_t s, int off0 = 0, const double* Mc = nullptr,
+                       int* slow_ws = nullptr);
 void galerkin_child_matrices(int dim, const double* K0, double* Mc_host);
 void elements_from_E(const LevelGeom& g, const double* E, const uint8_t* mask, double* elm, cudaStream_t s);
 // identity_fixed: identity rows at fixed DOFs (K); false for G (zero rows/cols)

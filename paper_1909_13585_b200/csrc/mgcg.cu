@@ -549,6 +549,13 @@ static mg_status coarsest_solve(mg_ctx* c, int R, const int* active, const int* 
 }
 
 // ---------------------------------------------------------------- operators (per design)
+// MG_GAL_WARP (default on): 3D level-1 Galerkin by a warp per coarse element for the elements whose
+// fine nodes are all free (sum_c E_c M_c), the general kernel on the listed rest
+static bool gal_warp() {
+    static const bool v = !getenv("MG_GAL_WARP") || atoi(getenv("MG_GAL_WARP")) != 0;
+    return v;
+}
+
 static mg_status compute_operators(mg_ctx* c) {
     cudaStream_t s = c->stream;
     const int L = c->L, dim = c->dim;
@@ -595,7 +602,9 @@ static mg_status compute_operators(mg_ctx* c) {
             Level& g = sl.lv[l];
             double* elm = (l & 1) ? sl.elmA : sl.elmB;
             double* elm_prev = (l & 1) ? sl.elmB : sl.elmA;
-            galerkin_elements(g.g, f.g, l == 1 ? sl.E : nullptr, elm_prev, f.mask, g.mask, elm, s, sl.gl, c->Mc);
+            // level 1 (3D): the list of masked coarse elements lives in the idle level-2 buffer
+            int* ws = (l == 1 && c->dim == 3 && gal_warp()) ? reinterpret_cast<int*>(sl.elmB) : nullptr;
+            galerkin_elements(g.g, f.g, l == 1 ? sl.E : nullptr, elm_prev, f.mask, g.mask, elm, s, sl.gl, c->Mc, ws);
             c->launches++;
         }
         CHECK_LAUNCH();
@@ -1427,7 +1436,8 @@ static mg_status setup_impl(mg_ctx* c, const mg_grid* grid, const double* E_e, c
         }
         // element-matrix ping-pong buffers (level 1 in A, level 2 in B, ...)
         const long long nA = levels >= 2 ? sl.lv[1].g.nelem : (levels == 1 ? g0.nelem : 1);
-        const long long nB = levels >= 3 ? sl.lv[2].g.nelem : 1;
+        // (elmB also holds the level-1 Galerkin's list of masked elements: nA + 1 ints)
+        const long long nB = std::max<long long>(levels >= 3 ? sl.lv[2].g.nelem : 1, (nA + 1 + 2 * NL * NL - 1) / (2 * NL * NL));
         CU(cudaMalloc(&sl.elmA, sizeof(double) * nA * NL * NL));
         CU(cudaMalloc(&sl.elmB, sizeof(double) * nB * NL * NL));
         // owned fixed planes -> fine mask

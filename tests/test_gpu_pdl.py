@@ -71,3 +71,14 @@ def test_z2_in_post_bitwise():
     on, off = _run(names, MG_Z2_IN_POST="1"), _run(names, MG_Z2_IN_POST="0")
     for n in names:
         assert on[n] == off[n], n
+
+
+@pytest.mark.gpu
+def test_galerkin_warp_bitwise():
+    """3D level-1 Galerkin: the warp-per-element kernel for elements with free fine nodes plus the
+    general kernel on the listed rest (MG_GAL_WARP=1, default) builds bit for bit the coarse
+    operators of the general kernel alone (=0), hence the same solves (slab grids included)."""
+    names = ["T3a", "T3d", "T3f", "C4"]
+    on, off = _run(names, MG_GAL_WARP="1"), _run(names, MG_GAL_WARP="0")
+    for n in names:
+        assert on[n] == off[n], n
