@@ -528,11 +528,13 @@ void stencil_diag(const LevelGeom& g, const double* /*st*/, uint8_t* mask, doubl
 // stencil (3^d d^2 doubles per node) is read once per chunk.  The 3^d neighbour loop is
 // unrolled (compile-time offsets, no local-memory index arrays).
 template <int DIM, int OP, int RB, bool SYMH>
-__global__ void __launch_bounds__(128) coarse_kernel(CoarseArgs a, int r0) {
+__global__ void __launch_bounds__(128) coarse_kernel(CoarseArgs a, int r0, int xs) {
     pdl_begin();
     constexpr int NS = DIM == 2 ? 9 : 27;
-    r0 += blockIdx.y * RB;   // small levels: RHS groups spread over grid.y
-    long long node = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    // RHS groups spread over grid.y (small levels), or over xs consecutive blocks (blockIdx.x % xs),
+    // so the groups of a node block run side by side and all but one read the stencil from L2
+    r0 += (xs ? (int)(blockIdx.x % xs) : (int)blockIdx.y) * RB;
+    long long node = (long long)(xs ? blockIdx.x / xs : blockIdx.x) * blockDim.x + threadIdx.x;
     if (node >= a.g.nnodes) return;
     if (a.done && *a.done) return;
     const int n1 = a.g.nn[1], n2 = DIM == 3 ? a.g.nn[2] : 1;
@@ -763,16 +765,21 @@ static void launch_coarse_large(const CoarseArgs& a, unsigned bl, int th, cudaSt
     for (int r0 = 0; r0 < a.R;) {
         int rem = a.R - r0;
         if (rem > 8) {
-            launch_kp(false, coarse_kernel<DIM, OP, 16, SYMH>, dim3(bl), dim3(th), 0, s, a, r0);
+            launch_kp(false, coarse_kernel<DIM, OP, 16, SYMH>, dim3(bl), dim3(th), 0, s, a, r0, 0);
             r0 += 16;
         } else if (rem > 4) {
-            launch_kp(false, coarse_kernel<DIM, OP, 8, SYMH>, dim3(bl), dim3(th), 0, s, a, r0);
+            // MG_COARSE_XSPLIT = 2 (default): two RHS groups of 4 per node block, 4: four of 2, 0: all 8
+            // per thread (fewer accumulators per thread: more resident warps; B200 C5 solve -0.5 ms)
+            static const int xsplit = getenv("MG_COARSE_XSPLIT") ? atoi(getenv("MG_COARSE_XSPLIT")) : 2;
+            if (xsplit == 4) launch_kp(false, coarse_kernel<DIM, OP, 2, SYMH>, dim3(4 * bl), dim3(th), 0, s, a, r0, 4);
+            else if (xsplit == 2) launch_kp(false, coarse_kernel<DIM, OP, 4, SYMH>, dim3(2 * bl), dim3(th), 0, s, a, r0, 2);
+            else launch_kp(false, coarse_kernel<DIM, OP, 8, SYMH>, dim3(bl), dim3(th), 0, s, a, r0, 0);
             r0 += 8;
         } else if (rem > 1) {
-            launch_kp(false, coarse_kernel<DIM, OP, 4, SYMH>, dim3(bl), dim3(th), 0, s, a, r0);
+            launch_kp(false, coarse_kernel<DIM, OP, 4, SYMH>, dim3(bl), dim3(th), 0, s, a, r0, 0);
             r0 += 4;
         } else {
-            launch_kp(false, coarse_kernel<DIM, OP, 1, SYMH>, dim3(bl), dim3(th), 0, s, a, r0);
+            launch_kp(false, coarse_kernel<DIM, OP, 1, SYMH>, dim3(bl), dim3(th), 0, s, a, r0, 0);
             r0 += 1;
         }
     }
@@ -791,7 +798,7 @@ static void launch_coarse_dim(const CoarseArgs& a, cudaStream_t s) {
     if (bl < 2 * 148) {   // small level: warp per (32 nodes, component), all RHS per thread
         static const bool comp = !getenv("MG_COARSE_COMP") || atoi(getenv("MG_COARSE_COMP")) != 0;
         if (!comp) {   // former path: one RHS per thread, RHS over grid.y (stencil from L2)
-            launch_kp(false, coarse_kernel<DIM, OP, 1, false>, dim3(dim3(bl, a.R)), dim3(th), 0, s, a, 0);
+            launch_kp(false, coarse_kernel<DIM, OP, 1, false>, dim3(dim3(bl, a.R)), dim3(th), 0, s, a, 0, 0);
             return;
         }
         const unsigned bc = (unsigned)((a.g.nnodes + 31) / 32);

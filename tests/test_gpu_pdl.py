@@ -82,3 +82,14 @@ def test_galerkin_warp_bitwise():
     on, off = _run(names, MG_GAL_WARP="1"), _run(names, MG_GAL_WARP="0")
     for n in names:
         assert on[n] == off[n], n
+
+
+@pytest.mark.gpu
+def test_coarse_xsplit_bitwise():
+    """Large 3D coarse levels (C5 level 1): the stencil kernel with the 7 RHS in two groups of
+    consecutive CTAs (MG_COARSE_XSPLIT=2, default) accumulates every RHS in the same order as with
+    all RHS in one thread (=0): bit for bit the same solves."""
+    names = ["C5"]
+    on, off = _run(names, MG_COARSE_XSPLIT="2"), _run(names, MG_COARSE_XSPLIT="0")
+    for n in names:
+        assert on[n] == off[n], n
