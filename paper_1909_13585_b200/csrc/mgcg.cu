@@ -280,6 +280,8 @@ struct mg_ctx {
     long long cpack_cap = 0;
     double* gj_work = nullptr;
     double* Mc = nullptr;                        // Galerkin child matrices Q_c^T K0 Q_c
+    double* Estage = nullptr;                    // mg_update_modulus: host E staged here (allocated once)
+    long long Estage_n = 0;
     double* gstage = nullptr;                    // G(u) phi host-path staging
     long long gstage_cap = 0;
     // G(u) phi with host buffers on one slab: phi chunks copied in / y chunks copied out on two
@@ -1631,19 +1633,24 @@ mg_status mg_update_modulus(mg_handle c, const double* E_e) {
     const bool edev = is_device_ptr(E_e);
     double* stage = nullptr;
     const double* src = E_e;
-    if (!edev) {
-        CU(cudaMallocAsync((void**)&stage, sizeof(double) * std::max<long long>(m, 1), s));
+    if (!edev) {   // a staging buffer kept by the handle: no pool allocation (and trim) per call
+        if (c->Estage_n < std::max<long long>(m, 1)) {
+            CU(cudaStreamSynchronize(s));
+            if (c->Estage) cudaFree(c->Estage);
+            c->Estage = nullptr;
+            CU(cudaMalloc((void**)&c->Estage, sizeof(double) * std::max<long long>(m, 1)));
+            c->Estage_n = std::max<long long>(m, 1);
+        }
+        stage = c->Estage;
         CU(cudaMemcpyAsync(stage, E_e, sizeof(double) * m, cudaMemcpyHostToDevice, s));
         src = stage;
     }
-    auto release = [&]() { if (stage) cudaFreeAsync(stage, s); };
     int bad = 0;
-    if (cudaMemsetAsync(c->d_status, 0, sizeof(int), s) != cudaSuccess) { release(); return fail(MG_ERR_CUDA, "memset"); }
+    if (cudaMemsetAsync(c->d_status, 0, sizeof(int), s) != cudaSuccess) return fail(MG_ERR_CUDA, "memset");
     if (m > 0) check_modulus_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(m, src, c->d_status);
     c->launches++;
     if (cudaMemcpyAsync(c->h_pinned, c->d_status, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
         cudaStreamSynchronize(s) != cudaSuccess) {
-        release();
         return fail(MG_ERR_CUDA, "mg_update_modulus: modulus check");
     }
     bad = c->h_pinned[0];
@@ -1653,13 +1660,11 @@ mg_status mg_update_modulus(mg_handle c, const double* E_e) {
             !comm_allreduce_sum(c->comm, c->sums, 1, s) ||
             cudaMemcpyAsync(&f, c->sums, sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
             cudaStreamSynchronize(s) != cudaSuccess) {
-            release();
             return fail(MG_ERR_NCCL, "mg_update_modulus: modulus check allreduce");
         }
         bad = f != 0.0;
     }
     if (bad) {
-        release();
         return fail(MG_ERR_MODULUS, "E_e must be positive and finite (handle unchanged)");
     }
     const int rp0 = c->rank_p0[c->comm.rank];
@@ -1668,11 +1673,9 @@ mg_status mg_update_modulus(mg_handle c, const double* E_e) {
         const long long le = g0.nelem / g0.N[0];
         if (cudaMemcpyAsync(sl.E + sl.gl * le, src + (long long)(sl.e0 - rp0) * le, sizeof(double) * (sl.e1 - sl.e0) * le,
                             cudaMemcpyDeviceToDevice, s) != cudaSuccess) {
-            release();
             return fail(MG_ERR_CUDA, "mg_update_modulus: copy");
         }
     }
-    release();
     // E changes the stencils but not the masks; the masks of coarse levels may have been
     // augmented by zero-diagonal DOFs, which stay valid for the same BCs.
     return compute_operators(c);
@@ -2726,6 +2729,7 @@ mg_status mg_destroy(mg_handle c) {
             if (p) cudaFree(p);
         if (s.maskpad) cudaFree(s.maskpad);
     }
+    if (c->Estage) cudaFree(c->Estage);
     for (double* p : {c->Ainv, c->stg, c->cpack, c->cgath, c->gj_work, c->sums, c->Mc, c->gstage, c->wbuf, c->dlam,
                       c->bpart, c->bGam, c->bRho, c->bRhoN, c->bC})
         if (p) cudaFree(p);
