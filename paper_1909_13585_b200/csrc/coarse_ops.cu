@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(NT) galerkin_kernel(LevelGeom gc, LevelGeom gf
 // children order of galerkin_kernel's fast path (bitwise the same matrices) and scaled by the coarse
 // free-DOF factors; the others are appended to `list` (list[0] = count) for galerkin_kernel.  No
 // CTA barrier per element: 8 warps per CTA keep 8 elements in flight each.
-static constexpr int GALW_WARPS = 8;
+static constexpr int GALW_WARPS = 8, GALW_EPW = 4;
 __global__ void __launch_bounds__(32 * GALW_WARPS) galerkin_warp3_kernel(LevelGeom gc, LevelGeom gf,
                                                                          const double* __restrict__ E,
                                                                          const uint8_t* __restrict__ mask_f,
@@ -261,45 +261,67 @@ __global__ void __launch_bounds__(32 * GALW_WARPS) galerkin_warp3_kernel(LevelGe
     for (int e = threadIdx.x; e < 8 * NE; e += blockDim.x) Ms[e] = Mc[e];
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (long long Ec = (long long)blockIdx.x * GALW_WARPS + warp; Ec < gc.nelem; Ec += (long long)gridDim.x * GALW_WARPS) {
-        int ci[3];
-        long long tt = Ec;
-        for (int k = 2; k >= 0; --k) { ci[k] = (int)(tt % gc.N[k]); tt /= gc.N[k]; }
-        if (ci[0] < off0) continue;   // slab ghost element layer: filled by the halo exchange
-        int fixed_here = 0;
-        if (lane < 27) {
-            int q = lane, fc[3];
-            for (int k = 2; k >= 0; --k) { fc[k] = 2 * ci[k] + q % 3 - (k == 0 ? off0 : 0); q /= 3; }
-            const bool inside = fc[0] >= 0 && fc[0] < gf.nn[0] && fc[1] < gf.nn[1] && fc[2] < gf.nn[2];
-            fixed_here = inside ? mask_f[((long long)fc[0] * gf.nn[1] + fc[1]) * gf.nn[2] + fc[2]] != 0 : 1;
-        }
-        if (__any_sync(0xffffffffu, fixed_here)) {
-            if (lane == 0) list[1 + atomicAdd(list, 1)] = (int)Ec;
-            continue;
-        }
-        double fr = 0.0, ev = 0.0;
-        if (lane < NL) {   // coarse free-DOF factor of local DOF lane
-            const int a = lane / 3, comp = lane % 3;
-            const long long node = ((long long)(ci[0] + (a >> 2)) * gc.nn[1] + ci[1] + ((a >> 1) & 1)) * gc.nn[2] + ci[2] + (a & 1);
-            fr = ((mask_c[node] >> comp) & 1) ? 0.0 : 1.0;
-        }
-        if (lane < 8) {    // child lane's modulus
-            const long long fe = ((long long)(2 * ci[0] + (lane >> 2) - off0) * gf.N[1] + 2 * ci[1] + ((lane >> 1) & 1)) * gf.N[2] +
-                                 2 * ci[2] + (lane & 1);
-            ev = E[fe];
-        }
-        double evc[8];
+    // GALW_EPW consecutive elements per warp iteration: every M_c entry read from shared memory
+    // serves all of them (the kernel is bound by those reads otherwise)
+    const long long stride = (long long)gridDim.x * GALW_WARPS * GALW_EPW;
+    for (long long E0 = ((long long)blockIdx.x * GALW_WARPS + warp) * GALW_EPW; E0 < gc.nelem; E0 += stride) {
+        bool fast[GALW_EPW];
+        double fr[GALW_EPW], evc[GALW_EPW][8];
 #pragma unroll
-        for (int ch = 0; ch < 8; ++ch) evc[ch] = __shfl_sync(0xffffffffu, ev, ch);
-        double* out = elm_c + Ec * NE;
+        for (int q = 0; q < GALW_EPW; ++q) {
+            const long long Ec = E0 + q;
+            fast[q] = false;
+            fr[q] = 0.0;
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) evc[q][ch] = 0.0;
+            if (Ec >= gc.nelem) continue;   // warp-uniform
+            int ci[3];
+            long long tt = Ec;
+            for (int k = 2; k >= 0; --k) { ci[k] = (int)(tt % gc.N[k]); tt /= gc.N[k]; }
+            if (ci[0] < off0) continue;   // slab ghost element layer: filled by the halo exchange
+            int fixed_here = 0;
+            if (lane < 27) {
+                int qq = lane, fc[3];
+                for (int k = 2; k >= 0; --k) { fc[k] = 2 * ci[k] + qq % 3 - (k == 0 ? off0 : 0); qq /= 3; }
+                const bool inside = fc[0] >= 0 && fc[0] < gf.nn[0] && fc[1] < gf.nn[1] && fc[2] < gf.nn[2];
+                fixed_here = inside ? mask_f[((long long)fc[0] * gf.nn[1] + fc[1]) * gf.nn[2] + fc[2]] != 0 : 1;
+            }
+            if (__any_sync(0xffffffffu, fixed_here)) {
+                if (lane == 0) list[1 + atomicAdd(list, 1)] = (int)Ec;
+                continue;
+            }
+            fast[q] = true;
+            if (lane < NL) {   // coarse free-DOF factor of local DOF lane
+                const int a = lane / 3, comp = lane % 3;
+                const long long node = ((long long)(ci[0] + (a >> 2)) * gc.nn[1] + ci[1] + ((a >> 1) & 1)) * gc.nn[2] + ci[2] + (a & 1);
+                fr[q] = ((mask_c[node] >> comp) & 1) ? 0.0 : 1.0;
+            }
+            double ev = 0.0;
+            if (lane < 8) {    // child lane's modulus
+                const long long fe = ((long long)(2 * ci[0] + (lane >> 2) - off0) * gf.N[1] + 2 * ci[1] + ((lane >> 1) & 1)) * gf.N[2] +
+                                     2 * ci[2] + (lane & 1);
+                ev = E[fe];
+            }
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) evc[q][ch] = __shfl_sync(0xffffffffu, ev, ch);
+        }
 #pragma unroll 2
         for (int u = 0; u < NE / 32; ++u) {
             const int t = lane + 32 * u, row = t / NL, col = t % NL;
-            double acc = 0.0;
+            double acc[GALW_EPW];
 #pragma unroll
-            for (int ch = 0; ch < 8; ++ch) acc = fma(evc[ch], Ms[ch * NE + t], acc);
-            const double frow = __shfl_sync(0xffffffffu, fr, row), fcol = __shfl_sync(0xffffffffu, fr, col);
-            out[t] = acc * frow * fcol;
+            for (int q = 0; q < GALW_EPW; ++q) acc[q] = 0.0;
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) {
+                const double mv = Ms[ch * NE + t];
+#pragma unroll
+                for (int q = 0; q < GALW_EPW; ++q) acc[q] = fma(evc[q][ch], mv, acc[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < GALW_EPW; ++q) {
+                const double frow = __shfl_sync(0xffffffffu, fr[q], row), fcol = __shfl_sync(0xffffffffu, fr[q], col);
+                if (fast[q]) elm_c[(E0 + q) * NE + t] = acc[q] * frow * fcol;
+            }
         }
     }
 }
@@ -323,7 +345,7 @@ void galerkin_elements(const LevelGeom& gc, const LevelGeom& gf, const double* E
         static bool at = (cudaFuncSetAttribute(galerkin_warp3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), true);
         (void)at;
         cudaMemsetAsync(slow_ws, 0, sizeof(int), s);
-        const long long nb = (gc.nelem + GALW_WARPS - 1) / GALW_WARPS;
+        const long long nb = (gc.nelem + GALW_WARPS * GALW_EPW - 1) / (GALW_WARPS * GALW_EPW);
         const unsigned gw = (unsigned)(nb < 148LL * 48 ? nb : 148LL * 48);
         galerkin_warp3_kernel<<<gw, 32 * GALW_WARPS, sm, s>>>(gc, gf, E, mask_f, mask_c, elm_c, off0, Mc, slow_ws);
         galerkin_kernel<3, 1, GAL3_NT><<<bl, GAL3_NT, 0, s>>>(gc, gf, E, elm_f, mask_f, mask_c, elm_c, off0, Mc, slow_ws);
