@@ -11,6 +11,7 @@
 // exchanges in comm.cu at the points listed in DESIGN.md §7.  With S = 1 every exchange is
 // a no-op and the code path is the single-GPU one.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -390,11 +391,26 @@ static mg_status ensure_constants(mg_ctx* c) {
     return MG_OK;
 }
 
+// NVTX ranges: one per C-ABI call (named after the function) and one per phase of a solve, for
+// nsys / `ncu --nvtx` timelines.  Header-only NVTX3: without an attached tool a push / pop is a
+// check of a null function pointer.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    void next(const char* name) {   // close the current phase, open the next
+        nvtxRangePop();
+        nvtxRangePushA(name);
+    }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 struct ApiScope {
+    NvtxRange nv;   // first member: the range spans the lock, the stream join and the call
     mg_ctx* c;
     std::lock_guard<std::recursive_mutex> lk;
     mg_status status;
-    explicit ApiScope(mg_ctx* c_) : c(c_), lk(g_api_mu), status(MG_OK) {
+    ApiScope(mg_ctx* c_, const char* fn) : nv(fn), c(c_), lk(g_api_mu), status(MG_OK) {
         stream_enter(c);
         status = ensure_constants(c);
     }
@@ -402,8 +418,8 @@ struct ApiScope {
     ApiScope(const ApiScope&) = delete;
     ApiScope& operator=(const ApiScope&) = delete;
 };
-#define API_SCOPE(c)          \
-    ApiScope api_scope_(c);   \
+#define API_SCOPE(c)                    \
+    ApiScope api_scope_(c, __func__);   \
     TRY(api_scope_.status)
 
 // ---------------------------------------------------------------- partition (host)
@@ -1568,6 +1584,7 @@ mg_status mg_nccl_unique_id(void* out128) {
 
 mg_status mg_setup_dist(const mg_grid* grid, const double* E_e, const uint8_t* fixed, int levels, const mg_opts* opts,
                         const mg_dist* dist, void* stream, mg_handle* out) {
+    NvtxRange nv(__func__);
     if (!grid || !E_e || !fixed || !out) return fail(MG_ERR_ARG, "NULL argument");
     if (grid->dim != 2 && grid->dim != 3) return fail(MG_ERR_ARG, "dim must be 2 or 3");
     if (grid->element != MG_ELEM_STD && grid->element != MG_ELEM_WILSON) return fail(MG_ERR_ARG, "unknown element");
@@ -1699,11 +1716,13 @@ mg_status mgcg_solve(mg_handle c, const double* rhs, int nrhs, double tol, doubl
     }
     const bool rdev = is_device_ptr(rhs), xdev = is_device_ptr(x);
     const double* rsrc = rhs;
+    NvtxRange phase("mgcg_solve: rhs in");
     if (!rdev) {
         CU(cudaMemcpyAsync(c->stage, rhs, sizeof(double) * n * nrhs, cudaMemcpyHostToDevice, s));
         rsrc = c->stage;
     }
     TRY(scatter_fine(c, rsrc, nrhs, true, &Slab::b));
+    phase.next("mgcg_solve: iterate");
     CU(cudaMemsetAsync(c->ctl.status, 0, sizeof(int), s));
     CU(cudaGraphLaunch(c->g_init, s));
     CU(cudaGraphLaunch(c->g_restart, s));
@@ -1775,6 +1794,7 @@ mg_status mgcg_solve(mg_handle c, const double* rhs, int nrhs, double tol, doubl
         klaunch += c->n_restart + nslab(c);
     }
     // copy x out
+    phase.next("mgcg_solve: x out");
     double* xdst = xdev ? x : c->stage;
     TRY(gather_fine(c, &Slab::x, nrhs, xdst));
     if (!xdev) CU(cudaMemcpyAsync(x, c->stage, sizeof(double) * n * nrhs, cudaMemcpyDeviceToHost, s));

@@ -56,6 +56,15 @@ def test_sass_is_sm100a(libpath):
     assert "sm_100a" in out
 
 
+def test_nvtx_ranges_compiled_in(libpath):
+    """Every C-ABI call opens an NVTX range named after itself; mgcg_solve adds its phases."""
+    blob = open(libpath, "rb").read()
+    for name in (b"mg_setup_dist", b"mg_update_modulus", b"mgcg_solve", b"stress_stiffness_apply",
+                 b"mgcg_solve: rhs in", b"mgcg_solve: iterate", b"mgcg_solve: x out"):
+        assert name + b"\0" in blob, name
+    assert b"nvtxGetExportTable" in blob or b"NVTX_INJECTION64_PATH" in blob
+
+
 def test_product_path_does_not_import_oracle():
     pkg = os.path.join(ROOT, "paper_1909_13585_b200")
     for dirpath, _, files in os.walk(pkg):
