@@ -211,6 +211,21 @@ static constexpr int T_VW = 100, T_EW = 34, T_MW = 48;
 // (row offset 0 / 1), rows 128-byte aligned in shared memory
 static constexpr int T_VWC = 112, T_RB = 102;
 __host__ __device__ constexpr int t_r128(int b) { return (b + 127) / 128 * 128; }
+// Tail tile (round 2d): when the last column tile owns <= 9 node columns (C5: 129 = 4 x 30 + 9), its
+// CTA stacks three row groups of 10 lanes (lanes 30, 31 idle copies of lane 29) instead of using 10
+// of 32 lanes: group g = lane / 10 marches element rows j0 + 7 g + w, i.e. three ordinary 7-row
+// tiles side by side in one warp set (same per-lane arithmetic, same exchange).  Boxes: vectors
+// {34 doubles, 23 rows}, E {12, 22}, masks {32 bytes, 23 rows} placed in the A field's slack.
+static constexpr int TT_G = 10, TT_VW = 34, TT_EW = 12, TT_MW = 32;
+template <int TR>
+struct TLT {
+    static constexpr int BR = 3 * (TR - 1) + 2;   // node rows per box
+    static constexpr int ER = 3 * (TR - 1) + 1;   // element rows per box
+    static constexpr int VB = BR * TT_VW * 8;
+    static constexpr int EB = ER * TT_EW * 8;
+    static constexpr int MB = BR * TT_MW;
+    static constexpr int OMA = t_r128(VB);        // mask box offset inside the A field
+};
 template <int OP, int TR, int NB>
 struct TL {
     static constexpr int BR = TR + 1;                    // node rows per box
@@ -228,6 +243,13 @@ struct TL {
     static constexpr int SINV = NB * TR * 6 * 32 * 8;   // row -> row+1 exchange, NB buffers
 };
 
+template <int OP, int TR, int NB>
+constexpr bool h8t_tail_fits() {
+    using T = TL<OP, TR, NB>;
+    using U = TLT<TR>;
+    return OP != FOP_GPHI && U::VB <= T::VB && U::OMA + U::MB <= t_r128(T::VB) && U::EB <= T::EB;
+}
+
 template <int OP, int TR, int NS, int NB>
 static constexpr size_t h8t_smem_bytes() {
     using T = TL<OP, TR, NB>;
@@ -241,18 +263,28 @@ __host__ __device__ constexpr unsigned h8t_tx_bytes(bool hasC) {
     using T = TL<OP, TR, 1>;
     return (unsigned)(T::VB + (T::HB ? T::VB : 0) + ((T::HC && hasC) ? T::VB : 0) + T::EB + T::MB);
 }
+template <int OP, int TR>
+__host__ __device__ constexpr unsigned h8t_tx_bytes_tail(bool hasC) {
+    using T = TL<OP, TR, 1>;
+    using U = TLT<TR>;
+    return (unsigned)(U::VB + (T::HB ? U::VB : 0) + ((T::HC && hasC) ? U::VB : 0) + U::EB + U::MB);
+}
 
 struct H8TMaps {
     CUtensorMap A, B, C, E, M;
 };
 
-template <int OP, bool C03, int TR, int NS, int NB, int MINB>
+template <int OP, bool C03, int TR, int NS, int NB, int MINB, bool TAIL>
 __global__ void __launch_bounds__(32 * TR, MINB)
     h8t_kernel(const __grid_constant__ FineArgs a, const __grid_constant__ H8TMaps tm, int ntc, int ntr, int nch,
-               int hch, int hasC) {
+               int hch, int hasC, int tc0, int toff) {
     pdl_begin();
     using T = TL<OP, TR, NB>;
+    using U = TLT<TR>;
+    static_assert(!TAIL || h8t_tail_fits<OP, TR, NB>(), "tail boxes must fit the slot");
     constexpr int OWNR = TR - 1;
+    constexpr int VW = TAIL ? TT_VW : T_VW, EW = TAIL ? TT_EW : T_EW, MW = TAIL ? TT_MW : T_MW;
+    constexpr int OMK = TAIL ? T::OA + U::OMA : T::OM;   // mask box offset in a slot
     extern __shared__ __align__(128) unsigned char t_sm[];
     unsigned char* ring = t_sm;
     double* sinv = reinterpret_cast<double*>(t_sm + NS * T::SLOT);                       // [NB][TR][6][32]
@@ -270,14 +302,18 @@ __global__ void __launch_bounds__(32 * TR, MINB)
     if (tile >= nt * nch) return;
     if (a.done && *a.done) return;
     if (a.active && !a.active[r]) return;
-    const int tc = tile % ntc, tr = (tile / ntc) % ntr, ch = tile / nt;
+    const int tc = tc0 + tile % ntc, tr = (tile / ntc) % ntr, ch = tile / nt;
     const int n0 = a.g.nn[0], n1 = a.g.nn[1], n2 = a.g.nn[2];
     const int p2 = a.g.p2;
-    const int c0 = 30 * tc - 1, j0 = OWNR * tr - 1;
+    const int c0 = 30 * tc - 1, j0 = (TAIL ? 3 * OWNR : OWNR) * tr - 1;
     const int cm0 = (c0 - 1) & ~15;   // mask box start (16-byte aligned)
-    const int mlane = lane + (c0 - cm0);
-    const int j = j0 + w, c = c0 + lane;
-    const bool own = w >= 1 && lane >= 1 && lane <= 30 && j < n1 && c < n2;
+    // tail: row group g, lane gl within it (lanes 30, 31 duplicate lane 29 and own nothing)
+    const int tg = TAIL ? min(lane / TT_G, 2) : 0;
+    const int gl = TAIL ? min(lane - TT_G * tg, TT_G - 1) : lane;
+    const int rb = TAIL ? OWNR * tg : 0;   // box row of this lane's element row w
+    const int mlane = gl + (c0 - cm0);
+    const int j = j0 + rb + w, c = c0 + gl;
+    const bool own = w >= 1 && gl >= 1 && (TAIL ? lane < 3 * TT_G : lane <= 30) && j < n1 && c < n2;
     const int i0 = ch * hch, i1 = min(i0 + hch, n0);
     const int nq = i1 - i0 + 2;   // planes i0-1 .. i1
     const long long vbase = (long long)r * a.g.vstr + (OP == FOP_GPHI ? a.goffA : 0);
@@ -301,7 +337,7 @@ __global__ void __launch_bounds__(32 * TR, MINB)
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-    const unsigned txb = h8t_tx_bytes<OP, TR>(hasC != 0);
+    const unsigned txb = TAIL ? h8t_tx_bytes_tail<OP, TR>(hasC != 0) : h8t_tx_bytes<OP, TR>(hasC != 0);
     auto issue = [&](int q) {   // plane Q = i0 - 1 + q into slot q % NS
         const int s = q % NS, Q = i0 - 1 + q;
         unsigned char* sl = ring + s * T::SLOT;
@@ -333,16 +369,16 @@ __global__ void __launch_bounds__(32 * TR, MINB)
             else t_tma3(sl + T::OC, &tm.C, cv, j0, Q, &full[s]);
         }
         t_tma3(sl + T::OE, &tm.E, c0 - 1, j0, Q, &full[s]);
-        t_tma3(sl + T::OM, &tm.M, cm0, j0, Q, &full[s]);
+        t_tma3(sl + OMK, &tm.M, cm0, j0, Q, &full[s]);
     };
     if (threadIdx.x == 0)
         for (int q = 0; q < NS && q < nq; ++q) issue(q);
 
-    auto fA = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OA) + row * T_VW + 3 * (lane + 1); };
-    auto fB = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OB) + row * T_VW + 3 * (lane + 1); };
-    auto fC = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OC) + row * T_VW + 3 * (lane + 1); };
-    auto fE = [&](int s) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OE)[w * T_EW + lane + 1]; };
-    auto fM = [&](int s, int row) { return (int)(ring + s * T::SLOT + T::OM)[row * T_MW + mlane]; };
+    auto fA = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OA) + (rb + row) * VW + 3 * (gl + 1); };
+    auto fB = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OB) + (rb + row) * VW + 3 * (gl + 1); };
+    auto fC = [&](int s, int row) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OC) + (rb + row) * VW + 3 * (gl + 1); };
+    auto fE = [&](int s) { return reinterpret_cast<const double*>(ring + s * T::SLOT + T::OE)[(rb + w) * EW + gl + 1]; };
+    auto fM = [&](int s, int row) { return (int)(ring + s * T::SLOT + OMK)[(rb + row) * MW + mlane]; };
 
     // G(u) phi: compact rows (row offset 0 / 1 double), rows outside the grid were not loaded
     const bool colok = c >= 0 && c < n2;
@@ -695,7 +731,7 @@ __global__ void __launch_bounds__(32 * TR, MINB)
             double t = 0.0;
 #pragma unroll
             for (int q = 0; q < TR; ++q) t += s_dot[q];
-            a.partial[(long long)r * a.pstride + tile] = t;
+            a.partial[(long long)r * a.pstride + toff + tile] = t;
         }
     }
 }
@@ -730,22 +766,53 @@ static bool t_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* 
 }
 
 // vectors (R, n0, n1, p2, 3) as a 4-D tensor {3 n2, n1, n0, R} (row pitch 3 p2)
-static bool t_map_vec(CUtensorMap* m, const FineArgs& a, const double* v, int BR, bool perR) {
+static bool t_map_vec(CUtensorMap* m, const FineArgs& a, const double* v, int BR, bool perR, int VW = T_VW) {
     const LevelGeom& g = a.g;
     cuuint64_t dims[4] = {(cuuint64_t)3 * g.nn[2], (cuuint64_t)g.nn[1], (cuuint64_t)g.nn[0], (cuuint64_t)std::max(a.R, 1)};
     cuuint64_t str[3] = {(cuuint64_t)3 * g.p2 * 8, (cuuint64_t)3 * g.p2 * g.nn[1] * 8, (cuuint64_t)g.vstr * 8};
-    cuuint32_t box[4] = {(cuuint32_t)T_VW, (cuuint32_t)BR, 1, 1};
+    cuuint32_t box[4] = {(cuuint32_t)VW, (cuuint32_t)BR, 1, 1};
     return t_map(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, perR ? 4 : 3, v, dims, str, box);
 }
 
-template <int OP, int TR, int NS, int NB, int MINB>
-static bool launch_h8t_t(const FineArgs& a, cudaStream_t s) {
+// MG_H8T_TAIL=0: the last column tile as an ordinary tile even when it owns <= 9 node columns
+static bool h8t_tail_enabled() {
+    static bool v = [] {
+        const char* e = getenv("MG_H8T_TAIL");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return v;
+}
+
+// Tiling of one launch: ntc x ntr ordinary tiles per chunk (nch chunks of hch planes), plus, in tail
+// mode, ntr3 stacked-row tiles of the last column (nch3 chunks of hch3 planes) in a second launch
+// whose dot partials follow the first launch's.
+struct H8TPlan {
+    bool tail = false;
+    int ntc = 0, ntr = 0, nch = 1, hch = 0;
+    int ntr3 = 0, nch3 = 1, hch3 = 0;
+    int items() const { return ntc * ntr * nch + (tail ? ntr3 * nch3 : 0); }
+};
+
+static H8TPlan h8t_plan(int TR, int minb, const LevelGeom& g, int R, bool allow_tail) {
+    H8TPlan p;
+    const int ntc_all = (g.nn[2] + 29) / 30;
+    p.tail = allow_tail && TR == 8 && h8t_tail_enabled() && ntc_all >= 2 &&
+             g.nn[2] - 1 - (30 * (ntc_all - 1) - 1) <= TT_G - 1;
+    p.ntc = p.tail ? ntc_all - 1 : ntc_all;
+    p.ntr = (g.nn[1] + TR - 2) / (TR - 1);
+    h8t_chunks(TR, minb, p.ntc * p.ntr, g, R, &p.nch, &p.hch);
+    if (p.tail) {
+        p.ntr3 = (g.nn[1] + 3 * (TR - 1) - 1) / (3 * (TR - 1));
+        h8t_chunks(TR, minb, p.ntr3, g, R, &p.nch3, &p.hch3);
+    }
+    return p;
+}
+
+template <int OP, int TR, int NS, int NB, int MINB, bool TAIL>
+static bool launch_h8t_part(const FineArgs& a, cudaStream_t s, int ntc, int ntr, int nch, int hch, int tc0, int toff) {
     using T = TL<OP, TR, NB>;
+    using U = TLT<TR>;
     const LevelGeom& g = a.g;
-    const int ntc = (g.nn[2] + 29) / 30;
-    const int ntr = (g.nn[1] + TR - 2) / (TR - 1);
-    int nch, hch;
-    h8t_chunks(TR, MINB, g, a.R, &nch, &hch);
     H8TMaps tm;
     memset(&tm, 0, sizeof(tm));
     const double* vA = OP == FOP_CGP ? a.pin : (OP == FOP_RESTR3 ? a.rin : a.x);
@@ -759,26 +826,27 @@ static bool launch_h8t_t(const FineArgs& a, cudaStream_t s) {
         ok = t_map(&tm.A, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 1, vA - a.goffA, dA, nostr, box) &&
              t_map(&tm.B, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 1, vB - a.goffB, dB, nostr, box);
     } else {
-        ok = t_map_vec(&tm.A, a, vA, T::BR, true);
-        if (T::HB) ok = ok && t_map_vec(&tm.B, a, vB, T::BR, true);
-        if (hasC) ok = ok && t_map_vec(&tm.C, a, OP == FOP_CGP ? a.xv : a.Dinv, T::BR, OP == FOP_CGP);
+        const int BR = TAIL ? U::BR : T::BR, VW = TAIL ? TT_VW : T_VW;
+        ok = t_map_vec(&tm.A, a, vA, BR, true, VW);
+        if (T::HB) ok = ok && t_map_vec(&tm.B, a, vB, BR, true, VW);
+        if (hasC) ok = ok && t_map_vec(&tm.C, a, OP == FOP_CGP ? a.xv : a.Dinv, BR, OP == FOP_CGP, VW);
     }
     {
         cuuint64_t dims[3] = {(cuuint64_t)g.N[2], (cuuint64_t)g.N[1], (cuuint64_t)g.N[0]};
         cuuint64_t str[2] = {(cuuint64_t)a.ep2 * 8, (cuuint64_t)a.ep2 * g.N[1] * 8};
-        cuuint32_t box[3] = {(cuuint32_t)T_EW, (cuuint32_t)TR, 1};
+        cuuint32_t box[3] = {(cuuint32_t)(TAIL ? TT_EW : T_EW), (cuuint32_t)(TAIL ? U::ER : TR), 1};
         ok = ok && t_map(&tm.E, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, a.E, dims, str, box);
     }
     {
         cuuint64_t dims[3] = {(cuuint64_t)g.nn[2], (cuuint64_t)g.nn[1], (cuuint64_t)g.nn[0]};
         cuuint64_t str[2] = {(cuuint64_t)a.m2, (cuuint64_t)a.m2 * g.nn[1]};
-        cuuint32_t box[3] = {(cuuint32_t)T_MW, (cuuint32_t)T::BR, 1};
+        cuuint32_t box[3] = {(cuuint32_t)(TAIL ? TT_MW : T_MW), (cuuint32_t)(TAIL ? U::BR : T::BR), 1};
         ok = ok && t_map(&tm.M, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, a.mask, dims, str, box);
     }
     if (!ok) return false;
     const size_t smem = h8t_smem_bytes<OP, TR, NS, NB>();
-    auto k03 = h8t_kernel<OP, true, TR, NS, NB, MINB>;
-    auto kgn = h8t_kernel<OP, false, TR, NS, NB, MINB>;
+    auto k03 = h8t_kernel<OP, true, TR, NS, NB, MINB, TAIL>;
+    auto kgn = h8t_kernel<OP, false, TR, NS, NB, MINB, TAIL>;
     static bool attr = [&] {
         cudaFuncSetAttribute(k03, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(kgn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -786,8 +854,23 @@ static bool launch_h8t_t(const FineArgs& a, cudaStream_t s) {
     }();
     (void)attr;
     const unsigned nb = (unsigned)((long long)ntc * ntr * nch * a.R);
-    if (a.nu_paper) launch_kp(false, k03, dim3(nb), dim3(32 * TR), smem, s, a, tm, ntc, ntr, nch, hch, hasC ? 1 : 0);
-    else launch_kp(false, kgn, dim3(nb), dim3(32 * TR), smem, s, a, tm, ntc, ntr, nch, hch, hasC ? 1 : 0);
+    if (a.nu_paper)
+        launch_kp(false, k03, dim3(nb), dim3(32 * TR), smem, s, a, tm, ntc, ntr, nch, hch, hasC ? 1 : 0, tc0, toff);
+    else
+        launch_kp(false, kgn, dim3(nb), dim3(32 * TR), smem, s, a, tm, ntc, ntr, nch, hch, hasC ? 1 : 0, tc0, toff);
+    return true;
+}
+
+template <int OP, int TR, int NS, int NB, int MINB>
+static bool launch_h8t_t(const FineArgs& a, cudaStream_t s) {
+    constexpr bool TAILOK = h8t_tail_fits<OP, TR, NB>();
+    const H8TPlan p = h8t_plan(TR, MINB, a.g, a.R, TAILOK);
+    if (!launch_h8t_part<OP, TR, NS, NB, MINB, false>(a, s, p.ntc, p.ntr, p.nch, p.hch, 0, 0)) return false;
+    if constexpr (TAILOK) {
+        if (p.tail)
+            return launch_h8t_part<OP, TR, NS, NB, MINB, true>(a, s, 1, p.ntr3, p.nch3, p.hch3, p.ntc,
+                                                               p.ntc * p.ntr * p.nch);
+    }
     return true;
 }
 
@@ -824,9 +907,8 @@ constexpr int h8t_auto_ns() {
 
 // chunking along axis 0: between 16 and 64 planes per chunk, picked so that the CTA count fills
 // the resident slots (148 SMs x CTAs per SM) with the smallest tail wave
-void h8t_chunks(int TR, int minb, const LevelGeom& g, int R, int* nch_out, int* hch_out) {
-    const int ntc = (g.nn[2] + 29) / 30;
-    const int ntr = (g.nn[1] + TR - 2) / (TR - 1);
+void h8t_chunks(int TR, int minb, int tiles, const LevelGeom& g, int R, int* nch_out, int* hch_out) {
+    (void)TR;
     const long long slots = 148LL * minb;
     const int n0 = g.nn[0];
     int best = 1;
@@ -834,7 +916,7 @@ void h8t_chunks(int TR, int minb, const LevelGeom& g, int R, int* nch_out, int* 
     for (int nch = 1; nch <= std::max(1, n0 / 8); ++nch) {
         const int hch = (n0 + nch - 1) / nch;
         const int nc = (n0 + hch - 1) / hch;
-        const long long ctas = (long long)ntc * ntr * nc * R;
+        const long long ctas = (long long)tiles * nc * R;
         const double waves = (double)ctas / slots;
         const double fill = waves / std::ceil(waves);
         const double eff = fill * hch / (hch + 1.0);   // + one prologue plane per chunk
@@ -844,13 +926,10 @@ void h8t_chunks(int TR, int minb, const LevelGeom& g, int R, int* nch_out, int* 
     *hch_out = (n0 + best - 1) / best;
 }
 
+// dot-partial items per RHS (sizing): the larger of the plans with and without the tail launch
 int h8t_items(const LevelGeom& g, int R) {
-    const int TR = h8t_tr();
-    const int ntc = (g.nn[2] + 29) / 30;
-    const int ntr = (g.nn[1] + TR - 2) / (TR - 1);
-    int nch, hch;
-    h8t_chunks(TR, TR == 8 ? 2 : 1, g, R, &nch, &hch);
-    return ntc * ntr * nch;
+    const int TR = h8t_tr(), minb = TR == 8 ? 2 : 1;
+    return std::max(h8t_plan(TR, minb, g, R, true).items(), h8t_plan(TR, minb, g, R, false).items());
 }
 
 template <int OP>
@@ -865,6 +944,7 @@ static bool launch_h8t_op(const FineArgs& a, cudaStream_t s) {
 }
 
 int h8t_apply(int op, const FineArgs& a, cudaStream_t s) {
+    const int TR = h8t_tr();
     bool ok;
     switch (op) {
         case FOP_GPHI: ok = launch_h8t_op<FOP_GPHI>(a, s); break;
@@ -874,7 +954,7 @@ int h8t_apply(int op, const FineArgs& a, cudaStream_t s) {
         case FOP_RESTR3: ok = launch_h8t_op<FOP_RESTR3>(a, s); break;
         default: ok = launch_h8t_op<FOP_CGP>(a, s); break;
     }
-    return ok ? h8t_items(a.g, a.R) : -1;
+    return ok ? h8t_plan(TR, TR == 8 ? 2 : 1, a.g, a.R, op != FOP_GPHI).items() : -1;
 }
 
 // ---------------------------------------------------------------- padded 3D fine layout

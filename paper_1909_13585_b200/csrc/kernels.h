@@ -70,7 +70,7 @@ void pad3_elems(const LevelGeom& g, const Pad3& p, const double* E, double* Ep, 
 void h8t_set_constants(const double* K0, double nu, cudaStream_t s);
 int h8t_apply(int op, const FineArgs& a, cudaStream_t s);
 int h8t_items(const LevelGeom& g, int R);
-void h8t_chunks(int TR, int minb, const LevelGeom& g, int R, int* nch_out, int* hch_out);
+void h8t_chunks(int TR, int minb, int tiles, const LevelGeom& g, int R, int* nch_out, int* hch_out);
 
 // ---------------------------------------------------------------- 2D fused march kernels (fine2d.cu)
 enum March2Op { M2_MATVEC = 0, M2_RESID = 1, M2_JACOBI = 2, M2_CGP = 3, M2_RESTRICT = 4, M2_POST = 5 };

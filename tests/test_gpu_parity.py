@@ -48,7 +48,7 @@ def rel(a, b):
     return np.linalg.norm(a - b, axis=-1) / np.linalg.norm(b, axis=-1)
 
 
-MATVEC_CASES = ["T2a", "T2b", "T2c", "C1", "C2", "T3a", "T3b", "T3c", "T3d", "T3f", "T3g"]
+MATVEC_CASES = ["T2a", "T2b", "T2c", "C1", "C2", "T3a", "T3b", "T3c", "T3d", "T3f", "T3g", "T3h"]
 
 
 @pytest.mark.parametrize("name", MATVEC_CASES)
@@ -100,7 +100,7 @@ def test_stress_stiffness_host_buffers_bitwise(name, nphi):
     assert np.array_equal(py.numpy(), ref)
 
 
-SOLVE_CASES = ["T2a", "T2b", "T2c", "C1", "C2", "T3a", "T3b", "T3c", "T3f", "T3g"]
+SOLVE_CASES = ["T2a", "T2b", "T2c", "C1", "C2", "T3a", "T3b", "T3c", "T3f", "T3g", "T3h"]
 
 
 @pytest.mark.parametrize("name", SOLVE_CASES)

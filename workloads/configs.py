@@ -65,6 +65,9 @@ CONFIGS = {
     # a full last tile (N2 = 64, the grid's last node column right of it) and a ragged one (N2 = 70)
     "T3f": Config("T3f", (8, 12, 64), 3, 3, nphi=2, seed=3006),
     "T3g": Config("T3g", (8, 10, 70), 2, 2, nphi=2, seed=3007),
+    # last column tile owning 7 node columns (n2 = 37 = 30 + 7): the stacked-row tail tile of the
+    # fine kernels (h8t.cu TAIL), 3 tail row tiles of 21 rows over n1 = 45 (ragged)
+    "T3h": Config("T3h", (8, 44, 36), 3, 3, nphi=2, seed=3008),
 }
 
 
