@@ -861,15 +861,57 @@ static bool launch_h8t_part(const FineArgs& a, cudaStream_t s, int ntc, int ntr,
     return true;
 }
 
+// MG_H8T_TAIL_FORK=0: the tail launch follows the main launch on the same stream; default: it is
+// forked onto a side stream right after the main launch (joined before the next operation), so its
+// CTAs fill the slots the main grid's last wave leaves free instead of running as a wave of its own.
+// Process-wide side stream and events: every C-ABI call holds the API lock, and inside a graph
+// capture the event wait pulls the side stream into the capture (a fork / join of kernel nodes).
+static bool h8t_tail_fork(cudaStream_t* side, cudaEvent_t* ev) {
+    static const bool on = [] {
+        const char* e = getenv("MG_H8T_TAIL_FORK");
+        return e ? atoi(e) != 0 : true;
+    }();
+    static cudaStream_t ss = nullptr;
+    static cudaEvent_t ee[2] = {nullptr, nullptr};
+    if (!on) return false;
+    if (!ss) {
+        if (cudaStreamCreateWithFlags(&ss, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ee[0], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ee[1], cudaEventDisableTiming) != cudaSuccess) {
+            ss = nullptr;
+            return false;
+        }
+    }
+    *side = ss;
+    ev[0] = ee[0];
+    ev[1] = ee[1];
+    return true;
+}
+
 template <int OP, int TR, int NS, int NB, int MINB>
 static bool launch_h8t_t(const FineArgs& a, cudaStream_t s) {
     constexpr bool TAILOK = h8t_tail_fits<OP, TR, NB>();
     const H8TPlan p = h8t_plan(TR, MINB, a.g, a.R, TAILOK);
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev[2];
+    const bool fork = p.tail && h8t_tail_fork(&side, ev);
+    if (fork) cudaEventRecord(ev[0], s);
     if (!launch_h8t_part<OP, TR, NS, NB, MINB, false>(a, s, p.ntc, p.ntr, p.nch, p.hch, 0, 0)) return false;
     if constexpr (TAILOK) {
-        if (p.tail)
-            return launch_h8t_part<OP, TR, NS, NB, MINB, true>(a, s, 1, p.ntr3, p.nch3, p.hch3, p.ntc,
-                                                               p.ntc * p.ntr * p.nch);
+        if (p.tail) {
+            cudaStream_t st = s;
+            if (fork) {
+                cudaStreamWaitEvent(side, ev[0], 0);
+                st = side;
+            }
+            const bool ok = launch_h8t_part<OP, TR, NS, NB, MINB, true>(a, st, 1, p.ntr3, p.nch3, p.hch3, p.ntc,
+                                                                        p.ntc * p.ntr * p.nch);
+            if (fork) {
+                cudaEventRecord(ev[1], side);
+                cudaStreamWaitEvent(s, ev[1], 0);
+            }
+            return ok;
+        }
     }
     return true;
 }
