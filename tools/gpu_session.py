@@ -111,7 +111,7 @@ def evidence(tag):
     launches(tag, "C5")
     launches(tag, "C3")
     # roofline kernels and the G(u) phi kernels, one ncu --set full capture each
-    ncu(tag, "C5", "h8t_kernel<\\(int\\)3,", "1", "3")
+    ncu(tag, "C5", "h8t_kernel<\\(int\\)3,", "2", "6")   # main + tail launch of one CGP
     ncu(tag, "C5", "h8t_kernel<\\(int\\)6,", "1", "1")
     ncu(tag, "C3", "march2_kernel<\\(int\\)3,", "1", "3")
     ncu(tag, "C3", "stress_apply_kernel", "1", "1")
