@@ -115,7 +115,7 @@ def evidence(tag):
     ncu(tag, "C5", "h8t_kernel<\\(int\\)6,", "1", "1")
     ncu(tag, "C3", "march2_kernel<\\(int\\)3,", "1", "3")
     ncu(tag, "C3", "stress_apply_kernel", "1", "1")
-    ncu(tag, "C5", "coarse_kernel<\\(int\\)3, \\(int\\)1, \\(int\\)8", "1", "3")
+    ncu(tag, "C5", "coarse_kernel<\\(int\\)3, \\(int\\)1, \\(int\\)4", "1", "3")
 
 
 if __name__ == "__main__":
