@@ -18,7 +18,9 @@
 // through a double-buffered shared array with point-to-point mbarriers (warp w -> warp w + 1):
 // no CTA-wide barrier inside the march.  Per thread the march carries the element's two forward
 // faces and the axis-0 carry of its element results in registers (the loop is unrolled by two
-// planes so the faces ping-pong between two register sets without moves).
+// planes so the faces ping-pong between two register sets without moves).  A last column tile
+// that owns <= 9 node columns is marched by a second (TAIL) launch that stacks three such 7-row
+// tiles in the lanes of one CTA (three groups of 10 lanes, see TLT below).
 //
 // Layout (padded 3D fine level, mgcg.cu): vectors (R, n0, n1, p2, 3) with p2 = n2 rounded up to
 // even (TMA row strides are multiples of 16 bytes); D^-1 (n0, n1, p2, 3); masks (n0, n1, m2) bytes,
