@@ -285,7 +285,7 @@ def run_ours(args, cfg):
         "iters": reps[-1]["iters"], "true_relres_max": max(reps[-1]["true_relres"]),
         "first_setup_s": setup_first_s,
         "gpu_launches": int(launches),
-        "roofline": {"kernel": "CG direction + fine EbE matvec (march2_kernel<M2_CGP> 2D / h8t_kernel<FOP_CGP> 3D)",
+        "roofline": {"kernel": "CG direction + fine EbE matvec (march2_kernel<M2_CGP> 2D / h8t_kernel<FOP_CGP> 3D, main + tail-tile launch)",
                      "bound": "hbm", "achieved": achieved, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic_from_profiles(cfg.name),
                      "alg_bytes_per_launch": alg[dom], "kernel_ms": kms[dom],
