@@ -234,8 +234,7 @@ def run_ours(args, cfg):
 
         def e2e_step():
             t_a = time.perf_counter()
-            mg.mg_update_modulus(h, hE)
-            torch.cuda.synchronize()
+            mg.mg_update_modulus(h, hE)   # returns once the operators are enqueued
             t_b = time.perf_counter()
             rep = mg.mgcg_solve(h, hrhs, cfg.tol, hx)
             t_c = time.perf_counter()
@@ -267,7 +266,10 @@ def run_ours(args, cfg):
         e2e = {"value": its / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": 1e3 * dt / nst,
                "phase_ms": {"setup": 1e3 * e2e_ph[0] / nst, "solve": 1e3 * e2e_ph[1] / nst,
-                            "stress_apply": 1e3 * e2e_ph[2] / nst}}
+                            "stress_apply": 1e3 * e2e_ph[2] / nst},
+               "phase_note": "host wall time per call; mg_update_modulus returns once the operators are "
+                             "enqueued, so the solve call's time includes the rest of the setup, which "
+                             "overlaps its right-hand-side upload"}
 
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,

@@ -160,7 +160,12 @@ mg_status mg_nccl_unique_id(void* out128);
 /* This rank's owned DOF / element counts and its element-layer range. */
 mg_status mg_local_info(mg_handle h, long long* ndof_local, long long* nelem_local, int* e_begin, int* e_end);
 
-/* Same grid and BCs, new design: recompute all level operators from E_e. */
+/* Same grid and BCs, new design: recompute all level operators from E_e.
+ * E_e is validated (positive, finite: else MG_ERR_MODULUS, handle unchanged) and copied before the
+ * call returns; the call returns once the new operators are enqueued on the handle's stream.  A
+ * non-positive pivot of the coarsest SPD inverse (MG_ERR_SINGULAR) is reported by the next call on
+ * the handle, which first waits for the operators; mgcg_solve uploads host right-hand sides before
+ * that wait, so the upload overlaps the setup. */
 mg_status mg_update_modulus(mg_handle h, const double* E_e);
 
 /* Solve K x_k = rhs_k, k < nrhs, by multigrid-preconditioned CG

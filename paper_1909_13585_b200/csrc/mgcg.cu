@@ -283,6 +283,16 @@ struct mg_ctx {
     double* Mc = nullptr;                        // Galerkin child matrices Q_c^T K0 Q_c
     double* Estage = nullptr;                    // mg_update_modulus: host E staged here (allocated once)
     long long Estage_n = 0;
+    // mg_update_modulus returns once the operators are enqueued; the coarsest inverse's pivot status
+    // is copied to h_setup_st behind them and checked by the next call (setup_check)
+    int* h_setup_st = nullptr;
+    cudaEvent_t ev_setup = nullptr;
+    bool setup_pending = false;
+    // mgcg_solve with host right-hand sides: uploaded on cs_in into rstage while the handle stream
+    // still runs an earlier (deferred-checked) setup
+    double* rstage = nullptr;
+    long long rstage_n = 0;
+    cudaEvent_t ev_rhs = nullptr;
     double* gstage = nullptr;                    // G(u) phi host-path staging
     long long gstage_cap = 0;
     // G(u) phi with host buffers on one slab: phi chunks copied in / y chunks copied out on two
@@ -405,14 +415,18 @@ struct NvtxRange {
     NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
+static mg_status setup_check(mg_ctx* c);
+
 struct ApiScope {
     NvtxRange nv;   // first member: the range spans the lock, the stream join and the call
     mg_ctx* c;
     std::lock_guard<std::recursive_mutex> lk;
     mg_status status;
-    ApiScope(mg_ctx* c_, const char* fn) : nv(fn), c(c_), lk(g_api_mu), status(MG_OK) {
+    // defer: the caller runs setup_check itself (mgcg_solve: after enqueueing its host upload)
+    ApiScope(mg_ctx* c_, const char* fn, bool defer = false) : nv(fn), c(c_), lk(g_api_mu), status(MG_OK) {
         stream_enter(c);
         status = ensure_constants(c);
+        if (status == MG_OK && !defer) status = setup_check(c);
     }
     ~ApiScope() { stream_leave(c); }
     ApiScope(const ApiScope&) = delete;
@@ -420,6 +434,9 @@ struct ApiScope {
 };
 #define API_SCOPE(c)                    \
     ApiScope api_scope_(c, __func__);   \
+    TRY(api_scope_.status)
+#define API_SCOPE_DEFER_SETUP(c)              \
+    ApiScope api_scope_(c, __func__, true);   \
     TRY(api_scope_.status)
 
 // ---------------------------------------------------------------- partition (host)
@@ -574,7 +591,7 @@ static bool gal_warp() {
     return v;
 }
 
-static mg_status compute_operators(mg_ctx* c) {
+static mg_status compute_operators(mg_ctx* c, bool defer_check = false) {
     cudaStream_t s = c->stream;
     const int L = c->L, dim = c->dim;
     const int NL = dim * (1 << dim);
@@ -666,11 +683,45 @@ static mg_status compute_operators(mg_ctx* c) {
     CU(cudaGraphLaunch(c->g_gj, s));
     c->launches += (c->npad > c->nL ? 2 : 1) + dense_spd_inverse_launches(c->npad);
     CHECK_LAUNCH();
+    if (defer_check) {   // status read back behind the operators, checked by the next call
+        if (!c->h_setup_st) CU(cudaMallocHost(&c->h_setup_st, sizeof(int)));
+        if (!c->ev_setup) CU(cudaEventCreateWithFlags(&c->ev_setup, cudaEventDisableTiming));
+        CU(cudaMemcpyAsync(c->h_setup_st, c->d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CU(cudaEventRecord(c->ev_setup, s));
+        c->setup_pending = true;
+        return MG_OK;
+    }
     int st[1] = {0};
     CU(cudaMemcpyAsync(st, c->d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
     if (st[0] & 4) return fail(MG_ERR_MODULUS, "E_e must be positive and finite");
     if (st[0]) return fail(MG_ERR_SINGULAR, "coarsest operator: non-positive pivot in the SPD inverse");
+    return MG_OK;
+}
+
+// copy streams and their events (host-buffer pipelines of G(u) phi and of the solve's upload)
+static mg_status ensure_copy_streams(mg_ctx* c) {
+    if (c->cs_in) return MG_OK;
+    CU(cudaStreamCreateWithFlags(&c->cs_in, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&c->cs_out, cudaStreamNonBlocking));
+    for (int k = 0; k < mg_ctx::NCHUNK_EV; ++k) {
+        CU(cudaEventCreateWithFlags(&c->gev_in[k], cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&c->gev_k[k], cudaEventDisableTiming));
+    }
+    CU(cudaEventCreateWithFlags(&c->gev_sig, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&c->gev_done, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&c->ev_rhs, cudaEventDisableTiming));
+    return MG_OK;
+}
+
+// pivot status of a deferred-checked setup (mg_update_modulus): waits for the operators
+static mg_status setup_check(mg_ctx* c) {
+    if (!c->setup_pending) return MG_OK;
+    c->setup_pending = false;
+    CU(cudaEventSynchronize(c->ev_setup));
+    const int st = *c->h_setup_st;
+    if (st & 4) return fail(MG_ERR_MODULUS, "E_e must be positive and finite");
+    if (st) return fail(MG_ERR_SINGULAR, "coarsest operator: non-positive pivot in the SPD inverse (last mg_update_modulus)");
     return MG_OK;
 }
 
@@ -1694,8 +1745,9 @@ mg_status mg_update_modulus(mg_handle c, const double* E_e) {
         }
     }
     // E changes the stencils but not the masks; the masks of coarse levels may have been
-    // augmented by zero-diagonal DOFs, which stay valid for the same BCs.
-    return compute_operators(c);
+    // augmented by zero-diagonal DOFs, which stay valid for the same BCs.  Returns once the
+    // operators are enqueued: the coarsest pivot status is checked by the next call.
+    return compute_operators(c, true);
 }
 
 mg_status mgcg_solve(mg_handle c, const double* rhs, int nrhs, double tol, double* x, mg_report* rep) {
@@ -1704,7 +1756,27 @@ mg_status mgcg_solve(mg_handle c, const double* rhs, int nrhs, double tol, doubl
     if (!(tol > 0.0) || !(tol < 1.0)) return fail(MG_ERR_ARG, "tol must be in (0,1)");
     const long long n = c->n_rank;
     cudaStream_t s = c->stream;
-    API_SCOPE(c);
+    API_SCOPE_DEFER_SETUP(c);
+    const bool rdev = is_device_ptr(rhs), xdev = is_device_ptr(x);
+    NvtxRange phase("mgcg_solve: rhs in");
+    if (!rdev) {
+        // host right-hand sides: uploaded on the copy stream into a buffer only this upload and the
+        // scatter below use (the previous solve's scatter finished: every solve ends synchronised),
+        // overlapping a setup that mg_update_modulus may still be running on the handle stream
+        if (c->rstage_n < n * nrhs) {
+            CU(cudaStreamSynchronize(s));
+            if (c->cs_in) CU(cudaStreamSynchronize(c->cs_in));
+            if (c->rstage) cudaFree(c->rstage);
+            c->rstage = nullptr;
+            c->rstage_n = 0;
+            CU(cudaMalloc(&c->rstage, sizeof(double) * n * nrhs));
+            c->rstage_n = n * nrhs;
+        }
+        TRY(ensure_copy_streams(c));
+        CU(cudaMemcpyAsync(c->rstage, rhs, sizeof(double) * n * nrhs, cudaMemcpyHostToDevice, c->cs_in));
+        CU(cudaEventRecord(c->ev_rhs, c->cs_in));
+    }
+    TRY(setup_check(c));
     cudaEvent_t e0, e1;
     CU(cudaEventCreate(&e0));
     CU(cudaEventCreate(&e1));
@@ -1714,12 +1786,10 @@ mg_status mgcg_solve(mg_handle c, const double* rhs, int nrhs, double tol, doubl
         TRY(build_graphs(c, nrhs, tol));
         c->graph_tol = tol;
     }
-    const bool rdev = is_device_ptr(rhs), xdev = is_device_ptr(x);
     const double* rsrc = rhs;
-    NvtxRange phase("mgcg_solve: rhs in");
     if (!rdev) {
-        CU(cudaMemcpyAsync(c->stage, rhs, sizeof(double) * n * nrhs, cudaMemcpyHostToDevice, s));
-        rsrc = c->stage;
+        CU(cudaStreamWaitEvent(s, c->ev_rhs, 0));
+        rsrc = c->rstage;
     }
     TRY(scatter_fine(c, rsrc, nrhs, true, &Slab::b));
     phase.next("mgcg_solve: iterate");
@@ -1943,16 +2013,7 @@ mg_status stress_stiffness_apply(mg_handle c, const double* Es_e, const double* 
             CU(cudaMalloc(&c->gstage, sizeof(double) * need));
             c->gstage_cap = need;
         }
-        if (!c->cs_in) {
-            CU(cudaStreamCreateWithFlags(&c->cs_in, cudaStreamNonBlocking));
-            CU(cudaStreamCreateWithFlags(&c->cs_out, cudaStreamNonBlocking));
-            for (int k = 0; k < mg_ctx::NCHUNK_EV; ++k) {
-                CU(cudaEventCreateWithFlags(&c->gev_in[k], cudaEventDisableTiming));
-                CU(cudaEventCreateWithFlags(&c->gev_k[k], cudaEventDisableTiming));
-            }
-            CU(cudaEventCreateWithFlags(&c->gev_sig, cudaEventDisableTiming));
-            CU(cudaEventCreateWithFlags(&c->gev_done, cudaEventDisableTiming));
-        }
+        TRY(ensure_copy_streams(c));
         double* dEs = c->gstage;
         double* du = dEs + m;
         double* dphi = du + n;
@@ -2766,6 +2827,10 @@ mg_status mg_destroy(mg_handle c) {
         if (c->gev_k[k]) cudaEventDestroy(c->gev_k[k]);
     }
     if (c->gev_sig) cudaEventDestroy(c->gev_sig);
+    if (c->ev_rhs) cudaEventDestroy(c->ev_rhs);
+    if (c->ev_setup) cudaEventDestroy(c->ev_setup);
+    if (c->h_setup_st) cudaFreeHost(c->h_setup_st);
+    if (c->rstage) cudaFree(c->rstage);
     if (c->gev_done) cudaEventDestroy(c->gev_done);
     if (c->cs_in) cudaStreamDestroy(c->cs_in);
     if (c->cs_out) cudaStreamDestroy(c->cs_out);

@@ -106,3 +106,26 @@ def test_invalid_update_modulus_leaves_handle_unchanged(bad, host):
     x1 = torch.empty_like(x0)
     mg.mgcg_solve(h, to_dev(inp["rhs"]), cfg.tol, x1)
     assert torch.equal(x0, x1)   # same operators, same graphs: bitwise
+
+
+@pytest.mark.parametrize("name", ["T2b", "T3c", "T3h"])
+def test_update_modulus_then_host_solve(name):
+    """mg_update_modulus returns with the new operators only enqueued; a host-buffer mgcg_solve
+    uploads its right-hand sides while they are built and then waits for them.  The result equals
+    the device-buffer path bit for bit and the direct oracle solve for the new E."""
+    import paper_1909_13585_b200 as mg
+    cfg, inp, _ = case(name)
+    h = mg.mg_setup(cfg.nel, to_dev(inp["E"]), to_dev(inp["fixed"]), cfg.levels)
+    E2 = np.ascontiguousarray(inp["E"] * np.linspace(0.5, 2.0, inp["E"].size))
+    rhs_h = torch.from_numpy(np.ascontiguousarray(inp["rhs"])).pin_memory()
+    x_h = torch.empty(rhs_h.shape, dtype=torch.float64).pin_memory()
+    x_d = torch.empty(rhs_h.shape, dtype=torch.float64, device=DEV)
+    for _ in range(2):   # the second round reuses the upload buffer and the graphs
+        mg.mg_update_modulus(h, torch.from_numpy(E2).pin_memory().numpy())
+        mg.mgcg_solve(h, rhs_h.numpy(), cfg.tol, x_h.numpy())
+        mg.mg_update_modulus(h, to_dev(E2))
+        mg.mgcg_solve(h, to_dev(inp["rhs"]), cfg.tol, x_d)
+        assert torch.equal(x_h, x_d.cpu())
+    K2 = assemble.assemble_K(cfg.nel, E2, inp["fixed"])
+    U = solve.direct_solve(K2, inp["rhs"], inp["fixed"])
+    assert rel(x_h.numpy(), U).max() < 1e-8
